@@ -1,0 +1,173 @@
+/*
+ * lcp_b200.h — C ABI of the B200-native LCP top-k retrieval library.
+ *
+ * This is the drop-in boundary for the hot path of arXiv 2602.04936's
+ * reference package `lcpsearch` (/root/reference/pkg/src/lcpsearch).  The
+ * reference has no FFI: its boundary is the Python API re-exported from
+ * `src/__init__.py:21-24,44-79`.  Each entry point below names the reference
+ * function it replaces (paths relative to pkg/src/lcpsearch/).  The Python
+ * package `paper_2602_04936_b200` binds these symbols with ctypes and keeps
+ * the reference's names, argument meanings and exception types.
+ *
+ * Conventions
+ *  - Every function returns an lcp_status; it never throws across the ABI.
+ *    On failure lcp_last_error() returns a thread-local message whose text
+ *    matches the reference's exception message where one exists.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = the workspace's own
+ *    stream for *_host calls, legacy default stream otherwise).
+ *  - "_host" entry points take host pointers (pinned or pageable) and are
+ *    synchronous: they include the host<->device copies.  The others take
+ *    device pointers and are asynchronous on `stream`.
+ *  - A built lcp_index is immutable; concurrent queries are safe as long as
+ *    each thread uses its own lcp_workspace (reference: trie.py:19-20,
+ *    SPEC.md:197-198 "queried concurrently without synchronization").
+ */
+#ifndef LCP_B200_H
+#define LCP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LCP_ABI_VERSION 1
+
+/* Status codes.  3/4 mirror the reference CLI exit codes for
+ * InvalidInputError / InternalInvariantError (cli.py:55-58, 418-431). */
+typedef enum lcp_status {
+  LCP_OK = 0,
+  LCP_ERR_INVALID_INPUT = 3, /* core.InvalidInputError  (core.py:29-30) */
+  LCP_ERR_INTERNAL = 4,      /* core.InternalInvariantError (core.py:41-42) */
+  LCP_ERR_CUDA = 5,          /* CUDA runtime failure (no reference counterpart) */
+  LCP_ERR_STATE = 6          /* core.InvalidStateError (core.py:37-38) */
+} lcp_status;
+
+/* Query modes; numeric values equal trie.MODE_CODES (trie.py:49). */
+typedef enum lcp_mode {
+  LCP_MODE_STRICT = 0,
+  LCP_MODE_COMPLETE = 1,
+  LCP_MODE_TAL = 2
+} lcp_mode;
+
+typedef struct lcp_index lcp_index;
+typedef struct lcp_workspace lcp_workspace;
+
+typedef struct lcp_index_info {
+  int64_t n;              /* items                                   */
+  int32_t length;         /* L, symbols per item                     */
+  int32_t sigma;          /* alphabet size                           */
+  int32_t bits;           /* bits per packed symbol (power of two)   */
+  int32_t syms_per_word;  /* 64 / bits                               */
+  int32_t words;          /* u64 words per packed key                */
+  int32_t search_levels;  /* levels of the k-ary search tree         */
+  int32_t tal_depth;      /* TAL bucket depth d, -1 if none          */
+  int32_t has_directory;  /* dense TAL directory present             */
+  int64_t tal_buckets;    /* sigma**d (0 if no TAL structure)        */
+  int64_t device_bytes;   /* bytes of device memory held by the index */
+} lcp_index_info;
+
+int lcp_abi_version(void);
+const char* lcp_last_error(void);
+
+/* ---- index build ---------------------------------------------------------
+ * Replaces trie.build (trie.py:397-431): core.lexicographic_order
+ * (core.py:162-174) + core.adjacent_lcp (core.py:177-184) + the per-depth
+ * boundary tables; and, when tal_depth >= 0, the TalEngine constructor
+ * (tal.py:42-82) for bucket depth tal_depth (directory when
+ * sigma**d <= 2**24, tal.py:26).
+ * rows: n*length uint16 row-major, host or device pointer.  Synchronous.
+ * Errors: symbol >= sigma, length not in [1, 65535], sigma not in
+ * [2, 65536], n >= 2**31  ->  LCP_ERR_INVALID_INPUT.                      */
+int lcp_index_build(const uint16_t* rows, int64_t n, int32_t length, int32_t sigma,
+                    int32_t tal_depth, lcp_index** out);
+int lcp_index_free(lcp_index* index);
+int lcp_index_get_info(const lcp_index* index, lcp_index_info* info);
+
+/* Parity / introspection exports (host or device destination, synchronous).
+ * order         : n int32   == TrieIndex.order (trie.py:425) / TalEngine.item_index
+ * sorted_keys   : n*words u64 packed keys in sorted order
+ * adjacent_lcp  : n-1 uint16 == core.adjacent_lcp(rows[order]) (core.py:177-184)
+ * directory     : sigma**d + 1 int64 == TalEngine.directory (tal.py:76-82)
+ * level_offset  : length+2 int64 == TrieIndex.level_offset (trie.py:405-421)
+ * trie tables   : node_count int32 row_lo + uint16 edge_symbol (trie.py:409-419) */
+int lcp_index_export_order(const lcp_index* index, int32_t* order);
+int lcp_index_export_sorted_keys(const lcp_index* index, uint64_t* keys);
+int lcp_index_export_adjacent_lcp(const lcp_index* index, uint16_t* adj);
+int lcp_index_export_directory(const lcp_index* index, int64_t* directory);
+int lcp_index_trie_level_offsets(const lcp_index* index, int64_t* level_offset);
+int lcp_index_export_trie(const lcp_index* index, int32_t* row_lo, uint16_t* edge_symbol);
+/* TalEngine.bucket_range_search (tal.py:124-136): binary search on the packed
+ * d-prefixes, independent of the directory. q: `count` host queries; lo/hi host. */
+int lcp_index_bucket_range_search(const lcp_index* index, const uint16_t* queries,
+                                  int32_t count, int64_t* lo, int64_t* hi);
+
+/* ---- workspace -------------------------------------------------------- */
+int lcp_workspace_create(lcp_workspace** out);
+int lcp_workspace_free(lcp_workspace* ws);
+/* The workspace's own CUDA stream (cudaStream_t as void*). */
+void* lcp_workspace_stream(lcp_workspace* ws);
+
+/* ---- batched top-k query ------------------------------------------------
+ * Replaces TrieIndex.query (trie.py:290-342) for mode strict/complete and
+ * TalEngine.query (tal.py:155-194) for mode tal, over `count` queries.
+ * queries      : count*length uint16
+ * ids, lcps    : count*out_stride; row q holds hits[q] results ordered by
+ *                (lcp desc, id asc).  out_stride >= min(k, n).
+ * hits         : count int32
+ * matched_depth: count uint16 (descent depth d_max; bucket depth for tal)
+ * aux          : count*2 uint64 work counters, so the host can rebuild the
+ *                reference WorkReport exactly (work.py:36-81):
+ *                strict/complete: aux[2q] = d_max | (d_star << 32),
+ *                                 aux[2q+1] = |R(d*)| | (first row of R(d*) << 32)
+ *                                 (R(d*) = sorted rows sharing q's d*-prefix)
+ *                tal            : aux[2q] = items_scanned,
+ *                                 aux[2q+1] = symbols_compared
+ * Errors: k < 1, bad mode, no TAL structure for tal, query symbol >= sigma. */
+int lcp_query(const lcp_index* index, lcp_workspace* ws, const uint16_t* queries,
+              int32_t count, int32_t k, int32_t mode, int32_t out_stride, uint32_t* ids,
+              uint16_t* lcps, int32_t* hits, uint16_t* matched_depth, uint64_t* aux,
+              void* stream);
+int lcp_query_host(const lcp_index* index, lcp_workspace* ws, const uint16_t* queries,
+                   int32_t count, int32_t k, int32_t mode, int32_t out_stride, uint32_t* ids,
+                   uint16_t* lcps, int32_t* hits, uint16_t* matched_depth, uint64_t* aux);
+/* Device-side error flag raised by lcp_query (invalid query symbol); reading
+ * it synchronises `stream`.  Returns LCP_OK or LCP_ERR_INVALID_INPUT and clears it. */
+int lcp_workspace_check(lcp_workspace* ws, void* stream);
+
+/* ---- brute-force full scan ----------------------------------------------
+ * Replaces oracle.oracle_top_k (oracle.py:38-59): top-min(k,n) over every
+ * item in original row order, (lcp desc, id asc).  Same buffers as lcp_query
+ * minus matched_depth/aux. */
+int lcp_fullscan(const lcp_index* index, lcp_workspace* ws, const uint16_t* queries,
+                 int32_t count, int32_t k, int32_t out_stride, uint32_t* ids, uint16_t* lcps,
+                 int32_t* hits, void* stream);
+int lcp_fullscan_host(const lcp_index* index, lcp_workspace* ws, const uint16_t* queries,
+                      int32_t count, int32_t k, int32_t out_stride, uint32_t* ids,
+                      uint16_t* lcps, int32_t* hits);
+
+/* ---- shard merge (multi-GPU; no reference counterpart) ------
+ * encode: per-shard results -> candidates ((length-lcp) << 32 | (id+id_offset)),
+ *         padded with UINT64_MAX: cand[count*k].
+ * merge : cand[shards][count][k] -> global top-min(k, n_total) per query,
+ *         optionally keeping only lcp == max lcp across shards (strict). */
+int lcp_encode_candidates(const uint32_t* ids, const uint16_t* lcps, const int32_t* hits,
+                          int32_t count, int32_t k, int32_t in_stride, int32_t length,
+                          int64_t id_offset, uint64_t* cand, void* stream);
+int lcp_merge_candidates(const uint64_t* cand, int32_t shards, int32_t count, int32_t k,
+                         int32_t take, int32_t length, int32_t strict, uint32_t* ids,
+                         uint16_t* lcps, int32_t* hits, void* stream);
+/* (ids/lcps of lcp_merge_candidates have row stride max(1, take).) */
+
+/* ---- host staging (no reference counterpart) -----------------------------
+ * Page-locked host buffers so *_host calls DMA directly (cudaHostAlloc). */
+int lcp_pinned_alloc(int64_t bytes, void** out);
+int lcp_pinned_free(void* p);
+/* Synchronise a stream (cudaStream_t as void*). */
+int lcp_stream_sync(void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LCP_B200_H */

@@ -1,0 +1,203 @@
+"""ctypes binding of the C ABI in ``include/lcp_b200.h``.
+
+The shared library ``_lcp_b200.so`` is built in-tree for sm_100a by
+:func:`paper_2602_04936_b200._build.build_native`.  There is no CPU fallback:
+if the library is missing every entry point raises
+:class:`NativeLibraryMissing` instead of computing anything on the host.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .core import InternalInvariantError, InvalidInputError, InvalidStateError
+
+LIB_NAME = "_lcp_b200.so"
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+
+LCP_OK = 0
+LCP_ERR_INVALID_INPUT = 3
+LCP_ERR_INTERNAL = 4
+LCP_ERR_CUDA = 5
+LCP_ERR_STATE = 6
+
+MODE_CODES = {"strict": 0, "complete": 1, "tal": 2}
+
+
+class NativeLibraryMissing(RuntimeError):
+    """The sm_100a extension is not built; there is deliberately no fallback."""
+
+
+class CudaError(RuntimeError):
+    """A CUDA runtime call inside the extension failed."""
+
+
+class IndexInfo(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_int64),
+        ("length", ctypes.c_int32),
+        ("sigma", ctypes.c_int32),
+        ("bits", ctypes.c_int32),
+        ("syms_per_word", ctypes.c_int32),
+        ("words", ctypes.c_int32),
+        ("search_levels", ctypes.c_int32),
+        ("tal_depth", ctypes.c_int32),
+        ("has_directory", ctypes.c_int32),
+        ("tal_buckets", ctypes.c_int64),
+        ("device_bytes", ctypes.c_int64),
+    ]
+
+
+_P = ctypes.c_void_p
+_I32 = ctypes.c_int32
+_I64 = ctypes.c_int64
+
+# name -> (restype, argtypes); the exported surface of include/lcp_b200.h
+SIGNATURES = {
+    "lcp_abi_version": (ctypes.c_int, []),
+    "lcp_last_error": (ctypes.c_char_p, []),
+    "lcp_index_build": (ctypes.c_int, [_P, _I64, _I32, _I32, _I32, ctypes.POINTER(_P)]),
+    "lcp_index_free": (ctypes.c_int, [_P]),
+    "lcp_index_get_info": (ctypes.c_int, [_P, ctypes.POINTER(IndexInfo)]),
+    "lcp_index_export_order": (ctypes.c_int, [_P, _P]),
+    "lcp_index_export_sorted_keys": (ctypes.c_int, [_P, _P]),
+    "lcp_index_export_adjacent_lcp": (ctypes.c_int, [_P, _P]),
+    "lcp_index_export_directory": (ctypes.c_int, [_P, _P]),
+    "lcp_index_trie_level_offsets": (ctypes.c_int, [_P, _P]),
+    "lcp_index_export_trie": (ctypes.c_int, [_P, _P, _P]),
+    "lcp_index_bucket_range_search": (ctypes.c_int, [_P, _P, _I32, _P, _P]),
+    "lcp_workspace_create": (ctypes.c_int, [ctypes.POINTER(_P)]),
+    "lcp_workspace_free": (ctypes.c_int, [_P]),
+    "lcp_workspace_stream": (_P, [_P]),
+    "lcp_workspace_check": (ctypes.c_int, [_P, _P]),
+    "lcp_query": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P]),
+    "lcp_query_host": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P]),
+    "lcp_fullscan": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _P]),
+    "lcp_fullscan_host": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _I32, _P, _P, _P]),
+    "lcp_encode_candidates": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _I32, _I32, _I64, _P, _P]),
+    "lcp_merge_candidates": (ctypes.c_int, [_P, _I32, _I32, _I32, _I32, _I32, _I32, _P, _P, _P, _P]),
+    "lcp_pinned_alloc": (ctypes.c_int, [_I64, ctypes.POINTER(_P)]),
+    "lcp_pinned_free": (ctypes.c_int, [_P]),
+    "lcp_stream_sync": (ctypes.c_int, [_P]),
+}
+
+_lock = threading.Lock()
+_lib: ctypes.CDLL | None = None
+
+
+def load() -> ctypes.CDLL:
+    """Load the extension once; raise NativeLibraryMissing if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise NativeLibraryMissing(
+                f"{LIB_PATH} is not built; run __graft_entry__.build() "
+                "(there is no CPU fallback for the LCP hot path)"
+            )
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def last_error() -> str:
+    msg = load().lcp_last_error()
+    return msg.decode("utf-8", "replace") if msg else ""
+
+
+def check(status: int) -> None:
+    """Map an lcp_status to the reference exception taxonomy (core.py:29-42)."""
+    if status == LCP_OK:
+        return
+    msg = last_error()
+    if status == LCP_ERR_INVALID_INPUT:
+        raise InvalidInputError(msg)
+    if status == LCP_ERR_STATE:
+        raise InvalidStateError(msg)
+    if status == LCP_ERR_INTERNAL:
+        raise InternalInvariantError(msg)
+    if status == LCP_ERR_CUDA:
+        raise CudaError(msg)
+    raise RuntimeError(f"lcp status {status}: {msg}")
+
+
+def ptr(arr) -> int | None:
+    """Raw data pointer of a numpy array or torch tensor (None passes through)."""
+    if arr is None:
+        return None
+    if hasattr(arr, "data_ptr"):
+        return int(arr.data_ptr())
+    return int(arr.ctypes.data)
+
+
+class Workspace:
+    """One lcp_workspace (own CUDA stream + scratch); not shared across threads."""
+
+    def __init__(self) -> None:
+        lib = load()
+        h = ctypes.c_void_p()
+        check(lib.lcp_workspace_create(ctypes.byref(h)))
+        self.handle = h
+
+    @property
+    def stream(self) -> int:
+        return int(load().lcp_workspace_stream(self.handle) or 0)
+
+    def close(self) -> None:
+        if self.handle:
+            load().lcp_workspace_free(self.handle)
+            self.handle = None
+
+    def __del__(self) -> None:  # pragma: no cover - interpreter shutdown order
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_tls = threading.local()
+
+
+def workspace() -> Workspace:
+    """Per-thread workspace: concurrent readers never share scratch."""
+    ws = getattr(_tls, "ws", None)
+    if ws is None:
+        ws = Workspace()
+        _tls.ws = ws
+    return ws
+
+
+class PinnedArray:
+    """Page-locked host buffer exposed as a numpy array (for *_host DMA)."""
+
+    def __init__(self, shape, dtype) -> None:
+        import numpy as np
+
+        self.dtype = np.dtype(dtype)
+        self.shape = tuple(int(s) for s in (shape if isinstance(shape, (tuple, list)) else (shape,)))
+        nbytes = int(np.prod(self.shape, dtype=np.int64)) * self.dtype.itemsize
+        p = ctypes.c_void_p()
+        check(load().lcp_pinned_alloc(max(nbytes, 1), ctypes.byref(p)))
+        self._ptr = p
+        buf = (ctypes.c_uint8 * max(nbytes, 1)).from_address(p.value)
+        self.array = np.frombuffer(buf, dtype=self.dtype, count=nbytes // self.dtype.itemsize).reshape(self.shape)
+
+    def close(self) -> None:
+        if self._ptr:
+            load().lcp_pinned_free(self._ptr)
+            self._ptr = None
+
+    def __del__(self) -> None:  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass

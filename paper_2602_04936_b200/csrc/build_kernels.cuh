@@ -1,0 +1,327 @@
+// build_kernels.cuh — index construction on sm_100a.
+//
+// Replaces, from the reference (pkg/src/lcpsearch/):
+//   core.lexicographic_order (core.py:162-174)  -> k_pack + stable LSD radix sort
+//   core.adjacent_lcp        (core.py:177-184)  -> k_adjacent_lcp
+//   trie.build level loop    (trie.py:409-419)  -> k_adj_hist + k_trie_* (lazy export)
+//   TalEngine directory      (tal.py:76-82)     -> k_directory
+// plus the k-ary search levels that stand in for the trie descent
+// (trie.py:229-256): k_gather_level.
+#pragma once
+
+#include "common.cuh"
+
+// ---------------------------------------------------------------------------
+// pack: uint16 rows (n, L) -> packed keys (n, W); ids = 0..n-1
+// ---------------------------------------------------------------------------
+__global__ void k_pack(const uint16_t* __restrict__ rows, long long n, int L, int W, int b,
+                       int spw, int sigma, u64* __restrict__ keys, u32* __restrict__ ids,
+                       int* __restrict__ err) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long total = n * W;
+  if (t >= total) return;
+  long long row = t / W;
+  int w = (int)(t - row * W);
+  int j0 = w * spw;
+  int j1 = min(L, j0 + spw);
+  const uint16_t* r = rows + row * (long long)L;
+  u64 acc = 0;
+  bool bad = false;
+  for (int j = j0; j < j1; ++j) {
+    u32 s = r[j];
+    bad |= (int)s >= sigma;
+    acc |= (u64)s << (64 - b * (j - j0 + 1));
+  }
+  if (bad) atomicOr(err, 1);
+  keys[t] = acc;
+  if (ids != nullptr && w == 0) ids[row] = (u32)row;
+}
+
+__global__ void k_iota(u32* __restrict__ v, long long n) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = (u32)i;
+}
+
+// kw[i] = keys[perm[i]*W + w]
+__global__ void k_gather_word(const u64* __restrict__ keys, const u32* __restrict__ perm,
+                              long long n, int W, int w, u64* __restrict__ kw) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) kw[i] = keys[(long long)perm[i] * W + w];
+}
+
+// out[i*W + w] = keys[perm[i]*W + w]
+__global__ void k_gather_keys(const u64* __restrict__ keys, const u32* __restrict__ perm,
+                              long long n, int W, u64* __restrict__ out) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * W) return;
+  long long i = t / W;
+  int w = (int)(t - i * W);
+  out[t] = keys[(long long)perm[i] * W + w];
+}
+
+// ---------------------------------------------------------------------------
+// Stable LSD radix sort of (u64 key, u32 value), 8-bit digits.
+//   upsweep   : per-tile digit counts, digit-major [256][ntiles]
+//   scan      : exclusive scan of the counts -> global scatter offsets
+//   downsweep : stable in-tile ranks (warp match_any multisplit) + scatter
+// Stability: a tile is split into 8 contiguous warp segments; a warp walks
+// its segment 32 items at a time in index order, so rank = items of the
+// same digit in earlier tiles + earlier warps + earlier steps + lower lanes.
+// ---------------------------------------------------------------------------
+constexpr int RS_THREADS = 256;
+constexpr int RS_WARPS = RS_THREADS / 32;
+constexpr int RS_ITEMS = 16;                     // per lane
+constexpr int RS_TILE = RS_THREADS * RS_ITEMS;   // 4096 keys
+constexpr int RS_WARP_SEG = 32 * RS_ITEMS;       // 512 keys
+
+// all eight digit histograms of one word in one pass (pass-skip detection)
+__global__ void k_digit_hist8(const u64* __restrict__ k, long long n, u32* __restrict__ hist) {
+  __shared__ u32 h[8 * 256];
+  for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    u64 v = k[i];
+#pragma unroll
+    for (int p = 0; p < 8; ++p) atomicAdd(&h[p * 256 + (int)((v >> (8 * p)) & 255)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x)
+    if (h[i]) atomicAdd(&hist[i], h[i]);
+}
+
+__global__ void __launch_bounds__(RS_THREADS) k_rs_upsweep(const u64* __restrict__ keys, long long n,
+                                                           int shift, int ntiles,
+                                                           u32* __restrict__ counts) {
+  __shared__ u32 h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  long long base = (long long)blockIdx.x * RS_TILE;
+#pragma unroll 4
+  for (int j = 0; j < RS_ITEMS; ++j) {
+    long long i = base + j * RS_THREADS + threadIdx.x;
+    if (i < n) atomicAdd(&h[(int)((keys[i] >> shift) & 255)], 1u);
+  }
+  __syncthreads();
+  counts[(long long)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(RS_THREADS) k_rs_downsweep(
+    const u64* __restrict__ kin, const u32* __restrict__ vin, u64* __restrict__ kout,
+    u32* __restrict__ vout, long long n, int shift, int ntiles, const u32* __restrict__ offsets) {
+  __shared__ u32 wcnt[RS_WARPS][256];
+  __shared__ u32 gofs[256];
+  const int lane = lane_id();
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < RS_WARPS * 256; i += RS_THREADS) (&wcnt[0][0])[i] = 0;
+  gofs[threadIdx.x] = offsets[(long long)threadIdx.x * ntiles + blockIdx.x];
+  __syncthreads();
+
+  const long long seg = (long long)blockIdx.x * RS_TILE + (long long)warp * RS_WARP_SEG;
+  u64 key[RS_ITEMS];
+  u32 val[RS_ITEMS];
+  u32 rank[RS_ITEMS];
+#pragma unroll
+  for (int j = 0; j < RS_ITEMS; ++j) {
+    long long i = seg + j * 32 + lane;
+    bool ok = i < n;
+    key[j] = ok ? kin[i] : 0;
+    val[j] = ok ? vin[i] : 0;
+    u32 d = ok ? (u32)((key[j] >> shift) & 255) : 256u;
+    unsigned peers = __match_any_sync(LCP_FULL_MASK, d);
+    unsigned lower = peers & ((1u << lane) - 1u);
+    u32 before = 0;
+    if (ok) before = wcnt[warp][d];
+    __syncwarp();
+    if (ok && lower == 0) wcnt[warp][d] = before + __popc(peers);
+    __syncwarp();
+    rank[j] = before + __popc(lower);
+  }
+  __syncthreads();
+  // exclusive prefix over warps, per digit
+  {
+    u32 run = 0;
+    for (int w = 0; w < RS_WARPS; ++w) {
+      u32 c = wcnt[w][threadIdx.x];
+      wcnt[w][threadIdx.x] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < RS_ITEMS; ++j) {
+    long long i = seg + j * 32 + lane;
+    if (i < n) {
+      u32 d = (u32)((key[j] >> shift) & 255);
+      long long pos = (long long)gofs[d] + wcnt[warp][d] + rank[j];
+      kout[pos] = key[j];
+      vout[pos] = val[j];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Exclusive scan (in place), recursive over tiles.  T = u32 or u64.
+// ---------------------------------------------------------------------------
+constexpr int SC_THREADS = 512;
+constexpr int SC_ITEMS = 8;
+constexpr int SC_TILE = SC_THREADS * SC_ITEMS;
+
+template <typename T>
+__device__ T block_excl_scan(T v, T* total, T* sh /* >= 32 */) {
+  const int lane = lane_id(), warp = threadIdx.x >> 5;
+  T x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T y = __shfl_up_sync(LCP_FULL_MASK, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int nw = blockDim.x >> 5;
+    T s = lane < nw ? sh[lane] : (T)0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      T y = __shfl_up_sync(LCP_FULL_MASK, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < nw) sh[lane] = s;
+  }
+  __syncthreads();
+  T wprefix = warp ? sh[warp - 1] : (T)0;
+  *total = sh[(blockDim.x >> 5) - 1];
+  __syncthreads();
+  return wprefix + x - v;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(SC_THREADS) k_scan_tiles(T* __restrict__ data, long long m,
+                                                           T* __restrict__ tile_sums) {
+  __shared__ T sh[32];
+  long long base = (long long)blockIdx.x * SC_TILE + (long long)threadIdx.x * SC_ITEMS;
+  T v[SC_ITEMS];
+  T s = 0;
+#pragma unroll
+  for (int j = 0; j < SC_ITEMS; ++j) {
+    v[j] = (base + j < m) ? data[base + j] : (T)0;
+    s += v[j];
+  }
+  T total;
+  T ex = block_excl_scan<T>(s, &total, sh);
+#pragma unroll
+  for (int j = 0; j < SC_ITEMS; ++j) {
+    if (base + j < m) data[base + j] = ex;
+    ex += v[j];
+  }
+  if (threadIdx.x == 0 && tile_sums) tile_sums[blockIdx.x] = total;
+}
+
+template <typename T>
+__global__ void k_scan_add(T* __restrict__ data, long long m, const T* __restrict__ tile_prefix) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) data[i] += tile_prefix[i / SC_TILE];
+}
+
+// ---------------------------------------------------------------------------
+// adjacent LCP of sorted keys: adj[i] = lcp(keys[i], keys[i+1])
+// ---------------------------------------------------------------------------
+template <int WMAX>
+__global__ void k_adjacent_lcp(DevIndex ix, uint16_t* __restrict__ adj) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i + 1 >= ix.n) return;
+  adj[i] = (uint16_t)key_lcp<WMAX>(ix.keys + i * ix.W, ix.keys + (i + 1) * ix.W, ix);
+}
+
+// search level: out[e*W + w] = keys[(e*stride)*W + w]
+__global__ void k_gather_level(const u64* __restrict__ keys, long long cnt, long long stride,
+                               int W, u64* __restrict__ out) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= cnt * W) return;
+  long long e = t / W;
+  int w = (int)(t - e * W);
+  out[t] = keys[e * stride * W + w];
+}
+
+// ---------------------------------------------------------------------------
+// TAL dense directory: dir[c] = #items whose d-prefix code < c
+// (== np.searchsorted(codes, arange(sigma**d + 1)), tal.py:76-82).
+// The d-prefix fits word 0 whenever sigma**d <= 2**24.
+// ---------------------------------------------------------------------------
+__global__ void k_directory(DevIndex ix, int d, long long buckets, long long* __restrict__ dir) {
+  long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > buckets) return;
+  if (c == buckets) {
+    dir[c] = ix.n;
+    return;
+  }
+  // decode base-sigma code into d symbols, pack into a word-0 prefix
+  u64 pre = 0;
+  long long rem = c;
+  for (int j = d - 1; j >= 0; --j) {
+    u64 s = (u64)(rem % ix.sigma);
+    rem /= ix.sigma;
+    pre |= s << (64 - ix.b * (j + 1));
+  }
+  int keep = d * ix.b;
+  u64 mask = keep >= 64 ? ~0ull : (~0ull << (64 - keep));
+  long long lo = 0, hi = ix.n;
+  while (lo < hi) {
+    long long mid = (lo + hi) >> 1;
+    if ((ix.keys[mid * ix.W] & mask) < pre) lo = mid + 1;
+    else hi = mid;
+  }
+  dir[c] = lo;
+}
+
+// ---------------------------------------------------------------------------
+// Per-depth trie tables (TrieIndex.row_lo / edge_symbol / level_offset).
+// Level d (1..L) starts a node at row 0 and at every row i with adj[i-1] < d.
+// ---------------------------------------------------------------------------
+__global__ void k_adj_hist(const uint16_t* __restrict__ adj, long long m,
+                           unsigned long long* __restrict__ hist) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) atomicAdd(&hist[adj[i]], 1ull);
+}
+
+constexpr int TT_THREADS = 256;
+// counts[(d-1)*nblk + blk] = #{i in block : adj[i-1] < d}, rows i in [1, n)
+__global__ void __launch_bounds__(TT_THREADS) k_trie_count(const uint16_t* __restrict__ adj, long long n,
+                                                           int nblk, unsigned long long* __restrict__ counts) {
+  int d = blockIdx.y + 1;
+  long long i = 1 + (long long)blockIdx.x * TT_THREADS + threadIdx.x;
+  bool f = i < n && (int)adj[i - 1] < d;
+  int c = __syncthreads_count(f);
+  if (threadIdx.x == 0) counts[(long long)(d - 1) * nblk + blockIdx.x] = (unsigned long long)c;
+}
+
+__global__ void __launch_bounds__(TT_THREADS) k_trie_scatter(DevIndex ix, const uint16_t* __restrict__ adj,
+                                                             int nblk, const unsigned long long* __restrict__ scan,
+                                                             const long long* __restrict__ level_offset,
+                                                             int* __restrict__ row_lo,
+                                                             uint16_t* __restrict__ edge) {
+  __shared__ int wsum[TT_THREADS / 32];
+  int d = blockIdx.y + 1;
+  long long n = ix.n;
+  long long i = 1 + (long long)blockIdx.x * TT_THREADS + threadIdx.x;
+  bool f = i < n && (int)adj[i - 1] < d;
+  const int lane = lane_id(), warp = threadIdx.x >> 5;
+  unsigned m = __ballot_sync(LCP_FULL_MASK, f);
+  if (lane == 0) wsum[warp] = __popc(m);
+  __syncthreads();
+  int before = 0;
+  for (int w = 0; w < warp; ++w) before += wsum[w];
+  before += __popc(m & ((1u << lane) - 1u));
+  // flat scan covers levels 1..d-1 non-root starts; roots of levels 0..d
+  // take d+1 slots ahead of this level's first non-root start.
+  unsigned long long pos = scan[(long long)(d - 1) * nblk + blockIdx.x] + before + d + 1;
+  if (f) {
+    row_lo[pos] = (int)i;
+    edge[pos] = (uint16_t)key_symbol(ix.keys + i * ix.W, d - 1, ix);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    long long r = level_offset[d];
+    row_lo[r] = 0;
+    edge[r] = (uint16_t)key_symbol(ix.keys, d - 1, ix);
+  }
+}

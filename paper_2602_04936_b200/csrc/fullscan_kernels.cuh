@@ -1,0 +1,230 @@
+// fullscan_kernels.cuh — brute-force streaming scan + candidate merges.
+//
+// Replaces oracle._lcp_profile + oracle.oracle_top_k (oracle.py:38-59): every
+// item, in original row order, against every query; top-min(k,n) by
+// (lcp desc, id asc).
+//
+// Layout: one thread owns one query (packed key in registers and a private
+// sorted top-k list); a CTA of FS_THREADS queries streams a chunk of the
+// packed keys through shared memory in 16 KB stages (TMA bulk copies,
+// double-buffered on mbarriers), so each key read from HBM/L2 is broadcast
+// to FS_THREADS queries.  Keys arrive in ascending id order, so a key only
+// enters a full list if its lcp strictly beats the list's worst lcp: for
+// W == 1 that test is one 64-bit compare  (key ^ q) <= limm1.
+// Per-(query, chunk) lists go to scratch and are merged by k_merge.
+#pragma once
+
+#include "common.cuh"
+
+constexpr int FS_THREADS = 128;
+constexpr int FS_STAGE_BYTES = 16384;
+
+template <int KCAP>
+__device__ __forceinline__ void list_insert(u64 (&list)[KCAP], u64 c) {
+#pragma unroll
+  for (int i = KCAP - 1; i > 0; --i) {
+    u64 prev = list[i - 1];
+    list[i] = (c < prev) ? prev : ((c < list[i]) ? c : list[i]);
+  }
+  list[0] = c < list[0] ? c : list[0];
+}
+
+template <int KCAP>
+__device__ __forceinline__ u64 list_get(const u64 (&list)[KCAP], int idx) {
+  u64 v = ~0ull;
+#pragma unroll
+  for (int i = 0; i < KCAP; ++i)
+    if (i == idx) v = list[i];
+  return v;
+}
+
+template <int WMAX, int KCAP>
+__global__ void __launch_bounds__(FS_THREADS)
+    k_fullscan(DevIndex ix, const uint16_t* __restrict__ queries, int count, int need,
+               long long chunk, int nchunks, u64* __restrict__ partial, int* __restrict__ err) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  u64* bars = reinterpret_cast<u64*>(smem_raw);               // 2 mbarriers
+  u64* stage = reinterpret_cast<u64*>(smem_raw + 16);         // 2 x FS_STAGE_BYTES
+  const int W = ix.W;
+  const int L = ix.L;
+  const long long n = ix.n;
+  const long long qi = (long long)blockIdx.x * FS_THREADS + threadIdx.x;
+  const bool active = qi < count;
+
+  // pack this thread's query
+  u64 qk[WMAX];
+#pragma unroll
+  for (int w = 0; w < WMAX; ++w) qk[w] = 0;
+  if (active) {
+    const uint16_t* qrow = queries + qi * L;
+    bool bad = false;
+    for (int j = 0; j < L; ++j) {
+      u32 s = qrow[j];
+      bad |= (int)s >= ix.sigma;
+      int wj = j >> (6 - ix.lb);
+      u64 v = (u64)s << sym_shift(j, ix);
+#pragma unroll
+      for (int w = 0; w < WMAX; ++w)
+        if (w == wj) qk[w] |= v;
+    }
+    if (bad && blockIdx.y == 0) atomicOr(err, 1);
+  }
+
+  u64 list[KCAP];
+#pragma unroll
+  for (int i = 0; i < KCAP; ++i) list[i] = ~0ull;
+  int filled = 0;
+  u64 thr = ~0ull;    // list[need-1] once filled
+  u64 limm1 = ~0ull;  // W==1: accept iff (key ^ q) <= limm1
+  bool done = false;  // list full of exact matches
+
+  const long long c0 = (long long)blockIdx.y * chunk;
+  const long long c1 = min(n, c0 + chunk);
+  const int per_stage = FS_STAGE_BYTES / (8 * W);
+  const long long nst = c1 > c0 ? (c1 - c0 + per_stage - 1) / per_stage : 0;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](long long s) {
+    long long a = c0 + s * per_stage;
+    long long rows = min((long long)per_stage, c1 - a);
+    u32 bytes = (u32)(((rows * W * 8) + 15) & ~15ll);
+    u64* dst = stage + (s & 1) * (FS_STAGE_BYTES / 8);
+    mbar_arrive_expect_tx(&bars[s & 1], bytes);
+    bulk_g2s(dst, ix.keys_orig + a * W, bytes, &bars[s & 1]);
+  };
+  if (threadIdx.x == 0) {
+    if (nst > 0) issue(0);
+    if (nst > 1) issue(1);
+  }
+
+  for (long long s = 0; s < nst; ++s) {
+    mbar_wait(&bars[s & 1], (u32)((s >> 1) & 1));
+    const u64* buf = stage + (s & 1) * (FS_STAGE_BYTES / 8);
+    const long long a = c0 + s * per_stage;
+    const int rows = (int)min((long long)per_stage, c1 - a);
+    if (active && !done) {
+      if constexpr (WMAX == 1) {
+        const u64 q0 = qk[0];
+        int r = 0;
+        for (; r + 1 < rows; r += 2) {
+          ulonglong2 kv = *reinterpret_cast<const ulonglong2*>(buf + r);
+          u64 x0 = kv.x ^ q0, x1 = kv.y ^ q0;
+          if (x0 <= limm1 || x1 <= limm1) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              u64 x = h ? x1 : x0;
+              if (x <= limm1 && !done) {
+                int l = x ? (__clzll((long long)x) >> ix.lb) : L;
+                u64 c = make_composite(l, (u32)(a + r + h), L);
+                if (c < thr) {
+                  list_insert<KCAP>(list, c);
+                  if (++filled >= need) {
+                    thr = list_get<KCAP>(list, need - 1);
+                    int t = L - (int)(thr >> 32);  // worst kept lcp
+                    if (t >= L) done = true;
+                    else {
+                      int bits = (t + 1) * ix.b;  // <= 64
+                      limm1 = bits >= 64 ? 0ull : ((1ull << (64 - bits)) - 1ull);
+                    }
+                  }
+                }
+              }
+            }
+          }
+        }
+        if (r < rows && !done) {
+          u64 x = buf[r] ^ q0;
+          if (x <= limm1) {
+            int l = x ? (__clzll((long long)x) >> ix.lb) : L;
+            u64 c = make_composite(l, (u32)(a + r), L);
+            if (c < thr) {
+              list_insert<KCAP>(list, c);
+              if (++filled >= need) thr = list_get<KCAP>(list, need - 1);
+            }
+          }
+        }
+      } else {
+        for (int r = 0; r < rows; ++r) {
+          int l = key_lcp<WMAX>(buf + r * W, qk, ix);
+          u64 c = make_composite(l, (u32)(a + r), L);
+          if (c < thr) {
+            list_insert<KCAP>(list, c);
+            if (++filled >= need) thr = list_get<KCAP>(list, need - 1);
+          }
+        }
+      }
+    }
+    __syncthreads();  // everyone done with this buffer
+    if (threadIdx.x == 0 && s + 2 < nst) issue(s + 2);
+  }
+
+  if (active) {
+    u64* out = partial + (qi * nchunks + blockIdx.y) * (long long)need;
+    for (int j = 0; j < need; ++j) out[j] = list_get<KCAP>(list, j);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// merge: per query, the `take` smallest of `shards` candidate lists of `kin`
+// entries each (UINT64_MAX = empty).  cand index = s*s_stride + q*q_stride + j.
+// strict: keep only candidates whose lcp equals the best lcp over all lists
+// (global strict mode = R(d_max) over the union).
+// One warp per query; take <= 32.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+    k_merge(const u64* __restrict__ cand, int shards, int count, int kin, long long s_stride,
+            long long q_stride, int take, int L, int strict, u32* __restrict__ out_ids,
+            uint16_t* __restrict__ out_lcps, int* __restrict__ out_hits, int out_stride) {
+  const int lane = lane_id();
+  const long long qi = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (qi >= count) return;
+  u64 best = ~0ull;
+  if (strict) {
+    for (int s = 0; s < shards; ++s)
+      for (int j = lane; j < kin; j += 32) {
+        u64 c = cand[s * s_stride + qi * q_stride + j];
+        best = c < best ? c : best;
+      }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      u64 y = __shfl_xor_sync(LCP_FULL_MASK, best, o);
+      best = y < best ? y : best;
+    }
+  }
+  const u64 tier = best >> 32;
+  u64 slot = ~0ull, thr = ~0ull;
+  int valid = 0;
+  for (int s = 0; s < shards; ++s) {
+    for (int j0 = 0; j0 < kin; j0 += 32) {
+      int j = j0 + lane;
+      u64 c = j < kin ? cand[s * s_stride + qi * q_stride + j] : ~0ull;
+      if (strict && (c >> 32) != tier) c = ~0ull;
+      valid += __popc(__ballot_sync(LCP_FULL_MASK, c != ~0ull));
+      warp_offer(slot, thr, c, take);
+    }
+  }
+  const int hits = min(take, valid);
+  if (lane < hits) {
+    out_ids[qi * out_stride + lane] = (u32)(slot & 0xffffffffull);
+    out_lcps[qi * out_stride + lane] = (uint16_t)(L - (int)(slot >> 32));
+  }
+  if (lane == 0) out_hits[qi] = hits;
+}
+
+__global__ void k_encode(const u32* __restrict__ ids, const uint16_t* __restrict__ lcps,
+                         const int* __restrict__ hits, int count, int k, int in_stride, int L,
+                         long long id_offset, u64* __restrict__ cand) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)count * k) return;
+  long long q = t / k;
+  int j = (int)(t - q * k);
+  u64 c = ~0ull;
+  if (j < hits[q])
+    c = make_composite(lcps[q * in_stride + j], (u32)(ids[q * in_stride + j] + id_offset), L);
+  cand[t] = c;
+}

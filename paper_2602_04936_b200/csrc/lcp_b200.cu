@@ -1,0 +1,960 @@
+// lcp_b200.cu — C-ABI implementation (include/lcp_b200.h).
+//
+// Host orchestration of the sm_100a kernels.  No torch types cross this
+// boundary; device memory is owned by the index / workspace objects.
+// There is no CPU compute path: every query, scan, sort and merge below is
+// a kernel launch.
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/lcp_b200.h"
+#include "build_kernels.cuh"
+#include "common.cuh"
+#include "fullscan_kernels.cuh"
+#include "query_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define LCP_CK(call)                                                                  \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      return fail(LCP_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));  \
+  } while (0)
+
+#define LCP_CK_LAUNCH()                                                               \
+  do {                                                                                \
+    cudaError_t e_ = cudaGetLastError();                                              \
+    if (e_ != cudaSuccess)                                                            \
+      return fail(LCP_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define LCP_TRY(expr)        \
+  do {                       \
+    int r_ = (expr);         \
+    if (r_ != LCP_OK) return r_; \
+  } while (0)
+
+constexpr int kSmemStageCap = 32768;    // bytes of search levels staged per CTA
+constexpr long long kMaxDirectory = 1ll << 24;  // tal.py:26 MAX_DIRECTORY_ENTRIES
+
+bool is_device_ptr(const void* p) {
+  if (p == nullptr) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+unsigned blocks_for(long long work, int threads) {
+  long long b = (work + threads - 1) / threads;
+  return (unsigned)std::max(1ll, b);
+}
+
+template <typename T>
+int dalloc(T** p, long long count, long long* acct) {
+  size_t bytes = (size_t)std::max(1ll, count) * sizeof(T);
+  cudaError_t e = cudaMalloc((void**)p, bytes);
+  if (e != cudaSuccess)
+    return fail(LCP_ERR_CUDA, std::string("cudaMalloc(") + std::to_string(bytes) +
+                                  " bytes): " + cudaGetErrorString(e));
+  if (acct) *acct += (long long)bytes;
+  return LCP_OK;
+}
+
+// grow-only device buffer
+struct DBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  int ensure(size_t bytes) {
+    if (bytes <= cap) return LCP_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max<size_t>(bytes, 4096);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e != cudaSuccess)
+      return fail(LCP_ERR_CUDA, std::string("workspace cudaMalloc: ") + cudaGetErrorString(e));
+    cap = want;
+    return LCP_OK;
+  }
+  template <typename T>
+  T* as() const { return reinterpret_cast<T*>(p); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
+      sms = 148;
+  }
+  return sms;
+}
+
+// ---- exclusive scan ------------------------------------------------------
+template <typename T>
+int scan_exclusive(T* data, long long m, cudaStream_t st) {
+  if (m <= 0) return LCP_OK;
+  long long ntiles = (m + SC_TILE - 1) / SC_TILE;
+  if (ntiles == 1) {
+    k_scan_tiles<T><<<1, SC_THREADS, 0, st>>>(data, m, (T*)nullptr);
+    LCP_CK_LAUNCH();
+    return LCP_OK;
+  }
+  T* sums = nullptr;
+  LCP_CK(cudaMallocAsync((void**)&sums, (size_t)ntiles * sizeof(T), st));
+  k_scan_tiles<T><<<(unsigned)ntiles, SC_THREADS, 0, st>>>(data, m, sums);
+  LCP_CK_LAUNCH();
+  int r = scan_exclusive<T>(sums, ntiles, st);
+  if (r != LCP_OK) return r;
+  k_scan_add<T><<<blocks_for(m, 256), 256, 0, st>>>(data, m, sums);
+  LCP_CK_LAUNCH();
+  LCP_CK(cudaFreeAsync(sums, st));
+  return LCP_OK;
+}
+
+// ---- stable LSD radix sort of (u64 key, u32 val) ---------------------------
+// Sorts in place semantically: on return (*k, *v) point at the sorted data
+// (buffers may have been swapped with the alternates).
+int radix_sort_pairs(u64** k, u32** v, u64** k_alt, u32** v_alt, long long n, cudaStream_t st) {
+  if (n <= 1) return LCP_OK;
+  u32* hist = nullptr;
+  LCP_CK(cudaMallocAsync((void**)&hist, 8 * 256 * sizeof(u32), st));
+  LCP_CK(cudaMemsetAsync(hist, 0, 8 * 256 * sizeof(u32), st));
+  unsigned hb = (unsigned)std::min<long long>(blocks_for(n, 256), 4ll * num_sms());
+  k_digit_hist8<<<hb, 256, 0, st>>>(*k, n, hist);
+  LCP_CK_LAUNCH();
+  std::vector<u32> h(8 * 256);
+  LCP_CK(cudaMemcpyAsync(h.data(), hist, h.size() * sizeof(u32), cudaMemcpyDeviceToHost, st));
+  LCP_CK(cudaStreamSynchronize(st));
+  LCP_CK(cudaFreeAsync(hist, st));
+
+  const long long ntiles = (n + RS_TILE - 1) / RS_TILE;
+  u32* counts = nullptr;
+  LCP_CK(cudaMallocAsync((void**)&counts, (size_t)ntiles * 256 * sizeof(u32), st));
+  for (int p = 0; p < 8; ++p) {
+    bool trivial = false;
+    for (int d = 0; d < 256; ++d)
+      if ((long long)h[p * 256 + d] == n) trivial = true;
+    if (trivial) continue;  // every key has the same digit: pass is the identity
+    k_rs_upsweep<<<(unsigned)ntiles, RS_THREADS, 0, st>>>(*k, n, 8 * p, (int)ntiles, counts);
+    LCP_CK_LAUNCH();
+    LCP_TRY(scan_exclusive<u32>(counts, ntiles * 256, st));
+    k_rs_downsweep<<<(unsigned)ntiles, RS_THREADS, 0, st>>>(*k, *v, *k_alt, *v_alt, n, 8 * p,
+                                                            (int)ntiles, counts);
+    LCP_CK_LAUNCH();
+    std::swap(*k, *k_alt);
+    std::swap(*v, *v_alt);
+  }
+  LCP_CK(cudaFreeAsync(counts, st));
+  return LCP_OK;
+}
+
+int pow2_bits(int sigma) {
+  int need = 0;
+  while ((1 << need) < sigma) ++need;  // ceil(log2 sigma)
+  int b = 1;
+  while (b < need) b <<= 1;
+  return b;
+}
+
+int ilog2(int v) {
+  int r = 0;
+  while ((1 << r) < v) ++r;
+  return r;
+}
+
+}  // namespace
+
+// ===========================================================================
+struct lcp_index {
+  DevIndex dv{};
+  int tal_depth = -1;
+  long long tal_buckets = 0;  // -1: overflow (> 2^62)
+  long long device_bytes = 0;
+  u64* keys = nullptr;
+  u64* keys_orig = nullptr;
+  u32* order = nullptr;
+  uint16_t* adj = nullptr;
+  u64* levels = nullptr;
+  long long* directory = nullptr;
+  std::vector<long long> level_offset;  // cached trie level offsets
+};
+
+struct lcp_workspace {
+  cudaStream_t stream = nullptr;
+  int* d_err = nullptr;
+  int* h_err = nullptr;  // pinned
+  DBuf qkeys, partial, q_in, ids, lcps, hits, md, aux;
+};
+
+extern "C" {
+
+int lcp_abi_version(void) { return LCP_ABI_VERSION; }
+
+const char* lcp_last_error(void) { return g_err.c_str(); }
+
+int lcp_index_free(lcp_index* ix) {
+  if (!ix) return LCP_OK;
+  cudaFree(ix->keys);
+  cudaFree(ix->keys_orig);
+  cudaFree(ix->order);
+  cudaFree(ix->adj);
+  cudaFree(ix->levels);
+  cudaFree(ix->directory);
+  delete ix;
+  return LCP_OK;
+}
+
+static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, int sigma,
+                      int tal_depth, cudaStream_t st) {
+  DevIndex& dv = ix->dv;
+  const int W = dv.W;
+  long long* acct = &ix->device_bytes;
+
+  // rows -> device
+  const uint16_t* d_rows = rows;
+  uint16_t* owned_rows = nullptr;
+  if (!is_device_ptr(rows)) {
+    LCP_CK(cudaMalloc((void**)&owned_rows, (size_t)n * L * sizeof(uint16_t)));
+    LCP_CK(cudaMemcpyAsync(owned_rows, rows, (size_t)n * L * sizeof(uint16_t),
+                           cudaMemcpyHostToDevice, st));
+    d_rows = owned_rows;
+  }
+  struct RowsGuard {
+    uint16_t* p;
+    ~RowsGuard() { if (p) cudaFree(p); }
+  } rows_guard{owned_rows};
+
+  const long long pad = 64;
+  LCP_TRY(dalloc(&ix->keys_orig, (n + pad) * W, acct));
+  LCP_CK(cudaMemsetAsync(ix->keys_orig, 0, (size_t)(n + pad) * W * 8, st));
+  u32* perm = nullptr;
+  u32* perm_alt = nullptr;
+  u64* kw = nullptr;
+  u64* kw_alt = nullptr;
+  int* d_err = nullptr;
+  LCP_CK(cudaMalloc((void**)&perm, (size_t)(n + pad) * 4));
+  LCP_CK(cudaMalloc((void**)&perm_alt, (size_t)(n + pad) * 4));
+  LCP_CK(cudaMalloc((void**)&kw, (size_t)(n + pad) * 8));
+  LCP_CK(cudaMalloc((void**)&kw_alt, (size_t)(n + pad) * 8));
+  LCP_CK(cudaMalloc((void**)&d_err, sizeof(int)));
+  struct TmpGuard {
+    std::vector<void*> ps;
+    ~TmpGuard() { for (void* p : ps) if (p) cudaFree(p); }
+  } tmp{{perm_alt, kw_alt, d_err}};
+  LCP_CK(cudaMemsetAsync(d_err, 0, sizeof(int), st));
+
+  k_pack<<<blocks_for(n * W, 256), 256, 0, st>>>(d_rows, n, L, W, dv.b, dv.spw, sigma,
+                                                  ix->keys_orig, perm, d_err);
+  LCP_CK_LAUNCH();
+  int h_err = 0;
+  LCP_CK(cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  LCP_CK(cudaStreamSynchronize(st));
+  if (h_err) {
+    cudaFree(perm);
+    cudaFree(kw);
+    return fail(LCP_ERR_INVALID_INPUT,
+                "symbol out of range for alphabet of size " + std::to_string(sigma));
+  }
+
+  // stable LSD over words (least significant word first) — core.py:162-174
+  for (int w = W - 1; w >= 0; --w) {
+    if (W == 1) {
+      LCP_CK(cudaMemcpyAsync(kw, ix->keys_orig, (size_t)n * 8, cudaMemcpyDeviceToDevice, st));
+    } else {
+      k_gather_word<<<blocks_for(n, 256), 256, 0, st>>>(ix->keys_orig, perm, n, W, w, kw);
+      LCP_CK_LAUNCH();
+    }
+    u64* kb = kw;
+    u32* vb = perm;
+    u64* ka = kw_alt;
+    u32* va = perm_alt;
+    LCP_TRY(radix_sort_pairs(&kb, &vb, &ka, &va, n, st));
+    kw = kb;
+    perm = vb;
+    kw_alt = ka;
+    perm_alt = va;
+  }
+  tmp.ps = {perm_alt, kw_alt, d_err};
+  ix->order = perm;
+  *acct += (n + pad) * 4;
+  if (W == 1) {
+    ix->keys = kw;
+    *acct += (n + pad) * 8;
+  } else {
+    tmp.ps.push_back(kw);
+    LCP_TRY(dalloc(&ix->keys, (n + pad) * W, acct));
+    LCP_CK(cudaMemsetAsync(ix->keys, 0, (size_t)(n + pad) * W * 8, st));
+    k_gather_keys<<<blocks_for(n * W, 256), 256, 0, st>>>(ix->keys_orig, perm, n, W, ix->keys);
+    LCP_CK_LAUNCH();
+  }
+  dv.keys = ix->keys;
+  dv.keys_orig = ix->keys_orig;
+  dv.order = ix->order;
+
+  // adjacent lcp — core.py:177-184
+  LCP_TRY(dalloc(&ix->adj, std::max(1ll, n - 1), acct));
+  if (n > 1) {
+    if (W == 1) k_adjacent_lcp<1><<<blocks_for(n - 1, 256), 256, 0, st>>>(dv, ix->adj);
+    else k_adjacent_lcp<0><<<blocks_for(n - 1, 256), 256, 0, st>>>(dv, ix->adj);
+    LCP_CK_LAUNCH();
+  }
+
+  // k-ary search levels (stand-in for the trie descent, trie.py:229-256)
+  int h = 0;
+  {
+    long long cap = 64;
+    while (n > cap && h < LCP_MAX_LEVELS - 1) {
+      cap *= 64;
+      ++h;
+    }
+  }
+  dv.nlevels = h;
+  long long total = 0;
+  std::vector<long long> strides(h);
+  for (int j = 0; j < h; ++j) {
+    long long s = 1;
+    for (int t = 0; t < h - j; ++t) s *= 64;
+    strides[j] = s;
+    long long cnt = (n + s - 1) / s;
+    dv.level_cnt[j] = cnt;
+    dv.level_off[j] = total;
+    total += (cnt + 1) & ~1ll;  // even -> 16-byte aligned bulk copies
+  }
+  LCP_TRY(dalloc(&ix->levels, std::max(2ll, total) * W, acct));
+  for (int j = 0; j < h; ++j) {
+    k_gather_level<<<blocks_for(dv.level_cnt[j] * W, 256), 256, 0, st>>>(
+        ix->keys, dv.level_cnt[j], strides[j], W, ix->levels + dv.level_off[j] * W);
+    LCP_CK_LAUNCH();
+  }
+  dv.levels = ix->levels;
+  dv.smem_levels = 0;
+  dv.smem_entries = 0;
+  for (int j = 0; j < h; ++j) {
+    long long end = dv.level_off[j] + ((dv.level_cnt[j] + 1) & ~1ll);
+    if (end * W * 8 > kSmemStageCap) break;
+    dv.smem_levels = j + 1;
+    dv.smem_entries = (int)end;
+  }
+
+  // TAL bucket structure — tal.py:42-82
+  if (tal_depth >= 0) {
+    ix->tal_depth = tal_depth;
+    long long buckets = 1;
+    bool overflow = false;
+    for (int j = 0; j < tal_depth; ++j) {
+      if (buckets > (1ll << 62) / sigma) {
+        overflow = true;
+        break;
+      }
+      buckets *= sigma;
+    }
+    ix->tal_buckets = overflow ? -1 : buckets;
+    if (tal_depth > 0 && !overflow && buckets <= kMaxDirectory) {
+      LCP_TRY(dalloc(&ix->directory, buckets + 1, acct));
+      k_directory<<<blocks_for(buckets + 1, 256), 256, 0, st>>>(dv, tal_depth, buckets,
+                                                               ix->directory);
+      LCP_CK_LAUNCH();
+    }
+  }
+  dv.tal_depth = ix->tal_depth;
+  dv.tal_buckets = ix->tal_buckets;
+  dv.directory = ix->directory;
+  LCP_CK(cudaStreamSynchronize(st));
+  return LCP_OK;
+}
+
+int lcp_index_build(const uint16_t* rows, int64_t n, int32_t length, int32_t sigma,
+                    int32_t tal_depth, lcp_index** out) {
+  if (!out) return fail(LCP_ERR_INVALID_INPUT, "out must not be null");
+  *out = nullptr;
+  if (sigma < 2 || sigma > 65536)
+    return fail(LCP_ERR_INVALID_INPUT,
+                "alphabet size must be in [2, 65536], got " + std::to_string(sigma));
+  if (length < 1 || length > 65535)
+    return fail(LCP_ERR_INVALID_INPUT,
+                "sequence length must be in [1, 65535], got " + std::to_string(length));
+  if (n < 0 || n >= (1ll << 31))
+    return fail(LCP_ERR_INVALID_INPUT, "n must be in [0, 2**31), got " + std::to_string(n));
+  if (tal_depth > length)
+    return fail(LCP_ERR_INVALID_INPUT, "tal depth exceeds the sequence length");
+  if (n > 0 && !rows) return fail(LCP_ERR_INVALID_INPUT, "rows must not be null");
+
+  lcp_index* ix = new lcp_index();
+  DevIndex& dv = ix->dv;
+  dv.n = n;
+  dv.L = length;
+  dv.sigma = sigma;
+  dv.b = pow2_bits(sigma);
+  dv.lb = ilog2(dv.b);
+  dv.spw = 64 / dv.b;
+  dv.W = (length + dv.spw - 1) / dv.spw;
+  dv.tal_depth = -1;
+  if (n == 0) {
+    if (tal_depth >= 0) {
+      ix->tal_depth = tal_depth;
+      long long buckets = 1;
+      for (int j = 0; j < tal_depth && buckets <= (1ll << 40); ++j) buckets *= sigma;
+      ix->tal_buckets = buckets;
+      dv.tal_depth = tal_depth;
+      dv.tal_buckets = buckets;
+      if (tal_depth > 0 && buckets <= kMaxDirectory) {
+        int r = dalloc(&ix->directory, buckets + 1, &ix->device_bytes);
+        if (r != LCP_OK) {
+          lcp_index_free(ix);
+          return r;
+        }
+        cudaMemset(ix->directory, 0, (size_t)(buckets + 1) * 8);
+        dv.directory = ix->directory;
+      }
+    }
+    *out = ix;
+    return LCP_OK;
+  }
+  cudaStream_t st;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ix;
+    return fail(LCP_ERR_CUDA, "cudaStreamCreate failed");
+  }
+  int r = build_impl(ix, rows, n, length, sigma, tal_depth, st);
+  cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  if (r != LCP_OK) {
+    std::string keep = g_err;
+    lcp_index_free(ix);
+    g_err = keep;
+    return r;
+  }
+  *out = ix;
+  return LCP_OK;
+}
+
+int lcp_index_get_info(const lcp_index* ix, lcp_index_info* info) {
+  if (!ix || !info) return fail(LCP_ERR_INVALID_INPUT, "null argument");
+  const DevIndex& dv = ix->dv;
+  info->n = dv.n;
+  info->length = dv.L;
+  info->sigma = dv.sigma;
+  info->bits = dv.b;
+  info->syms_per_word = dv.spw;
+  info->words = dv.W;
+  info->search_levels = dv.nlevels + 1;
+  info->tal_depth = ix->tal_depth;
+  info->has_directory = ix->directory != nullptr;
+  info->tal_buckets = ix->tal_buckets;
+  info->device_bytes = ix->device_bytes;
+  return LCP_OK;
+}
+
+static int copy_out(void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return LCP_OK;
+  if (!dst) return fail(LCP_ERR_INVALID_INPUT, "destination must not be null");
+  LCP_CK(cudaMemcpy(dst, src, bytes, cudaMemcpyDefault));
+  return LCP_OK;
+}
+
+int lcp_index_export_order(const lcp_index* ix, int32_t* order) {
+  if (!ix) return fail(LCP_ERR_INVALID_INPUT, "null index");
+  return copy_out(order, ix->order, (size_t)ix->dv.n * 4);
+}
+
+int lcp_index_export_sorted_keys(const lcp_index* ix, uint64_t* keys) {
+  if (!ix) return fail(LCP_ERR_INVALID_INPUT, "null index");
+  return copy_out(keys, ix->keys, (size_t)ix->dv.n * ix->dv.W * 8);
+}
+
+int lcp_index_export_adjacent_lcp(const lcp_index* ix, uint16_t* adj) {
+  if (!ix) return fail(LCP_ERR_INVALID_INPUT, "null index");
+  if (ix->dv.n <= 1) return LCP_OK;
+  return copy_out(adj, ix->adj, (size_t)(ix->dv.n - 1) * 2);
+}
+
+int lcp_index_export_directory(const lcp_index* ix, int64_t* directory) {
+  if (!ix) return fail(LCP_ERR_INVALID_INPUT, "null index");
+  if (!ix->directory) return fail(LCP_ERR_STATE, "no dense TAL directory was built");
+  return copy_out(directory, ix->directory, (size_t)(ix->tal_buckets + 1) * 8);
+}
+
+static int level_offsets(lcp_index* ix) {
+  if (!ix->level_offset.empty()) return LCP_OK;
+  const long long n = ix->dv.n;
+  const int L = ix->dv.L;
+  std::vector<long long> off(L + 2, 0);
+  if (n == 0) {
+    for (int d = 1; d < L + 2; ++d) off[d] = 1;  // trie.py:421 level_offset[1:] = 1
+    ix->level_offset = off;
+    return LCP_OK;
+  }
+  std::vector<unsigned long long> hist(L + 1, 0);
+  if (n > 1) {
+    unsigned long long* d_hist = nullptr;
+    LCP_CK(cudaMalloc((void**)&d_hist, (L + 1) * sizeof(unsigned long long)));
+    LCP_CK(cudaMemset(d_hist, 0, (L + 1) * sizeof(unsigned long long)));
+    k_adj_hist<<<blocks_for(n - 1, 256), 256>>>(ix->adj, n - 1, d_hist);
+    LCP_CK_LAUNCH();
+    LCP_CK(cudaMemcpy(hist.data(), d_hist, (L + 1) * sizeof(unsigned long long),
+                      cudaMemcpyDeviceToHost));
+    cudaFree(d_hist);
+  }
+  off[0] = 0;
+  off[1] = 1;
+  unsigned long long below = 0;  // #adj < d
+  for (int d = 1; d <= L; ++d) {
+    below += hist[d - 1];
+    off[d + 1] = off[d] + 1 + (long long)below;
+  }
+  ix->level_offset = off;
+  return LCP_OK;
+}
+
+int lcp_index_trie_level_offsets(const lcp_index* cix, int64_t* level_offset) {
+  if (!cix || !level_offset) return fail(LCP_ERR_INVALID_INPUT, "null argument");
+  lcp_index* ix = const_cast<lcp_index*>(cix);
+  LCP_TRY(level_offsets(ix));
+  for (size_t i = 0; i < ix->level_offset.size(); ++i) level_offset[i] = ix->level_offset[i];
+  return LCP_OK;
+}
+
+int lcp_index_export_trie(const lcp_index* cix, int32_t* row_lo, uint16_t* edge_symbol) {
+  if (!cix) return fail(LCP_ERR_INVALID_INPUT, "null index");
+  lcp_index* ix = const_cast<lcp_index*>(cix);
+  LCP_TRY(level_offsets(ix));
+  const long long n = ix->dv.n;
+  const int L = ix->dv.L;
+  const long long nodes = ix->level_offset[L + 1];
+  if (n == 0) {
+    int32_t z = 0;
+    uint16_t zs = 0;
+    LCP_TRY(copy_out(row_lo, &z, 4));
+    LCP_TRY(copy_out(edge_symbol, &zs, 2));
+    return LCP_OK;
+  }
+  int* d_row = nullptr;
+  uint16_t* d_edge = nullptr;
+  long long* d_off = nullptr;
+  unsigned long long* d_cnt = nullptr;
+  const int nblk = (int)blocks_for(n - 1 > 0 ? n - 1 : 1, TT_THREADS);
+  LCP_CK(cudaMalloc((void**)&d_row, (size_t)nodes * 4));
+  LCP_CK(cudaMalloc((void**)&d_edge, (size_t)nodes * 2));
+  LCP_CK(cudaMalloc((void**)&d_off, (size_t)(L + 2) * 8));
+  LCP_CK(cudaMalloc((void**)&d_cnt, (size_t)nblk * L * 8));
+  LCP_CK(cudaMemcpy(d_off, ix->level_offset.data(), (size_t)(L + 2) * 8, cudaMemcpyHostToDevice));
+  int root_row = 0;
+  uint16_t root_sym = 0;
+  LCP_CK(cudaMemcpy(d_row, &root_row, 4, cudaMemcpyHostToDevice));
+  LCP_CK(cudaMemcpy(d_edge, &root_sym, 2, cudaMemcpyHostToDevice));
+  dim3 grid(nblk, L);
+  k_trie_count<<<grid, TT_THREADS>>>(ix->adj, n, nblk, d_cnt);
+  LCP_CK_LAUNCH();
+  LCP_TRY(scan_exclusive<unsigned long long>(d_cnt, (long long)nblk * L, 0));
+  k_trie_scatter<<<grid, TT_THREADS>>>(ix->dv, ix->adj, nblk, d_cnt, d_off, d_row, d_edge);
+  LCP_CK_LAUNCH();
+  LCP_CK(cudaDeviceSynchronize());
+  int r = copy_out(row_lo, d_row, (size_t)nodes * 4);
+  if (r == LCP_OK) r = copy_out(edge_symbol, d_edge, (size_t)nodes * 2);
+  cudaFree(d_row);
+  cudaFree(d_edge);
+  cudaFree(d_off);
+  cudaFree(d_cnt);
+  return r;
+}
+
+}  // extern "C"
+
+__global__ void k_bucket_search(DevIndex ix, const u64* __restrict__ qkeys, int count,
+                                long long* __restrict__ lo, long long* __restrict__ hi) {
+  int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= count) return;
+  const u64* qk = qkeys + (long long)q * ix.W;
+  int d = ix.tal_depth;
+  lo[q] = d ? prefix_bound(ix, qk, d, false) : 0;
+  hi[q] = d ? prefix_bound(ix, qk, d, true) : ix.n;
+}
+
+extern "C" {
+
+int lcp_index_bucket_range_search(const lcp_index* ix, const uint16_t* queries, int32_t count,
+                                  int64_t* lo, int64_t* hi) {
+  if (!ix) return fail(LCP_ERR_INVALID_INPUT, "null index");
+  if (ix->tal_depth < 0) return fail(LCP_ERR_STATE, "index has no TAL bucket structure");
+  if (count <= 0) return LCP_OK;
+  const DevIndex& dv = ix->dv;
+  if (dv.n == 0) {
+    for (int i = 0; i < count; ++i) lo[i] = hi[i] = 0;
+    return LCP_OK;
+  }
+  uint16_t* d_q = nullptr;
+  u64* d_k = nullptr;
+  long long *d_lo = nullptr, *d_hi = nullptr;
+  int* d_err = nullptr;
+  LCP_CK(cudaMalloc((void**)&d_q, (size_t)count * dv.L * 2));
+  LCP_CK(cudaMalloc((void**)&d_k, (size_t)count * dv.W * 8));
+  LCP_CK(cudaMalloc((void**)&d_lo, (size_t)count * 8));
+  LCP_CK(cudaMalloc((void**)&d_hi, (size_t)count * 8));
+  LCP_CK(cudaMalloc((void**)&d_err, 4));
+  LCP_CK(cudaMemset(d_err, 0, 4));
+  LCP_CK(cudaMemcpy(d_q, queries, (size_t)count * dv.L * 2, cudaMemcpyDefault));
+  k_pack<<<blocks_for((long long)count * dv.W, 256), 256>>>(d_q, count, dv.L, dv.W, dv.b, dv.spw,
+                                                            dv.sigma, d_k, nullptr, d_err);
+  LCP_CK_LAUNCH();
+  k_bucket_search<<<blocks_for(count, 128), 128>>>(dv, d_k, count, d_lo, d_hi);
+  LCP_CK_LAUNCH();
+  int h_err = 0;
+  LCP_CK(cudaMemcpy(&h_err, d_err, 4, cudaMemcpyDeviceToHost));
+  int r = LCP_OK;
+  if (h_err)
+    r = fail(LCP_ERR_INVALID_INPUT,
+             "query symbol out of range for alphabet of size " + std::to_string(dv.sigma));
+  if (r == LCP_OK) r = copy_out(lo, d_lo, (size_t)count * 8);
+  if (r == LCP_OK) r = copy_out(hi, d_hi, (size_t)count * 8);
+  cudaFree(d_q);
+  cudaFree(d_k);
+  cudaFree(d_lo);
+  cudaFree(d_hi);
+  cudaFree(d_err);
+  return r;
+}
+
+// ---- workspace --------------------------------------------------------------
+int lcp_workspace_create(lcp_workspace** out) {
+  if (!out) return fail(LCP_ERR_INVALID_INPUT, "out must not be null");
+  lcp_workspace* ws = new lcp_workspace();
+  cudaError_t e = cudaStreamCreateWithFlags(&ws->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&ws->d_err, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(ws->d_err, 0, sizeof(int));
+  if (e == cudaSuccess) e = cudaHostAlloc((void**)&ws->h_err, sizeof(int), cudaHostAllocDefault);
+  if (e != cudaSuccess) {
+    delete ws;
+    return fail(LCP_ERR_CUDA, std::string("workspace: ") + cudaGetErrorString(e));
+  }
+  *ws->h_err = 0;
+  *out = ws;
+  return LCP_OK;
+}
+
+int lcp_workspace_free(lcp_workspace* ws) {
+  if (!ws) return LCP_OK;
+  if (ws->stream) cudaStreamSynchronize(ws->stream);
+  for (DBuf* b : {&ws->qkeys, &ws->partial, &ws->q_in, &ws->ids, &ws->lcps, &ws->hits, &ws->md,
+                  &ws->aux})
+    b->release();
+  cudaFree(ws->d_err);
+  cudaFreeHost(ws->h_err);
+  if (ws->stream) cudaStreamDestroy(ws->stream);
+  delete ws;
+  return LCP_OK;
+}
+
+void* lcp_workspace_stream(lcp_workspace* ws) { return ws ? (void*)ws->stream : nullptr; }
+
+int lcp_workspace_check(lcp_workspace* ws, void* stream) {
+  if (!ws) return fail(LCP_ERR_INVALID_INPUT, "null workspace");
+  cudaStream_t st = (cudaStream_t)stream;
+  LCP_CK(cudaMemcpyAsync(ws->h_err, ws->d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  LCP_CK(cudaStreamSynchronize(st));
+  if (*ws->h_err) {
+    *ws->h_err = 0;
+    LCP_CK(cudaMemsetAsync(ws->d_err, 0, sizeof(int), st));
+    LCP_CK(cudaStreamSynchronize(st));
+    return fail(LCP_ERR_INVALID_INPUT, "query symbol out of range for alphabet");
+  }
+  return LCP_OK;
+}
+
+}  // extern "C"
+
+__global__ void k_fill_empty(int count, int md, int* hits, uint16_t* out_md, u64* aux) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  hits[i] = 0;
+  if (out_md) out_md[i] = (uint16_t)md;
+  if (aux) {
+    aux[2 * i] = 0;
+    aux[2 * i + 1] = 0;
+  }
+}
+
+template <int WMAX>
+static void launch_fast(const lcp_index* ix, const uint16_t* q, int count, int k, int mode,
+                        int stride, u32* ids, uint16_t* lcps, int* hits, uint16_t* md, u64* aux,
+                        int* err, cudaStream_t st) {
+  const DevIndex& dv = ix->dv;
+  if (mode == LCP_MODE_TAL) {
+    unsigned grid = (unsigned)std::min<long long>(count, 8ll * num_sms());
+    k_query_tal<WMAX><<<grid, QT_THREADS, 0, st>>>(dv, q, count, k, stride, ids, lcps, hits, md,
+                                                   aux, err);
+  } else {
+    unsigned grid = (unsigned)std::min<long long>((count + QW_WARPS - 1) / QW_WARPS,
+                                                  8ll * num_sms());
+    size_t smem = 16 + (size_t)dv.smem_entries * dv.W * 8;
+    k_query_warp<WMAX><<<grid, QW_THREADS, smem, st>>>(dv, q, count, k, mode, stride, ids, lcps,
+                                                       hits, md, aux, err);
+  }
+}
+
+extern "C" {
+
+int lcp_query(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries, int32_t count,
+              int32_t k, int32_t mode, int32_t out_stride, uint32_t* ids, uint16_t* lcps,
+              int32_t* hits, uint16_t* matched_depth, uint64_t* aux, void* stream) {
+  if (!ix || !ws) return fail(LCP_ERR_INVALID_INPUT, "null index or workspace");
+  if (k < 1) return fail(LCP_ERR_INVALID_INPUT, "k must be >= 1, got " + std::to_string(k));
+  if (mode < 0 || mode > 2)
+    return fail(LCP_ERR_INVALID_INPUT, "mode must be 'strict', 'complete' or 'tal', got " +
+                                           std::to_string(mode));
+  if (mode == LCP_MODE_TAL && ix->tal_depth < 0)
+    return fail(LCP_ERR_STATE, "index was built without a TAL bucket structure");
+  const DevIndex& dv = ix->dv;
+  if (count < 0) return fail(LCP_ERR_INVALID_INPUT, "count must be >= 0");
+  if (count == 0) return LCP_OK;
+  const long long need_stride = std::min<long long>(k, std::max(1ll, dv.n));
+  if (out_stride < need_stride)
+    return fail(LCP_ERR_INVALID_INPUT, "out_stride must be >= min(k, n)");
+  if (!queries || !hits) return fail(LCP_ERR_INVALID_INPUT, "null query or output buffer");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dv.n == 0) {
+    k_fill_empty<<<blocks_for(count, 256), 256, 0, st>>>(
+        count, mode == LCP_MODE_TAL ? ix->tal_depth : 0, hits, matched_depth, reinterpret_cast<u64*>(aux));
+    LCP_CK_LAUNCH();
+    return LCP_OK;
+  }
+  // matched_depth / aux are optional for callers; route to scratch if absent
+  uint16_t* md = matched_depth;
+  u64* ax = reinterpret_cast<u64*>(aux);
+  if (!md) {
+    LCP_TRY(ws->md.ensure((size_t)count * 2));
+    md = ws->md.as<uint16_t>();
+  }
+  if (!ax) {
+    LCP_TRY(ws->aux.ensure((size_t)count * 16));
+    ax = ws->aux.as<u64>();
+  }
+  if (dv.W <= 8 && k <= FAST_KMAX) {
+    if (dv.W == 1) launch_fast<1>(ix, queries, count, k, mode, out_stride, ids, lcps, hits, md, ax, ws->d_err, st);
+    else if (dv.W == 2) launch_fast<2>(ix, queries, count, k, mode, out_stride, ids, lcps, hits, md, ax, ws->d_err, st);
+    else if (dv.W <= 4) launch_fast<4>(ix, queries, count, k, mode, out_stride, ids, lcps, hits, md, ax, ws->d_err, st);
+    else launch_fast<8>(ix, queries, count, k, mode, out_stride, ids, lcps, hits, md, ax, ws->d_err, st);
+    LCP_CK_LAUNCH();
+    return LCP_OK;
+  }
+  LCP_TRY(ws->qkeys.ensure((size_t)count * dv.W * 8));
+  k_pack<<<blocks_for((long long)count * dv.W, 256), 256, 0, st>>>(
+      queries, count, dv.L, dv.W, dv.b, dv.spw, dv.sigma, ws->qkeys.as<u64>(), nullptr, ws->d_err);
+  LCP_CK_LAUNCH();
+  unsigned grid = (unsigned)std::min<long long>(count, 8ll * num_sms());
+  k_query_general<<<grid, GEN_THREADS, 0, st>>>(dv, ws->qkeys.as<u64>(), queries, count, k, mode,
+                                                0, out_stride, ids, lcps, hits, md, ax);
+  LCP_CK_LAUNCH();
+  return LCP_OK;
+}
+
+static int host_finish(lcp_workspace* ws) {
+  LCP_CK(cudaMemcpyAsync(ws->h_err, ws->d_err, sizeof(int), cudaMemcpyDeviceToHost, ws->stream));
+  LCP_CK(cudaStreamSynchronize(ws->stream));
+  if (*ws->h_err) {
+    *ws->h_err = 0;
+    LCP_CK(cudaMemsetAsync(ws->d_err, 0, sizeof(int), ws->stream));
+    LCP_CK(cudaStreamSynchronize(ws->stream));
+    return LCP_ERR_INVALID_INPUT;
+  }
+  return LCP_OK;
+}
+
+int lcp_query_host(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries, int32_t count,
+                   int32_t k, int32_t mode, int32_t out_stride, uint32_t* ids, uint16_t* lcps,
+                   int32_t* hits, uint16_t* matched_depth, uint64_t* aux) {
+  if (!ix || !ws) return fail(LCP_ERR_INVALID_INPUT, "null index or workspace");
+  if (count <= 0) return lcp_query(ix, ws, queries, count, k, mode, out_stride, ids, lcps, hits,
+                                   matched_depth, aux, ws->stream);
+  const DevIndex& dv = ix->dv;
+  cudaStream_t st = ws->stream;
+  const size_t qb = (size_t)count * dv.L * 2;
+  const size_t ob = (size_t)count * std::max(1, out_stride);
+  LCP_TRY(ws->q_in.ensure(qb));
+  LCP_TRY(ws->ids.ensure(ob * 4));
+  LCP_TRY(ws->lcps.ensure(ob * 2));
+  LCP_TRY(ws->hits.ensure((size_t)count * 4));
+  LCP_TRY(ws->md.ensure((size_t)count * 2));
+  LCP_TRY(ws->aux.ensure((size_t)count * 16));
+  LCP_CK(cudaMemcpyAsync(ws->q_in.p, queries, qb, cudaMemcpyHostToDevice, st));
+  LCP_TRY(lcp_query(ix, ws, ws->q_in.as<uint16_t>(), count, k, mode, out_stride,
+                    ws->ids.as<u32>(), ws->lcps.as<uint16_t>(), ws->hits.as<int>(),
+                    ws->md.as<uint16_t>(), reinterpret_cast<uint64_t*>(ws->aux.as<u64>()), st));
+  if (ids) LCP_CK(cudaMemcpyAsync(ids, ws->ids.p, ob * 4, cudaMemcpyDeviceToHost, st));
+  if (lcps) LCP_CK(cudaMemcpyAsync(lcps, ws->lcps.p, ob * 2, cudaMemcpyDeviceToHost, st));
+  LCP_CK(cudaMemcpyAsync(hits, ws->hits.p, (size_t)count * 4, cudaMemcpyDeviceToHost, st));
+  if (matched_depth)
+    LCP_CK(cudaMemcpyAsync(matched_depth, ws->md.p, (size_t)count * 2, cudaMemcpyDeviceToHost, st));
+  if (aux) LCP_CK(cudaMemcpyAsync(aux, ws->aux.p, (size_t)count * 16, cudaMemcpyDeviceToHost, st));
+  if (host_finish(ws) != LCP_OK)
+    return fail(LCP_ERR_INVALID_INPUT,
+                "query symbol out of range for alphabet of size " + std::to_string(dv.sigma));
+  return LCP_OK;
+}
+
+// ---- full scan ----------------------------------------------------------------
+}  // extern "C"
+
+template <int WMAX, int KCAP>
+static void launch_fullscan(const DevIndex& dv, const uint16_t* q, int count, int need,
+                            long long chunk, int nchunks, u64* partial, int* err,
+                            cudaStream_t st) {
+  dim3 grid((count + FS_THREADS - 1) / FS_THREADS, nchunks);
+  size_t smem = 16 + 2 * FS_STAGE_BYTES;
+  k_fullscan<WMAX, KCAP><<<grid, FS_THREADS, smem, st>>>(dv, q, count, need, chunk, nchunks,
+                                                          partial, err);
+}
+
+template <int WMAX>
+static void launch_fullscan_k(const DevIndex& dv, const uint16_t* q, int count, int need,
+                              long long chunk, int nchunks, u64* partial, int* err,
+                              cudaStream_t st) {
+  if (need <= 8) launch_fullscan<WMAX, 8>(dv, q, count, need, chunk, nchunks, partial, err, st);
+  else if (need <= 16) launch_fullscan<WMAX, 16>(dv, q, count, need, chunk, nchunks, partial, err, st);
+  else launch_fullscan<WMAX, 32>(dv, q, count, need, chunk, nchunks, partial, err, st);
+}
+
+extern "C" {
+
+int lcp_fullscan(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries, int32_t count,
+                 int32_t k, int32_t out_stride, uint32_t* ids, uint16_t* lcps, int32_t* hits,
+                 void* stream) {
+  if (!ix || !ws) return fail(LCP_ERR_INVALID_INPUT, "null index or workspace");
+  if (k < 1) return fail(LCP_ERR_INVALID_INPUT, "k must be >= 1, got " + std::to_string(k));
+  const DevIndex& dv = ix->dv;
+  if (count <= 0) return LCP_OK;
+  if (out_stride < std::min<long long>(k, std::max(1ll, dv.n)))
+    return fail(LCP_ERR_INVALID_INPUT, "out_stride must be >= min(k, n)");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dv.n == 0) {
+    k_fill_empty<<<blocks_for(count, 256), 256, 0, st>>>(count, 0, hits, nullptr, nullptr);
+    LCP_CK_LAUNCH();
+    return LCP_OK;
+  }
+  const int take = (int)std::min<long long>(k, dv.n);
+  if (dv.W <= 8 && take <= FAST_KMAX) {
+    const int per_stage = FS_STAGE_BYTES / (8 * dv.W);
+    const long long qtiles = (count + FS_THREADS - 1) / FS_THREADS;
+    const long long max_chunks = (dv.n + per_stage - 1) / per_stage;
+    long long want = std::max(1ll, (4ll * num_sms() + qtiles - 1) / qtiles);
+    want = std::min(want, max_chunks);
+    long long chunk = (dv.n + want - 1) / want;
+    chunk = (chunk + per_stage - 1) / per_stage * per_stage;
+    const int nchunks = (int)((dv.n + chunk - 1) / chunk);
+    LCP_TRY(ws->partial.ensure((size_t)count * nchunks * take * 8));
+    u64* partial = ws->partial.as<u64>();
+    if (dv.W == 1) launch_fullscan_k<1>(dv, queries, count, take, chunk, nchunks, partial, ws->d_err, st);
+    else if (dv.W == 2) launch_fullscan_k<2>(dv, queries, count, take, chunk, nchunks, partial, ws->d_err, st);
+    else if (dv.W <= 4) launch_fullscan_k<4>(dv, queries, count, take, chunk, nchunks, partial, ws->d_err, st);
+    else launch_fullscan_k<8>(dv, queries, count, take, chunk, nchunks, partial, ws->d_err, st);
+    LCP_CK_LAUNCH();
+    k_merge<<<blocks_for((long long)count * 32, 256), 256, 0, st>>>(
+        partial, nchunks, count, take, take, (long long)nchunks * take, take, dv.L, 0, ids, lcps,
+        hits, out_stride);
+    LCP_CK_LAUNCH();
+    return LCP_OK;
+  }
+  LCP_TRY(ws->qkeys.ensure((size_t)count * dv.W * 8));
+  k_pack<<<blocks_for((long long)count * dv.W, 256), 256, 0, st>>>(
+      queries, count, dv.L, dv.W, dv.b, dv.spw, dv.sigma, ws->qkeys.as<u64>(), nullptr, ws->d_err);
+  LCP_CK_LAUNCH();
+  unsigned grid = (unsigned)std::min<long long>(count, 8ll * num_sms());
+  k_query_general<<<grid, GEN_THREADS, 0, st>>>(dv, ws->qkeys.as<u64>(), queries, count, k, 1, 1,
+                                                out_stride, ids, lcps, hits, nullptr, nullptr);
+  LCP_CK_LAUNCH();
+  return LCP_OK;
+}
+
+int lcp_fullscan_host(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries,
+                      int32_t count, int32_t k, int32_t out_stride, uint32_t* ids, uint16_t* lcps,
+                      int32_t* hits) {
+  if (!ix || !ws) return fail(LCP_ERR_INVALID_INPUT, "null index or workspace");
+  if (count <= 0) return LCP_OK;
+  const DevIndex& dv = ix->dv;
+  cudaStream_t st = ws->stream;
+  const size_t qb = (size_t)count * dv.L * 2;
+  const size_t ob = (size_t)count * std::max(1, out_stride);
+  LCP_TRY(ws->q_in.ensure(qb));
+  LCP_TRY(ws->ids.ensure(ob * 4));
+  LCP_TRY(ws->lcps.ensure(ob * 2));
+  LCP_TRY(ws->hits.ensure((size_t)count * 4));
+  LCP_CK(cudaMemcpyAsync(ws->q_in.p, queries, qb, cudaMemcpyHostToDevice, st));
+  LCP_TRY(lcp_fullscan(ix, ws, ws->q_in.as<uint16_t>(), count, k, out_stride, ws->ids.as<u32>(),
+                       ws->lcps.as<uint16_t>(), ws->hits.as<int>(), st));
+  if (ids) LCP_CK(cudaMemcpyAsync(ids, ws->ids.p, ob * 4, cudaMemcpyDeviceToHost, st));
+  if (lcps) LCP_CK(cudaMemcpyAsync(lcps, ws->lcps.p, ob * 2, cudaMemcpyDeviceToHost, st));
+  LCP_CK(cudaMemcpyAsync(hits, ws->hits.p, (size_t)count * 4, cudaMemcpyDeviceToHost, st));
+  if (host_finish(ws) != LCP_OK)
+    return fail(LCP_ERR_INVALID_INPUT,
+                "query symbol out of range for alphabet of size " + std::to_string(dv.sigma));
+  return LCP_OK;
+}
+
+// ---- shard candidates ------------------------------------------------------------
+int lcp_encode_candidates(const uint32_t* ids, const uint16_t* lcps, const int32_t* hits,
+                          int32_t count, int32_t k, int32_t in_stride, int32_t length,
+                          int64_t id_offset, uint64_t* cand, void* stream) {
+  if (count <= 0) return LCP_OK;
+  if (k < 1 || in_stride < 1) return fail(LCP_ERR_INVALID_INPUT, "k and in_stride must be >= 1");
+  k_encode<<<blocks_for((long long)count * k, 256), 256, 0, (cudaStream_t)stream>>>(
+      ids, lcps, hits, count, k, in_stride, length, id_offset, (u64*)cand);
+  LCP_CK_LAUNCH();
+  return LCP_OK;
+}
+
+int lcp_merge_candidates(const uint64_t* cand, int32_t shards, int32_t count, int32_t k,
+                         int32_t take, int32_t length, int32_t strict, uint32_t* ids,
+                         uint16_t* lcps, int32_t* hits, void* stream) {
+  if (count <= 0) return LCP_OK;
+  if (shards < 1 || k < 1) return fail(LCP_ERR_INVALID_INPUT, "shards and k must be >= 1");
+  if (take < 0 || take > FAST_KMAX)
+    return fail(LCP_ERR_INVALID_INPUT, "merge supports take in [0, 32]");
+  k_merge<<<blocks_for((long long)count * 32, 256), 256, 0, (cudaStream_t)stream>>>(
+      (const u64*)cand, shards, count, k, (long long)count * k, k, take, length, strict, ids,
+      lcps, hits, std::max(1, take));
+  LCP_CK_LAUNCH();
+  return LCP_OK;
+}
+
+int lcp_pinned_alloc(int64_t bytes, void** out) {
+  if (!out || bytes < 0) return fail(LCP_ERR_INVALID_INPUT, "bad pinned allocation request");
+  *out = nullptr;
+  LCP_CK(cudaHostAlloc(out, (size_t)std::max<int64_t>(bytes, 1), cudaHostAllocDefault));
+  return LCP_OK;
+}
+
+int lcp_pinned_free(void* p) {
+  if (p) LCP_CK(cudaFreeHost(p));
+  return LCP_OK;
+}
+
+int lcp_stream_sync(void* stream) {
+  LCP_CK(cudaStreamSynchronize((cudaStream_t)stream));
+  return LCP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,589 @@
+// query_kernels.cuh — batched top-k LCP queries on sm_100a.
+//
+// Replaces (pkg/src/lcpsearch/):
+//   TrieIndex._descend          trie.py:229-256  -> warp k-ary lower_bound over packed keys
+//   TrieIndex.query strict/complete trie.py:290-342 -> window d* + bounded range scan + warp top-k
+//   TalEngine.bucket_range/query tal.py:116-194   -> directory lookup + CTA bucket scan
+//
+// Complete mode without backtracking: with need = min(k, n),
+// d* = max{d : |R(d)| >= need}; the answer is the `need` smallest
+// (L-lcp)<<32|id over the contiguous sorted range R(d*).  Because lcp is
+// non-decreasing before pos = lower_bound(q) and non-increasing after it,
+// d* is the need-th largest lcp inside the 64-key window [pos-32, pos+32)
+// for need <= 32, and R(d*) is found by extending that window outward.
+// The reference's ancestor walk visits exactly d_max - d* ancestors, which
+// is how the host rebuilds WorkReport.nodes_visited.
+#pragma once
+
+#include "common.cuh"
+
+constexpr int QW_THREADS = 256;                 // 8 warps, one query per warp
+constexpr int QW_WARPS = QW_THREADS / 32;
+constexpr int FAST_KMAX = 32;                   // warp top-k capacity
+
+// pack one query row into W words held by every lane; returns false if a
+// symbol is >= sigma (reference: trie.py:223-226 / tal.py:104-107)
+template <int WMAX>
+__device__ __forceinline__ bool warp_pack_query(const uint16_t* __restrict__ qrow,
+                                                const DevIndex& ix, u64 (&qk)[WMAX]) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int w = 0; w < WMAX; ++w) qk[w] = 0;
+  bool bad = false;
+  for (int j = lane; j < ix.L; j += 32) {
+    u32 s = qrow[j];
+    bad |= (int)s >= ix.sigma;
+    int wj = j >> (6 - ix.lb);
+    u64 v = (u64)s << sym_shift(j, ix);
+#pragma unroll
+    for (int w = 0; w < WMAX; ++w)
+      if (w == wj) qk[w] |= v;
+  }
+#pragma unroll
+  for (int w = 0; w < WMAX; ++w) qk[w] = warp_or64(qk[w]);
+  return !__any_sync(LCP_FULL_MASK, bad);
+}
+
+// lower_bound(keys, q) by a 64-ary search: every level is one coalesced
+// 64-separator read per warp (2 per lane) + 2 ballots.  Top levels come
+// from shared memory (staged by TMA bulk copy), the rest from L2/HBM.
+template <int WMAX>
+__device__ __forceinline__ long long warp_lower_bound(const DevIndex& ix, const u64* staged,
+                                                      const u64 (&qk)[WMAX]) {
+  const int lane = lane_id();
+  const int W = ix.W;
+  long long blk = 0;
+  for (int j = 0;; ++j) {
+    const u64* tab;
+    long long cnt;
+    if (j == ix.nlevels) {
+      tab = ix.keys;
+      cnt = ix.n;
+    } else if (j < ix.smem_levels) {
+      tab = staged + ix.level_off[j] * W;
+      cnt = ix.level_cnt[j];
+    } else {
+      tab = ix.levels + ix.level_off[j] * W;
+      cnt = ix.level_cnt[j];
+    }
+    long long base = blk * LCP_SEARCH_FANOUT;
+    long long i0 = base + 2 * lane;
+    bool lt0 = false, lt1 = false;
+    if constexpr (WMAX == 1) {
+      if (i0 + 1 < cnt) {
+        ulonglong2 v = *reinterpret_cast<const ulonglong2*>(tab + i0);
+        lt0 = v.x < qk[0];
+        lt1 = v.y < qk[0];
+      } else if (i0 < cnt) {
+        lt0 = tab[i0] < qk[0];
+      }
+    } else {
+      if (i0 < cnt) lt0 = key_less<WMAX>(tab + i0 * W, qk, ix);
+      if (i0 + 1 < cnt) lt1 = key_less<WMAX>(tab + (i0 + 1) * W, qk, ix);
+    }
+    int c = __popc(__ballot_sync(LCP_FULL_MASK, lt0)) + __popc(__ballot_sync(LCP_FULL_MASK, lt1));
+    if (j == ix.nlevels) return base + c;
+    if (c == 0) return 0;  // only reachable at the root level
+    blk = base + c - 1;
+  }
+}
+
+template <int WMAX>
+__device__ __forceinline__ int lcp_at(const DevIndex& ix, long long i, const u64 (&qk)[WMAX]) {
+  if constexpr (WMAX == 1) {
+    u64 x = ix.keys[i] ^ qk[0];
+    return x ? (__clzll((long long)x) >> ix.lb) : ix.L;
+  } else {
+    return key_lcp<WMAX>(ix.keys + i * ix.W, qk, ix);
+  }
+}
+
+// Stage the top search levels into shared memory with one TMA bulk copy.
+__device__ __forceinline__ void stage_levels(const DevIndex& ix, u64* bar, u64* staged) {
+  if (ix.smem_levels <= 0) return;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    u32 bytes = (u32)ix.smem_entries * (u32)ix.W * 8u;
+    mbar_arrive_expect_tx(bar, bytes);
+    bulk_g2s(staged, ix.levels, bytes, bar);
+  }
+  mbar_wait(bar, 0);
+}
+
+// ---------------------------------------------------------------------------
+// strict / complete, k <= 32, W <= WMAX <= 8: one warp per query.
+// ---------------------------------------------------------------------------
+template <int WMAX>
+__global__ void __launch_bounds__(QW_THREADS, 4)
+    k_query_warp(DevIndex ix, const uint16_t* __restrict__ queries, int count, int k, int mode,
+                 int stride, u32* __restrict__ out_ids, uint16_t* __restrict__ out_lcps,
+                 int* __restrict__ out_hits, uint16_t* __restrict__ out_md,
+                 u64* __restrict__ out_aux, int* __restrict__ err) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  u64* bar = reinterpret_cast<u64*>(smem_raw);
+  u64* staged = reinterpret_cast<u64*>(smem_raw + 16);
+  stage_levels(ix, bar, staged);
+
+  const int lane = lane_id();
+  const int warp = threadIdx.x >> 5;
+  const long long n = ix.n;
+  const int L = ix.L;
+  const bool complete = mode == 1;
+
+  for (long long qi = (long long)blockIdx.x * QW_WARPS + warp; qi < count;
+       qi += (long long)gridDim.x * QW_WARPS) {
+    u64 qk[WMAX];
+    if (!warp_pack_query<WMAX>(queries + qi * L, ix, qk)) {
+      if (lane == 0) {
+        atomicOr(err, 1);
+        out_hits[qi] = 0;
+        out_md[qi] = 0;
+        out_aux[2 * qi] = 0;
+        out_aux[2 * qi + 1] = 0;
+      }
+      continue;
+    }
+    const long long pos = warp_lower_bound<WMAX>(ix, staged, qk);
+
+    // 64-key window around pos
+    const long long wlo = pos >= 32 ? pos - 32 : 0;
+    const long long whi = pos + 32 <= n ? pos + 32 : n;
+    const long long i0 = wlo + lane, i1 = wlo + 32 + lane;
+    const int l0 = i0 < whi ? lcp_at<WMAX>(ix, i0, qk) : -1;
+    const int l1 = i1 < whi ? lcp_at<WMAX>(ix, i1, qk) : -1;
+    int dmax = max(l0, l1);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) dmax = max(dmax, __shfl_xor_sync(LCP_FULL_MASK, dmax, o));
+
+    const int need = complete ? (int)min((long long)k, n) : k;
+    int dstar = dmax;
+    if (complete) {
+      int lo = 0, hi = dmax;
+      while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        int c = __popc(__ballot_sync(LCP_FULL_MASK, l0 >= mid)) +
+                __popc(__ballot_sync(LCP_FULL_MASK, l1 >= mid));
+        if (c >= need) lo = mid;
+        else hi = mid - 1;
+      }
+      dstar = lo;
+    }
+
+    // scan R(d*): window first, then outward in 32-key chunks
+    u64 slot = ~0ull, thr = ~0ull;
+    const bool c0 = l0 >= dstar, c1 = l1 >= dstar;
+    u64 comp0 = c0 ? make_composite(l0, ix.order[i0], L) : ~0ull;
+    u64 comp1 = c1 ? make_composite(l1, ix.order[i1], L) : ~0ull;
+    warp_offer(slot, thr, comp0, need);
+    warp_offer(slot, thr, comp1, need);
+    long long rsize = __popc(__ballot_sync(LCP_FULL_MASK, c0)) + __popc(__ballot_sync(LCP_FULL_MASK, c1));
+    long long rlo = c0 ? i0 : (c1 ? i1 : n);  // first row of R(d*) (warp-min below)
+
+    // left: the window's first key is in R(d*) -> range continues below wlo
+    bool go = wlo > 0 && __shfl_sync(LCP_FULL_MASK, l0, 0) >= dstar;
+    long long e = wlo;
+    while (go) {
+      long long i = e - 32 + lane;
+      int l = i >= 0 ? lcp_at<WMAX>(ix, i, qk) : -1;
+      bool c = l >= dstar;
+      warp_offer(slot, thr, c ? make_composite(l, ix.order[i], L) : ~0ull, need);
+      unsigned m = __ballot_sync(LCP_FULL_MASK, c);
+      rsize += __popc(m);
+      if (c) rlo = min(rlo, i);
+      e -= 32;
+      go = m == LCP_FULL_MASK && e > 0;
+    }
+    // right: the window's last key is in R(d*) -> range continues at whi
+    const int last_lane = (int)((whi - 1 - wlo) & 31);
+    const int l_last = (whi - 1 - wlo) >= 32 ? __shfl_sync(LCP_FULL_MASK, l1, last_lane)
+                                              : __shfl_sync(LCP_FULL_MASK, l0, last_lane);
+    go = whi < n && l_last >= dstar;
+    e = whi;
+    while (go) {
+      long long i = e + lane;
+      int l = i < n ? lcp_at<WMAX>(ix, i, qk) : -1;
+      bool c = l >= dstar;
+      warp_offer(slot, thr, c ? make_composite(l, ix.order[i], L) : ~0ull, need);
+      unsigned m = __ballot_sync(LCP_FULL_MASK, c);
+      rsize += __popc(m);
+      e += 32;
+      go = m == LCP_FULL_MASK && e < n;
+    }
+
+#pragma unroll
+    for (int o = 16; o; o >>= 1) rlo = min(rlo, __shfl_xor_sync(LCP_FULL_MASK, rlo, o));
+    const int take = (int)min((long long)need, rsize);
+    if (lane < take) {
+      out_ids[qi * stride + lane] = (u32)(slot & 0xffffffffull);
+      out_lcps[qi * stride + lane] = (uint16_t)(L - (int)(slot >> 32));
+    }
+    if (lane == 0) {
+      out_hits[qi] = take;
+      out_md[qi] = (uint16_t)dmax;
+      out_aux[2 * qi] = (u64)(u32)dmax | ((u64)(u32)dstar << 32);
+      out_aux[2 * qi + 1] = (u64)rsize | ((u64)rlo << 32);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// TAL, k <= 32, W <= WMAX <= 8: one CTA per query scans its prefix bucket.
+// ---------------------------------------------------------------------------
+constexpr int QT_THREADS = 256;
+constexpr int QT_WARPS = QT_THREADS / 32;
+
+// bucket [lo, hi) of the query's d-prefix: dense directory (tal.py:138-143)
+// or binary search on the packed d-prefixes (tal.py:124-136)
+__device__ __forceinline__ void tal_bucket(const DevIndex& ix, const u64* qk,
+                                           const uint16_t* qrow, long long& lo,
+                                           long long& hi) {
+  const int d = ix.tal_depth;
+  if (d == 0) {
+    lo = 0;
+    hi = ix.n;
+    return;
+  }
+  if (ix.directory) {
+    long long code = 0;
+    for (int j = 0; j < d; ++j) code = code * ix.sigma + qrow[j];
+    lo = ix.directory[code];
+    hi = ix.directory[code + 1];
+    return;
+  }
+  long long a = 0, b = ix.n;
+  while (a < b) {
+    long long m = (a + b) >> 1;
+    if (prefix_cmp(ix.keys + m * ix.W, qk, d, ix) < 0) a = m + 1;
+    else b = m;
+  }
+  lo = a;
+  b = ix.n;
+  while (a < b) {
+    long long m = (a + b) >> 1;
+    if (prefix_cmp(ix.keys + m * ix.W, qk, d, ix) <= 0) a = m + 1;
+    else b = m;
+  }
+  hi = a;
+}
+
+template <int WMAX>
+__global__ void __launch_bounds__(QT_THREADS)
+    k_query_tal(DevIndex ix, const uint16_t* __restrict__ queries, int count, int k, int stride,
+                u32* __restrict__ out_ids, uint16_t* __restrict__ out_lcps,
+                int* __restrict__ out_hits, uint16_t* __restrict__ out_md,
+                u64* __restrict__ out_aux, int* __restrict__ err) {
+  __shared__ u64 s_q[WMAX];
+  __shared__ long long s_lo, s_hi;
+  __shared__ int s_bad;
+  __shared__ u64 s_list[QT_WARPS][32];
+  __shared__ unsigned long long s_sym[QT_WARPS];
+  const int lane = lane_id();
+  const int warp = threadIdx.x >> 5;
+  const int L = ix.L;
+
+  for (long long qi = blockIdx.x; qi < count; qi += gridDim.x) {
+    const uint16_t* qrow = queries + qi * L;
+    if (warp == 0) {
+      u64 qk[WMAX];
+      bool ok = warp_pack_query<WMAX>(qrow, ix, qk);
+      if (lane == 0) {
+#pragma unroll
+        for (int w = 0; w < WMAX; ++w) s_q[w] = qk[w];
+        s_bad = !ok;
+        long long lo = 0, hi = 0;
+        if (ok) tal_bucket(ix, s_q, qrow, lo, hi);
+        s_lo = lo;
+        s_hi = hi;
+      }
+    }
+    __syncthreads();
+    u64 qk[WMAX];
+#pragma unroll
+    for (int w = 0; w < WMAX; ++w) qk[w] = s_q[w];
+    const long long lo = s_lo, hi = s_hi;
+    const bool bad = s_bad;
+
+    u64 slot = ~0ull, thr = ~0ull;
+    unsigned long long sym = 0;
+    if (!bad) {
+      for (long long base = lo + warp * 32; base < hi; base += QT_THREADS) {
+        long long i = base + lane;
+        u64 comp = ~0ull;
+        if (i < hi) {
+          int l = key_lcp<WMAX>(ix.keys + i * ix.W, qk, ix);
+          sym += (unsigned long long)min(l + 1, L);
+          comp = make_composite(l, ix.order[i], L);
+        }
+        warp_offer(slot, thr, comp, k);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sym += __shfl_xor_sync(LCP_FULL_MASK, sym, o);
+    s_list[warp][lane] = slot;
+    if (lane == 0) s_sym[warp] = sym;
+    __syncthreads();
+    if (warp == 0) {
+      u64 fs = ~0ull, ft = ~0ull;
+      for (int w = 0; w < QT_WARPS; ++w) warp_offer(fs, ft, s_list[w][lane], k);
+      const long long size = hi - lo;
+      const int take = bad ? 0 : (int)min((long long)k, size);
+      if (lane < take) {
+        out_ids[qi * stride + lane] = (u32)(fs & 0xffffffffull);
+        out_lcps[qi * stride + lane] = (uint16_t)(L - (int)(fs >> 32));
+      }
+      if (lane == 0) {
+        unsigned long long tot = 0;
+        for (int w = 0; w < QT_WARPS; ++w) tot += s_sym[w];
+        if (bad) atomicOr(err, 1);
+        out_hits[qi] = take;
+        out_md[qi] = (uint16_t)ix.tal_depth;
+        out_aux[2 * qi] = bad ? 0ull : (u64)size;
+        out_aux[2 * qi + 1] = bad ? 0ull : tot;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// General path: any k, any W, all modes + full scan.  One CTA per query;
+// the query's range [lo, hi) is emitted as its `take` smallest composites in
+// ascending order, in rounds of GEN_CAP (8-pass radix select + smem bitonic
+// sort).  Queries are pre-packed by k_pack into qkeys.
+// ---------------------------------------------------------------------------
+constexpr int GEN_THREADS = 256;
+constexpr int GEN_CAP = 2048;
+
+__device__ __forceinline__ void bitonic_sort_smem(u64* buf, int P) {
+  for (int k2 = 2; k2 <= P; k2 <<= 1) {
+    for (int j = k2 >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        int ixj = i ^ j;
+        if (ixj > i) {
+          u64 a = buf[i], b = buf[ixj];
+          bool up = (i & k2) == 0;
+          if ((a > b) == up) {
+            buf[i] = b;
+            buf[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// first index in [0, n) whose d-prefix compares >= q (strict=false) or > q (strict=true)
+__device__ __forceinline__ long long prefix_bound(const DevIndex& ix, const u64* q, int d,
+                                                  bool upper) {
+  long long a = 0, b = ix.n;
+  while (a < b) {
+    long long m = (a + b) >> 1;
+    int c = prefix_cmp(ix.keys + m * ix.W, q, d, ix);
+    if (c < 0 || (upper && c == 0)) a = m + 1;
+    else b = m;
+  }
+  return a;
+}
+
+struct GenItem {
+  const DevIndex* ix;
+  const u64* q;
+  bool fullscan;
+  __device__ __forceinline__ u64 comp(long long i, int* lcp_out) const {
+    const u64* key = fullscan ? ix->keys_orig + i * ix->W : ix->keys + i * ix->W;
+    int l = key_lcp<0>(key, q, *ix);
+    *lcp_out = l;
+    u32 id = fullscan ? (u32)i : ix->order[i];
+    return make_composite(l, id, ix->L);
+  }
+};
+
+__global__ void __launch_bounds__(GEN_THREADS)
+    k_query_general(DevIndex ix, const u64* __restrict__ qkeys, const uint16_t* __restrict__ queries,
+                    int count, int k, int mode, int fullscan, int stride,
+                    u32* __restrict__ out_ids, uint16_t* __restrict__ out_lcps,
+                    int* __restrict__ out_hits, uint16_t* __restrict__ out_md,
+                    u64* __restrict__ out_aux) {
+  __shared__ u64 buf[GEN_CAP];
+  __shared__ u32 hist[256];
+  __shared__ long long s_lo, s_hi, s_take;
+  __shared__ int s_dmax, s_dstar, s_md;
+  __shared__ u32 s_cnt;
+  __shared__ u64 s_prefix;
+  __shared__ u32 s_rank;
+  __shared__ unsigned long long s_sym;
+  const int L = ix.L;
+
+  for (long long qi = blockIdx.x; qi < count; qi += gridDim.x) {
+    const u64* q = qkeys + qi * ix.W;
+    if (threadIdx.x == 0) {
+      long long lo = 0, hi = ix.n, take = 0;
+      int dmax = 0, dstar = 0, md = 0;
+      if (fullscan) {
+        take = min((long long)k, ix.n);
+      } else if (mode == 2) {
+        tal_bucket(ix, q, queries + qi * L, lo, hi);
+        take = min((long long)k, hi - lo);
+        md = ix.tal_depth;
+      } else {
+        long long a = 0, b = ix.n;
+        while (a < b) {
+          long long m = (a + b) >> 1;
+          if (key_less<0>(ix.keys + m * ix.W, q, ix)) a = m + 1;
+          else b = m;
+        }
+        const long long pos = a;
+        if (pos > 0) dmax = key_lcp<0>(ix.keys + (pos - 1) * ix.W, q, ix);
+        if (pos < ix.n) dmax = max(dmax, key_lcp<0>(ix.keys + pos * ix.W, q, ix));
+        if (mode == 0) {
+          dstar = dmax;
+          lo = prefix_bound(ix, q, dmax, false);
+          hi = prefix_bound(ix, q, dmax, true);
+          take = min((long long)k, hi - lo);
+        } else {
+          const long long need = min((long long)k, ix.n);
+          int d = dmax;
+          for (;;) {
+            lo = d ? prefix_bound(ix, q, d, false) : 0;
+            hi = d ? prefix_bound(ix, q, d, true) : ix.n;
+            if (hi - lo >= need || d == 0) break;
+            --d;
+          }
+          dstar = d;
+          take = need;
+        }
+        md = dmax;
+      }
+      s_lo = lo;
+      s_hi = hi;
+      s_take = take;
+      s_dmax = dmax;
+      s_dstar = dstar;
+      s_md = md;
+      s_sym = 0;
+    }
+    __syncthreads();
+    const long long lo = s_lo, hi = s_hi, take = s_take;
+    const long long size = hi - lo;
+    GenItem it{&ix, q, fullscan != 0};
+    unsigned long long sym = 0;
+
+    if (size <= GEN_CAP) {
+      int P = 1;
+      while (P < size) P <<= 1;
+      for (int t = threadIdx.x; t < P; t += GEN_THREADS) {
+        u64 c = ~0ull;
+        if (t < size) {
+          int l;
+          c = it.comp(lo + t, &l);
+          sym += (unsigned long long)min(l + 1, L);
+        }
+        buf[t] = c;
+      }
+      __syncthreads();
+      bitonic_sort_smem(buf, P);
+      for (int t = threadIdx.x; t < take; t += GEN_THREADS) {
+        u64 c = buf[t];
+        out_ids[qi * stride + t] = (u32)(c & 0xffffffffull);
+        out_lcps[qi * stride + t] = (uint16_t)(L - (int)(c >> 32));
+      }
+    } else {
+      long long emitted = 0;
+      u64 last = 0;
+      bool first = true;
+      while (emitted < take) {
+        const u32 want = (u32)min((long long)GEN_CAP, take - emitted);
+        // --- radix select: want-th smallest composite greater than `last`
+        if (threadIdx.x == 0) {
+          s_prefix = 0;
+          s_rank = want;
+        }
+        __syncthreads();
+        for (int shift = 56; shift >= 0; shift -= 8) {
+          for (int t = threadIdx.x; t < 256; t += GEN_THREADS) hist[t] = 0;
+          __syncthreads();
+          const u64 prefix = s_prefix;
+          const u64 hmask = shift == 56 ? 0ull : (~0ull << (shift + 8));
+          for (long long i = lo + threadIdx.x; i < hi; i += GEN_THREADS) {
+            int l;
+            u64 c = it.comp(i, &l);
+            if (first && shift == 56) sym += (unsigned long long)min(l + 1, L);
+            if ((first || c > last) && (c & hmask) == prefix)
+              atomicAdd(&hist[(c >> shift) & 255], 1u);
+          }
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            u32 r = s_rank, cum = 0;
+            int dg = 0;
+            for (; dg < 256; ++dg) {
+              if (cum + hist[dg] >= r) break;
+              cum += hist[dg];
+            }
+            if (dg == 256) dg = 255;  // fewer candidates than `want`: cannot happen
+            s_rank = r - cum;
+            s_prefix = prefix | ((u64)dg << shift);
+          }
+          __syncthreads();
+        }
+        const u64 T = s_prefix;
+        // --- collect (last, T] : exactly `want` composites
+        if (threadIdx.x == 0) s_cnt = 0;
+        __syncthreads();
+        for (long long i = lo + threadIdx.x; i < hi; i += GEN_THREADS) {
+          int l;
+          u64 c = it.comp(i, &l);
+          if ((first || c > last) && c <= T) {
+            u32 slotp = atomicAdd(&s_cnt, 1u);
+            if (slotp < GEN_CAP) buf[slotp] = c;
+          }
+        }
+        __syncthreads();
+        int P = 1;
+        while (P < (int)want) P <<= 1;
+        for (int t = (int)want + threadIdx.x; t < P; t += GEN_THREADS) buf[t] = ~0ull;
+        __syncthreads();
+        bitonic_sort_smem(buf, P);
+        for (int t = threadIdx.x; t < (int)want; t += GEN_THREADS) {
+          u64 c = buf[t];
+          out_ids[qi * stride + emitted + t] = (u32)(c & 0xffffffffull);
+          out_lcps[qi * stride + emitted + t] = (uint16_t)(L - (int)(c >> 32));
+        }
+        __syncthreads();
+        last = T;
+        first = false;
+        emitted += want;
+      }
+      if (take == 0 && mode == 2 && !fullscan) {
+        for (long long i = lo + threadIdx.x; i < hi; i += GEN_THREADS) {
+          int l;
+          it.comp(i, &l);
+          sym += (unsigned long long)min(l + 1, L);
+        }
+      }
+    }
+    // reduce symbols_compared (TAL accounting)
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sym += __shfl_xor_sync(LCP_FULL_MASK, sym, o);
+    if ((threadIdx.x & 31) == 0 && sym) atomicAdd(&s_sym, sym);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      out_hits[qi] = (int)take;
+      if (!fullscan) {
+        out_md[qi] = (uint16_t)s_md;
+        if (mode == 2) {
+          out_aux[2 * qi] = (u64)size;
+          out_aux[2 * qi + 1] = s_sym;
+        } else {
+          out_aux[2 * qi] = (u64)(u32)s_dmax | ((u64)(u32)s_dstar << 32);
+          out_aux[2 * qi + 1] = (u64)size | ((u64)lo << 32);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}

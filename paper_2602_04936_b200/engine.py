@@ -1,0 +1,210 @@
+"""Owner of one device-resident index built by the sm_100a extension.
+
+``NativeIndex`` wraps an ``lcp_index*`` (include/lcp_b200.h) and exposes the
+batched entry points with numpy (host, synchronous) or torch/device-pointer
+(asynchronous) buffers.  TrieIndex, TalEngine and the full scan are thin
+reference-compatible views over it.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native
+from ._native import IndexInfo, PinnedArray, check, load, ptr, workspace
+from .core import InvalidInputError, SYMBOL_DTYPE
+from .result import BatchResult
+
+MODES = _native.MODE_CODES
+
+
+class NativeIndex:
+    """Packed, sorted, searchable corpus on the GPU (immutable after build)."""
+
+    def __init__(self, items: np.ndarray, length: int, sigma: int, tal_depth: int = -1):
+        lib = load()
+        items = np.ascontiguousarray(items, dtype=SYMBOL_DTYPE)
+        n = int(items.shape[0])
+        h = ctypes.c_void_p()
+        check(lib.lcp_index_build(ptr(items) if n else None, n, int(length), int(sigma),
+                                  int(tal_depth), ctypes.byref(h)))
+        self._h = h
+        info = IndexInfo()
+        check(lib.lcp_index_get_info(h, ctypes.byref(info)))
+        self.info = info
+        self.n = int(info.n)
+        self.length = int(info.length)
+        self.sigma = int(info.sigma)
+        self.words = int(info.words)
+        self.bits = int(info.bits)
+
+    @classmethod
+    def from_device(cls, rows_ptr: int, n: int, length: int, sigma: int, tal_depth: int = -1):
+        """Build from a device pointer (e.g. a CUDA uint16 tensor's data_ptr())."""
+        self = cls.__new__(cls)
+        lib = load()
+        h = ctypes.c_void_p()
+        check(lib.lcp_index_build(rows_ptr if n else None, int(n), int(length), int(sigma),
+                                  int(tal_depth), ctypes.byref(h)))
+        self._h = h
+        info = IndexInfo()
+        check(lib.lcp_index_get_info(h, ctypes.byref(info)))
+        self.info = info
+        self.n, self.length, self.sigma = int(info.n), int(info.length), int(info.sigma)
+        self.words, self.bits = int(info.words), int(info.bits)
+        return self
+
+    @property
+    def handle(self):
+        if not self._h:
+            raise RuntimeError("index has been closed")
+        return self._h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            load().lcp_index_free(self._h)
+            self._h = None
+
+    def __del__(self) -> None:  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def device_bytes(self) -> int:
+        return int(self.info.device_bytes)
+
+    # -- exports (parity / introspection) ------------------------------------
+    def export_order(self) -> np.ndarray:
+        out = np.empty(self.n, dtype=np.int32)
+        if self.n:
+            check(load().lcp_index_export_order(self.handle, ptr(out)))
+        return out
+
+    def export_sorted_keys(self) -> np.ndarray:
+        out = np.empty((self.n, self.words), dtype=np.uint64)
+        if self.n:
+            check(load().lcp_index_export_sorted_keys(self.handle, ptr(out)))
+        return out
+
+    def export_adjacent_lcp(self) -> np.ndarray:
+        out = np.empty(max(0, self.n - 1), dtype=np.uint16)
+        if self.n > 1:
+            check(load().lcp_index_export_adjacent_lcp(self.handle, ptr(out)))
+        return out
+
+    def export_directory(self) -> np.ndarray:
+        out = np.empty(int(self.info.tal_buckets) + 1, dtype=np.int64)
+        check(load().lcp_index_export_directory(self.handle, ptr(out)))
+        return out
+
+    def level_offsets(self) -> np.ndarray:
+        out = np.empty(self.length + 2, dtype=np.int64)
+        check(load().lcp_index_trie_level_offsets(self.handle, ptr(out)))
+        return out
+
+    def export_trie(self) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+        off = self.level_offsets()
+        nodes = int(off[-1])
+        row_lo = np.empty(nodes, dtype=np.int32)
+        edge = np.empty(nodes, dtype=np.uint16)
+        check(load().lcp_index_export_trie(self.handle, ptr(row_lo), ptr(edge)))
+        return row_lo, edge, off
+
+    def bucket_range_search(self, queries: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+        q = np.ascontiguousarray(queries, dtype=np.uint16).reshape(-1, self.length)
+        lo = np.empty(q.shape[0], dtype=np.int64)
+        hi = np.empty(q.shape[0], dtype=np.int64)
+        check(load().lcp_index_bucket_range_search(self.handle, ptr(q), q.shape[0], ptr(lo), ptr(hi)))
+        return lo, hi
+
+    def unpack_sorted_rows(self) -> np.ndarray:
+        """Sorted uint16 rows decoded from the device's packed keys."""
+        keys = self.export_sorted_keys()
+        b = self.bits
+        spw = 64 // b
+        j = np.arange(self.length)
+        word = keys[:, j // spw]
+        shift = (64 - b * (j % spw + 1)).astype(np.uint64)
+        return ((word >> shift) & np.uint64((1 << b) - 1)).astype(np.uint16)
+
+    # -- queries -----------------------------------------------------------
+    def stride_for(self, k: int) -> int:
+        return max(1, min(int(k), self.n))
+
+    def alloc_batch(self, count: int, k: int, mode: str = "complete", pinned: bool = True) -> BatchResult:
+        """Output buffers for ``count`` queries (page-locked when pinned)."""
+        stride = self.stride_for(k)
+        owners: list = []
+
+        def mk(shape, dt):
+            if not pinned:
+                return np.empty(shape, dtype=dt)
+            p = PinnedArray(shape, dt)
+            owners.append(p)
+            return p.array
+
+        out = BatchResult(
+            ids=mk((count, stride), np.uint32),
+            lcps=mk((count, stride), np.uint16),
+            hits=mk((count,), np.int32),
+            matched_depth=mk((count,), np.uint16),
+            aux=mk((count, 2), np.uint64),
+            mode=mode,
+        )
+        out._owners = owners  # page-locked buffers live as long as the result
+        return out
+
+    def query_host(self, queries: np.ndarray, k: int, mode: str,
+                   out: BatchResult | None = None) -> BatchResult:
+        """Synchronous batched query through lcp_query_host (H2D + kernel + D2H)."""
+        if mode not in MODES:
+            raise InvalidInputError(f"unknown mode {mode!r}")
+        if k < 1:
+            raise InvalidInputError(f"k must be >= 1, got {k}")
+        count = int(queries.shape[0])
+        k_eff = self.stride_for(k)
+        if out is None:
+            out = self.alloc_batch(count, k, mode, pinned=False)
+        out.mode = mode
+        ws = workspace()
+        check(load().lcp_query_host(
+            self.handle, ws.handle, ptr(queries), count, k_eff, MODES[mode], out.ids.shape[1],
+            ptr(out.ids), ptr(out.lcps), ptr(out.hits), ptr(out.matched_depth), ptr(out.aux)))
+        return out
+
+    def query_device(self, queries, k: int, mode: str, ids, lcps, hits, matched_depth=None,
+                     aux=None, stream: int | None = None, ws=None) -> None:
+        """Asynchronous batched query on device buffers (torch CUDA tensors or
+        raw pointers); launches on ``stream`` (default: the workspace stream)."""
+        count = int(queries.shape[0])
+        ws = ws or workspace()
+        st = ws.stream if stream is None else stream
+        stride = int(ids.shape[1])
+        check(load().lcp_query(
+            self.handle, ws.handle, ptr(queries), count, self.stride_for(k), MODES[mode], stride,
+            ptr(ids), ptr(lcps), ptr(hits), ptr(matched_depth), ptr(aux), st))
+
+    def fullscan_host(self, queries: np.ndarray, k: int, out: BatchResult | None = None) -> BatchResult:
+        if k < 1:
+            raise InvalidInputError(f"k must be >= 1, got {k}")
+        count = int(queries.shape[0])
+        k_eff = self.stride_for(k)
+        if out is None:
+            out = self.alloc_batch(count, k, "complete", pinned=False)
+        ws = workspace()
+        check(load().lcp_fullscan_host(
+            self.handle, ws.handle, ptr(queries), count, k_eff, out.ids.shape[1],
+            ptr(out.ids), ptr(out.lcps), ptr(out.hits)))
+        return out
+
+    def fullscan_device(self, queries, k: int, ids, lcps, hits, stream: int | None = None, ws=None) -> None:
+        count = int(queries.shape[0])
+        ws = ws or workspace()
+        st = ws.stream if stream is None else stream
+        check(load().lcp_fullscan(
+            self.handle, ws.handle, ptr(queries), count, self.stride_for(k), int(ids.shape[1]),
+            ptr(ids), ptr(lcps), ptr(hits), st))

@@ -1,0 +1,261 @@
+"""GPU parity: the sm_100a path through the C ABI vs the golden vectors
+(produced by the reference) and vs the pinned C oracle.  Bit-exact for every
+id, lcp, hit count, matched depth, work counter and serialized byte."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import paper_2602_04936_b200 as lg
+from golden_util import case_dataset, expected_rows, sha
+
+pytestmark = pytest.mark.gpu
+
+
+def _batch_rows(b, i):
+    return b.pairs(i)
+
+
+@pytest.mark.parametrize("idx", range(16))
+def test_golden_cases(gpu, golden, idx):
+    manifest, arrays = golden
+    cases = manifest["cases"]
+    case = cases[idx]
+    name, pre = case["name"], case["name"] + "/"
+    ds = case_dataset(case)
+    qs = arrays[pre + "queries"]
+    ks = arrays[pre + "k"]
+    index = lg.build(ds)
+    # build parity: order, adjacent lcp, per-depth arena
+    assert np.array_equal(index.order, arrays[pre + "order"])
+    assert np.array_equal(index.level_offset, arrays[pre + "level_offset"])
+    if ds.n:
+        assert np.array_equal(index.native.export_adjacent_lcp().astype(np.int64), arrays[pre + "adjacent_lcp"])
+    assert index.node_count == case["node_count"]
+    assert sha(index.row_lo) == case["row_lo_sha256"]
+    assert sha(index.edge_symbol) == case["edge_symbol_sha256"]
+    index.check_invariants()
+
+    for mode in ("strict", "complete"):
+        mp = f"{pre}{mode}/"
+        digest = hashlib.sha256()
+        for k in sorted(set(ks.tolist())):
+            sel = np.flatnonzero(ks == k)
+            w = index.new_work_report()
+            b = index.query_batch(qs[sel], int(k), mode, work=w)
+            for j, i in enumerate(sel):
+                assert _batch_rows(b, j) == expected_rows(arrays, mp, i), (name, mode, i, k)
+                assert int(b.matched_depth[j]) == arrays[mp + "md"][i], (name, mode, i)
+            assert w.symbols_compared == int(arrays[mp + "sym"][sel].sum())
+            assert w.nodes_visited == int(arrays[mp + "nodes"][sel].sum())
+            assert w.queries == len(sel)
+        for i, q in enumerate(qs):  # single-query API, canonical bytes
+            w = index.new_work_report()
+            r = index.query(q, int(ks[i]), mode, work=w)
+            digest.update(r.to_bytes())
+            assert w.symbols_compared == arrays[mp + "sym"][i]
+            assert w.nodes_visited == arrays[mp + "nodes"][i]
+        assert digest.hexdigest() == case[f"{mode}_bytes_sha256"], (name, mode)
+
+    # brute-force scan kernel vs the reference oracle
+    digest = hashlib.sha256()
+    for k in sorted(set(ks.tolist())):
+        sel = np.flatnonzero(ks == k)
+        b = index.fullscan_batch(qs[sel], int(k))
+        for j, i in enumerate(sel):
+            assert _batch_rows(b, j) == expected_rows(arrays, pre + "oracle/", i), (name, "fullscan", i)
+    for i, q in enumerate(qs):
+        digest.update(lg.fullscan_top_k(ds, q, int(ks[i])).to_bytes())
+    assert digest.hexdigest() == case["oracle_bytes_sha256"]
+
+    for tal in case["tal"]:
+        tp = f"{pre}tal{tal['B']}/"
+        eng = lg.build_tal(ds, tal["B"])
+        assert eng.bucket_depth == tal["depth"] and eng.bucket_count == tal["bucket_count"]
+        assert (eng.directory is not None) == tal["has_directory"]
+        if tp + "directory" in arrays:
+            assert np.array_equal(eng.directory, arrays[tp + "directory"])
+        digest = hashlib.sha256()
+        for i, q in enumerate(qs):
+            r, rep = eng.query(q, int(ks[i]))
+            digest.update(r.to_bytes())
+            assert rep.items_scanned == arrays[tp + "items"][i]
+            assert rep.symbols_compared == arrays[tp + "sym"][i]
+            assert eng.bucket_range(q) == (arrays[tp + "lo"][i], arrays[tp + "hi"][i])
+            if eng.directory is not None:
+                assert eng.bucket_range_search(q) == eng.bucket_range_directory(q)
+        assert digest.hexdigest() == tal["bytes_sha256"], (name, tal["B"])
+        for k in sorted(set(ks.tolist())):
+            sel = np.flatnonzero(ks == k)
+            w = eng.new_work_report()
+            b = eng.query_batch(qs[sel], int(k), work=w)
+            for j, i in enumerate(sel):
+                assert _batch_rows(b, j) == expected_rows(arrays, tp, i)
+            assert w.items_scanned == int(arrays[tp + "items"][sel].sum())
+            assert w.symbols_compared == int(arrays[tp + "sym"][sel].sum())
+
+
+def test_hand_cases(gpu, golden):
+    hand = golden[0]["hand"]
+    idx = lg.build(lg.Dataset.from_rows([[0, 0], [0, 1], [1, 0]], 2))
+    assert idx.query([0, 0], 3, "complete").pairs() == [tuple(p) for p in hand["complete_3item"]]
+    r = idx.query([0, 0], 3, "strict")
+    assert r.pairs() == [tuple(p) for p in hand["strict_3item"]] and r.matched_depth == 2
+    assert idx.query([0, 0], 3, "complete").to_bytes().hex() == hand["result_bytes"]
+    two = lg.build(lg.Dataset.from_rows([[0, 1], [0, 2]], 4))
+    assert two.node_count == 4 and two.root.subtree_size == 2
+    same = lg.build(lg.Dataset.from_rows([[1, 2, 3]] * 9, 4))
+    leaf = same.root.children()[0].children()[0].children()[0]
+    assert leaf.posting.tolist() == list(range(9))
+    dup = lg.build(lg.Dataset.from_rows([[7, 7]] * 2 + [[1, 1]], 8))
+    node, depth = dup.descend([7, 7])
+    assert depth == 2 and dup.collect_top_k(node, 1).tolist() == [0]
+    ds = lg.Dataset.from_rows([[3, 3]] * 3, 4)
+    assert lg.fullscan_top_k(ds, [3, 3], 2).pairs() == [tuple(p) for p in hand["oracle_dups"]]
+
+
+def test_errors_are_reference_exceptions(gpu):
+    idx = lg.build(lg.Dataset.from_rows([[0, 1]], 4))
+    with pytest.raises(lg.InvalidInputError):
+        idx.query([0, 1], 0)
+    with pytest.raises(lg.InvalidInputError):
+        idx.query([0, 1], 2, "both")
+    with pytest.raises(lg.InvalidInputError):
+        idx.query([0], 2)
+    with pytest.raises(lg.InvalidInputError):
+        idx.query([0, 99], 2)
+    # device-side symbol validation in the batched path
+    with pytest.raises(lg.InvalidInputError):
+        idx.query_batch(np.array([[0, 1], [0, 3], [0, 9]], dtype=np.uint16), 2)
+    # the workspace error flag is cleared afterwards
+    assert idx.query_batch(np.array([[0, 1]], dtype=np.uint16), 2).pairs(0) == [(0, 2)]
+    ds = lg.generate_dataset(16, 3, 2, seed=4)
+    with pytest.raises(lg.InvalidInputError):
+        lg.build_tal(ds, 9)
+    eng = lg.build_tal(ds, 8)
+    with pytest.raises(lg.InvalidInputError):
+        eng.query([0, 1, 0], 0)
+
+
+def test_empty_and_degenerate(gpu):
+    empty = lg.build(lg.Dataset.from_rows(np.zeros((0, 5), dtype=np.uint16), 4))
+    assert empty.node_count == 1 and empty.root.subtree_size == 0
+    empty.check_invariants()
+    w = empty.new_work_report()
+    r = empty.query([0, 1, 2, 3, 0], 3, "complete", work=w)
+    assert r.pairs() == [] and r.matched_depth == 0 and w.nodes_visited == 1 and w.symbols_compared == 0
+    eng = lg.build_tal(lg.Dataset.from_rows(np.zeros((0, 6), dtype=np.uint16), 2), 4)
+    r, rep = eng.query([0, 1, 0, 1, 0, 1], 3)
+    assert r.pairs() == [] and rep.items_scanned == 0
+    zeros = lg.build_tal(lg.Dataset.from_rows(np.zeros((8, 6), dtype=np.uint16), 2), 4)
+    r, rep = zeros.query(np.array([1, 1, 0, 0, 0, 0]), 5)
+    assert r.pairs() == [] and rep.items_scanned == 0 and rep.energy_work_units == 0.0
+    ds = lg.generate_dataset(35, 8, 4, seed=10)
+    idx = lg.build(ds)
+    for k in (1, 7, 35, 60, 10**9):
+        assert len(idx.query(ds.items[0], k, "complete").indices) == min(k, 35)
+
+
+def _random_cases(seed, count):
+    rng = np.random.default_rng(seed)
+    for t in range(count):
+        n = int(rng.integers(0, 3000))
+        L = int(rng.choice([1, 2, 3, 5, 8, 13, 16, 24, 31, 32, 33, 40, 64, 100]))
+        sigma = int(rng.choice([2, 3, 4, 5, 7, 16, 17, 255, 256, 1000, 65536]))
+        yield t, n, L, sigma, str(rng.choice(["uniform", "clustered"]))
+
+
+@pytest.mark.parametrize("chunk", range(4))
+def test_random_vs_oracle(gpu, oracle_lib, chunk):
+    """Fuzz: random (n, L, sigma, k, mode) vs the pinned C oracle."""
+    for t, n, L, sigma, dist in _random_cases(1000 + chunk, 12):
+        ds = lg.generate_dataset(n, L, sigma, seed=7 * t + chunk, distribution=dist)
+        idx = lg.build(ds)
+        ot = oracle_lib.OracleTrie(ds.items, sigma)
+        assert np.array_equal(idx.order, ot.tables()[0]), (n, L, sigma)
+        qs = lg.generate_queries(ds, 48, seed=t + 99)
+        if n:
+            qs = np.vstack([qs, lg.generate_queries(ds, 48, seed=t + 98, prefix_len=L // 2)])
+        for k in (1, 3, 10, 32, 33, 70):
+            for mode in ("complete", "strict"):
+                b = idx.query_batch(qs, k, mode)
+                ids, lcps, hits, md, sym, nodes = ot.query_batch(qs, k, mode)
+                for i in range(len(qs)):
+                    exp = list(zip(ids[i, :hits[i]].tolist(), lcps[i, :hits[i]].tolist()))
+                    assert b.pairs(i) == exp, (n, L, sigma, dist, k, mode, i)
+                    assert int(b.matched_depth[i]) == md[i]
+            fb = idx.fullscan_batch(qs, k)
+            oid, olcp, oh = oracle_lib.oracle_top_k_batch(ds.items, qs, k)
+            for i in range(len(qs)):
+                assert fb.pairs(i) == list(zip(oid[i, :oh[i]].tolist(), olcp[i, :oh[i]].tolist()))
+        d = min(L, 3)
+        if sigma**d <= 1 << 26:
+            eng = lg.build_tal(ds, sigma**d)
+            ote = oracle_lib.OracleTal(ds.items, sigma, eng.bucket_depth)
+            for k in (1, 10, 40):
+                b = eng.query_batch(qs, k)
+                ids, lcps, hits, items, sym = ote.query_batch(qs, k)
+                for i in range(len(qs)):
+                    assert b.pairs(i) == list(zip(ids[i, :hits[i]].tolist(), lcps[i, :hits[i]].tolist()))
+                assert np.array_equal(b.aux[:, 0].astype(np.int64), items)
+                assert np.array_equal(b.aux[:, 1].astype(np.int64), sym)
+
+
+def test_determinism_across_builds(gpu):
+    ds = lg.generate_dataset(20_000, 20, 4, seed=20)
+    qs = lg.generate_queries(ds, 500, seed=21, prefix_len=10)
+    a, b = lg.build(ds), lg.build(ds)
+    for mode in ("strict", "complete"):
+        ra = a.query_batch(qs, 9, mode)
+        rb = b.query_batch(qs, 9, mode)
+        for i in range(len(qs)):
+            assert ra.result(i).to_bytes() == rb.result(i).to_bytes()
+        rc = a.query_batch(qs, 9, mode)
+        assert np.array_equal(ra.ids, rc.ids) and np.array_equal(ra.hits, rc.hits)
+
+
+def test_full_size_properties(gpu, oracle_lib):
+    """BASELINE config 3 (N=2M, L=32, sigma=4, k=10): indexed complete mode must
+    equal the independent full-scan kernel on every query, and the oracle on a
+    sample; the sorted order must be a stable lexicographic permutation."""
+    ds = lg.generate_dataset(2_000_000, 32, 4, seed=3)
+    idx = lg.build(ds)
+    order = idx.order
+    assert np.array_equal(np.sort(order), np.arange(ds.n))
+    keys = idx.native.export_sorted_keys()[:, 0]
+    assert np.all(keys[1:] >= keys[:-1])
+    ties = keys[1:] == keys[:-1]
+    assert np.all(order[1:][ties] > order[:-1][ties])  # stable id tiebreak
+    qs = np.vstack([lg.generate_queries(ds, 2048, seed=4), lg.generate_queries(ds, 2048, seed=5, prefix_len=16)])
+    b = idx.query_batch(qs, 10, "complete")
+    f = idx.fullscan_batch(qs, 10)
+    assert np.array_equal(b.hits, f.hits)
+    assert np.array_equal(b.ids, f.ids) and np.array_equal(b.lcps, f.lcps)
+    sample = np.r_[0:32, 2048:2080]
+    oid, olcp, oh = oracle_lib.oracle_top_k_batch(ds.items, qs[sample], 10, nthreads=8)
+    for j, i in enumerate(sample):
+        assert b.pairs(i) == list(zip(oid[j, :oh[j]].tolist(), olcp[j, :oh[j]].tolist()))
+    # strict mode: every hit has the deepest lcp, and is a prefix of complete
+    s = idx.query_batch(qs, 10, "strict")
+    for i in range(0, len(qs), 97):
+        assert s.pairs(i) == b.pairs(i)[: s.hits[i]]
+        assert all(v == s.matched_depth[i] for _, v in s.pairs(i))
+
+
+def test_device_api_with_torch(gpu):
+    import torch
+
+    ds = lg.generate_dataset(50_000, 24, 4, seed=4)
+    idx = lg.build(ds)
+    qs = lg.generate_queries(ds, 1000, seed=5, prefix_len=12)
+    host = idx.query_batch(qs, 5, "complete")
+    dq = torch.from_numpy(qs).cuda()
+    ids = torch.empty((1000, 5), dtype=torch.int32, device="cuda")
+    lcps = torch.empty((1000, 5), dtype=torch.int16, device="cuda")
+    hits = torch.empty(1000, dtype=torch.int32, device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+    idx.native.query_device(dq, 5, "complete", ids, lcps, hits, stream=stream)
+    torch.cuda.synchronize()
+    assert np.array_equal(ids.cpu().numpy().view(np.uint32), host.ids)
+    assert np.array_equal(hits.cpu().numpy(), host.hits)
