@@ -143,6 +143,89 @@ __device__ __forceinline__ void warp_offer(u64& slot, u64& thr, u64 comp, int ne
   }
 }
 
+__device__ __forceinline__ u64 umin64(u64 a, u64 b) { return a < b ? a : b; }
+__device__ __forceinline__ u64 umax64(u64 a, u64 b) { return a < b ? b : a; }
+
+// Bitonic sort of 32 values, one per lane: lane i ends with the i-th smallest.
+__device__ __forceinline__ u64 warp_sort32(u64 v) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      u64 p = __shfl_xor_sync(LCP_FULL_MASK, v, j);
+      bool keep_min = ((lane & k) == 0) == ((lane & j) == 0);
+      v = keep_min ? umin64(v, p) : umax64(v, p);
+    }
+  }
+  return v;
+}
+
+// Bitonic sort of 64 values a[lane] = v0, a[lane + 32] = v1 (ascending).
+__device__ __forceinline__ void warp_sort64(u64& v0, u64& v1) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int k = 2; k <= 64; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j == 32) {
+        u64 lo = umin64(v0, v1), hi = umax64(v0, v1);
+        v0 = lo;
+        v1 = hi;
+      } else {
+        u64 p0 = __shfl_xor_sync(LCP_FULL_MASK, v0, j);
+        u64 p1 = __shfl_xor_sync(LCP_FULL_MASK, v1, j);
+        const bool lower = (lane & j) == 0;
+        const bool up0 = (lane & k) == 0;
+        const bool up1 = ((lane + 32) & k) == 0;
+        v0 = (up0 == lower) ? umin64(v0, p0) : umax64(v0, p0);
+        v1 = (up1 == lower) ? umin64(v1, p1) : umax64(v1, p1);
+      }
+    }
+  }
+}
+
+template <int T>
+__device__ __forceinline__ u64 pick_slot(const u64 (&v)[T], int t) {
+  u64 r = ~0ull;
+#pragma unroll
+  for (int i = 0; i < T; ++i)
+    if (i == t) r = v[i];
+  return r;
+}
+
+// Candidates form one contiguous run [r0, r0 + c) of a warp-strided array
+// (item index t*32 + lane lives in comp[t] of `lane`).  Returns the run
+// sorted ascending in slot layout (lane i = i-th smallest) for c <= 64;
+// beyond that it keeps the 32 smallest via serial warp insertion.
+template <int T>
+__device__ __forceinline__ u64 sort_run(const u64 (&comp)[T], int r0, int c, int need) {
+  const int lane = lane_id();
+  const int t0 = r0 >> 5;
+  if (c <= 32) {
+    const int e = r0 + lane;
+    u64 a = __shfl_sync(LCP_FULL_MASK, pick_slot<T>(comp, t0), e & 31);
+    u64 b = __shfl_sync(LCP_FULL_MASK, pick_slot<T>(comp, t0 + 1), e & 31);
+    u64 v = lane < c ? (((e >> 5) == t0) ? a : b) : ~0ull;
+    return warp_sort32(v);
+  }
+  if (c <= 64) {
+    const int e0 = r0 + lane, e1 = r0 + 32 + lane;
+    u64 a = __shfl_sync(LCP_FULL_MASK, pick_slot<T>(comp, t0), e0 & 31);
+    u64 b = __shfl_sync(LCP_FULL_MASK, pick_slot<T>(comp, t0 + 1), e0 & 31);
+    u64 cc = __shfl_sync(LCP_FULL_MASK, pick_slot<T>(comp, t0 + 2), e0 & 31);
+    u64 v0 = ((e0 >> 5) == t0) ? a : b;
+    u64 v1 = ((e1 >> 5) == t0 + 1) ? b : cc;
+    if (32 + lane >= c) v1 = ~0ull;
+    warp_sort64(v0, v1);
+    return v0;
+  }
+  u64 slot = ~0ull, thr = ~0ull;
+#pragma unroll
+  for (int t = 0; t < T; ++t) warp_offer(slot, thr, comp[t], need);
+  return slot;
+}
+
 __device__ __forceinline__ int warp_sum(int v) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(LCP_FULL_MASK, v, o);

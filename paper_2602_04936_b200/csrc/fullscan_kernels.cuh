@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(FS_THREADS)
 
   const long long c0 = (long long)blockIdx.y * chunk;
   const long long c1 = min(n, c0 + chunk);
-  const int per_stage = FS_STAGE_BYTES / (8 * W);
+  const int per_stage = (FS_STAGE_BYTES / (8 * W)) & ~1;  // even: 16-byte aligned stages
   const long long nst = c1 > c0 ? (c1 - c0 + per_stage - 1) / per_stage : 0;
 
   if (threadIdx.x == 0) {

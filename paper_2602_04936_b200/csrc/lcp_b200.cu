@@ -711,8 +711,12 @@ static void launch_fast(const lcp_index* ix, const uint16_t* q, int count, int k
     unsigned grid = (unsigned)std::min<long long>((count + QW_WARPS - 1) / QW_WARPS,
                                                   8ll * num_sms());
     size_t smem = 16 + (size_t)dv.smem_entries * dv.W * 8;
-    k_query_warp<WMAX><<<grid, QW_THREADS, smem, st>>>(dv, q, count, k, mode, stride, ids, lcps,
-                                                       hits, md, aux, err);
+    if constexpr (WMAX == 1)
+      k_query_w1<<<grid, QW_THREADS, smem, st>>>(dv, q, count, k, mode, stride, ids, lcps, hits,
+                                                 md, aux, err);
+    else
+      k_query_warp<WMAX><<<grid, QW_THREADS, smem, st>>>(dv, q, count, k, mode, stride, ids,
+                                                         lcps, hits, md, aux, err);
   }
 }
 
@@ -857,7 +861,7 @@ int lcp_fullscan(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries
   }
   const int take = (int)std::min<long long>(k, dv.n);
   if (dv.W <= 8 && take <= FAST_KMAX) {
-    const int per_stage = FS_STAGE_BYTES / (8 * dv.W);
+    const int per_stage = (FS_STAGE_BYTES / (8 * dv.W)) & ~1;
     const long long qtiles = (count + FS_THREADS - 1) / FS_THREADS;
     const long long max_chunks = (dv.n + per_stage - 1) / per_stage;
     long long want = std::max(1ll, (4ll * num_sms() + qtiles - 1) / qtiles);

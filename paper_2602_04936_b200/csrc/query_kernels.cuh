@@ -115,7 +115,195 @@ __device__ __forceinline__ void stage_levels(const DevIndex& ix, u64* bar, u64* 
 }
 
 // ---------------------------------------------------------------------------
-// strict / complete, k <= 32, W <= WMAX <= 8: one warp per query.
+// Shared tail of the warp query kernels: R(d*) may continue past the loaded
+// window on either side; scan outward 32 keys at a time (rare at config 3).
+// ---------------------------------------------------------------------------
+template <int WMAX>
+__device__ __forceinline__ void extend_range(const DevIndex& ix, const u64 (&qk)[WMAX], int dstar,
+                                             int need, bool left, long long lo_edge, bool right,
+                                             long long hi_edge, u64& slot, u64& thr,
+                                             long long& rsize, long long& rlo) {
+  const int lane = lane_id();
+  const long long n = ix.n;
+  const int L = ix.L;
+  if (left || right) thr = __shfl_sync(LCP_FULL_MASK, slot, need - 1);
+  long long e = lo_edge;
+  bool go = left;
+  while (go) {
+    long long i = e - 32 + lane;
+    int l = i >= 0 ? lcp_at<WMAX>(ix, i, qk) : -1;
+    bool c = l >= dstar;
+    warp_offer(slot, thr, c ? make_composite(l, ix.order[i], L) : ~0ull, need);
+    unsigned m = __ballot_sync(LCP_FULL_MASK, c);
+    rsize += __popc(m);
+    if (m) rlo = e - 32 + (__ffs(m) - 1);
+    e -= 32;
+    go = m == LCP_FULL_MASK && e > 0;
+  }
+  e = hi_edge;
+  go = right;
+  while (go) {
+    long long i = e + lane;
+    int l = i < n ? lcp_at<WMAX>(ix, i, qk) : -1;
+    bool c = l >= dstar;
+    warp_offer(slot, thr, c ? make_composite(l, ix.order[i], L) : ~0ull, need);
+    unsigned m = __ballot_sync(LCP_FULL_MASK, c);
+    rsize += __popc(m);
+    e += 32;
+    go = m == LCP_FULL_MASK && e < n;
+  }
+}
+
+__device__ __forceinline__ void write_result(long long qi, int stride, int take, int L, u64 slot,
+                                             int dmax, int dstar, long long rsize, long long rlo,
+                                             u32* out_ids, uint16_t* out_lcps, int* out_hits,
+                                             uint16_t* out_md, u64* out_aux) {
+  const int lane = lane_id();
+  if (lane < take) {
+    out_ids[qi * stride + lane] = (u32)(slot & 0xffffffffull);
+    out_lcps[qi * stride + lane] = (uint16_t)(L - (int)(slot >> 32));
+  }
+  if (lane == 0) {
+    out_hits[qi] = take;
+    out_md[qi] = (uint16_t)dmax;
+    out_aux[2 * qi] = (u64)(u32)dmax | ((u64)(u32)dstar << 32);
+    out_aux[2 * qi + 1] = (u64)rsize | ((u64)rlo << 32);
+  }
+}
+
+// d* = max{d : #{window items with lcp >= d} >= need}  (binary search on d)
+template <int T>
+__device__ __forceinline__ int window_dstar(const int (&l)[T], int dmax, int need) {
+  int lo = 0, hi = dmax;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    int c = 0;
+#pragma unroll
+    for (int t = 0; t < T; ++t) c += __popc(__ballot_sync(LCP_FULL_MASK, l[t] >= mid));
+    if (c >= need) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// ---------------------------------------------------------------------------
+// strict / complete, k <= 32, W == 1 (the config-3 hot path): one warp per
+// query.  The upper search levels narrow lower_bound(q) to a 64-key leaf
+// block [b, b+64); the warp then loads the 128-key region [b-32, b+96) with
+// its ids in one coalesced round trip.  That region contains the window
+// [pos-32, pos+32) for any pos in [b, b+64], so it serves the leaf search,
+// d* and the candidate scan at once.  Candidates (lcp >= d*) form one run;
+// it is compacted to one per lane and bitonic-sorted by (L-lcp)<<32|id.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(QW_THREADS, 4)
+    k_query_w1(DevIndex ix, const uint16_t* __restrict__ queries, int count, int k, int mode,
+               int stride, u32* __restrict__ out_ids, uint16_t* __restrict__ out_lcps,
+               int* __restrict__ out_hits, uint16_t* __restrict__ out_md,
+               u64* __restrict__ out_aux, int* __restrict__ err) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  u64* bar = reinterpret_cast<u64*>(smem_raw);
+  u64* staged = reinterpret_cast<u64*>(smem_raw + 16);
+  stage_levels(ix, bar, staged);
+
+  const int lane = lane_id();
+  const int warp = threadIdx.x >> 5;
+  const long long n = ix.n;
+  const int L = ix.L;
+  const bool complete = mode == 1;
+
+  for (long long qi = (long long)blockIdx.x * QW_WARPS + warp; qi < count;
+       qi += (long long)gridDim.x * QW_WARPS) {
+    u64 qk[1];
+    if (!warp_pack_query<1>(queries + qi * L, ix, qk)) {
+      if (lane == 0) {
+        atomicOr(err, 1);
+        out_hits[qi] = 0;
+        out_md[qi] = 0;
+        out_aux[2 * qi] = 0;
+        out_aux[2 * qi + 1] = 0;
+      }
+      continue;
+    }
+    const u64 q = qk[0];
+    // upper levels: leaf block index
+    long long blk = 0;
+    for (int j = 0; j < ix.nlevels; ++j) {
+      const u64* tab = j < ix.smem_levels ? staged + ix.level_off[j] : ix.levels + ix.level_off[j];
+      const long long cnt = ix.level_cnt[j];
+      const long long base = blk * LCP_SEARCH_FANOUT;
+      const long long i0 = base + 2 * lane;
+      bool lt0 = false, lt1 = false;
+      if (i0 + 1 < cnt) {
+        ulonglong2 v = *reinterpret_cast<const ulonglong2*>(tab + i0);
+        lt0 = v.x < q;
+        lt1 = v.y < q;
+      } else if (i0 < cnt) {
+        lt0 = tab[i0] < q;
+      }
+      int c = __popc(__ballot_sync(LCP_FULL_MASK, lt0)) + __popc(__ballot_sync(LCP_FULL_MASK, lt1));
+      if (c == 0) {  // q <= every key: pos = 0 (root level only)
+        blk = 0;
+        break;
+      }
+      blk = base + c - 1;
+    }
+    // leaf region [s, s + 128), warp-strided: item t*32 + lane
+    const long long s = blk * LCP_SEARCH_FANOUT - 32;
+    u64 key[4];
+    u32 id[4];
+    bool valid[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const long long i = s + t * 32 + lane;
+      valid[t] = i >= 0 && i < n;
+      key[t] = valid[t] ? __ldg(ix.keys + i) : 0ull;
+      id[t] = valid[t] ? __ldg(ix.order + i) : 0u;
+    }
+    // (pos = max(s, 0) + #{region keys < q}; the region is a superset of
+    // the window [pos-32, pos+32), which is all d* needs, so pos itself is
+    // never materialised.)
+    int l[4];
+    int dmax = -1;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      u64 x = key[t] ^ q;
+      l[t] = valid[t] ? (x ? (__clzll((long long)x) >> ix.lb) : L) : -1;
+      dmax = max(dmax, l[t]);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) dmax = max(dmax, __shfl_xor_sync(LCP_FULL_MASK, dmax, o));
+
+    const int need = complete ? (int)min((long long)k, n) : k;
+    const int dstar = complete ? window_dstar<4>(l, dmax, need) : dmax;
+
+    u64 comp[4];
+    int cnt = 0, r0 = 128;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const bool c = l[t] >= dstar;
+      comp[t] = c ? make_composite(l[t], id[t], L) : ~0ull;
+      const unsigned m = __ballot_sync(LCP_FULL_MASK, c);
+      cnt += __popc(m);
+      if (m && r0 == 128) r0 = t * 32 + __ffs(m) - 1;
+    }
+    u64 slot = sort_run<4>(comp, r0, cnt, need);
+    u64 thr = ~0ull;
+    long long rsize = cnt, rlo = s + r0;
+    const long long first_valid = s < 0 ? -s : 0;
+    const long long end = min(s + 128, n);
+    const bool left = s > 0 && r0 == first_valid;
+    const bool right = end < n && s + r0 + cnt == end;
+    extend_range<1>(ix, qk, dstar, need, left, s, right, end, slot, thr, rsize, rlo);
+
+    const int take = (int)min((long long)need, rsize);
+    write_result(qi, stride, take, L, slot, dmax, dstar, rsize, rlo, out_ids, out_lcps, out_hits,
+                 out_md, out_aux);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// strict / complete, k <= 32, 2 <= W <= WMAX <= 8: one warp per query;
+// 64-ary search to pos, then the 64-key window [pos-32, pos+32).
 // ---------------------------------------------------------------------------
 template <int WMAX>
 __global__ void __launch_bounds__(QW_THREADS, 4)
@@ -148,85 +336,43 @@ __global__ void __launch_bounds__(QW_THREADS, 4)
       continue;
     }
     const long long pos = warp_lower_bound<WMAX>(ix, staged, qk);
-
-    // 64-key window around pos
-    const long long wlo = pos >= 32 ? pos - 32 : 0;
-    const long long whi = pos + 32 <= n ? pos + 32 : n;
-    const long long i0 = wlo + lane, i1 = wlo + 32 + lane;
-    const int l0 = i0 < whi ? lcp_at<WMAX>(ix, i0, qk) : -1;
-    const int l1 = i1 < whi ? lcp_at<WMAX>(ix, i1, qk) : -1;
-    int dmax = max(l0, l1);
+    const long long s = pos - 32;  // window [s, s+64), warp-strided
+    int l[2];
+    u32 id[2];
+    int dmax = -1;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const long long i = s + t * 32 + lane;
+      const bool ok = i >= 0 && i < n;
+      l[t] = ok ? lcp_at<WMAX>(ix, i, qk) : -1;
+      id[t] = ok ? ix.order[i] : 0u;
+      dmax = max(dmax, l[t]);
+    }
 #pragma unroll
     for (int o = 16; o; o >>= 1) dmax = max(dmax, __shfl_xor_sync(LCP_FULL_MASK, dmax, o));
-
     const int need = complete ? (int)min((long long)k, n) : k;
-    int dstar = dmax;
-    if (complete) {
-      int lo = 0, hi = dmax;
-      while (lo < hi) {
-        int mid = (lo + hi + 1) >> 1;
-        int c = __popc(__ballot_sync(LCP_FULL_MASK, l0 >= mid)) +
-                __popc(__ballot_sync(LCP_FULL_MASK, l1 >= mid));
-        if (c >= need) lo = mid;
-        else hi = mid - 1;
-      }
-      dstar = lo;
-    }
-
-    // scan R(d*): window first, then outward in 32-key chunks
-    u64 slot = ~0ull, thr = ~0ull;
-    const bool c0 = l0 >= dstar, c1 = l1 >= dstar;
-    u64 comp0 = c0 ? make_composite(l0, ix.order[i0], L) : ~0ull;
-    u64 comp1 = c1 ? make_composite(l1, ix.order[i1], L) : ~0ull;
-    warp_offer(slot, thr, comp0, need);
-    warp_offer(slot, thr, comp1, need);
-    long long rsize = __popc(__ballot_sync(LCP_FULL_MASK, c0)) + __popc(__ballot_sync(LCP_FULL_MASK, c1));
-    long long rlo = c0 ? i0 : (c1 ? i1 : n);  // first row of R(d*) (warp-min below)
-
-    // left: the window's first key is in R(d*) -> range continues below wlo
-    bool go = wlo > 0 && __shfl_sync(LCP_FULL_MASK, l0, 0) >= dstar;
-    long long e = wlo;
-    while (go) {
-      long long i = e - 32 + lane;
-      int l = i >= 0 ? lcp_at<WMAX>(ix, i, qk) : -1;
-      bool c = l >= dstar;
-      warp_offer(slot, thr, c ? make_composite(l, ix.order[i], L) : ~0ull, need);
-      unsigned m = __ballot_sync(LCP_FULL_MASK, c);
-      rsize += __popc(m);
-      if (c) rlo = min(rlo, i);
-      e -= 32;
-      go = m == LCP_FULL_MASK && e > 0;
-    }
-    // right: the window's last key is in R(d*) -> range continues at whi
-    const int last_lane = (int)((whi - 1 - wlo) & 31);
-    const int l_last = (whi - 1 - wlo) >= 32 ? __shfl_sync(LCP_FULL_MASK, l1, last_lane)
-                                              : __shfl_sync(LCP_FULL_MASK, l0, last_lane);
-    go = whi < n && l_last >= dstar;
-    e = whi;
-    while (go) {
-      long long i = e + lane;
-      int l = i < n ? lcp_at<WMAX>(ix, i, qk) : -1;
-      bool c = l >= dstar;
-      warp_offer(slot, thr, c ? make_composite(l, ix.order[i], L) : ~0ull, need);
-      unsigned m = __ballot_sync(LCP_FULL_MASK, c);
-      rsize += __popc(m);
-      e += 32;
-      go = m == LCP_FULL_MASK && e < n;
-    }
-
+    const int dstar = complete ? window_dstar<2>(l, dmax, need) : dmax;
+    u64 comp[2];
+    int cnt = 0, r0 = 64;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) rlo = min(rlo, __shfl_xor_sync(LCP_FULL_MASK, rlo, o));
+    for (int t = 0; t < 2; ++t) {
+      const bool c = l[t] >= dstar;
+      comp[t] = c ? make_composite(l[t], id[t], L) : ~0ull;
+      const unsigned m = __ballot_sync(LCP_FULL_MASK, c);
+      cnt += __popc(m);
+      if (m && r0 == 64) r0 = t * 32 + __ffs(m) - 1;
+    }
+    u64 slot = sort_run<2>(comp, r0, cnt, need);
+    u64 thr = ~0ull;
+    long long rsize = cnt, rlo = s + r0;
+    const long long first_valid = s < 0 ? -s : 0;
+    const long long end = min(s + 64, n);
+    const bool left = s > 0 && r0 == first_valid;
+    const bool right = end < n && s + r0 + cnt == end;
+    extend_range<WMAX>(ix, qk, dstar, need, left, s, right, end, slot, thr, rsize, rlo);
     const int take = (int)min((long long)need, rsize);
-    if (lane < take) {
-      out_ids[qi * stride + lane] = (u32)(slot & 0xffffffffull);
-      out_lcps[qi * stride + lane] = (uint16_t)(L - (int)(slot >> 32));
-    }
-    if (lane == 0) {
-      out_hits[qi] = take;
-      out_md[qi] = (uint16_t)dmax;
-      out_aux[2 * qi] = (u64)(u32)dmax | ((u64)(u32)dstar << 32);
-      out_aux[2 * qi + 1] = (u64)rsize | ((u64)rlo << 32);
-    }
+    write_result(qi, stride, take, L, slot, dmax, dstar, rsize, rlo, out_ids, out_lcps, out_hits,
+                 out_md, out_aux);
   }
 }
 
