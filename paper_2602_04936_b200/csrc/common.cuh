@@ -36,6 +36,7 @@ struct DevIndex {
   int L, W, b, lb, spw, sigma;
   int tal_depth;           // -1 when no TAL structure
   long long tal_buckets;   // sigma**tal_depth
+  int idbits;              // id bits of the compact u32 composite (32: use u64)
 };
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
@@ -117,25 +118,45 @@ __device__ __forceinline__ u64 make_composite(int lcp, u32 id, int L) {
   return ((u64)(u32)(L - lcp) << 32) | (u64)id;
 }
 
+// Compact composite: (L - lcp) << idbits | id in 32 bits when
+// n <= 2**idbits and L < 2**(32 - idbits) (config 3: 6 + 26 bits); the
+// order is the same as the u64 form, so it is used for selection only.
+template <typename C>
+__device__ __forceinline__ C make_comp(int lcp, u32 id, int L, int idbits) {
+  return ((C)(u32)(L - lcp) << idbits) | (C)id;
+}
+
+template <typename C>
+__device__ __forceinline__ u64 widen_comp(C c, int idbits) {
+  if constexpr (sizeof(C) == 8) {
+    return c;
+  } else {
+    if (c == ~C(0)) return ~0ull;
+    return ((u64)(c >> idbits) << 32) | (u64)(c & ((1u << idbits) - 1u));
+  }
+}
+
 // ---- warp top-k (slot i on lane i holds the i-th smallest) ---------------
 
-__device__ __forceinline__ void warp_insert(u64& slot, u64 c) {
+template <typename C>
+__device__ __forceinline__ void warp_insert(C& slot, C c) {
   const int lane = lane_id();
   unsigned lt = __ballot_sync(LCP_FULL_MASK, slot < c);
   int p = __popc(lt);
-  u64 up = __shfl_up_sync(LCP_FULL_MASK, slot, 1);
+  C up = __shfl_up_sync(LCP_FULL_MASK, slot, 1);
   if (lane > p) slot = up;
   else if (lane == p) slot = c;
 }
 
-// Offer one candidate per lane (UINT64_MAX = none); keeps the `need`
+// Offer one candidate per lane (all-ones = none); keeps the `need`
 // smallest.  thr caches slot[need-1].
-__device__ __forceinline__ void warp_offer(u64& slot, u64& thr, u64 comp, int need) {
+template <typename C>
+__device__ __forceinline__ void warp_offer(C& slot, C& thr, C comp, int need) {
   unsigned m = __ballot_sync(LCP_FULL_MASK, comp < thr);
   while (m) {
     int src = __ffs(m) - 1;
     m &= m - 1;
-    u64 c = __shfl_sync(LCP_FULL_MASK, comp, src);
+    C c = __shfl_sync(LCP_FULL_MASK, comp, src);
     if (c < thr) {
       warp_insert(slot, c);
       thr = __shfl_sync(LCP_FULL_MASK, slot, need - 1);
@@ -143,51 +164,55 @@ __device__ __forceinline__ void warp_offer(u64& slot, u64& thr, u64 comp, int ne
   }
 }
 
-__device__ __forceinline__ u64 umin64(u64 a, u64 b) { return a < b ? a : b; }
-__device__ __forceinline__ u64 umax64(u64 a, u64 b) { return a < b ? b : a; }
+template <typename C>
+__device__ __forceinline__ C cmin(C a, C b) { return a < b ? a : b; }
+template <typename C>
+__device__ __forceinline__ C cmax(C a, C b) { return a < b ? b : a; }
 
 // Bitonic sort of 32 values, one per lane: lane i ends with the i-th smallest.
-__device__ __forceinline__ u64 warp_sort32(u64 v) {
+template <typename C>
+__device__ __forceinline__ C warp_sort32(C v) {
   const int lane = lane_id();
 #pragma unroll
   for (int k = 2; k <= 32; k <<= 1) {
 #pragma unroll
     for (int j = k >> 1; j > 0; j >>= 1) {
-      u64 p = __shfl_xor_sync(LCP_FULL_MASK, v, j);
+      C p = __shfl_xor_sync(LCP_FULL_MASK, v, j);
       bool keep_min = ((lane & k) == 0) == ((lane & j) == 0);
-      v = keep_min ? umin64(v, p) : umax64(v, p);
+      v = keep_min ? cmin(v, p) : cmax(v, p);
     }
   }
   return v;
 }
 
 // Bitonic sort of 64 values a[lane] = v0, a[lane + 32] = v1 (ascending).
-__device__ __forceinline__ void warp_sort64(u64& v0, u64& v1) {
+template <typename C>
+__device__ __forceinline__ void warp_sort64(C& v0, C& v1) {
   const int lane = lane_id();
 #pragma unroll
   for (int k = 2; k <= 64; k <<= 1) {
 #pragma unroll
     for (int j = k >> 1; j > 0; j >>= 1) {
       if (j == 32) {
-        u64 lo = umin64(v0, v1), hi = umax64(v0, v1);
+        C lo = cmin(v0, v1), hi = cmax(v0, v1);
         v0 = lo;
         v1 = hi;
       } else {
-        u64 p0 = __shfl_xor_sync(LCP_FULL_MASK, v0, j);
-        u64 p1 = __shfl_xor_sync(LCP_FULL_MASK, v1, j);
+        C p0 = __shfl_xor_sync(LCP_FULL_MASK, v0, j);
+        C p1 = __shfl_xor_sync(LCP_FULL_MASK, v1, j);
         const bool lower = (lane & j) == 0;
         const bool up0 = (lane & k) == 0;
         const bool up1 = ((lane + 32) & k) == 0;
-        v0 = (up0 == lower) ? umin64(v0, p0) : umax64(v0, p0);
-        v1 = (up1 == lower) ? umin64(v1, p1) : umax64(v1, p1);
+        v0 = (up0 == lower) ? cmin(v0, p0) : cmax(v0, p0);
+        v1 = (up1 == lower) ? cmin(v1, p1) : cmax(v1, p1);
       }
     }
   }
 }
 
-template <int T>
-__device__ __forceinline__ u64 pick_slot(const u64 (&v)[T], int t) {
-  u64 r = ~0ull;
+template <typename C, int T>
+__device__ __forceinline__ C pick_slot(const C (&v)[T], int t) {
+  C r = ~C(0);
 #pragma unroll
   for (int i = 0; i < T; ++i)
     if (i == t) r = v[i];
@@ -197,30 +222,30 @@ __device__ __forceinline__ u64 pick_slot(const u64 (&v)[T], int t) {
 // Candidates form one contiguous run [r0, r0 + c) of a warp-strided array
 // (item index t*32 + lane lives in comp[t] of `lane`).  Returns the run
 // sorted ascending in slot layout (lane i = i-th smallest) for c <= 64;
-// beyond that it keeps the 32 smallest via serial warp insertion.
-template <int T>
-__device__ __forceinline__ u64 sort_run(const u64 (&comp)[T], int r0, int c, int need) {
+// beyond that it keeps the `need` smallest via serial warp insertion.
+template <typename C, int T>
+__device__ __forceinline__ C sort_run(const C (&comp)[T], int r0, int c, int need) {
   const int lane = lane_id();
   const int t0 = r0 >> 5;
   if (c <= 32) {
     const int e = r0 + lane;
-    u64 a = __shfl_sync(LCP_FULL_MASK, pick_slot<T>(comp, t0), e & 31);
-    u64 b = __shfl_sync(LCP_FULL_MASK, pick_slot<T>(comp, t0 + 1), e & 31);
-    u64 v = lane < c ? (((e >> 5) == t0) ? a : b) : ~0ull;
+    C a = __shfl_sync(LCP_FULL_MASK, pick_slot<C, T>(comp, t0), e & 31);
+    C b = __shfl_sync(LCP_FULL_MASK, pick_slot<C, T>(comp, t0 + 1), e & 31);
+    C v = lane < c ? (((e >> 5) == t0) ? a : b) : ~C(0);
     return warp_sort32(v);
   }
   if (c <= 64) {
     const int e0 = r0 + lane, e1 = r0 + 32 + lane;
-    u64 a = __shfl_sync(LCP_FULL_MASK, pick_slot<T>(comp, t0), e0 & 31);
-    u64 b = __shfl_sync(LCP_FULL_MASK, pick_slot<T>(comp, t0 + 1), e0 & 31);
-    u64 cc = __shfl_sync(LCP_FULL_MASK, pick_slot<T>(comp, t0 + 2), e0 & 31);
-    u64 v0 = ((e0 >> 5) == t0) ? a : b;
-    u64 v1 = ((e1 >> 5) == t0 + 1) ? b : cc;
-    if (32 + lane >= c) v1 = ~0ull;
+    C a = __shfl_sync(LCP_FULL_MASK, pick_slot<C, T>(comp, t0), e0 & 31);
+    C b = __shfl_sync(LCP_FULL_MASK, pick_slot<C, T>(comp, t0 + 1), e0 & 31);
+    C cc = __shfl_sync(LCP_FULL_MASK, pick_slot<C, T>(comp, t0 + 2), e0 & 31);
+    C v0 = ((e0 >> 5) == t0) ? a : b;
+    C v1 = ((e1 >> 5) == t0 + 1) ? b : cc;
+    if (32 + lane >= c) v1 = ~C(0);
     warp_sort64(v0, v1);
     return v0;
   }
-  u64 slot = ~0ull, thr = ~0ull;
+  C slot = ~C(0), thr = ~C(0);
 #pragma unroll
   for (int t = 0; t < T; ++t) warp_offer(slot, thr, comp[t], need);
   return slot;

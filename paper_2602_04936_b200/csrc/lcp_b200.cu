@@ -7,6 +7,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -414,6 +415,16 @@ int lcp_index_build(const uint16_t* rows, int64_t n, int32_t length, int32_t sig
   dv.spw = 64 / dv.b;
   dv.W = (length + dv.spw - 1) / dv.spw;
   dv.tal_depth = -1;
+  {
+    // compact u32 composite: (L - lcp) needs ceil(log2(L + 1)) bits, ids the rest
+    int lbits = 0;
+    while ((1 << lbits) < length + 1) ++lbits;
+    const int idb = 32 - lbits;
+    dv.idbits = (idb >= 1 && n <= (1ll << idb)) ? idb : 32;
+    // test hook: exercise the u64 selection path on small inputs
+    const char* wide = getenv("LCP_FORCE_WIDE_COMPOSITE");
+    if (wide && wide[0] == '1') dv.idbits = 32;
+  }
   if (n == 0) {
     if (tal_depth >= 0) {
       ix->tal_depth = tal_depth;
@@ -711,9 +722,14 @@ static void launch_fast(const lcp_index* ix, const uint16_t* q, int count, int k
     unsigned grid = (unsigned)std::min<long long>((count + QW_WARPS - 1) / QW_WARPS,
                                                   8ll * num_sms());
     size_t smem = 16 + (size_t)dv.smem_entries * dv.W * 8;
-    if constexpr (WMAX == 1)
-      k_query_w1<<<grid, QW_THREADS, smem, st>>>(dv, q, count, k, mode, stride, ids, lcps, hits,
-                                                 md, aux, err);
+    if constexpr (WMAX == 1) {
+      if (dv.idbits < 32)
+        k_query_w1<u32><<<grid, QW_THREADS, smem, st>>>(dv, q, count, k, mode, stride, ids, lcps,
+                                                        hits, md, aux, err);
+      else
+        k_query_w1<u64><<<grid, QW_THREADS, smem, st>>>(dv, q, count, k, mode, stride, ids, lcps,
+                                                        hits, md, aux, err);
+    }
     else
       k_query_warp<WMAX><<<grid, QW_THREADS, smem, st>>>(dv, q, count, k, mode, stride, ids,
                                                          lcps, hits, md, aux, err);

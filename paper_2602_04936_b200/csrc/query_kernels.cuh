@@ -44,6 +44,22 @@ __device__ __forceinline__ bool warp_pack_query(const uint16_t* __restrict__ qro
   return !__any_sync(LCP_FULL_MASK, bad);
 }
 
+// W == 1: every lane packs its symbols, two REDUX.OR combine the halves.
+__device__ __forceinline__ bool warp_pack_w1(const uint16_t* __restrict__ qrow, const DevIndex& ix,
+                                             u64& q) {
+  u64 v = 0;
+  bool bad = false;
+  for (int j = lane_id(); j < ix.L; j += 32) {
+    u32 s = qrow[j];
+    bad |= (int)s >= ix.sigma;
+    v |= (u64)s << sym_shift(j, ix);
+  }
+  const u32 lo = __reduce_or_sync(LCP_FULL_MASK, (u32)v);
+  const u32 hi = __reduce_or_sync(LCP_FULL_MASK, (u32)(v >> 32));
+  q = ((u64)hi << 32) | lo;
+  return !__any_sync(LCP_FULL_MASK, bad);
+}
+
 // lower_bound(keys, q) by a 64-ary search: every level is one coalesced
 // 64-separator read per warp (2 per lane) + 2 ballots.  Top levels come
 // from shared memory (staged by TMA bulk copy), the rest from L2/HBM.
@@ -99,7 +115,9 @@ __device__ __forceinline__ int lcp_at(const DevIndex& ix, long long i, const u64
 }
 
 // Stage the top search levels into shared memory with one TMA bulk copy.
-__device__ __forceinline__ void stage_levels(const DevIndex& ix, u64* bar, u64* staged) {
+// stage_issue starts the copy; stage_wait blocks on its mbarrier (phase 0),
+// so warps can load and pack their first query while the copy is in flight.
+__device__ __forceinline__ void stage_issue(const DevIndex& ix, u64* bar, u64* staged) {
   if (ix.smem_levels <= 0) return;
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
@@ -111,29 +129,38 @@ __device__ __forceinline__ void stage_levels(const DevIndex& ix, u64* bar, u64* 
     mbar_arrive_expect_tx(bar, bytes);
     bulk_g2s(staged, ix.levels, bytes, bar);
   }
-  mbar_wait(bar, 0);
+}
+
+__device__ __forceinline__ void stage_wait(const DevIndex& ix, u64* bar) {
+  if (ix.smem_levels > 0) mbar_wait(bar, 0);
+}
+
+__device__ __forceinline__ void stage_levels(const DevIndex& ix, u64* bar, u64* staged) {
+  stage_issue(ix, bar, staged);
+  stage_wait(ix, bar);
 }
 
 // ---------------------------------------------------------------------------
 // Shared tail of the warp query kernels: R(d*) may continue past the loaded
 // window on either side; scan outward 32 keys at a time (rare at config 3).
 // ---------------------------------------------------------------------------
-template <int WMAX>
+template <typename C, int WMAX>
 __device__ __forceinline__ void extend_range(const DevIndex& ix, const u64 (&qk)[WMAX], int dstar,
                                              int need, bool left, long long lo_edge, bool right,
-                                             long long hi_edge, u64& slot, u64& thr,
+                                             long long hi_edge, int idbits, C& slot,
                                              long long& rsize, long long& rlo) {
   const int lane = lane_id();
   const long long n = ix.n;
   const int L = ix.L;
-  if (left || right) thr = __shfl_sync(LCP_FULL_MASK, slot, need - 1);
+  if (!(left || right)) return;
+  C thr = __shfl_sync(LCP_FULL_MASK, slot, need - 1);
   long long e = lo_edge;
   bool go = left;
   while (go) {
     long long i = e - 32 + lane;
     int l = i >= 0 ? lcp_at<WMAX>(ix, i, qk) : -1;
     bool c = l >= dstar;
-    warp_offer(slot, thr, c ? make_composite(l, ix.order[i], L) : ~0ull, need);
+    warp_offer(slot, thr, c ? make_comp<C>(l, ix.order[i], L, idbits) : ~C(0), need);
     unsigned m = __ballot_sync(LCP_FULL_MASK, c);
     rsize += __popc(m);
     if (m) rlo = e - 32 + (__ffs(m) - 1);
@@ -146,7 +173,7 @@ __device__ __forceinline__ void extend_range(const DevIndex& ix, const u64 (&qk)
     long long i = e + lane;
     int l = i < n ? lcp_at<WMAX>(ix, i, qk) : -1;
     bool c = l >= dstar;
-    warp_offer(slot, thr, c ? make_composite(l, ix.order[i], L) : ~0ull, need);
+    warp_offer(slot, thr, c ? make_comp<C>(l, ix.order[i], L, idbits) : ~C(0), need);
     unsigned m = __ballot_sync(LCP_FULL_MASK, c);
     rsize += __popc(m);
     e += 32;
@@ -154,14 +181,16 @@ __device__ __forceinline__ void extend_range(const DevIndex& ix, const u64 (&qk)
   }
 }
 
-__device__ __forceinline__ void write_result(long long qi, int stride, int take, int L, u64 slot,
-                                             int dmax, int dstar, long long rsize, long long rlo,
-                                             u32* out_ids, uint16_t* out_lcps, int* out_hits,
-                                             uint16_t* out_md, u64* out_aux) {
+template <typename C>
+__device__ __forceinline__ void write_result(long long qi, int stride, int take, int L, C slot,
+                                             int idbits, int dmax, int dstar, long long rsize,
+                                             long long rlo, u32* out_ids, uint16_t* out_lcps,
+                                             int* out_hits, uint16_t* out_md, u64* out_aux) {
   const int lane = lane_id();
   if (lane < take) {
-    out_ids[qi * stride + lane] = (u32)(slot & 0xffffffffull);
-    out_lcps[qi * stride + lane] = (uint16_t)(L - (int)(slot >> 32));
+    const u64 w = widen_comp<C>(slot, idbits);
+    out_ids[qi * stride + lane] = (u32)(w & 0xffffffffull);
+    out_lcps[qi * stride + lane] = (uint16_t)(L - (int)(w >> 32));
   }
   if (lane == 0) {
     out_hits[qi] = take;
@@ -177,9 +206,10 @@ __device__ __forceinline__ int window_dstar(const int (&l)[T], int dmax, int nee
   int lo = 0, hi = dmax;
   while (lo < hi) {
     int mid = (lo + hi + 1) >> 1;
-    int c = 0;
+    u32 mine = 0;
 #pragma unroll
-    for (int t = 0; t < T; ++t) c += __popc(__ballot_sync(LCP_FULL_MASK, l[t] >= mid));
+    for (int t = 0; t < T; ++t) mine += l[t] >= mid;
+    const int c = (int)__reduce_add_sync(LCP_FULL_MASK, mine);
     if (c >= need) lo = mid;
     else hi = mid - 1;
   }
@@ -195,6 +225,7 @@ __device__ __forceinline__ int window_dstar(const int (&l)[T], int dmax, int nee
 // d* and the candidate scan at once.  Candidates (lcp >= d*) form one run;
 // it is compacted to one per lane and bitonic-sorted by (L-lcp)<<32|id.
 // ---------------------------------------------------------------------------
+template <typename C>
 __global__ void __launch_bounds__(QW_THREADS, 4)
     k_query_w1(DevIndex ix, const uint16_t* __restrict__ queries, int count, int k, int mode,
                int stride, u32* __restrict__ out_ids, uint16_t* __restrict__ out_lcps,
@@ -203,7 +234,7 @@ __global__ void __launch_bounds__(QW_THREADS, 4)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   u64* bar = reinterpret_cast<u64*>(smem_raw);
   u64* staged = reinterpret_cast<u64*>(smem_raw + 16);
-  stage_levels(ix, bar, staged);
+  stage_issue(ix, bar, staged);
 
   const int lane = lane_id();
   const int warp = threadIdx.x >> 5;
@@ -214,7 +245,9 @@ __global__ void __launch_bounds__(QW_THREADS, 4)
   for (long long qi = (long long)blockIdx.x * QW_WARPS + warp; qi < count;
        qi += (long long)gridDim.x * QW_WARPS) {
     u64 qk[1];
-    if (!warp_pack_query<1>(queries + qi * L, ix, qk)) {
+    const bool ok = warp_pack_w1(queries + qi * L, ix, qk[0]);
+    stage_wait(ix, bar);  // first iteration: the query load overlaps the copy
+    if (!ok) {
       if (lane == 0) {
         atomicOr(err, 1);
         out_hits[qi] = 0;
@@ -232,22 +265,23 @@ __global__ void __launch_bounds__(QW_THREADS, 4)
       const long long cnt = ix.level_cnt[j];
       const long long base = blk * LCP_SEARCH_FANOUT;
       const long long i0 = base + 2 * lane;
-      bool lt0 = false, lt1 = false;
+      u32 lt = 0;
       if (i0 + 1 < cnt) {
         ulonglong2 v = *reinterpret_cast<const ulonglong2*>(tab + i0);
-        lt0 = v.x < q;
-        lt1 = v.y < q;
+        lt = (u32)(v.x < q) + (u32)(v.y < q);
       } else if (i0 < cnt) {
-        lt0 = tab[i0] < q;
+        lt = tab[i0] < q;
       }
-      int c = __popc(__ballot_sync(LCP_FULL_MASK, lt0)) + __popc(__ballot_sync(LCP_FULL_MASK, lt1));
+      const int c = (int)__reduce_add_sync(LCP_FULL_MASK, lt);
       if (c == 0) {  // q <= every key: pos = 0 (root level only)
         blk = 0;
         break;
       }
       blk = base + c - 1;
     }
-    // leaf region [s, s + 128), warp-strided: item t*32 + lane
+    // leaf region [s, s + 128), warp-strided: item t*32 + lane.  It holds
+    // the window [pos-32, pos+32) for pos = max(s,0) + #{region keys < q},
+    // which is all d* needs, so pos itself is never materialised.
     const long long s = blk * LCP_SEARCH_FANOUT - 32;
     u64 key[4];
     u32 id[4];
@@ -259,9 +293,6 @@ __global__ void __launch_bounds__(QW_THREADS, 4)
       key[t] = valid[t] ? __ldg(ix.keys + i) : 0ull;
       id[t] = valid[t] ? __ldg(ix.order + i) : 0u;
     }
-    // (pos = max(s, 0) + #{region keys < q}; the region is a superset of
-    // the window [pos-32, pos+32), which is all d* needs, so pos itself is
-    // never materialised.)
     int l[4];
     int dmax = -1;
 #pragma unroll
@@ -270,34 +301,32 @@ __global__ void __launch_bounds__(QW_THREADS, 4)
       l[t] = valid[t] ? (x ? (__clzll((long long)x) >> ix.lb) : L) : -1;
       dmax = max(dmax, l[t]);
     }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) dmax = max(dmax, __shfl_xor_sync(LCP_FULL_MASK, dmax, o));
+    dmax = (int)__reduce_max_sync(LCP_FULL_MASK, (unsigned)(dmax + 1)) - 1;
 
     const int need = complete ? (int)min((long long)k, n) : k;
     const int dstar = complete ? window_dstar<4>(l, dmax, need) : dmax;
 
-    u64 comp[4];
+    C comp[4];
     int cnt = 0, r0 = 128;
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       const bool c = l[t] >= dstar;
-      comp[t] = c ? make_composite(l[t], id[t], L) : ~0ull;
+      comp[t] = c ? make_comp<C>(l[t], id[t], L, ix.idbits) : ~C(0);
       const unsigned m = __ballot_sync(LCP_FULL_MASK, c);
       cnt += __popc(m);
       if (m && r0 == 128) r0 = t * 32 + __ffs(m) - 1;
     }
-    u64 slot = sort_run<4>(comp, r0, cnt, need);
-    u64 thr = ~0ull;
+    C slot = sort_run<C, 4>(comp, r0, cnt, need);
     long long rsize = cnt, rlo = s + r0;
     const long long first_valid = s < 0 ? -s : 0;
     const long long end = min(s + 128, n);
     const bool left = s > 0 && r0 == first_valid;
     const bool right = end < n && s + r0 + cnt == end;
-    extend_range<1>(ix, qk, dstar, need, left, s, right, end, slot, thr, rsize, rlo);
+    extend_range<C, 1>(ix, qk, dstar, need, left, s, right, end, ix.idbits, slot, rsize, rlo);
 
     const int take = (int)min((long long)need, rsize);
-    write_result(qi, stride, take, L, slot, dmax, dstar, rsize, rlo, out_ids, out_lcps, out_hits,
-                 out_md, out_aux);
+    write_result<C>(qi, stride, take, L, slot, ix.idbits, dmax, dstar, rsize, rlo, out_ids,
+                    out_lcps, out_hits, out_md, out_aux);
   }
 }
 
@@ -357,22 +386,21 @@ __global__ void __launch_bounds__(QW_THREADS, 4)
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
       const bool c = l[t] >= dstar;
-      comp[t] = c ? make_composite(l[t], id[t], L) : ~0ull;
+      comp[t] = c ? make_comp<u64>(l[t], id[t], L, 32) : ~0ull;
       const unsigned m = __ballot_sync(LCP_FULL_MASK, c);
       cnt += __popc(m);
       if (m && r0 == 64) r0 = t * 32 + __ffs(m) - 1;
     }
-    u64 slot = sort_run<2>(comp, r0, cnt, need);
-    u64 thr = ~0ull;
+    u64 slot = sort_run<u64, 2>(comp, r0, cnt, need);
     long long rsize = cnt, rlo = s + r0;
     const long long first_valid = s < 0 ? -s : 0;
     const long long end = min(s + 64, n);
     const bool left = s > 0 && r0 == first_valid;
     const bool right = end < n && s + r0 + cnt == end;
-    extend_range<WMAX>(ix, qk, dstar, need, left, s, right, end, slot, thr, rsize, rlo);
+    extend_range<u64, WMAX>(ix, qk, dstar, need, left, s, right, end, 32, slot, rsize, rlo);
     const int take = (int)min((long long)need, rsize);
-    write_result(qi, stride, take, L, slot, dmax, dstar, rsize, rlo, out_ids, out_lcps, out_hits,
-                 out_md, out_aux);
+    write_result<u64>(qi, stride, take, L, slot, 32, dmax, dstar, rsize, rlo, out_ids, out_lcps,
+                      out_hits, out_md, out_aux);
   }
 }
 

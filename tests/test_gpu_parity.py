@@ -167,8 +167,11 @@ def _random_cases(seed, count):
 
 
 @pytest.mark.parametrize("chunk", range(4))
-def test_random_vs_oracle(gpu, oracle_lib, chunk):
-    """Fuzz: random (n, L, sigma, k, mode) vs the pinned C oracle."""
+def test_random_vs_oracle(gpu, oracle_lib, chunk, monkeypatch):
+    """Fuzz: random (n, L, sigma, k, mode) vs the pinned C oracle.  Odd chunks
+    force the 64-bit composite selection path."""
+    if chunk % 2:
+        monkeypatch.setenv("LCP_FORCE_WIDE_COMPOSITE", "1")
     for t, n, L, sigma, dist in _random_cases(1000 + chunk, 12):
         ds = lg.generate_dataset(n, L, sigma, seed=7 * t + chunk, distribution=dist)
         idx = lg.build(ds)
