@@ -20,6 +20,7 @@ typedef unsigned int u32;
 #define LCP_FULL_MASK 0xffffffffu
 #define LCP_MAX_LEVELS 12
 #define LCP_SEARCH_FANOUT 64  // k-ary search: 32 lanes x 2 separators
+#define LCP_LEAF_KEYS 32      // the last search table resolves a 32-key leaf block
 
 struct DevIndex {
   const u64* keys;        // sorted packed keys, n*W

@@ -326,9 +326,11 @@ static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, i
   }
 
   // k-ary search levels (stand-in for the trie descent, trie.py:229-256)
+  // Tables j = 0..h-1 sample every LCP_LEAF_KEYS * 64**(h-1-j)-th key; the
+  // last one resolves lower_bound(q) to a 32-key leaf block.
   int h = 0;
   {
-    long long cap = 64;
+    long long cap = LCP_LEAF_KEYS;
     while (n > cap && h < LCP_MAX_LEVELS - 1) {
       cap *= 64;
       ++h;
@@ -338,8 +340,8 @@ static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, i
   long long total = 0;
   std::vector<long long> strides(h);
   for (int j = 0; j < h; ++j) {
-    long long s = 1;
-    for (int t = 0; t < h - j; ++t) s *= 64;
+    long long s = LCP_LEAF_KEYS;
+    for (int t = 0; t < h - 1 - j; ++t) s *= 64;
     strides[j] = s;
     long long cnt = (n + s - 1) / s;
     dv.level_cnt[j] = cnt;
@@ -719,19 +721,36 @@ static void launch_fast(const lcp_index* ix, const uint16_t* q, int count, int k
     k_query_tal<WMAX><<<grid, QT_THREADS, 0, st>>>(dv, q, count, k, stride, ids, lcps, hits, md,
                                                    aux, err);
   } else {
-    unsigned grid = (unsigned)std::min<long long>((count + QW_WARPS - 1) / QW_WARPS,
-                                                  8ll * num_sms());
+    // One query per warp; spread the batch evenly over the SMs with one CTA
+    // per SM (so each SM stages the search levels once), up to 1024 threads;
+    // larger batches get more CTAs (2 x 1024 threads fit an SM).
+    const long long sms = num_sms();
+    long long wpc = std::min<long long>(32, std::max<long long>(1, (count + sms - 1) / sms));
+    const unsigned block = (unsigned)(wpc * 32);
+    unsigned grid = (unsigned)std::min<long long>((count + wpc - 1) / wpc, 4ll * sms);
     size_t smem = 16 + (size_t)dv.smem_entries * dv.W * 8;
     if constexpr (WMAX == 1) {
-      if (dv.idbits < 32)
-        k_query_w1<u32><<<grid, QW_THREADS, smem, st>>>(dv, q, count, k, mode, stride, ids, lcps,
-                                                        hits, md, aux, err);
-      else
-        k_query_w1<u64><<<grid, QW_THREADS, smem, st>>>(dv, q, count, k, mode, stride, ids, lcps,
-                                                        hits, md, aux, err);
+      // leaf region: 64 keys cover the +-need window for need <= 16, 96 keys for <= 32
+      const long long need = mode == LCP_MODE_COMPLETE ? std::min<long long>(k, dv.n) : k;
+      const bool narrow = need <= 16;
+      if (dv.idbits < 32) {
+        if (narrow)
+          k_query_w1<u32, 2><<<grid, block, smem, st>>>(dv, q, count, k, mode, stride, ids, lcps,
+                                                         hits, md, aux, err);
+        else
+          k_query_w1<u32, 3><<<grid, block, smem, st>>>(dv, q, count, k, mode, stride, ids, lcps,
+                                                         hits, md, aux, err);
+      } else {
+        if (narrow)
+          k_query_w1<u64, 2><<<grid, block, smem, st>>>(dv, q, count, k, mode, stride, ids, lcps,
+                                                         hits, md, aux, err);
+        else
+          k_query_w1<u64, 3><<<grid, block, smem, st>>>(dv, q, count, k, mode, stride, ids, lcps,
+                                                         hits, md, aux, err);
+      }
     }
     else
-      k_query_warp<WMAX><<<grid, QW_THREADS, smem, st>>>(dv, q, count, k, mode, stride, ids,
+      k_query_warp<WMAX><<<grid, block, smem, st>>>(dv, q, count, k, mode, stride, ids,
                                                          lcps, hits, md, aux, err);
   }
 }
@@ -976,5 +995,13 @@ int lcp_stream_sync(void* stream) {
   LCP_CK(cudaStreamSynchronize((cudaStream_t)stream));
   return LCP_OK;
 }
+
+#ifdef LCP_TRACE
+int lcp_debug_trace(uint64_t* host, int64_t entries) {
+  LCP_CK(cudaDeviceSynchronize());
+  LCP_CK(cudaMemcpyFromSymbol(host, lcp_trace_buf, (size_t)entries * 8));
+  return LCP_OK;
+}
+#endif
 
 }  // extern "C"

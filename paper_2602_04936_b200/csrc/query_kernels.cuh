@@ -17,8 +17,21 @@
 
 #include "common.cuh"
 
-constexpr int QW_THREADS = 256;                 // 8 warps, one query per warp
-constexpr int QW_WARPS = QW_THREADS / 32;
+constexpr int QW_MAX_THREADS = 1024;            // one CTA per SM, one query per warp
+
+#ifdef LCP_TRACE
+// Debug-only per-query stage timestamps (SM clock), compiled into the trace
+// build of tools/trace_query.py, never into the shipped library.
+__device__ unsigned long long lcp_trace_buf[65536 * 8];
+#define LCP_STAMP(qi, slot)                                                      \
+  do {                                                                          \
+    if (lane_id() == 0 && (qi) < 65536) lcp_trace_buf[(qi) * 8 + (slot)] = clock64(); \
+  } while (0)
+#else
+#define LCP_STAMP(qi, slot) \
+  do {                      \
+  } while (0)
+#endif
 constexpr int FAST_KMAX = 32;                   // warp top-k capacity
 
 // pack one query row into W words held by every lane; returns false if a
@@ -72,15 +85,18 @@ __device__ __forceinline__ long long warp_lower_bound(const DevIndex& ix, const 
   for (int j = 0;; ++j) {
     const u64* tab;
     long long cnt;
-    if (j == ix.nlevels) {
-      tab = ix.keys;
-      cnt = ix.n;
-    } else if (j < ix.smem_levels) {
+    if (j < ix.smem_levels) {
       tab = staged + ix.level_off[j] * W;
       cnt = ix.level_cnt[j];
     } else {
       tab = ix.levels + ix.level_off[j] * W;
       cnt = ix.level_cnt[j];
+    }
+    if (j == ix.nlevels) {  // leaf block: 32 keys, one per lane
+      const long long base = blk * LCP_LEAF_KEYS;
+      const long long i = base + lane;
+      const bool lt = i < ix.n && key_less<WMAX>(ix.keys + i * W, qk, ix);
+      return base + (int)__reduce_add_sync(LCP_FULL_MASK, (u32)lt);
     }
     long long base = blk * LCP_SEARCH_FANOUT;
     long long i0 = base + 2 * lane;
@@ -98,7 +114,6 @@ __device__ __forceinline__ long long warp_lower_bound(const DevIndex& ix, const 
       if (i0 + 1 < cnt) lt1 = key_less<WMAX>(tab + (i0 + 1) * W, qk, ix);
     }
     int c = __popc(__ballot_sync(LCP_FULL_MASK, lt0)) + __popc(__ballot_sync(LCP_FULL_MASK, lt1));
-    if (j == ix.nlevels) return base + c;
     if (c == 0) return 0;  // only reachable at the root level
     blk = base + c - 1;
   }
@@ -225,8 +240,22 @@ __device__ __forceinline__ int window_dstar(const int (&l)[T], int dmax, int nee
 // d* and the candidate scan at once.  Candidates (lcp >= d*) form one run;
 // it is compacted to one per lane and bitonic-sorted by (L-lcp)<<32|id.
 // ---------------------------------------------------------------------------
-template <typename C>
-__global__ void __launch_bounds__(QW_THREADS, 4)
+// One 64-ary search step over a level table: number of entries < q among
+// the 64 separators [blk*64, blk*64+64) (two per lane).
+__device__ __forceinline__ int level_count(const u64* __restrict__ tab, int cnt, int blk, u64 q) {
+  const int i0 = blk * LCP_SEARCH_FANOUT + 2 * lane_id();
+  u32 lt = 0;
+  if (i0 + 1 < cnt) {
+    const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(tab + i0);
+    lt = (u32)(v.x < q) + (u32)(v.y < q);
+  } else if (i0 < cnt) {
+    lt = tab[i0] < q;
+  }
+  return (int)__reduce_add_sync(LCP_FULL_MASK, lt);
+}
+
+template <typename C, int T>
+__global__ void __launch_bounds__(QW_MAX_THREADS, 1)
     k_query_w1(DevIndex ix, const uint16_t* __restrict__ queries, int count, int k, int mode,
                int stride, u32* __restrict__ out_ids, uint16_t* __restrict__ out_lcps,
                int* __restrict__ out_hits, uint16_t* __restrict__ out_md,
@@ -238,16 +267,32 @@ __global__ void __launch_bounds__(QW_THREADS, 4)
 
   const int lane = lane_id();
   const int warp = threadIdx.x >> 5;
-  const long long n = ix.n;
+  const int warps = blockDim.x >> 5;
+  const int n = (int)ix.n;  // < 2**31 by contract
   const int L = ix.L;
+  const int b = ix.b, lb = ix.lb;
+  const int idbits = ix.idbits;
   const bool complete = mode == 1;
+  const int need = complete ? min(k, n) : k;
+  const u64* __restrict__ keys = ix.keys;
+  const u32* __restrict__ order = ix.order;
+  // W == 1  =>  L <= 64: lane packs symbols lane and lane + 32
+  const bool has0 = lane < L, has1 = lane + 32 < L;
+  const int sh0 = 64 - b * (lane + 1), sh1 = 64 - b * (lane + 33);
 
-  for (long long qi = (long long)blockIdx.x * QW_WARPS + warp; qi < count;
-       qi += (long long)gridDim.x * QW_WARPS) {
-    u64 qk[1];
-    const bool ok = warp_pack_w1(queries + qi * L, ix, qk[0]);
+  for (int qi = blockIdx.x * warps + warp; qi < count; qi += gridDim.x * warps) {
+    LCP_STAMP(qi, 0);
+    const uint16_t* qrow = queries + (size_t)qi * L;
+    const u32 s0 = has0 ? qrow[lane] : 0u;
+    const u32 s1 = has1 ? qrow[lane + 32] : 0u;
+    const bool bad = (has0 && (int)s0 >= ix.sigma) || (has1 && (int)s1 >= ix.sigma);
+    const u64 v = (has0 ? (u64)s0 << sh0 : 0ull) | (has1 ? (u64)s1 << sh1 : 0ull);
+    const u64 q = ((u64)__reduce_or_sync(LCP_FULL_MASK, (u32)(v >> 32)) << 32) |
+                  (u64)__reduce_or_sync(LCP_FULL_MASK, (u32)v);
+    const bool any_bad = __any_sync(LCP_FULL_MASK, bad);
     stage_wait(ix, bar);  // first iteration: the query load overlaps the copy
-    if (!ok) {
+    LCP_STAMP(qi, 1);
+    if (any_bad) {
       if (lane == 0) {
         atomicOr(err, 1);
         out_hits[qi] = 0;
@@ -257,76 +302,99 @@ __global__ void __launch_bounds__(QW_THREADS, 4)
       }
       continue;
     }
-    const u64 q = qk[0];
-    // upper levels: leaf block index
-    long long blk = 0;
-    for (int j = 0; j < ix.nlevels; ++j) {
-      const u64* tab = j < ix.smem_levels ? staged + ix.level_off[j] : ix.levels + ix.level_off[j];
-      const long long cnt = ix.level_cnt[j];
-      const long long base = blk * LCP_SEARCH_FANOUT;
-      const long long i0 = base + 2 * lane;
-      u32 lt = 0;
-      if (i0 + 1 < cnt) {
-        ulonglong2 v = *reinterpret_cast<const ulonglong2*>(tab + i0);
-        lt = (u32)(v.x < q) + (u32)(v.y < q);
-      } else if (i0 < cnt) {
-        lt = tab[i0] < q;
-      }
-      const int c = (int)__reduce_add_sync(LCP_FULL_MASK, lt);
-      if (c == 0) {  // q <= every key: pos = 0 (root level only)
-        blk = 0;
-        break;
-      }
-      blk = base + c - 1;
+    // 64-ary search down to the 32-key leaf block holding lower_bound(q)
+    int blk = 0;
+    bool at_root_min = false;  // q <= every key (pos = 0)
+    int j = 0;
+    for (; j < ix.smem_levels; ++j) {
+      const int c = level_count(staged + (int)ix.level_off[j], (int)ix.level_cnt[j], blk, q);
+      if (c == 0) { at_root_min = true; break; }
+      blk = blk * LCP_SEARCH_FANOUT + c - 1;
     }
-    // leaf region [s, s + 128), warp-strided: item t*32 + lane.  It holds
-    // the window [pos-32, pos+32) for pos = max(s,0) + #{region keys < q},
-    // which is all d* needs, so pos itself is never materialised.
-    const long long s = blk * LCP_SEARCH_FANOUT - 32;
-    u64 key[4];
-    u32 id[4];
-    bool valid[4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const long long i = s + t * 32 + lane;
-      valid[t] = i >= 0 && i < n;
-      key[t] = valid[t] ? __ldg(ix.keys + i) : 0ull;
-      id[t] = valid[t] ? __ldg(ix.order + i) : 0u;
+    if (!at_root_min) {
+      for (; j < ix.nlevels; ++j) {
+        const int c = level_count(ix.levels + (int)ix.level_off[j], (int)ix.level_cnt[j], blk, q);
+        if (c == 0) { at_root_min = true; break; }
+        blk = blk * LCP_SEARCH_FANOUT + c - 1;
+      }
     }
-    int l[4];
+    if (at_root_min) blk = 0;
+    LCP_STAMP(qi, 2);
+    // Leaf block [B, B+32) holds pos = lower_bound(q) in (B, B+32] (or
+    // pos = 0).  The region [B-16, B+48) (T=2) / [B-32, B+64) (T=3), warp-
+    // strided (item t*32 + lane), contains the window [pos-need, pos+need)
+    // for need <= 16 / 32, which is all d* needs; pos is never materialised.
+    const int s = blk * LCP_LEAF_KEYS - (T == 2 ? 16 : 32);
+    int l[T];
+    u32 id[T];
     int dmax = -1;
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      u64 x = key[t] ^ q;
-      l[t] = valid[t] ? (x ? (__clzll((long long)x) >> ix.lb) : L) : -1;
+    for (int t = 0; t < T; ++t) {
+      const int i = s + t * 32 + lane;
+      const bool ok = (unsigned)i < (unsigned)n;
+      const u64 key = ok ? __ldg(keys + i) : 0ull;
+      id[t] = ok ? __ldg(order + i) : 0u;
+      const u64 x = key ^ q;
+      l[t] = ok ? (x ? (__clzll((long long)x) >> lb) : L) : -1;
       dmax = max(dmax, l[t]);
     }
     dmax = (int)__reduce_max_sync(LCP_FULL_MASK, (unsigned)(dmax + 1)) - 1;
+    LCP_STAMP(qi, 3);
+    const int dstar = complete ? window_dstar<T>(l, dmax, need) : dmax;
 
-    const int need = complete ? (int)min((long long)k, n) : k;
-    const int dstar = complete ? window_dstar<4>(l, dmax, need) : dmax;
-
-    C comp[4];
-    int cnt = 0, r0 = 128;
+    C comp[T];
+    int cnt = 0, r0 = 32 * T;
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
+    for (int t = 0; t < T; ++t) {
       const bool c = l[t] >= dstar;
-      comp[t] = c ? make_comp<C>(l[t], id[t], L, ix.idbits) : ~C(0);
+      comp[t] = c ? make_comp<C>(l[t], id[t], L, idbits) : ~C(0);
       const unsigned m = __ballot_sync(LCP_FULL_MASK, c);
       cnt += __popc(m);
-      if (m && r0 == 128) r0 = t * 32 + __ffs(m) - 1;
+      if (m && r0 == 32 * T) r0 = t * 32 + __ffs(m) - 1;
     }
-    C slot = sort_run<C, 4>(comp, r0, cnt, need);
-    long long rsize = cnt, rlo = s + r0;
-    const long long first_valid = s < 0 ? -s : 0;
-    const long long end = min(s + 128, n);
+    const int first_valid = s < 0 ? -s : 0;
+    const int end = min(s + 32 * T, n);
     const bool left = s > 0 && r0 == first_valid;
     const bool right = end < n && s + r0 + cnt == end;
-    extend_range<C, 1>(ix, qk, dstar, need, left, s, right, end, ix.idbits, slot, rsize, rlo);
-
+    LCP_STAMP(qi, 4);
+    if (!left && !right && cnt <= 32) {
+      // R(d*) lies inside the region: compact the run to one candidate per
+      // lane and rank it by all-pairs comparison (independent shuffles, no
+      // sorting network); the lane of rank r writes output slot r.
+      const int t0 = r0 >> 5, e = r0 + lane;
+      const C a = __shfl_sync(LCP_FULL_MASK, pick_slot<C, T>(comp, t0), e & 31);
+      const C bb = __shfl_sync(LCP_FULL_MASK, pick_slot<C, T>(comp, t0 + 1), e & 31);
+      const C cv = lane < cnt ? (((e >> 5) == t0) ? a : bb) : ~C(0);
+      int rank = 0;
+#pragma unroll 8
+      for (int jj = 0; jj < cnt; ++jj) rank += __shfl_sync(LCP_FULL_MASK, cv, jj) < cv;
+      LCP_STAMP(qi, 5);
+      const int take = min(need, cnt);
+      if (lane < cnt && rank < take) {
+        const u64 w = widen_comp<C>(cv, idbits);
+        out_ids[(size_t)qi * stride + rank] = (u32)(w & 0xffffffffull);
+        out_lcps[(size_t)qi * stride + rank] = (uint16_t)(L - (int)(w >> 32));
+      }
+      if (lane == 0) {
+        out_hits[qi] = take;
+        out_md[qi] = (uint16_t)dmax;
+        out_aux[2 * qi] = (u64)(u32)dmax | ((u64)(u32)dstar << 32);
+        out_aux[2 * qi + 1] = (u64)(u32)cnt | ((u64)(u32)(s + r0) << 32);
+      }
+      LCP_STAMP(qi, 6);
+      LCP_STAMP(qi, 7);
+      continue;
+    }
+    C slot = sort_run<C, T>(comp, r0, cnt, need);
+    LCP_STAMP(qi, 5);
+    u64 qk[1] = {q};
+    long long rsize = cnt, rlo = s + r0;
+    extend_range<C, 1>(ix, qk, dstar, need, left, s, right, end, idbits, slot, rsize, rlo);
+    LCP_STAMP(qi, 6);
     const int take = (int)min((long long)need, rsize);
-    write_result<C>(qi, stride, take, L, slot, ix.idbits, dmax, dstar, rsize, rlo, out_ids,
+    write_result<C>(qi, stride, take, L, slot, idbits, dmax, dstar, rsize, rlo, out_ids,
                     out_lcps, out_hits, out_md, out_aux);
+    LCP_STAMP(qi, 7);
   }
 }
 
@@ -335,7 +403,7 @@ __global__ void __launch_bounds__(QW_THREADS, 4)
 // 64-ary search to pos, then the 64-key window [pos-32, pos+32).
 // ---------------------------------------------------------------------------
 template <int WMAX>
-__global__ void __launch_bounds__(QW_THREADS, 4)
+__global__ void __launch_bounds__(QW_MAX_THREADS, 1)
     k_query_warp(DevIndex ix, const uint16_t* __restrict__ queries, int count, int k, int mode,
                  int stride, u32* __restrict__ out_ids, uint16_t* __restrict__ out_lcps,
                  int* __restrict__ out_hits, uint16_t* __restrict__ out_md,
@@ -351,8 +419,9 @@ __global__ void __launch_bounds__(QW_THREADS, 4)
   const int L = ix.L;
   const bool complete = mode == 1;
 
-  for (long long qi = (long long)blockIdx.x * QW_WARPS + warp; qi < count;
-       qi += (long long)gridDim.x * QW_WARPS) {
+  const int warps = blockDim.x >> 5;
+  for (long long qi = (long long)blockIdx.x * warps + warp; qi < count;
+       qi += (long long)gridDim.x * warps) {
     u64 qk[WMAX];
     if (!warp_pack_query<WMAX>(queries + qi * L, ix, qk)) {
       if (lane == 0) {
