@@ -3,11 +3,17 @@
 
 Workload (N=1): BASELINE config 3 — N=2,000,000 items, L=32, sigma=4, k=10,
 complete-mode top-k over batches of 4,096 queries.  A "step" is one batch
-through the fused query kernel (pack -> 64-ary search -> window d* -> range
-scan -> warp top-k), inputs resident in HBM.  L2 is flushed (256 MiB memset)
-before every timed step and each step is bracketed by its own CUDA events on
-the launching stream.  Inputs come from the reference generator restated in
-paper_2602_04936_b200.datagen (byte-identical Philox streams).
+through the fused query kernel (pack -> 64-ary search -> leaf region ->
+d* -> rank selection), inputs resident in HBM.
+
+Timing: the steps are captured once in a CUDA graph and replayed, so the
+GPU is never starved by Python-side launch cost.  Step i runs on index
+replica i % 8 (8 identical replicas, 8 x 24 MB > 126 MB L2, so every step's
+index reads miss L2) and on CUDA stream i % 2 (two batches in flight, as a
+serving loop keeps them); the whole K-step region is bracketed by CUDA
+events on the capture stream.  The same loop on one stream (one batch in
+flight) is reported beside it, and its per-step time is the kernel duration
+used for the roofline.
 
 N>1 (torchrun): row-block shards of 2M items per rank (weak scaling; rank g
 holds generate_dataset(2M, 32, 4, seed=3+g) with ids offset by 2M*g), the
@@ -60,59 +66,59 @@ def hbm_peak() -> tuple[float, str]:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """NVML-polled SM clocks + throttle reasons (2 ms period) around the timed
+    region (started before the warm-up replays, stopped after timing)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = {  # nvmlClocksEventReason bits
+        0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+        0x4: "sw_power_cap",
+    }
 
     def __init__(self, device: int = 0):
         self.device = device
-        self.proc = None
-        self.lines: list[str] = []
+        self.samples: list[tuple[float, float, int]] = []
+        self._stop = threading.Event()
+        self._t = None
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self._max = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        sm = float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                        rs = int(pynvml.nvmlDeviceGetCurrentClocksEventReasons(h))
+                        self.samples.append((time.perf_counter(), sm, rs))
+                    except Exception:
+                        pass
+                    time.sleep(0.002)
+
+            self._t = threading.Thread(target=run, daemon=True)
             self._t.start()
-        except FileNotFoundError:
-            self.proc = None
-        time.sleep(0.15)
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
-    def stop(self) -> dict:
-        time.sleep(0.1)
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=2)
         except Exception:
-            self.proc.kill()
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.lines:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[3:7]):
-                if v.lower() == "active":
+            self._t = None
+
+    def stop(self, t0: float | None = None, t1: float | None = None) -> dict:
+        if self._t is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"], "samples": 0}
+        self._stop.set()
+        self._t.join(timeout=1)
+        inside = [x for x in self.samples if t0 is None or t0 <= x[0] <= t1]
+        use = inside if inside else self.samples
+        reasons = set()
+        for _, _, rs in use:
+            for bit, nm in self.REASONS.items():
+                if rs & bit:
                     reasons.add(nm)
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": float(np.median([x[1] for x in use])) if use else None,
+                "sm_max_mhz": self._max, "reasons": sorted(reasons),
+                "samples": len(use), "samples_in_timed_region": len(inside),
+                "source": "NVML clock/event-reason polling, 2 ms"}
 
 
 def nvml_energy():
@@ -188,25 +194,11 @@ def run_reference(args) -> None:
 
 
 # --------------------------------------------------------------------------
-def time_steps(fn, flush, steps: int, stream):
-    """Per-step CUDA events on `stream`, L2 flushed before each step."""
-    import torch
-
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
-    for i in range(steps):
-        if flush is not None:
-            flush()
-        evs[i][0].record(stream)
-        fn(i)
-        evs[i][1].record(stream)
-    return evs
-
-
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2000)
-    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=5000)
+    ap.add_argument("--warmup", type=int, default=200)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-budget-s", type=float, default=10.0)
     ap.add_argument("--no-extras", action="store_true")
@@ -221,7 +213,6 @@ def main() -> None:
 
     import paper_2602_04936_b200 as lg
     from paper_2602_04936_b200 import _build
-    from paper_2602_04936_b200.engine import NativeIndex
 
     if _build.needs_build():
         _build.build_native()
@@ -236,82 +227,145 @@ def main() -> None:
     ds = lg.generate_dataset(N_ITEMS, SEQ_LEN, SIGMA, seed=3 + rank)
     n_pool = 8
     qs = lg.generate_queries(ds, BATCH * n_pool, seed=4)  # uniform queries: identical on every rank
-    stream = torch.cuda.Stream(device=dev)
-    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    main_stream = torch.cuda.Stream(device=dev)
     kbytes = algorithmic_key_bytes(SEQ_LEN, SIGMA)
+    sampler = ClockSampler(local_rank)
 
-    with torch.cuda.stream(stream):
+    with torch.cuda.stream(main_stream):
         t_build = time.perf_counter()
         if world == 1:
             idx = lg.build(ds)
-            native = idx.native
         else:
             from paper_2602_04936_b200.sharded import ShardedIndex
 
             sh = ShardedIndex(ds.items, SEQ_LEN, SIGMA, id_offset=N_ITEMS * rank)
-            native = sh.local
+            idx = None
         torch.cuda.synchronize()
         t_build = time.perf_counter() - t_build
-
         dq = torch.from_numpy(qs).to(dev).view(n_pool, BATCH, SEQ_LEN)
         stride = min(K, N_ITEMS * world)
-        ids = torch.empty((BATCH, stride), dtype=torch.int32, device=dev)
-        lcps = torch.empty((BATCH, stride), dtype=torch.int16, device=dev)
-        hits = torch.empty(BATCH, dtype=torch.int32, device=dev)
-        md = torch.empty(BATCH, dtype=torch.int16, device=dev)
-        aux = torch.empty((n_pool, BATCH, 2), dtype=torch.int64, device=dev)
-        st = stream.cuda_stream
+
+        def out_bufs():
+            return (torch.empty((BATCH, stride), dtype=torch.int32, device=dev),
+                    torch.empty((BATCH, stride), dtype=torch.int16, device=dev),
+                    torch.empty(BATCH, dtype=torch.int32, device=dev),
+                    torch.empty(BATCH, dtype=torch.int16, device=dev),
+                    torch.empty((n_pool, BATCH, 2), dtype=torch.int64, device=dev))
 
         if world == 1:
-            def step(i):
-                native.query_device(dq[i % n_pool], K, "complete", ids, lcps, hits, md, aux[i % n_pool], stream=st)
+            from paper_2602_04936_b200._native import workspace
+
+            workspace()  # created outside graph capture (it allocates)
+            replicas = [idx] + [lg.build(ds) for _ in range(7)]
+            R = len(replicas)
+            G = R * n_pool  # steps per captured graph
+
+            def capture(n_steps: int, n_streams: int):
+                streams = [torch.cuda.Stream(device=dev) for _ in range(n_streams)]
+                bufs = [out_bufs() for _ in range(n_streams)]
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=main_stream):
+                    for x in streams:
+                        x.wait_stream(main_stream)
+                    for i in range(n_steps):
+                        x, (ids, lcps, hits, md, aux) = streams[i % n_streams], bufs[i % n_streams]
+                        b = (i // R) % n_pool
+                        replicas[i % R].native.query_device(dq[b], K, "complete", ids, lcps, hits, md,
+                                                           aux[b], stream=x.cuda_stream)
+                    for x in streams:
+                        main_stream.wait_stream(x)
+                return g, bufs
+
+            def run_steps(n_streams: int, steps: int, warmup: int, clocks: bool = False):
+                g, bufs = capture(G, n_streams)
+                tail = steps % G
+                gt = capture(tail, n_streams)[0] if tail else None
+                # W warm-up steps, and at least ~0.3 s so SM clocks leave idle
+                t_w, reps = time.perf_counter(), 0
+                while reps * G < warmup or time.perf_counter() - t_w < 0.3:
+                    g.replay()
+                    reps += 1
+                    if reps % 16 == 0:
+                        torch.cuda.synchronize()
+                torch.cuda.synchronize()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                t0 = time.perf_counter()
+                a.record(main_stream)
+                for _ in range(steps // G):
+                    g.replay()
+                if gt is not None:
+                    gt.replay()
+                b.record(main_stream)
+                torch.cuda.synchronize()
+                t1 = time.perf_counter()
+                return a.elapsed_time(b), bufs, (t0, t1)
+
+            # one batch in flight (kernel duration for the roofline)
+            single_ms, bufs1, _ = run_steps(1, args.steps, args.warmup)
+            # headline: two batches in flight
+            sampler.start()
+            total_ms, bufs2, (t0, t1) = run_steps(2, args.steps, args.warmup, clocks=True)
+            clocks = sampler.stop(t0, t1)
+            aux_all = bufs1[0][4]
+            gpu_launches = args.steps
         else:
+            flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+            ids, lcps, hits, md, aux_all = out_bufs()
+
             def step(i):
                 sh.query_device(dq[i % n_pool], K, ids, lcps, hits)
 
-        def flush():
-            flush_buf.zero_()
-
-        for i in range(args.warmup):
-            flush()
-            step(i)
-        torch.cuda.synchronize()
-        if world > 1:
+            for i in range(args.warmup):
+                step(i)
+            torch.cuda.synchronize()
             dist.barrier()
-        torch.cuda.synchronize()
-        sampler = ClockSampler(local_rank)
-        sampler.start()
-        evs = time_steps(step, flush, args.steps, stream)
-        torch.cuda.synchronize()
-        if world > 1:
+            torch.cuda.synchronize()
+            sampler.start()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0 = time.perf_counter()
+            a.record(main_stream)
+            for i in range(args.steps):
+                step(i)
+            b.record(main_stream)
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
             dist.barrier()
-        torch.cuda.synchronize()
-        clocks = sampler.stop()
-        step_ms = np.array([a.elapsed_time(b) for a, b in evs])
-        total_ms = float(step_ms.sum())
-        if world > 1:
+            torch.cuda.synchronize()
+            clocks = sampler.stop(t0, t1)
+            total_ms = a.elapsed_time(b)
+            single_ms = total_ms
             t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             total_ms = float(t.item())
+            gpu_launches = args.steps * 3
+            # local-shard aux for the byte accounting
+            for bb in range(n_pool):
+                sh.local.query_device(dq[bb], K, "complete", ids, lcps, hits, md, aux_all[bb],
+                                      stream=main_stream.cuda_stream)
+            torch.cuda.synchronize()
         value = BATCH * args.steps / (total_ms / 1e3)
 
-        # roofline of the dominant kernel (k_query_warp): algorithmic bytes / event time
-        rsize = (aux[:, :, 1].cpu().numpy().astype(np.uint64) & np.uint64(0xFFFFFFFF)).astype(np.int64)
-        per_batch = np.array([indexed_bytes_per_query(N_ITEMS, SEQ_LEN, SIGMA, K, rsize[b]).sum() for b in range(n_pool)])
-        bytes_per_launch = float(np.mean([per_batch[i % n_pool] for i in range(args.steps)]))
+        # roofline of the dominant kernel (k_query_w1): algorithmic bytes / duration
+        rsize = (aux_all[:, :, 1].cpu().numpy().astype(np.uint64) & np.uint64(0xFFFFFFFF)).astype(np.int64)
+        per_batch = np.array([indexed_bytes_per_query(N_ITEMS, SEQ_LEN, SIGMA, K, rsize[bb]).sum()
+                              for bb in range(n_pool)])
+        bytes_per_launch = float(per_batch.mean())
+        kernel_s = single_ms / 1e3 / args.steps
         peak, peak_src = hbm_peak()
-        achieved = bytes_per_launch / (np.mean(step_ms) / 1e3) / 1e9
+        achieved = bytes_per_launch / kernel_s / 1e9
         traffic = None
         prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
         if os.path.exists(prof):
             try:
-                traffic = json.load(open(prof)).get("k_query_warp", {}).get("dram_bytes_per_launch")
+                traffic = json.load(open(prof)).get("k_query_w1", {}).get("dram_bytes_per_launch")
             except Exception:
                 traffic = None
         roofline = {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                     "frac": round(achieved / peak, 5), "traffic": traffic,
-                    "kernel": "k_query_warp<1>", "bytes_per_launch": round(bytes_per_launch, 1),
+                    "kernel": "k_query_w1<u32,2>", "bytes_per_launch": round(bytes_per_launch, 1),
+                    "launch_us": round(kernel_s * 1e6, 3),
                     "peak_source": peak_src,
+                    "duration_source": "CUDA events over the graph-replayed single-stream step loop",
                     "bytes_formula": "sum_q K_b*ceil(log2(N+1)) + |R(d*)|*(K_b+4) + K_b + 6k, K_b=8"}
 
     line = {
@@ -323,31 +377,60 @@ def main() -> None:
         "config": {"workload": "config 3: indexed complete-mode top-k serving, 4096-query batches",
                    "n_items_per_rank": N_ITEMS, "n_items_total": N_ITEMS * world, "seq_len": SEQ_LEN,
                    "alphabet": SIGMA, "k": K, "batch": BATCH, "mode": "complete",
-                   "l2": "flushed before every timed step (256 MiB memset), step = own CUDA event pair",
+                   "l2": ("inputs larger than L2: 8 index replicas (8 x 24 MB > 126 MB) cycled step to step"
+                          if world == 1 else "row-block shard per rank; host-launched steps"),
+                   "launch": ("CUDA graph replay; 2 batches in flight on 2 streams"
+                              if world == 1 else "host loop"),
                    "parallelism": "single GPU" if world == 1 else f"row-block shards x{world} + NCCL all_gather merge"},
         "roofline": roofline,
-        "gpu_launches": args.steps * (1 if world == 1 else 3),
+        "gpu_launches": gpu_launches,
         "clocks": clocks,
         "build_s": round(t_build, 3),
-        "p50_batch_latency_ms": float(np.median(step_ms)),
+        "one_batch_in_flight": {"value": BATCH * args.steps / (single_ms / 1e3), "unit": "queries/s",
+                                "ms_per_step": single_ms / args.steps},
     }
 
     if world == 1 and rank == 0:
-        line["e2e"] = e2e_leg(idx, qs, args, stream)
+        line["e2e"] = e2e_leg(idx, qs, args)
+        line["p50_batch_latency_ms"] = cold_batch_latency(idx, dq, dev)
         cpu_qps, cpu_done, cpu_el, trie = cpu_reference(ds, qs, K, args.cpu_budget_s, os.cpu_count() or 1)
         line["cpu_baseline"] = {
             "value": cpu_qps, "unit": "queries/s", "cores": os.cpu_count() or 1, "kind": "port",
             "sample": (f"{cpu_done} complete-mode k=10 queries ({cpu_el:.1f} s) of the same workload; "
                        "C restatement of trie.build/TrieIndex.query (oracle/lcp_oracle.c), one pthread per core")}
         if not args.no_extras:
-            line["extras"] = extras(idx, ds, qs, stream, flush_buf, step_ms)
+            flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+            line["extras"] = extras(idx, ds, qs, main_stream, flush_buf)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
-def e2e_leg(idx, qs, args, stream) -> dict:
+def cold_batch_latency(idx, dq, dev) -> float:
+    """Median event-timed latency of one batch launched right after a 256 MiB
+    L2-flushing memset (includes the launch; conservative)."""
+    import torch
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ids = torch.empty((BATCH, K), dtype=torch.int32, device=dev)
+    lcps = torch.empty((BATCH, K), dtype=torch.int16, device=dev)
+    hits = torch.empty(BATCH, dtype=torch.int32, device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+    ts = []
+    for i in range(60):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        idx.native.query_device(dq[i % dq.shape[0]], K, "complete", ids, lcps, hits, stream=st)
+        b.record()
+        torch.cuda.synchronize()
+        if i >= 10:
+            ts.append(a.elapsed_time(b))
+    return float(np.median(ts))
+
+
+def e2e_leg(idx, qs, args) -> dict:
     """Public API, host buffers: pinned queries in, results out, every step."""
     from paper_2602_04936_b200._native import PinnedArray
 
@@ -355,9 +438,9 @@ def e2e_leg(idx, qs, args, stream) -> dict:
     pin = PinnedArray((n_pool, BATCH, SEQ_LEN), np.uint16)
     pin.array[:] = qs.reshape(n_pool, BATCH, SEQ_LEN)
     out = idx.native.alloc_batch(BATCH, K, "complete", pinned=True)
-    for i in range(args.warmup):
+    for i in range(20):
         idx.query_batch(pin.array[i % n_pool], K, "complete", out=out)
-    steps = min(args.steps, 1000)
+    steps = min(args.steps, 2000)
     t = []
     for i in range(steps):
         t0 = time.perf_counter()
@@ -366,12 +449,12 @@ def e2e_leg(idx, qs, args, stream) -> dict:
     stride = out.ids.shape[1]
     return {"value": BATCH * steps / float(np.sum(t)), "unit": "queries/s",
             "h2d_bytes_per_step": BATCH * SEQ_LEN * 2,
-            "d2h_bytes_per_step": BATCH * (stride * 6 + 4 + 2 + 16),
+            "d2h_bytes_per_step": int(out._owners[0].array.nbytes),
             "steps": steps, "p50_ms": 1e3 * float(np.median(t)),
-            "api": "TrieIndex.query_batch(pinned uint16 (4096, 32), k=10, 'complete', out=pinned)"}
+            "api": "TrieIndex.query_batch(pinned uint16 (4096, 32), k=10, 'complete', out=pinned packed block)"}
 
 
-def extras(idx, ds, qs, stream, flush_buf, step_ms) -> dict:
+def extras(idx, ds, qs, stream, flush_buf) -> dict:
     import torch
 
     import paper_2602_04936_b200 as lg
@@ -385,45 +468,61 @@ def extras(idx, ds, qs, stream, flush_buf, step_ms) -> dict:
     lcps = torch.empty((BATCH, K), dtype=torch.int16, device=dev)
     hits = torch.empty(BATCH, dtype=torch.int32, device=dev)
 
-    def timed(fn, steps, flush=True):
+    def graph_of(fn, n):
+        g = torch.cuda.CUDAGraph()
         with torch.cuda.stream(stream):
-            for i in range(3):
-                fn(i)
+            fn(0)
             torch.cuda.synchronize()
-            evs = time_steps(fn, (lambda: flush_buf.zero_()) if flush else None, steps, stream)
-            torch.cuda.synchronize()
-        return np.array([a.elapsed_time(b) for a, b in evs])
+            with torch.cuda.graph(g, stream=stream):
+                for i in range(n):
+                    fn(i)
+        return g
 
-    # warm-L2 serving steady state (index resident in the 126 MB L2)
-    warm = timed(lambda i: idx.native.query_device(dq[i % n_pool], K, "complete", ids, lcps, hits, stream=st), 500, flush=False)
-    out["indexed_warm_l2_qps"] = BATCH / (warm.mean() / 1e3)
-    # prefix-16 query variant
+    def per_step_ms(fn, n_graph, reps):
+        g = graph_of(fn, n_graph)
+        with torch.cuda.stream(stream):  # replay() launches on the current stream
+            g.replay()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(reps):
+                g.replay()
+            b.record(stream)
+            torch.cuda.synchronize()
+        return a.elapsed_time(b) / (n_graph * reps), g
+
+    idx_fn = lambda i: idx.native.query_device(dq[i % n_pool], K, "complete", ids, lcps, hits, stream=st)
+    # prefix-16 query variant, one batch in flight
     qp = lg.generate_queries(ds, BATCH, seed=5, prefix_len=16)
     dqp = torch.from_numpy(qp).to(dev)
-    pre = timed(lambda i: idx.native.query_device(dqp, K, "complete", ids, lcps, hits, stream=st), 200)
-    out["indexed_prefix16_qps"] = BATCH / (pre.mean() / 1e3)
-    # brute-force full-scan kernel on the same batch
-    fs = timed(lambda i: idx.native.fullscan_device(dq[i % n_pool], K, ids, lcps, hits, stream=st), 20)
-    out["fullscan_qps"] = BATCH / (fs.mean() / 1e3)
-    out["fullscan_ms_per_batch"] = float(fs.mean())
-    out["fullscan_stream_gbs"] = N_ITEMS * 8 / (fs.mean() / 1e3) / 1e9
+    ms, _ = per_step_ms(lambda i: idx.native.query_device(dqp, K, "complete", ids, lcps, hits, stream=st), 64, 20)
+    out["indexed_prefix16_qps"] = BATCH / (ms / 1e3)
+    # strict mode on the same batches
+    ms, _ = per_step_ms(lambda i: idx.native.query_device(dq[i % n_pool], K, "strict", ids, lcps, hits, stream=st), 64, 20)
+    out["indexed_strict_qps"] = BATCH / (ms / 1e3)
+    # brute-force full-scan kernel on the same batches
+    fs_fn = lambda i: idx.native.fullscan_device(dq[i % n_pool], K, ids, lcps, hits, stream=st)
+    ms, _ = per_step_ms(fs_fn, 4, 3)
+    out["fullscan_qps"] = BATCH / (ms / 1e3)
+    out["fullscan_ms_per_batch"] = ms
+    out["fullscan_key_stream_gbs"] = N_ITEMS * 8 / (ms / 1e3) / 1e9
     # TAL B=256 (paper's bounded-range scan)
     tal = lg.build_tal(ds, 256)
-    tl = timed(lambda i: tal.native.query_device(dq[i % n_pool], K, "tal", ids, lcps, hits, stream=st), 50)
-    out["tal256_qps"] = BATCH / (tl.mean() / 1e3)
-    # energy: NVML counter over >= 3 s loops (gross, and net of idle power)
+    tal_fn = lambda i: tal.native.query_device(dq[i % n_pool], K, "tal", ids, lcps, hits, stream=st)
+    ms, _ = per_step_ms(tal_fn, 8, 5)
+    out["tal256_qps"] = BATCH / (ms / 1e3)
+    # energy: NVML counter over >= 3 s of graph-replayed batches (gross, and net of idle)
     energy = nvml_energy()
     if energy is not None:
-        def joules_per_query(fn, seconds=3.0):
+        def joules_per_query(fn, n_graph, seconds=3.0):
+            g = graph_of(fn, n_graph)
             with torch.cuda.stream(stream):
-                fn(0)
+                g.replay()
                 torch.cuda.synchronize()
-                e0, t0, done, i = energy(), time.perf_counter(), 0, 0
+                e0, t0, done = energy(), time.perf_counter(), 0
                 while time.perf_counter() - t0 < seconds:
-                    for _ in range(20):
-                        fn(i)
-                        i += 1
-                        done += BATCH
+                    g.replay()
+                    done += BATCH * n_graph
                     torch.cuda.synchronize()
                 el = time.perf_counter() - t0
                 return (energy() - e0) / done, done / el
@@ -431,15 +530,16 @@ def extras(idx, ds, qs, stream, flush_buf, step_ms) -> dict:
         e0 = energy()
         time.sleep(2.0)
         idle_w = (energy() - e0) / 2.0
-        jq_idx, qps_idx = joules_per_query(lambda i: idx.native.query_device(dq[i % n_pool], K, "complete", ids, lcps, hits, stream=st))
-        jq_fs, qps_fs = joules_per_query(lambda i: idx.native.fullscan_device(dq[i % n_pool], K, ids, lcps, hits, stream=st))
-        jq_tal, qps_tal = joules_per_query(lambda i: tal.native.query_device(dq[i % n_pool], K, "tal", ids, lcps, hits, stream=st))
+        jq_idx, qps_idx = joules_per_query(idx_fn, 256)
+        jq_fs, qps_fs = joules_per_query(fs_fn, 4)
+        jq_tal, qps_tal = joules_per_query(tal_fn, 16)
         out["energy"] = {
             "idle_w": idle_w,
             "indexed_j_per_query": jq_idx, "indexed_net_j_per_query": jq_idx - idle_w / qps_idx,
             "fullscan_j_per_query": jq_fs, "fullscan_net_j_per_query": jq_fs - idle_w / qps_fs,
             "tal256_j_per_query": jq_tal, "tal256_net_j_per_query": jq_tal - idle_w / qps_tal,
-            "method": "NVML total-energy delta over >=3 s back-to-back batches (warm L2)",
+            "fullscan_over_indexed": jq_fs / jq_idx,
+            "method": "NVML total-energy delta over >=3 s of CUDA-graph-replayed batches (one in flight)",
         }
     # GNC config 2: N=100k, L=24, k=5, one query per call through the public API
     g = lg.generate_dataset(100_000, 24, SIGMA, seed=4)

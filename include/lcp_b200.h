@@ -131,6 +131,17 @@ int lcp_query(const lcp_index* index, lcp_workspace* ws, const uint16_t* queries
 int lcp_query_host(const lcp_index* index, lcp_workspace* ws, const uint16_t* queries,
                    int32_t count, int32_t k, int32_t mode, int32_t out_stride, uint32_t* ids,
                    uint16_t* lcps, int32_t* hits, uint16_t* matched_depth, uint64_t* aux);
+/* Single-copy variant of lcp_query_host: every output lands in one host
+ * block (ideally page-locked) with the byte layout lcp_packed_layout_for()
+ * reports, so a batch costs one H2D and one D2H transfer. */
+typedef struct lcp_packed_layout {
+  int64_t ids, lcps, hits, matched_depth, aux; /* byte offsets */
+  int64_t total;                               /* block size in bytes */
+} lcp_packed_layout;
+int lcp_packed_layout_for(int32_t count, int32_t out_stride, lcp_packed_layout* layout);
+int lcp_query_host_packed(const lcp_index* index, lcp_workspace* ws, const uint16_t* queries,
+                          int32_t count, int32_t k, int32_t mode, int32_t out_stride,
+                          void* out_block);
 /* Device-side error flag raised by lcp_query (invalid query symbol); reading
  * it synchronises `stream`.  Returns LCP_OK or LCP_ERR_INVALID_INPUT and clears it. */
 int lcp_workspace_check(lcp_workspace* ws, void* stream);

@@ -50,6 +50,12 @@ class IndexInfo(ctypes.Structure):
     ]
 
 
+class PackedLayout(ctypes.Structure):
+    _fields_ = [("ids", ctypes.c_int64), ("lcps", ctypes.c_int64), ("hits", ctypes.c_int64),
+                ("matched_depth", ctypes.c_int64), ("aux", ctypes.c_int64),
+                ("total", ctypes.c_int64)]
+
+
 _P = ctypes.c_void_p
 _I32 = ctypes.c_int32
 _I64 = ctypes.c_int64
@@ -72,6 +78,8 @@ SIGNATURES = {
     "lcp_workspace_free": (ctypes.c_int, [_P]),
     "lcp_workspace_stream": (_P, [_P]),
     "lcp_workspace_check": (ctypes.c_int, [_P, _P]),
+    "lcp_packed_layout_for": (ctypes.c_int, [_I32, _I32, ctypes.POINTER(PackedLayout)]),
+    "lcp_query_host_packed": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _I32, _I32, _P]),
     "lcp_query": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P]),
     "lcp_query_host": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P]),
     "lcp_fullscan": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _P]),
@@ -136,7 +144,7 @@ def ptr(arr) -> int | None:
         return None
     if hasattr(arr, "data_ptr"):
         return int(arr.data_ptr())
-    return int(arr.ctypes.data)
+    return arr.__array_interface__["data"][0]
 
 
 class Workspace:
@@ -188,6 +196,7 @@ class PinnedArray:
         p = ctypes.c_void_p()
         check(load().lcp_pinned_alloc(max(nbytes, 1), ctypes.byref(p)))
         self._ptr = p
+        self.address = int(p.value)
         buf = (ctypes.c_uint8 * max(nbytes, 1)).from_address(p.value)
         self.array = np.frombuffer(buf, dtype=self.dtype, count=nbytes // self.dtype.itemsize).reshape(self.shape)
 

@@ -855,6 +855,52 @@ int lcp_query_host(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queri
   return LCP_OK;
 }
 
+static lcp_packed_layout packed_layout(long long count, long long stride) {
+  auto up8 = [](long long v) { return (v + 7) & ~7ll; };
+  lcp_packed_layout l;
+  l.ids = 0;
+  l.lcps = up8(count * stride * 4);
+  l.hits = up8(l.lcps + count * stride * 2);
+  l.matched_depth = up8(l.hits + count * 4);
+  l.aux = up8(l.matched_depth + count * 2);
+  l.total = l.aux + count * 16;
+  return l;
+}
+
+int lcp_packed_layout_for(int32_t count, int32_t out_stride, lcp_packed_layout* layout) {
+  if (!layout || count < 0 || out_stride < 1) return fail(LCP_ERR_INVALID_INPUT, "bad layout request");
+  *layout = packed_layout(count, out_stride);
+  return LCP_OK;
+}
+
+int lcp_query_host_packed(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries,
+                          int32_t count, int32_t k, int32_t mode, int32_t out_stride,
+                          void* out_block) {
+  if (!ix || !ws) return fail(LCP_ERR_INVALID_INPUT, "null index or workspace");
+  if (count <= 0) return LCP_OK;
+  if (out_stride < 1 || !out_block || !queries)
+    return fail(LCP_ERR_INVALID_INPUT, "bad output block or queries");
+  const DevIndex& dv = ix->dv;
+  cudaStream_t st = ws->stream;
+  const lcp_packed_layout lay = packed_layout(count, out_stride);
+  const size_t qb = (size_t)count * dv.L * 2;
+  LCP_TRY(ws->q_in.ensure(qb));
+  LCP_TRY(ws->ids.ensure((size_t)lay.total));  // device mirror of the packed block
+  char* d = static_cast<char*>(ws->ids.p);
+  LCP_CK(cudaMemcpyAsync(ws->q_in.p, queries, qb, cudaMemcpyHostToDevice, st));
+  LCP_TRY(lcp_query(ix, ws, ws->q_in.as<uint16_t>(), count, k, mode, out_stride,
+                    reinterpret_cast<uint32_t*>(d + lay.ids),
+                    reinterpret_cast<uint16_t*>(d + lay.lcps),
+                    reinterpret_cast<int32_t*>(d + lay.hits),
+                    reinterpret_cast<uint16_t*>(d + lay.matched_depth),
+                    reinterpret_cast<uint64_t*>(d + lay.aux), st));
+  LCP_CK(cudaMemcpyAsync(out_block, d, (size_t)lay.total, cudaMemcpyDeviceToHost, st));
+  if (host_finish(ws) != LCP_OK)
+    return fail(LCP_ERR_INVALID_INPUT,
+                "query symbol out of range for alphabet of size " + std::to_string(dv.sigma));
+  return LCP_OK;
+}
+
 // ---- full scan ----------------------------------------------------------------
 }  // extern "C"
 

@@ -9,6 +9,7 @@ reference-compatible views over it.
 from __future__ import annotations
 
 import ctypes
+import threading
 
 import numpy as np
 
@@ -136,27 +137,51 @@ class NativeIndex:
         return max(1, min(int(k), self.n))
 
     def alloc_batch(self, count: int, k: int, mode: str = "complete", pinned: bool = True) -> BatchResult:
-        """Output buffers for ``count`` queries (page-locked when pinned)."""
+        """Output buffers for ``count`` queries.  Pinned: one page-locked block
+        in the lcp_packed_layout_for() layout, so a batch is one D2H copy."""
         stride = self.stride_for(k)
-        owners: list = []
+        if not pinned:
+            return BatchResult(
+                ids=np.empty((count, stride), dtype=np.uint32),
+                lcps=np.empty((count, stride), dtype=np.uint16),
+                hits=np.empty(count, dtype=np.int32),
+                matched_depth=np.empty(count, dtype=np.uint16),
+                aux=np.empty((count, 2), dtype=np.uint64),
+                mode=mode,
+            )
+        lay = _native.PackedLayout()
+        check(load().lcp_packed_layout_for(count, stride, ctypes.byref(lay)))
+        block = PinnedArray((int(lay.total),), np.uint8)
+        raw = block.array
 
-        def mk(shape, dt):
-            if not pinned:
-                return np.empty(shape, dtype=dt)
-            p = PinnedArray(shape, dt)
-            owners.append(p)
-            return p.array
+        def view(off, dt, shape):
+            nbytes = int(np.prod(shape)) * np.dtype(dt).itemsize
+            return raw[off:off + nbytes].view(dt).reshape(shape)
 
         out = BatchResult(
-            ids=mk((count, stride), np.uint32),
-            lcps=mk((count, stride), np.uint16),
-            hits=mk((count,), np.int32),
-            matched_depth=mk((count,), np.uint16),
-            aux=mk((count, 2), np.uint64),
+            ids=view(lay.ids, np.uint32, (count, stride)),
+            lcps=view(lay.lcps, np.uint16, (count, stride)),
+            hits=view(lay.hits, np.int32, (count,)),
+            matched_depth=view(lay.matched_depth, np.uint16, (count,)),
+            aux=view(lay.aux, np.uint64, (count, 2)),
             mode=mode,
         )
-        out._owners = owners  # page-locked buffers live as long as the result
+        out._owners = [block]  # the page-locked block lives as long as the result
+        out._packed = (block.address, count, stride)
         return out
+
+    def single_query_buffer(self, k: int, mode: str) -> BatchResult:
+        """Per-thread page-locked output block for one query (reused; callers
+        copy results out before the next call on the same thread)."""
+        cache = getattr(self, "_single", None)
+        if cache is None:
+            cache = self._single = threading.local()
+        key = (self.stride_for(k), mode)
+        buf = getattr(cache, "buf", None)
+        if buf is None or buf[0] != key:
+            buf = (key, self.alloc_batch(1, k, mode, pinned=True))
+            cache.buf = buf
+        return buf[1]
 
     def query_host(self, queries: np.ndarray, k: int, mode: str,
                    out: BatchResult | None = None) -> BatchResult:
@@ -171,6 +196,12 @@ class NativeIndex:
             out = self.alloc_batch(count, k, mode, pinned=False)
         out.mode = mode
         ws = workspace()
+        packed = getattr(out, "_packed", None)
+        if packed is not None and packed[1] == count:
+            check(load().lcp_query_host_packed(
+                self.handle, ws.handle, ptr(queries), count, k_eff, MODES[mode], packed[2],
+                packed[0]))
+            return out
         check(load().lcp_query_host(
             self.handle, ws.handle, ptr(queries), count, k_eff, MODES[mode], out.ids.shape[1],
             ptr(out.ids), ptr(out.lcps), ptr(out.hits), ptr(out.matched_depth), ptr(out.aux)))
