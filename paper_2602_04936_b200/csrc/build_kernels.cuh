@@ -37,6 +37,17 @@ __global__ void k_pack(const uint16_t* __restrict__ rows, long long n, int L, in
   if (ids != nullptr && w == 0) ids[row] = (u32)row;
 }
 
+// split W == 1 keys into hi / lo 32-bit planes (full-scan layout)
+__global__ void k_split_words(const u64* __restrict__ keys, long long n, u32* __restrict__ hi,
+                              u32* __restrict__ lo) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const u64 k = keys[i];
+    hi[i] = (u32)(k >> 32);
+    lo[i] = (u32)k;
+  }
+}
+
 __global__ void k_iota(u32* __restrict__ v, long long n) {
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) v[i] = (u32)i;

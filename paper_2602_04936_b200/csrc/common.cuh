@@ -26,6 +26,8 @@ struct DevIndex {
   const u64* keys;        // sorted packed keys, n*W
   const u32* order;       // sorted position -> original item id
   const u64* keys_orig;   // packed keys in original row order, n*W (full scan)
+  const u32* keys_hi;     // W == 1: high 32 bits of keys_orig (SoA plane for the scan)
+  const u32* keys_lo;     // W == 1: low 32 bits of keys_orig
   const u64* levels;      // concatenated search-level tables (W words per entry)
   const long long* directory;  // TAL dense directory (sigma**d + 1) or null
   long long n;

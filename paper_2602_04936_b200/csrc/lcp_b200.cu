@@ -199,6 +199,8 @@ struct lcp_index {
   u64* keys = nullptr;
   u64* keys_orig = nullptr;
   u32* order = nullptr;
+  u32* keys_hi = nullptr;
+  u32* keys_lo = nullptr;
   uint16_t* adj = nullptr;
   u64* levels = nullptr;
   long long* directory = nullptr;
@@ -209,7 +211,7 @@ struct lcp_workspace {
   cudaStream_t stream = nullptr;
   int* d_err = nullptr;
   int* h_err = nullptr;  // pinned
-  DBuf qkeys, partial, q_in, ids, lcps, hits, md, aux;
+  DBuf qkeys, partial, hint, q_in, ids, lcps, hits, md, aux;
 };
 
 extern "C" {
@@ -223,6 +225,8 @@ int lcp_index_free(lcp_index* ix) {
   cudaFree(ix->keys);
   cudaFree(ix->keys_orig);
   cudaFree(ix->order);
+  cudaFree(ix->keys_hi);
+  cudaFree(ix->keys_lo);
   cudaFree(ix->adj);
   cudaFree(ix->levels);
   cudaFree(ix->directory);
@@ -316,6 +320,17 @@ static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, i
   dv.keys = ix->keys;
   dv.keys_orig = ix->keys_orig;
   dv.order = ix->order;
+  if (W == 1) {  // hi / lo word planes of the original-order keys for the full scan
+    const long long pn = (n + 4095) / 4096 * 4096 + 64;  // whole 16 KB stages
+    LCP_TRY(dalloc(&ix->keys_hi, pn, acct));
+    LCP_TRY(dalloc(&ix->keys_lo, pn, acct));
+    LCP_CK(cudaMemsetAsync(ix->keys_hi, 0, (size_t)pn * 4, st));
+    LCP_CK(cudaMemsetAsync(ix->keys_lo, 0, (size_t)pn * 4, st));
+    k_split_words<<<blocks_for(n, 256), 256, 0, st>>>(ix->keys_orig, n, ix->keys_hi, ix->keys_lo);
+    LCP_CK_LAUNCH();
+  }
+  dv.keys_hi = ix->keys_hi;
+  dv.keys_lo = ix->keys_lo;
 
   // adjacent lcp — core.py:177-184
   LCP_TRY(dalloc(&ix->adj, std::max(1ll, n - 1), acct));
@@ -672,8 +687,8 @@ int lcp_workspace_create(lcp_workspace** out) {
 int lcp_workspace_free(lcp_workspace* ws) {
   if (!ws) return LCP_OK;
   if (ws->stream) cudaStreamSynchronize(ws->stream);
-  for (DBuf* b : {&ws->qkeys, &ws->partial, &ws->q_in, &ws->ids, &ws->lcps, &ws->hits, &ws->md,
-                  &ws->aux})
+  for (DBuf* b : {&ws->qkeys, &ws->partial, &ws->hint, &ws->q_in, &ws->ids, &ws->lcps, &ws->hits,
+                  &ws->md, &ws->aux})
     b->release();
   cudaFree(ws->d_err);
   cudaFreeHost(ws->h_err);
@@ -914,6 +929,45 @@ static void launch_fullscan(const DevIndex& dv, const uint16_t* q, int count, in
                                                           partial, err);
 }
 
+template <typename C, int KCAP>
+static int launch_fullscan_w1_k(const DevIndex& dv, const uint16_t* q, int count, int need,
+                                long long chunk, int nchunks, u64* partial, int* hint, int* err,
+                                cudaStream_t st) {
+  const size_t smem = 16 + 2 * 2 * FS1_STAGE_KEYS * 4;  // 2 stages x (hi + lo) planes
+  static bool attr = false;
+  if (!attr) {
+    LCP_CK(cudaFuncSetAttribute(k_fullscan_w1<C, KCAP>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  dim3 grid((count + FS_THREADS - 1) / FS_THREADS, nchunks);
+  k_fullscan_w1<C, KCAP><<<grid, FS_THREADS, smem, st>>>(dv, q, count, need, chunk, nchunks,
+                                                         partial, hint, err);
+  return LCP_OK;
+}
+
+// list length = need exactly for the common k, else the next size up
+template <typename C>
+static int launch_fullscan_w1_c(const DevIndex& dv, const uint16_t* q, int count, int need,
+                                long long chunk, int nchunks, u64* partial, int* hint, int* err,
+                                cudaStream_t st) {
+#define LCP_FS_CASE(K) \
+  if (need <= K) return launch_fullscan_w1_k<C, K>(dv, q, count, need, chunk, nchunks, partial, hint, err, st);
+  LCP_FS_CASE(1) LCP_FS_CASE(2) LCP_FS_CASE(3) LCP_FS_CASE(4) LCP_FS_CASE(5) LCP_FS_CASE(6)
+  LCP_FS_CASE(8) LCP_FS_CASE(10) LCP_FS_CASE(12) LCP_FS_CASE(16) LCP_FS_CASE(20)
+  LCP_FS_CASE(24) LCP_FS_CASE(32)
+#undef LCP_FS_CASE
+  return fail(LCP_ERR_INTERNAL, "full scan: need > 32 on the fast path");
+}
+
+static int launch_fullscan_w1(const DevIndex& dv, const uint16_t* q, int count, int need,
+                              long long chunk, int nchunks, u64* partial, int* hint, int* err,
+                              cudaStream_t st) {
+  if (dv.idbits < 32)
+    return launch_fullscan_w1_c<u32>(dv, q, count, need, chunk, nchunks, partial, hint, err, st);
+  return launch_fullscan_w1_c<u64>(dv, q, count, need, chunk, nchunks, partial, hint, err, st);
+}
+
 template <int WMAX>
 static void launch_fullscan_k(const DevIndex& dv, const uint16_t* q, int count, int need,
                               long long chunk, int nchunks, u64* partial, int* err,
@@ -942,18 +996,23 @@ int lcp_fullscan(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries
   }
   const int take = (int)std::min<long long>(k, dv.n);
   if (dv.W <= 8 && take <= FAST_KMAX) {
-    const int per_stage = (FS_STAGE_BYTES / (8 * dv.W)) & ~1;
+    const int per_stage = dv.W == 1 ? FS1_STAGE_KEYS : (FS_STAGE_BYTES / (8 * dv.W)) & ~1;
     const long long qtiles = (count + FS_THREADS - 1) / FS_THREADS;
     const long long max_chunks = (dv.n + per_stage - 1) / per_stage;
     long long want = std::max(1ll, (4ll * num_sms() + qtiles - 1) / qtiles);
+    if (const char* fc = getenv("LCP_FULLSCAN_CHUNKS")) want = std::max(1ll, atoll(fc));  // tuning hook
     want = std::min(want, max_chunks);
     long long chunk = (dv.n + want - 1) / want;
     chunk = (chunk + per_stage - 1) / per_stage * per_stage;
     const int nchunks = (int)((dv.n + chunk - 1) / chunk);
     LCP_TRY(ws->partial.ensure((size_t)count * nchunks * take * 8));
     u64* partial = ws->partial.as<u64>();
-    if (dv.W == 1) launch_fullscan_k<1>(dv, queries, count, take, chunk, nchunks, partial, ws->d_err, st);
-    else if (dv.W == 2) launch_fullscan_k<2>(dv, queries, count, take, chunk, nchunks, partial, ws->d_err, st);
+    if (dv.W == 1) {
+      LCP_TRY(ws->hint.ensure((size_t)count * 4));
+      LCP_CK(cudaMemsetAsync(ws->hint.p, 0, (size_t)count * 4, st));
+      LCP_TRY(launch_fullscan_w1(dv, queries, count, take, chunk, nchunks, partial,
+                                 ws->hint.as<int>(), ws->d_err, st));
+    } else if (dv.W == 2) launch_fullscan_k<2>(dv, queries, count, take, chunk, nchunks, partial, ws->d_err, st);
     else if (dv.W <= 4) launch_fullscan_k<4>(dv, queries, count, take, chunk, nchunks, partial, ws->d_err, st);
     else launch_fullscan_k<8>(dv, queries, count, take, chunk, nchunks, partial, ws->d_err, st);
     LCP_CK_LAUNCH();
