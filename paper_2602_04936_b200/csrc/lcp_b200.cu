@@ -726,12 +726,24 @@ __global__ void k_fill_empty(int count, int md, int* hits, uint16_t* out_md, u64
   }
 }
 
+template <typename C, int T>
+static void launch_w1(const DevIndex& dv, int mode, unsigned grid, unsigned block, size_t smem,
+                      cudaStream_t st, const uint16_t* q, int count, int k, int stride, u32* ids,
+                      uint16_t* lcps, int* hits, uint16_t* md, u64* aux, int* err) {
+  if (mode == LCP_MODE_STRICT)
+    k_query_w1<C, T, 0><<<grid, block, smem, st>>>(dv, q, count, k, stride, ids, lcps, hits, md, aux, err);
+  else if (mode == LCP_MODE_COMPLETE)
+    k_query_w1<C, T, 1><<<grid, block, smem, st>>>(dv, q, count, k, stride, ids, lcps, hits, md, aux, err);
+  else
+    k_query_w1<C, T, 2><<<grid, block, smem, st>>>(dv, q, count, k, stride, ids, lcps, hits, md, aux, err);
+}
+
 template <int WMAX>
 static void launch_fast(const lcp_index* ix, const uint16_t* q, int count, int k, int mode,
                         int stride, u32* ids, uint16_t* lcps, int* hits, uint16_t* md, u64* aux,
                         int* err, cudaStream_t st) {
   const DevIndex& dv = ix->dv;
-  if (mode == LCP_MODE_TAL) {
+  if (mode == LCP_MODE_TAL && WMAX > 1) {
     unsigned grid = (unsigned)std::min<long long>(count, 8ll * num_sms());
     k_query_tal<WMAX><<<grid, QT_THREADS, 0, st>>>(dv, q, count, k, stride, ids, lcps, hits, md,
                                                    aux, err);
@@ -747,21 +759,12 @@ static void launch_fast(const lcp_index* ix, const uint16_t* q, int count, int k
     if constexpr (WMAX == 1) {
       // leaf region: 64 keys cover the +-need window for need <= 16, 96 keys for <= 32
       const long long need = mode == LCP_MODE_COMPLETE ? std::min<long long>(k, dv.n) : k;
-      const bool narrow = need <= 16;
       if (dv.idbits < 32) {
-        if (narrow)
-          k_query_w1<u32, 2><<<grid, block, smem, st>>>(dv, q, count, k, mode, stride, ids, lcps,
-                                                         hits, md, aux, err);
-        else
-          k_query_w1<u32, 3><<<grid, block, smem, st>>>(dv, q, count, k, mode, stride, ids, lcps,
-                                                         hits, md, aux, err);
+        if (need <= 16) launch_w1<u32, 2>(dv, mode, grid, block, smem, st, q, count, k, stride, ids, lcps, hits, md, aux, err);
+        else launch_w1<u32, 3>(dv, mode, grid, block, smem, st, q, count, k, stride, ids, lcps, hits, md, aux, err);
       } else {
-        if (narrow)
-          k_query_w1<u64, 2><<<grid, block, smem, st>>>(dv, q, count, k, mode, stride, ids, lcps,
-                                                         hits, md, aux, err);
-        else
-          k_query_w1<u64, 3><<<grid, block, smem, st>>>(dv, q, count, k, mode, stride, ids, lcps,
-                                                         hits, md, aux, err);
+        if (need <= 16) launch_w1<u64, 2>(dv, mode, grid, block, smem, st, q, count, k, stride, ids, lcps, hits, md, aux, err);
+        else launch_w1<u64, 3>(dv, mode, grid, block, smem, st, q, count, k, stride, ids, lcps, hits, md, aux, err);
       }
     }
     else

@@ -240,6 +240,9 @@ __device__ __forceinline__ int window_dstar(const int (&l)[T], int dmax, int nee
 // d* and the candidate scan at once.  Candidates (lcp >= d*) form one run;
 // it is compacted to one per lane and bitonic-sorted by (L-lcp)<<32|id.
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ long long prefix_bound(const DevIndex& ix, const u64* q, int d,
+                                                  bool upper);
+
 // One 64-ary search step over a level table: number of entries < q among
 // the 64 separators [blk*64, blk*64+64) (two per lane).
 __device__ __forceinline__ int level_count(const u64* __restrict__ tab, int cnt, int blk, u64 q) {
@@ -254,12 +257,13 @@ __device__ __forceinline__ int level_count(const u64* __restrict__ tab, int cnt,
   return (int)__reduce_add_sync(LCP_FULL_MASK, lt);
 }
 
-template <typename C, int T>
+template <typename C, int T, int MODE>
 __global__ void __launch_bounds__(QW_MAX_THREADS, 1)
-    k_query_w1(DevIndex ix, const uint16_t* __restrict__ queries, int count, int k, int mode,
+    k_query_w1(DevIndex ix, const uint16_t* __restrict__ queries, int count, int k,
                int stride, u32* __restrict__ out_ids, uint16_t* __restrict__ out_lcps,
                int* __restrict__ out_hits, uint16_t* __restrict__ out_md,
                u64* __restrict__ out_aux, int* __restrict__ err) {
+  // MODE: 0 strict, 1 complete, 2 tal (trie.MODE_CODES)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   u64* bar = reinterpret_cast<u64*>(smem_raw);
   u64* staged = reinterpret_cast<u64*>(smem_raw + 16);
@@ -272,8 +276,9 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, 1)
   const int L = ix.L;
   const int b = ix.b, lb = ix.lb;
   const int idbits = ix.idbits;
-  const bool complete = mode == 1;
-  const int need = complete ? min(k, n) : k;
+  // complete: min(k, n) hits; strict: up to k; tal: the top-k of the bucket,
+  // which is the complete-mode answer with need = k whenever |bucket| >= k
+  const int need = MODE == 1 ? min(k, n) : k;
   const u64* __restrict__ keys = ix.keys;
   const u32* __restrict__ order = ix.order;
   // W == 1  =>  L <= 64: lane packs symbols lane and lane + 32
@@ -290,9 +295,8 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, 1)
     const u64 q = ((u64)__reduce_or_sync(LCP_FULL_MASK, (u32)(v >> 32)) << 32) |
                   (u64)__reduce_or_sync(LCP_FULL_MASK, (u32)v);
     const bool any_bad = __any_sync(LCP_FULL_MASK, bad);
-    stage_wait(ix, bar);  // first iteration: the query load overlaps the copy
-    LCP_STAMP(qi, 1);
     if (any_bad) {
+      stage_wait(ix, bar);
       if (lane == 0) {
         atomicOr(err, 1);
         out_hits[qi] = 0;
@@ -302,6 +306,27 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, 1)
       }
       continue;
     }
+    // TAL: the query's d-prefix bucket [blo, bhi) (tal.py:116-143), looked up
+    // before the search so the directory read overlaps it
+    int blo = 0, bhi = n;
+    if constexpr (MODE == 2) {
+      const int d = ix.tal_depth;
+      if (d > 0) {
+        if (ix.directory) {
+          long long code = 0;
+          for (int j = 0; j < d; ++j)
+            code = code * ix.sigma + (long long)((q >> (64 - b * (j + 1))) & ((1ull << b) - 1));
+          blo = (int)__ldg(ix.directory + code);
+          bhi = (int)__ldg(ix.directory + code + 1);
+        } else {
+          u64 qk1[1] = {q};
+          blo = (int)prefix_bound(ix, qk1, d, false);
+          bhi = (int)prefix_bound(ix, qk1, d, true);
+        }
+      }
+    }
+    stage_wait(ix, bar);  // first iteration: the query load overlaps the copy
+    LCP_STAMP(qi, 1);
     // 64-ary search down to the 32-key leaf block holding lower_bound(q)
     int blk = 0;
     bool at_root_min = false;  // q <= every key (pos = 0)
@@ -340,8 +365,73 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, 1)
     }
     dmax = (int)__reduce_max_sync(LCP_FULL_MASK, (unsigned)(dmax + 1)) - 1;
     LCP_STAMP(qi, 3);
-    const int dstar = complete ? window_dstar<T>(l, dmax, need) : dmax;
 
+    int md = dmax;
+    u64 aux0 = 0, aux1 = 0;
+    bool tal_small = false;  // bucket smaller than k: answer = the whole bucket
+    if constexpr (MODE == 2) {
+      // symbols_compared = sum over the bucket of min(lcp + 1, L)
+      // (tal.py:173-177): every bucket item's lcp, coalesced 16-byte loads
+      unsigned long long sym = 0;
+      for (int i = blo + 2 * lane; i < bhi; i += 64) {
+        u64 k0, k1 = q;
+        if (i + 1 < bhi && !(i & 1)) {
+          const ulonglong2 kv = __ldg(reinterpret_cast<const ulonglong2*>(keys + i));
+          k0 = kv.x;
+          k1 = kv.y;
+        } else {
+          k0 = __ldg(keys + i);
+          if (i + 1 < bhi) k1 = __ldg(keys + i + 1);
+        }
+        const u64 x0 = k0 ^ q, x1 = k1 ^ q;
+        sym += (unsigned)min((x0 ? (__clzll((long long)x0) >> lb) : L) + 1, L);
+        if (i + 1 < bhi) sym += (unsigned)min((x1 ? (__clzll((long long)x1) >> lb) : L) + 1, L);
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) sym += __shfl_xor_sync(LCP_FULL_MASK, sym, o);
+      md = ix.tal_depth;
+      aux0 = (u64)(bhi - blo);
+      aux1 = sym;
+      tal_small = bhi - blo < k;
+      if (bhi == blo) {  // empty bucket: no hits, nothing scanned (tal.py:168-171)
+        if (lane == 0) {
+          out_hits[qi] = 0;
+          out_md[qi] = (uint16_t)md;
+          out_aux[2 * qi] = 0;
+          out_aux[2 * qi + 1] = 0;
+        }
+        continue;
+      }
+    }
+    if (tal_small) {
+      // |bucket| < k <= 32: rank the whole bucket, one item per lane
+      const int bs = bhi - blo;
+      C cv = ~C(0);
+      if (lane < bs) {
+        const u64 x = __ldg(keys + blo + lane) ^ q;
+        const int ll = x ? (__clzll((long long)x) >> lb) : L;
+        cv = make_comp<C>(ll, __ldg(order + blo + lane), L, idbits);
+      }
+      int rank = 0;
+      for (int jj = 0; jj < bs; ++jj) rank += __shfl_sync(LCP_FULL_MASK, cv, jj) < cv;
+      if (lane < bs) {
+        const u64 w = widen_comp<C>(cv, idbits);
+        out_ids[(size_t)qi * stride + rank] = (u32)(w & 0xffffffffull);
+        out_lcps[(size_t)qi * stride + rank] = (uint16_t)(L - (int)(w >> 32));
+      }
+      if (lane == 0) {
+        out_hits[qi] = bs;
+        out_md[qi] = (uint16_t)md;
+        out_aux[2 * qi] = aux0;
+        out_aux[2 * qi + 1] = aux1;
+      }
+      continue;
+    }
+
+    const int dstar = MODE == 0 ? dmax : window_dstar<T>(l, dmax, need);
+    if constexpr (MODE != 2) {
+      aux0 = (u64)(u32)dmax | ((u64)(u32)dstar << 32);
+    }
     C comp[T];
     int cnt = 0, r0 = 32 * T;
 #pragma unroll
@@ -377,9 +467,9 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, 1)
       }
       if (lane == 0) {
         out_hits[qi] = take;
-        out_md[qi] = (uint16_t)dmax;
-        out_aux[2 * qi] = (u64)(u32)dmax | ((u64)(u32)dstar << 32);
-        out_aux[2 * qi + 1] = (u64)(u32)cnt | ((u64)(u32)(s + r0) << 32);
+        out_md[qi] = (uint16_t)md;
+        out_aux[2 * qi] = aux0;
+        out_aux[2 * qi + 1] = MODE == 2 ? aux1 : ((u64)(u32)cnt | ((u64)(u32)(s + r0) << 32));
       }
       LCP_STAMP(qi, 6);
       LCP_STAMP(qi, 7);
@@ -392,8 +482,17 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, 1)
     extend_range<C, 1>(ix, qk, dstar, need, left, s, right, end, idbits, slot, rsize, rlo);
     LCP_STAMP(qi, 6);
     const int take = (int)min((long long)need, rsize);
-    write_result<C>(qi, stride, take, L, slot, idbits, dmax, dstar, rsize, rlo, out_ids,
-                    out_lcps, out_hits, out_md, out_aux);
+    if (lane < take) {
+      const u64 w = widen_comp<C>(slot, idbits);
+      out_ids[(size_t)qi * stride + lane] = (u32)(w & 0xffffffffull);
+      out_lcps[(size_t)qi * stride + lane] = (uint16_t)(L - (int)(w >> 32));
+    }
+    if (lane == 0) {
+      out_hits[qi] = take;
+      out_md[qi] = (uint16_t)md;
+      out_aux[2 * qi] = aux0;
+      out_aux[2 * qi + 1] = MODE == 2 ? aux1 : ((u64)rsize | ((u64)rlo << 32));
+    }
     LCP_STAMP(qi, 7);
   }
 }
