@@ -262,3 +262,78 @@ def test_device_api_with_torch(gpu):
     torch.cuda.synchronize()
     assert np.array_equal(ids.cpu().numpy().view(np.uint32), host.ids)
     assert np.array_equal(hits.cpu().numpy(), host.hits)
+
+
+def test_shard_encode_merge_kernels(gpu, oracle_lib):
+    """k_encode + k_merge over 3 row-block shards (gathered in one process)
+    equal the whole-corpus oracle, complete and strict."""
+    import torch
+
+    from paper_2602_04936_b200 import _native
+    from paper_2602_04936_b200.engine import NativeIndex
+    from paper_2602_04936_b200.sharded import ShardPlan
+
+    lib = _native.load()
+    ds = lg.generate_dataset(5000, 16, 4, seed=21)
+    qs = np.vstack([lg.generate_queries(ds, 300, seed=22), lg.generate_queries(ds, 300, seed=23, prefix_len=8)])
+    dq = torch.from_numpy(qs).cuda()
+    world, count = 3, len(qs)
+    plan = ShardPlan(ds.n, world)
+    shards = [NativeIndex(ds.items[lo:hi], 16, 4) for lo, hi in (plan.bounds(r) for r in range(world))]
+    full = oracle_lib.OracleTrie(ds.items, 4)
+    for k in (1, 10, 32):
+        for mode in ("complete", "strict"):
+            gathered = torch.empty((world, count, k), dtype=torch.int64, device="cuda")
+            for r, sh in enumerate(shards):
+                ls = sh.stride_for(k)
+                ids = torch.empty((count, ls), dtype=torch.int32, device="cuda")
+                lcps = torch.empty((count, ls), dtype=torch.int16, device="cuda")
+                hits = torch.empty(count, dtype=torch.int32, device="cuda")
+                sh.query_device(dq, k, mode, ids, lcps, hits, stream=0)
+                _native.check(lib.lcp_encode_candidates(ids.data_ptr(), lcps.data_ptr(), hits.data_ptr(), count,
+                                                        k, ls, 16, plan.bounds(r)[0], gathered[r].data_ptr(), 0))
+            take = min(k, ds.n)
+            oids = torch.empty((count, take), dtype=torch.int32, device="cuda")
+            olcps = torch.empty((count, take), dtype=torch.int16, device="cuda")
+            ohits = torch.empty(count, dtype=torch.int32, device="cuda")
+            _native.check(lib.lcp_merge_candidates(gathered.data_ptr(), world, count, k, take, 16,
+                                                   1 if mode == "strict" else 0, oids.data_ptr(),
+                                                   olcps.data_ptr(), ohits.data_ptr(), 0))
+            torch.cuda.synchronize()
+            ids_h, lcps_h, hits_h = oids.cpu().numpy().view(np.uint32), olcps.cpu().numpy(), ohits.cpu().numpy()
+            fids, flcps, fhits, _, _, _ = full.query_batch(qs, k, mode)
+            for i in range(count):
+                got = list(zip(ids_h[i, :hits_h[i]].tolist(), lcps_h[i, :hits_h[i]].tolist()))
+                assert got == list(zip(fids[i, :fhits[i]].tolist(), flcps[i, :fhits[i]].tolist())), (k, mode, i)
+
+
+def test_sharded_index_single_rank_nccl(gpu):
+    """ShardedIndex end to end on a 1-rank NCCL group (the collective path
+    with world size 1) equals the unsharded index."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2602_04936_b200.sharded import ShardedIndex
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        ds = lg.generate_dataset(20_000, 24, 4, seed=31)
+        qs = lg.generate_queries(ds, 512, seed=32, prefix_len=12)
+        sh = ShardedIndex(ds.items, 24, 4, id_offset=0)
+        dq = torch.from_numpy(qs).cuda()
+        ids = torch.empty((512, 10), dtype=torch.int32, device="cuda")
+        lcps = torch.empty((512, 10), dtype=torch.int16, device="cuda")
+        hits = torch.empty(512, dtype=torch.int32, device="cuda")
+        sh.query_device(dq, 10, ids, lcps, hits)
+        torch.cuda.synchronize()
+        ref = lg.build(ds).query_batch(qs, 10, "complete")
+        assert np.array_equal(hits.cpu().numpy(), ref.hits)
+        assert np.array_equal(ids.cpu().numpy().view(np.uint32), ref.ids)
+        assert np.array_equal(lcps.cpu().numpy().view(np.uint16), ref.lcps)
+    finally:
+        dist.destroy_process_group()
