@@ -142,6 +142,18 @@ int lcp_packed_layout_for(int32_t count, int32_t out_stride, lcp_packed_layout* 
 int lcp_query_host_packed(const lcp_index* index, lcp_workspace* ws, const uint16_t* queries,
                           int32_t count, int32_t k, int32_t mode, int32_t out_stride,
                           void* out_block);
+/* Asynchronous lcp_query_host_packed: enqueues the H2D copy, the query kernel
+ * and the single D2H copy on the workspace's stream and returns at once.  The
+ * host buffers must stay untouched until lcp_workspace_wait(ws) returns.  At
+ * most one batch in flight per workspace; use several workspaces to overlap
+ * consecutive batches (transfers, kernels and host work run concurrently). */
+#define LCP_PACKED_NO_WORK 1 /* flags: skip matched_depth/aux in the D2H copy */
+int lcp_query_host_packed_async(const lcp_index* index, lcp_workspace* ws,
+                                const uint16_t* queries, int32_t count, int32_t k, int32_t mode,
+                                int32_t out_stride, void* out_block, int32_t flags);
+/* Wait for the workspace's in-flight batch; LCP_ERR_INVALID_INPUT if it had
+ * a query symbol >= sigma.  A no-op when nothing is in flight. */
+int lcp_workspace_wait(lcp_workspace* ws);
 /* Device-side error flag raised by lcp_query (invalid query symbol); reading
  * it synchronises `stream`.  Returns LCP_OK or LCP_ERR_INVALID_INPUT and clears it. */
 int lcp_workspace_check(lcp_workspace* ws, void* stream);

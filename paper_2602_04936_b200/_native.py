@@ -80,6 +80,8 @@ SIGNATURES = {
     "lcp_workspace_check": (ctypes.c_int, [_P, _P]),
     "lcp_packed_layout_for": (ctypes.c_int, [_I32, _I32, ctypes.POINTER(PackedLayout)]),
     "lcp_query_host_packed": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _I32, _I32, _P]),
+    "lcp_query_host_packed_async": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _I32, _I32, _P, _I32]),
+    "lcp_workspace_wait": (ctypes.c_int, [_P]),
     "lcp_query": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P]),
     "lcp_query_host": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P]),
     "lcp_fullscan": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _P]),
@@ -155,6 +157,14 @@ class Workspace:
         h = ctypes.c_void_p()
         check(lib.lcp_workspace_create(ctypes.byref(h)))
         self.handle = h
+        self.submitted = 0  # async batches submitted on this workspace
+        self.completed = 0  # ... and waited for
+
+    def wait(self) -> None:
+        """Complete the in-flight async batch (if any)."""
+        if self.completed < self.submitted:
+            self.completed = self.submitted
+            check(load().lcp_workspace_wait(self.handle))
 
     @property
     def stream(self) -> int:
@@ -181,6 +191,22 @@ def workspace() -> Workspace:
     if ws is None:
         ws = Workspace()
         _tls.ws = ws
+    return ws
+
+
+ASYNC_DEPTH = 4  # batches in flight per thread for the async host path
+
+
+def async_workspace() -> Workspace:
+    """Next workspace of this thread's async ring; waits for the batch that
+    last used it (one batch in flight per workspace)."""
+    ring = getattr(_tls, "ring", None)
+    if ring is None:
+        ring = _tls.ring = [Workspace() for _ in range(ASYNC_DEPTH)]
+        _tls.ring_pos = 0
+    ws = ring[_tls.ring_pos]
+    _tls.ring_pos = (_tls.ring_pos + 1) % len(ring)
+    ws.wait()
     return ws
 
 

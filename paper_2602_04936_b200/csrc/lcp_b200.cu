@@ -11,6 +11,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
 #include <cstdio>
 #include <string>
 #include <vector>
@@ -193,6 +194,7 @@ int ilog2(int v) {
 // ===========================================================================
 struct lcp_index {
   DevIndex dv{};
+  unsigned long long generation = 0;  // unique per build: keys cached graphs
   int tal_depth = -1;
   long long tal_buckets = 0;  // -1: overflow (> 2^62)
   long long device_bytes = 0;
@@ -207,8 +209,32 @@ struct lcp_index {
   std::vector<long long> level_offset;  // cached trie level offsets
 };
 
+// One captured async submission (H2D -> query kernel -> D2H -> error word),
+// replayed with a single cudaGraphLaunch when the same buffers come back.
+struct GraphKey {
+  unsigned long long gen;
+  const void* queries;
+  void* out;
+  int count, k, mode, stride;
+  bool operator==(const GraphKey& o) const {
+    return gen == o.gen && queries == o.queries && out == o.out && count == o.count &&
+           k == o.k && mode == o.mode && stride == o.stride;
+  }
+};
+struct CachedGraph {
+  GraphKey key;
+  cudaGraphExec_t exec;
+  unsigned long long last_use;
+};
+constexpr int kGraphCache = 16;
+
 struct lcp_workspace {
   cudaStream_t stream = nullptr;
+  std::vector<CachedGraph> graphs;
+  unsigned long long tick = 0;
+  cudaEvent_t done = nullptr;  // completion of the in-flight async batch
+  bool pending = false;
+  int pending_sigma = 0;
   int* d_err = nullptr;
   int* h_err = nullptr;  // pinned
   DBuf qkeys, partial, hint, q_in, ids, lcps, hits, md, aux;
@@ -423,6 +449,12 @@ int lcp_index_build(const uint16_t* rows, int64_t n, int32_t length, int32_t sig
   if (n > 0 && !rows) return fail(LCP_ERR_INVALID_INPUT, "rows must not be null");
 
   lcp_index* ix = new lcp_index();
+  {
+    static unsigned long long next_gen = 1;
+    static std::mutex gen_mu;
+    std::lock_guard<std::mutex> lock(gen_mu);
+    ix->generation = next_gen++;
+  }
   DevIndex& dv = ix->dv;
   dv.n = n;
   dv.L = length;
@@ -675,6 +707,7 @@ int lcp_workspace_create(lcp_workspace** out) {
   if (e == cudaSuccess) e = cudaMalloc((void**)&ws->d_err, sizeof(int));
   if (e == cudaSuccess) e = cudaMemset(ws->d_err, 0, sizeof(int));
   if (e == cudaSuccess) e = cudaHostAlloc((void**)&ws->h_err, sizeof(int), cudaHostAllocDefault);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ws->done, cudaEventDisableTiming);
   if (e != cudaSuccess) {
     delete ws;
     return fail(LCP_ERR_CUDA, std::string("workspace: ") + cudaGetErrorString(e));
@@ -687,11 +720,14 @@ int lcp_workspace_create(lcp_workspace** out) {
 int lcp_workspace_free(lcp_workspace* ws) {
   if (!ws) return LCP_OK;
   if (ws->stream) cudaStreamSynchronize(ws->stream);
+  for (auto& g : ws->graphs) cudaGraphExecDestroy(g.exec);
+  ws->graphs.clear();
   for (DBuf* b : {&ws->qkeys, &ws->partial, &ws->hint, &ws->q_in, &ws->ids, &ws->lcps, &ws->hits,
                   &ws->md, &ws->aux})
     b->release();
   cudaFree(ws->d_err);
   cudaFreeHost(ws->h_err);
+  if (ws->done) cudaEventDestroy(ws->done);
   if (ws->stream) cudaStreamDestroy(ws->stream);
   delete ws;
   return LCP_OK;
@@ -916,6 +952,96 @@ int lcp_query_host_packed(const lcp_index* ix, lcp_workspace* ws, const uint16_t
   if (host_finish(ws) != LCP_OK)
     return fail(LCP_ERR_INVALID_INPUT,
                 "query symbol out of range for alphabet of size " + std::to_string(dv.sigma));
+  return LCP_OK;
+}
+
+int lcp_query_host_packed_async(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries,
+                                int32_t count, int32_t k, int32_t mode, int32_t out_stride,
+                                void* out_block, int32_t flags) {
+  if (!ix || !ws) return fail(LCP_ERR_INVALID_INPUT, "null index or workspace");
+  if (ws->pending) return fail(LCP_ERR_STATE, "workspace already has a batch in flight");
+  if (count <= 0) return LCP_OK;
+  if (out_stride < 1 || !out_block || !queries)
+    return fail(LCP_ERR_INVALID_INPUT, "bad output block or queries");
+  const DevIndex& dv = ix->dv;
+  cudaStream_t st = ws->stream;
+  const lcp_packed_layout lay = packed_layout(count, out_stride);
+  const size_t qb = (size_t)count * dv.L * 2;
+  const GraphKey key{ix->generation, queries, out_block, count, k, mode | (flags << 8), out_stride};
+  const size_t d2h = (flags & LCP_PACKED_NO_WORK) ? (size_t)lay.matched_depth : (size_t)lay.total;
+  static const bool no_graphs = getenv("LCP_NO_GRAPH_CACHE") != nullptr;  // A/B switch
+  ++ws->tick;
+  for (auto& g : ws->graphs) {
+    if (g.key == key) {  // replay: one launch for the whole submission
+      g.last_use = ws->tick;
+      LCP_CK(cudaGraphLaunch(g.exec, st));
+      LCP_CK(cudaEventRecord(ws->done, st));
+      ws->pending = true;
+      ws->pending_sigma = dv.sigma;
+      return LCP_OK;
+    }
+  }
+  // every buffer the submission touches exists before capture (no allocation inside)
+  LCP_TRY(ws->q_in.ensure(qb));
+  LCP_TRY(ws->ids.ensure((size_t)lay.total));
+  LCP_TRY(ws->qkeys.ensure((size_t)count * dv.W * 8));
+  char* d = static_cast<char*>(ws->ids.p);
+  auto enqueue = [&]() -> int {
+    LCP_CK(cudaMemcpyAsync(ws->q_in.p, queries, qb, cudaMemcpyHostToDevice, st));
+    LCP_TRY(lcp_query(ix, ws, ws->q_in.as<uint16_t>(), count, k, mode, out_stride,
+                      reinterpret_cast<uint32_t*>(d + lay.ids),
+                      reinterpret_cast<uint16_t*>(d + lay.lcps),
+                      reinterpret_cast<int32_t*>(d + lay.hits),
+                      reinterpret_cast<uint16_t*>(d + lay.matched_depth),
+                      reinterpret_cast<uint64_t*>(d + lay.aux), st));
+    LCP_CK(cudaMemcpyAsync(out_block, d, d2h, cudaMemcpyDeviceToHost, st));
+    LCP_CK(cudaMemcpyAsync(ws->h_err, ws->d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    return LCP_OK;
+  };
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  bool captured = false;
+  if (!no_graphs && cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+    const int r = enqueue();
+    const cudaError_t e = cudaStreamEndCapture(st, &graph);
+    if (r == LCP_OK && e == cudaSuccess && graph &&
+        cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess)
+      captured = true;
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();  // a failed capture leaves nothing enqueued
+  }
+  if (captured) {
+    if ((int)ws->graphs.size() >= kGraphCache) {
+      auto old = std::min_element(ws->graphs.begin(), ws->graphs.end(),
+                                  [](const CachedGraph& a, const CachedGraph& b) {
+                                    return a.last_use < b.last_use;
+                                  });
+      cudaGraphExecDestroy(old->exec);
+      ws->graphs.erase(old);
+    }
+    ws->graphs.push_back({key, exec, ws->tick});
+    LCP_CK(cudaGraphLaunch(exec, st));
+  } else {
+    LCP_TRY(enqueue());
+  }
+  LCP_CK(cudaEventRecord(ws->done, st));
+  ws->pending = true;
+  ws->pending_sigma = dv.sigma;
+  return LCP_OK;
+}
+
+int lcp_workspace_wait(lcp_workspace* ws) {
+  if (!ws) return fail(LCP_ERR_INVALID_INPUT, "null workspace");
+  if (!ws->pending) return LCP_OK;
+  ws->pending = false;
+  LCP_CK(cudaEventSynchronize(ws->done));
+  if (*ws->h_err) {
+    *ws->h_err = 0;
+    LCP_CK(cudaMemsetAsync(ws->d_err, 0, sizeof(int), ws->stream));
+    LCP_CK(cudaStreamSynchronize(ws->stream));
+    return fail(LCP_ERR_INVALID_INPUT, "query symbol out of range for alphabet of size " +
+                                           std::to_string(ws->pending_sigma));
+  }
   return LCP_OK;
 }
 

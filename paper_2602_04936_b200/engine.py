@@ -136,9 +136,12 @@ class NativeIndex:
     def stride_for(self, k: int) -> int:
         return max(1, min(int(k), self.n))
 
-    def alloc_batch(self, count: int, k: int, mode: str = "complete", pinned: bool = True) -> BatchResult:
+    def alloc_batch(self, count: int, k: int, mode: str = "complete", pinned: bool = True,
+                    with_work: bool = True) -> BatchResult:
         """Output buffers for ``count`` queries.  Pinned: one page-locked block
-        in the lcp_packed_layout_for() layout, so a batch is one D2H copy."""
+        in the lcp_packed_layout_for() layout, so a batch is one D2H copy.
+        with_work=False (async path only) leaves matched_depth/aux out of
+        the copy (BatchResult.matched_depth/aux are None)."""
         stride = self.stride_for(k)
         if not pinned:
             return BatchResult(
@@ -168,6 +171,10 @@ class NativeIndex:
         )
         out._owners = [block]  # the page-locked block lives as long as the result
         out._packed = (block.address, count, stride)
+        out._flags = 0 if with_work else 1  # LCP_PACKED_NO_WORK
+        if not with_work:
+            out.matched_depth = None
+            out.aux = None
         return out
 
     def single_query_buffer(self, k: int, mode: str) -> BatchResult:
@@ -197,6 +204,8 @@ class NativeIndex:
         out.mode = mode
         ws = workspace()
         packed = getattr(out, "_packed", None)
+        if packed is not None and getattr(out, "_flags", 0):
+            raise InvalidInputError("with_work=False blocks are for query_batch_async only")
         if packed is not None and packed[1] == count:
             check(load().lcp_query_host_packed(
                 self.handle, ws.handle, ptr(queries), count, k_eff, MODES[mode], packed[2],
@@ -206,6 +215,25 @@ class NativeIndex:
             self.handle, ws.handle, ptr(queries), count, k_eff, MODES[mode], out.ids.shape[1],
             ptr(out.ids), ptr(out.lcps), ptr(out.hits), ptr(out.matched_depth), ptr(out.aux)))
         return out
+
+    def query_host_async(self, queries: np.ndarray, k: int, mode: str, out: BatchResult) -> "PendingBatch":
+        """Enqueue H2D + kernel + D2H for one batch into a pinned packed block
+        (from alloc_batch(pinned=True)) and return at once; .result() waits."""
+        if mode not in MODES:
+            raise InvalidInputError(f"unknown mode {mode!r}")
+        if k < 1:
+            raise InvalidInputError(f"k must be >= 1, got {k}")
+        packed = getattr(out, "_packed", None)
+        count = int(queries.shape[0])
+        if packed is None or packed[1] != count:
+            raise InvalidInputError("async queries need a pinned output block from alloc_batch")
+        out.mode = mode
+        ws = _native.async_workspace()
+        check(load().lcp_query_host_packed_async(
+            self._h, ws.handle, queries.__array_interface__["data"][0], count,
+            self.stride_for(k), MODES[mode], packed[2], packed[0], out._flags))
+        ws.submitted += 1
+        return PendingBatch(ws, ws.submitted, out)
 
     def query_device(self, queries, k: int, mode: str, ids, lcps, hits, matched_depth=None,
                      aux=None, stream: int | None = None, ws=None) -> None:
@@ -239,3 +267,20 @@ class NativeIndex:
         check(load().lcp_fullscan(
             self.handle, ws.handle, ptr(queries), count, self.stride_for(k), int(ids.shape[1]),
             ptr(ids), ptr(lcps), ptr(hits), st))
+
+
+class PendingBatch:
+    """An in-flight async batch; result() blocks until its D2H copy landed."""
+
+    __slots__ = ("_ws", "_seq", "_out")
+
+    def __init__(self, ws, seq: int, out: BatchResult):
+        self._ws = ws
+        self._seq = seq
+        self._out = out
+
+    def result(self) -> BatchResult:
+        ws = self._ws
+        if ws.completed < self._seq:  # still this workspace's in-flight batch
+            ws.wait()
+        return self._out

@@ -219,6 +219,22 @@ class TrieIndex:
             self._account(res, mode, work)
         return res
 
+    def query_batch_async(self, queries, k: int, mode: str = "complete", out: BatchResult | None = None):
+        """Asynchronous query_batch for pipelined serving: returns a pending
+        batch whose result() yields the BatchResult.  ``queries`` and ``out``
+        (pinned, from native.alloc_batch) must stay alive until then; up to
+        _native.ASYNC_DEPTH batches per thread overlap copies and kernels."""
+        if mode not in ("strict", "complete"):
+            raise InvalidInputError(f"mode must be 'strict' or 'complete', got {mode!r}")
+        if (type(queries) is np.ndarray and queries.dtype == np.uint16 and queries.ndim == 2
+                and queries.shape[1] == self.length and queries.flags.c_contiguous):
+            qs = queries  # already in the wire format; symbols are checked on the device
+        else:
+            qs = validate_query_batch(queries, self.length, self.sigma)
+        if out is None:
+            out = self._native.alloc_batch(qs.shape[0], k, mode, pinned=True)
+        return self._native.query_host_async(qs, k, mode, out)
+
     def fullscan_batch(self, queries, k: int, out: BatchResult | None = None) -> BatchResult:
         """Brute-force top-k over the same corpus (oracle.py:46-59 semantics)."""
         if k < 1:

@@ -337,3 +337,30 @@ def test_sharded_index_single_rank_nccl(gpu):
         assert np.array_equal(lcps.cpu().numpy().view(np.uint16), ref.lcps)
     finally:
         dist.destroy_process_group()
+
+
+def test_async_pipeline_matches_sync(gpu):
+    ds = lg.generate_dataset(100_000, 24, 4, seed=41)
+    idx = lg.build(ds)
+    batches = [lg.generate_queries(ds, 777, seed=42 + b, prefix_len=b * 3) for b in range(7)]
+    outs = [idx.native.alloc_batch(777, 5, "complete", pinned=True) for _ in range(3)]
+    pending, got = [], []
+    for b, qs in enumerate(batches):
+        if len(pending) == 3:
+            r = pending.pop(0).result()
+            got.append((r.ids.copy(), r.lcps.copy(), r.hits.copy(), r.aux.copy()))
+        pending.append(idx.query_batch_async(qs, 5, "complete", out=outs[b % 3]))
+    for p in pending:
+        r = p.result()
+        got.append((r.ids.copy(), r.lcps.copy(), r.hits.copy(), r.aux.copy()))
+    for qs, (ids, lcps, hits, aux) in zip(batches, got):
+        ref = idx.query_batch(qs, 5, "complete")
+        assert np.array_equal(ids, ref.ids) and np.array_equal(lcps, ref.lcps)
+        assert np.array_equal(hits, ref.hits) and np.array_equal(aux, ref.aux)
+    bad = batches[0].copy()
+    bad[3, 2] = 9
+    out = idx.native.alloc_batch(777, 5, "complete", pinned=True)
+    with pytest.raises(lg.InvalidInputError):
+        idx.query_batch_async(bad, 5, "complete", out=out).result()
+    r = idx.query_batch_async(batches[1], 5, "complete", out=out).result()
+    assert np.array_equal(r.ids, idx.query_batch(batches[1], 5, "complete").ids)
