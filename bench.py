@@ -9,7 +9,7 @@ d* -> rank selection), inputs resident in HBM.
 Timing: the steps are captured once in a CUDA graph and replayed, so the
 GPU is never starved by Python-side launch cost.  Step i runs on index
 replica i % 8 (8 identical replicas, 8 x 24 MB > 126 MB L2, so every step's
-index reads miss L2) and on CUDA stream i % 2 (two batches in flight, as a
+index reads miss L2) and on CUDA stream i % 3 (three batches in flight, as a
 serving loop keeps them); the whole K-step region is bracketed by CUDA
 events on the capture stream.  The same loop on one stream (one batch in
 flight) is reported beside it, and its per-step time is the kernel duration
@@ -41,6 +41,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "top-k LCP queries/sec at N=2M, L=32, k=10 (HBM GB/s frac); p50 latency; J/query"
 N_ITEMS, SEQ_LEN, SIGMA, K, BATCH = 2_000_000, 32, 4, 10, 4096
+INFLIGHT = 3  # batches in flight in the headline timed loop (streams)
 FALLBACK_HBM_GBS = 6650.0
 
 
@@ -302,9 +303,9 @@ def main() -> None:
 
             # one batch in flight (kernel duration for the roofline)
             single_ms, bufs1, _ = run_steps(1, args.steps, args.warmup)
-            # headline: two batches in flight
+            # headline: three batches in flight (a serving pipeline)
             sampler.start()
-            total_ms, bufs2, (t0, t1) = run_steps(2, args.steps, args.warmup, clocks=True)
+            total_ms, bufs2, (t0, t1) = run_steps(INFLIGHT, args.steps, args.warmup, clocks=True)
             clocks = sampler.stop(t0, t1)
             aux_all = bufs1[0][4]
             gpu_launches = args.steps
@@ -379,7 +380,7 @@ def main() -> None:
                    "alphabet": SIGMA, "k": K, "batch": BATCH, "mode": "complete",
                    "l2": ("inputs larger than L2: 8 index replicas (8 x 24 MB > 126 MB) cycled step to step"
                           if world == 1 else "row-block shard per rank; host-launched steps"),
-                   "launch": ("CUDA graph replay; 2 batches in flight on 2 streams"
+                   "launch": (f"CUDA graph replay; {INFLIGHT} batches in flight on {INFLIGHT} streams"
                               if world == 1 else "host loop"),
                    "parallelism": "single GPU" if world == 1 else f"row-block shards x{world} + NCCL all_gather merge"},
         "roofline": roofline,
@@ -561,6 +562,28 @@ def extras(idx, ds, qs, stream, flush_buf) -> dict:
             "fullscan_over_indexed": jq_fs / jq_idx,
             "method": "NVML total-energy delta over >=3 s of CUDA-graph-replayed batches (one in flight)",
         }
+    # config 4: the N x N materialisation wall vs the index (PAPER.md:493-496,
+    # reference bench.memory_wall: n*n*2 bytes of fp16 similarities)
+    n4 = 500_000
+    free_b, total_b = torch.cuda.mem_get_info()
+    mat_b = n4 * n4 * 2
+    try:
+        wall = torch.empty((n4, n4), dtype=torch.float16, device=dev)
+        alloc = "succeeded (unexpected)"
+        del wall
+    except torch.OutOfMemoryError as e:
+        alloc = "torch.OutOfMemoryError: " + str(e).split("\n")[0][:120]
+    d4 = lg.generate_dataset(n4, 32, SIGMA, seed=5)
+    i4 = lg.build(d4)
+    q4 = torch.from_numpy(lg.generate_queries(d4, BATCH, seed=6)).to(dev)
+    ms4, _ = per_step_ms(lambda i: i4.native.query_device(q4, K, "complete", ids, lcps, hits, stream=st), 64, 20)
+    out["oom_boundary_config4"] = {
+        "n": n4, "materialization_bytes": mat_b, "materialization_gib": mat_b / 2**30,
+        "free_hbm_bytes": int(free_b), "feasible": mat_b <= free_b, "nxn_fp16_alloc": alloc,
+        "index_device_bytes": i4.nbytes, "reference_arena_bytes": i4.arena_nbytes,
+        "materialization_over_index": mat_b / i4.nbytes,
+        "indexed_qps": BATCH / (ms4 / 1e3),
+    }
     # GNC config 2: N=100k, L=24, k=5, one query per call through the public API
     g = lg.generate_dataset(100_000, 24, SIGMA, seed=4)
     gi = lg.build(g)

@@ -762,10 +762,25 @@ __global__ void k_fill_empty(int count, int md, int* hits, uint16_t* out_md, u64
   }
 }
 
+// Reserve enough shared memory that two query CTAs (two batches in flight)
+// fit on one SM; the default carve-out for a 4 KB-smem kernel admits one.
+template <typename K>
+static void prefer_smem_carveout(K kernel) {
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 25);
+    cudaGetLastError();
+    done = true;
+  }
+}
+
 template <typename C, int T>
 static void launch_w1(const DevIndex& dv, int mode, unsigned grid, unsigned block, size_t smem,
                       cudaStream_t st, const uint16_t* q, int count, int k, int stride, u32* ids,
                       uint16_t* lcps, int* hits, uint16_t* md, u64* aux, int* err) {
+  prefer_smem_carveout(k_query_w1<C, T, 0>);
+  prefer_smem_carveout(k_query_w1<C, T, 1>);
+  prefer_smem_carveout(k_query_w1<C, T, 2>);
   if (mode == LCP_MODE_STRICT)
     k_query_w1<C, T, 0><<<grid, block, smem, st>>>(dv, q, count, k, stride, ids, lcps, hits, md, aux, err);
   else if (mode == LCP_MODE_COMPLETE)

@@ -258,7 +258,7 @@ __device__ __forceinline__ int level_count(const u64* __restrict__ tab, int cnt,
 }
 
 template <typename C, int T, int MODE>
-__global__ void __launch_bounds__(QW_MAX_THREADS, 1)
+__global__ void __launch_bounds__(QW_MAX_THREADS, 2)  // <= 32 regs: two batches share an SM
     k_query_w1(DevIndex ix, const uint16_t* __restrict__ queries, int count, int k,
                int stride, u32* __restrict__ out_ids, uint16_t* __restrict__ out_lcps,
                int* __restrict__ out_hits, uint16_t* __restrict__ out_md,

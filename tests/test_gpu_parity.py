@@ -357,6 +357,11 @@ def test_async_pipeline_matches_sync(gpu):
         ref = idx.query_batch(qs, 5, "complete")
         assert np.array_equal(ids, ref.ids) and np.array_equal(lcps, ref.lcps)
         assert np.array_equal(hits, ref.hits) and np.array_equal(aux, ref.aux)
+    lean = idx.native.alloc_batch(777, 5, "complete", pinned=True, with_work=False)
+    r = idx.query_batch_async(batches[2], 5, "complete", out=lean).result()
+    ref = idx.query_batch(batches[2], 5, "complete")
+    assert r.aux is None and r.matched_depth is None
+    assert np.array_equal(r.ids, ref.ids) and np.array_equal(r.hits, ref.hits)
     bad = batches[0].copy()
     bad[3, 2] = 9
     out = idx.native.alloc_batch(777, 5, "complete", pinned=True)
