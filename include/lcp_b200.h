@@ -97,6 +97,17 @@ int lcp_index_export_adjacent_lcp(const lcp_index* index, uint16_t* adj);
 int lcp_index_export_directory(const lcp_index* index, int64_t* directory);
 int lcp_index_trie_level_offsets(const lcp_index* index, int64_t* level_offset);
 int lcp_index_export_trie(const lcp_index* index, int32_t* row_lo, uint16_t* edge_symbol);
+/* LCPI index snapshot (storage.index_snapshot_bytes, storage.py:155-210),
+ * generated on the GPU and byte-identical to the reference.  Call with
+ * out == NULL to get the size in *size; then with a buffer of *size bytes
+ * (host or device).  Synchronous. */
+int lcp_index_snapshot(const lcp_index* index, uint8_t* out, int64_t* size);
+/* Load an LCPI snapshot (storage.index_from_snapshot_bytes,
+ * storage.py:226-389): validates the stream (bad magic / version / widths,
+ * truncation, level order, child ids, posting permutation, trailing bytes ->
+ * LCP_ERR_INVALID_INPUT), recovers the rows, rebuilds on the GPU and checks
+ * the rebuilt snapshot is byte-identical.  raw is a host buffer. */
+int lcp_index_from_snapshot(const uint8_t* raw, int64_t size, lcp_index** out);
 /* TalEngine.bucket_range_search (tal.py:124-136): binary search on the packed
  * d-prefixes, independent of the directory. q: `count` host queries; lo/hi host. */
 int lcp_index_bucket_range_search(const lcp_index* index, const uint16_t* queries,

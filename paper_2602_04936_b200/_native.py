@@ -74,6 +74,8 @@ SIGNATURES = {
     "lcp_index_trie_level_offsets": (ctypes.c_int, [_P, _P]),
     "lcp_index_export_trie": (ctypes.c_int, [_P, _P, _P]),
     "lcp_index_bucket_range_search": (ctypes.c_int, [_P, _P, _I32, _P, _P]),
+    "lcp_index_snapshot": (ctypes.c_int, [_P, _P, ctypes.POINTER(_I64)]),
+    "lcp_index_from_snapshot": (ctypes.c_int, [_P, _I64, ctypes.POINTER(_P)]),
     "lcp_workspace_create": (ctypes.c_int, [ctypes.POINTER(_P)]),
     "lcp_workspace_free": (ctypes.c_int, [_P]),
     "lcp_workspace_stream": (_P, [_P]),

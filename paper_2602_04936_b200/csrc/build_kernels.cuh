@@ -336,3 +336,129 @@ __global__ void __launch_bounds__(TT_THREADS) k_trie_scatter(DevIndex ix, const 
     edge[r] = (uint16_t)key_symbol(ix.keys, d - 1, ix);
   }
 }
+
+// ---------------------------------------------------------------------------
+// LCPI index snapshot (storage.py:12-27, 155-210), generated on the GPU from
+// the per-depth arena.  Record of node v at depth d, in node-id order:
+//   u16 depth | u32 posting_len | (d == L: u32 ids[posting_len]) | u16 child_count |
+//   (d < L: child_count x (u16 symbol, u32 child_id))
+// Children of a depth-d node covering rows [lo, hi) are the depth-(d+1) nodes
+// whose first row falls in [lo, hi); a leaf's posting is order[lo, hi).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ long long lower_i32(const int* a, long long m, long long v) {
+  long long lo = 0, hi = m;
+  while (lo < hi) {
+    long long mid = (lo + hi) >> 1;
+    if ((long long)a[mid] < v) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ int node_depth(const long long* off, int L, long long v) {
+  int lo = 0, hi = L + 1;  // largest d with off[d] <= v
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (off[mid] <= v) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ void put_u16(unsigned char* p, unsigned v) {
+  p[0] = (unsigned char)v;
+  p[1] = (unsigned char)(v >> 8);
+}
+__device__ __forceinline__ void put_u32(unsigned char* p, unsigned v) {
+  p[0] = (unsigned char)v;
+  p[1] = (unsigned char)(v >> 8);
+  p[2] = (unsigned char)(v >> 16);
+  p[3] = (unsigned char)(v >> 24);
+}
+
+// record sizes (bytes) of every node
+__global__ void k_snap_sizes(const int* __restrict__ row_lo, const long long* __restrict__ off,
+                             long long nodes, long long n, int L,
+                             unsigned long long* __restrict__ size) {
+  long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nodes) return;
+  const int d = node_depth(off, L, v);
+  const long long lo = row_lo[v];
+  const long long hi = v + 1 < off[d + 1] ? row_lo[v + 1] : n;
+  if (d == L) {
+    size[v] = 8ull + 4ull * (unsigned long long)(hi - lo);
+  } else {
+    const int* nxt = row_lo + off[d + 1];
+    const long long m = off[d + 2] - off[d + 1];
+    const long long cc = lower_i32(nxt, m, hi) - lower_i32(nxt, m, lo);
+    size[v] = 8ull + 6ull * (unsigned long long)cc;
+  }
+}
+
+// node headers: depth, posting_len, child_count
+__global__ void k_snap_headers(const int* __restrict__ row_lo, const long long* __restrict__ off,
+                               const unsigned long long* __restrict__ start, long long nodes,
+                               long long n, int L, unsigned char* __restrict__ out) {
+  long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nodes) return;
+  const int d = node_depth(off, L, v);
+  const long long lo = row_lo[v];
+  const long long hi = v + 1 < off[d + 1] ? row_lo[v + 1] : n;
+  unsigned char* p = out + start[v];
+  put_u16(p, (unsigned)d);
+  if (d == L) {
+    const unsigned plen = (unsigned)(hi - lo);
+    put_u32(p + 2, plen);
+    put_u16(p + 6 + 4ull * plen, 0u);
+  } else {
+    const int* nxt = row_lo + off[d + 1];
+    const long long m = off[d + 2] - off[d + 1];
+    const long long cc = lower_i32(nxt, m, hi) - lower_i32(nxt, m, lo);
+    put_u32(p + 2, 0u);
+    put_u16(p + 6, (unsigned)cc);
+  }
+}
+
+// child entries: node c (depth >= 1) is entry rank of its parent's list
+__global__ void k_snap_children(const int* __restrict__ row_lo, const uint16_t* __restrict__ edge,
+                                const long long* __restrict__ off,
+                                const unsigned long long* __restrict__ start, long long nodes,
+                                int L, unsigned char* __restrict__ out) {
+  long long c = 1 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nodes) return;
+  const int d = node_depth(off, L, c);  // >= 1
+  const long long row = row_lo[c];
+  const int* par = row_lo + off[d - 1];
+  const long long pm = off[d] - off[d - 1];
+  // parent: last depth-(d-1) node starting at or before row
+  long long lo = 0, hi = pm;
+  while (lo < hi) {
+    long long mid = (lo + hi) >> 1;
+    if ((long long)par[mid] <= row) lo = mid + 1;
+    else hi = mid;
+  }
+  const long long p = off[d - 1] + lo - 1;
+  const long long first = off[d] + lower_i32(row_lo + off[d], off[d + 1] - off[d], row_lo[p]);
+  unsigned char* q = out + start[p] + 8 + 6ull * (unsigned long long)(c - first);
+  put_u16(q, edge[c]);
+  put_u32(q + 2, (unsigned)c);
+}
+
+// postings: row i lands in the leaf covering it, in row order
+__global__ void k_snap_postings(const int* __restrict__ row_lo, const long long* __restrict__ off,
+                                const unsigned long long* __restrict__ start,
+                                const u32* __restrict__ order, long long n, int L,
+                                unsigned char* __restrict__ out) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int* leaf = row_lo + off[L];
+  const long long m = off[L + 1] - off[L];
+  long long lo = 0, hi = m;
+  while (lo < hi) {
+    long long mid = (lo + hi) >> 1;
+    if ((long long)leaf[mid] <= i) lo = mid + 1;
+    else hi = mid;
+  }
+  const long long v = off[L] + lo - 1;
+  put_u32(out + start[v] + 6 + 4ull * (unsigned long long)(i - leaf[lo - 1]), order[i]);
+}

@@ -599,6 +599,35 @@ int lcp_index_trie_level_offsets(const lcp_index* cix, int64_t* level_offset) {
   return LCP_OK;
 }
 
+// Per-depth arena (row_lo, edge_symbol, level_offset) materialised on the
+// device; the caller frees the three buffers.  n > 0.
+static int arena_device(lcp_index* ix, int** d_row, uint16_t** d_edge, long long** d_off) {
+  LCP_TRY(level_offsets(ix));
+  const long long n = ix->dv.n;
+  const int L = ix->dv.L;
+  const long long nodes = ix->level_offset[L + 1];
+  unsigned long long* d_cnt = nullptr;
+  const int nblk = (int)blocks_for(n - 1 > 0 ? n - 1 : 1, TT_THREADS);
+  LCP_CK(cudaMalloc((void**)d_row, (size_t)nodes * 4));
+  LCP_CK(cudaMalloc((void**)d_edge, (size_t)nodes * 2));
+  LCP_CK(cudaMalloc((void**)d_off, (size_t)(L + 2) * 8));
+  LCP_CK(cudaMalloc((void**)&d_cnt, (size_t)nblk * L * 8));
+  LCP_CK(cudaMemcpy(*d_off, ix->level_offset.data(), (size_t)(L + 2) * 8, cudaMemcpyHostToDevice));
+  int root_row = 0;
+  uint16_t root_sym = 0;
+  LCP_CK(cudaMemcpy(*d_row, &root_row, 4, cudaMemcpyHostToDevice));
+  LCP_CK(cudaMemcpy(*d_edge, &root_sym, 2, cudaMemcpyHostToDevice));
+  dim3 grid(nblk, L);
+  k_trie_count<<<grid, TT_THREADS>>>(ix->adj, n, nblk, d_cnt);
+  LCP_CK_LAUNCH();
+  LCP_TRY(scan_exclusive<unsigned long long>(d_cnt, (long long)nblk * L, 0));
+  k_trie_scatter<<<grid, TT_THREADS>>>(ix->dv, ix->adj, nblk, d_cnt, *d_off, *d_row, *d_edge);
+  LCP_CK_LAUNCH();
+  LCP_CK(cudaDeviceSynchronize());
+  cudaFree(d_cnt);
+  return LCP_OK;
+}
+
 int lcp_index_export_trie(const lcp_index* cix, int32_t* row_lo, uint16_t* edge_symbol) {
   if (!cix) return fail(LCP_ERR_INVALID_INPUT, "null index");
   lcp_index* ix = const_cast<lcp_index*>(cix);
@@ -616,34 +645,219 @@ int lcp_index_export_trie(const lcp_index* cix, int32_t* row_lo, uint16_t* edge_
   int* d_row = nullptr;
   uint16_t* d_edge = nullptr;
   long long* d_off = nullptr;
-  unsigned long long* d_cnt = nullptr;
-  const int nblk = (int)blocks_for(n - 1 > 0 ? n - 1 : 1, TT_THREADS);
-  LCP_CK(cudaMalloc((void**)&d_row, (size_t)nodes * 4));
-  LCP_CK(cudaMalloc((void**)&d_edge, (size_t)nodes * 2));
-  LCP_CK(cudaMalloc((void**)&d_off, (size_t)(L + 2) * 8));
-  LCP_CK(cudaMalloc((void**)&d_cnt, (size_t)nblk * L * 8));
-  LCP_CK(cudaMemcpy(d_off, ix->level_offset.data(), (size_t)(L + 2) * 8, cudaMemcpyHostToDevice));
-  int root_row = 0;
-  uint16_t root_sym = 0;
-  LCP_CK(cudaMemcpy(d_row, &root_row, 4, cudaMemcpyHostToDevice));
-  LCP_CK(cudaMemcpy(d_edge, &root_sym, 2, cudaMemcpyHostToDevice));
-  dim3 grid(nblk, L);
-  k_trie_count<<<grid, TT_THREADS>>>(ix->adj, n, nblk, d_cnt);
-  LCP_CK_LAUNCH();
-  LCP_TRY(scan_exclusive<unsigned long long>(d_cnt, (long long)nblk * L, 0));
-  k_trie_scatter<<<grid, TT_THREADS>>>(ix->dv, ix->adj, nblk, d_cnt, d_off, d_row, d_edge);
-  LCP_CK_LAUNCH();
-  LCP_CK(cudaDeviceSynchronize());
-  int r = copy_out(row_lo, d_row, (size_t)nodes * 4);
+  int r = arena_device(ix, &d_row, &d_edge, &d_off);
+  if (r == LCP_OK) r = copy_out(row_lo, d_row, (size_t)nodes * 4);
   if (r == LCP_OK) r = copy_out(edge_symbol, d_edge, (size_t)nodes * 2);
   cudaFree(d_row);
   cudaFree(d_edge);
   cudaFree(d_off);
-  cudaFree(d_cnt);
+  return r;
+}
+
+int lcp_index_snapshot(const lcp_index* cix, uint8_t* out, int64_t* size) {
+  if (!cix || !size) return fail(LCP_ERR_INVALID_INPUT, "null argument");
+  lcp_index* ix = const_cast<lcp_index*>(cix);
+  LCP_TRY(level_offsets(ix));
+  const long long n = ix->dv.n;
+  const int L = ix->dv.L;
+  const long long nodes = ix->level_offset[L + 1];
+  // header (storage.py:44, "<4sH6BQIIQ"): magic version widths[6] n length sigma node_count
+  unsigned char header[36];
+  memcpy(header, "LCPI", 4);
+  const uint16_t version = 1;
+  memcpy(header + 4, &version, 2);
+  const unsigned char widths[6] = {2, 4, 4, 2, 4, 2};  // storage.py:45
+  memcpy(header + 6, widths, 6);
+  const uint64_t n64 = (uint64_t)n, nodes64 = (uint64_t)nodes;
+  const uint32_t len32 = (uint32_t)L, sig32 = (uint32_t)ix->dv.sigma;
+  memcpy(header + 12, &n64, 8);
+  memcpy(header + 20, &len32, 4);
+  memcpy(header + 24, &sig32, 4);
+  memcpy(header + 28, &nodes64, 8);
+  if (n == 0) {  // a bare root: depth 0, no posting, no children
+    const long long total = 36 + 8;
+    if (!out) {
+      *size = total;
+      return LCP_OK;
+    }
+    if (*size < total) return fail(LCP_ERR_INVALID_INPUT, "snapshot buffer too small");
+    unsigned char rec[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    LCP_TRY(copy_out(out, header, 36));
+    LCP_TRY(copy_out(out + 36, rec, 8));
+    *size = total;
+    return LCP_OK;
+  }
+  int* d_row = nullptr;
+  uint16_t* d_edge = nullptr;
+  long long* d_off = nullptr;
+  LCP_TRY(arena_device(ix, &d_row, &d_edge, &d_off));
+  unsigned long long* d_start = nullptr;
+  LCP_CK(cudaMalloc((void**)&d_start, (size_t)(nodes + 1) * 8));
+  LCP_CK(cudaMemset(d_start + nodes, 0, 8));
+  k_snap_sizes<<<blocks_for(nodes, 256), 256>>>(d_row, d_off, nodes, n, L, d_start);
+  LCP_CK_LAUNCH();
+  LCP_TRY(scan_exclusive<unsigned long long>(d_start, nodes + 1, 0));
+  unsigned long long body = 0;
+  LCP_CK(cudaMemcpy(&body, d_start + nodes, 8, cudaMemcpyDeviceToHost));
+  const long long total = 36 + (long long)body;
+  int r = LCP_OK;
+  if (!out) {
+    *size = total;
+  } else if (*size < total) {
+    r = fail(LCP_ERR_INVALID_INPUT, "snapshot buffer too small");
+  } else {
+    unsigned char* d_out = nullptr;
+    if (cudaMalloc((void**)&d_out, (size_t)total) != cudaSuccess) {
+      r = fail(LCP_ERR_CUDA, "cudaMalloc for the snapshot failed");
+    } else {
+      cudaMemcpy(d_out, header, 36, cudaMemcpyHostToDevice);
+      k_snap_headers<<<blocks_for(nodes, 256), 256>>>(d_row, d_off, d_start, nodes, n, L, d_out + 36);
+      if (nodes > 1)
+        k_snap_children<<<blocks_for(nodes - 1, 256), 256>>>(d_row, d_edge, d_off, d_start, nodes, L,
+                                                             d_out + 36);
+      k_snap_postings<<<blocks_for(n, 256), 256>>>(d_row, d_off, d_start, ix->order, n, L, d_out + 36);
+      if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
+        r = fail(LCP_ERR_CUDA, "snapshot kernels failed");
+      if (r == LCP_OK) r = copy_out(out, d_out, (size_t)total);
+      cudaFree(d_out);
+      *size = total;
+    }
+  }
+  cudaFree(d_start);
+  cudaFree(d_row);
+  cudaFree(d_edge);
+  cudaFree(d_off);
   return r;
 }
 
 }  // extern "C"
+
+// Host-side reader of an LCPI snapshot (storage.py:226-389): validates the
+// stream like the reference, recovers the dataset rows from the arena (each
+// depth-d node's edge symbol is symbol d-1 of every row it covers), rebuilds
+// the index on the GPU and checks the rebuilt snapshot is byte-identical.
+int lcp_index_from_snapshot(const uint8_t* raw, int64_t size, lcp_index** out) {
+  if (!raw || !out) return fail(LCP_ERR_INVALID_INPUT, "null argument");
+  *out = nullptr;
+  auto rd16 = [&](long long p) { return (unsigned)raw[p] | ((unsigned)raw[p + 1] << 8); };
+  auto rd32 = [&](long long p) {
+    return (unsigned long long)raw[p] | ((unsigned long long)raw[p + 1] << 8) |
+           ((unsigned long long)raw[p + 2] << 16) | ((unsigned long long)raw[p + 3] << 24);
+  };
+  if (size < 36) return fail(LCP_ERR_INVALID_INPUT, "truncated index header");
+  if (memcmp(raw, "LCPI", 4) != 0) return fail(LCP_ERR_INVALID_INPUT, "not an index snapshot (bad magic)");
+  if (rd16(4) != 1) return fail(LCP_ERR_INVALID_INPUT, "unsupported snapshot version " + std::to_string(rd16(4)));
+  const unsigned char widths[6] = {2, 4, 4, 2, 4, 2};
+  if (memcmp(raw + 6, widths, 6) != 0) return fail(LCP_ERR_INVALID_INPUT, "unsupported field widths");
+  unsigned long long n64, nodes64;
+  uint32_t L32, sig32;
+  memcpy(&n64, raw + 12, 8);
+  memcpy(&L32, raw + 20, 4);
+  memcpy(&sig32, raw + 24, 4);
+  memcpy(&nodes64, raw + 28, 8);
+  const long long n = (long long)n64, nodes = (long long)nodes64;
+  const int L = (int)L32;
+  if (n < 0 || n >= (1ll << 31) || L < 1 || L > 65535 || sig32 < 2 || sig32 > 65536)
+    return fail(LCP_ERR_INVALID_INPUT, "snapshot header out of range");
+  // walk the records level by level
+  std::vector<long long> lvl_count, rec_start;
+  std::vector<unsigned> ccs, plens;
+  std::vector<uint16_t> edge(std::max(1ll, nodes), 0);
+  long long pos = 36, parsed = 0, expected = 1, next_id = 1;
+  while (parsed < nodes) {
+    const int d = (int)lvl_count.size();
+    for (long long i = 0; i < expected; ++i) {
+      if (pos + 8 > size) return fail(LCP_ERR_INVALID_INPUT, "truncated node record at byte " + std::to_string(pos));
+      const unsigned depth = rd16(pos);
+      const unsigned long long plen = rd32(pos + 2);
+      const long long cc_at = pos + 6 + 4 * (long long)plen;
+      if (cc_at + 2 > size) return fail(LCP_ERR_INVALID_INPUT, "truncated posting list at byte " + std::to_string(pos));
+      const unsigned cc = rd16(cc_at);
+      if ((int)depth != d) return fail(LCP_ERR_INVALID_INPUT, "expected depth " + std::to_string(d) + ", found " + std::to_string(depth));
+      if (cc_at + 2 + 6ll * cc > size) return fail(LCP_ERR_INVALID_INPUT, "truncated child list at byte " + std::to_string(pos));
+      for (unsigned c = 0; c < cc; ++c) {
+        const long long e = cc_at + 2 + 6ll * c;
+        const unsigned long long cid = rd32(e + 2);
+        if ((long long)cid != next_id || next_id >= nodes)
+          return fail(LCP_ERR_INVALID_INPUT, "child ids at depth " + std::to_string(d) + " are not the next level");
+        edge[next_id++] = (uint16_t)rd16(e);
+      }
+      rec_start.push_back(pos);
+      plens.push_back((unsigned)plen);
+      ccs.push_back(cc);
+      pos = cc_at + 2 + 6ll * cc;
+    }
+    lvl_count.push_back(expected);
+    parsed += expected;
+    long long nxt = 0;
+    for (long long i = parsed - expected; i < parsed; ++i) nxt += ccs[i];
+    expected = nxt;
+    if (expected == 0) break;
+  }
+  if (parsed != nodes)
+    return fail(LCP_ERR_INVALID_INPUT, "header claims " + std::to_string(nodes) + " nodes, file holds " + std::to_string(parsed));
+  if (pos != size) return fail(LCP_ERR_INVALID_INPUT, std::to_string(size - pos) + " trailing bytes");
+  const int depths = (int)lvl_count.size() - 1;
+  if (depths > L) return fail(LCP_ERR_INVALID_INPUT, "node depth exceeds declared length");
+  if (n > 0 && depths != L) return fail(LCP_ERR_INVALID_INPUT, "leaf level is not at full depth");
+  // postings of the last level form the sort permutation
+  std::vector<long long> lvl_off(lvl_count.size() + 1, 0);
+  for (size_t d = 0; d < lvl_count.size(); ++d) lvl_off[d + 1] = lvl_off[d] + lvl_count[d];
+  std::vector<uint32_t> order;
+  order.reserve(n);
+  const size_t leaf0 = lvl_off[depths];
+  for (size_t v = leaf0; v < (size_t)parsed; ++v)
+    for (unsigned j = 0; j < plens[v]; ++j) order.push_back((uint32_t)rd32(rec_start[v] + 6 + 4ll * j));
+  if ((long long)order.size() != n)
+    return fail(LCP_ERR_INVALID_INPUT, "posting lists hold " + std::to_string(order.size()) + " items, header claims " + std::to_string(n));
+  std::vector<char> seen(std::max(1ll, n), 0);
+  for (uint32_t id : order) {
+    if ((long long)id >= n || seen[id]) return fail(LCP_ERR_INVALID_INPUT, "posting ids are not a permutation");
+    seen[id] = 1;
+  }
+  if (n == 0) return lcp_index_build(nullptr, 0, L, (int)sig32, -1, out);
+  // subtree sizes bottom-up -> each node's row range; rows from the paths
+  std::vector<long long> sz(parsed, 0);
+  for (size_t v = leaf0; v < (size_t)parsed; ++v) sz[v] = plens[v];
+  for (int d = depths - 1; d >= 0; --d) {
+    long long child = lvl_off[d + 1];
+    for (long long v = lvl_off[d]; v < lvl_off[d + 1]; ++v) {
+      if (ccs[v] < 1) return fail(LCP_ERR_INVALID_INPUT, "childless interior node at depth " + std::to_string(d));
+      long long t = 0;
+      for (unsigned c = 0; c < ccs[v]; ++c) t += sz[child++];
+      sz[v] = t;
+    }
+  }
+  std::vector<uint16_t> items((size_t)n * L);
+  for (int d = 1; d <= depths; ++d) {
+    long long row = 0;
+    for (long long v = lvl_off[d]; v < lvl_off[d + 1]; ++v) {
+      if (edge[v] >= sig32) return fail(LCP_ERR_INVALID_INPUT, "edge symbol out of range for the alphabet");
+      for (long long r = row; r < row + sz[v]; ++r) items[(size_t)order[r] * L + d - 1] = edge[v];
+      row += sz[v];
+    }
+  }
+  lcp_index* ix = nullptr;
+  LCP_TRY(lcp_index_build(items.data(), n, L, (int)sig32, -1, &ix));
+  // integrity: the rebuilt index must serialise to exactly these bytes
+  int64_t rsize = 0;
+  int r = lcp_index_snapshot(ix, nullptr, &rsize);
+  if (r == LCP_OK && rsize != size) r = fail(LCP_ERR_INVALID_INPUT, "snapshot is not canonical (size mismatch)");
+  if (r == LCP_OK) {
+    std::vector<uint8_t> again((size_t)rsize);
+    r = lcp_index_snapshot(ix, again.data(), &rsize);
+    if (r == LCP_OK && memcmp(again.data(), raw, (size_t)size) != 0)
+      r = fail(LCP_ERR_INVALID_INPUT, "snapshot is not canonical (rebuilt bytes differ)");
+  }
+  if (r != LCP_OK) {
+    std::string keep = g_err;
+    lcp_index_free(ix);
+    g_err = keep;
+    return r;
+  }
+  *out = ix;
+  return LCP_OK;
+}
 
 __global__ void k_bucket_search(DevIndex ix, const u64* __restrict__ qkeys, int count,
                                 long long* __restrict__ lo, long long* __restrict__ hi) {

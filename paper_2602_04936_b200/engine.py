@@ -42,6 +42,18 @@ class NativeIndex:
         self.bits = int(info.bits)
 
     @classmethod
+    def from_handle(cls, h: ctypes.c_void_p):
+        """Adopt an lcp_index* built by the library (e.g. from a snapshot)."""
+        self = cls.__new__(cls)
+        self._h = h
+        info = IndexInfo()
+        check(load().lcp_index_get_info(h, ctypes.byref(info)))
+        self.info = info
+        self.n, self.length, self.sigma = int(info.n), int(info.length), int(info.sigma)
+        self.words, self.bits = int(info.words), int(info.bits)
+        return self
+
+    @classmethod
     def from_device(cls, rows_ptr: int, n: int, length: int, sigma: int, tal_depth: int = -1):
         """Build from a device pointer (e.g. a CUDA uint16 tensor's data_ptr())."""
         self = cls.__new__(cls)

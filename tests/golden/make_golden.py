@@ -55,6 +55,7 @@ def sha(a: np.ndarray) -> str:
 def main() -> int:
     sys.path.insert(0, REF_SRC)
     import lcpsearch as ref  # noqa: E402
+    import lcpsearch.storage  # noqa: E402,F401  (ref.storage)
 
     arrays: dict[str, np.ndarray] = {}
     manifest = []
@@ -83,6 +84,12 @@ def main() -> int:
             "edge_symbol_sha256": sha(index.edge_symbol.astype(np.uint16)),
             "node_count": index.node_count,
         }
+        snap = ref.storage.index_snapshot_bytes(index)
+        entry["snapshot_sha256"] = hashlib.sha256(snap).hexdigest()
+        entry["snapshot_size"] = len(snap)
+        if len(snap) <= 64 * 1024:  # small reference snapshots for the loader tests
+            with open(os.path.join(HERE, f"snap_{name}.lcpi"), "wb") as fh:
+                fh.write(snap)
         for mode in ("strict", "complete"):
             ids = np.full((count, kmax), -1, dtype=np.int64)
             lcps = np.full((count, kmax), -1, dtype=np.int64)

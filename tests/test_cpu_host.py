@@ -168,3 +168,16 @@ def test_batch_result_views():
     assert r.pairs() == [(4, 3), (2, 1)] and r.indices.dtype == np.int64 and r.matched_depth == 3
     b.hits[0] = 0
     assert b.result(0).pairs() == [] and b.result(0).matched_depth == 3
+
+
+def test_dataset_file_round_trip(tmp_path):
+    from paper_2602_04936_b200 import storage
+
+    ds = generate_dataset(321, 7, 5, seed=3)
+    path = tmp_path / "d.lcpd"
+    storage.write_dataset(str(path), ds)
+    back = storage.read_dataset(str(path))
+    assert np.array_equal(back.items, ds.items) and back.alphabet.size == 5
+    path.write_bytes(b"NOPE" + path.read_bytes()[4:])
+    with pytest.raises(InvalidInputError):
+        storage.read_dataset(str(path))

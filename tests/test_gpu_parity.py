@@ -369,3 +369,50 @@ def test_async_pipeline_matches_sync(gpu):
         idx.query_batch_async(bad, 5, "complete", out=out).result()
     r = idx.query_batch_async(batches[1], 5, "complete", out=out).result()
     assert np.array_equal(r.ids, idx.query_batch(batches[1], 5, "complete").ids)
+
+
+def test_snapshot_bytes_match_reference(gpu, golden):
+    """index_snapshot_bytes(gpu_index) is byte-identical to the reference's
+    storage.index_snapshot_bytes for every golden case (storage.py:155-210)."""
+    import os
+
+    from paper_2602_04936_b200 import storage
+
+    for case in golden[0]["cases"]:
+        ds = case_dataset(case)
+        snap = storage.index_snapshot_bytes(lg.build(ds))
+        assert len(snap) == case["snapshot_size"], case["name"]
+        assert hashlib.sha256(snap).hexdigest() == case["snapshot_sha256"], case["name"]
+        path = os.path.join(os.path.dirname(__file__), "golden", f"snap_{case['name']}.lcpi")
+        if os.path.exists(path):  # load the reference's own bytes onto the GPU
+            raw = open(path, "rb").read()
+            assert raw == snap
+            loaded = storage.index_from_snapshot_bytes(raw)
+            assert loaded.n == ds.n and loaded.length == ds.length and loaded.sigma == ds.alphabet.size
+            assert np.array_equal(loaded.order, golden[1][case["name"] + "/order"])
+            qs = golden[1][case["name"] + "/queries"]
+            if len(qs):
+                a = loaded.query_batch(qs, 5, "complete")
+                b = lg.build(ds).query_batch(qs, 5, "complete")
+                assert np.array_equal(a.ids, b.ids) and np.array_equal(a.hits, b.hits)
+
+
+def test_snapshot_corruption_is_detected(gpu, golden, tmp_path):
+    import os
+
+    from paper_2602_04936_b200 import storage
+
+    raw = open(os.path.join(os.path.dirname(__file__), "golden", "snap_trie500.lcpi"), "rb").read()
+    bad = [raw[:20], b"XXXX" + raw[4:], raw[:4] + b"\x02\x00" + raw[6:], raw + b"\x00",
+           raw[:-3], raw[:40] + b"\x07\x00" + raw[42:]]
+    for blob in bad:
+        with pytest.raises(lg.InvalidInputError):
+            storage.index_from_snapshot_bytes(blob)
+    path = tmp_path / "x.lcpi"
+    idx = lg.build(lg.generate_dataset(777, 9, 3, seed=5))
+    storage.write_index(str(path), idx)
+    again = storage.read_index(str(path))
+    assert storage.index_snapshot_bytes(again) == path.read_bytes()
+    empty = lg.build(lg.Dataset.from_rows(np.zeros((0, 4), dtype=np.uint16), 4))
+    e = storage.index_snapshot_bytes(empty)
+    assert storage.index_snapshot_bytes(storage.index_from_snapshot_bytes(e)) == e
