@@ -562,6 +562,14 @@ def extras(idx, ds, qs, stream, flush_buf) -> dict:
             "fullscan_over_indexed": jq_fs / jq_idx,
             "method": "NVML total-energy delta over >=3 s of CUDA-graph-replayed batches (one in flight)",
         }
+    # config 3 with sigma = 65536: W = 8 (64-byte keys), index 2M x 76 B > L2
+    d8 = lg.generate_dataset(N_ITEMS, SEQ_LEN, 65536, seed=3)
+    i8 = lg.build(d8)
+    q8 = torch.from_numpy(lg.generate_queries(d8, BATCH, seed=4, prefix_len=2)).to(dev)
+    ms8, _ = per_step_ms(lambda i: i8.native.query_device(q8, K, "complete", ids, lcps, hits, stream=st), 16, 10)
+    out["indexed_sigma65536_qps"] = BATCH / (ms8 / 1e3)
+    out["indexed_sigma65536_device_bytes"] = i8.nbytes
+    del i8, d8
     # config 4: the N x N materialisation wall vs the index (PAPER.md:493-496,
     # reference bench.memory_wall: n*n*2 bytes of fp16 similarities)
     n4 = 500_000

@@ -416,3 +416,17 @@ def test_snapshot_corruption_is_detected(gpu, golden, tmp_path):
     empty = lg.build(lg.Dataset.from_rows(np.zeros((0, 4), dtype=np.uint16), 4))
     e = storage.index_snapshot_bytes(empty)
     assert storage.index_snapshot_bytes(storage.index_from_snapshot_bytes(e)) == e
+
+
+def test_wide_keys_at_scale(gpu, oracle_lib):
+    """sigma = 65536 at N = 2M (W = 8, 64-byte keys, index larger than L2):
+    the generic warp kernel must equal the full scan and the oracle."""
+    ds = lg.generate_dataset(2_000_000, 32, 65536, seed=3)
+    idx = lg.build(ds)
+    qs = np.vstack([lg.generate_queries(ds, 256, seed=4), lg.generate_queries(ds, 256, seed=5, prefix_len=2)])
+    b = idx.query_batch(qs, 10, "complete")
+    f = idx.fullscan_batch(qs, 10)
+    assert np.array_equal(b.hits, f.hits) and np.array_equal(b.ids, f.ids) and np.array_equal(b.lcps, f.lcps)
+    oid, olcp, oh = oracle_lib.oracle_top_k_batch(ds.items, qs[250:262], 10, nthreads=8)
+    for j, i in enumerate(range(250, 262)):
+        assert b.pairs(i) == list(zip(oid[j, :oh[j]].tolist(), olcp[j, :oh[j]].tolist()))
