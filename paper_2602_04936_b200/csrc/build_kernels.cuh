@@ -255,6 +255,40 @@ __global__ void k_gather_level(const u64* __restrict__ keys, long long cnt, long
 }
 
 // ---------------------------------------------------------------------------
+// id sketch level: block b of the output holds the LCP_SK_LIST smallest of
+// src[b*GROUP, (b+1)*GROUP) ascending.  Level 0 reads `order` (GROUP = 256
+// sorted positions); level j+1 reads level j's lists (GROUP = 32 lists x 32).
+// One CTA per output block, bitonic sort in shared memory (build time only).
+// ---------------------------------------------------------------------------
+constexpr int SK_THREADS = 256;
+template <int GROUP>
+__global__ void __launch_bounds__(SK_THREADS) k_id_sketch(const u32* __restrict__ src,
+                                                          long long src_len,
+                                                          u32* __restrict__ dst) {
+  __shared__ u32 buf[GROUP];
+  const long long base = (long long)blockIdx.x * GROUP;
+  for (int t = threadIdx.x; t < GROUP; t += SK_THREADS)
+    buf[t] = base + t < src_len ? src[base + t] : 0xffffffffu;
+  __syncthreads();
+  for (int k2 = 2; k2 <= GROUP; k2 <<= 1) {
+    for (int j = k2 >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < GROUP; i += SK_THREADS) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const u32 a = buf[i], c = buf[ixj];
+          if ((a > c) == ((i & k2) == 0)) {
+            buf[i] = c;
+            buf[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x < LCP_SK_LIST) dst[(long long)blockIdx.x * LCP_SK_LIST + threadIdx.x] = buf[threadIdx.x];
+}
+
+// ---------------------------------------------------------------------------
 // TAL dense directory: dir[c] = #items whose d-prefix code < c
 // (== np.searchsorted(codes, arange(sigma**d + 1)), tal.py:76-82).
 // The d-prefix fits word 0 whenever sigma**d <= 2**24.

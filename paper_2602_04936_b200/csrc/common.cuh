@@ -21,6 +21,9 @@ typedef unsigned int u32;
 #define LCP_MAX_LEVELS 12
 #define LCP_SEARCH_FANOUT 64  // k-ary search: 32 lanes x 2 separators
 #define LCP_LEAF_KEYS 32      // the last search table resolves a 32-key leaf block
+#define LCP_SK_BLOCK 256      // id sketch: level-0 block of sorted positions
+#define LCP_SK_FANOUT 32      // id sketch: child blocks per block above level 0
+#define LCP_SK_LIST 32        // id sketch: smallest ids kept per block (ascending)
 
 struct DevIndex {
   const u64* keys;        // sorted packed keys, n*W
@@ -40,6 +43,13 @@ struct DevIndex {
   int tal_depth;           // -1 when no TAL structure
   long long tal_buckets;   // sigma**tal_depth
   int idbits;              // id bits of the compact u32 composite (32: use u64)
+  // id sketch: for every block of LCP_SK_BLOCK * LCP_SK_FANOUT**j sorted
+  // positions, its LCP_SK_LIST smallest ids ascending (0xffffffff padded).
+  // Serves "smallest ids in a long sorted range" when R(d*) is huge.
+  const u32* sketch;
+  long long sk_off[LCP_MAX_LEVELS];  // block offset of level j (lists of LCP_SK_LIST)
+  long long sk_cnt[LCP_MAX_LEVELS];  // blocks at level j
+  int sk_levels;
 };
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }

@@ -206,6 +206,7 @@ struct lcp_index {
   uint16_t* adj = nullptr;
   u64* levels = nullptr;
   long long* directory = nullptr;
+  u32* sketch = nullptr;
   std::vector<long long> level_offset;  // cached trie level offsets
 };
 
@@ -256,6 +257,7 @@ int lcp_index_free(lcp_index* ix) {
   cudaFree(ix->adj);
   cudaFree(ix->levels);
   cudaFree(ix->directory);
+  cudaFree(ix->sketch);
   delete ix;
   return LCP_OK;
 }
@@ -403,6 +405,33 @@ static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, i
     if (end * W * 8 > kSmemStageCap) break;
     dv.smem_levels = j + 1;
     dv.smem_entries = (int)end;
+  }
+
+  // id sketch (smallest ids per block of sorted positions): bounds the work
+  // of a query whose R(d*) spans far more than the loaded region
+  {
+    long long cnt = (n + LCP_SK_BLOCK - 1) / LCP_SK_BLOCK, tot = 0;
+    int lv = 0;
+    for (;;) {
+      dv.sk_off[lv] = tot;
+      dv.sk_cnt[lv] = cnt;
+      tot += cnt;
+      ++lv;
+      if (cnt <= LCP_SK_FANOUT || lv == LCP_MAX_LEVELS) break;
+      cnt = (cnt + LCP_SK_FANOUT - 1) / LCP_SK_FANOUT;
+    }
+    dv.sk_levels = lv;
+    LCP_TRY(dalloc(&ix->sketch, tot * LCP_SK_LIST, acct));
+    k_id_sketch<LCP_SK_BLOCK><<<(unsigned)dv.sk_cnt[0], SK_THREADS, 0, st>>>(
+        ix->order, n, ix->sketch);
+    LCP_CK_LAUNCH();
+    for (int j = 1; j < lv; ++j) {
+      k_id_sketch<LCP_SK_FANOUT * LCP_SK_LIST><<<(unsigned)dv.sk_cnt[j], SK_THREADS, 0, st>>>(
+          ix->sketch + dv.sk_off[j - 1] * LCP_SK_LIST, dv.sk_cnt[j - 1] * LCP_SK_LIST,
+          ix->sketch + dv.sk_off[j] * LCP_SK_LIST);
+      LCP_CK_LAUNCH();
+    }
+    dv.sketch = ix->sketch;
   }
 
   // TAL bucket structure — tal.py:42-82

@@ -156,8 +156,97 @@ __device__ __forceinline__ void stage_levels(const DevIndex& ix, u64* bar, u64* 
 }
 
 // ---------------------------------------------------------------------------
+// Long runs.  Outside the loaded region every item of R(d*) has lcp exactly
+// d* (R(d*+1) has < need items and surrounds pos, so it lies inside the
+// region), so the tail of the answer is "the smallest ids in a sorted-position
+// range".  run_edge finds where the run ends; tier_offer reads the smallest
+// ids of that range from the id sketch instead of scanning it.
+// ---------------------------------------------------------------------------
+constexpr int EXT_SCAN_CHUNKS = 4;  // 32-key chunks scanned per side before the sketch path
+
+// Last position of the run {lcp >= d} walking from `in` (inside the run)
+// toward `out` (outside it, or the sentinel -1 / n): 32-ary warp search,
+// ceil(log32 |in - out|) rounds of one scattered probe per lane.
+template <int WMAX>
+__device__ __forceinline__ long long run_edge(const DevIndex& ix, const u64 (&qk)[WMAX], int d,
+                                              long long in, long long out) {
+  const long long dir = out > in ? 1 : -1;
+  for (;;) {
+    const long long span = (out - in) * dir;
+    if (span <= 1) return in;
+    const long long step = (span + 31) >> 5;
+    const long long off = step * (lane_id() + 1);
+    const bool inside = off < span && lcp_at<WMAX>(ix, in + dir * off, qk) >= d;
+    const long long c = __popc(__ballot_sync(LCP_FULL_MASK, inside));
+    if (step * (c + 1) < span) out = in + dir * step * (c + 1);
+    in += dir * step * c;
+  }
+}
+
+// offer tier|order[i] for i in [x, y)
+template <typename C>
+__device__ __forceinline__ void offer_positions(const DevIndex& ix, long long x, long long y,
+                                                C tier, C& slot, C& thr, int need) {
+  for (long long base = x; base < y; base += 32) {
+    const long long i = base + lane_id();
+    warp_offer(slot, thr, i < y ? (tier | (C)__ldg(ix.order + i)) : ~C(0), need);
+  }
+}
+
+// offer the id lists of sketch blocks [x, y) of one level; a block whose
+// smallest id cannot enter the top-need is skipped after one load
+template <typename C>
+__device__ __forceinline__ void offer_lists(const u32* __restrict__ lists, long long x, long long y,
+                                            C tier, C& slot, C& thr, int need) {
+  for (long long base = x; base < y; base += 32) {
+    const long long blk = base + lane_id();
+    const u32 mn = blk < y ? __ldg(lists + blk * LCP_SK_LIST) : 0xffffffffu;
+    const C cm = mn == 0xffffffffu ? ~C(0) : (tier | (C)mn);
+    unsigned m = __ballot_sync(LCP_FULL_MASK, cm < thr);
+    while (m) {
+      const int src = __ffs(m) - 1;
+      m &= m - 1;
+      if (__shfl_sync(LCP_FULL_MASK, cm, src) < thr) {
+        const u32 v = __ldg(lists + (base + src) * LCP_SK_LIST + lane_id());
+        warp_offer(slot, thr, v == 0xffffffffu ? ~C(0) : (tier | (C)v), need);
+      }
+    }
+  }
+}
+
+// the `need` smallest of tier|id over sorted positions [a, b): the partial
+// level-0 blocks at either end position by position, then at each sketch
+// level the blocks not covered by a whole block of the level above
+template <typename C>
+__device__ __noinline__ C tier_offer(const DevIndex& ix, long long a, long long b, C tier,
+                                     C slot, int need) {
+  // out of line: keeps the cold path's registers off the hot loop's budget
+  C thr = __shfl_sync(LCP_FULL_MASK, slot, need - 1);
+  long long A = (a + LCP_SK_BLOCK - 1) / LCP_SK_BLOCK, B = b / LCP_SK_BLOCK;
+  if (A >= B) {
+    offer_positions<C>(ix, a, b, tier, slot, thr, need);
+    return slot;
+  }
+  offer_positions<C>(ix, a, A * LCP_SK_BLOCK, tier, slot, thr, need);
+  offer_positions<C>(ix, B * LCP_SK_BLOCK, b, tier, slot, thr, need);
+  for (int j = 0;; ++j) {
+    const u32* lists = ix.sketch + ix.sk_off[j] * LCP_SK_LIST;
+    const long long A2 = (A + LCP_SK_FANOUT - 1) / LCP_SK_FANOUT, B2 = B / LCP_SK_FANOUT;
+    if (j + 1 >= ix.sk_levels || A2 >= B2) {
+      offer_lists<C>(lists, A, B, tier, slot, thr, need);
+      return slot;
+    }
+    offer_lists<C>(lists, A, A2 * LCP_SK_FANOUT, tier, slot, thr, need);
+    offer_lists<C>(lists, B2 * LCP_SK_FANOUT, B, tier, slot, thr, need);
+    A = A2;
+    B = B2;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Shared tail of the warp query kernels: R(d*) may continue past the loaded
-// window on either side; scan outward 32 keys at a time (rare at config 3).
+// region on either side.  Scan outward 32 keys at a time; a run still going
+// after EXT_SCAN_CHUNKS chunks is finished by run_edge + tier_offer.
 // ---------------------------------------------------------------------------
 template <typename C, int WMAX>
 __device__ __forceinline__ void extend_range(const DevIndex& ix, const u64 (&qk)[WMAX], int dstar,
@@ -169,9 +258,18 @@ __device__ __forceinline__ void extend_range(const DevIndex& ix, const u64 (&qk)
   const int L = ix.L;
   if (!(left || right)) return;
   C thr = __shfl_sync(LCP_FULL_MASK, slot, need - 1);
-  long long e = lo_edge;
+  const C tier = make_comp<C>(dstar, 0u, L, idbits);
+  long long e = lo_edge;  // [e, ...) is known to lie in R(d*)
   bool go = left;
-  while (go) {
+  for (int chunk = 0; go; ++chunk) {
+    if (chunk == EXT_SCAN_CHUNKS) {
+      const long long r = dstar ? run_edge<WMAX>(ix, qk, dstar, e, -1) : 0;
+      slot = tier_offer<C>(ix, r, e, tier, slot, need);
+      thr = __shfl_sync(LCP_FULL_MASK, slot, need - 1);
+      rsize += e - r;
+      rlo = r;
+      break;
+    }
     long long i = e - 32 + lane;
     int l = i >= 0 ? lcp_at<WMAX>(ix, i, qk) : -1;
     bool c = l >= dstar;
@@ -182,9 +280,15 @@ __device__ __forceinline__ void extend_range(const DevIndex& ix, const u64 (&qk)
     e -= 32;
     go = m == LCP_FULL_MASK && e > 0;
   }
-  e = hi_edge;
+  e = hi_edge;  // [..., e) is known to lie in R(d*)
   go = right;
-  while (go) {
+  for (int chunk = 0; go; ++chunk) {
+    if (chunk == EXT_SCAN_CHUNKS) {
+      const long long r = dstar ? run_edge<WMAX>(ix, qk, dstar, e - 1, n) + 1 : n;
+      slot = tier_offer<C>(ix, e, r, tier, slot, need);
+      rsize += r - e;
+      break;
+    }
     long long i = e + lane;
     int l = i < n ? lcp_at<WMAX>(ix, i, qk) : -1;
     bool c = l >= dstar;
@@ -259,7 +363,7 @@ __device__ __forceinline__ int level_count(const u64* __restrict__ tab, int cnt,
 
 template <typename C, int T, int MODE>
 __global__ void __launch_bounds__(QW_MAX_THREADS, 2)  // <= 32 regs: two batches share an SM
-    k_query_w1(DevIndex ix, const uint16_t* __restrict__ queries, int count, int k,
+    k_query_w1(const __grid_constant__ DevIndex ix, const uint16_t* __restrict__ queries, int count, int k,
                int stride, u32* __restrict__ out_ids, uint16_t* __restrict__ out_lcps,
                int* __restrict__ out_hits, uint16_t* __restrict__ out_md,
                u64* __restrict__ out_aux, int* __restrict__ err) {
@@ -503,7 +607,7 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, 2)  // <= 32 regs: two batches
 // ---------------------------------------------------------------------------
 template <int WMAX>
 __global__ void __launch_bounds__(QW_MAX_THREADS, 1)
-    k_query_warp(DevIndex ix, const uint16_t* __restrict__ queries, int count, int k, int mode,
+    k_query_warp(const __grid_constant__ DevIndex ix, const uint16_t* __restrict__ queries, int count, int k, int mode,
                  int stride, u32* __restrict__ out_ids, uint16_t* __restrict__ out_lcps,
                  int* __restrict__ out_hits, uint16_t* __restrict__ out_md,
                  u64* __restrict__ out_aux, int* __restrict__ err) {

@@ -430,3 +430,56 @@ def test_wide_keys_at_scale(gpu, oracle_lib):
     oid, olcp, oh = oracle_lib.oracle_top_k_batch(ds.items, qs[250:262], 10, nthreads=8)
     for j, i in enumerate(range(250, 262)):
         assert b.pairs(i) == list(zip(oid[j, :oh[j]].tolist(), olcp[j, :oh[j]].tolist()))
+
+
+def _long_run_cases():
+    """Corpora whose queries have an R(d*) far wider than the loaded region."""
+    rng = np.random.default_rng(77)
+    # d* = 0 for most queries: the first symbol occurs ~4.6 times per 300K items
+    ds = lg.generate_dataset(300_000, 8, 65536, seed=71)
+    yield "s65536", ds, np.vstack([lg.generate_queries(ds, 96, seed=72),
+                                   rng.integers(0, 65536, (96, 8)).astype(np.uint16)])
+    # W == 1: R(1) holds ~1200 items, R(2) ~5
+    ds = lg.generate_dataset(300_000, 8, 256, seed=73)
+    yield "s256", ds, np.vstack([lg.generate_queries(ds, 96, seed=74),
+                                 rng.integers(0, 256, (96, 8)).astype(np.uint16)])
+    # half the corpus shares the prefix 0^6 with symbol 6 in {0,1,2}; queries
+    # 0^6 3 ... sit in a 150K-item R(6) whose R(7) is (nearly) empty
+    items = rng.integers(0, 4, (300_000, 16)).astype(np.uint16)
+    items[:150_000, :6] = 0
+    items[:150_000, 6] = rng.integers(0, 3, 150_000)
+    ds = lg.Dataset.from_rows(items, 4)
+    qs = rng.integers(0, 4, (128, 16)).astype(np.uint16)
+    qs[:96, :6] = 0
+    qs[:96, 6] = 3
+    yield "skew", ds, qs
+
+
+@pytest.mark.parametrize("wide", [False, True])
+def test_long_runs_vs_oracle(gpu, oracle_lib, wide, monkeypatch):
+    """R(d*) spanning up to the whole corpus: the run-edge search + id sketch
+    must give exactly the oracle's answers (complete, strict and TAL)."""
+    if wide:
+        monkeypatch.setenv("LCP_FORCE_WIDE_COMPOSITE", "1")
+    for name, ds, qs in _long_run_cases():
+        idx = lg.build(ds)
+        ot = oracle_lib.OracleTrie(ds.items, ds.alphabet.size)
+        for k in (1, 10, 16, 17, 32):
+            for mode in ("complete", "strict"):
+                b = idx.query_batch(qs, k, mode)
+                ids, lcps, hits, md, sym, nodes = ot.query_batch(qs, k, mode)
+                for i in range(len(qs)):
+                    exp = list(zip(ids[i, :hits[i]].tolist(), lcps[i, :hits[i]].tolist()))
+                    assert b.pairs(i) == exp, (name, k, mode, i)
+                    assert int(b.matched_depth[i]) == md[i]
+                w = idx.new_work_report()
+                idx.query_batch(qs, k, mode, work=w)
+                assert w.symbols_compared == int(sym.sum()) and w.nodes_visited == int(nodes.sum())
+        eng = lg.build_tal(ds, ds.alphabet.size)
+        ote = oracle_lib.OracleTal(ds.items, ds.alphabet.size, eng.bucket_depth)
+        for k in (1, 10, 32):
+            b = eng.query_batch(qs, k)
+            ids, lcps, hits, items_, sym = ote.query_batch(qs, k)
+            for i in range(len(qs)):
+                assert b.pairs(i) == list(zip(ids[i, :hits[i]].tolist(), lcps[i, :hits[i]].tolist())), (name, k, i)
+            assert np.array_equal(b.aux[:, 1].astype(np.int64), sym)
