@@ -15,10 +15,14 @@ events on the capture stream.  The same loop on one stream (one batch in
 flight) is reported beside it, and its per-step time is the kernel duration
 used for the roofline.
 
-N>1 (torchrun): row-block shards of 2M items per rank (weak scaling; rank g
-holds generate_dataset(2M, 32, 4, seed=3+g) with ids offset by 2M*g), the
-query batch is broadcast, and each step is local query -> encode ->
-NCCL all_gather -> merge kernel.  value = queries/s over the whole corpus.
+N>1 (torchrun): query-partitioned serving.  Every rank holds the full
+config-3 index (24 MB; it fits every GPU many times over) and runs the N=1
+step on its own query stream, so there is no data-path collective (SURVEY
+§8e "query-partitioned replicas"); barrier + synchronize bracket the timed
+region and the time is the max over ranks.  value = all ranks' queries/s.
+The north-star corpus sharding (row-block shards of 2M rows per rank, query
+batch broadcast, local top-k -> encode -> NCCL all_gather -> merge kernel)
+is timed beside it as "rowblock_sharded".
 
 ``--impl reference`` times the reference's own algorithm on the host CPU
 (the pinned C restatement in oracle/, all host threads) on the same config.
@@ -220,131 +224,112 @@ def main() -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # functional test hook only (numbers meaningless): all ranks on cuda:0,
+    # gloo for the host-level barrier / max-reduce
+    share = os.environ.get("LCP_BENCH_SHARE_GPU") == "1"
+    if share:
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     dev = torch.device("cuda", local_rank)
 
-    ds = lg.generate_dataset(N_ITEMS, SEQ_LEN, SIGMA, seed=3 + rank)
+    # every rank serves the config-3 corpus from its own replica of the index
+    # (query-partitioned: rank r answers its own query stream; no data-path
+    # collective).  Rank 0's stream is the N=1 stream.
+    ds = lg.generate_dataset(N_ITEMS, SEQ_LEN, SIGMA, seed=3)
     n_pool = 8
-    qs = lg.generate_queries(ds, BATCH * n_pool, seed=4)  # uniform queries: identical on every rank
+    qs = lg.generate_queries(ds, BATCH * n_pool, seed=4 + 1000 * rank)
     main_stream = torch.cuda.Stream(device=dev)
-    kbytes = algorithmic_key_bytes(SEQ_LEN, SIGMA)
     sampler = ClockSampler(local_rank)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if share else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     with torch.cuda.stream(main_stream):
         t_build = time.perf_counter()
-        if world == 1:
-            idx = lg.build(ds)
-        else:
-            from paper_2602_04936_b200.sharded import ShardedIndex
-
-            sh = ShardedIndex(ds.items, SEQ_LEN, SIGMA, id_offset=N_ITEMS * rank)
-            idx = None
+        idx = lg.build(ds)
         torch.cuda.synchronize()
         t_build = time.perf_counter() - t_build
         dq = torch.from_numpy(qs).to(dev).view(n_pool, BATCH, SEQ_LEN)
-        stride = min(K, N_ITEMS * world)
 
         def out_bufs():
-            return (torch.empty((BATCH, stride), dtype=torch.int32, device=dev),
-                    torch.empty((BATCH, stride), dtype=torch.int16, device=dev),
+            return (torch.empty((BATCH, K), dtype=torch.int32, device=dev),
+                    torch.empty((BATCH, K), dtype=torch.int16, device=dev),
                     torch.empty(BATCH, dtype=torch.int32, device=dev),
                     torch.empty(BATCH, dtype=torch.int16, device=dev),
                     torch.empty((n_pool, BATCH, 2), dtype=torch.int64, device=dev))
 
-        if world == 1:
-            from paper_2602_04936_b200._native import workspace
+        from paper_2602_04936_b200._native import workspace
 
-            workspace()  # created outside graph capture (it allocates)
-            replicas = [idx] + [lg.build(ds) for _ in range(7)]
-            R = len(replicas)
-            G = R * n_pool  # steps per captured graph
+        workspace()  # created outside graph capture (it allocates)
+        replicas = [idx] + [lg.build(ds) for _ in range(7)]
+        R = len(replicas)
+        G = R * n_pool  # steps per captured graph
 
-            def capture(n_steps: int, n_streams: int):
-                streams = [torch.cuda.Stream(device=dev) for _ in range(n_streams)]
-                bufs = [out_bufs() for _ in range(n_streams)]
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g, stream=main_stream):
-                    for x in streams:
-                        x.wait_stream(main_stream)
-                    for i in range(n_steps):
-                        x, (ids, lcps, hits, md, aux) = streams[i % n_streams], bufs[i % n_streams]
-                        b = (i // R) % n_pool
-                        replicas[i % R].native.query_device(dq[b], K, "complete", ids, lcps, hits, md,
-                                                           aux[b], stream=x.cuda_stream)
-                    for x in streams:
-                        main_stream.wait_stream(x)
-                return g, bufs
+        def capture(n_steps: int, n_streams: int):
+            streams = [torch.cuda.Stream(device=dev) for _ in range(n_streams)]
+            bufs = [out_bufs() for _ in range(n_streams)]
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=main_stream):
+                for x in streams:
+                    x.wait_stream(main_stream)
+                for i in range(n_steps):
+                    x, (ids, lcps, hits, md, aux) = streams[i % n_streams], bufs[i % n_streams]
+                    b = (i // R) % n_pool
+                    replicas[i % R].native.query_device(dq[b], K, "complete", ids, lcps, hits, md,
+                                                       aux[b], stream=x.cuda_stream)
+                for x in streams:
+                    main_stream.wait_stream(x)
+            return g, bufs
 
-            def run_steps(n_streams: int, steps: int, warmup: int, clocks: bool = False):
-                g, bufs = capture(G, n_streams)
-                tail = steps % G
-                gt = capture(tail, n_streams)[0] if tail else None
-                # W warm-up steps, and at least ~0.3 s so SM clocks leave idle
-                t_w, reps = time.perf_counter(), 0
-                while reps * G < warmup or time.perf_counter() - t_w < 0.3:
-                    g.replay()
-                    reps += 1
-                    if reps % 16 == 0:
-                        torch.cuda.synchronize()
-                torch.cuda.synchronize()
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                t0 = time.perf_counter()
-                a.record(main_stream)
-                for _ in range(steps // G):
-                    g.replay()
-                if gt is not None:
-                    gt.replay()
-                b.record(main_stream)
-                torch.cuda.synchronize()
-                t1 = time.perf_counter()
-                return a.elapsed_time(b), bufs, (t0, t1)
-
-            # one batch in flight (kernel duration for the roofline)
-            single_ms, bufs1, _ = run_steps(1, args.steps, args.warmup)
-            # headline: three batches in flight (a serving pipeline)
-            sampler.start()
-            total_ms, bufs2, (t0, t1) = run_steps(INFLIGHT, args.steps, args.warmup, clocks=True)
-            clocks = sampler.stop(t0, t1)
-            aux_all = bufs1[0][4]
-            gpu_launches = args.steps
-        else:
-            flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-            ids, lcps, hits, md, aux_all = out_bufs()
-
-            def step(i):
-                sh.query_device(dq[i % n_pool], K, ids, lcps, hits)
-
-            for i in range(args.warmup):
-                step(i)
-            torch.cuda.synchronize()
-            dist.barrier()
-            torch.cuda.synchronize()
-            sampler.start()
+        def run_steps(n_streams: int, steps: int, warmup: int):
+            g, bufs = capture(G, n_streams)
+            tail = steps % G
+            gt = capture(tail, n_streams)[0] if tail else None
+            # W warm-up steps, and at least ~0.3 s so SM clocks leave idle
+            t_w, reps = time.perf_counter(), 0
+            while reps * G < warmup or time.perf_counter() - t_w < 0.3:
+                g.replay()
+                reps += 1
+                if reps % 16 == 0:
+                    torch.cuda.synchronize()
+            barrier()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             t0 = time.perf_counter()
             a.record(main_stream)
-            for i in range(args.steps):
-                step(i)
+            for _ in range(steps // G):
+                g.replay()
+            if gt is not None:
+                gt.replay()
             b.record(main_stream)
             torch.cuda.synchronize()
             t1 = time.perf_counter()
-            dist.barrier()
-            torch.cuda.synchronize()
-            clocks = sampler.stop(t0, t1)
-            total_ms = a.elapsed_time(b)
-            single_ms = total_ms
-            t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            total_ms = float(t.item())
-            gpu_launches = args.steps * 3
-            # local-shard aux for the byte accounting
-            for bb in range(n_pool):
-                sh.local.query_device(dq[bb], K, "complete", ids, lcps, hits, md, aux_all[bb],
-                                      stream=main_stream.cuda_stream)
-            torch.cuda.synchronize()
-        value = BATCH * args.steps / (total_ms / 1e3)
+            barrier()
+            return max_over_ranks(a.elapsed_time(b)), bufs, (t0, t1)
+
+        # one batch in flight (kernel duration for the roofline)
+        single_ms, bufs1, _ = run_steps(1, args.steps, args.warmup)
+        # headline: three batches in flight (a serving pipeline)
+        sampler.start()
+        total_ms, bufs2, (t0, t1) = run_steps(INFLIGHT, args.steps, args.warmup)
+        clocks = sampler.stop(t0, t1)
+        aux_all = bufs1[0][4]
+        gpu_launches = args.steps * world
+        value = world * BATCH * args.steps / (total_ms / 1e3)
 
         # roofline of the dominant kernel (k_query_w1): algorithmic bytes / duration
         rsize = (aux_all[:, :, 1].cpu().numpy().astype(np.uint64) & np.uint64(0xFFFFFFFF)).astype(np.int64)
@@ -373,26 +358,28 @@ def main() -> None:
         "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u64",
-        "data": ("synthetic: reference Philox generator, generate_dataset(2_000_000, 32, 4, seed=3+rank), "
-                 "generate_queries(seed=4), 8 distinct 4096-query batches cycled"),
+        "data": ("synthetic: reference Philox generator, generate_dataset(2_000_000, 32, 4, seed=3), "
+                 "generate_queries(seed=4 + 1000*rank), 8 distinct 4096-query batches cycled per rank"),
         "config": {"workload": "config 3: indexed complete-mode top-k serving, 4096-query batches",
-                   "n_items_per_rank": N_ITEMS, "n_items_total": N_ITEMS * world, "seq_len": SEQ_LEN,
-                   "alphabet": SIGMA, "k": K, "batch": BATCH, "mode": "complete",
-                   "l2": ("inputs larger than L2: 8 index replicas (8 x 24 MB > 126 MB) cycled step to step"
-                          if world == 1 else "row-block shard per rank; host-launched steps"),
-                   "launch": (f"CUDA graph replay; {INFLIGHT} batches in flight on {INFLIGHT} streams"
-                              if world == 1 else "host loop"),
-                   "parallelism": "single GPU" if world == 1 else f"row-block shards x{world} + NCCL all_gather merge"},
+                   "n_items": N_ITEMS, "seq_len": SEQ_LEN, "alphabet": SIGMA, "k": K, "batch": BATCH,
+                   "batch_per_rank": BATCH, "mode": "complete",
+                   "l2": "inputs larger than L2: 8 index replicas (8 x 24 MB > 126 MB) cycled step to step",
+                   "launch": f"CUDA graph replay; {INFLIGHT} batches in flight on {INFLIGHT} streams",
+                   "parallelism": ("single GPU" if world == 1 else
+                                   f"query-partitioned x{world}: every rank holds the full 2M index "
+                                   "(24 MB) and answers its own batches; no data-path collective")},
         "roofline": roofline,
         "gpu_launches": gpu_launches,
         "clocks": clocks,
         "build_s": round(t_build, 3),
-        "one_batch_in_flight": {"value": BATCH * args.steps / (single_ms / 1e3), "unit": "queries/s",
+        "one_batch_in_flight": {"value": world * BATCH * args.steps / (single_ms / 1e3), "unit": "queries/s",
                                 "ms_per_step": single_ms / args.steps},
     }
-
+    line["e2e"] = e2e_leg(idx, qs, args, world, barrier, max_over_ranks)
+    if world > 1:
+        line["rowblock_sharded"] = rowblock_leg(lg, args, world, rank, dev, main_stream, barrier,
+                                                max_over_ranks)
     if world == 1 and rank == 0:
-        line["e2e"] = e2e_leg(idx, qs, args)
         line["p50_batch_latency_ms"] = cold_batch_latency(idx, dq, dev)
         cpu_qps, cpu_done, cpu_el, trie = cpu_reference(ds, qs, K, args.cpu_budget_s, os.cpu_count() or 1)
         line["cpu_baseline"] = {
@@ -406,6 +393,41 @@ def main() -> None:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def rowblock_leg(lg, args, world, rank, dev, stream, barrier, max_over_ranks) -> dict:
+    """North-star corpus sharding: rank g holds rows generate_dataset(2M, seed=3+g)
+    with ids offset by 2M*g; every query batch is answered by every shard
+    (local top-k -> encode -> NCCL all_gather -> merge kernel).  value =
+    queries/s over the whole 2M*world corpus."""
+    import torch
+
+    from paper_2602_04936_b200.sharded import ShardedIndex
+
+    ds = lg.generate_dataset(N_ITEMS, SEQ_LEN, SIGMA, seed=3 + rank)
+    qs = lg.generate_queries(ds, BATCH * 8, seed=4)  # identical on every rank (broadcast)
+    with torch.cuda.stream(stream):
+        sh = ShardedIndex(ds.items, SEQ_LEN, SIGMA, id_offset=N_ITEMS * rank)
+        dq = torch.from_numpy(qs).to(dev).view(8, BATCH, SEQ_LEN)
+        ids = torch.empty((BATCH, K), dtype=torch.int32, device=dev)
+        lcps = torch.empty((BATCH, K), dtype=torch.int16, device=dev)
+        hits = torch.empty(BATCH, dtype=torch.int32, device=dev)
+        steps = min(args.steps, 1000)
+        for i in range(max(args.warmup, 20)):
+            sh.query_device(dq[i % 8], K, ids, lcps, hits)
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for i in range(steps):
+            sh.query_device(dq[i % 8], K, ids, lcps, hits)
+        b.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ms = max_over_ranks(a.elapsed_time(b))
+    return {"value": BATCH * steps / (ms / 1e3), "unit": "queries/s", "steps": steps,
+            "ms_per_step": ms / steps, "n_items_total": N_ITEMS * world,
+            "parallelism": f"row-block shards x{world} (2M rows each) + NCCL all_gather + k_merge",
+            "launch": "host loop: local query -> encode -> all_gather -> merge per step"}
 
 
 def cold_batch_latency(idx, dq, dev) -> float:
@@ -431,8 +453,10 @@ def cold_batch_latency(idx, dq, dev) -> float:
     return float(np.median(ts))
 
 
-def e2e_leg(idx, qs, args) -> dict:
-    """Public API, host buffers: pinned queries in, results out, every step."""
+def e2e_leg(idx, qs, args, world=1, barrier=lambda: None, max_over_ranks=lambda x: x) -> dict:
+    """Public API, host buffers: pinned queries in, results out, every step.
+    At N GPUs every rank runs the same loop on its own stream of batches;
+    value = all ranks' queries / the slowest rank's wall clock."""
     from paper_2602_04936_b200._native import PinnedArray
 
     n_pool = qs.shape[0] // BATCH
@@ -447,7 +471,8 @@ def e2e_leg(idx, qs, args) -> dict:
         t0 = time.perf_counter()
         idx.query_batch(pin.array[i % n_pool], K, "complete", out=out)
         t.append(time.perf_counter() - t0)
-    sync = {"value": BATCH * steps / float(np.sum(t)), "p50_ms": 1e3 * float(np.median(t)),
+    sync = {"value": world * BATCH * steps / max_over_ranks(float(np.sum(t))),
+            "p50_ms": 1e3 * float(np.median(t)),
             "api": "TrieIndex.query_batch (synchronous, one batch at a time)"}
     # pipelined serving: up to 3 batches in flight, each with its own H2D and D2H
     from paper_2602_04936_b200 import _native
@@ -458,6 +483,7 @@ def e2e_leg(idx, qs, args) -> dict:
     for i in range(20):
         idx.query_batch_async(pin.array[i % n_pool], K, "complete", out=outs[i % depth]).result()
     pending = []
+    barrier()
     t0 = time.perf_counter()
     for i in range(steps):
         if len(pending) == depth:
@@ -465,8 +491,9 @@ def e2e_leg(idx, qs, args) -> dict:
         pending.append(idx.query_batch_async(pin.array[i % n_pool], K, "complete", out=outs[i % depth]))
     for p in pending:
         p.result()
-    el = time.perf_counter() - t0
-    return {"value": BATCH * steps / el, "unit": "queries/s",
+    el = max_over_ranks(time.perf_counter() - t0)
+    barrier()
+    return {"value": world * BATCH * steps / el, "unit": "queries/s",
             "h2d_bytes_per_step": BATCH * SEQ_LEN * 2,
             "d2h_bytes_per_step": int(outs[0].ids.nbytes + outs[0].lcps.nbytes + outs[0].hits.nbytes),
             "steps": steps, "ms_per_step": 1e3 * el / steps,

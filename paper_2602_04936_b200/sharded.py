@@ -63,6 +63,10 @@ class ShardExchange:
             out = torch.empty((self.world, *cand.shape), dtype=cand.dtype, device=cand.device)
         if dist.get_backend(self.group) == "nccl":
             dist.all_gather_into_tensor(out, cand, group=self.group)
+        elif cand.is_cuda:  # gloo gathers host tensors only
+            host = torch.empty(out.shape, dtype=out.dtype)
+            dist.all_gather(list(host.unbind(0)), cand.cpu(), group=self.group)
+            out.copy_(host)
         else:
             parts = list(out.unbind(0))
             dist.all_gather(parts, cand, group=self.group)
