@@ -1007,11 +1007,12 @@ __global__ void k_fill_empty(int count, int md, int* hits, uint16_t* out_md, u64
 
 // Reserve enough shared memory that two query CTAs (two batches in flight)
 // fit on one SM; the default carve-out for a 4 KB-smem kernel admits one.
-template <typename K>
-static void prefer_smem_carveout(K kernel) {
+// preferred L1 / shared split, set once per kernel (the static is per kernel)
+template <auto Kernel>
+static void prefer_carveout(int pct) {
   static bool done = false;
   if (!done) {
-    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 25);
+    cudaFuncSetAttribute(Kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
     cudaGetLastError();
     done = true;
   }
@@ -1020,22 +1021,29 @@ static void prefer_smem_carveout(K kernel) {
 template <typename C, int T>
 static void launch_w1(const DevIndex& dv, int mode, unsigned grid, unsigned block, size_t smem,
                       cudaStream_t st, const uint16_t* q, int count, int k, int stride, u32* ids,
-                      uint16_t* lcps, int* hits, uint16_t* md, u64* aux, int* err) {
-  prefer_smem_carveout(k_query_w1<C, T, 0>);
-  prefer_smem_carveout(k_query_w1<C, T, 1>);
-  prefer_smem_carveout(k_query_w1<C, T, 2>);
-  if (mode == LCP_MODE_STRICT)
-    k_query_w1<C, T, 0><<<grid, block, smem, st>>>(dv, q, count, k, stride, ids, lcps, hits, md, aux, err);
-  else if (mode == LCP_MODE_COMPLETE)
-    k_query_w1<C, T, 1><<<grid, block, smem, st>>>(dv, q, count, k, stride, ids, lcps, hits, md, aux, err);
-  else
-    k_query_w1<C, T, 2><<<grid, block, smem, st>>>(dv, q, count, k, stride, ids, lcps, hits, md, aux, err);
+                      uint16_t* lcps, int* hits, uint16_t* md, u64* aux, int* err,
+                      lcp_workspace* ws) {
+  // strict / complete keep 25 % shared memory (two 1024-thread batches per SM);
+  // TAL wants the largest L1 for the grouped bucket sweep
+  prefer_carveout<k_query_w1<C, T, 0>>(25);
+  prefer_carveout<k_query_w1<C, T, 1>>(25);
+  prefer_carveout<k_query_w1<C, T, 2>>(0);
+  if (mode == LCP_MODE_STRICT) {
+    k_query_w1<C, T, 0><<<grid, block, smem, st>>>(dv, q, count, k, stride, ids, lcps, hits, md, aux,
+                                                  err);
+  } else if (mode == LCP_MODE_COMPLETE) {
+    k_query_w1<C, T, 1><<<grid, block, smem, st>>>(dv, q, count, k, stride, ids, lcps, hits, md, aux,
+                                                  err);
+  } else {
+    k_query_w1<C, T, 2><<<grid, block, smem, st>>>(dv, q, count, k, stride, ids, lcps, hits, md, aux,
+                                                  err);
+  }
 }
 
 template <int WMAX>
 static void launch_fast(const lcp_index* ix, const uint16_t* q, int count, int k, int mode,
                         int stride, u32* ids, uint16_t* lcps, int* hits, uint16_t* md, u64* aux,
-                        int* err, cudaStream_t st) {
+                        int* err, cudaStream_t st, lcp_workspace* ws) {
   const DevIndex& dv = ix->dv;
   if (mode == LCP_MODE_TAL && WMAX > 1) {
     unsigned grid = (unsigned)std::min<long long>(count, 8ll * num_sms());
@@ -1054,11 +1062,11 @@ static void launch_fast(const lcp_index* ix, const uint16_t* q, int count, int k
       // leaf region: 64 keys cover the +-need window for need <= 16, 96 keys for <= 32
       const long long need = mode == LCP_MODE_COMPLETE ? std::min<long long>(k, dv.n) : k;
       if (dv.idbits < 32) {
-        if (need <= 16) launch_w1<u32, 2>(dv, mode, grid, block, smem, st, q, count, k, stride, ids, lcps, hits, md, aux, err);
-        else launch_w1<u32, 3>(dv, mode, grid, block, smem, st, q, count, k, stride, ids, lcps, hits, md, aux, err);
+        if (need <= 16) launch_w1<u32, 2>(dv, mode, grid, block, smem, st, q, count, k, stride, ids, lcps, hits, md, aux, err, ws);
+        else launch_w1<u32, 3>(dv, mode, grid, block, smem, st, q, count, k, stride, ids, lcps, hits, md, aux, err, ws);
       } else {
-        if (need <= 16) launch_w1<u64, 2>(dv, mode, grid, block, smem, st, q, count, k, stride, ids, lcps, hits, md, aux, err);
-        else launch_w1<u64, 3>(dv, mode, grid, block, smem, st, q, count, k, stride, ids, lcps, hits, md, aux, err);
+        if (need <= 16) launch_w1<u64, 2>(dv, mode, grid, block, smem, st, q, count, k, stride, ids, lcps, hits, md, aux, err, ws);
+        else launch_w1<u64, 3>(dv, mode, grid, block, smem, st, q, count, k, stride, ids, lcps, hits, md, aux, err, ws);
       }
     }
     else
@@ -1105,10 +1113,10 @@ int lcp_query(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries, i
     ax = ws->aux.as<u64>();
   }
   if (dv.W <= 8 && k <= FAST_KMAX) {
-    if (dv.W == 1) launch_fast<1>(ix, queries, count, k, mode, out_stride, ids, lcps, hits, md, ax, ws->d_err, st);
-    else if (dv.W == 2) launch_fast<2>(ix, queries, count, k, mode, out_stride, ids, lcps, hits, md, ax, ws->d_err, st);
-    else if (dv.W <= 4) launch_fast<4>(ix, queries, count, k, mode, out_stride, ids, lcps, hits, md, ax, ws->d_err, st);
-    else launch_fast<8>(ix, queries, count, k, mode, out_stride, ids, lcps, hits, md, ax, ws->d_err, st);
+    if (dv.W == 1) launch_fast<1>(ix, queries, count, k, mode, out_stride, ids, lcps, hits, md, ax, ws->d_err, st, ws);
+    else if (dv.W == 2) launch_fast<2>(ix, queries, count, k, mode, out_stride, ids, lcps, hits, md, ax, ws->d_err, st, ws);
+    else if (dv.W <= 4) launch_fast<4>(ix, queries, count, k, mode, out_stride, ids, lcps, hits, md, ax, ws->d_err, st, ws);
+    else launch_fast<8>(ix, queries, count, k, mode, out_stride, ids, lcps, hits, md, ax, ws->d_err, st, ws);
     LCP_CK_LAUNCH();
     return LCP_OK;
   }

@@ -361,8 +361,10 @@ __device__ __forceinline__ int level_count(const u64* __restrict__ tab, int cnt,
   return (int)__reduce_add_sync(LCP_FULL_MASK, lt);
 }
 
+// strict / complete: <= 32 regs, so two batches share an SM; TAL: 64 regs
+// for the unrolled bucket sweep
 template <typename C, int T, int MODE>
-__global__ void __launch_bounds__(QW_MAX_THREADS, 2)  // <= 32 regs: two batches share an SM
+__global__ void __launch_bounds__(QW_MAX_THREADS, MODE == 2 ? 1 : 2)
     k_query_w1(const __grid_constant__ DevIndex ix, const uint16_t* __restrict__ queries, int count, int k,
                int stride, u32* __restrict__ out_ids, uint16_t* __restrict__ out_lcps,
                int* __restrict__ out_hits, uint16_t* __restrict__ out_md,
@@ -476,20 +478,38 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, 2)  // <= 32 regs: two batches
     if constexpr (MODE == 2) {
       // symbols_compared = sum over the bucket of min(lcp + 1, L)
       // (tal.py:173-177): every bucket item's lcp, coalesced 16-byte loads
+      // W == 1: bits past symbol L are zero in keys and query, so x = key ^ q
+      // is nonzero exactly when lcp < L, and min(lcp + 1, L) =
+      // 1 + min(clz64(x) >> lb, L - 1) with no branch (clz64(0) = 64).
+      // Aligned interior: 16-byte pairs, 8 keys per lane in flight; the odd
+      // keys at either end are added by lane 0.
+      const int lm1 = L - 1;
       unsigned long long sym = 0;
-      for (int i = blo + 2 * lane; i < bhi; i += 64) {
-        u64 k0, k1 = q;
-        if (i + 1 < bhi && !(i & 1)) {
-          const ulonglong2 kv = __ldg(reinterpret_cast<const ulonglong2*>(keys + i));
-          k0 = kv.x;
-          k1 = kv.y;
-        } else {
-          k0 = __ldg(keys + i);
-          if (i + 1 < bhi) k1 = __ldg(keys + i + 1);
+      const int a0 = (blo + 1) & ~1, e0 = bhi & ~1;
+      constexpr int TAL_UNROLL = 8;
+      int base = a0 + 2 * lane;
+      for (; base + 64 * (TAL_UNROLL - 1) < e0; base += 64 * TAL_UNROLL) {
+        ulonglong2 kv[TAL_UNROLL];
+#pragma unroll
+        for (int u = 0; u < TAL_UNROLL; ++u)
+          kv[u] = __ldg(reinterpret_cast<const ulonglong2*>(keys + base + 64 * u));
+        u32 part = 0;
+#pragma unroll
+        for (int u = 0; u < TAL_UNROLL; ++u) {
+          part += (u32)min(__clzll((long long)(kv[u].x ^ q)) >> lb, lm1);
+          part += (u32)min(__clzll((long long)(kv[u].y ^ q)) >> lb, lm1);
         }
-        const u64 x0 = k0 ^ q, x1 = k1 ^ q;
-        sym += (unsigned)min((x0 ? (__clzll((long long)x0) >> lb) : L) + 1, L);
-        if (i + 1 < bhi) sym += (unsigned)min((x1 ? (__clzll((long long)x1) >> lb) : L) + 1, L);
+        sym += part;
+      }
+      for (; base < e0; base += 64) {
+        const ulonglong2 kv = __ldg(reinterpret_cast<const ulonglong2*>(keys + base));
+        sym += (u32)min(__clzll((long long)(kv.x ^ q)) >> lb, lm1);
+        sym += (u32)min(__clzll((long long)(kv.y ^ q)) >> lb, lm1);
+      }
+      if (lane == 0) {
+        if (blo & 1) sym += (u32)min(__clzll((long long)(__ldg(keys + blo) ^ q)) >> lb, lm1);
+        if ((bhi & 1) && e0 >= a0) sym += (u32)min(__clzll((long long)(__ldg(keys + e0) ^ q)) >> lb, lm1);
+        sym += (unsigned long long)(bhi - blo);  // the "+1" of every item
       }
 #pragma unroll
       for (int o = 16; o; o >>= 1) sym += __shfl_xor_sync(LCP_FULL_MASK, sym, o);
