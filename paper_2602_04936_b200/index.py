@@ -336,3 +336,50 @@ def memoized_query(index: TrieIndex, q, k: int, mode: str = "strict",
             work.queries += 1
         return hit
     return cache.insert(key, index.query(query, k, mode, work=work))
+
+
+def memoized_query_batch(index: TrieIndex, queries, k: int, mode: str = "strict",
+                         cache: QueryCache | None = None,
+                         work: WorkReport | None = None) -> list[QueryResult]:
+    """memoized_query over a batch with one GPU launch for the misses.
+
+    Same results and counters as calling memoized_query on each row in order
+    (trie.py:464-488): the first occurrence of a key that is not cached is a
+    miss (answered by one query_batch over all misses); later occurrences in
+    the batch and cached keys are hits (cache_hits += 1, no scan work)."""
+    if cache is None:
+        raise InvalidInputError("memoized_query requires a cache")
+    if mode not in ("strict", "complete"):
+        raise InvalidInputError(f"mode must be 'strict' or 'complete', got {mode!r}")
+    if k < 1:
+        raise InvalidInputError(f"k must be >= 1, got {k}")
+    qs = validate_query_batch(queries, index.length, index.sigma)
+    keys = [(row.tobytes(), int(k), mode) for row in qs]
+    out: list = [None] * len(keys)
+    first: dict = {}
+    miss_rows: list[int] = []
+    hits = 0
+    for i, key in enumerate(keys):
+        if key in first:  # repeat inside this batch: served by the first occurrence
+            hits += 1
+            with cache._lock:
+                cache.hits += 1
+            continue
+        res = cache.lookup(key)
+        if res is not None:
+            out[i] = res
+            hits += 1
+        else:
+            first[key] = i
+            miss_rows.append(i)
+    if miss_rows:
+        b = index.query_batch(qs[miss_rows], k, mode, work=work)
+        for j, i in enumerate(miss_rows):
+            out[i] = cache.insert(keys[i], b.result(j))
+    for i, key in enumerate(keys):
+        if out[i] is None:
+            out[i] = out[first[key]]
+    if work is not None:
+        work.cache_hits += hits
+        work.queries += hits
+    return out
