@@ -597,6 +597,16 @@ def extras(idx, ds, qs, stream, flush_buf) -> dict:
     out["indexed_sigma65536_qps"] = BATCH / (ms8 / 1e3)
     out["indexed_sigma65536_device_bytes"] = i8.nbytes
     del i8, d8
+    # config 3, clustered stress (datagen.py:42-52: skew 1.1, depth 8): long
+    # shared prefixes make R(d*) wide for many queries
+    dc = lg.generate_dataset(N_ITEMS, SEQ_LEN, SIGMA, seed=3, distribution="clustered")
+    ic = lg.build(dc)
+    for tag, pl in (("uniform", None), ("prefix16", 16)):
+        qc = torch.from_numpy(lg.generate_queries(dc, BATCH, seed=4, prefix_len=pl)).to(dev)
+        msc, _ = per_step_ms(lambda i: ic.native.query_device(qc, K, "complete", ids, lcps, hits,
+                                                             stream=st), 32, 20)
+        out[f"indexed_clustered_{tag}_qps"] = BATCH / (msc / 1e3)
+    del ic, dc
     # config 4: the N x N materialisation wall vs the index (PAPER.md:493-496,
     # reference bench.memory_wall: n*n*2 bytes of fp16 similarities)
     n4 = 500_000

@@ -483,3 +483,20 @@ def test_long_runs_vs_oracle(gpu, oracle_lib, wide, monkeypatch):
             for i in range(len(qs)):
                 assert b.pairs(i) == list(zip(ids[i, :hits[i]].tolist(), lcps[i, :hits[i]].tolist())), (name, k, i)
             assert np.array_equal(b.aux[:, 1].astype(np.int64), sym)
+
+
+def test_clustered_at_scale(gpu, oracle_lib):
+    """Config 3 shape with the clustered generator (long shared prefixes):
+    indexed complete mode == independent full scan on every query, == oracle
+    on a sample."""
+    ds = lg.generate_dataset(2_000_000, 32, 4, seed=3, distribution="clustered")
+    idx = lg.build(ds)
+    qs = np.vstack([lg.generate_queries(ds, 2048, seed=4), lg.generate_queries(ds, 2048, seed=5, prefix_len=16)])
+    for k in (10, 32):
+        b = idx.query_batch(qs, k, "complete")
+        f = idx.fullscan_batch(qs, k)
+        assert np.array_equal(b.hits, f.hits) and np.array_equal(b.ids, f.ids) and np.array_equal(b.lcps, f.lcps)
+    sample = np.r_[0:24, 2048:2072]
+    oid, olcp, oh = oracle_lib.oracle_top_k_batch(ds.items, qs[sample], 32, nthreads=8)
+    for j, i in enumerate(sample):
+        assert b.pairs(i) == list(zip(oid[j, :oh[j]].tolist(), olcp[j, :oh[j]].tolist()))
