@@ -379,6 +379,8 @@ def main() -> None:
     if world > 1:
         line["rowblock_sharded"] = rowblock_leg(lg, args, world, rank, dev, main_stream, barrier,
                                                 max_over_ranks)
+        line["range_sharded"] = range_leg(lg, args, world, rank, dev, main_stream, barrier,
+                                          max_over_ranks)
     if world == 1 and rank == 0:
         line["p50_batch_latency_ms"] = cold_batch_latency(idx, dq, dev)
         cpu_qps, cpu_done, cpu_el, trie = cpu_reference(ds, qs, K, args.cpu_budget_s, os.cpu_count() or 1)
@@ -428,6 +430,40 @@ def rowblock_leg(lg, args, world, rank, dev, stream, barrier, max_over_ranks) ->
             "ms_per_step": ms / steps, "n_items_total": N_ITEMS * world,
             "parallelism": f"row-block shards x{world} (2M rows each) + NCCL all_gather + k_merge",
             "launch": "host loop: local query -> encode -> all_gather -> merge per step"}
+
+
+def range_leg(lg, args, world, rank, dev, stream, barrier, max_over_ranks) -> dict:
+    """Lexicographic range shards (rangeshard.py): 2M rows per rank, re-split
+    by key range; a broadcast batch of world*4096 queries per step, each rank
+    answering the ~4096 it owns (+ consulted neighbours), consult flags by
+    all_reduce, candidates by all_gather, merge kernel.  value = queries/s."""
+    import torch
+
+    from paper_2602_04936_b200.rangeshard import RangeShardedIndex
+
+    ds = lg.generate_dataset(N_ITEMS, SEQ_LEN, SIGMA, seed=3 + rank)
+    qs = lg.generate_queries(ds, BATCH * world * 4, seed=4)  # identical on every rank (broadcast)
+    with torch.cuda.stream(stream):
+        sh = RangeShardedIndex(ds.items, SEQ_LEN, SIGMA, id_offset=N_ITEMS * rank)
+        dq = torch.from_numpy(qs).to(dev).view(4, BATCH * world, SEQ_LEN)
+        steps = min(args.steps, 200)
+        for i in range(max(args.warmup, 10)):
+            sh.query(dq[i % 4], K, "complete")
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for i in range(steps):
+            sh.query(dq[i % 4], K, "complete")
+        b.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ms = max_over_ranks(a.elapsed_time(b))
+    return {"value": BATCH * world * steps / (ms / 1e3), "unit": "queries/s", "steps": steps,
+            "ms_per_step": ms / steps, "n_items_total": N_ITEMS * world, "n_items_local": sh.n_local,
+            "batch_broadcast": BATCH * world,
+            "parallelism": f"lexicographic range shards x{world} + routed queries (consult rule) "
+                           "+ all_reduce + all_gather + k_merge",
+            "launch": "host loop (routing bookkeeping syncs the host each step)"}
 
 
 def cold_batch_latency(idx, dq, dev) -> float:

@@ -1,0 +1,295 @@
+"""Lexicographic range sharding with routed queries.
+
+The reference has no multi-device path.  Row-block sharding
+(sharded.py) answers every query on every shard; here each shard owns a
+contiguous range of the global sorted order, so a query is answered by the
+shard that owns its key range and, only when the answer may spill over a
+range boundary, by the neighbouring shards.
+
+Build (collective, once):
+  1. every rank samples its rows; the gathered samples are sorted and
+     world-1 splitter rows are taken at the quantiles (identical on all ranks);
+  2. rows go to the shard owning their range (route = number of splitters
+     <= row, lexicographically) with all_to_all, together with their global
+     ids; received rows arrive in global-id order (sources in rank order, each
+     in row order), so local ids rank exactly like global ids;
+  3. each rank indexes its range and publishes its first / last sorted row.
+
+Query step (the batch is broadcast, as in sharded.py):
+  1. owner(q) by the same route; a rank answers only the queries it owns;
+  2. t = the lcp of the owner's need-th hit (complete) or its d_max
+     (strict), -1 when the owner holds fewer than need items.  Another shard s
+     can contribute only items with lcp >= t, and the best lcp any item of s
+     reaches is max(lcp(q, first_s), lcp(q, last_s)) because q lies outside
+     s's range; such shards are "consulted" (flags combined by all_reduce MAX)
+     and answer the query locally too;
+  3. every rank encodes its answers as (L - lcp) << 32 | global id (UINT64_MAX
+     elsewhere), one all_gather, and the merge kernel keeps the top-take —
+     exact because (lcp desc, id asc) is a total order and every item that can
+     enter the global answer is in an answering shard's local top-k.
+
+Routing and the consult rule are tensor bookkeeping (they run on the device
+with NCCL, and on CPU tensors under gloo for the multi-process tests); the
+local top-k and the merge are the CUDA kernels.  Local engines are pluggable
+so the protocol is testable without a GPU.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .core import InvalidInputError
+
+U64_MAX_AS_I64 = -1  # UINT64_MAX bit pattern in an int64 tensor
+
+
+def lcp_rows(a, b, length: int):
+    """Per-row lcp of broadcastable integer row tensors [..., L]."""
+    import torch
+
+    neq = a != b
+    first = neq.to(torch.int8).argmax(dim=-1)
+    return torch.where(neq.any(dim=-1), first, torch.full_like(first, length))
+
+
+def route(rows, splitters, length: int, chunk: int = 1 << 16):
+    """Owner shard of each row: #splitters <= row (lexicographic)."""
+    import torch
+
+    out = torch.empty(rows.shape[0], dtype=torch.int64, device=rows.device)
+    if splitters.shape[0] == 0:
+        return out.zero_()
+    spl = splitters.to(torch.int32)
+    for s in range(0, rows.shape[0], chunk):
+        r = rows[s:s + chunk].to(torch.int32)
+        j = lcp_rows(r[:, None, :], spl[None, :, :], length)          # [m, S]
+        jc = j.clamp(max=length - 1)
+        rv = torch.gather(r, 1, jc)                                     # r[j] per splitter
+        sv = spl[torch.arange(spl.shape[0], device=r.device)[None, :], jc]
+        ge = (j == length) | (rv > sv)
+        out[s:s + chunk] = ge.sum(dim=1)
+    return out
+
+
+class _Collectives:
+    """NCCL collectives on device tensors; any other backend (gloo) through host."""
+
+    def __init__(self, group):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.nccl = dist.get_backend(group) == "nccl"
+
+    def _in(self, t):
+        return t if (self.nccl or t.device.type == "cpu") else t.cpu()
+
+    def all_gather(self, t):
+        import torch
+
+        x = self._in(t.contiguous())
+        out = torch.empty((self.world, *x.shape), dtype=x.dtype, device=x.device)
+        if self.nccl:
+            self.dist.all_gather_into_tensor(out, x, group=self.group)
+        else:
+            self.dist.all_gather(list(out.unbind(0)), x, group=self.group)
+        return out.to(t.device)
+
+    def all_reduce_max(self, t):
+        x = self._in(t.contiguous())
+        self.dist.all_reduce(x, op=self.dist.ReduceOp.MAX, group=self.group)
+        return x.to(t.device)
+
+    def all_reduce_sum(self, t):
+        x = self._in(t.contiguous())
+        self.dist.all_reduce(x, group=self.group)
+        return x.to(t.device)
+
+    def all_to_all(self, t, send_counts: list[int], recv_counts: list[int], row_elems: int):
+        import torch
+
+        x = self._in(t.contiguous())
+        out = torch.empty((sum(recv_counts) * row_elems,), dtype=x.dtype, device=x.device)
+        self.dist.all_to_all_single(out, x.reshape(-1), [c * row_elems for c in recv_counts],
+                                    [c * row_elems for c in send_counts], group=self.group)
+        return out.to(t.device)
+
+
+class GpuEngine:
+    """Local top-k on this rank's range: the CUDA index (NativeIndex)."""
+
+    def __init__(self, rows: np.ndarray, length: int, sigma: int):
+        from .engine import NativeIndex
+
+        self.length, self.n = int(length), int(rows.shape[0])
+        self.native = NativeIndex(rows, length, sigma) if self.n else None
+        self.device = "cuda"
+
+    def first_last_rows(self) -> np.ndarray:
+        if not self.n:
+            return np.zeros((2, self.length), dtype=np.int64)
+        rows = self.native.unpack_sorted_rows()
+        return np.stack([rows[0], rows[-1]]).astype(np.int64)
+
+    def query(self, queries, k: int, mode: str):
+        """queries: (m, L) uint16/int16 CUDA tensor -> (ids, lcps, hits, md) int64."""
+        import torch
+
+        m = int(queries.shape[0])
+        stride = self.native.stride_for(k)
+        ids = torch.empty((m, stride), dtype=torch.int32, device=queries.device)
+        lcps = torch.empty((m, stride), dtype=torch.int16, device=queries.device)
+        hits = torch.empty(m, dtype=torch.int32, device=queries.device)
+        md = torch.empty(m, dtype=torch.int16, device=queries.device)
+        self.native.query_device(queries.contiguous(), k, mode, ids, lcps, hits, md,
+                                 stream=torch.cuda.current_stream().cuda_stream)
+        return ids.long(), lcps.long() & 0xFFFF, hits.long(), md.long() & 0xFFFF
+
+    def merge(self, gathered, take: int, strict: bool):
+        """gathered: (world, count, k) int64 (u64 bits) CUDA tensor -> merged top-take."""
+        import torch
+
+        from . import _native
+
+        world, count, k = (int(s) for s in gathered.shape)
+        stride = max(1, take)
+        ids = torch.empty((count, stride), dtype=torch.int32, device=gathered.device)
+        lcps = torch.empty((count, stride), dtype=torch.int16, device=gathered.device)
+        hits = torch.empty(count, dtype=torch.int32, device=gathered.device)
+        _native.check(_native.load().lcp_merge_candidates(
+            gathered.contiguous().data_ptr(), world, count, k, take, self.length, 1 if strict else 0,
+            ids.data_ptr(), lcps.data_ptr(), hits.data_ptr(), torch.cuda.current_stream().cuda_stream))
+        return ids.long() & 0xFFFFFFFF, lcps.long() & 0xFFFF, hits.long()
+
+
+class RangeShardedIndex:
+    """One rank's lexicographic range of a corpus split over a process group.
+
+    ``items``: this rank's rows (uint16 (n, L)); their global ids are
+    ``id_offset + row``.  Collective: every rank of ``group`` constructs it."""
+
+    SAMPLES = 1024  # rows sampled per rank for the splitters
+
+    def __init__(self, items, length: int, sigma: int, id_offset: int, group=None,
+                 engine_factory=GpuEngine, device=None):
+        import torch
+
+        self.coll = _Collectives(group)
+        self.world, self.rank = self.coll.world, self.coll.rank
+        self.length, self.sigma = int(length), int(sigma)
+        items = np.ascontiguousarray(items, dtype=np.uint16).reshape(-1, self.length)
+        n_local = items.shape[0]
+        if device is None:
+            device = "cuda" if engine_factory is GpuEngine else "cpu"
+        self.device = torch.device(device)
+        L = self.length
+
+        # 1. splitters from the gathered samples
+        take = min(self.SAMPLES, n_local)
+        samp = np.zeros((self.SAMPLES, L), dtype=np.int64)
+        if take:
+            samp[:take] = items[np.linspace(0, n_local - 1, take).astype(np.int64)]
+        valid = np.zeros(self.SAMPLES, dtype=np.int64)
+        valid[:take] = 1
+        g_samp = self.coll.all_gather(torch.from_numpy(samp).to(self.device)).cpu().numpy()
+        g_valid = self.coll.all_gather(torch.from_numpy(valid).to(self.device)).cpu().numpy()
+        pool = g_samp.reshape(-1, L)[g_valid.reshape(-1) == 1]
+        if pool.shape[0]:
+            pool = pool[np.lexsort(pool.T[::-1])]
+            cut = [(i + 1) * pool.shape[0] // self.world for i in range(self.world - 1)]
+            spl = pool[np.minimum(cut, pool.shape[0] - 1)] if cut else np.zeros((0, L), np.int64)
+        else:
+            spl = np.zeros((self.world - 1, L), dtype=np.int64)
+        self.splitters = torch.from_numpy(np.ascontiguousarray(spl)).to(self.device)
+
+        # 2. rows (+ global ids) to the owner of their range, in global-id order
+        rows_t = torch.from_numpy(items.astype(np.int32)).to(self.device)
+        dest = route(rows_t, self.splitters, L) if n_local else torch.zeros(0, dtype=torch.int64,
+                                                                            device=self.device)
+        perm = torch.sort(dest, stable=True).indices
+        send_counts = torch.bincount(dest, minlength=self.world).to(torch.int64)
+        recv_counts = self.coll.all_gather(send_counts)[:, self.rank]
+        sc, rc = send_counts.cpu().tolist(), recv_counts.cpu().tolist()
+        gids = torch.arange(id_offset, id_offset + n_local, dtype=torch.int64, device=self.device)
+        my_rows = self.coll.all_to_all(rows_t[perm], sc, rc, L).reshape(-1, L)
+        self.gids = self.coll.all_to_all(gids[perm], sc, rc, 1)
+        local = my_rows.cpu().numpy().astype(np.uint16)
+        self.engine = engine_factory(local, L, sigma)
+        self.n_local = int(local.shape[0])
+
+        # 3. range boundaries of every shard, corpus size
+        fl = torch.from_numpy(self.engine.first_last_rows()).to(self.device)
+        g_fl = self.coll.all_gather(fl)
+        self.first, self.last = g_fl[:, 0, :].to(torch.int32), g_fl[:, 1, :].to(torch.int32)
+        self.nonempty = self.coll.all_gather(torch.tensor([self.n_local], device=self.device))[:, 0] > 0
+        self.n_total = int(self.coll.all_reduce_sum(torch.tensor([n_local], device=self.device)).item())
+
+    # ---------------------------------------------------------------- queries
+    def _encode(self, ids, lcps, hits, k: int):
+        """Local answers -> (m, k) int64 u64-bit composites, UINT64_MAX padded."""
+        import torch
+
+        m = ids.shape[0]
+        cand = torch.full((m, k), U64_MAX_AS_I64, dtype=torch.int64, device=ids.device)
+        w = min(k, ids.shape[1])
+        gid = self.gids[ids[:, :w].clamp(min=0, max=max(0, self.n_local - 1))]
+        comp = ((self.length - lcps[:, :w]) << 32) | gid
+        valid = torch.arange(w, device=ids.device)[None, :] < hits[:, None]
+        cand[:, :w] = torch.where(valid, comp, torch.full_like(comp, U64_MAX_AS_I64))
+        return cand
+
+    def _answer(self, queries, sel, k: int, mode: str, cand):
+        if sel.numel() == 0 or self.n_local == 0:
+            return None
+        ids, lcps, hits, md = self.engine.query(queries.index_select(0, sel), k, mode)
+        cand[sel] = self._encode(ids, lcps, hits, k)
+        return ids, lcps, hits, md
+
+    def query(self, queries, k: int, mode: str = "complete"):
+        """Global top-k for a broadcast (count, L) batch (same on every rank).
+
+        Returns (ids, lcps, hits): int64 tensors (count, max(1, take)), (count,)."""
+        import torch
+
+        if mode not in ("complete", "strict"):
+            raise InvalidInputError(f"sharded mode must be 'strict' or 'complete', got {mode!r}")
+        if k < 1:
+            raise InvalidInputError(f"k must be >= 1, got {k}")
+        take = max(0, min(int(k), self.n_total))
+        if take > 32:
+            raise InvalidInputError("sharded merge supports k <= 32")
+        q = queries.to(self.device)
+        count, L = int(q.shape[0]), self.length
+        kk = max(1, take)
+        cand = torch.full((count, kk), U64_MAX_AS_I64, dtype=torch.int64, device=self.device)
+        q32 = q.to(torch.int32) & 0xFFFF
+        owner = route(q32, self.splitters, L)
+        own = (owner == self.rank).nonzero().squeeze(1)
+        consult = torch.zeros((count, self.world), dtype=torch.int32, device=self.device)
+        if own.numel():
+            res = self._answer(q, own, kk, mode, cand)
+            if mode == "complete":
+                need = min(int(k), self.n_total)
+                if res is None or need == 0 or res[1].shape[1] < need:  # owner holds < need items
+                    t = torch.full((own.numel(),), -1, dtype=torch.int64, device=self.device)
+                else:
+                    _, lcps, hits, _ = res
+                    t = torch.where(hits >= need, lcps[:, need - 1], torch.full_like(hits, -1))
+            else:
+                if res is None:
+                    t = torch.full((own.numel(),), -1, dtype=torch.int64, device=self.device)
+                else:
+                    _, _, hits, md = res
+                    t = torch.where(hits > 0, md, torch.full_like(hits, -1))
+            qo = q32.index_select(0, own)[:, None, :]
+            best = torch.maximum(lcp_rows(qo, self.first[None], L), lcp_rows(qo, self.last[None], L))
+            c = (best >= t[:, None]) & self.nonempty[None, :]
+            c[:, self.rank] = False
+            consult[own] = c.to(torch.int32)
+        consult = self.coll.all_reduce_max(consult)
+        mine = (consult[:, self.rank] > 0).nonzero().squeeze(1)
+        self._answer(q, mine, kk, mode, cand)
+        gathered = self.coll.all_gather(cand)
+        return self.engine.merge(gathered, take, mode == "strict")

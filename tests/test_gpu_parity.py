@@ -500,3 +500,51 @@ def test_clustered_at_scale(gpu, oracle_lib):
     oid, olcp, oh = oracle_lib.oracle_top_k_batch(ds.items, qs[sample], 32, nthreads=8)
     for j, i in enumerate(sample):
         assert b.pairs(i) == list(zip(oid[j, :oh[j]].tolist(), olcp[j, :oh[j]].tolist()))
+
+
+def _range_gpu_worker(rank, world, port, backend):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    from paper_2602_04936_b200.rangeshard import RangeShardedIndex
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group(backend, rank=rank, world_size=world)
+    try:
+        for n, L, sigma, seed in ((50_000, 16, 4, 31), (4000, 8, 2, 32), (20_000, 12, 65536, 33)):
+            ds = lg.generate_dataset(n, L, sigma, seed=seed)
+            qs = np.vstack([lg.generate_queries(ds, 200, seed=seed + 1),
+                            lg.generate_queries(ds, 200, seed=seed + 2, prefix_len=L // 2)])
+            lo, hi = n * rank // world, n * (rank + 1) // world
+            sh = RangeShardedIndex(ds.items[lo:hi], L, sigma, id_offset=lo)
+            full = oracle.OracleTrie(ds.items, sigma)
+            dq = torch.from_numpy(qs).cuda()
+            for k in (1, 10, 32):
+                for mode in ("complete", "strict"):
+                    ids, lcps, hits = (t.cpu() for t in sh.query(dq, k, mode))
+                    fids, flcps, fhits, _, _, _ = full.query_batch(qs, k, mode)
+                    for i in range(len(qs)):
+                        h = int(hits[i])
+                        assert list(zip(ids[i, :h].tolist(), lcps[i, :h].tolist())) == \
+                            list(zip(fids[i, :fhits[i]].tolist(), flcps[i, :fhits[i]].tolist())), (n, k, mode, i)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,backend", [(1, "nccl"), (2, "gloo"), (3, "gloo")])
+def test_range_sharded_gpu_engine(gpu, oracle_lib, world, backend):
+    """RangeShardedIndex with the CUDA engine and merge kernel.  world > 1
+    shares the single GPU with gloo collectives (host-level exchange only)."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mp.spawn(_range_gpu_worker, args=(world, port, backend), nprocs=world, join=True)
