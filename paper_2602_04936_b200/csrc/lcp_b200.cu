@@ -389,9 +389,12 @@ static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, i
     long long cnt = (n + s - 1) / s;
     dv.level_cnt[j] = cnt;
     dv.level_off[j] = total;
-    total += (cnt + 1) & ~1ll;  // even -> 16-byte aligned bulk copies
+    // whole 64-entry blocks, padded with all-ones keys (never < q): the
+    // W == 1 search reads a full block per level with no bounds checks
+    total += (cnt + LCP_SEARCH_FANOUT - 1) / LCP_SEARCH_FANOUT * LCP_SEARCH_FANOUT;
   }
   LCP_TRY(dalloc(&ix->levels, std::max(2ll, total) * W, acct));
+  LCP_CK(cudaMemsetAsync(ix->levels, 0xFF, (size_t)std::max(2ll, total) * W * 8, st));
   for (int j = 0; j < h; ++j) {
     k_gather_level<<<blocks_for(dv.level_cnt[j] * W, 256), 256, 0, st>>>(
         ix->keys, dv.level_cnt[j], strides[j], W, ix->levels + dv.level_off[j] * W);
@@ -401,7 +404,8 @@ static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, i
   dv.smem_levels = 0;
   dv.smem_entries = 0;
   for (int j = 0; j < h; ++j) {
-    long long end = dv.level_off[j] + ((dv.level_cnt[j] + 1) & ~1ll);
+    long long end = dv.level_off[j] +
+                    (dv.level_cnt[j] + LCP_SEARCH_FANOUT - 1) / LCP_SEARCH_FANOUT * LCP_SEARCH_FANOUT;
     if (end * W * 8 > kSmemStageCap) break;
     dv.smem_levels = j + 1;
     dv.smem_entries = (int)end;

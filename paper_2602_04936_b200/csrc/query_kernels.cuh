@@ -348,17 +348,15 @@ __device__ __forceinline__ long long prefix_bound(const DevIndex& ix, const u64*
                                                   bool upper);
 
 // One 64-ary search step over a level table: number of entries < q among
-// the 64 separators [blk*64, blk*64+64) (two per lane).
-__device__ __forceinline__ int level_count(const u64* __restrict__ tab, int cnt, int blk, u64 q) {
-  const int i0 = blk * LCP_SEARCH_FANOUT + 2 * lane_id();
-  u32 lt = 0;
-  if (i0 + 1 < cnt) {
-    const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(tab + i0);
-    lt = (u32)(v.x < q) + (u32)(v.y < q);
-  } else if (i0 < cnt) {
-    lt = tab[i0] < q;
-  }
-  return (int)__reduce_add_sync(LCP_FULL_MASK, lt);
+// the 64 separators [blk*64, blk*64+64) (two per lane).  Tables are padded
+// to whole blocks with all-ones keys, which never compare below q.
+__device__ __forceinline__ int level_count(const u64* tab, int blk, u64 q) {
+  const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(tab + blk * LCP_SEARCH_FANOUT + 2 * lane_id());
+  return (int)__reduce_add_sync(LCP_FULL_MASK, (u32)(v.x < q) + (u32)(v.y < q));
+}
+__device__ __forceinline__ int level_count_g(const u64* __restrict__ tab, int blk, u64 q) {
+  const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(tab + blk * LCP_SEARCH_FANOUT) + lane_id());
+  return (int)__reduce_add_sync(LCP_FULL_MASK, (u32)(v.x < q) + (u32)(v.y < q));
 }
 
 // strict / complete: <= 32 regs, so two batches share an SM; TAL: 64 regs
@@ -433,23 +431,23 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, MODE == 2 ? 1 : 2)
     }
     stage_wait(ix, bar);  // first iteration: the query load overlaps the copy
     LCP_STAMP(qi, 1);
-    // 64-ary search down to the 32-key leaf block holding lower_bound(q)
+    // 64-ary search down to the 32-key leaf block holding lower_bound(q).
+    // Only the root can count 0 separators below q (q <= every key: pos = 0);
+    // below it, a child block starts with its parent's separator, which is < q.
     int blk = 0;
-    bool at_root_min = false;  // q <= every key (pos = 0)
-    int j = 0;
-    for (; j < ix.smem_levels; ++j) {
-      const int c = level_count(staged + (int)ix.level_off[j], (int)ix.level_cnt[j], blk, q);
-      if (c == 0) { at_root_min = true; break; }
-      blk = blk * LCP_SEARCH_FANOUT + c - 1;
-    }
-    if (!at_root_min) {
-      for (; j < ix.nlevels; ++j) {
-        const int c = level_count(ix.levels + (int)ix.level_off[j], (int)ix.level_cnt[j], blk, q);
-        if (c == 0) { at_root_min = true; break; }
-        blk = blk * LCP_SEARCH_FANOUT + c - 1;
+    if (ix.nlevels > 0) {
+      const int c0 = ix.smem_levels > 0 ? level_count(staged, 0, q) : level_count_g(ix.levels, 0, q);
+      if (c0 > 0) {
+        blk = c0 - 1;
+        int j = 1;
+#pragma unroll 1
+        for (; j < ix.smem_levels; ++j)
+          blk = blk * LCP_SEARCH_FANOUT + level_count(staged + (int)ix.level_off[j], blk, q) - 1;
+#pragma unroll 1
+        for (; j < ix.nlevels; ++j)
+          blk = blk * LCP_SEARCH_FANOUT + level_count_g(ix.levels + (int)ix.level_off[j], blk, q) - 1;
       }
     }
-    if (at_root_min) blk = 0;
     LCP_STAMP(qi, 2);
     // Leaf block [B, B+32) holds pos = lower_bound(q) in (B, B+32] (or
     // pos = 0).  The region [B-16, B+48) (T=2) / [B-32, B+64) (T=3), warp-
@@ -459,14 +457,16 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, MODE == 2 ? 1 : 2)
     int l[T];
     u32 id[T];
     int dmax = -1;
+    // unconditional loads at a clamped index (n >= 1), masked afterwards;
+    // lcp = min(clz64(key ^ q) >> lb, L) is exact for W == 1 (clz64(0) = 64)
 #pragma unroll
     for (int t = 0; t < T; ++t) {
       const int i = s + t * 32 + lane;
       const bool ok = (unsigned)i < (unsigned)n;
-      const u64 key = ok ? __ldg(keys + i) : 0ull;
-      id[t] = ok ? __ldg(order + i) : 0u;
-      const u64 x = key ^ q;
-      l[t] = ok ? (x ? (__clzll((long long)x) >> lb) : L) : -1;
+      const int ic = min(max(i, 0), n - 1);
+      const u64 key = __ldg(keys + ic);
+      id[t] = __ldg(order + ic);
+      l[t] = ok ? min(__clzll((long long)(key ^ q)) >> lb, L) : -1;
       dmax = max(dmax, l[t]);
     }
     dmax = (int)__reduce_max_sync(LCP_FULL_MASK, (unsigned)(dmax + 1)) - 1;
