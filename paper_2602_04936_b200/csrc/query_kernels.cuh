@@ -579,9 +579,15 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, MODE == 2 ? 1 : 2)
       const C a = __shfl_sync(LCP_FULL_MASK, pick_slot<C, T>(comp, t0), e & 31);
       const C bb = __shfl_sync(LCP_FULL_MASK, pick_slot<C, T>(comp, t0 + 1), e & 31);
       const C cv = lane < cnt ? (((e >> 5) == t0) ? a : bb) : ~C(0);
+      // all-pairs rank in blocks of 8 with immediate shuffle lanes; lanes >= cnt
+      // hold all-ones and never count, so only the block guard is needed
       int rank = 0;
-#pragma unroll 8
-      for (int jj = 0; jj < cnt; ++jj) rank += __shfl_sync(LCP_FULL_MASK, cv, jj) < cv;
+#pragma unroll
+      for (int blk8 = 0; blk8 < 32; blk8 += 8) {
+        if (blk8 >= cnt) break;
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) rank += __shfl_sync(LCP_FULL_MASK, cv, blk8 + jj) < cv;
+      }
       LCP_STAMP(qi, 5);
       const int take = min(need, cnt);
       if (lane < cnt && rank < take) {
