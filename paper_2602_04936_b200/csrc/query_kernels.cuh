@@ -319,10 +319,25 @@ __device__ __forceinline__ void write_result(long long qi, int stride, int take,
   }
 }
 
-// d* = max{d : #{window items with lcp >= d} >= need}  (binary search on d)
+// d* = max{d : #{window items with lcp >= d} >= need}.  One REDUX counts the
+// four levels d_max .. d_max-3 at once (8-bit fields; a window holds <= 96
+// items), which settles most queries; the rest binary-search below them.
 template <int T>
 __device__ __forceinline__ int window_dstar(const int (&l)[T], int dmax, int need) {
-  int lo = 0, hi = dmax;
+  if (dmax <= 0) return 0;
+  u32 mine = 0;
+#pragma unroll
+  for (int t = 0; t < T; ++t)
+    mine += (u32)(l[t] >= dmax) | ((u32)(l[t] >= dmax - 1) << 8) | ((u32)(l[t] >= dmax - 2) << 16) |
+            ((u32)(l[t] >= dmax - 3) << 24);
+  const u32 tot = __reduce_add_sync(LCP_FULL_MASK, mine);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    if (dmax - c < 0) return 0;
+    if ((int)((tot >> (8 * c)) & 0xffu) >= need) return dmax - c;
+  }
+  int lo = 0, hi = dmax - 4;  // every level above failed
+  if (hi <= 0) return 0;
   while (lo < hi) {
     int mid = (lo + hi + 1) >> 1;
     u32 mine = 0;
