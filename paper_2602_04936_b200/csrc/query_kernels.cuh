@@ -877,6 +877,44 @@ __device__ __forceinline__ long long prefix_bound(const DevIndex& ix, const u64*
   return a;
 }
 
+// lower_bound(keys, q) for any W by one warp: 64-ary over the global search
+// tables (two separators per lane per level), then the 32-key leaf block
+__device__ __forceinline__ long long warp_lower_bound_any(const DevIndex& ix, const u64* q) {
+  const int lane = lane_id();
+  const int W = ix.W;
+  long long blk = 0;
+  for (int j = 0; j < ix.nlevels; ++j) {
+    const u64* tab = ix.levels + ix.level_off[j] * W;
+    const long long cnt = ix.level_cnt[j];
+    const long long i0 = blk * LCP_SEARCH_FANOUT + 2 * lane;
+    const bool lt0 = i0 < cnt && key_less<0>(tab + i0 * W, q, ix);
+    const bool lt1 = i0 + 1 < cnt && key_less<0>(tab + (i0 + 1) * W, q, ix);
+    const int c = __popc(__ballot_sync(LCP_FULL_MASK, lt0)) + __popc(__ballot_sync(LCP_FULL_MASK, lt1));
+    if (c == 0) return 0;  // only at the root: q <= every key
+    blk = blk * LCP_SEARCH_FANOUT + c - 1;
+  }
+  const long long base = blk * LCP_LEAF_KEYS;
+  const long long i = base + lane;
+  const bool lt = i < ix.n && key_less<0>(ix.keys + i * W, q, ix);
+  return base + __popc(__ballot_sync(LCP_FULL_MASK, lt));
+}
+
+// run_edge for any W (see run_edge): last position of {lcp >= d} from `in` toward `out`
+__device__ __forceinline__ long long run_edge_any(const DevIndex& ix, const u64* q, int d,
+                                                  long long in, long long out) {
+  const long long dir = out > in ? 1 : -1;
+  for (;;) {
+    const long long span = (out - in) * dir;
+    if (span <= 1) return in;
+    const long long step = (span + 31) >> 5;
+    const long long off = step * (lane_id() + 1);
+    const bool inside = off < span && key_lcp<0>(ix.keys + (in + dir * off) * ix.W, q, ix) >= d;
+    const long long c = __popc(__ballot_sync(LCP_FULL_MASK, inside));
+    if (step * (c + 1) < span) out = in + dir * step * (c + 1);
+    in += dir * step * c;
+  }
+}
+
 struct GenItem {
   const DevIndex* ix;
   const u64* q;
@@ -904,11 +942,90 @@ __global__ void __launch_bounds__(GEN_THREADS)
   __shared__ u64 s_prefix;
   __shared__ u32 s_rank;
   __shared__ unsigned long long s_sym;
+  __shared__ long long s_pos;
+  __shared__ long long s_part[GEN_THREADS / 32][2];
   const int L = ix.L;
+  const int lane = lane_id(), warp = threadIdx.x >> 5;
 
   for (long long qi = blockIdx.x; qi < count; qi += gridDim.x) {
     const u64* q = qkeys + qi * ix.W;
-    if (threadIdx.x == 0) {
+    // strict / complete with need <= GEN_CAP / 2: CTA-cooperative setup.
+    // pos by warp 0's 64-ary search; d* from the window [pos - need,
+    // pos + need) (R(d*+1) lies inside it); R(d*) from the window, extended by
+    // run_edge_any when the run reaches a window edge.
+    if (!fullscan && mode != 2 && ix.n > 0 && (long long)k <= GEN_CAP / 2) {
+      if (warp == 0) {
+        const long long pos = warp_lower_bound_any(ix, q);
+        if (lane == 0) s_pos = pos;
+      }
+      __syncthreads();
+      const long long pos = s_pos;
+      const long long need = mode == 1 ? min((long long)k, ix.n) : (long long)k;
+      const long long wlo = max(0ll, pos - need), whi = min(ix.n, pos + need);
+      const int wn = (int)(whi - wlo);
+      int* wl = reinterpret_cast<int*>(buf);  // window lcps (<= GEN_CAP ints)
+      int mymax = -1;
+      for (int i = threadIdx.x; i < wn; i += GEN_THREADS) {
+        const int l = key_lcp<0>(ix.keys + (wlo + i) * ix.W, q, ix);
+        wl[i] = l;
+        mymax = max(mymax, l);
+      }
+      auto block_pair = [&](long long a, long long b, bool is_min) {
+        // block-wide (min|max, max) of per-thread pairs via s_part
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          const long long oa = __shfl_xor_sync(LCP_FULL_MASK, a, o);
+          a = is_min ? min(a, oa) : a + oa;
+          b = max(b, __shfl_xor_sync(LCP_FULL_MASK, b, o));
+        }
+        if (lane == 0) {
+          s_part[warp][0] = a;
+          s_part[warp][1] = b;
+        }
+        __syncthreads();
+        long long ra = s_part[0][0], rb = s_part[0][1];
+        for (int w = 1; w < GEN_THREADS / 32; ++w) {
+          ra = is_min ? min(ra, s_part[w][0]) : ra + s_part[w][0];
+          rb = max(rb, s_part[w][1]);
+        }
+        __syncthreads();
+        return make_longlong2(ra, rb);
+      };
+      const int dmax = (int)block_pair(0, mymax, false).y;
+      int dstar = dmax;
+      if (mode == 1) {
+        int dl = 0, dh = dmax;
+        while (dl < dh) {
+          const int mid = (dl + dh + 1) >> 1;
+          long long c = 0;
+          for (int i = threadIdx.x; i < wn; i += GEN_THREADS) c += wl[i] >= mid;
+          if (block_pair(c, 0, false).x >= need) dl = mid;
+          else dh = mid - 1;
+        }
+        dstar = dl;
+      }
+      long long first = LLONG_MAX, last = -1;
+      for (int i = threadIdx.x; i < wn; i += GEN_THREADS)
+        if (wl[i] >= dstar) {
+          first = min(first, (long long)i);
+          last = max(last, (long long)i);
+        }
+      const longlong2 fl = block_pair(first, last, true);
+      long long lo = wlo + fl.x, hi = wlo + fl.y + 1;
+      if (warp == 0) {
+        if (lo == wlo && wlo > 0) lo = dstar ? run_edge_any(ix, q, dstar, lo, -1) : 0;
+        if (hi == whi && whi < ix.n) hi = dstar ? run_edge_any(ix, q, dstar, hi - 1, ix.n) + 1 : ix.n;
+        if (lane == 0) {
+          s_lo = lo;
+          s_hi = hi;
+          s_take = mode == 1 ? need : min((long long)k, hi - lo);
+          s_dmax = dmax;
+          s_dstar = dstar;
+          s_md = dmax;
+          s_sym = 0;
+        }
+      }
+    } else if (threadIdx.x == 0) {
       long long lo = 0, hi = ix.n, take = 0;
       int dmax = 0, dstar = 0, md = 0;
       if (fullscan) {
