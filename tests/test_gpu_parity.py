@@ -548,3 +548,36 @@ def test_range_sharded_gpu_engine(gpu, oracle_lib, world, backend):
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
     mp.spawn(_range_gpu_worker, args=(world, port, backend), nprocs=world, join=True)
+
+
+def test_concurrent_readers(gpu):
+    """A built index is safe for concurrent readers (trie.py:19-20): threads
+    with their own workspaces get exactly the serial answers."""
+    import threading
+
+    ds = lg.generate_dataset(200_000, 24, 4, seed=40)
+    idx = lg.build(ds)
+    batches = [lg.generate_queries(ds, 512, seed=41 + t, prefix_len=(None if t % 2 else 12)) for t in range(8)]
+    serial = [(idx.query_batch(b, 10, "complete"), idx.query_batch(b, 7, "strict")) for b in batches]
+    errors = []
+
+    def worker(t):
+        try:
+            for rep in range(5):
+                for j in range(t, len(batches), 4):
+                    c = idx.query_batch(batches[j], 10, "complete")
+                    s = idx.query_batch(batches[j], 7, "strict")
+                    for got, exp in ((c, serial[j][0]), (s, serial[j][1])):
+                        assert np.array_equal(got.ids, exp.ids) and np.array_equal(got.hits, exp.hits)
+                        assert np.array_equal(got.lcps, exp.lcps)
+                    r = idx.query(batches[j][rep], 10, "complete")
+                    assert r.pairs() == serial[j][0].pairs(rep)
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(repr(e))
+
+    threads = [threading.Thread(target=worker, args=(t,)) for t in range(4)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors
