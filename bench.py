@@ -353,6 +353,23 @@ def main() -> None:
                     "peak_source": peak_src,
                     "duration_source": "CUDA events over the graph-replayed single-stream step loop",
                     "bytes_formula": "sum_q K_b*ceil(log2(N+1)) + |R(d*)|*(K_b+4) + K_b + 6k, K_b=8"}
+        # the kernel is issue-bound, not HBM-bound: instruction roofline from the
+        # committed ncu capture (warp instructions per query) and the live rate
+        try:
+            prof_q = json.load(open(prof))["k_query_w1"]
+            ipq = prof_q["warp_instructions"] / BATCH
+            mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz")
+            sms = torch.cuda.get_device_properties(dev).multi_processor_count
+            peak_gi = sms * 4 * mhz * 1e6 / 1e9  # 4 schedulers x 1 warp instruction / clock
+            ach_gi = value / world * ipq / 1e9   # per GPU
+            roofline["issue"] = {
+                "warp_instructions_per_query": round(ipq, 1), "achieved": round(ach_gi, 1),
+                "peak": round(peak_gi, 1), "unit": "G warp-instructions/s per GPU",
+                "frac": round(ach_gi / peak_gi, 4),
+                "source": "profiles/ncu_summary.json smsp__inst_executed.sum / 4096 queries; "
+                          "peak = SMs x 4 schedulers x median SM clock in the timed region"}
+        except Exception:
+            pass
 
     line = {
         "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
