@@ -9,7 +9,7 @@ d* -> rank selection), inputs resident in HBM.
 Timing: the steps are captured once in a CUDA graph and replayed, so the
 GPU is never starved by Python-side launch cost.  Step i runs on index
 replica i % 8 (8 identical replicas, 8 x 24 MB > 126 MB L2, so every step's
-index reads miss L2) and on CUDA stream i % 3 (three batches in flight, as a
+index reads miss L2) and on CUDA stream i % 4 (four batches in flight, as a
 serving loop keeps them); the whole K-step region is bracketed by CUDA
 events on the capture stream.  The same loop on one stream (one batch in
 flight) is reported beside it, and its per-step time is the kernel duration
@@ -45,7 +45,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "top-k LCP queries/sec at N=2M, L=32, k=10 (HBM GB/s frac); p50 latency; J/query"
 N_ITEMS, SEQ_LEN, SIGMA, K, BATCH = 2_000_000, 32, 4, 10, 4096
-INFLIGHT = 3  # batches in flight in the headline timed loop (streams)
+INFLIGHT = 4  # batches in flight in the headline timed loop (streams); swept 2..5: 1.02/1.44/1.49/1.49 G q/s
+INFLIGHT = int(os.environ.get("LCP_BENCH_INFLIGHT", INFLIGHT))  # sweep hook
 FALLBACK_HBM_GBS = 6650.0
 
 
