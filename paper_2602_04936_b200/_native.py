@@ -196,7 +196,7 @@ def workspace() -> Workspace:
     return ws
 
 
-ASYNC_DEPTH = 4  # batches in flight per thread for the async host path
+ASYNC_DEPTH = 8  # batches in flight per thread for the async host path (swept 1..16: 8 is best)
 
 
 def async_workspace() -> Workspace:
