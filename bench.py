@@ -139,12 +139,13 @@ def nvml_energy():
 
 
 # --------------------------------------------------------------------------
-def cpu_reference(ds, queries: np.ndarray, k: int, budget_s: float, nthreads: int):
+def cpu_reference(ds, queries: np.ndarray, k: int, budget_s: float, nthreads: int, trie=None):
     """Time the reference algorithm (C port in oracle/) on the host cores."""
     import oracle
 
-    oracle.build()
-    trie = oracle.OracleTrie(ds.items, SIGMA)
+    if trie is None:
+        oracle.build()
+        trie = oracle.OracleTrie(ds.items, SIGMA)
     trie.query_batch(queries[:256], k, "complete", nthreads=nthreads)  # warm
     done, t0 = 0, time.perf_counter()
     nb = queries.shape[0] // BATCH
@@ -406,6 +407,14 @@ def main() -> None:
             "value": cpu_qps, "unit": "queries/s", "cores": os.cpu_count() or 1, "kind": "port",
             "sample": (f"{cpu_done} complete-mode k=10 queries ({cpu_el:.1f} s) of the same workload; "
                        "C restatement of trie.build/TrieIndex.query (oracle/lcp_oracle.c), one pthread per core")}
+        # host-thread scaling of the same CPU path (w in {1, 2, 4, all})
+        sweep = {}
+        for w in sorted({1, 2, 4, os.cpu_count() or 1}):
+            if w == (os.cpu_count() or 1):
+                sweep[str(w)] = cpu_qps
+                continue
+            sweep[str(w)] = cpu_reference(ds, qs, K, min(1.5, args.cpu_budget_s), w, trie=trie)[0]
+        line["cpu_baseline"]["threads_sweep"] = sweep
         if not args.no_extras:
             flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
             line["extras"] = extras(idx, ds, qs, main_stream, flush_buf)
