@@ -11,6 +11,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <mutex>
 #include <cstdio>
 #include <string>
@@ -69,10 +70,29 @@ unsigned blocks_for(long long work, int threads) {
   return (unsigned)std::max(1ll, b);
 }
 
+// Index memory comes from the device's stream-ordered pool, which keeps freed
+// memory mapped (release threshold = max): rebuilding an index reuses it
+// instead of unmapping and remapping hundreds of MB through the driver.
+void keep_pool_mapped() {
+  static std::mutex mu;
+  static std::vector<int> done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  std::lock_guard<std::mutex> lock(mu);
+  if (std::find(done.begin(), done.end(), dev) != done.end()) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    unsigned long long thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  cudaGetLastError();
+  done.push_back(dev);
+}
+
 template <typename T>
-int dalloc(T** p, long long count, long long* acct) {
+int dalloc(T** p, long long count, long long* acct, cudaStream_t st) {
   size_t bytes = (size_t)std::max(1ll, count) * sizeof(T);
-  cudaError_t e = cudaMalloc((void**)p, bytes);
+  cudaError_t e = cudaMallocAsync((void**)p, bytes, st);
   if (e != cudaSuccess)
     return fail(LCP_ERR_CUDA, std::string("cudaMalloc(") + std::to_string(bytes) +
                                   " bytes): " + cudaGetErrorString(e));
@@ -249,15 +269,19 @@ const char* lcp_last_error(void) { return g_err.c_str(); }
 
 int lcp_index_free(lcp_index* ix) {
   if (!ix) return LCP_OK;
-  cudaFree(ix->keys);
-  cudaFree(ix->keys_orig);
-  cudaFree(ix->order);
-  cudaFree(ix->keys_hi);
-  cudaFree(ix->keys_lo);
-  cudaFree(ix->adj);
-  cudaFree(ix->levels);
-  cudaFree(ix->directory);
-  cudaFree(ix->sketch);
+  // like cudaFree: nothing may still use the index; the memory returns to the
+  // (mapped) stream-ordered pool
+  cudaDeviceSynchronize();
+  if (ix->keys) cudaFreeAsync(ix->keys, 0);
+  if (ix->keys_orig) cudaFreeAsync(ix->keys_orig, 0);
+  if (ix->order) cudaFreeAsync(ix->order, 0);
+  if (ix->keys_hi) cudaFreeAsync(ix->keys_hi, 0);
+  if (ix->keys_lo) cudaFreeAsync(ix->keys_lo, 0);
+  if (ix->adj) cudaFreeAsync(ix->adj, 0);
+  if (ix->levels) cudaFreeAsync(ix->levels, 0);
+  if (ix->directory) cudaFreeAsync(ix->directory, 0);
+  if (ix->sketch) cudaFreeAsync(ix->sketch, 0);
+  cudaStreamSynchronize(0);
   delete ix;
   return LCP_OK;
 }
@@ -267,38 +291,50 @@ static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, i
   DevIndex& dv = ix->dv;
   const int W = dv.W;
   long long* acct = &ix->device_bytes;
+  // LCP_BUILD_TRACE=1: per-phase wall times on stderr (diagnostics only)
+  static const bool trace = getenv("LCP_BUILD_TRACE") != nullptr;
+  auto t_start = std::chrono::steady_clock::now();
+  auto phase = [&](const char* what) {
+    if (!trace) return;
+    cudaStreamSynchronize(st);
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+    fprintf(stderr, "[build] %-10s %8.2f ms\n", what, ms);
+  };
 
   // rows -> device
   const uint16_t* d_rows = rows;
   uint16_t* owned_rows = nullptr;
   if (!is_device_ptr(rows)) {
-    LCP_CK(cudaMalloc((void**)&owned_rows, (size_t)n * L * sizeof(uint16_t)));
+    LCP_CK(cudaMallocAsync((void**)&owned_rows, (size_t)n * L * sizeof(uint16_t), st));
     LCP_CK(cudaMemcpyAsync(owned_rows, rows, (size_t)n * L * sizeof(uint16_t),
                            cudaMemcpyHostToDevice, st));
     d_rows = owned_rows;
   }
   struct RowsGuard {
     uint16_t* p;
-    ~RowsGuard() { if (p) cudaFree(p); }
-  } rows_guard{owned_rows};
+    cudaStream_t st;
+    ~RowsGuard() { if (p) cudaFreeAsync(p, st); }
+  } rows_guard{owned_rows, st};
 
+  phase("rows");
   const long long pad = 64;
-  LCP_TRY(dalloc(&ix->keys_orig, (n + pad) * W, acct));
+  LCP_TRY(dalloc(&ix->keys_orig, (n + pad) * W, acct, st));
   LCP_CK(cudaMemsetAsync(ix->keys_orig, 0, (size_t)(n + pad) * W * 8, st));
   u32* perm = nullptr;
   u32* perm_alt = nullptr;
   u64* kw = nullptr;
   u64* kw_alt = nullptr;
   int* d_err = nullptr;
-  LCP_CK(cudaMalloc((void**)&perm, (size_t)(n + pad) * 4));
-  LCP_CK(cudaMalloc((void**)&perm_alt, (size_t)(n + pad) * 4));
-  LCP_CK(cudaMalloc((void**)&kw, (size_t)(n + pad) * 8));
-  LCP_CK(cudaMalloc((void**)&kw_alt, (size_t)(n + pad) * 8));
-  LCP_CK(cudaMalloc((void**)&d_err, sizeof(int)));
+  LCP_CK(cudaMallocAsync((void**)&perm, (size_t)(n + pad) * 4, st));
+  LCP_CK(cudaMallocAsync((void**)&perm_alt, (size_t)(n + pad) * 4, st));
+  LCP_CK(cudaMallocAsync((void**)&kw, (size_t)(n + pad) * 8, st));
+  LCP_CK(cudaMallocAsync((void**)&kw_alt, (size_t)(n + pad) * 8, st));
+  LCP_CK(cudaMallocAsync((void**)&d_err, sizeof(int), st));
   struct TmpGuard {
     std::vector<void*> ps;
-    ~TmpGuard() { for (void* p : ps) if (p) cudaFree(p); }
-  } tmp{{perm_alt, kw_alt, d_err}};
+    cudaStream_t st;
+    ~TmpGuard() { for (void* p : ps) if (p) cudaFreeAsync(p, st); }
+  } tmp{{perm_alt, kw_alt, d_err}, st};
   LCP_CK(cudaMemsetAsync(d_err, 0, sizeof(int), st));
 
   k_pack<<<blocks_for(n * W, 256), 256, 0, st>>>(d_rows, n, L, W, dv.b, dv.spw, sigma,
@@ -308,12 +344,13 @@ static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, i
   LCP_CK(cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
   LCP_CK(cudaStreamSynchronize(st));
   if (h_err) {
-    cudaFree(perm);
-    cudaFree(kw);
+    cudaFreeAsync(perm, st);
+    cudaFreeAsync(kw, st);
     return fail(LCP_ERR_INVALID_INPUT,
                 "symbol out of range for alphabet of size " + std::to_string(sigma));
   }
 
+  phase("pack");
   // stable LSD over words (least significant word first) — core.py:162-174
   for (int w = W - 1; w >= 0; --w) {
     if (W == 1) {
@@ -332,6 +369,7 @@ static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, i
     kw_alt = ka;
     perm_alt = va;
   }
+  phase("sort");
   tmp.ps = {perm_alt, kw_alt, d_err};
   ix->order = perm;
   *acct += (n + pad) * 4;
@@ -340,7 +378,7 @@ static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, i
     *acct += (n + pad) * 8;
   } else {
     tmp.ps.push_back(kw);
-    LCP_TRY(dalloc(&ix->keys, (n + pad) * W, acct));
+    LCP_TRY(dalloc(&ix->keys, (n + pad) * W, acct, st));
     LCP_CK(cudaMemsetAsync(ix->keys, 0, (size_t)(n + pad) * W * 8, st));
     k_gather_keys<<<blocks_for(n * W, 256), 256, 0, st>>>(ix->keys_orig, perm, n, W, ix->keys);
     LCP_CK_LAUNCH();
@@ -350,8 +388,8 @@ static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, i
   dv.order = ix->order;
   if (W == 1) {  // hi / lo word planes of the original-order keys for the full scan
     const long long pn = (n + 4095) / 4096 * 4096 + 64;  // whole 16 KB stages
-    LCP_TRY(dalloc(&ix->keys_hi, pn, acct));
-    LCP_TRY(dalloc(&ix->keys_lo, pn, acct));
+    LCP_TRY(dalloc(&ix->keys_hi, pn, acct, st));
+    LCP_TRY(dalloc(&ix->keys_lo, pn, acct, st));
     LCP_CK(cudaMemsetAsync(ix->keys_hi, 0, (size_t)pn * 4, st));
     LCP_CK(cudaMemsetAsync(ix->keys_lo, 0, (size_t)pn * 4, st));
     k_split_words<<<blocks_for(n, 256), 256, 0, st>>>(ix->keys_orig, n, ix->keys_hi, ix->keys_lo);
@@ -360,14 +398,16 @@ static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, i
   dv.keys_hi = ix->keys_hi;
   dv.keys_lo = ix->keys_lo;
 
+  phase("planes");
   // adjacent lcp — core.py:177-184
-  LCP_TRY(dalloc(&ix->adj, std::max(1ll, n - 1), acct));
+  LCP_TRY(dalloc(&ix->adj, std::max(1ll, n - 1), acct, st));
   if (n > 1) {
     if (W == 1) k_adjacent_lcp<1><<<blocks_for(n - 1, 256), 256, 0, st>>>(dv, ix->adj);
     else k_adjacent_lcp<0><<<blocks_for(n - 1, 256), 256, 0, st>>>(dv, ix->adj);
     LCP_CK_LAUNCH();
   }
 
+  phase("adj");
   // k-ary search levels (stand-in for the trie descent, trie.py:229-256)
   // Tables j = 0..h-1 sample every LCP_LEAF_KEYS * 64**(h-1-j)-th key; the
   // last one resolves lower_bound(q) to a 32-key leaf block.
@@ -393,7 +433,7 @@ static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, i
     // W == 1 search reads a full block per level with no bounds checks
     total += (cnt + LCP_SEARCH_FANOUT - 1) / LCP_SEARCH_FANOUT * LCP_SEARCH_FANOUT;
   }
-  LCP_TRY(dalloc(&ix->levels, std::max(2ll, total) * W, acct));
+  LCP_TRY(dalloc(&ix->levels, std::max(2ll, total) * W, acct, st));
   LCP_CK(cudaMemsetAsync(ix->levels, 0xFF, (size_t)std::max(2ll, total) * W * 8, st));
   for (int j = 0; j < h; ++j) {
     k_gather_level<<<blocks_for(dv.level_cnt[j] * W, 256), 256, 0, st>>>(
@@ -411,6 +451,7 @@ static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, i
     dv.smem_entries = (int)end;
   }
 
+  phase("levels");
   // id sketch (smallest ids per block of sorted positions): bounds the work
   // of a query whose R(d*) spans far more than the loaded region
   {
@@ -425,7 +466,7 @@ static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, i
       cnt = (cnt + LCP_SK_FANOUT - 1) / LCP_SK_FANOUT;
     }
     dv.sk_levels = lv;
-    LCP_TRY(dalloc(&ix->sketch, tot * LCP_SK_LIST, acct));
+    LCP_TRY(dalloc(&ix->sketch, tot * LCP_SK_LIST, acct, st));
     k_id_sketch<LCP_SK_BLOCK><<<(unsigned)dv.sk_cnt[0], SK_THREADS, 0, st>>>(
         ix->order, n, ix->sketch);
     LCP_CK_LAUNCH();
@@ -438,6 +479,7 @@ static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, i
     dv.sketch = ix->sketch;
   }
 
+  phase("sketch");
   // TAL bucket structure — tal.py:42-82
   if (tal_depth >= 0) {
     ix->tal_depth = tal_depth;
@@ -452,7 +494,7 @@ static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, i
     }
     ix->tal_buckets = overflow ? -1 : buckets;
     if (tal_depth > 0 && !overflow && buckets <= kMaxDirectory) {
-      LCP_TRY(dalloc(&ix->directory, buckets + 1, acct));
+      LCP_TRY(dalloc(&ix->directory, buckets + 1, acct, st));
       k_directory<<<blocks_for(buckets + 1, 256), 256, 0, st>>>(dv, tal_depth, buckets,
                                                                ix->directory);
       LCP_CK_LAUNCH();
@@ -462,6 +504,7 @@ static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, i
   dv.tal_buckets = ix->tal_buckets;
   dv.directory = ix->directory;
   LCP_CK(cudaStreamSynchronize(st));
+  phase("done");
   return LCP_OK;
 }
 
@@ -516,7 +559,7 @@ int lcp_index_build(const uint16_t* rows, int64_t n, int32_t length, int32_t sig
       dv.tal_depth = tal_depth;
       dv.tal_buckets = buckets;
       if (tal_depth > 0 && buckets <= kMaxDirectory) {
-        int r = dalloc(&ix->directory, buckets + 1, &ix->device_bytes);
+        int r = dalloc(&ix->directory, buckets + 1, &ix->device_bytes, (cudaStream_t)0);
         if (r != LCP_OK) {
           lcp_index_free(ix);
           return r;
@@ -528,6 +571,7 @@ int lcp_index_build(const uint16_t* rows, int64_t n, int32_t length, int32_t sig
     *out = ix;
     return LCP_OK;
   }
+  keep_pool_mapped();
   cudaStream_t st;
   if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
     delete ix;
