@@ -278,7 +278,10 @@ def main() -> None:
         from paper_2602_04936_b200._native import workspace
 
         workspace()  # created outside graph capture (it allocates)
+        t_rep = time.perf_counter()
         replicas = [idx] + [lg.build(ds) for _ in range(7)]
+        torch.cuda.synchronize()
+        build_ms_steady = 1e3 * (time.perf_counter() - t_rep) / 7
         R = len(replicas)
         G = R * n_pool  # steps per captured graph
 
@@ -391,6 +394,7 @@ def main() -> None:
         "gpu_launches": gpu_launches,
         "clocks": clocks,
         "build_s": round(t_build, 3),
+        "build_ms_steady": round(build_ms_steady, 2),  # mean of 7 replica builds from host rows
         "one_batch_in_flight": {"value": world * BATCH * args.steps / (single_ms / 1e3), "unit": "queries/s",
                                 "ms_per_step": single_ms / args.steps},
     }
