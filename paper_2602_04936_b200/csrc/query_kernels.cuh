@@ -842,7 +842,7 @@ __global__ void __launch_bounds__(QT_THREADS)
 // ascending order, in rounds of GEN_CAP (8-pass radix select + smem bitonic
 // sort).  Queries are pre-packed by k_pack into qkeys.
 // ---------------------------------------------------------------------------
-constexpr int GEN_THREADS = 256;
+constexpr int GEN_THREADS = 128;
 constexpr int GEN_CAP = 2048;
 
 __device__ __forceinline__ void bitonic_sort_smem(u64* buf, int P) {
