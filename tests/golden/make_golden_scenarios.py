@@ -41,12 +41,22 @@ def main() -> int:
     sys.path.insert(0, REF_SRC)
     import lcpsearch as ref  # noqa: E402
 
+    # a reference snapshot, served by the sustained scenario through index_path
+    snap = os.path.join(HERE, "snap_scenario.lcpi")
+    import lcpsearch.storage  # noqa: E402,F401
+
+    ref.storage.write_index(snap, ref.build(ref.generate_dataset(1000, 10, 4, seed=21)))
+    configs = CONFIGS + [dict(scenario="sustained", seed=22, seq_len=10, alphabet=4, k=10, query_count=400,
+                              index_path="tests/golden/snap_scenario.lcpi")]
     out = []
-    for cfg in CONFIGS:
+    cwd = os.getcwd()
+    os.chdir(os.path.dirname(os.path.dirname(HERE)))  # index_path is relative to the repo root
+    for cfg in configs:
         rep = ref.run_scenario(ref.ScenarioConfig(**cfg)).to_machine()
         out.append({"args": {k: (list(v) if isinstance(v, tuple) else v) for k, v in cfg.items()},
                     "config": rep["config"], "results": rep["results"],
                     "schema_version": rep["schema_version"]})
+    os.chdir(cwd)
     with open(os.path.join(HERE, "scenarios_v1.json"), "w") as f:
         json.dump({"generator": "tests/golden/make_golden_scenarios.py", "reference": REF_SRC,
                    "reports": out}, f, indent=1, sort_keys=True)

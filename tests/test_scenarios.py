@@ -66,8 +66,9 @@ def test_text_rendering_matches_reference_format():
 # ------------------------------------------------------------------ GPU
 @pytest.mark.gpu
 @pytest.mark.parametrize("i", range(len(GOLDEN)))
-def test_results_equal_reference_runner(gpu, i):
+def test_results_equal_reference_runner(gpu, i, monkeypatch):
     g = GOLDEN[i]
+    monkeypatch.chdir(os.path.dirname(HERE))  # index_path cases are relative to the repo root
     rep = json.loads(json.dumps(run_scenario(ScenarioConfig(**g["args"])).to_machine()))
     assert rep["schema_version"] == g["schema_version"]
     assert rep["config"] == g["config"]
