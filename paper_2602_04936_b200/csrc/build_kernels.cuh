@@ -37,12 +37,12 @@ __global__ void k_pack(const uint16_t* __restrict__ rows, long long n, int L, in
   if (ids != nullptr && w == 0) ids[row] = (u32)row;
 }
 
-// split W == 1 keys into hi / lo 32-bit planes (full-scan layout)
-__global__ void k_split_words(const u64* __restrict__ keys, long long n, u32* __restrict__ hi,
-                              u32* __restrict__ lo) {
+// hi / lo 32-bit planes of each key's first word (full-scan layout)
+__global__ void k_split_words(const u64* __restrict__ keys, long long n, int W,
+                              u32* __restrict__ hi, u32* __restrict__ lo) {
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) {
-    const u64 k = keys[i];
+    const u64 k = keys[i * W];
     hi[i] = (u32)(k >> 32);
     lo[i] = (u32)k;
   }

@@ -17,7 +17,7 @@
 #include "common.cuh"
 
 constexpr int FS_THREADS = 256;
-constexpr int FS_STAGE_BYTES = 16384;
+constexpr int FS1_STAGE_KEYS = 2048;  // keys per shared-memory stage (hi + lo planes: 16 KB)
 
 template <int KCAP>
 __device__ __forceinline__ void list_insert(u64 (&list)[KCAP], u64 c) {
@@ -38,166 +38,6 @@ __device__ __forceinline__ u64 list_get(const u64 (&list)[KCAP], int idx) {
   return v;
 }
 
-template <int WMAX, int KCAP>
-__global__ void __launch_bounds__(FS_THREADS)
-    k_fullscan(DevIndex ix, const uint16_t* __restrict__ queries, int count, int need,
-               long long chunk, int nchunks, u64* __restrict__ partial, int* __restrict__ err) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  u64* bars = reinterpret_cast<u64*>(smem_raw);               // 2 mbarriers
-  u64* stage = reinterpret_cast<u64*>(smem_raw + 16);         // 2 x FS_STAGE_BYTES
-  const int W = ix.W;
-  const int L = ix.L;
-  const long long n = ix.n;
-  const long long qi = (long long)blockIdx.x * FS_THREADS + threadIdx.x;
-  const bool active = qi < count;
-
-  // pack this thread's query
-  u64 qk[WMAX];
-#pragma unroll
-  for (int w = 0; w < WMAX; ++w) qk[w] = 0;
-  if (active) {
-    const uint16_t* qrow = queries + qi * L;
-    bool bad = false;
-    for (int j = 0; j < L; ++j) {
-      u32 s = qrow[j];
-      bad |= (int)s >= ix.sigma;
-      int wj = j >> (6 - ix.lb);
-      u64 v = (u64)s << sym_shift(j, ix);
-#pragma unroll
-      for (int w = 0; w < WMAX; ++w)
-        if (w == wj) qk[w] |= v;
-    }
-    if (bad && blockIdx.y == 0) atomicOr(err, 1);
-  }
-
-  u64 list[KCAP];
-#pragma unroll
-  for (int i = 0; i < KCAP; ++i) list[i] = ~0ull;
-  int filled = 0;
-  u64 thr = ~0ull;    // list[need-1] once filled
-  u64 limm1 = ~0ull;  // W==1: accept iff (key ^ q) <= limm1
-  bool done = false;  // list full of exact matches
-
-  const long long c0 = (long long)blockIdx.y * chunk;
-  const long long c1 = min(n, c0 + chunk);
-  // W == 1 streams the 32-bit hi-word plane (4096 keys per 16 KB stage);
-  // otherwise whole keys, an even count per stage (16-byte aligned copies)
-  const int per_stage = WMAX == 1 ? FS_STAGE_BYTES / 4 : (FS_STAGE_BYTES / (8 * W)) & ~1;
-  const long long nst = c1 > c0 ? (c1 - c0 + per_stage - 1) / per_stage : 0;
-
-  if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    fence_barrier_init();
-  }
-  __syncthreads();
-  auto issue = [&](long long s) {
-    long long a = c0 + s * per_stage;
-    long long rows = min((long long)per_stage, c1 - a);
-    u64* dst = stage + (s & 1) * (FS_STAGE_BYTES / 8);
-    if constexpr (WMAX == 1) {
-      u32 bytes = (u32)(((rows * 4) + 15) & ~15ll);
-      mbar_arrive_expect_tx(&bars[s & 1], bytes);
-      bulk_g2s(dst, ix.keys_hi + a, bytes, &bars[s & 1]);
-    } else {
-      u32 bytes = (u32)(((rows * W * 8) + 15) & ~15ll);
-      mbar_arrive_expect_tx(&bars[s & 1], bytes);
-      bulk_g2s(dst, ix.keys_orig + a * W, bytes, &bars[s & 1]);
-    }
-  };
-  if (threadIdx.x == 0) {
-    if (nst > 0) issue(0);
-    if (nst > 1) issue(1);
-  }
-
-  for (long long s = 0; s < nst; ++s) {
-    mbar_wait(&bars[s & 1], (u32)((s >> 1) & 1));
-    const u64* buf = stage + (s & 1) * (FS_STAGE_BYTES / 8);
-    const long long a = c0 + s * per_stage;
-    const int rows = (int)min((long long)per_stage, c1 - a);
-    if (active && !done) {
-      if constexpr (WMAX == 1) {
-        // Fast test on the hi word only: x = key ^ q passes (x <= limm1,
-        // limm1 = 2^m - 1) only if hi(x) <= lim_hi (= 2^(m-32) - 1 for
-        // m >= 32, else 0); the lo word is fetched for those rare keys.
-        const u64 q0 = qk[0];
-        const u32 qh = (u32)(q0 >> 32);
-        const u32* hb = reinterpret_cast<const u32*>(buf);
-        u32 lim_hi = (u32)(limm1 >> 32);
-        auto offer = [&](long long id) {
-          const u64 x = ix.keys_orig[id] ^ q0;
-          if (x > limm1) return;
-          const int l = x ? (__clzll((long long)x) >> ix.lb) : L;
-          const u64 c = make_composite(l, (u32)id, L);
-          if (c >= thr) return;
-          list_insert<KCAP>(list, c);
-          if (++filled >= need) {
-            thr = list_get<KCAP>(list, need - 1);
-            const int t = L - (int)(thr >> 32);  // worst kept lcp
-            if (t >= L) {
-              done = true;
-            } else {
-              const int bits = (t + 1) * ix.b;  // <= 64
-              limm1 = bits >= 64 ? 0ull : ((1ull << (64 - bits)) - 1ull);
-              lim_hi = (u32)(limm1 >> 32);
-            }
-          }
-        };
-        int r = 0;
-        for (; r + 7 < rows; r += 8) {
-          const uint4 h0 = *reinterpret_cast<const uint4*>(hb + r);
-          const uint4 h1 = *reinterpret_cast<const uint4*>(hb + r + 4);
-          const u32 x[8] = {h0.x ^ qh, h0.y ^ qh, h0.z ^ qh, h0.w ^ qh,
-                            h1.x ^ qh, h1.y ^ qh, h1.z ^ qh, h1.w ^ qh};
-          const u32 m = min(min(min(x[0], x[1]), min(x[2], x[3])),
-                            min(min(x[4], x[5]), min(x[6], x[7])));
-          if (m <= lim_hi) {  // rare once the list is full
-#pragma unroll
-            for (int e = 0; e < 8; ++e)
-              if (x[e] <= lim_hi && !done) offer(a + r + e);
-            if (done) break;
-          }
-        }
-        for (; r < rows && !done; ++r)
-          if ((hb[r] ^ qh) <= lim_hi) offer(a + r);
-      } else {
-        for (int r = 0; r < rows; ++r) {
-          int l = key_lcp<WMAX>(buf + r * W, qk, ix);
-          u64 c = make_composite(l, (u32)(a + r), L);
-          if (c < thr) {
-            list_insert<KCAP>(list, c);
-            if (++filled >= need) thr = list_get<KCAP>(list, need - 1);
-          }
-        }
-      }
-    }
-    __syncthreads();  // everyone done with this buffer
-    if (threadIdx.x == 0 && s + 2 < nst) issue(s + 2);
-  }
-
-  if (active) {
-    u64* out = partial + (qi * nchunks + blockIdx.y) * (long long)need;
-    for (int j = 0; j < need; ++j) out[j] = list_get<KCAP>(list, j);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// W == 1 full scan.  The key stream is two SoA planes (hi / lo 32-bit words
-// of the packed keys, original row order), staged 2048 keys per 16 KB stage
-// by TMA bulk copies.  The hot loop tests 16 keys per iteration on the hi
-// plane only; the lo plane is read from shared memory for the rare keys
-// that survive.  A key survives iff lcp >= a, where a is the larger of the
-// thread's own bound (worst kept lcp + 1 once its list is full) and a
-// per-query hint g shared through global memory: a thread whose list is
-// full publishes its worst kept lcp t with atomicMax, since then >= need
-// items with lcp >= t exist and no item with lcp < t can be in the final
-// top-need.  The hint only prunes, so the merged result is exact and
-// deterministic whatever the timing.  Survivors go into a sorted per-thread
-// list of KCAP composites (C = u32 when ids fit, see make_comp) by the
-// branch-free insertion new[i] = max(old[i-1], min(old[i], c)).
-// ---------------------------------------------------------------------------
-constexpr int FS1_STAGE_KEYS = 2048;
-
 template <typename C, int KCAP>
 __device__ __forceinline__ void list_insert_mm(C (&list)[KCAP], C c) {
 #pragma unroll
@@ -217,9 +57,12 @@ __device__ __forceinline__ C list_at(const C (&list)[KCAP], int idx) {
 
 template <typename C, int KCAP>
 __global__ void __launch_bounds__(FS_THREADS)
-    k_fullscan_w1(DevIndex ix, const uint16_t* __restrict__ queries, int count, int need,
-                  long long chunk, int nchunks, u64* __restrict__ partial,
+    k_fullscan_w1(DevIndex ix, const uint16_t* __restrict__ queries, const u64* __restrict__ qkeys,
+                  int count, int need, long long chunk, int nchunks, u64* __restrict__ partial,
                   int* __restrict__ hint, int* __restrict__ err) {
+  // Any W: the filter and the first-word lcp run on the hi / lo planes of each
+  // key's first word; only keys equal to q in the whole first word (lcp >= spw)
+  // read their remaining words (keys_orig) against the packed query (qkeys).
   extern __shared__ __align__(16) unsigned char smem_raw[];
   u64* bars = reinterpret_cast<u64*>(smem_raw);
   u32* stage = reinterpret_cast<u32*>(smem_raw + 16);  // [2][hi | lo] x FS1_STAGE_KEYS
@@ -236,11 +79,12 @@ __global__ void __launch_bounds__(FS_THREADS)
     for (int j = 0; j < L; ++j) {
       const u32 s = qrow[j];
       bad |= (int)s >= ix.sigma;
-      q0 |= (u64)s << (64 - ix.b * (j + 1));
+      if (j < ix.spw) q0 |= (u64)s << (64 - ix.b * (j + 1));
     }
     if (bad && blockIdx.y == 0) atomicOr(err, 1);
   }
   const u32 qh = (u32)(q0 >> 32), ql = (u32)q0;
+  const int W = ix.W;
 
   C list[KCAP];
 #pragma unroll
@@ -301,7 +145,20 @@ __global__ void __launch_bounds__(FS_THREADS)
     auto offer = [&](int r) {
       const u64 x = ((u64)(hb[r] ^ qh) << 32) | (u64)(lb[r] ^ ql);
       if (x > limm1) return;
-      const int l = x ? (__clzll((long long)x) >> ix.lb) : L;
+      int l = x ? (__clzll((long long)x) >> ix.lb) : L;
+      if (!x && W > 1) {  // first word equal: finish on the remaining words
+        const u64* key = ix.keys_orig + (base + r) * W;
+        const u64* qk = qkeys + qi * W;
+        l = L;
+        for (int w = 1; w < W; ++w) {
+          const u64 y = key[w] ^ qk[w];
+          if (y) {
+            l = w * ix.spw + (__clzll((long long)y) >> ix.lb);
+            break;
+          }
+        }
+        if (l < a) return;
+      }
       const C c = make_comp<C>(l, (u32)(base + r), L, idbits);
       if (c >= thr) return;
       list_insert_mm<C, KCAP>(list, c);

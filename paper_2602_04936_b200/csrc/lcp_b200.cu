@@ -386,13 +386,13 @@ static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, i
   dv.keys = ix->keys;
   dv.keys_orig = ix->keys_orig;
   dv.order = ix->order;
-  if (W == 1) {  // hi / lo word planes of the original-order keys for the full scan
+  {  // hi / lo planes of the original-order keys' first word, for the full scan
     const long long pn = (n + 4095) / 4096 * 4096 + 64;  // whole 16 KB stages
     LCP_TRY(dalloc(&ix->keys_hi, pn, acct, st));
     LCP_TRY(dalloc(&ix->keys_lo, pn, acct, st));
     LCP_CK(cudaMemsetAsync(ix->keys_hi, 0, (size_t)pn * 4, st));
     LCP_CK(cudaMemsetAsync(ix->keys_lo, 0, (size_t)pn * 4, st));
-    k_split_words<<<blocks_for(n, 256), 256, 0, st>>>(ix->keys_orig, n, ix->keys_hi, ix->keys_lo);
+    k_split_words<<<blocks_for(n, 256), 256, 0, st>>>(ix->keys_orig, n, W, ix->keys_hi, ix->keys_lo);
     LCP_CK_LAUNCH();
   }
   dv.keys_hi = ix->keys_hi;
@@ -1362,20 +1362,10 @@ int lcp_workspace_wait(lcp_workspace* ws) {
 // ---- full scan ----------------------------------------------------------------
 }  // extern "C"
 
-template <int WMAX, int KCAP>
-static void launch_fullscan(const DevIndex& dv, const uint16_t* q, int count, int need,
-                            long long chunk, int nchunks, u64* partial, int* err,
-                            cudaStream_t st) {
-  dim3 grid((count + FS_THREADS - 1) / FS_THREADS, nchunks);
-  size_t smem = 16 + 2 * FS_STAGE_BYTES;
-  k_fullscan<WMAX, KCAP><<<grid, FS_THREADS, smem, st>>>(dv, q, count, need, chunk, nchunks,
-                                                          partial, err);
-}
-
 template <typename C, int KCAP>
-static int launch_fullscan_w1_k(const DevIndex& dv, const uint16_t* q, int count, int need,
-                                long long chunk, int nchunks, u64* partial, int* hint, int* err,
-                                cudaStream_t st) {
+static int launch_fullscan_w1_k(const DevIndex& dv, const uint16_t* q, const u64* qkeys, int count,
+                                int need, long long chunk, int nchunks, u64* partial, int* hint,
+                                int* err, cudaStream_t st) {
   const size_t smem = 16 + 2 * 2 * FS1_STAGE_KEYS * 4;  // 2 stages x (hi + lo) planes
   static bool attr = false;
   if (!attr) {
@@ -1384,18 +1374,18 @@ static int launch_fullscan_w1_k(const DevIndex& dv, const uint16_t* q, int count
     attr = true;
   }
   dim3 grid((count + FS_THREADS - 1) / FS_THREADS, nchunks);
-  k_fullscan_w1<C, KCAP><<<grid, FS_THREADS, smem, st>>>(dv, q, count, need, chunk, nchunks,
+  k_fullscan_w1<C, KCAP><<<grid, FS_THREADS, smem, st>>>(dv, q, qkeys, count, need, chunk, nchunks,
                                                          partial, hint, err);
   return LCP_OK;
 }
 
 // list length = need exactly for the common k, else the next size up
 template <typename C>
-static int launch_fullscan_w1_c(const DevIndex& dv, const uint16_t* q, int count, int need,
-                                long long chunk, int nchunks, u64* partial, int* hint, int* err,
-                                cudaStream_t st) {
+static int launch_fullscan_w1_c(const DevIndex& dv, const uint16_t* q, const u64* qkeys, int count,
+                                int need, long long chunk, int nchunks, u64* partial, int* hint,
+                                int* err, cudaStream_t st) {
 #define LCP_FS_CASE(K) \
-  if (need <= K) return launch_fullscan_w1_k<C, K>(dv, q, count, need, chunk, nchunks, partial, hint, err, st);
+  if (need <= K) return launch_fullscan_w1_k<C, K>(dv, q, qkeys, count, need, chunk, nchunks, partial, hint, err, st);
   LCP_FS_CASE(1) LCP_FS_CASE(2) LCP_FS_CASE(3) LCP_FS_CASE(4) LCP_FS_CASE(5) LCP_FS_CASE(6)
   LCP_FS_CASE(8) LCP_FS_CASE(10) LCP_FS_CASE(12) LCP_FS_CASE(16) LCP_FS_CASE(20)
   LCP_FS_CASE(24) LCP_FS_CASE(32)
@@ -1403,22 +1393,14 @@ static int launch_fullscan_w1_c(const DevIndex& dv, const uint16_t* q, int count
   return fail(LCP_ERR_INTERNAL, "full scan: need > 32 on the fast path");
 }
 
-static int launch_fullscan_w1(const DevIndex& dv, const uint16_t* q, int count, int need,
-                              long long chunk, int nchunks, u64* partial, int* hint, int* err,
-                              cudaStream_t st) {
+static int launch_fullscan_w1(const DevIndex& dv, const uint16_t* q, const u64* qkeys, int count,
+                              int need, long long chunk, int nchunks, u64* partial, int* hint,
+                              int* err, cudaStream_t st) {
   if (dv.idbits < 32)
-    return launch_fullscan_w1_c<u32>(dv, q, count, need, chunk, nchunks, partial, hint, err, st);
-  return launch_fullscan_w1_c<u64>(dv, q, count, need, chunk, nchunks, partial, hint, err, st);
+    return launch_fullscan_w1_c<u32>(dv, q, qkeys, count, need, chunk, nchunks, partial, hint, err, st);
+  return launch_fullscan_w1_c<u64>(dv, q, qkeys, count, need, chunk, nchunks, partial, hint, err, st);
 }
 
-template <int WMAX>
-static void launch_fullscan_k(const DevIndex& dv, const uint16_t* q, int count, int need,
-                              long long chunk, int nchunks, u64* partial, int* err,
-                              cudaStream_t st) {
-  if (need <= 8) launch_fullscan<WMAX, 8>(dv, q, count, need, chunk, nchunks, partial, err, st);
-  else if (need <= 16) launch_fullscan<WMAX, 16>(dv, q, count, need, chunk, nchunks, partial, err, st);
-  else launch_fullscan<WMAX, 32>(dv, q, count, need, chunk, nchunks, partial, err, st);
-}
 
 extern "C" {
 
@@ -1438,8 +1420,8 @@ int lcp_fullscan(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries
     return LCP_OK;
   }
   const int take = (int)std::min<long long>(k, dv.n);
-  if (dv.W <= 8 && take <= FAST_KMAX) {
-    const int per_stage = dv.W == 1 ? FS1_STAGE_KEYS : (FS_STAGE_BYTES / (8 * dv.W)) & ~1;
+  if (take <= FAST_KMAX) {
+    const int per_stage = FS1_STAGE_KEYS;
     const long long qtiles = (count + FS_THREADS - 1) / FS_THREADS;
     const long long max_chunks = (dv.n + per_stage - 1) / per_stage;
     long long want = std::max(1ll, (4ll * num_sms() + qtiles - 1) / qtiles);
@@ -1450,14 +1432,20 @@ int lcp_fullscan(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries
     const int nchunks = (int)((dv.n + chunk - 1) / chunk);
     LCP_TRY(ws->partial.ensure((size_t)count * nchunks * take * 8));
     u64* partial = ws->partial.as<u64>();
-    if (dv.W == 1) {
-      LCP_TRY(ws->hint.ensure((size_t)count * 4));
-      LCP_CK(cudaMemsetAsync(ws->hint.p, 0, (size_t)count * 4, st));
-      LCP_TRY(launch_fullscan_w1(dv, queries, count, take, chunk, nchunks, partial,
-                                 ws->hint.as<int>(), ws->d_err, st));
-    } else if (dv.W == 2) launch_fullscan_k<2>(dv, queries, count, take, chunk, nchunks, partial, ws->d_err, st);
-    else if (dv.W <= 4) launch_fullscan_k<4>(dv, queries, count, take, chunk, nchunks, partial, ws->d_err, st);
-    else launch_fullscan_k<8>(dv, queries, count, take, chunk, nchunks, partial, ws->d_err, st);
+    // W > 1: the kernel filters on the first word and reads the rest of the
+    // packed query for keys that match it entirely
+    const u64* qk = nullptr;
+    if (dv.W > 1) {
+      LCP_TRY(ws->qkeys.ensure((size_t)count * dv.W * 8));
+      k_pack<<<blocks_for((long long)count * dv.W, 256), 256, 0, st>>>(
+          queries, count, dv.L, dv.W, dv.b, dv.spw, dv.sigma, ws->qkeys.as<u64>(), nullptr, ws->d_err);
+      LCP_CK_LAUNCH();
+      qk = ws->qkeys.as<u64>();
+    }
+    LCP_TRY(ws->hint.ensure((size_t)count * 4));
+    LCP_CK(cudaMemsetAsync(ws->hint.p, 0, (size_t)count * 4, st));
+    LCP_TRY(launch_fullscan_w1(dv, queries, qk, count, take, chunk, nchunks, partial,
+                               ws->hint.as<int>(), ws->d_err, st));
     LCP_CK_LAUNCH();
     k_merge<<<blocks_for((long long)count * 32, 256), 256, 0, st>>>(
         partial, nchunks, count, take, take, (long long)nchunks * take, take, dv.L, 0, ids, lcps,
