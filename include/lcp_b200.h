@@ -191,7 +191,9 @@ int lcp_encode_candidates(const uint32_t* ids, const uint16_t* lcps, const int32
 int lcp_merge_candidates(const uint64_t* cand, int32_t shards, int32_t count, int32_t k,
                          int32_t take, int32_t length, int32_t strict, uint32_t* ids,
                          uint16_t* lcps, int32_t* hits, void* stream);
-/* (ids/lcps of lcp_merge_candidates have row stride max(1, take).) */
+/* (ids/lcps of lcp_merge_candidates have row stride max(1, take); take <= 32
+ *  merges with one warp per query, larger take with one CTA per query for
+ *  shards * k <= 8192.) */
 
 /* ---- host staging (no reference counterpart) -----------------------------
  * Page-locked host buffers so *_host calls DMA directly (cudaHostAlloc). */

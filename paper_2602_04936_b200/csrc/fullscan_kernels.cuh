@@ -260,6 +260,72 @@ __global__ void __launch_bounds__(256)
   if (lane == 0) out_hits[qi] = hits;
 }
 
+// merge for take > 32: one CTA per query sorts all shards' candidates
+// (shards * kin <= MERGE_SORT_CAP, padded to a power of two) in shared memory
+constexpr int MERGE_SORT_THREADS = 256;
+constexpr int MERGE_SORT_CAP = 8192;
+
+__global__ void __launch_bounds__(MERGE_SORT_THREADS)
+    k_merge_sort(const u64* __restrict__ cand, int shards, int count, int kin, long long s_stride,
+                 long long q_stride, int take, int L, int strict, u32* __restrict__ out_ids,
+                 uint16_t* __restrict__ out_lcps, int* __restrict__ out_hits, int out_stride) {
+  extern __shared__ __align__(16) u64 sbuf[];
+  __shared__ u64 s_best[MERGE_SORT_THREADS / 32];
+  __shared__ int s_valid;
+  const int m = shards * kin;
+  int P = 1;
+  while (P < m) P <<= 1;
+  for (long long qi = blockIdx.x; qi < count; qi += gridDim.x) {
+    u64 best = ~0ull;
+    for (int t = threadIdx.x; t < P; t += MERGE_SORT_THREADS) {
+      const u64 c = t < m ? cand[(t / kin) * s_stride + qi * q_stride + (t % kin)] : ~0ull;
+      sbuf[t] = c;
+      best = c < best ? c : best;
+    }
+    if (threadIdx.x == 0) s_valid = 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const u64 y = __shfl_xor_sync(LCP_FULL_MASK, best, o);
+      best = y < best ? y : best;
+    }
+    if (lane_id() == 0) s_best[threadIdx.x >> 5] = best;
+    __syncthreads();
+    for (int w = 0; w < MERGE_SORT_THREADS / 32; ++w) best = s_best[w] < best ? s_best[w] : best;
+    int valid = 0;
+    for (int t = threadIdx.x; t < P; t += MERGE_SORT_THREADS) {
+      u64 c = sbuf[t];
+      if (strict && (c >> 32) != (best >> 32)) c = ~0ull;  // strict: the best lcp tier only
+      sbuf[t] = c;
+      valid += c != ~0ull;
+    }
+    atomicAdd(&s_valid, valid);
+    __syncthreads();
+    for (int k2 = 2; k2 <= P; k2 <<= 1) {
+      for (int j = k2 >> 1; j > 0; j >>= 1) {
+        for (int i = threadIdx.x; i < P; i += MERGE_SORT_THREADS) {
+          const int ixj = i ^ j;
+          if (ixj > i) {
+            const u64 a = sbuf[i], b = sbuf[ixj];
+            if ((a > b) == ((i & k2) == 0)) {
+              sbuf[i] = b;
+              sbuf[ixj] = a;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    const int hits = min(take, s_valid);
+    for (int t = threadIdx.x; t < hits; t += MERGE_SORT_THREADS) {
+      const u64 c = sbuf[t];
+      out_ids[qi * out_stride + t] = (u32)(c & 0xffffffffull);
+      out_lcps[qi * out_stride + t] = (uint16_t)(L - (int)(c >> 32));
+    }
+    if (threadIdx.x == 0) out_hits[qi] = hits;
+    __syncthreads();
+  }
+}
+
 __global__ void k_encode(const u32* __restrict__ ids, const uint16_t* __restrict__ lcps,
                          const int* __restrict__ hits, int count, int k, int in_stride, int L,
                          long long id_offset, u64* __restrict__ cand) {

@@ -1506,11 +1506,29 @@ int lcp_merge_candidates(const uint64_t* cand, int32_t shards, int32_t count, in
                          uint16_t* lcps, int32_t* hits, void* stream) {
   if (count <= 0) return LCP_OK;
   if (shards < 1 || k < 1) return fail(LCP_ERR_INVALID_INPUT, "shards and k must be >= 1");
-  if (take < 0 || take > FAST_KMAX)
-    return fail(LCP_ERR_INVALID_INPUT, "merge supports take in [0, 32]");
-  k_merge<<<blocks_for((long long)count * 32, 256), 256, 0, (cudaStream_t)stream>>>(
-      (const u64*)cand, shards, count, k, (long long)count * k, k, take, length, strict, ids,
-      lcps, hits, std::max(1, take));
+  if (take < 0 || take > k)
+    return fail(LCP_ERR_INVALID_INPUT, "merge needs 0 <= take <= k");
+  if (take <= FAST_KMAX) {  // one warp per query
+    k_merge<<<blocks_for((long long)count * 32, 256), 256, 0, (cudaStream_t)stream>>>(
+        (const u64*)cand, shards, count, k, (long long)count * k, k, take, length, strict, ids,
+        lcps, hits, std::max(1, take));
+  } else {  // one CTA per query, shared-memory sort of all candidates
+    if ((long long)shards * k > MERGE_SORT_CAP)
+      return fail(LCP_ERR_INVALID_INPUT, "merge supports shards * k <= " + std::to_string(MERGE_SORT_CAP));
+    int P = 1;
+    while (P < shards * k) P <<= 1;
+    const size_t smem = (size_t)P * 8;
+    static bool attr = false;
+    if (!attr) {
+      LCP_CK(cudaFuncSetAttribute(k_merge_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  MERGE_SORT_CAP * 8));
+      attr = true;
+    }
+    const unsigned grid = (unsigned)std::min<long long>(count, 8ll * num_sms());
+    k_merge_sort<<<grid, MERGE_SORT_THREADS, smem, (cudaStream_t)stream>>>(
+        (const u64*)cand, shards, count, k, (long long)count * k, k, take, length, strict, ids,
+        lcps, hits, std::max(1, take));
+  }
   LCP_CK_LAUNCH();
   return LCP_OK;
 }

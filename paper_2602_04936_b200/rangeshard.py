@@ -258,8 +258,8 @@ class RangeShardedIndex:
         if k < 1:
             raise InvalidInputError(f"k must be >= 1, got {k}")
         take = max(0, min(int(k), self.n_total))
-        if take > 32:
-            raise InvalidInputError("sharded merge supports k <= 32")
+        if take * self.world > 8192:
+            raise InvalidInputError("sharded merge supports world * min(k, n) <= 8192")
         q = queries.to(self.device)
         count, L = int(q.shape[0]), self.length
         kk = max(1, take)

@@ -120,8 +120,8 @@ class ShardedIndex:
         if k < 1:
             raise InvalidInputError(f"k must be >= 1, got {k}")
         take = max(0, min(int(k), self.n_total))
-        if take > 32:
-            raise InvalidInputError("sharded merge supports k <= 32")
+        if take * self.world > 8192:
+            raise InvalidInputError("sharded merge supports world * min(k, n) <= 8192")
         count = int(queries.shape[0])
         b = self._buffers(count, k)
         st = torch.cuda.current_stream().cuda_stream

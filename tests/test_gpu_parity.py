@@ -281,7 +281,7 @@ def test_shard_encode_merge_kernels(gpu, oracle_lib):
     plan = ShardPlan(ds.n, world)
     shards = [NativeIndex(ds.items[lo:hi], 16, 4) for lo, hi in (plan.bounds(r) for r in range(world))]
     full = oracle_lib.OracleTrie(ds.items, 4)
-    for k in (1, 10, 32):
+    for k in (1, 10, 32, 33, 100):  # > 32: the CTA-per-query merge
         for mode in ("complete", "strict"):
             gathered = torch.empty((world, count, k), dtype=torch.int64, device="cuda")
             for r, sh in enumerate(shards):
@@ -524,7 +524,7 @@ def _range_gpu_worker(rank, world, port, backend):
             sh = RangeShardedIndex(ds.items[lo:hi], L, sigma, id_offset=lo)
             full = oracle.OracleTrie(ds.items, sigma)
             dq = torch.from_numpy(qs).cuda()
-            for k in (1, 10, 32):
+            for k in (1, 10, 32, 50):
                 for mode in ("complete", "strict"):
                     ids, lcps, hits = (t.cpu() for t in sh.query(dq, k, mode))
                     fids, flcps, fhits, _, _, _ = full.query_batch(qs, k, mode)

@@ -126,7 +126,7 @@ def _worker(rank, world, port, cfg):
 
 
 @pytest.mark.parametrize("world,cfg", [
-    (2, ("uniform", 3000, 12, 4, (1, 10, 32))),
+    (2, ("uniform", 3000, 12, 4, (1, 10, 32, 50))),
     (3, ("uniform", 2000, 8, 2, (5, 17))),
     (3, ("dups", 600, 6, 4, (1, 10, 32))),
     (2, ("skew", 1500, 10, 4, (10, 32))),
