@@ -1160,6 +1160,28 @@ int lcp_query(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries, i
     LCP_TRY(ws->aux.ensure((size_t)count * 16));
     ax = ws->aux.as<u64>();
   }
+  const long long need64 = mode == LCP_MODE_COMPLETE ? std::min<long long>(k, dv.n) : k;
+  if (dv.W == 1 && mode != LCP_MODE_TAL && k > FAST_KMAX && need64 <= 64) {
+    // 32 < need <= 64: warp per query with a two-slot top-k list
+    const long long sms = num_sms();
+    const long long wpc = std::min<long long>(32, std::max<long long>(1, (count + sms - 1) / sms));
+    const unsigned block = (unsigned)(wpc * 32);
+    const unsigned grid = (unsigned)std::min<long long>((count + wpc - 1) / wpc, 4ll * sms);
+    const size_t smem = 16 + (size_t)dv.smem_entries * 8;
+    if (dv.idbits < 32) {
+      if (mode == LCP_MODE_STRICT)
+        k_query_w1_k64<u32, 0><<<grid, block, smem, st>>>(dv, queries, count, k, out_stride, ids, lcps, hits, md, ax, ws->d_err);
+      else
+        k_query_w1_k64<u32, 1><<<grid, block, smem, st>>>(dv, queries, count, k, out_stride, ids, lcps, hits, md, ax, ws->d_err);
+    } else {
+      if (mode == LCP_MODE_STRICT)
+        k_query_w1_k64<u64, 0><<<grid, block, smem, st>>>(dv, queries, count, k, out_stride, ids, lcps, hits, md, ax, ws->d_err);
+      else
+        k_query_w1_k64<u64, 1><<<grid, block, smem, st>>>(dv, queries, count, k, out_stride, ids, lcps, hits, md, ax, ws->d_err);
+    }
+    LCP_CK_LAUNCH();
+    return LCP_OK;
+  }
   if (dv.W <= 8 && k <= FAST_KMAX) {
     if (dv.W == 1) launch_fast<1>(ix, queries, count, k, mode, out_stride, ids, lcps, hits, md, ax, ws->d_err, st, ws);
     else if (dv.W == 2) launch_fast<2>(ix, queries, count, k, mode, out_stride, ids, lcps, hits, md, ax, ws->d_err, st, ws);

@@ -643,6 +643,243 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, MODE == 2 ? 1 : 2)
 }
 
 // ---------------------------------------------------------------------------
+// strict / complete, 32 < need <= 64, W == 1: one warp per query with a
+// two-slot top-k list (lane i holds ranks i and i + 32).  Same search as
+// k_query_w1; the 160-key region [B-64, B+96) contains [pos-64, pos+64).
+// ---------------------------------------------------------------------------
+template <typename C>
+struct TopK64 {
+  C s0, s1, thr;
+  __device__ __forceinline__ void init() { s0 = s1 = thr = ~C(0); }
+  __device__ __forceinline__ void insert(C c, int need) {
+    const int lane = lane_id();
+    const int p = __popc(__ballot_sync(LCP_FULL_MASK, s0 < c)) + __popc(__ballot_sync(LCP_FULL_MASK, s1 < c));
+    const C up0 = __shfl_up_sync(LCP_FULL_MASK, s0, 1);
+    const C up1 = __shfl_up_sync(LCP_FULL_MASK, s1, 1);
+    const C top0 = __shfl_sync(LCP_FULL_MASK, s0, 31);
+    const int h = lane + 32;
+    const C n1 = h > p ? (lane == 0 ? top0 : up1) : (h == p ? c : s1);
+    const C n0 = lane > p ? up0 : (lane == p ? c : s0);
+    s0 = n0;
+    s1 = n1;
+    const int r = need - 1;
+    thr = __shfl_sync(LCP_FULL_MASK, r < 32 ? s0 : s1, r & 31);
+  }
+  // one candidate per lane (all-ones = none)
+  __device__ __forceinline__ void offer(C comp, int need) {
+    unsigned m = __ballot_sync(LCP_FULL_MASK, comp < thr);
+    while (m) {
+      const int src = __ffs(m) - 1;
+      m &= m - 1;
+      const C c = __shfl_sync(LCP_FULL_MASK, comp, src);
+      if (c < thr) insert(c, need);
+    }
+  }
+};
+
+// tier|id over sorted positions [a, b) through the id sketch (see tier_offer);
+// valid while the tier contributes at most 32 items (one sketch list each)
+template <typename C>
+__device__ __noinline__ TopK64<C> tier_offer64(const DevIndex& ix, long long a, long long b, C tier,
+                                              TopK64<C> lst, int need) {
+  auto positions = [&](long long x, long long y) {
+    for (long long base = x; base < y; base += 32) {
+      const long long i = base + lane_id();
+      lst.offer(i < y ? (tier | (C)__ldg(ix.order + i)) : ~C(0), need);
+    }
+  };
+  auto lists = [&](const u32* __restrict__ ls, long long x, long long y) {
+    for (long long base = x; base < y; base += 32) {
+      const long long blk = base + lane_id();
+      const u32 mn = blk < y ? __ldg(ls + blk * LCP_SK_LIST) : 0xffffffffu;
+      const C cm = mn == 0xffffffffu ? ~C(0) : (tier | (C)mn);
+      unsigned m = __ballot_sync(LCP_FULL_MASK, cm < lst.thr);
+      while (m) {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        if (__shfl_sync(LCP_FULL_MASK, cm, src) < lst.thr) {
+          const u32 v = __ldg(ls + (base + src) * LCP_SK_LIST + lane_id());
+          lst.offer(v == 0xffffffffu ? ~C(0) : (tier | (C)v), need);
+        }
+      }
+    }
+  };
+  long long A = (a + LCP_SK_BLOCK - 1) / LCP_SK_BLOCK, B = b / LCP_SK_BLOCK;
+  if (A >= B) {
+    positions(a, b);
+    return lst;
+  }
+  positions(a, A * LCP_SK_BLOCK);
+  positions(B * LCP_SK_BLOCK, b);
+  for (int j = 0;; ++j) {
+    const u32* ls = ix.sketch + ix.sk_off[j] * LCP_SK_LIST;
+    const long long A2 = (A + LCP_SK_FANOUT - 1) / LCP_SK_FANOUT, B2 = B / LCP_SK_FANOUT;
+    if (j + 1 >= ix.sk_levels || A2 >= B2) {
+      lists(ls, A, B);
+      return lst;
+    }
+    lists(ls, A, A2 * LCP_SK_FANOUT);
+    lists(ls, B2 * LCP_SK_FANOUT, B);
+    A = A2;
+    B = B2;
+  }
+}
+
+template <typename C, int MODE>
+__global__ void __launch_bounds__(QW_MAX_THREADS, 1)
+    k_query_w1_k64(const __grid_constant__ DevIndex ix, const uint16_t* __restrict__ queries,
+                   int count, int k, int stride, u32* __restrict__ out_ids,
+                   uint16_t* __restrict__ out_lcps, int* __restrict__ out_hits,
+                   uint16_t* __restrict__ out_md, u64* __restrict__ out_aux, int* __restrict__ err) {
+  // MODE: 0 strict, 1 complete
+  constexpr int T = 5;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  u64* bar = reinterpret_cast<u64*>(smem_raw);
+  u64* staged = reinterpret_cast<u64*>(smem_raw + 16);
+  stage_issue(ix, bar, staged);
+  const int lane = lane_id();
+  const int warp = threadIdx.x >> 5;
+  const int warps = blockDim.x >> 5;
+  const int n = (int)ix.n;
+  const int L = ix.L;
+  const int b = ix.b, lb = ix.lb;
+  const int idbits = ix.idbits;
+  const int need = MODE == 1 ? min(k, n) : k;
+  const u64* __restrict__ keys = ix.keys;
+  const u32* __restrict__ order = ix.order;
+  const bool has0 = lane < L, has1 = lane + 32 < L;
+  const int sh0 = 64 - b * (lane + 1), sh1 = 64 - b * (lane + 33);
+
+  for (int qi = blockIdx.x * warps + warp; qi < count; qi += gridDim.x * warps) {
+    const uint16_t* qrow = queries + (size_t)qi * L;
+    const u32 s0 = has0 ? qrow[lane] : 0u;
+    const u32 s1 = has1 ? qrow[lane + 32] : 0u;
+    const bool bad = (has0 && (int)s0 >= ix.sigma) || (has1 && (int)s1 >= ix.sigma);
+    const u64 v = (has0 ? (u64)s0 << sh0 : 0ull) | (has1 ? (u64)s1 << sh1 : 0ull);
+    const u64 q = ((u64)__reduce_or_sync(LCP_FULL_MASK, (u32)(v >> 32)) << 32) |
+                  (u64)__reduce_or_sync(LCP_FULL_MASK, (u32)v);
+    stage_wait(ix, bar);
+    if (__any_sync(LCP_FULL_MASK, bad)) {
+      if (lane == 0) {
+        atomicOr(err, 1);
+        out_hits[qi] = 0;
+        out_md[qi] = 0;
+        out_aux[2 * qi] = 0;
+        out_aux[2 * qi + 1] = 0;
+      }
+      continue;
+    }
+    int blk = 0;
+    if (ix.nlevels > 0) {
+      const int c0 = ix.smem_levels > 0 ? level_count(staged, 0, q) : level_count_g(ix.levels, 0, q);
+      if (c0 > 0) {
+        blk = c0 - 1;
+        int j = 1;
+#pragma unroll 1
+        for (; j < ix.smem_levels; ++j)
+          blk = blk * LCP_SEARCH_FANOUT + level_count(staged + (int)ix.level_off[j], blk, q) - 1;
+#pragma unroll 1
+        for (; j < ix.nlevels; ++j)
+          blk = blk * LCP_SEARCH_FANOUT + level_count_g(ix.levels + (int)ix.level_off[j], blk, q) - 1;
+      }
+    }
+    const int s = blk * LCP_LEAF_KEYS - 64;
+    int l[T];
+    u32 id[T];
+    int dmax = -1;
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const int i = s + t * 32 + lane;
+      const bool ok = (unsigned)i < (unsigned)n;
+      const int ic = min(max(i, 0), n - 1);
+      const u64 key = __ldg(keys + ic);
+      id[t] = __ldg(order + ic);
+      l[t] = ok ? min(__clzll((long long)(key ^ q)) >> lb, L) : -1;
+      dmax = max(dmax, l[t]);
+    }
+    dmax = (int)__reduce_max_sync(LCP_FULL_MASK, (unsigned)(dmax + 1)) - 1;
+    const int dstar = MODE == 0 ? dmax : window_dstar<T>(l, dmax, need);
+    TopK64<C> lst;
+    lst.init();
+    int cnt = 0, r0 = 32 * T, above = 0;
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const bool c = l[t] >= dstar;
+      const unsigned m = __ballot_sync(LCP_FULL_MASK, c);
+      cnt += __popc(m);
+      above += __popc(__ballot_sync(LCP_FULL_MASK, l[t] > dstar));
+      if (m && r0 == 32 * T) r0 = t * 32 + __ffs(m) - 1;
+      lst.offer(c ? make_comp<C>(l[t], id[t], L, idbits) : ~C(0), need);
+    }
+    const int first_valid = s < 0 ? -s : 0;
+    const int end = min(s + 32 * T, n);
+    long long rsize = cnt, rlo = s + r0;
+    // R(d*) past the region: outside it every item has lcp == d*
+    const C tier = make_comp<C>(dstar, 0u, L, idbits);
+    const bool sketch_ok = need - above <= LCP_SK_LIST;  // tier supplies <= 32 items
+    if (s > 0 && r0 == first_valid) {
+      long long e = s;
+      for (int chunk = 0;; ++chunk) {
+        if (chunk == EXT_SCAN_CHUNKS && sketch_ok) {
+          u64 qk1[1] = {q};
+          const long long r = dstar ? run_edge<1>(ix, qk1, dstar, e, -1) : 0;
+          lst = tier_offer64<C>(ix, r, e, tier, lst, need);
+          rsize += e - r;
+          rlo = r;
+          break;
+        }
+        const long long i = e - 32 + lane;
+        const int li = i >= 0 ? min(__clzll((long long)(__ldg(keys + i) ^ q)) >> lb, L) : -1;
+        const bool c = li >= dstar;
+        lst.offer(c ? make_comp<C>(li, __ldg(order + i), L, idbits) : ~C(0), need);
+        const unsigned m = __ballot_sync(LCP_FULL_MASK, c);
+        rsize += __popc(m);
+        if (m) rlo = e - 32 + (__ffs(m) - 1);
+        e -= 32;
+        if (!(m == LCP_FULL_MASK && e > 0)) break;
+      }
+    }
+    if (end < n && s + r0 + cnt == end) {
+      long long e = end;
+      for (int chunk = 0;; ++chunk) {
+        if (chunk == EXT_SCAN_CHUNKS && sketch_ok) {
+          u64 qk1[1] = {q};
+          const long long r = dstar ? run_edge<1>(ix, qk1, dstar, e - 1, n) + 1 : n;
+          lst = tier_offer64<C>(ix, e, r, tier, lst, need);
+          rsize += r - e;
+          break;
+        }
+        const long long i = e + lane;
+        const int li = i < n ? min(__clzll((long long)(__ldg(keys + i) ^ q)) >> lb, L) : -1;
+        const bool c = li >= dstar;
+        lst.offer(c ? make_comp<C>(li, __ldg(order + i), L, idbits) : ~C(0), need);
+        const unsigned m = __ballot_sync(LCP_FULL_MASK, c);
+        rsize += __popc(m);
+        e += 32;
+        if (!(m == LCP_FULL_MASK && e < n)) break;
+      }
+    }
+    const int take = (int)min((long long)need, rsize);
+    if (lane < take) {
+      const u64 w = widen_comp<C>(lst.s0, idbits);
+      out_ids[(size_t)qi * stride + lane] = (u32)(w & 0xffffffffull);
+      out_lcps[(size_t)qi * stride + lane] = (uint16_t)(L - (int)(w >> 32));
+    }
+    if (lane + 32 < take) {
+      const u64 w = widen_comp<C>(lst.s1, idbits);
+      out_ids[(size_t)qi * stride + lane + 32] = (u32)(w & 0xffffffffull);
+      out_lcps[(size_t)qi * stride + lane + 32] = (uint16_t)(L - (int)(w >> 32));
+    }
+    if (lane == 0) {
+      out_hits[qi] = take;
+      out_md[qi] = (uint16_t)dmax;
+      out_aux[2 * qi] = (u64)(u32)dmax | ((u64)(u32)dstar << 32);
+      out_aux[2 * qi + 1] = (u64)rsize | ((u64)rlo << 32);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // strict / complete, k <= 32, 2 <= W <= WMAX <= 8: one warp per query;
 // 64-ary search to pos, then the 64-key window [pos-32, pos+32).
 // ---------------------------------------------------------------------------
