@@ -48,6 +48,12 @@ __global__ void k_split_words(const u64* __restrict__ keys, long long n, int W,
   }
 }
 
+// first word of each W-word key (the W > 1 TAL sweep plane)
+__global__ void k_first_word(const u64* __restrict__ keys, long long n, int W, u64* __restrict__ w0) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) w0[i] = keys[i * W];
+}
+
 __global__ void k_iota(u32* __restrict__ v, long long n) {
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) v[i] = (u32)i;

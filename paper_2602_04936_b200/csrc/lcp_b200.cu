@@ -227,6 +227,7 @@ struct lcp_index {
   u64* levels = nullptr;
   long long* directory = nullptr;
   u32* sketch = nullptr;
+  u64* keys_w0 = nullptr;
   std::vector<long long> level_offset;  // cached trie level offsets
 };
 
@@ -281,6 +282,7 @@ int lcp_index_free(lcp_index* ix) {
   if (ix->levels) cudaFreeAsync(ix->levels, 0);
   if (ix->directory) cudaFreeAsync(ix->directory, 0);
   if (ix->sketch) cudaFreeAsync(ix->sketch, 0);
+  if (ix->keys_w0) cudaFreeAsync(ix->keys_w0, 0);
   cudaStreamSynchronize(0);
   delete ix;
   return LCP_OK;
@@ -482,6 +484,12 @@ static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, i
   phase("sketch");
   // TAL bucket structure — tal.py:42-82
   if (tal_depth >= 0) {
+    if (W > 1) {  // first-word plane of the sorted keys for the coalesced bucket sweep
+      LCP_TRY(dalloc(&ix->keys_w0, n, acct, st));
+      k_first_word<<<blocks_for(n, 256), 256, 0, st>>>(ix->keys, n, W, ix->keys_w0);
+      LCP_CK_LAUNCH();
+      dv.keys_w0 = ix->keys_w0;
+    }
     ix->tal_depth = tal_depth;
     long long buckets = 1;
     bool overflow = false;
@@ -1094,9 +1102,13 @@ static void launch_fast(const lcp_index* ix, const uint16_t* q, int count, int k
                         int* err, cudaStream_t st, lcp_workspace* ws) {
   const DevIndex& dv = ix->dv;
   if (mode == LCP_MODE_TAL && WMAX > 1) {
-    unsigned grid = (unsigned)std::min<long long>(count, 8ll * num_sms());
-    k_query_tal<WMAX><<<grid, QT_THREADS, 0, st>>>(dv, q, count, k, stride, ids, lcps, hits, md,
-                                                   aux, err);
+    const long long sms = num_sms();
+    const long long wpc = std::min<long long>(32, std::max<long long>(1, (count + sms - 1) / sms));
+    const unsigned block = (unsigned)(wpc * 32);
+    const unsigned grid = (unsigned)std::min<long long>((count + wpc - 1) / wpc, 4ll * sms);
+    const size_t smem = 16 + (size_t)dv.smem_entries * dv.W * 8;
+    k_query_warp_tal<WMAX><<<grid, block, smem, st>>>(dv, q, count, k, stride, ids, lcps, hits, md,
+                                                      aux, err);
   } else {
     // One query per warp; spread the batch evenly over the SMs with one CTA
     // per SM (so each SM stages the search levels once), up to 1024 threads;

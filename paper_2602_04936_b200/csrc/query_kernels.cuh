@@ -954,12 +954,6 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, 1)
   }
 }
 
-// ---------------------------------------------------------------------------
-// TAL, k <= 32, W <= WMAX <= 8: one CTA per query scans its prefix bucket.
-// ---------------------------------------------------------------------------
-constexpr int QT_THREADS = 256;
-constexpr int QT_WARPS = QT_THREADS / 32;
-
 // bucket [lo, hi) of the query's d-prefix: dense directory (tal.py:138-143)
 // or binary search on the packed d-prefixes (tal.py:124-136)
 __device__ __forceinline__ void tal_bucket(const DevIndex& ix, const u64* qk,
@@ -994,84 +988,130 @@ __device__ __forceinline__ void tal_bucket(const DevIndex& ix, const u64* qk,
   hi = a;
 }
 
+// ---------------------------------------------------------------------------
+// TAL, k <= 32, 2 <= W <= WMAX <= 8 (tal.py:116-194): one warp per query.
+// The answer is the complete-mode answer with need = k whenever the bucket
+// holds >= k items (then d* >= depth, so R(d*) lies inside the bucket);
+// smaller buckets are ranked whole.  symbols_compared = sum over the bucket of
+// min(lcp + 1, L) comes from a coalesced sweep of the sorted first-word plane;
+// only keys equal to q in the whole first word compare further words.
+// ---------------------------------------------------------------------------
 template <int WMAX>
-__global__ void __launch_bounds__(QT_THREADS)
-    k_query_tal(DevIndex ix, const uint16_t* __restrict__ queries, int count, int k, int stride,
-                u32* __restrict__ out_ids, uint16_t* __restrict__ out_lcps,
-                int* __restrict__ out_hits, uint16_t* __restrict__ out_md,
-                u64* __restrict__ out_aux, int* __restrict__ err) {
-  __shared__ u64 s_q[WMAX];
-  __shared__ long long s_lo, s_hi;
-  __shared__ int s_bad;
-  __shared__ u64 s_list[QT_WARPS][32];
-  __shared__ unsigned long long s_sym[QT_WARPS];
+__global__ void __launch_bounds__(QW_MAX_THREADS, 1)
+    k_query_warp_tal(const __grid_constant__ DevIndex ix, const uint16_t* __restrict__ queries,
+                     int count, int k, int stride, u32* __restrict__ out_ids,
+                     uint16_t* __restrict__ out_lcps, int* __restrict__ out_hits,
+                     uint16_t* __restrict__ out_md, u64* __restrict__ out_aux,
+                     int* __restrict__ err) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  u64* bar = reinterpret_cast<u64*>(smem_raw);
+  u64* staged = reinterpret_cast<u64*>(smem_raw + 16);
+  stage_levels(ix, bar, staged);
   const int lane = lane_id();
   const int warp = threadIdx.x >> 5;
-  const int L = ix.L;
-
-  for (long long qi = blockIdx.x; qi < count; qi += gridDim.x) {
-    const uint16_t* qrow = queries + qi * L;
-    if (warp == 0) {
-      u64 qk[WMAX];
-      bool ok = warp_pack_query<WMAX>(qrow, ix, qk);
-      if (lane == 0) {
-#pragma unroll
-        for (int w = 0; w < WMAX; ++w) s_q[w] = qk[w];
-        s_bad = !ok;
-        long long lo = 0, hi = 0;
-        if (ok) tal_bucket(ix, s_q, qrow, lo, hi);
-        s_lo = lo;
-        s_hi = hi;
-      }
-    }
-    __syncthreads();
+  const int warps = blockDim.x >> 5;
+  const long long n = ix.n;
+  const int L = ix.L, lb = ix.lb, W = ix.W;
+  const int depth = ix.tal_depth;
+  for (long long qi = (long long)blockIdx.x * warps + warp; qi < count;
+       qi += (long long)gridDim.x * warps) {
     u64 qk[WMAX];
-#pragma unroll
-    for (int w = 0; w < WMAX; ++w) qk[w] = s_q[w];
-    const long long lo = s_lo, hi = s_hi;
-    const bool bad = s_bad;
-
-    u64 slot = ~0ull, thr = ~0ull;
+    if (!warp_pack_query<WMAX>(queries + qi * L, ix, qk)) {
+      if (lane == 0) {
+        atomicOr(err, 1);
+        out_hits[qi] = 0;
+        out_md[qi] = 0;
+        out_aux[2 * qi] = 0;
+        out_aux[2 * qi + 1] = 0;
+      }
+      continue;
+    }
+    long long blo, bhi;
+    tal_bucket(ix, qk, queries + qi * L, blo, bhi);
+    // symbols_compared over the bucket
     unsigned long long sym = 0;
-    if (!bad) {
-      for (long long base = lo + warp * 32; base < hi; base += QT_THREADS) {
-        long long i = base + lane;
-        u64 comp = ~0ull;
-        if (i < hi) {
-          int l = key_lcp<WMAX>(ix.keys + i * ix.W, qk, ix);
-          sym += (unsigned long long)min(l + 1, L);
-          comp = make_composite(l, ix.order[i], L);
+    for (long long i0 = blo + lane; i0 < bhi; i0 += 128) {  // 4 independent loads per lane
+      u64 x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const long long i = i0 + 32 * u;
+        x[u] = i < bhi ? __ldg(ix.keys_w0 + i) ^ qk[0] : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const long long i = i0 + 32 * u;
+        if (i < bhi) {
+          const int li = x[u] ? (__clzll((long long)x[u]) >> lb) : lcp_at<WMAX>(ix, i, qk);
+          sym += (unsigned)min(li + 1, L);
         }
-        warp_offer(slot, thr, comp, k);
       }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) sym += __shfl_xor_sync(LCP_FULL_MASK, sym, o);
-    s_list[warp][lane] = slot;
-    if (lane == 0) s_sym[warp] = sym;
-    __syncthreads();
-    if (warp == 0) {
-      u64 fs = ~0ull, ft = ~0ull;
-      for (int w = 0; w < QT_WARPS; ++w) warp_offer(fs, ft, s_list[w][lane], k);
-      const long long size = hi - lo;
-      const int take = bad ? 0 : (int)min((long long)k, size);
-      if (lane < take) {
-        out_ids[qi * stride + lane] = (u32)(fs & 0xffffffffull);
-        out_lcps[qi * stride + lane] = (uint16_t)(L - (int)(fs >> 32));
+    const long long bs = bhi - blo;
+    if (bs < k) {  // the whole bucket (empty: no hits, nothing scanned, tal.py:168-171)
+      u64 cv = ~0ull;
+      if (lane < bs) cv = make_comp<u64>(lcp_at<WMAX>(ix, blo + lane, qk), ix.order[blo + lane], L, 32);
+      int rank = 0;
+      for (int jj = 0; jj < (int)bs; ++jj) rank += __shfl_sync(LCP_FULL_MASK, cv, jj) < cv;
+      if (lane < bs) {
+        out_ids[qi * stride + rank] = (u32)(cv & 0xffffffffull);
+        out_lcps[qi * stride + rank] = (uint16_t)(L - (int)(cv >> 32));
       }
       if (lane == 0) {
-        unsigned long long tot = 0;
-        for (int w = 0; w < QT_WARPS; ++w) tot += s_sym[w];
-        if (bad) atomicOr(err, 1);
-        out_hits[qi] = take;
-        out_md[qi] = (uint16_t)ix.tal_depth;
-        out_aux[2 * qi] = bad ? 0ull : (u64)size;
-        out_aux[2 * qi + 1] = bad ? 0ull : tot;
+        out_hits[qi] = (int)bs;
+        out_md[qi] = (uint16_t)depth;
+        out_aux[2 * qi] = (u64)bs;
+        out_aux[2 * qi + 1] = bs ? sym : 0ull;
       }
+      continue;
     }
-    __syncthreads();
+    // complete-mode answer with need = k (as k_query_warp)
+    const long long pos = warp_lower_bound<WMAX>(ix, staged, qk);
+    const long long s = pos - 32;
+    int l[2];
+    u32 id[2];
+    int dmax = -1;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const long long i = s + t * 32 + lane;
+      const bool ok = i >= 0 && i < n;
+      l[t] = ok ? lcp_at<WMAX>(ix, i, qk) : -1;
+      id[t] = ok ? ix.order[i] : 0u;
+      dmax = max(dmax, l[t]);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) dmax = max(dmax, __shfl_xor_sync(LCP_FULL_MASK, dmax, o));
+    const int dstar = window_dstar<2>(l, dmax, k);
+    u64 comp[2];
+    int cnt = 0, r0 = 64;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const bool c = l[t] >= dstar;
+      comp[t] = c ? make_comp<u64>(l[t], id[t], L, 32) : ~0ull;
+      const unsigned m = __ballot_sync(LCP_FULL_MASK, c);
+      cnt += __popc(m);
+      if (m && r0 == 64) r0 = t * 32 + __ffs(m) - 1;
+    }
+    u64 slot = sort_run<u64, 2>(comp, r0, cnt, k);
+    long long rsize = cnt, rlo = s + r0;
+    const long long first_valid = s < 0 ? -s : 0;
+    const long long end = min(s + 64, n);
+    extend_range<u64, WMAX>(ix, qk, dstar, k, s > 0 && r0 == first_valid, s, end < n && s + r0 + cnt == end,
+                            end, 32, slot, rsize, rlo);
+    if (lane < k) {
+      out_ids[qi * stride + lane] = (u32)(slot & 0xffffffffull);
+      out_lcps[qi * stride + lane] = (uint16_t)(L - (int)(slot >> 32));
+    }
+    if (lane == 0) {
+      out_hits[qi] = k;
+      out_md[qi] = (uint16_t)depth;
+      out_aux[2 * qi] = (u64)bs;
+      out_aux[2 * qi + 1] = sym;
+    }
   }
 }
+
 
 // ---------------------------------------------------------------------------
 // General path: any k, any W, all modes + full scan.  One CTA per query;
