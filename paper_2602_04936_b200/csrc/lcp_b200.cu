@@ -1172,25 +1172,26 @@ int lcp_query(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries, i
     LCP_TRY(ws->aux.ensure((size_t)count * 16));
     ax = ws->aux.as<u64>();
   }
-  const long long need64 = mode == LCP_MODE_COMPLETE ? std::min<long long>(k, dv.n) : k;
-  if (dv.W == 1 && mode != LCP_MODE_TAL && k > FAST_KMAX && need64 <= 64) {
-    // 32 < need <= 64: warp per query with a two-slot top-k list
+  const long long needk = mode == LCP_MODE_COMPLETE ? std::min<long long>(k, dv.n) : k;
+  if (dv.W == 1 && mode != LCP_MODE_TAL && k > FAST_KMAX && needk <= 128) {
+    // 32 < need <= 128: warp per query with a 2- or 4-slot top-k list
     const long long sms = num_sms();
-    const long long wpc = std::min<long long>(32, std::max<long long>(1, (count + sms - 1) / sms));
+    const long long wmax = needk <= 64 ? 32 : 16;  // 4-slot lists: 512-thread CTAs
+    const long long wpc = std::min<long long>(wmax, std::max<long long>(1, (count + sms - 1) / sms));
     const unsigned block = (unsigned)(wpc * 32);
-    const unsigned grid = (unsigned)std::min<long long>((count + wpc - 1) / wpc, 4ll * sms);
+    const unsigned grid = (unsigned)std::min<long long>((count + wpc - 1) / wpc, 8ll * sms);
     const size_t smem = 16 + (size_t)dv.smem_entries * 8;
+#define LCP_KN(C, M, NS) \
+  k_query_w1_kn<C, M, NS><<<grid, block, smem, st>>>(dv, queries, count, k, out_stride, ids, lcps, hits, md, ax, ws->d_err)
+    const bool strict = mode == LCP_MODE_STRICT;
     if (dv.idbits < 32) {
-      if (mode == LCP_MODE_STRICT)
-        k_query_w1_k64<u32, 0><<<grid, block, smem, st>>>(dv, queries, count, k, out_stride, ids, lcps, hits, md, ax, ws->d_err);
-      else
-        k_query_w1_k64<u32, 1><<<grid, block, smem, st>>>(dv, queries, count, k, out_stride, ids, lcps, hits, md, ax, ws->d_err);
+      if (needk <= 64) { if (strict) LCP_KN(u32, 0, 2); else LCP_KN(u32, 1, 2); }
+      else { if (strict) LCP_KN(u32, 0, 4); else LCP_KN(u32, 1, 4); }
     } else {
-      if (mode == LCP_MODE_STRICT)
-        k_query_w1_k64<u64, 0><<<grid, block, smem, st>>>(dv, queries, count, k, out_stride, ids, lcps, hits, md, ax, ws->d_err);
-      else
-        k_query_w1_k64<u64, 1><<<grid, block, smem, st>>>(dv, queries, count, k, out_stride, ids, lcps, hits, md, ax, ws->d_err);
+      if (needk <= 64) { if (strict) LCP_KN(u64, 0, 2); else LCP_KN(u64, 1, 2); }
+      else { if (strict) LCP_KN(u64, 0, 4); else LCP_KN(u64, 1, 4); }
     }
+#undef LCP_KN
     LCP_CK_LAUNCH();
     return LCP_OK;
   }

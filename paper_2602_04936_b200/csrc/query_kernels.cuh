@@ -325,18 +325,23 @@ __device__ __forceinline__ void write_result(long long qi, int stride, int take,
 template <int T>
 __device__ __forceinline__ int window_dstar(const int (&l)[T], int dmax, int need) {
   if (dmax <= 0) return 0;
+  // counts <= 32*T: four 8-bit fields while they fit, else two 16-bit fields
+  constexpr int FB = 32 * T < 256 ? 8 : 16;
+  constexpr int NL = 32 / FB;
+  constexpr u32 FM = (1u << FB) - 1u;
   u32 mine = 0;
 #pragma unroll
-  for (int t = 0; t < T; ++t)
-    mine += (u32)(l[t] >= dmax) | ((u32)(l[t] >= dmax - 1) << 8) | ((u32)(l[t] >= dmax - 2) << 16) |
-            ((u32)(l[t] >= dmax - 3) << 24);
+  for (int t = 0; t < T; ++t) {
+#pragma unroll
+    for (int c = 0; c < NL; ++c) mine += (u32)(l[t] >= dmax - c) << (FB * c);
+  }
   const u32 tot = __reduce_add_sync(LCP_FULL_MASK, mine);
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
+  for (int c = 0; c < NL; ++c) {
     if (dmax - c < 0) return 0;
-    if ((int)((tot >> (8 * c)) & 0xffu) >= need) return dmax - c;
+    if ((int)((tot >> (FB * c)) & FM) >= need) return dmax - c;
   }
-  int lo = 0, hi = dmax - 4;  // every level above failed
+  int lo = 0, hi = dmax - NL;  // every level above failed
   if (hi <= 0) return 0;
   while (lo < hi) {
     int mid = (lo + hi + 1) >> 1;
@@ -643,27 +648,41 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, MODE == 2 ? 1 : 2)
 }
 
 // ---------------------------------------------------------------------------
-// strict / complete, 32 < need <= 64, W == 1: one warp per query with a
-// two-slot top-k list (lane i holds ranks i and i + 32).  Same search as
-// k_query_w1; the 160-key region [B-64, B+96) contains [pos-64, pos+64).
+// strict / complete, 32 < need <= 32 * NS (NS = 2 or 4), W == 1: one warp
+// per query with an NS-slot top-k list (lane i holds ranks i, i + 32, ...).
+// Same search as k_query_w1; the region [B - 32 NS, B + 32 + 32 NS) contains
+// [pos - 32 NS, pos + 32 NS).
 // ---------------------------------------------------------------------------
-template <typename C>
-struct TopK64 {
-  C s0, s1, thr;
-  __device__ __forceinline__ void init() { s0 = s1 = thr = ~C(0); }
+template <typename C, int NS>
+struct TopKN {
+  C s[NS];  // s[j] on lane i holds rank 32 * j + i
+  C thr;
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int j = 0; j < NS; ++j) s[j] = ~C(0);
+    thr = ~C(0);
+  }
   __device__ __forceinline__ void insert(C c, int need) {
     const int lane = lane_id();
-    const int p = __popc(__ballot_sync(LCP_FULL_MASK, s0 < c)) + __popc(__ballot_sync(LCP_FULL_MASK, s1 < c));
-    const C up0 = __shfl_up_sync(LCP_FULL_MASK, s0, 1);
-    const C up1 = __shfl_up_sync(LCP_FULL_MASK, s1, 1);
-    const C top0 = __shfl_sync(LCP_FULL_MASK, s0, 31);
-    const int h = lane + 32;
-    const C n1 = h > p ? (lane == 0 ? top0 : up1) : (h == p ? c : s1);
-    const C n0 = lane > p ? up0 : (lane == p ? c : s0);
-    s0 = n0;
-    s1 = n1;
+    int p = 0;
+#pragma unroll
+    for (int j = 0; j < NS; ++j) p += __popc(__ballot_sync(LCP_FULL_MASK, s[j] < c));
+    C top[NS];
+#pragma unroll
+    for (int j = 0; j < NS; ++j) top[j] = __shfl_sync(LCP_FULL_MASK, s[j], 31);
+#pragma unroll
+    for (int j = NS - 1; j >= 0; --j) {
+      const C up = __shfl_up_sync(LCP_FULL_MASK, s[j], 1);
+      const int h = lane + 32 * j;
+      const C prev = lane == 0 ? (j > 0 ? top[j > 0 ? j - 1 : 0] : s[j]) : up;
+      s[j] = h > p ? prev : (h == p ? c : s[j]);
+    }
     const int r = need - 1;
-    thr = __shfl_sync(LCP_FULL_MASK, r < 32 ? s0 : s1, r & 31);
+    C sel = s[0];
+#pragma unroll
+    for (int j = 1; j < NS; ++j)
+      if ((r >> 5) == j) sel = s[j];
+    thr = __shfl_sync(LCP_FULL_MASK, sel, r & 31);
   }
   // one candidate per lane (all-ones = none)
   __device__ __forceinline__ void offer(C comp, int need) {
@@ -679,9 +698,9 @@ struct TopK64 {
 
 // tier|id over sorted positions [a, b) through the id sketch (see tier_offer);
 // valid while the tier contributes at most 32 items (one sketch list each)
-template <typename C>
-__device__ __noinline__ TopK64<C> tier_offer64(const DevIndex& ix, long long a, long long b, C tier,
-                                              TopK64<C> lst, int need) {
+template <typename C, int NS>
+__device__ __noinline__ TopKN<C, NS> tier_offer_n(const DevIndex& ix, long long a, long long b, C tier,
+                                                 TopKN<C, NS> lst, int need) {
   auto positions = [&](long long x, long long y) {
     for (long long base = x; base < y; base += 32) {
       const long long i = base + lane_id();
@@ -725,14 +744,14 @@ __device__ __noinline__ TopK64<C> tier_offer64(const DevIndex& ix, long long a, 
   }
 }
 
-template <typename C, int MODE>
-__global__ void __launch_bounds__(QW_MAX_THREADS, 1)
-    k_query_w1_k64(const __grid_constant__ DevIndex ix, const uint16_t* __restrict__ queries,
+template <typename C, int MODE, int NS>
+__global__ void __launch_bounds__(NS > 2 ? QW_MAX_THREADS / 2 : QW_MAX_THREADS, 1)  // NS=4: 128 regs
+    k_query_w1_kn(const __grid_constant__ DevIndex ix, const uint16_t* __restrict__ queries,
                    int count, int k, int stride, u32* __restrict__ out_ids,
                    uint16_t* __restrict__ out_lcps, int* __restrict__ out_hits,
                    uint16_t* __restrict__ out_md, u64* __restrict__ out_aux, int* __restrict__ err) {
-  // MODE: 0 strict, 1 complete
-  constexpr int T = 5;
+  // MODE: 0 strict, 1 complete; need <= 32 * NS; region 32 * (2 NS + 1) keys
+  constexpr int T = 2 * NS + 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   u64* bar = reinterpret_cast<u64*>(smem_raw);
   u64* staged = reinterpret_cast<u64*>(smem_raw + 16);
@@ -783,7 +802,7 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, 1)
           blk = blk * LCP_SEARCH_FANOUT + level_count_g(ix.levels + (int)ix.level_off[j], blk, q) - 1;
       }
     }
-    const int s = blk * LCP_LEAF_KEYS - 64;
+    const int s = blk * LCP_LEAF_KEYS - 32 * NS;
     int l[T];
     u32 id[T];
     int dmax = -1;
@@ -799,7 +818,7 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, 1)
     }
     dmax = (int)__reduce_max_sync(LCP_FULL_MASK, (unsigned)(dmax + 1)) - 1;
     const int dstar = MODE == 0 ? dmax : window_dstar<T>(l, dmax, need);
-    TopK64<C> lst;
+    TopKN<C, NS> lst;
     lst.init();
     int cnt = 0, r0 = 32 * T, above = 0;
 #pragma unroll
@@ -823,7 +842,7 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, 1)
         if (chunk == EXT_SCAN_CHUNKS && sketch_ok) {
           u64 qk1[1] = {q};
           const long long r = dstar ? run_edge<1>(ix, qk1, dstar, e, -1) : 0;
-          lst = tier_offer64<C>(ix, r, e, tier, lst, need);
+          lst = tier_offer_n<C, NS>(ix, r, e, tier, lst, need);
           rsize += e - r;
           rlo = r;
           break;
@@ -845,7 +864,7 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, 1)
         if (chunk == EXT_SCAN_CHUNKS && sketch_ok) {
           u64 qk1[1] = {q};
           const long long r = dstar ? run_edge<1>(ix, qk1, dstar, e - 1, n) + 1 : n;
-          lst = tier_offer64<C>(ix, e, r, tier, lst, need);
+          lst = tier_offer_n<C, NS>(ix, e, r, tier, lst, need);
           rsize += r - e;
           break;
         }
@@ -860,15 +879,13 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, 1)
       }
     }
     const int take = (int)min((long long)need, rsize);
-    if (lane < take) {
-      const u64 w = widen_comp<C>(lst.s0, idbits);
-      out_ids[(size_t)qi * stride + lane] = (u32)(w & 0xffffffffull);
-      out_lcps[(size_t)qi * stride + lane] = (uint16_t)(L - (int)(w >> 32));
-    }
-    if (lane + 32 < take) {
-      const u64 w = widen_comp<C>(lst.s1, idbits);
-      out_ids[(size_t)qi * stride + lane + 32] = (u32)(w & 0xffffffffull);
-      out_lcps[(size_t)qi * stride + lane + 32] = (uint16_t)(L - (int)(w >> 32));
+#pragma unroll
+    for (int j = 0; j < NS; ++j) {
+      if (lane + 32 * j < take) {
+        const u64 w = widen_comp<C>(lst.s[j], idbits);
+        out_ids[(size_t)qi * stride + lane + 32 * j] = (u32)(w & 0xffffffffull);
+        out_lcps[(size_t)qi * stride + lane + 32 * j] = (uint16_t)(L - (int)(w >> 32));
+      }
     }
     if (lane == 0) {
       out_hits[qi] = take;

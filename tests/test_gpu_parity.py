@@ -464,7 +464,7 @@ def test_long_runs_vs_oracle(gpu, oracle_lib, wide, monkeypatch):
     for name, ds, qs in _long_run_cases():
         idx = lg.build(ds)
         ot = oracle_lib.OracleTrie(ds.items, ds.alphabet.size)
-        for k in (1, 10, 16, 17, 32, 33, 48, 64):
+        for k in (1, 10, 16, 17, 32, 33, 48, 64, 100, 128):
             for mode in ("complete", "strict"):
                 b = idx.query_batch(qs, k, mode)
                 ids, lcps, hits, md, sym, nodes = ot.query_batch(qs, k, mode)
