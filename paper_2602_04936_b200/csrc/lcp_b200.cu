@@ -70,9 +70,10 @@ unsigned blocks_for(long long work, int threads) {
   return (unsigned)std::max(1ll, b);
 }
 
-// Index memory comes from the device's stream-ordered pool, which keeps freed
-// memory mapped (release threshold = max): rebuilding an index reuses it
-// instead of unmapping and remapping hundreds of MB through the driver.
+// Index memory comes from the device's stream-ordered pool, which keeps up to
+// min(8 GB, 10 % of HBM) of freed memory mapped: rebuilding an index reuses it
+// instead of unmapping and remapping hundreds of MB through the driver, while
+// larger frees still return memory for other allocators (e.g. PyTorch's).
 void keep_pool_mapped() {
   static std::mutex mu;
   static std::vector<int> done;
@@ -82,7 +83,9 @@ void keep_pool_mapped() {
   if (std::find(done.begin(), done.end(), dev) != done.end()) return;
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    unsigned long long thr = ~0ull;
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    unsigned long long thr = std::min<unsigned long long>(8ull << 30, total_b / 10);
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
   cudaGetLastError();
