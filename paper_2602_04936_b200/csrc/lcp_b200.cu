@@ -129,13 +129,12 @@ struct DBuf {
 };
 
 int num_sms() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
+  static const int sms = [] {  // thread-safe one-time initialisation
+    int dev = 0, v = 0;
     cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
-      sms = 148;
-  }
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    return v;
+  }();
   return sms;
 }
 
@@ -1069,12 +1068,12 @@ __global__ void k_fill_empty(int count, int md, int* hits, uint16_t* out_md, u64
 // preferred L1 / shared split, set once per kernel (the static is per kernel)
 template <auto Kernel>
 static void prefer_carveout(int pct) {
-  static bool done = false;
-  if (!done) {
+  static const bool done = [pct] {  // thread-safe one-time initialisation
     cudaFuncSetAttribute(Kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
     cudaGetLastError();
-    done = true;
-  }
+    return true;
+  }();
+  (void)done;
 }
 
 template <typename C, int T>
@@ -1405,12 +1404,9 @@ static int launch_fullscan_w1_k(const DevIndex& dv, const uint16_t* q, const u64
                                 int need, long long chunk, int nchunks, u64* partial, int* hint,
                                 int* err, cudaStream_t st) {
   const size_t smem = 16 + 2 * 2 * FS1_STAGE_KEYS * 4;  // 2 stages x (hi + lo) planes
-  static bool attr = false;
-  if (!attr) {
-    LCP_CK(cudaFuncSetAttribute(k_fullscan_w1<C, KCAP>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  static const cudaError_t attr = cudaFuncSetAttribute(  // thread-safe one-time initialisation
+      k_fullscan_w1<C, KCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  LCP_CK(attr);
   dim3 grid((count + FS_THREADS - 1) / FS_THREADS, nchunks);
   k_fullscan_w1<C, KCAP><<<grid, FS_THREADS, smem, st>>>(dv, q, qkeys, count, need, chunk, nchunks,
                                                          partial, hint, err);
@@ -1556,12 +1552,9 @@ int lcp_merge_candidates(const uint64_t* cand, int32_t shards, int32_t count, in
     int P = 1;
     while (P < shards * k) P <<= 1;
     const size_t smem = (size_t)P * 8;
-    static bool attr = false;
-    if (!attr) {
-      LCP_CK(cudaFuncSetAttribute(k_merge_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  MERGE_SORT_CAP * 8));
-      attr = true;
-    }
+    static const cudaError_t attr = cudaFuncSetAttribute(  // thread-safe one-time initialisation
+        k_merge_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, MERGE_SORT_CAP * 8);
+    LCP_CK(attr);
     const unsigned grid = (unsigned)std::min<long long>(count, 8ll * num_sms());
     k_merge_sort<<<grid, MERGE_SORT_THREADS, smem, (cudaStream_t)stream>>>(
         (const u64*)cand, shards, count, k, (long long)count * k, k, take, length, strict, ids,
