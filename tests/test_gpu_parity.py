@@ -581,3 +581,27 @@ def test_concurrent_readers(gpu):
     for th in threads:
         th.join()
     assert not errors, errors
+
+
+@pytest.mark.parametrize("L,sigma", [(1000, 3), (4096, 2)])
+def test_long_keys_vs_oracle(gpu, oracle_lib, L, sigma):
+    """Very long keys (W = 32..64 words): search tables no longer fit shared
+    memory, the general kernel and the full scan's multi-word path run."""
+    ds = lg.generate_dataset(600, L, sigma, seed=L)
+    idx = lg.build(ds)
+    ot = oracle_lib.OracleTrie(ds.items, sigma)
+    qs = np.vstack([lg.generate_queries(ds, 20, seed=L + 1), lg.generate_queries(ds, 20, seed=L + 2, prefix_len=L // 2)])
+    # near-duplicates: share all but the last symbol with a corpus row
+    near = ds.items[:10].copy()
+    near[:, -1] = (near[:, -1] + 1) % sigma
+    qs = np.vstack([qs, near])
+    for k in (1, 10, 33):
+        for mode in ("complete", "strict"):
+            b = idx.query_batch(qs, k, mode)
+            ids, lcps, hits, md, _, _ = ot.query_batch(qs, k, mode)
+            for i in range(len(qs)):
+                assert b.pairs(i) == list(zip(ids[i, :hits[i]].tolist(), lcps[i, :hits[i]].tolist())), (k, mode, i)
+        f = idx.fullscan_batch(qs, k)
+        oid, olcp, oh = oracle_lib.oracle_top_k_batch(ds.items, qs, k)
+        for i in range(len(qs)):
+            assert f.pairs(i) == list(zip(oid[i, :oh[i]].tolist(), olcp[i, :oh[i]].tolist()))
