@@ -148,6 +148,8 @@ int lcp_query_host(const lcp_index* index, lcp_workspace* ws, const uint16_t* qu
 typedef struct lcp_packed_layout {
   int64_t ids, lcps, hits, matched_depth, aux; /* byte offsets */
   int64_t total;                               /* block size in bytes */
+  int64_t err; /* byte offset of the int32 invalid-query flag (between hits and
+                  matched_depth, so the LCP_PACKED_NO_WORK copy carries it) */
 } lcp_packed_layout;
 int lcp_packed_layout_for(int32_t count, int32_t out_stride, lcp_packed_layout* layout);
 int lcp_query_host_packed(const lcp_index* index, lcp_workspace* ws, const uint16_t* queries,

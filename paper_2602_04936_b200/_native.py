@@ -53,7 +53,7 @@ class IndexInfo(ctypes.Structure):
 class PackedLayout(ctypes.Structure):
     _fields_ = [("ids", ctypes.c_int64), ("lcps", ctypes.c_int64), ("hits", ctypes.c_int64),
                 ("matched_depth", ctypes.c_int64), ("aux", ctypes.c_int64),
-                ("total", ctypes.c_int64)]
+                ("total", ctypes.c_int64), ("err", ctypes.c_int64)]
 
 
 _P = ctypes.c_void_p

@@ -259,6 +259,7 @@ struct lcp_workspace {
   cudaEvent_t done = nullptr;  // completion of the in-flight async batch
   bool pending = false;
   int pending_sigma = 0;
+  const int* pending_err = nullptr;  // host flag inside the in-flight packed block
   int* d_err = nullptr;
   int* h_err = nullptr;  // pinned
   DBuf qkeys, partial, hint, q_in, ids, lcps, hits, md, aux;
@@ -1139,9 +1140,14 @@ static void launch_fast(const lcp_index* ix, const uint16_t* q, int count, int k
 
 extern "C" {
 
-int lcp_query(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries, int32_t count,
-              int32_t k, int32_t mode, int32_t out_stride, uint32_t* ids, uint16_t* lcps,
-              int32_t* hits, uint16_t* matched_depth, uint64_t* aux, void* stream) {
+}  // extern "C"
+
+// lcp_query's body; `errp` is the device int the kernels raise on an invalid
+// query symbol (the workspace's flag, or a slot of a packed output block)
+static int query_impl(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries,
+                      int32_t count, int32_t k, int32_t mode, int32_t out_stride, uint32_t* ids,
+                      uint16_t* lcps, int32_t* hits, uint16_t* matched_depth, uint64_t* aux,
+                      void* stream, int* errp) {
   if (!ix || !ws) return fail(LCP_ERR_INVALID_INPUT, "null index or workspace");
   if (k < 1) return fail(LCP_ERR_INVALID_INPUT, "k must be >= 1, got " + std::to_string(k));
   if (mode < 0 || mode > 2)
@@ -1184,7 +1190,7 @@ int lcp_query(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries, i
     const unsigned grid = (unsigned)std::min<long long>((count + wpc - 1) / wpc, 8ll * sms);
     const size_t smem = 16 + (size_t)dv.smem_entries * 8;
 #define LCP_KN(C, M, NS) \
-  k_query_w1_kn<C, M, NS><<<grid, block, smem, st>>>(dv, queries, count, k, out_stride, ids, lcps, hits, md, ax, ws->d_err)
+  k_query_w1_kn<C, M, NS><<<grid, block, smem, st>>>(dv, queries, count, k, out_stride, ids, lcps, hits, md, ax, errp)
     const bool strict = mode == LCP_MODE_STRICT;
     if (dv.idbits < 32) {
       if (needk <= 64) { if (strict) LCP_KN(u32, 0, 2); else LCP_KN(u32, 1, 2); }
@@ -1198,22 +1204,32 @@ int lcp_query(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries, i
     return LCP_OK;
   }
   if (dv.W <= 8 && k <= FAST_KMAX) {
-    if (dv.W == 1) launch_fast<1>(ix, queries, count, k, mode, out_stride, ids, lcps, hits, md, ax, ws->d_err, st, ws);
-    else if (dv.W == 2) launch_fast<2>(ix, queries, count, k, mode, out_stride, ids, lcps, hits, md, ax, ws->d_err, st, ws);
-    else if (dv.W <= 4) launch_fast<4>(ix, queries, count, k, mode, out_stride, ids, lcps, hits, md, ax, ws->d_err, st, ws);
-    else launch_fast<8>(ix, queries, count, k, mode, out_stride, ids, lcps, hits, md, ax, ws->d_err, st, ws);
+    if (dv.W == 1) launch_fast<1>(ix, queries, count, k, mode, out_stride, ids, lcps, hits, md, ax, errp, st, ws);
+    else if (dv.W == 2) launch_fast<2>(ix, queries, count, k, mode, out_stride, ids, lcps, hits, md, ax, errp, st, ws);
+    else if (dv.W <= 4) launch_fast<4>(ix, queries, count, k, mode, out_stride, ids, lcps, hits, md, ax, errp, st, ws);
+    else launch_fast<8>(ix, queries, count, k, mode, out_stride, ids, lcps, hits, md, ax, errp, st, ws);
     LCP_CK_LAUNCH();
     return LCP_OK;
   }
   LCP_TRY(ws->qkeys.ensure((size_t)count * dv.W * 8));
   k_pack<<<blocks_for((long long)count * dv.W, 256), 256, 0, st>>>(
-      queries, count, dv.L, dv.W, dv.b, dv.spw, dv.sigma, ws->qkeys.as<u64>(), nullptr, ws->d_err);
+      queries, count, dv.L, dv.W, dv.b, dv.spw, dv.sigma, ws->qkeys.as<u64>(), nullptr, errp);
   LCP_CK_LAUNCH();
   unsigned grid = (unsigned)std::min<long long>(count, 8ll * num_sms());
   k_query_general<<<grid, GEN_THREADS, 0, st>>>(dv, ws->qkeys.as<u64>(), queries, count, k, mode,
                                                 0, out_stride, ids, lcps, hits, md, ax);
   LCP_CK_LAUNCH();
   return LCP_OK;
+}
+
+extern "C" {
+
+int lcp_query(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries, int32_t count,
+              int32_t k, int32_t mode, int32_t out_stride, uint32_t* ids, uint16_t* lcps,
+              int32_t* hits, uint16_t* matched_depth, uint64_t* aux, void* stream) {
+  if (!ws) return fail(LCP_ERR_INVALID_INPUT, "null index or workspace");
+  return query_impl(ix, ws, queries, count, k, mode, out_stride, ids, lcps, hits, matched_depth,
+                    aux, stream, ws->d_err);
 }
 
 static int host_finish(lcp_workspace* ws) {
@@ -1266,7 +1282,8 @@ static lcp_packed_layout packed_layout(long long count, long long stride) {
   l.ids = 0;
   l.lcps = up8(count * stride * 4);
   l.hits = up8(l.lcps + count * stride * 2);
-  l.matched_depth = up8(l.hits + count * 4);
+  l.err = up8(l.hits + count * 4);  // rides in the same D2H copy as the results
+  l.matched_depth = l.err + 8;
   l.aux = up8(l.matched_depth + count * 2);
   l.total = l.aux + count * 16;
   return l;
@@ -1293,14 +1310,16 @@ int lcp_query_host_packed(const lcp_index* ix, lcp_workspace* ws, const uint16_t
   LCP_TRY(ws->ids.ensure((size_t)lay.total));  // device mirror of the packed block
   char* d = static_cast<char*>(ws->ids.p);
   LCP_CK(cudaMemcpyAsync(ws->q_in.p, queries, qb, cudaMemcpyHostToDevice, st));
-  LCP_TRY(lcp_query(ix, ws, ws->q_in.as<uint16_t>(), count, k, mode, out_stride,
-                    reinterpret_cast<uint32_t*>(d + lay.ids),
-                    reinterpret_cast<uint16_t*>(d + lay.lcps),
-                    reinterpret_cast<int32_t*>(d + lay.hits),
-                    reinterpret_cast<uint16_t*>(d + lay.matched_depth),
-                    reinterpret_cast<uint64_t*>(d + lay.aux), st));
+  LCP_CK(cudaMemsetAsync(d + lay.err, 0, 8, st));
+  LCP_TRY(query_impl(ix, ws, ws->q_in.as<uint16_t>(), count, k, mode, out_stride,
+                     reinterpret_cast<uint32_t*>(d + lay.ids),
+                     reinterpret_cast<uint16_t*>(d + lay.lcps),
+                     reinterpret_cast<int32_t*>(d + lay.hits),
+                     reinterpret_cast<uint16_t*>(d + lay.matched_depth),
+                     reinterpret_cast<uint64_t*>(d + lay.aux), st, reinterpret_cast<int*>(d + lay.err)));
   LCP_CK(cudaMemcpyAsync(out_block, d, (size_t)lay.total, cudaMemcpyDeviceToHost, st));
-  if (host_finish(ws) != LCP_OK)
+  LCP_CK(cudaStreamSynchronize(st));
+  if (*reinterpret_cast<const int*>(static_cast<const char*>(out_block) + lay.err))
     return fail(LCP_ERR_INVALID_INPUT,
                 "query symbol out of range for alphabet of size " + std::to_string(dv.sigma));
   return LCP_OK;
@@ -1329,6 +1348,7 @@ int lcp_query_host_packed_async(const lcp_index* ix, lcp_workspace* ws, const ui
       LCP_CK(cudaEventRecord(ws->done, st));
       ws->pending = true;
       ws->pending_sigma = dv.sigma;
+      ws->pending_err = reinterpret_cast<const int*>(static_cast<const char*>(out_block) + lay.err);
       return LCP_OK;
     }
   }
@@ -1337,16 +1357,18 @@ int lcp_query_host_packed_async(const lcp_index* ix, lcp_workspace* ws, const ui
   LCP_TRY(ws->ids.ensure((size_t)lay.total));
   LCP_TRY(ws->qkeys.ensure((size_t)count * dv.W * 8));
   char* d = static_cast<char*>(ws->ids.p);
+  // one H2D, the kernel, one D2H: the invalid-query flag lives in the block
+  // (lay.err), cleared on the device, so no separate small copy is needed
   auto enqueue = [&]() -> int {
     LCP_CK(cudaMemcpyAsync(ws->q_in.p, queries, qb, cudaMemcpyHostToDevice, st));
-    LCP_TRY(lcp_query(ix, ws, ws->q_in.as<uint16_t>(), count, k, mode, out_stride,
-                      reinterpret_cast<uint32_t*>(d + lay.ids),
-                      reinterpret_cast<uint16_t*>(d + lay.lcps),
-                      reinterpret_cast<int32_t*>(d + lay.hits),
-                      reinterpret_cast<uint16_t*>(d + lay.matched_depth),
-                      reinterpret_cast<uint64_t*>(d + lay.aux), st));
+    LCP_CK(cudaMemsetAsync(d + lay.err, 0, 8, st));
+    LCP_TRY(query_impl(ix, ws, ws->q_in.as<uint16_t>(), count, k, mode, out_stride,
+                       reinterpret_cast<uint32_t*>(d + lay.ids),
+                       reinterpret_cast<uint16_t*>(d + lay.lcps),
+                       reinterpret_cast<int32_t*>(d + lay.hits),
+                       reinterpret_cast<uint16_t*>(d + lay.matched_depth),
+                       reinterpret_cast<uint64_t*>(d + lay.aux), st, reinterpret_cast<int*>(d + lay.err)));
     LCP_CK(cudaMemcpyAsync(out_block, d, d2h, cudaMemcpyDeviceToHost, st));
-    LCP_CK(cudaMemcpyAsync(ws->h_err, ws->d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
     return LCP_OK;
   };
   cudaGraph_t graph = nullptr;
@@ -1378,6 +1400,7 @@ int lcp_query_host_packed_async(const lcp_index* ix, lcp_workspace* ws, const ui
   LCP_CK(cudaEventRecord(ws->done, st));
   ws->pending = true;
   ws->pending_sigma = dv.sigma;
+  ws->pending_err = reinterpret_cast<const int*>(static_cast<const char*>(out_block) + lay.err);
   return LCP_OK;
 }
 
@@ -1386,13 +1409,11 @@ int lcp_workspace_wait(lcp_workspace* ws) {
   if (!ws->pending) return LCP_OK;
   ws->pending = false;
   LCP_CK(cudaEventSynchronize(ws->done));
-  if (*ws->h_err) {
-    *ws->h_err = 0;
-    LCP_CK(cudaMemsetAsync(ws->d_err, 0, sizeof(int), ws->stream));
-    LCP_CK(cudaStreamSynchronize(ws->stream));
+  const int* e = ws->pending_err;
+  ws->pending_err = nullptr;
+  if (e && *e)
     return fail(LCP_ERR_INVALID_INPUT, "query symbol out of range for alphabet of size " +
                                            std::to_string(ws->pending_sigma));
-  }
   return LCP_OK;
 }
 

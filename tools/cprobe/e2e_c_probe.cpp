@@ -100,6 +100,59 @@ int main() {
     cudaEventElapsedTime(&m2, a, b2);
     printf("concurrent H2D 256K + D2H 264K: %.2f / %.2f us per pair\n", m1, m2);
   }
+  // aggregate PCIe with S streams, each doing H2D 256 KB + D2H 264 KB per step
+  for (int S : {1, 2, 4, 8}) {
+    std::vector<cudaStream_t> ss(S);
+    std::vector<void*> hs(S), ds(S), ho(S), dout(S);
+    for (int i = 0; i < S; ++i) {
+      cudaStreamCreateWithFlags(&ss[i], cudaStreamNonBlocking);
+      cudaMallocHost(&hs[i], 262144);
+      cudaMallocHost(&ho[i], 270336);
+      cudaMalloc(&ds[i], 262144);
+      cudaMalloc(&dout[i], 270336);
+    }
+    cudaDeviceSynchronize();
+    const int steps = 2000;
+    double t0 = now_us();
+    for (int i = 0; i < steps; ++i) {
+      const int j = i % S;
+      cudaMemcpyAsync(ds[j], hs[j], 262144, cudaMemcpyHostToDevice, ss[j]);
+      cudaMemcpyAsync(ho[j], dout[j], 270336, cudaMemcpyDeviceToHost, ss[j]);
+    }
+    cudaDeviceSynchronize();
+    double el = now_us() - t0;
+    printf("%d streams: %.2f us per (H2D 256K + D2H 264K) step, %.1f GB/s combined\n", S, el / steps,
+           (262144.0 + 270336.0) * steps / (el * 1e3));
+  }
+  // the same pipeline without graphs: per batch on stream j, H2D -> lcp_query -> D2H
+  for (int depth : {4, 6, 8}) {
+    std::vector<lcp_workspace*> ws(depth);
+    std::vector<cudaStream_t> ss(depth);
+    std::vector<uint16_t*> dq(depth);
+    std::vector<char*> dout(depth), hout(depth);
+    const size_t ob = (size_t)B * K * 6 + (size_t)B * 4;
+    for (int d = 0; d < depth; ++d) {
+      lcp_workspace_create(&ws[d]);
+      cudaStreamCreateWithFlags(&ss[d], cudaStreamNonBlocking);
+      cudaMalloc((void**)&dq[d], (size_t)B * L * 2);
+      cudaMalloc((void**)&dout[d], ob);
+      cudaMallocHost((void**)&hout[d], ob);
+    }
+    const int steps = 4000;
+    double t0 = 0;
+    for (int i = -100; i < steps; ++i) {
+      if (i == 0) t0 = now_us();
+      const int d = (i + 100) % depth;
+      cudaStreamSynchronize(ss[d]);
+      cudaMemcpyAsync(dq[d], q + (size_t)((i + 800) % 8) * B * L, (size_t)B * L * 2, cudaMemcpyHostToDevice, ss[d]);
+      lcp_query(ix, ws[d], dq[d], B, K, 1, K, (uint32_t*)dout[d], (uint16_t*)(dout[d] + (size_t)B * K * 4),
+                (int32_t*)(dout[d] + (size_t)B * K * 6), nullptr, nullptr, ss[d]);
+      cudaMemcpyAsync(hout[d], dout[d], ob, cudaMemcpyDeviceToHost, ss[d]);
+    }
+    for (int d = 0; d < depth; ++d) cudaStreamSynchronize(ss[d]);
+    const double el = now_us() - t0;
+    printf("no-graph pipeline depth %d: %.2f us/batch -> %.1f M q/s\n", depth, el / steps, B * steps / el);
+  }
   // zero-copy: the query kernel reads pinned host queries and writes pinned host results
   for (int depth : {1, 2, 4, 8}) {
     std::vector<lcp_workspace*> ws(depth);
