@@ -212,29 +212,72 @@ def async_workspace() -> Workspace:
     return ws
 
 
-class PinnedArray:
-    """Page-locked host buffer exposed as a numpy array (for *_host DMA)."""
+class _PinnedMemory:
+    """Owner of one page-locked block.  Freed (or returned to the per-size
+    pool) only when the last numpy view of it is gone: every view's base chain
+    ends here, so results stay valid as long as anything references them."""
 
-    def __init__(self, shape, dtype) -> None:
+    _pool: dict = {}          # nbytes -> [ptr, ...]
+    _pool_lock = threading.Lock()
+    POOL_PER_SIZE = 8
+
+    def __init__(self, nbytes: int, pooled: bool) -> None:
+        self.nbytes = max(int(nbytes), 1)
+        self.pooled = pooled
+        ptr = None
+        if pooled:
+            with self._pool_lock:
+                free = self._pool.get(self.nbytes)
+                if free:
+                    ptr = free.pop()
+        if ptr is None:
+            p = ctypes.c_void_p()
+            check(load().lcp_pinned_alloc(self.nbytes, ctypes.byref(p)))
+            ptr = int(p.value)
+        self.address = ptr
+
+    def release(self) -> None:
+        ptr, self.address = self.address, None
+        if not ptr:
+            return
+        if self.pooled:
+            with self._pool_lock:
+                free = self._pool.setdefault(self.nbytes, [])
+                if len(free) < self.POOL_PER_SIZE:
+                    free.append(ptr)
+                    return
+        load().lcp_pinned_free(ctypes.c_void_p(ptr))
+
+    def __del__(self) -> None:  # pragma: no cover - interpreter shutdown order
+        try:
+            self.release()
+        except Exception:
+            pass
+
+
+class _PinnedView:
+    """numpy view holder: keeps the _PinnedMemory alive through the array base."""
+
+    def __init__(self, mem: _PinnedMemory, shape, dtype) -> None:
+        self.mem = mem
+        self.__array_interface__ = {"shape": tuple(shape), "typestr": dtype.str,
+                                    "data": (mem.address, False), "version": 3}
+
+
+class PinnedArray:
+    """Page-locked host buffer exposed as a numpy array (for *_host DMA).
+    ``pooled``: reuse blocks of the same size (per-call output blocks)."""
+
+    def __init__(self, shape, dtype, pooled: bool = False) -> None:
         import numpy as np
 
         self.dtype = np.dtype(dtype)
         self.shape = tuple(int(s) for s in (shape if isinstance(shape, (tuple, list)) else (shape,)))
         nbytes = int(np.prod(self.shape, dtype=np.int64)) * self.dtype.itemsize
-        p = ctypes.c_void_p()
-        check(load().lcp_pinned_alloc(max(nbytes, 1), ctypes.byref(p)))
-        self._ptr = p
-        self.address = int(p.value)
-        buf = (ctypes.c_uint8 * max(nbytes, 1)).from_address(p.value)
-        self.array = np.frombuffer(buf, dtype=self.dtype, count=nbytes // self.dtype.itemsize).reshape(self.shape)
+        self._mem = _PinnedMemory(nbytes, pooled)
+        self.address = self._mem.address
+        self.array = np.asarray(_PinnedView(self._mem, self.shape, self.dtype))
 
     def close(self) -> None:
-        if self._ptr:
-            load().lcp_pinned_free(self._ptr)
-            self._ptr = None
-
-    def __del__(self) -> None:  # pragma: no cover
-        try:
-            self.close()
-        except Exception:
-            pass
+        """Drop this handle; the block is released once no view of it remains."""
+        self._mem = None

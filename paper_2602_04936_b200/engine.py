@@ -149,7 +149,7 @@ class NativeIndex:
         return max(1, min(int(k), self.n))
 
     def alloc_batch(self, count: int, k: int, mode: str = "complete", pinned: bool = True,
-                    with_work: bool = True) -> BatchResult:
+                    with_work: bool = True, pooled: bool = False) -> BatchResult:
         """Output buffers for ``count`` queries.  Pinned: one page-locked block
         in the lcp_packed_layout_for() layout, so a batch is one D2H copy.
         with_work=False (async path only) leaves matched_depth/aux out of
@@ -166,7 +166,7 @@ class NativeIndex:
             )
         lay = _native.PackedLayout()
         check(load().lcp_packed_layout_for(count, stride, ctypes.byref(lay)))
-        block = PinnedArray((int(lay.total),), np.uint8)
+        block = PinnedArray((int(lay.total),), np.uint8, pooled=pooled)
         raw = block.array
 
         def view(off, dt, shape):
@@ -211,8 +211,8 @@ class NativeIndex:
             raise InvalidInputError(f"k must be >= 1, got {k}")
         count = int(queries.shape[0])
         k_eff = self.stride_for(k)
-        if out is None:
-            out = self.alloc_batch(count, k, mode, pinned=False)
+        if out is None:  # a pooled page-locked block: one H2D + one D2H, no per-call pinning
+            out = self.alloc_batch(count, k, mode, pinned=True, pooled=True)
         out.mode = mode
         ws = workspace()
         packed = getattr(out, "_packed", None)

@@ -605,3 +605,22 @@ def test_long_keys_vs_oracle(gpu, oracle_lib, L, sigma):
         oid, olcp, oh = oracle_lib.oracle_top_k_batch(ds.items, qs, k)
         for i in range(len(qs)):
             assert f.pairs(i) == list(zip(oid[i, :oh[i]].tolist(), olcp[i, :oh[i]].tolist()))
+
+
+def test_result_views_outlive_their_batch(gpu):
+    """Views of a result (pinned, pooled block) stay valid after the result is
+    dropped and later batches reuse pooled blocks."""
+    import gc
+
+    ds = lg.generate_dataset(50_000, 16, 4, seed=50)
+    idx = lg.build(ds)
+    q1 = lg.generate_queries(ds, 1000, seed=51)
+    ref = idx.query_batch(q1, 10, "complete")
+    expect_ids, expect_lcps = ref.ids.copy(), ref.lcps.copy()
+    kept = idx.query_batch(q1, 10, "complete")
+    ids, lcps = kept.ids, kept.lcps
+    del kept
+    gc.collect()
+    for s in range(20):  # recycle pooled blocks with different answers
+        idx.query_batch(lg.generate_queries(ds, 1000, seed=60 + s), 10, "complete")
+    assert np.array_equal(ids, expect_ids) and np.array_equal(lcps, expect_lcps)
