@@ -230,6 +230,7 @@ struct lcp_index {
   long long* directory = nullptr;
   u32* sketch = nullptr;
   u64* keys_w0 = nullptr;
+  u32* keys_shi = nullptr;
   std::vector<long long> level_offset;  // cached trie level offsets
 };
 
@@ -286,6 +287,7 @@ int lcp_index_free(lcp_index* ix) {
   if (ix->directory) cudaFreeAsync(ix->directory, 0);
   if (ix->sketch) cudaFreeAsync(ix->sketch, 0);
   if (ix->keys_w0) cudaFreeAsync(ix->keys_w0, 0);
+  if (ix->keys_shi) cudaFreeAsync(ix->keys_shi, 0);
   cudaStreamSynchronize(0);
   delete ix;
   return LCP_OK;
@@ -492,6 +494,12 @@ static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, i
       k_first_word<<<blocks_for(n, 256), 256, 0, st>>>(ix->keys, n, W, ix->keys_w0);
       LCP_CK_LAUNCH();
       dv.keys_w0 = ix->keys_w0;
+    } else {  // high-word plane of the sorted keys: the sweep reads 4 B per key
+      LCP_TRY(dalloc(&ix->keys_shi, n + 64, acct, st));
+      LCP_CK(cudaMemsetAsync(ix->keys_shi, 0, (size_t)(n + 64) * 4, st));
+      k_hi_word<<<blocks_for(n, 256), 256, 0, st>>>(ix->keys, n, ix->keys_shi);
+      LCP_CK_LAUNCH();
+      dv.keys_shi = ix->keys_shi;
     }
     ix->tal_depth = tal_depth;
     long long buckets = 1;

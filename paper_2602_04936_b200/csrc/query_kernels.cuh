@@ -501,36 +501,46 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, MODE == 2 ? 1 : 2)
       // W == 1: bits past symbol L are zero in keys and query, so x = key ^ q
       // is nonzero exactly when lcp < L, and min(lcp + 1, L) =
       // 1 + min(clz64(x) >> lb, L - 1) with no branch (clz64(0) = 64).
-      // Aligned interior: 16-byte pairs, 8 keys per lane in flight; the odd
-      // keys at either end are added by lane 0.
+      // The sweep reads the sorted high-word plane (4 B per key): clz64(x) =
+      // clz32(hi ^ qh) unless the high words match, and only then (lcp >=
+      // 32 / b symbols, rare inside a bucket) is the full key read.
+      // Aligned 16-byte groups of 4 keys, 16 keys per lane in flight; the
+      // keys at either end outside whole groups go one per lane.
       const int lm1 = L - 1;
+      const u32 qh = (u32)(q >> 32);
+      const u32* __restrict__ shi = ix.keys_shi;
+      auto term = [&](u32 h, int i) -> u32 {
+        const int c = h != qh ? __clz(h ^ qh) : __clzll((long long)(__ldg(keys + i) ^ q));
+        return (u32)min(c >> lb, lm1);
+      };
       unsigned long long sym = 0;
-      const int a0 = (blo + 1) & ~1, e0 = bhi & ~1;
-      constexpr int TAL_UNROLL = 8;
-      int base = a0 + 2 * lane;
-      for (; base + 64 * (TAL_UNROLL - 1) < e0; base += 64 * TAL_UNROLL) {
-        ulonglong2 kv[TAL_UNROLL];
+      const int a0 = (blo + 3) & ~3, e0 = bhi & ~3;
+      constexpr int TAL_UNROLL = 4;
+      int base = a0 + 4 * lane;
+      for (; base + 128 * (TAL_UNROLL - 1) < e0; base += 128 * TAL_UNROLL) {
+        uint4 hv[TAL_UNROLL];
 #pragma unroll
         for (int u = 0; u < TAL_UNROLL; ++u)
-          kv[u] = __ldg(reinterpret_cast<const ulonglong2*>(keys + base + 64 * u));
+          hv[u] = __ldg(reinterpret_cast<const uint4*>(shi + base + 128 * u));
         u32 part = 0;
 #pragma unroll
         for (int u = 0; u < TAL_UNROLL; ++u) {
-          part += (u32)min(__clzll((long long)(kv[u].x ^ q)) >> lb, lm1);
-          part += (u32)min(__clzll((long long)(kv[u].y ^ q)) >> lb, lm1);
+          const int i = base + 128 * u;
+          part += term(hv[u].x, i) + term(hv[u].y, i + 1) + term(hv[u].z, i + 2) + term(hv[u].w, i + 3);
         }
         sym += part;
       }
-      for (; base < e0; base += 64) {
-        const ulonglong2 kv = __ldg(reinterpret_cast<const ulonglong2*>(keys + base));
-        sym += (u32)min(__clzll((long long)(kv.x ^ q)) >> lb, lm1);
-        sym += (u32)min(__clzll((long long)(kv.y ^ q)) >> lb, lm1);
+      for (; base < e0; base += 128) {
+        const uint4 hv = __ldg(reinterpret_cast<const uint4*>(shi + base));
+        sym += term(hv.x, base) + term(hv.y, base + 1) + term(hv.z, base + 2) + term(hv.w, base + 3);
       }
-      if (lane == 0) {
-        if (blo & 1) sym += (u32)min(__clzll((long long)(__ldg(keys + blo) ^ q)) >> lb, lm1);
-        if ((bhi & 1) && e0 >= a0) sym += (u32)min(__clzll((long long)(__ldg(keys + e0) ^ q)) >> lb, lm1);
-        sym += (unsigned long long)(bhi - blo);  // the "+1" of every item
+      if (e0 >= a0) {  // up to 3 keys before a0 and after e0
+        const int i = lane < 3 ? blo + lane : e0 + lane - 3;
+        if ((lane < 3 && i < a0) || (lane >= 3 && lane < 6 && i < bhi)) sym += term(__ldg(shi + i), i);
+      } else if (lane < bhi - blo) {  // the whole bucket lies inside one group
+        sym += term(__ldg(shi + blo + lane), blo + lane);
       }
+      if (lane == 0) sym += (unsigned long long)(bhi - blo);  // the "+1" of every item
 #pragma unroll
       for (int o = 16; o; o >>= 1) sym += __shfl_xor_sync(LCP_FULL_MASK, sym, o);
       md = ix.tal_depth;
