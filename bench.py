@@ -357,6 +357,13 @@ def main() -> None:
                     "peak_source": peak_src,
                     "duration_source": "CUDA events over the graph-replayed single-stream step loop",
                     "bytes_formula": "sum_q K_b*ceil(log2(N+1)) + |R(d*)|*(K_b+4) + K_b + 6k, K_b=8"}
+        # the same algorithmic bytes over the pipelined (4-in-flight) per-step time
+        step_s = total_ms / 1e3 / args.steps
+        roofline["pipelined"] = {"achieved": round(bytes_per_launch / step_s / 1e9, 2), "unit": "GB/s",
+                                 "frac": round(bytes_per_launch / step_s / 1e9 / peak, 5),
+                                 "step_us": round(step_s * 1e6, 3),
+                                 "note": "algorithmic bytes per batch / headline per-step time "
+                                         f"({INFLIGHT} batches in flight); frac above is per launch"}
         # the kernel is issue-bound, not HBM-bound: instruction roofline from the
         # committed ncu capture (warp instructions per query) and the live rate
         try:
