@@ -20,7 +20,7 @@ typedef unsigned int u32;
 #define LCP_FULL_MASK 0xffffffffu
 #define LCP_MAX_LEVELS 12
 #define LCP_SEARCH_FANOUT 64  // k-ary search: 32 lanes x 2 separators
-#define LCP_LEAF_KEYS 32      // the last search table resolves a 32-key leaf block
+#define LCP_LEAF_KEYS 16      // the last search table resolves a 16-key leaf block
 #define LCP_SK_BLOCK 256      // id sketch: level-0 block of sorted positions
 #define LCP_SK_FANOUT 32      // id sketch: child blocks per block above level 0
 #define LCP_SK_LIST 32        // id sketch: smallest ids kept per block (ascending)

@@ -95,7 +95,7 @@ __device__ __forceinline__ long long warp_lower_bound(const DevIndex& ix, const 
     if (j == ix.nlevels) {  // leaf block: 32 keys, one per lane
       const long long base = blk * LCP_LEAF_KEYS;
       const long long i = base + lane;
-      const bool lt = i < ix.n && key_less<WMAX>(ix.keys + i * W, qk, ix);
+      const bool lt = lane < LCP_LEAF_KEYS && i < ix.n && key_less<WMAX>(ix.keys + i * W, qk, ix);
       return base + (int)__reduce_add_sync(LCP_FULL_MASK, (u32)lt);
     }
     long long base = blk * LCP_SEARCH_FANOUT;
@@ -473,7 +473,11 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, MODE == 2 ? 1 : 2)
     // pos = 0).  The region [B-16, B+48) (T=2) / [B-32, B+64) (T=3), warp-
     // strided (item t*32 + lane), contains the window [pos-need, pos+need)
     // for need <= 16 / 32, which is all d* needs; pos is never materialised.
-    const int s = blk * LCP_LEAF_KEYS - (T == 2 ? 16 : 32);
+    static_assert(LCP_LEAF_KEYS == 16, "region offsets below assume 16-key leaf blocks");
+    // pos in (B, B + 16]: the region [B - (16T - 8), ...) of 32T keys holds
+    // [pos - need, pos + need) for need <= 16 (T=2) / 32 (T=3) with the
+    // slack split evenly around the leaf block
+    const int s = blk * LCP_LEAF_KEYS - (16 * T - 8);
     int l[T];
     u32 id[T];
     int dmax = -1;
@@ -1199,7 +1203,7 @@ __device__ __forceinline__ long long warp_lower_bound_any(const DevIndex& ix, co
   }
   const long long base = blk * LCP_LEAF_KEYS;
   const long long i = base + lane;
-  const bool lt = i < ix.n && key_less<0>(ix.keys + i * W, q, ix);
+  const bool lt = lane < LCP_LEAF_KEYS && i < ix.n && key_less<0>(ix.keys + i * W, q, ix);
   return base + __popc(__ballot_sync(LCP_FULL_MASK, lt));
 }
 
