@@ -450,10 +450,14 @@ static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, i
   dv.levels = ix->levels;
   dv.smem_levels = 0;
   dv.smem_entries = 0;
+  static const long long smem_cap = [] {  // LCP_SMEM_STAGE_CAP: A/B hook (bytes)
+    const char* e = getenv("LCP_SMEM_STAGE_CAP");
+    return e ? atoll(e) : (long long)kSmemStageCap;
+  }();
   for (int j = 0; j < h; ++j) {
     long long end = dv.level_off[j] +
                     (dv.level_cnt[j] + LCP_SEARCH_FANOUT - 1) / LCP_SEARCH_FANOUT * LCP_SEARCH_FANOUT;
-    if (end * W * 8 > kSmemStageCap) break;
+    if (end * W * 8 > smem_cap) break;
     dv.smem_levels = j + 1;
     dv.smem_entries = (int)end;
   }
