@@ -417,7 +417,7 @@ static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, i
   phase("adj");
   // k-ary search levels (stand-in for the trie descent, trie.py:229-256)
   // Tables j = 0..h-1 sample every LCP_LEAF_KEYS * 64**(h-1-j)-th key; the
-  // last one resolves lower_bound(q) to a 32-key leaf block.
+  // last one resolves lower_bound(q) to a leaf block of LCP_LEAF_KEYS keys.
   int h = 0;
   {
     long long cap = LCP_LEAF_KEYS;

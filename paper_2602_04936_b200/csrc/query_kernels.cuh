@@ -9,8 +9,9 @@
 // d* = max{d : |R(d)| >= need}; the answer is the `need` smallest
 // (L-lcp)<<32|id over the contiguous sorted range R(d*).  Because lcp is
 // non-decreasing before pos = lower_bound(q) and non-increasing after it,
-// d* is the need-th largest lcp inside the 64-key window [pos-32, pos+32)
-// for need <= 32, and R(d*) is found by extending that window outward.
+// d* is the need-th largest lcp inside the window [pos-need, pos+need),
+// and R(d*) is found by extending that window outward (long runs: run-edge
+// search + id sketch).
 // The reference's ancestor walk visits exactly d_max - d* ancestors, which
 // is how the host rebuilds WorkReport.nodes_visited.
 #pragma once
@@ -356,13 +357,14 @@ __device__ __forceinline__ int window_dstar(const int (&l)[T], int dmax, int nee
 }
 
 // ---------------------------------------------------------------------------
-// strict / complete, k <= 32, W == 1 (the config-3 hot path): one warp per
-// query.  The upper search levels narrow lower_bound(q) to a 64-key leaf
-// block [b, b+64); the warp then loads the 128-key region [b-32, b+96) with
-// its ids in one coalesced round trip.  That region contains the window
-// [pos-32, pos+32) for any pos in [b, b+64], so it serves the leaf search,
-// d* and the candidate scan at once.  Candidates (lcp >= d*) form one run;
-// it is compacted to one per lane and bitonic-sorted by (L-lcp)<<32|id.
+// strict / complete / TAL, k <= 32, W == 1 (the config-3 hot path): one warp
+// per query.  The 64-ary search tables narrow lower_bound(q) to a 16-key
+// leaf block [B, B+16); the warp then loads a 64-key (need <= 16) or 96-key
+// region around it with its ids in one coalesced round trip.  That region
+// contains the window [pos-need, pos+need) for any pos in (B, B+16], so it
+// serves d* and the candidate scan at once.  Candidates (lcp >= d*) form one
+// run; it is compacted to one per lane and ranked by all-pairs comparison of
+// (L-lcp)<<idbits|id.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ long long prefix_bound(const DevIndex& ix, const u64* q, int d,
                                                   bool upper);
@@ -451,7 +453,7 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, MODE == 2 ? 1 : 2)
     }
     stage_wait(ix, bar);  // first iteration: the query load overlaps the copy
     LCP_STAMP(qi, 1);
-    // 64-ary search down to the 32-key leaf block holding lower_bound(q).
+    // 64-ary search down to the 16-key leaf block holding lower_bound(q).
     // Only the root can count 0 separators below q (q <= every key: pos = 0);
     // below it, a child block starts with its parent's separator, which is < q.
     int blk = 0;
@@ -469,10 +471,9 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, MODE == 2 ? 1 : 2)
       }
     }
     LCP_STAMP(qi, 2);
-    // Leaf block [B, B+32) holds pos = lower_bound(q) in (B, B+32] (or
-    // pos = 0).  The region [B-16, B+48) (T=2) / [B-32, B+64) (T=3), warp-
-    // strided (item t*32 + lane), contains the window [pos-need, pos+need)
-    // for need <= 16 / 32, which is all d* needs; pos is never materialised.
+    // Leaf block [B, B+16) holds pos = lower_bound(q) in (B, B+16] (or
+    // pos = 0); the region is warp-strided (item t*32 + lane) and pos is
+    // never materialised.
     static_assert(LCP_LEAF_KEYS == 16, "region offsets below assume 16-key leaf blocks");
     // pos in (B, B + 16]: the region [B - (16T - 8), ...) of 32T keys holds
     // [pos - need, pos + need) for need <= 16 (T=2) / 32 (T=3) with the
@@ -1186,7 +1187,7 @@ __device__ __forceinline__ long long prefix_bound(const DevIndex& ix, const u64*
 }
 
 // lower_bound(keys, q) for any W by one warp: 64-ary over the global search
-// tables (two separators per lane per level), then the 32-key leaf block
+// tables (two separators per lane per level), then the 16-key leaf block
 __device__ __forceinline__ long long warp_lower_bound_any(const DevIndex& ix, const u64* q) {
   const int lane = lane_id();
   const int W = ix.W;
