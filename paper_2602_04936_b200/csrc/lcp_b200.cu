@@ -1129,7 +1129,11 @@ static void launch_fast(const lcp_index* ix, const uint16_t* q, int count, int k
     // per SM (so each SM stages the search levels once), up to 1024 threads;
     // larger batches get more CTAs (2 x 1024 threads fit an SM).
     const long long sms = num_sms();
-    long long wpc = std::min<long long>(32, std::max<long long>(1, (count + sms - 1) / sms));
+    static const long long wpc_min = [] {  // LCP_WPC_MIN: A/B hook (warps per CTA floor)
+      const char* e = getenv("LCP_WPC_MIN");
+      return e ? std::max(1ll, std::min(32ll, atoll(e))) : 1ll;
+    }();
+    long long wpc = std::min<long long>(32, std::max<long long>(wpc_min, (count + sms - 1) / sms));
     const unsigned block = (unsigned)(wpc * 32);
     unsigned grid = (unsigned)std::min<long long>((count + wpc - 1) / wpc, 4ll * sms);
     size_t smem = 16 + (size_t)dv.smem_entries * dv.W * 8;
