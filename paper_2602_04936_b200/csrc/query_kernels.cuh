@@ -1043,7 +1043,7 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, 1)
   const int warp = threadIdx.x >> 5;
   const int warps = blockDim.x >> 5;
   const long long n = ix.n;
-  const int L = ix.L, lb = ix.lb, W = ix.W;
+  const int L = ix.L, lb = ix.lb;
   const int depth = ix.tal_depth;
   for (long long qi = (long long)blockIdx.x * warps + warp; qi < count;
        qi += (long long)gridDim.x * warps) {
