@@ -31,6 +31,7 @@ is timed beside it as "rowblock_sharded".
 from __future__ import annotations
 
 import argparse
+import datetime
 import json
 import os
 import sys
@@ -235,7 +236,9 @@ def main() -> None:
         if share:
             dist.init_process_group("gloo")
         else:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+            # bounded collective timeout: a failed rank ends the run instead of hanging it
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank),
+                                    timeout=datetime.timedelta(seconds=300))
     dev = torch.device("cuda", local_rank)
 
     # every rank serves the config-3 corpus from its own replica of the index
