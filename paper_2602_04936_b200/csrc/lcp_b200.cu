@@ -138,6 +138,18 @@ int num_sms() {
   return sms;
 }
 
+// k_query_general grid: every resident CTA slot (the kernel strides over queries)
+long long gen_grid(long long count) {
+  static const int per_sm = [] {  // thread-safe one-time initialisation
+    int v = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_query_general, GEN_THREADS, 0) !=
+            cudaSuccess || v <= 0)
+      v = 8;
+    return v;
+  }();
+  return std::min<long long>(count, (long long)per_sm * num_sms());
+}
+
 // ---- exclusive scan ------------------------------------------------------
 template <typename T>
 int scan_exclusive(T* data, long long m, cudaStream_t st) {
@@ -1231,7 +1243,7 @@ static int query_impl(const lcp_index* ix, lcp_workspace* ws, const uint16_t* qu
   k_pack<<<blocks_for((long long)count * dv.W, 256), 256, 0, st>>>(
       queries, count, dv.L, dv.W, dv.b, dv.spw, dv.sigma, ws->qkeys.as<u64>(), nullptr, errp);
   LCP_CK_LAUNCH();
-  unsigned grid = (unsigned)std::min<long long>(count, 8ll * num_sms());
+  unsigned grid = (unsigned)gen_grid(count);
   k_query_general<<<grid, GEN_THREADS, 0, st>>>(dv, ws->qkeys.as<u64>(), queries, count, k, mode,
                                                 0, out_stride, ids, lcps, hits, md, ax);
   LCP_CK_LAUNCH();
@@ -1528,7 +1540,7 @@ int lcp_fullscan(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries
   k_pack<<<blocks_for((long long)count * dv.W, 256), 256, 0, st>>>(
       queries, count, dv.L, dv.W, dv.b, dv.spw, dv.sigma, ws->qkeys.as<u64>(), nullptr, ws->d_err);
   LCP_CK_LAUNCH();
-  unsigned grid = (unsigned)std::min<long long>(count, 8ll * num_sms());
+  unsigned grid = (unsigned)gen_grid(count);
   k_query_general<<<grid, GEN_THREADS, 0, st>>>(dv, ws->qkeys.as<u64>(), queries, count, k, 1, 1,
                                                 out_stride, ids, lcps, hits, nullptr, nullptr);
   LCP_CK_LAUNCH();

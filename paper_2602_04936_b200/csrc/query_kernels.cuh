@@ -1154,23 +1154,122 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, 1)
 constexpr int GEN_THREADS = 128;
 constexpr int GEN_CAP = 2048;
 
+// ascending bitonic sort of buf[0, P) (P a power of two) by the whole CTA.
+// Threads walk pair indices t (i = t with a zero inserted at bit j), so every
+// lane does a compare-exchange at every stage.  A warp's pair indices
+// [32w, 32w + 32) + r * blockDim touch only its own 64-element segments when
+// j <= 32, so those stages need only a warp barrier; a CTA barrier precedes
+// every stage with j >= 64 (and follows the last one of each merge).
 __device__ __forceinline__ void bitonic_sort_smem(u64* buf, int P) {
+  const int half = P >> 1;
   for (int k2 = 2; k2 <= P; k2 <<= 1) {
     for (int j = k2 >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < P; i += blockDim.x) {
-        int ixj = i ^ j;
-        if (ixj > i) {
-          u64 a = buf[i], b = buf[ixj];
-          bool up = (i & k2) == 0;
-          if ((a > b) == up) {
-            buf[i] = b;
-            buf[ixj] = a;
-          }
+      for (int t = threadIdx.x; t < half; t += blockDim.x) {
+        const int i = 2 * t - (t & (j - 1));
+        const u64 a = buf[i], b = buf[i + j];
+        if ((a > b) == ((i & k2) == 0)) {
+          buf[i] = b;
+          buf[i + j] = a;
         }
       }
-      __syncthreads();
+      if (j > 32 || j == 1) __syncthreads();
+      else __syncwarp();
     }
   }
+}
+
+// block-wide AND / OR of per-thread values (all threads call; ends synchronized)
+__device__ __forceinline__ void block_and_or(u64& a, u64& o, u64 (*s_red)[2]) {
+  const int lane = lane_id(), warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int s = 16; s; s >>= 1) {
+    a &= __shfl_xor_sync(LCP_FULL_MASK, a, s);
+    o |= __shfl_xor_sync(LCP_FULL_MASK, o, s);
+  }
+  if (lane == 0) {
+    s_red[warp][0] = a;
+    s_red[warp][1] = o;
+  }
+  __syncthreads();
+  a = s_red[0][0];
+  o = s_red[0][1];
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+    a &= s_red[w][0];
+    o |= s_red[w][1];
+  }
+  __syncthreads();
+}
+
+// appends c to dst when pred (one shared atomic per warp); all lanes call
+__device__ __forceinline__ void warp_append(bool pred, u64 c, u64* dst, u32* cnt, u32 cap) {
+  const unsigned m = __ballot_sync(LCP_FULL_MASK, pred);
+  if (!m) return;
+  const int lane = lane_id(), leader = __ffs(m) - 1;
+  u32 base = 0;
+  if (lane == leader) base = atomicAdd(cnt, (u32)__popc(m));
+  base = __shfl_sync(LCP_FULL_MASK, base, leader);
+  const u32 slot = base + __popc(m & ((1u << lane) - 1u));
+  if (pred && slot < cap) dst[slot] = c;
+}
+
+// The want-th smallest value among {get(i) : i in [lo, hi), first || get(i) > last},
+// by 8-bit digits from the top.  Digits constant over the whole range
+// (vdiff = AND ^ OR of its values is zero there) come from vand without a pass;
+// histogram updates are aggregated per warp (__match_any_sync), so the few
+// distinct digits of the lcp field cost one shared atomic per warp each.
+// All threads call; the result is uniform.
+template <typename Get>
+__device__ __forceinline__ u64 radix_select(const Get& get, long long lo, long long hi, bool first,
+                                            u64 last, u32 want, u64 vand, u64 vdiff, u32* hist,
+                                            u64* s_prefix, u32* s_rank) {
+  const int lane = lane_id();
+  u64 prefix = 0, hmask = 0;
+  u32 rank = want;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    const u64 dmask = 255ull << shift;
+    if (!(vdiff & dmask)) {
+      prefix |= vand & dmask;
+      hmask |= dmask;
+      continue;
+    }
+    for (int t = threadIdx.x; t < 256; t += blockDim.x) hist[t] = 0;
+    __syncthreads();
+    for (long long b = lo; b < hi; b += blockDim.x) {
+      const long long i = b + threadIdx.x;
+      u32 dg = 256;
+      if (i < hi) {
+        const u64 c = get(i);
+        if ((first || c > last) && (c & hmask) == prefix) dg = (u32)((c >> shift) & 255);
+      }
+      const unsigned peers = __match_any_sync(LCP_FULL_MASK, dg);
+      if (dg < 256 && lane == __ffs(peers) - 1) atomicAdd(&hist[dg], (u32)__popc(peers));
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // warp 0: the bin holding the rank-th value
+      u32 v[8], s = 0;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) s += (v[r] = hist[lane * 8 + r]);
+      u32 inc = s;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 t = __shfl_up_sync(LCP_FULL_MASK, inc, o);
+        if (lane >= o) inc += t;
+      }
+      u32 cum = inc - s;
+      if (cum < rank && inc >= rank) {
+        int r = 0;
+        for (; r < 7 && cum + v[r] < rank; ++r) cum += v[r];
+        *s_prefix = prefix | ((u64)(lane * 8 + r) << shift);
+        *s_rank = rank - cum;
+      }
+    }
+    __syncthreads();
+    prefix = *s_prefix;
+    rank = *s_rank;
+    hmask |= dmask;
+  }
+  __syncthreads();  // s_prefix / s_rank reads done before any reuse
+  return prefix;
 }
 
 // first index in [0, n) whose d-prefix compares >= q (strict=false) or > q (strict=true)
@@ -1253,6 +1352,7 @@ __global__ void __launch_bounds__(GEN_THREADS)
   __shared__ unsigned long long s_sym;
   __shared__ long long s_pos;
   __shared__ long long s_part[GEN_THREADS / 32][2];
+  __shared__ u64 s_red[GEN_THREADS / 32][2];
   const int L = ix.L;
   const int lane = lane_id(), warp = threadIdx.x >> 5;
 
@@ -1334,6 +1434,45 @@ __global__ void __launch_bounds__(GEN_THREADS)
           s_sym = 0;
         }
       }
+    } else if (!fullscan && mode != 2 && ix.n > 0) {
+      // need beyond the window: warp 0 finds R(d) for any d by run_edge_any on
+      // both sides of the deepest match p0, and d* by binary search over depths
+      if (warp == 0) {
+        const long long pos = warp_lower_bound_any(ix, q);
+        const int lp = pos > 0 ? key_lcp<0>(ix.keys + (pos - 1) * ix.W, q, ix) : -1;
+        const int lq = pos < ix.n ? key_lcp<0>(ix.keys + pos * ix.W, q, ix) : -1;
+        const int dmax = max(lp, lq);
+        const long long p0 = lq == dmax ? pos : pos - 1;
+        auto range = [&](int d, long long& a, long long& b) {
+          a = d ? run_edge_any(ix, q, d, p0, -1) : 0;
+          b = d ? run_edge_any(ix, q, d, p0, ix.n) + 1 : ix.n;
+        };
+        long long lo, hi;
+        int dstar = dmax;
+        range(dmax, lo, hi);
+        const long long need = mode == 1 ? min((long long)k, ix.n) : (long long)k;
+        if (mode == 1 && hi - lo < need) {
+          int dl = 0, dh = dmax - 1;  // |R(0)| = n >= need
+          while (dl < dh) {
+            const int mid = (dl + dh + 1) >> 1;
+            long long a, b;
+            range(mid, a, b);
+            if (b - a >= need) dl = mid;
+            else dh = mid - 1;
+          }
+          dstar = dl;
+          range(dstar, lo, hi);
+        }
+        if (lane == 0) {
+          s_lo = lo;
+          s_hi = hi;
+          s_take = mode == 1 ? need : min((long long)k, hi - lo);
+          s_dmax = dmax;
+          s_dstar = dstar;
+          s_md = dmax;
+          s_sym = 0;
+        }
+      }
     } else if (threadIdx.x == 0) {
       long long lo = 0, hi = ix.n, take = 0;
       int dmax = 0, dstar = 0, md = 0;
@@ -1344,33 +1483,7 @@ __global__ void __launch_bounds__(GEN_THREADS)
         take = min((long long)k, hi - lo);
         md = ix.tal_depth;
       } else {
-        long long a = 0, b = ix.n;
-        while (a < b) {
-          long long m = (a + b) >> 1;
-          if (key_less<0>(ix.keys + m * ix.W, q, ix)) a = m + 1;
-          else b = m;
-        }
-        const long long pos = a;
-        if (pos > 0) dmax = key_lcp<0>(ix.keys + (pos - 1) * ix.W, q, ix);
-        if (pos < ix.n) dmax = max(dmax, key_lcp<0>(ix.keys + pos * ix.W, q, ix));
-        if (mode == 0) {
-          dstar = dmax;
-          lo = prefix_bound(ix, q, dmax, false);
-          hi = prefix_bound(ix, q, dmax, true);
-          take = min((long long)k, hi - lo);
-        } else {
-          const long long need = min((long long)k, ix.n);
-          int d = dmax;
-          for (;;) {
-            lo = d ? prefix_bound(ix, q, d, false) : 0;
-            hi = d ? prefix_bound(ix, q, d, true) : ix.n;
-            if (hi - lo >= need || d == 0) break;
-            --d;
-          }
-          dstar = d;
-          take = need;
-        }
-        md = dmax;
+        hi = 0;  // strict / complete over an empty index
       }
       s_lo = lo;
       s_hi = hi;
@@ -1385,75 +1498,85 @@ __global__ void __launch_bounds__(GEN_THREADS)
     const long long size = hi - lo;
     GenItem it{&ix, q, fullscan != 0};
     unsigned long long sym = 0;
+    u64 vand = ~0ull, vor = 0;
+    auto emit = [&](const u64* src, long long at, int n) {
+      for (int t = threadIdx.x; t < n; t += GEN_THREADS) {
+        const u64 c = src[t];
+        out_ids[qi * stride + at + t] = (u32)(c & 0xffffffffull);
+        out_lcps[qi * stride + at + t] = (uint16_t)(L - (int)(c >> 32));
+      }
+    };
 
     if (size <= GEN_CAP) {
-      int P = 1;
+      int P = 1, Pt = 1;
       while (P < size) P <<= 1;
-      for (int t = threadIdx.x; t < P; t += GEN_THREADS) {
-        u64 c = ~0ull;
+      while (Pt < take) Pt <<= 1;
+      constexpr int PER = GEN_CAP / GEN_THREADS;
+      u64 v[PER];
+#pragma unroll
+      for (int r = 0; r < PER; ++r) {
+        const int t = threadIdx.x + r * GEN_THREADS;
+        v[r] = ~0ull;
         if (t < size) {
           int l;
-          c = it.comp(lo + t, &l);
+          v[r] = it.comp(lo + t, &l);
           sym += (unsigned long long)min(l + 1, L);
+          vand &= v[r];
+          vor |= v[r];
         }
-        buf[t] = c;
+        if (t < P) buf[t] = v[r];
+      }
+      if (take > 0 && 2 * Pt <= P) {
+        // select, then sort only the take smallest (a power of two at least
+        // half as large): threshold by radix select over the staged values,
+        // compaction through registers back into buf
+        block_and_or(vand, vor, s_red);
+        const u64 T = radix_select([&](long long i) { return buf[i]; }, 0, size, true, 0ull,
+                                   (u32)take, vand, vand ^ vor, hist, &s_prefix, &s_rank);
+        if (threadIdx.x == 0) s_cnt = 0;
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < PER; ++r) warp_append(v[r] <= T, v[r], buf, &s_cnt, (u32)Pt);
+        __syncthreads();
+        for (int t = (int)take + threadIdx.x; t < Pt; t += GEN_THREADS) buf[t] = ~0ull;
+        P = Pt;
       }
       __syncthreads();
       bitonic_sort_smem(buf, P);
-      for (int t = threadIdx.x; t < take; t += GEN_THREADS) {
-        u64 c = buf[t];
-        out_ids[qi * stride + t] = (u32)(c & 0xffffffffull);
-        out_lcps[qi * stride + t] = (uint16_t)(L - (int)(c >> 32));
-      }
+      emit(buf, 0, (int)take);
     } else {
+      // one pass for symbols_compared and the value span, then rounds of
+      // GEN_CAP: radix select of the round's last value, collect (last, T], sort
+      for (long long i = lo + threadIdx.x; i < hi; i += GEN_THREADS) {
+        int l;
+        const u64 c = it.comp(i, &l);
+        sym += (unsigned long long)min(l + 1, L);
+        vand &= c;
+        vor |= c;
+      }
+      block_and_or(vand, vor, s_red);
       long long emitted = 0;
       u64 last = 0;
       bool first = true;
+      auto get = [&](long long i) {
+        int l;
+        return it.comp(i, &l);
+      };
       while (emitted < take) {
         const u32 want = (u32)min((long long)GEN_CAP, take - emitted);
-        // --- radix select: want-th smallest composite greater than `last`
-        if (threadIdx.x == 0) {
-          s_prefix = 0;
-          s_rank = want;
-        }
-        __syncthreads();
-        for (int shift = 56; shift >= 0; shift -= 8) {
-          for (int t = threadIdx.x; t < 256; t += GEN_THREADS) hist[t] = 0;
-          __syncthreads();
-          const u64 prefix = s_prefix;
-          const u64 hmask = shift == 56 ? 0ull : (~0ull << (shift + 8));
-          for (long long i = lo + threadIdx.x; i < hi; i += GEN_THREADS) {
-            int l;
-            u64 c = it.comp(i, &l);
-            if (first && shift == 56) sym += (unsigned long long)min(l + 1, L);
-            if ((first || c > last) && (c & hmask) == prefix)
-              atomicAdd(&hist[(c >> shift) & 255], 1u);
-          }
-          __syncthreads();
-          if (threadIdx.x == 0) {
-            u32 r = s_rank, cum = 0;
-            int dg = 0;
-            for (; dg < 256; ++dg) {
-              if (cum + hist[dg] >= r) break;
-              cum += hist[dg];
-            }
-            if (dg == 256) dg = 255;  // fewer candidates than `want`: cannot happen
-            s_rank = r - cum;
-            s_prefix = prefix | ((u64)dg << shift);
-          }
-          __syncthreads();
-        }
-        const u64 T = s_prefix;
-        // --- collect (last, T] : exactly `want` composites
+        const u64 T = radix_select(get, lo, hi, first, last, want, vand, vand ^ vor, hist,
+                                   &s_prefix, &s_rank);
         if (threadIdx.x == 0) s_cnt = 0;
         __syncthreads();
-        for (long long i = lo + threadIdx.x; i < hi; i += GEN_THREADS) {
-          int l;
-          u64 c = it.comp(i, &l);
-          if ((first || c > last) && c <= T) {
-            u32 slotp = atomicAdd(&s_cnt, 1u);
-            if (slotp < GEN_CAP) buf[slotp] = c;
+        for (long long b = lo; b < hi; b += GEN_THREADS) {
+          const long long i = b + threadIdx.x;
+          u64 c = 0;
+          bool in = false;
+          if (i < hi) {
+            c = get(i);
+            in = (first || c > last) && c <= T;
           }
+          warp_append(in, c, buf, &s_cnt, GEN_CAP);
         }
         __syncthreads();
         int P = 1;
@@ -1461,22 +1584,11 @@ __global__ void __launch_bounds__(GEN_THREADS)
         for (int t = (int)want + threadIdx.x; t < P; t += GEN_THREADS) buf[t] = ~0ull;
         __syncthreads();
         bitonic_sort_smem(buf, P);
-        for (int t = threadIdx.x; t < (int)want; t += GEN_THREADS) {
-          u64 c = buf[t];
-          out_ids[qi * stride + emitted + t] = (u32)(c & 0xffffffffull);
-          out_lcps[qi * stride + emitted + t] = (uint16_t)(L - (int)(c >> 32));
-        }
+        emit(buf, emitted, (int)want);
         __syncthreads();
         last = T;
         first = false;
         emitted += want;
-      }
-      if (take == 0 && mode == 2 && !fullscan) {
-        for (long long i = lo + threadIdx.x; i < hi; i += GEN_THREADS) {
-          int l;
-          it.comp(i, &l);
-          sym += (unsigned long long)min(l + 1, L);
-        }
       }
     }
     // reduce symbols_compared (TAL accounting)

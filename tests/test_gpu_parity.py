@@ -624,3 +624,51 @@ def test_result_views_outlive_their_batch(gpu):
     for s in range(20):  # recycle pooled blocks with different answers
         idx.query_batch(lg.generate_queries(ds, 1000, seed=60 + s), 10, "complete")
     assert np.array_equal(ids, expect_ids) and np.array_equal(lcps, expect_lcps)
+
+
+@pytest.mark.parametrize("wide", [False, True])
+def test_large_k_vs_oracle(gpu, oracle_lib, wide, monkeypatch):
+    """k_query_general at every branch: select-then-sort inside GEN_CAP, the
+    warp setup for need > GEN_CAP / 2, radix rounds beyond GEN_CAP (k up to
+    5000, ranges up to the whole corpus), for complete, strict, TAL and the
+    full scan, with both composite widths."""
+    if wide:
+        monkeypatch.setenv("LCP_FORCE_WIDE_COMPOSITE", "1")
+    rng = np.random.default_rng(31)
+    dup = rng.integers(0, 4, (40, 12)).astype(np.uint16)[rng.integers(0, 40, 6000)]
+    cases = [
+        ("uniform", lg.generate_dataset(20_000, 16, 4, seed=30)),
+        ("clustered", lg.generate_dataset(12_000, 24, 4, seed=32, distribution="clustered")),
+        ("dups", lg.Dataset.from_rows(dup, 4)),
+        ("wide", lg.generate_dataset(8_000, 40, 65536, seed=33)),
+    ]
+    for name, ds in cases:
+        idx = lg.build(ds)
+        sigma = ds.alphabet.size
+        ot = oracle_lib.OracleTrie(ds.items, sigma)
+        qs = np.vstack([lg.generate_queries(ds, 40, seed=34),
+                        lg.generate_queries(ds, 40, seed=35, prefix_len=ds.length // 4)])
+        for k in (200, 1000, 1024, 1025, 2048, 2049, 5000):
+            for mode in ("complete", "strict"):
+                b = idx.query_batch(qs, k, mode)
+                ids, lcps, hits, md, sym, nodes = ot.query_batch(qs, k, mode)
+                for i in range(len(qs)):
+                    exp = list(zip(ids[i, :hits[i]].tolist(), lcps[i, :hits[i]].tolist()))
+                    assert b.pairs(i) == exp, (name, k, mode, i)
+                    assert int(b.matched_depth[i]) == md[i]
+                w = idx.new_work_report()
+                idx.query_batch(qs, k, mode, work=w)
+                assert w.nodes_visited == int(nodes.sum()), (name, k, mode)
+        for k in (100, 3000):
+            fb = idx.fullscan_batch(qs[:8], k)
+            oid, olcp, oh = oracle_lib.oracle_top_k_batch(ds.items, qs[:8], k)
+            for i in range(8):
+                assert fb.pairs(i) == list(zip(oid[i, :oh[i]].tolist(), olcp[i, :oh[i]].tolist())), (name, k)
+        eng = lg.build_tal(ds, sigma)
+        ote = oracle_lib.OracleTal(ds.items, sigma, eng.bucket_depth)
+        for k in (100, 3000):
+            b = eng.query_batch(qs, k)
+            ids, lcps, hits, items_, sym = ote.query_batch(qs, k)
+            for i in range(len(qs)):
+                assert b.pairs(i) == list(zip(ids[i, :hits[i]].tolist(), lcps[i, :hits[i]].tolist())), (name, k, i)
+            assert np.array_equal(b.aux[:, 1].astype(np.int64), sym)

@@ -1,4 +1,5 @@
-"""Config-3 throughput for k beyond the warp path (k > 32 -> k_query_general)."""
+"""Config-3 throughput for large k: the warp paths (k <= 128) and k_query_general
+(select-then-sort within GEN_CAP, radix rounds beyond), complete and strict."""
 import os
 import sys
 
@@ -11,19 +12,35 @@ ds = lg.generate_dataset(2_000_000, 32, 4, seed=3)
 idx = lg.build(ds)
 B = 4096
 dq = torch.from_numpy(lg.generate_queries(ds, B, seed=4)).cuda()
-for k in (10, 32, 33, 64, 100, 1000):
+cases = [(k, "complete") for k in (10, 32, 33, 64, 100, 129, 256, 500, 1000, 2000, 5000)]
+cases += [(k, "strict") for k in (256, 1000)]
+for k, mode in cases:
     ids = torch.empty((B, k), dtype=torch.int32, device="cuda")
     lcps = torch.empty((B, k), dtype=torch.int16, device="cuda")
     hits = torch.empty(B, dtype=torch.int32, device="cuda")
     for _ in range(3):
-        idx.native.query_device(dq, k, "complete", ids, lcps, hits, stream=0)
+        idx.native.query_device(dq, k, mode, ids, lcps, hits, stream=0)
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    n = 20
+    n = 10
     a.record()
     for _ in range(n):
-        idx.native.query_device(dq, k, "complete", ids, lcps, hits, stream=0)
+        idx.native.query_device(dq, k, mode, ids, lcps, hits, stream=0)
     b.record()
     torch.cuda.synchronize()
     us = 1e3 * a.elapsed_time(b) / n
-    print(f"k={k}: {us:.1f} us/batch -> {B / us:.1f} M q/s")
+    print(f"{mode} k={k}: {us:.1f} us/batch -> {B / us:.2f} M q/s", flush=True)
+# full scan with k beyond the warp merge (general kernel over the whole corpus)
+fq = dq[:64]
+for k in (10, 64):
+    ids = torch.empty((64, k), dtype=torch.int32, device="cuda")
+    lcps = torch.empty((64, k), dtype=torch.int16, device="cuda")
+    hits = torch.empty(64, dtype=torch.int32, device="cuda")
+    idx.native.fullscan_device(fq, k, ids, lcps, hits, stream=0)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    idx.native.fullscan_device(fq, k, ids, lcps, hits, stream=0)
+    b.record()
+    torch.cuda.synchronize()
+    print(f"fullscan k={k}, 64 queries: {1e3 * a.elapsed_time(b):.1f} us", flush=True)
