@@ -11,12 +11,15 @@
 // to FS_THREADS queries.  Keys arrive in ascending id order, so a key only
 // enters a full list if its lcp strictly beats the list's worst lcp: for
 // W == 1 that test is one 64-bit compare  (key ^ q) <= limm1.
-// Per-(query, chunk) lists go to scratch and are merged by k_merge.
+// Per-(query, chunk) lists go to scratch and are merged by k_merge (take <=
+// 32) or k_merge_sort (lists of up to FS_KMAX_* entries, chunks * take <= 8192).
 #pragma once
 
 #include "common.cuh"
 
 constexpr int FS_THREADS = 256;
+constexpr int FS_KMAX_U32 = 128;  // register list capacity, 32-bit composites
+constexpr int FS_KMAX_U64 = 64;   // 64-bit composites
 constexpr int FS1_STAGE_KEYS = 2048;  // keys per shared-memory stage (hi + lo planes: 16 KB)
 
 template <int KCAP>
@@ -209,7 +212,9 @@ __global__ void __launch_bounds__(FS_THREADS)
 
   if (active) {
     u64* out = partial + (qi * nchunks + blockIdx.y) * (long long)need;
-    for (int j = 0; j < need; ++j) out[j] = widen_comp<C>(list_at<C, KCAP>(list, j), idbits);
+#pragma unroll
+    for (int j = 0; j < KCAP; ++j)
+      if (j < need) out[j] = widen_comp<C>(list[j], idbits);
   }
 }
 
@@ -300,21 +305,7 @@ __global__ void __launch_bounds__(MERGE_SORT_THREADS)
     }
     atomicAdd(&s_valid, valid);
     __syncthreads();
-    for (int k2 = 2; k2 <= P; k2 <<= 1) {
-      for (int j = k2 >> 1; j > 0; j >>= 1) {
-        for (int i = threadIdx.x; i < P; i += MERGE_SORT_THREADS) {
-          const int ixj = i ^ j;
-          if (ixj > i) {
-            const u64 a = sbuf[i], b = sbuf[ixj];
-            if ((a > b) == ((i & k2) == 0)) {
-              sbuf[i] = b;
-              sbuf[ixj] = a;
-            }
-          }
-        }
-        __syncthreads();
-      }
-    }
+    bitonic_sort_smem(sbuf, P);
     const int hits = min(take, s_valid);
     for (int t = threadIdx.x; t < hits; t += MERGE_SORT_THREADS) {
       const u64 c = sbuf[t];

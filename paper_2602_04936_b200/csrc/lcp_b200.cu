@@ -1471,9 +1471,12 @@ static int launch_fullscan_w1_c(const DevIndex& dv, const uint16_t* q, const u64
   if (need <= K) return launch_fullscan_w1_k<C, K>(dv, q, qkeys, count, need, chunk, nchunks, partial, hint, err, st);
   LCP_FS_CASE(1) LCP_FS_CASE(2) LCP_FS_CASE(3) LCP_FS_CASE(4) LCP_FS_CASE(5) LCP_FS_CASE(6)
   LCP_FS_CASE(8) LCP_FS_CASE(10) LCP_FS_CASE(12) LCP_FS_CASE(16) LCP_FS_CASE(20)
-  LCP_FS_CASE(24) LCP_FS_CASE(32)
+  LCP_FS_CASE(24) LCP_FS_CASE(32) LCP_FS_CASE(48) LCP_FS_CASE(64)
+  if constexpr (sizeof(C) == 4) {  // 32-bit composites: up to 128 list registers
+    LCP_FS_CASE(96) LCP_FS_CASE(128)
+  }
 #undef LCP_FS_CASE
-  return fail(LCP_ERR_INTERNAL, "full scan: need > 32 on the fast path");
+  return fail(LCP_ERR_INTERNAL, "full scan: need beyond the register lists");
 }
 
 static int launch_fullscan_w1(const DevIndex& dv, const uint16_t* q, const u64* qkeys, int count,
@@ -1484,6 +1487,31 @@ static int launch_fullscan_w1(const DevIndex& dv, const uint16_t* q, const u64* 
   return launch_fullscan_w1_c<u64>(dv, q, qkeys, count, need, chunk, nchunks, partial, hint, err, st);
 }
 
+
+// per query, the take smallest of `shards` candidate lists of kin entries
+// (cand index = s * s_stride + q * q_stride + j): a warp per query for
+// take <= 32, else a CTA sorting all shards * kin <= MERGE_SORT_CAP candidates
+static int launch_merge(const u64* cand, int shards, int count, int kin, long long s_stride,
+                        long long q_stride, int take, int L, int strict, u32* ids, uint16_t* lcps,
+                        int* hits, int out_stride, cudaStream_t st) {
+  if (take <= FAST_KMAX) {
+    k_merge<<<blocks_for((long long)count * 32, 256), 256, 0, st>>>(
+        cand, shards, count, kin, s_stride, q_stride, take, L, strict, ids, lcps, hits, out_stride);
+  } else {
+    if ((long long)shards * kin > MERGE_SORT_CAP)
+      return fail(LCP_ERR_INVALID_INPUT, "merge supports shards * k <= " + std::to_string(MERGE_SORT_CAP));
+    int P = 1;
+    while (P < shards * kin) P <<= 1;
+    static const cudaError_t attr = cudaFuncSetAttribute(  // thread-safe one-time initialisation
+        k_merge_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, MERGE_SORT_CAP * 8);
+    LCP_CK(attr);
+    const unsigned grid = (unsigned)std::min<long long>(count, 8ll * num_sms());
+    k_merge_sort<<<grid, MERGE_SORT_THREADS, (size_t)P * 8, st>>>(
+        cand, shards, count, kin, s_stride, q_stride, take, L, strict, ids, lcps, hits, out_stride);
+  }
+  LCP_CK_LAUNCH();
+  return LCP_OK;
+}
 
 extern "C" {
 
@@ -1503,13 +1531,14 @@ int lcp_fullscan(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries
     return LCP_OK;
   }
   const int take = (int)std::min<long long>(k, dv.n);
-  if (take <= FAST_KMAX) {
+  if (take <= (dv.idbits < 32 ? FS_KMAX_U32 : FS_KMAX_U64)) {
     const int per_stage = FS1_STAGE_KEYS;
     const long long qtiles = (count + FS_THREADS - 1) / FS_THREADS;
     const long long max_chunks = (dv.n + per_stage - 1) / per_stage;
     long long want = std::max(1ll, (4ll * num_sms() + qtiles - 1) / qtiles);
     if (const char* fc = getenv("LCP_FULLSCAN_CHUNKS")) want = std::max(1ll, atoll(fc));  // tuning hook
     want = std::min(want, max_chunks);
+    if (take > FAST_KMAX) want = std::min<long long>(want, MERGE_SORT_CAP / take);  // CTA merge capacity
     long long chunk = (dv.n + want - 1) / want;
     chunk = (chunk + per_stage - 1) / per_stage * per_stage;
     const int nchunks = (int)((dv.n + chunk - 1) / chunk);
@@ -1530,11 +1559,8 @@ int lcp_fullscan(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries
     LCP_TRY(launch_fullscan_w1(dv, queries, qk, count, take, chunk, nchunks, partial,
                                ws->hint.as<int>(), ws->d_err, st));
     LCP_CK_LAUNCH();
-    k_merge<<<blocks_for((long long)count * 32, 256), 256, 0, st>>>(
-        partial, nchunks, count, take, take, (long long)nchunks * take, take, dv.L, 0, ids, lcps,
-        hits, out_stride);
-    LCP_CK_LAUNCH();
-    return LCP_OK;
+    return launch_merge(partial, nchunks, count, take, take, (long long)nchunks * take, take, dv.L,
+                        0, ids, lcps, hits, out_stride, st);
   }
   LCP_TRY(ws->qkeys.ensure((size_t)count * dv.W * 8));
   k_pack<<<blocks_for((long long)count * dv.W, 256), 256, 0, st>>>(
@@ -1591,26 +1617,8 @@ int lcp_merge_candidates(const uint64_t* cand, int32_t shards, int32_t count, in
   if (shards < 1 || k < 1) return fail(LCP_ERR_INVALID_INPUT, "shards and k must be >= 1");
   if (take < 0 || take > k)
     return fail(LCP_ERR_INVALID_INPUT, "merge needs 0 <= take <= k");
-  if (take <= FAST_KMAX) {  // one warp per query
-    k_merge<<<blocks_for((long long)count * 32, 256), 256, 0, (cudaStream_t)stream>>>(
-        (const u64*)cand, shards, count, k, (long long)count * k, k, take, length, strict, ids,
-        lcps, hits, std::max(1, take));
-  } else {  // one CTA per query, shared-memory sort of all candidates
-    if ((long long)shards * k > MERGE_SORT_CAP)
-      return fail(LCP_ERR_INVALID_INPUT, "merge supports shards * k <= " + std::to_string(MERGE_SORT_CAP));
-    int P = 1;
-    while (P < shards * k) P <<= 1;
-    const size_t smem = (size_t)P * 8;
-    static const cudaError_t attr = cudaFuncSetAttribute(  // thread-safe one-time initialisation
-        k_merge_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, MERGE_SORT_CAP * 8);
-    LCP_CK(attr);
-    const unsigned grid = (unsigned)std::min<long long>(count, 8ll * num_sms());
-    k_merge_sort<<<grid, MERGE_SORT_THREADS, smem, (cudaStream_t)stream>>>(
-        (const u64*)cand, shards, count, k, (long long)count * k, k, take, length, strict, ids,
-        lcps, hits, std::max(1, take));
-  }
-  LCP_CK_LAUNCH();
-  return LCP_OK;
+  return launch_merge((const u64*)cand, shards, count, k, (long long)count * k, k, take, length,
+                      strict, ids, lcps, hits, std::max(1, take), (cudaStream_t)stream);
 }
 
 int lcp_pinned_alloc(int64_t bytes, void** out) {

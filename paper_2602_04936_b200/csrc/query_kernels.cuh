@@ -1154,30 +1154,6 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, 1)
 constexpr int GEN_THREADS = 128;
 constexpr int GEN_CAP = 2048;
 
-// ascending bitonic sort of buf[0, P) (P a power of two) by the whole CTA.
-// Threads walk pair indices t (i = t with a zero inserted at bit j), so every
-// lane does a compare-exchange at every stage.  A warp's pair indices
-// [32w, 32w + 32) + r * blockDim touch only its own 64-element segments when
-// j <= 32, so those stages need only a warp barrier; a CTA barrier precedes
-// every stage with j >= 64 (and follows the last one of each merge).
-__device__ __forceinline__ void bitonic_sort_smem(u64* buf, int P) {
-  const int half = P >> 1;
-  for (int k2 = 2; k2 <= P; k2 <<= 1) {
-    for (int j = k2 >> 1; j > 0; j >>= 1) {
-      for (int t = threadIdx.x; t < half; t += blockDim.x) {
-        const int i = 2 * t - (t & (j - 1));
-        const u64 a = buf[i], b = buf[i + j];
-        if ((a > b) == ((i & k2) == 0)) {
-          buf[i] = b;
-          buf[i + j] = a;
-        }
-      }
-      if (j > 32 || j == 1) __syncthreads();
-      else __syncwarp();
-    }
-  }
-}
-
 // block-wide AND / OR of per-thread values (all threads call; ends synchronized)
 __device__ __forceinline__ void block_and_or(u64& a, u64& o, u64 (*s_red)[2]) {
   const int lane = lane_id(), warp = threadIdx.x >> 5;

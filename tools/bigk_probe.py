@@ -31,11 +31,11 @@ for k, mode in cases:
     us = 1e3 * a.elapsed_time(b) / n
     print(f"{mode} k={k}: {us:.1f} us/batch -> {B / us:.2f} M q/s", flush=True)
 # full scan with k beyond the warp merge (general kernel over the whole corpus)
-fq = dq[:64]
-for k in (10, 64):
-    ids = torch.empty((64, k), dtype=torch.int32, device="cuda")
-    lcps = torch.empty((64, k), dtype=torch.int16, device="cuda")
-    hits = torch.empty(64, dtype=torch.int32, device="cuda")
+for nq, k in ((64, 10), (64, 64), (4096, 10), (4096, 32), (4096, 33), (4096, 64), (4096, 128), (64, 129)):
+    fq = dq[:nq]
+    ids = torch.empty((nq, k), dtype=torch.int32, device="cuda")
+    lcps = torch.empty((nq, k), dtype=torch.int16, device="cuda")
+    hits = torch.empty(nq, dtype=torch.int32, device="cuda")
     idx.native.fullscan_device(fq, k, ids, lcps, hits, stream=0)
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -43,4 +43,4 @@ for k in (10, 64):
     idx.native.fullscan_device(fq, k, ids, lcps, hits, stream=0)
     b.record()
     torch.cuda.synchronize()
-    print(f"fullscan k={k}, 64 queries: {1e3 * a.elapsed_time(b):.1f} us", flush=True)
+    print(f"fullscan k={k}, {nq} queries: {1e3 * a.elapsed_time(b):.1f} us", flush=True)
