@@ -1101,6 +1101,17 @@ static void prefer_carveout(int pct) {
   (void)done;
 }
 
+// opt in to more than 48 KB of dynamic shared memory, once per kernel
+template <auto Kernel>
+static void allow_dyn_smem() {
+  static const bool done = [] {  // thread-safe one-time initialisation
+    cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaGetLastError();
+    return true;
+  }();
+  (void)done;
+}
+
 template <typename C, int T>
 static void launch_w1(const DevIndex& dv, int mode, unsigned grid, unsigned block, size_t smem,
                       cudaStream_t st, const uint16_t* q, int count, int k, int stride, u32* ids,
@@ -1216,9 +1227,14 @@ static int query_impl(const lcp_index* ix, lcp_workspace* ws, const uint16_t* qu
     const long long wpc = std::min<long long>(wmax, std::max<long long>(1, (count + sms - 1) / sms));
     const unsigned block = (unsigned)(wpc * 32);
     const unsigned grid = (unsigned)std::min<long long>((count + wpc - 1) / wpc, 8ll * sms);
-    const size_t smem = 16 + (size_t)dv.smem_entries * 8;
-#define LCP_KN(C, M, NS) \
-  k_query_w1_kn<C, M, NS><<<grid, block, smem, st>>>(dv, queries, count, k, out_stride, ids, lcps, hits, md, ax, errp)
+    // staged levels, then one 32 * NS-entry merge buffer per warp
+    const size_t smem0 = 16 + (size_t)dv.smem_entries * 8;
+#define LCP_KN(C, M, NS)                                                                         \
+  do {                                                                                           \
+    allow_dyn_smem<k_query_w1_kn<C, M, NS>>();                                                   \
+    k_query_w1_kn<C, M, NS><<<grid, block, smem0 + (size_t)wpc * 32 * NS * sizeof(C), st>>>(    \
+        dv, queries, count, k, out_stride, ids, lcps, hits, md, ax, errp);                       \
+  } while (0)
     const bool strict = mode == LCP_MODE_STRICT;
     if (dv.idbits < 32) {
       if (needk <= 64) { if (strict) LCP_KN(u32, 0, 2); else LCP_KN(u32, 1, 2); }

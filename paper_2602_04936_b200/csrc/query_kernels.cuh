@@ -670,12 +670,68 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, MODE == 2 ? 1 : 2)
 // ---------------------------------------------------------------------------
 template <typename C, int NS>
 struct TopKN {
+  static constexpr int M = 32 * NS;
   C s[NS];  // s[j] on lane i holds rank 32 * j + i
   C thr;
-  __device__ __forceinline__ void init() {
+  C* sc;    // the warp's M-entry shared buffer (batch merges)
+  __device__ __forceinline__ void init(C* buf) {
 #pragma unroll
     for (int j = 0; j < NS; ++j) s[j] = ~C(0);
     thr = ~C(0);
+    sc = buf;
+  }
+  __device__ __forceinline__ void set_thr(int need) {
+    const int r = need - 1;
+    C sel = s[0];
+#pragma unroll
+    for (int j = 1; j < NS; ++j)
+      if ((r >> 5) == j) sel = s[j];
+    thr = __shfl_sync(LCP_FULL_MASK, sel, r & 31);
+  }
+  // Merges one candidate per lane at once: the batch is sorted across lanes
+  // (bitonic), list entry (lane, j) moves to rank 32 j + lane + #{batch < it}
+  // and batch entry q to q + #{list <= it} (ties list-first, so the ranks are
+  // a bijection onto [0, M + 32)); ranks below M are scattered through sc.
+  __device__ __forceinline__ void merge_batch(C x, int need) {
+    const int lane = lane_id();
+#pragma unroll
+    for (int k2 = 2; k2 <= 32; k2 <<= 1) {
+#pragma unroll
+      for (int j = k2 >> 1; j > 0; j >>= 1) {
+        const C y = __shfl_xor_sync(LCP_FULL_MASK, x, j);
+        x = (((lane & j) == 0) == ((lane & k2) == 0)) ? cmin(x, y) : cmax(x, y);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NS; ++j) sc[32 * j + lane] = s[j];
+    __syncwarp();
+    int nl = 0;
+#pragma unroll
+    for (int step = M / 2; step; step >>= 1)
+      if (sc[nl + step - 1] <= x) nl += step;
+    if (sc[nl] <= x) ++nl;
+    int nb[NS];
+#pragma unroll
+    for (int j = 0; j < NS; ++j) {
+      int p = 0;
+#pragma unroll
+      for (int step = 16; step; step >>= 1)
+        if (__shfl_sync(LCP_FULL_MASK, x, p + step - 1) < s[j]) p += step;
+      if (__shfl_sync(LCP_FULL_MASK, x, p) < s[j]) ++p;
+      nb[j] = p;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < NS; ++j) {
+      const int r = 32 * j + lane + nb[j];
+      if (r < M) sc[r] = s[j];
+    }
+    if (lane + nl < M) sc[lane + nl] = x;
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < NS; ++j) s[j] = sc[32 * j + lane];
+    __syncwarp();
+    set_thr(need);
   }
   __device__ __forceinline__ void insert(C c, int need) {
     const int lane = lane_id();
@@ -692,16 +748,16 @@ struct TopKN {
       const C prev = lane == 0 ? (j > 0 ? top[j > 0 ? j - 1 : 0] : s[j]) : up;
       s[j] = h > p ? prev : (h == p ? c : s[j]);
     }
-    const int r = need - 1;
-    C sel = s[0];
-#pragma unroll
-    for (int j = 1; j < NS; ++j)
-      if ((r >> 5) == j) sel = s[j];
-    thr = __shfl_sync(LCP_FULL_MASK, sel, r & 31);
+    set_thr(need);
   }
-  // one candidate per lane (all-ones = none)
+  // one candidate per lane (all-ones = none): a few by single insertions,
+  // more by one batch merge
   __device__ __forceinline__ void offer(C comp, int need) {
     unsigned m = __ballot_sync(LCP_FULL_MASK, comp < thr);
+    if (__popc(m) > 4) {
+      merge_batch(comp < thr ? comp : ~C(0), need);
+      return;
+    }
     while (m) {
       const int src = __ffs(m) - 1;
       m &= m - 1;
@@ -834,7 +890,7 @@ __global__ void __launch_bounds__(NS > 2 ? QW_MAX_THREADS / 2 : QW_MAX_THREADS, 
     dmax = (int)__reduce_max_sync(LCP_FULL_MASK, (unsigned)(dmax + 1)) - 1;
     const int dstar = MODE == 0 ? dmax : window_dstar<T>(l, dmax, need);
     TopKN<C, NS> lst;
-    lst.init();
+    lst.init(reinterpret_cast<C*>(smem_raw + 16 + (size_t)ix.smem_entries * 8) + warp * (32 * NS));
     int cnt = 0, r0 = 32 * T, above = 0;
 #pragma unroll
     for (int t = 0; t < T; ++t) {
