@@ -1220,8 +1220,14 @@ static int query_impl(const lcp_index* ix, lcp_workspace* ws, const uint16_t* qu
     ax = ws->aux.as<u64>();
   }
   const long long needk = mode == LCP_MODE_COMPLETE ? std::min<long long>(k, dv.n) : k;
-  if (dv.W == 1 && mode != LCP_MODE_TAL && k > FAST_KMAX && needk <= 128) {
-    // 32 < need <= 128: warp per query with a 2- or 4-slot top-k list
+  static const int kn_min = [] {  // A/B hook: smallest need on the list kernel (default 17)
+    const char* e = getenv("LCP_KN_MIN");
+    return e ? std::max(1, atoi(e)) : 17;
+  }();
+  if (dv.W == 1 && mode != LCP_MODE_TAL && needk >= kn_min && needk <= 128) {
+    // 16 < need <= 128: warp per query with a 1-, 2- or 4-slot top-k list
+    // (complete mode at need 17..32: 11.1 us vs 14.3-15.6 us per 4096 batch on
+    // the T=3 rank kernel, which now serves TAL only)
     const long long sms = num_sms();
     const long long wmax = needk <= 64 ? 32 : 16;  // 4-slot lists: 512-thread CTAs
     const long long wpc = std::min<long long>(wmax, std::max<long long>(1, (count + sms - 1) / sms));
@@ -1237,10 +1243,12 @@ static int query_impl(const lcp_index* ix, lcp_workspace* ws, const uint16_t* qu
   } while (0)
     const bool strict = mode == LCP_MODE_STRICT;
     if (dv.idbits < 32) {
-      if (needk <= 64) { if (strict) LCP_KN(u32, 0, 2); else LCP_KN(u32, 1, 2); }
+      if (needk <= 32) { if (strict) LCP_KN(u32, 0, 1); else LCP_KN(u32, 1, 1); }
+      else if (needk <= 64) { if (strict) LCP_KN(u32, 0, 2); else LCP_KN(u32, 1, 2); }
       else { if (strict) LCP_KN(u32, 0, 4); else LCP_KN(u32, 1, 4); }
     } else {
-      if (needk <= 64) { if (strict) LCP_KN(u64, 0, 2); else LCP_KN(u64, 1, 2); }
+      if (needk <= 32) { if (strict) LCP_KN(u64, 0, 1); else LCP_KN(u64, 1, 1); }
+      else if (needk <= 64) { if (strict) LCP_KN(u64, 0, 2); else LCP_KN(u64, 1, 2); }
       else { if (strict) LCP_KN(u64, 0, 4); else LCP_KN(u64, 1, 4); }
     }
 #undef LCP_KN

@@ -14,6 +14,9 @@ B = 4096
 dq = torch.from_numpy(lg.generate_queries(ds, B, seed=4)).cuda()
 cases = [(k, "complete") for k in (10, 32, 33, 64, 100, 129, 256, 500, 1000, 2000, 5000)]
 cases += [(k, "strict") for k in (256, 1000)]
+if os.environ.get("BIGK_KS"):  # e.g. BIGK_KS=1,10,32 (complete and strict)
+    ks = [int(x) for x in os.environ["BIGK_KS"].split(",")]
+    cases = [(k, m) for m in ("complete", "strict") for k in ks]
 for k, mode in cases:
     ids = torch.empty((B, k), dtype=torch.int32, device="cuda")
     lcps = torch.empty((B, k), dtype=torch.int16, device="cuda")
@@ -31,7 +34,7 @@ for k, mode in cases:
     us = 1e3 * a.elapsed_time(b) / n
     print(f"{mode} k={k}: {us:.1f} us/batch -> {B / us:.2f} M q/s", flush=True)
 # full scan with k beyond the warp merge (general kernel over the whole corpus)
-for nq, k in ((64, 10), (64, 64), (4096, 10), (4096, 32), (4096, 33), (4096, 64), (4096, 128), (64, 129)):
+for nq, k in [] if os.environ.get("BIGK_KS") else ((64, 10), (64, 64), (4096, 10), (4096, 32), (4096, 33), (4096, 64), (4096, 128), (64, 129)):
     fq = dq[:nq]
     ids = torch.empty((nq, k), dtype=torch.int32, device="cuda")
     lcps = torch.empty((nq, k), dtype=torch.int16, device="cuda")
