@@ -154,6 +154,11 @@ __device__ __forceinline__ u64 widen_comp(C c, int idbits) {
 // ---- warp top-k (slot i on lane i holds the i-th smallest) ---------------
 
 template <typename C>
+__device__ __forceinline__ C cmin(C a, C b) { return a < b ? a : b; }
+template <typename C>
+__device__ __forceinline__ C cmax(C a, C b) { return a < b ? b : a; }
+
+template <typename C>
 __device__ __forceinline__ void warp_insert(C& slot, C c) {
   const int lane = lane_id();
   unsigned lt = __ballot_sync(LCP_FULL_MASK, slot < c);
@@ -166,8 +171,36 @@ __device__ __forceinline__ void warp_insert(C& slot, C c) {
 // Offer one candidate per lane (all-ones = none); keeps the `need`
 // smallest.  thr caches slot[need-1].
 template <typename C>
+__device__ __forceinline__ C warp_sort32(C v);
+
+// Batch merge for warp_offer: sort the batch, reverse it against the sorted
+// list, keep the lane-wise minima (the 32 smallest of both, a bitonic
+// sequence) and finish with a bitonic merge.  Out of line so the callers'
+// hot loops keep their register budget (it runs on extension paths only).
+template <typename C>
+__device__ __noinline__ C warp_merge32(C slot, C batch) {
+  const int lane = lane_id();
+  C v = warp_sort32(batch);
+  v = cmin(slot, __shfl_sync(LCP_FULL_MASK, v, 31 - lane));
+#pragma unroll
+  for (int j = 16; j > 0; j >>= 1) {
+    const C p = __shfl_xor_sync(LCP_FULL_MASK, v, j);
+    v = (lane & j) == 0 ? cmin(v, p) : cmax(v, p);
+  }
+  return v;
+}
+
+// BATCH: merge more than six candidates at once (warp_merge32).  Off in the
+// 32-register query kernels and their out-of-line helpers: the extra call
+// level made k_query_w1 spill and cost 1 % of headline throughput.
+template <typename C, bool BATCH = false>
 __device__ __forceinline__ void warp_offer(C& slot, C& thr, C comp, int need) {
   unsigned m = __ballot_sync(LCP_FULL_MASK, comp < thr);
+  if (BATCH && __popc(m) > 6) {
+    slot = warp_merge32(slot, comp < thr ? comp : ~C(0));
+    thr = __shfl_sync(LCP_FULL_MASK, slot, need - 1);
+    return;
+  }
   while (m) {
     int src = __ffs(m) - 1;
     m &= m - 1;
@@ -178,11 +211,6 @@ __device__ __forceinline__ void warp_offer(C& slot, C& thr, C comp, int need) {
     }
   }
 }
-
-template <typename C>
-__device__ __forceinline__ C cmin(C a, C b) { return a < b ? a : b; }
-template <typename C>
-__device__ __forceinline__ C cmax(C a, C b) { return a < b ? b : a; }
 
 // Bitonic sort of 32 values, one per lane: lane i ends with the i-th smallest.
 template <typename C>

@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(256)
       u64 c = j < kin ? cand[s * s_stride + qi * q_stride + j] : ~0ull;
       if (strict && (c >> 32) != tier) c = ~0ull;
       valid += __popc(__ballot_sync(LCP_FULL_MASK, c != ~0ull));
-      warp_offer(slot, thr, c, take);
+      warp_offer<u64, true>(slot, thr, c, take);
     }
   }
   const int hits = min(take, valid);
