@@ -180,7 +180,7 @@ def test_random_vs_oracle(gpu, oracle_lib, chunk, monkeypatch):
         qs = lg.generate_queries(ds, 48, seed=t + 99)
         if n:
             qs = np.vstack([qs, lg.generate_queries(ds, 48, seed=t + 98, prefix_len=L // 2)])
-        for k in (1, 3, 10, 32, 33, 64, 70, 100, 129):  # warp k<=32 / 2-slot / 4-slot / CTA paths
+        for k in (1, 3, 10, 20, 24, 32, 33, 64, 70, 100, 129):  # rank k<=16 / 1-, 2-, 4-slot lists / CTA paths
             for mode in ("complete", "strict"):
                 b = idx.query_batch(qs, k, mode)
                 ids, lcps, hits, md, sym, nodes = ot.query_batch(qs, k, mode)

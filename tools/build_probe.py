@@ -26,3 +26,11 @@ for i in range(10):
     torch.cuda.synchronize()
     print(f"device-rows build {i}: {1e3 * (time.perf_counter() - t):.1f} ms")
     del ni
+# replicas kept alive (as bench.py does): pool growth instead of reuse
+kept = []
+for i in range(8):
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    kept.append(lg.build(ds))
+    torch.cuda.synchronize()
+    print(f"kept build {i}: {1e3 * (time.perf_counter() - t):.1f} ms")
