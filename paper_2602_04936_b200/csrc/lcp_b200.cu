@@ -1224,10 +1224,12 @@ static int query_impl(const lcp_index* ix, lcp_workspace* ws, const uint16_t* qu
     const char* e = getenv("LCP_KN_MIN");
     return e ? std::max(1, atoi(e)) : 17;
   }();
-  if (dv.W == 1 && mode != LCP_MODE_TAL && needk >= kn_min && needk <= 128) {
-    // 16 < need <= 128: warp per query with a 1-, 2- or 4-slot top-k list
-    // (complete mode at need 17..32: 11.1 us vs 14.3-15.6 us per 4096 batch on
-    // the T=3 rank kernel, which now serves TAL only)
+  const bool kn_ok = needk >= kn_min;
+  if (dv.W == 1 && kn_ok && needk <= 128) {
+    // 16 < need <= 128 (strict, complete, TAL): warp per query with a 1-, 2-
+    // or 4-slot top-k list.  At need 17..32 it beats the T=3 rank kernel
+    // (complete 11.1 vs 14.3-15.6 us, TAL 28.6 vs 33.3 us per 4096 batch),
+    // which now runs only when LCP_KN_MIN raises the threshold
     const long long sms = num_sms();
     const long long wmax = needk <= 64 ? 32 : 16;  // 4-slot lists: 512-thread CTAs
     const long long wpc = std::min<long long>(wmax, std::max<long long>(1, (count + sms - 1) / sms));
@@ -1241,15 +1243,15 @@ static int query_impl(const lcp_index* ix, lcp_workspace* ws, const uint16_t* qu
     k_query_w1_kn<C, M, NS><<<grid, block, smem0 + (size_t)wpc * 32 * NS * sizeof(C), st>>>(    \
         dv, queries, count, k, out_stride, ids, lcps, hits, md, ax, errp);                       \
   } while (0)
-    const bool strict = mode == LCP_MODE_STRICT;
+    const bool strict = mode == LCP_MODE_STRICT, tal = mode == LCP_MODE_TAL;
     if (dv.idbits < 32) {
-      if (needk <= 32) { if (strict) LCP_KN(u32, 0, 1); else LCP_KN(u32, 1, 1); }
-      else if (needk <= 64) { if (strict) LCP_KN(u32, 0, 2); else LCP_KN(u32, 1, 2); }
-      else { if (strict) LCP_KN(u32, 0, 4); else LCP_KN(u32, 1, 4); }
+      if (needk <= 32) { if (tal) LCP_KN(u32, 2, 1); else if (strict) LCP_KN(u32, 0, 1); else LCP_KN(u32, 1, 1); }
+      else if (needk <= 64) { if (tal) LCP_KN(u32, 2, 2); else if (strict) LCP_KN(u32, 0, 2); else LCP_KN(u32, 1, 2); }
+      else { if (tal) LCP_KN(u32, 2, 4); else if (strict) LCP_KN(u32, 0, 4); else LCP_KN(u32, 1, 4); }
     } else {
-      if (needk <= 32) { if (strict) LCP_KN(u64, 0, 1); else LCP_KN(u64, 1, 1); }
-      else if (needk <= 64) { if (strict) LCP_KN(u64, 0, 2); else LCP_KN(u64, 1, 2); }
-      else { if (strict) LCP_KN(u64, 0, 4); else LCP_KN(u64, 1, 4); }
+      if (needk <= 32) { if (tal) LCP_KN(u64, 2, 1); else if (strict) LCP_KN(u64, 0, 1); else LCP_KN(u64, 1, 1); }
+      else if (needk <= 64) { if (tal) LCP_KN(u64, 2, 2); else if (strict) LCP_KN(u64, 0, 2); else LCP_KN(u64, 1, 2); }
+      else { if (tal) LCP_KN(u64, 2, 4); else if (strict) LCP_KN(u64, 0, 4); else LCP_KN(u64, 1, 4); }
     }
 #undef LCP_KN
     LCP_CK_LAUNCH();

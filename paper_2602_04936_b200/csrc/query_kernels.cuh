@@ -383,6 +383,77 @@ __device__ __forceinline__ int level_count_g(const u64* __restrict__ tab, int bl
 
 // strict / complete: <= 32 regs, so two batches share an SM; TAL: 64 regs
 // for the unrolled bucket sweep
+// TAL bucket [blo, bhi) of the packed W == 1 query q (tal.py:116-143): the
+// dense directory when built, else the two prefix bounds
+__device__ __forceinline__ void tal_bucket_w1(const DevIndex& ix, u64 q, int& blo, int& bhi) {
+  const int d = ix.tal_depth, b = ix.b;
+  if (d > 0) {
+    if (ix.directory) {
+      long long code = 0;
+      for (int j = 0; j < d; ++j)
+        code = code * ix.sigma + (long long)((q >> (64 - b * (j + 1))) & ((1ull << b) - 1));
+      blo = (int)__ldg(ix.directory + code);
+      bhi = (int)__ldg(ix.directory + code + 1);
+    } else {
+      u64 qk1[1] = {q};
+      blo = (int)prefix_bound(ix, qk1, d, false);
+      bhi = (int)prefix_bound(ix, qk1, d, true);
+    }
+  }
+}
+
+// symbols_compared = sum over the bucket [blo, bhi) of min(lcp + 1, L)
+// (tal.py:173-177) for a W == 1 query; the warp total on every lane.
+// Bits past symbol L are zero in keys and query, so x = key ^ q is nonzero
+// exactly when lcp < L, and min(lcp + 1, L) = 1 + min(clz64(x) >> lb, L - 1)
+// with no branch (clz64(0) = 64).  The sweep reads the sorted high-word plane
+// (4 B per key): clz64(x) = clz32(hi ^ qh) unless the high words match, and
+// only then (lcp >= 32 / b symbols, rare inside a bucket) is the full key
+// read.  Aligned 16-byte groups of 4 keys, 16 keys per lane in flight; the
+// keys at either end outside whole groups go one per lane.
+__device__ __forceinline__ unsigned long long tal_sym_w1(const DevIndex& ix, u64 q, int blo, int bhi) {
+  const int lane = lane_id();
+  const int lb = ix.lb, lm1 = ix.L - 1;
+  const u32 qh = (u32)(q >> 32);
+  const u32* __restrict__ shi = ix.keys_shi;
+  const u64* __restrict__ keys = ix.keys;
+  auto term = [&](u32 h, int i) -> u32 {
+    const int c = h != qh ? __clz(h ^ qh) : __clzll((long long)(__ldg(keys + i) ^ q));
+    return (u32)min(c >> lb, lm1);
+  };
+  unsigned long long sym = 0;
+  const int a0 = (blo + 3) & ~3, e0 = bhi & ~3;
+  constexpr int TAL_UNROLL = 4;
+  int base = a0 + 4 * lane;
+  for (; base + 128 * (TAL_UNROLL - 1) < e0; base += 128 * TAL_UNROLL) {
+    uint4 hv[TAL_UNROLL];
+#pragma unroll
+    for (int u = 0; u < TAL_UNROLL; ++u)
+      hv[u] = __ldg(reinterpret_cast<const uint4*>(shi + base + 128 * u));
+    u32 part = 0;
+#pragma unroll
+    for (int u = 0; u < TAL_UNROLL; ++u) {
+      const int i = base + 128 * u;
+      part += term(hv[u].x, i) + term(hv[u].y, i + 1) + term(hv[u].z, i + 2) + term(hv[u].w, i + 3);
+    }
+    sym += part;
+  }
+  for (; base < e0; base += 128) {
+    const uint4 hv = __ldg(reinterpret_cast<const uint4*>(shi + base));
+    sym += term(hv.x, base) + term(hv.y, base + 1) + term(hv.z, base + 2) + term(hv.w, base + 3);
+  }
+  if (e0 >= a0) {  // up to 3 keys before a0 and after e0
+    const int i = lane < 3 ? blo + lane : e0 + lane - 3;
+    if ((lane < 3 && i < a0) || (lane >= 3 && lane < 6 && i < bhi)) sym += term(__ldg(shi + i), i);
+  } else if (lane < bhi - blo) {  // the whole bucket lies inside one group
+    sym += term(__ldg(shi + blo + lane), blo + lane);
+  }
+  if (lane == 0) sym += (unsigned long long)(bhi - blo);  // the "+1" of every item
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sym += __shfl_xor_sync(LCP_FULL_MASK, sym, o);
+  return sym;
+}
+
 template <typename C, int T, int MODE>
 __global__ void __launch_bounds__(QW_MAX_THREADS, MODE == 2 ? 1 : 2)
     k_query_w1(const __grid_constant__ DevIndex ix, const uint16_t* __restrict__ queries, int count, int k,
@@ -435,22 +506,7 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, MODE == 2 ? 1 : 2)
     // TAL: the query's d-prefix bucket [blo, bhi) (tal.py:116-143), looked up
     // before the search so the directory read overlaps it
     int blo = 0, bhi = n;
-    if constexpr (MODE == 2) {
-      const int d = ix.tal_depth;
-      if (d > 0) {
-        if (ix.directory) {
-          long long code = 0;
-          for (int j = 0; j < d; ++j)
-            code = code * ix.sigma + (long long)((q >> (64 - b * (j + 1))) & ((1ull << b) - 1));
-          blo = (int)__ldg(ix.directory + code);
-          bhi = (int)__ldg(ix.directory + code + 1);
-        } else {
-          u64 qk1[1] = {q};
-          blo = (int)prefix_bound(ix, qk1, d, false);
-          bhi = (int)prefix_bound(ix, qk1, d, true);
-        }
-      }
-    }
+    if constexpr (MODE == 2) tal_bucket_w1(ix, q, blo, bhi);
     stage_wait(ix, bar);  // first iteration: the query load overlaps the copy
     LCP_STAMP(qi, 1);
     // 64-ary search down to the 16-key leaf block holding lower_bound(q).
@@ -501,53 +557,7 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, MODE == 2 ? 1 : 2)
     u64 aux0 = 0, aux1 = 0;
     bool tal_small = false;  // bucket smaller than k: answer = the whole bucket
     if constexpr (MODE == 2) {
-      // symbols_compared = sum over the bucket of min(lcp + 1, L)
-      // (tal.py:173-177): every bucket item's lcp, coalesced 16-byte loads
-      // W == 1: bits past symbol L are zero in keys and query, so x = key ^ q
-      // is nonzero exactly when lcp < L, and min(lcp + 1, L) =
-      // 1 + min(clz64(x) >> lb, L - 1) with no branch (clz64(0) = 64).
-      // The sweep reads the sorted high-word plane (4 B per key): clz64(x) =
-      // clz32(hi ^ qh) unless the high words match, and only then (lcp >=
-      // 32 / b symbols, rare inside a bucket) is the full key read.
-      // Aligned 16-byte groups of 4 keys, 16 keys per lane in flight; the
-      // keys at either end outside whole groups go one per lane.
-      const int lm1 = L - 1;
-      const u32 qh = (u32)(q >> 32);
-      const u32* __restrict__ shi = ix.keys_shi;
-      auto term = [&](u32 h, int i) -> u32 {
-        const int c = h != qh ? __clz(h ^ qh) : __clzll((long long)(__ldg(keys + i) ^ q));
-        return (u32)min(c >> lb, lm1);
-      };
-      unsigned long long sym = 0;
-      const int a0 = (blo + 3) & ~3, e0 = bhi & ~3;
-      constexpr int TAL_UNROLL = 4;
-      int base = a0 + 4 * lane;
-      for (; base + 128 * (TAL_UNROLL - 1) < e0; base += 128 * TAL_UNROLL) {
-        uint4 hv[TAL_UNROLL];
-#pragma unroll
-        for (int u = 0; u < TAL_UNROLL; ++u)
-          hv[u] = __ldg(reinterpret_cast<const uint4*>(shi + base + 128 * u));
-        u32 part = 0;
-#pragma unroll
-        for (int u = 0; u < TAL_UNROLL; ++u) {
-          const int i = base + 128 * u;
-          part += term(hv[u].x, i) + term(hv[u].y, i + 1) + term(hv[u].z, i + 2) + term(hv[u].w, i + 3);
-        }
-        sym += part;
-      }
-      for (; base < e0; base += 128) {
-        const uint4 hv = __ldg(reinterpret_cast<const uint4*>(shi + base));
-        sym += term(hv.x, base) + term(hv.y, base + 1) + term(hv.z, base + 2) + term(hv.w, base + 3);
-      }
-      if (e0 >= a0) {  // up to 3 keys before a0 and after e0
-        const int i = lane < 3 ? blo + lane : e0 + lane - 3;
-        if ((lane < 3 && i < a0) || (lane >= 3 && lane < 6 && i < bhi)) sym += term(__ldg(shi + i), i);
-      } else if (lane < bhi - blo) {  // the whole bucket lies inside one group
-        sym += term(__ldg(shi + blo + lane), blo + lane);
-      }
-      if (lane == 0) sym += (unsigned long long)(bhi - blo);  // the "+1" of every item
-#pragma unroll
-      for (int o = 16; o; o >>= 1) sym += __shfl_xor_sync(LCP_FULL_MASK, sym, o);
+      const unsigned long long sym = tal_sym_w1(ix, q, blo, bhi);
       md = ix.tal_depth;
       aux0 = (u64)(bhi - blo);
       aux1 = sym;
@@ -821,7 +831,10 @@ __global__ void __launch_bounds__(NS > 2 ? QW_MAX_THREADS / 2 : QW_MAX_THREADS, 
                    int count, int k, int stride, u32* __restrict__ out_ids,
                    uint16_t* __restrict__ out_lcps, int* __restrict__ out_hits,
                    uint16_t* __restrict__ out_md, u64* __restrict__ out_aux, int* __restrict__ err) {
-  // MODE: 0 strict, 1 complete; need <= 32 * NS; region 32 * (2 NS + 1) keys
+  // MODE: 0 strict, 1 complete, 2 tal; need <= 32 * NS; region 32 * (2 NS + 1)
+  // keys.  TAL (k > 32 here): the complete answer with need = k when the
+  // bucket holds >= k items, else the whole bucket ranked; symbols_compared by
+  // the bucket sweep (see k_query_w1)
   constexpr int T = 2 * NS + 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   u64* bar = reinterpret_cast<u64*>(smem_raw);
@@ -859,6 +872,8 @@ __global__ void __launch_bounds__(NS > 2 ? QW_MAX_THREADS / 2 : QW_MAX_THREADS, 
       }
       continue;
     }
+    int blo = 0, bhi = n;
+    if constexpr (MODE == 2) tal_bucket_w1(ix, q, blo, bhi);
     int blk = 0;
     if (ix.nlevels > 0) {
       const int c0 = ix.smem_levels > 0 ? level_count(staged, 0, q) : level_count_g(ix.levels, 0, q);
@@ -888,9 +903,40 @@ __global__ void __launch_bounds__(NS > 2 ? QW_MAX_THREADS / 2 : QW_MAX_THREADS, 
       dmax = max(dmax, l[t]);
     }
     dmax = (int)__reduce_max_sync(LCP_FULL_MASK, (unsigned)(dmax + 1)) - 1;
-    const int dstar = MODE == 0 ? dmax : window_dstar<T>(l, dmax, need);
     TopKN<C, NS> lst;
     lst.init(reinterpret_cast<C*>(smem_raw + 16 + (size_t)ix.smem_entries * 8) + warp * (32 * NS));
+    unsigned long long tsym = 0;
+    if constexpr (MODE == 2) {
+      tsym = tal_sym_w1(ix, q, blo, bhi);
+      const int bs = bhi - blo;
+      if (bs < k) {  // the whole bucket, ranked (an empty one included)
+        for (int base = blo; base < bhi; base += 32) {
+          const int i = base + lane;
+          C cv = ~C(0);
+          if (i < bhi) {
+            const u64 x = __ldg(keys + i) ^ q;
+            cv = make_comp<C>(x ? (__clzll((long long)x) >> lb) : L, __ldg(order + i), L, idbits);
+          }
+          lst.offer(cv, k);
+        }
+#pragma unroll
+        for (int j = 0; j < NS; ++j) {
+          if (lane + 32 * j < bs) {
+            const u64 w = widen_comp<C>(lst.s[j], idbits);
+            out_ids[(size_t)qi * stride + lane + 32 * j] = (u32)(w & 0xffffffffull);
+            out_lcps[(size_t)qi * stride + lane + 32 * j] = (uint16_t)(L - (int)(w >> 32));
+          }
+        }
+        if (lane == 0) {
+          out_hits[qi] = bs;
+          out_md[qi] = (uint16_t)ix.tal_depth;
+          out_aux[2 * qi] = (u64)bs;
+          out_aux[2 * qi + 1] = tsym;
+        }
+        continue;
+      }
+    }
+    const int dstar = MODE == 0 ? dmax : window_dstar<T>(l, dmax, need);
     int cnt = 0, r0 = 32 * T, above = 0;
 #pragma unroll
     for (int t = 0; t < T; ++t) {
@@ -960,9 +1006,15 @@ __global__ void __launch_bounds__(NS > 2 ? QW_MAX_THREADS / 2 : QW_MAX_THREADS, 
     }
     if (lane == 0) {
       out_hits[qi] = take;
-      out_md[qi] = (uint16_t)dmax;
-      out_aux[2 * qi] = (u64)(u32)dmax | ((u64)(u32)dstar << 32);
-      out_aux[2 * qi + 1] = (u64)rsize | ((u64)rlo << 32);
+      if constexpr (MODE == 2) {
+        out_md[qi] = (uint16_t)ix.tal_depth;
+        out_aux[2 * qi] = (u64)(bhi - blo);
+        out_aux[2 * qi + 1] = tsym;
+      } else {
+        out_md[qi] = (uint16_t)dmax;
+        out_aux[2 * qi] = (u64)(u32)dmax | ((u64)(u32)dstar << 32);
+        out_aux[2 * qi + 1] = (u64)rsize | ((u64)rlo << 32);
+      }
     }
   }
 }
