@@ -508,3 +508,10 @@ __global__ void k_snap_postings(const int* __restrict__ row_lo, const long long*
   const long long v = off[L] + lo - 1;
   put_u32(out + start[v] + 6 + 4ull * (unsigned long long)(i - leaf[lo - 1]), order[i]);
 }
+
+// rank[order[i]] = i: original id -> sorted position
+__global__ void k_invert(const u32* __restrict__ order, long long n, u32* __restrict__ rank) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    rank[order[i]] = (u32)i;
+}

@@ -49,6 +49,7 @@ struct DevIndex {
   // positions, its LCP_SK_LIST smallest ids ascending (0xffffffff padded).
   // Serves "smallest ids in a long sorted range" when R(d*) is huge.
   const u32* sketch;
+  const u32* rank;  // original id -> sorted position (inverse of order)
   long long sk_off[LCP_MAX_LEVELS];  // block offset of level j (lists of LCP_SK_LIST)
   long long sk_cnt[LCP_MAX_LEVELS];  // blocks at level j
   int sk_levels;

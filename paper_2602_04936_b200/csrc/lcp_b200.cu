@@ -241,6 +241,7 @@ struct lcp_index {
   u64* levels = nullptr;
   long long* directory = nullptr;
   u32* sketch = nullptr;
+  u32* rank = nullptr;  // original id -> sorted position
   u64* keys_w0 = nullptr;
   u32* keys_shi = nullptr;
   std::vector<long long> level_offset;  // cached trie level offsets
@@ -298,6 +299,7 @@ int lcp_index_free(lcp_index* ix) {
   if (ix->levels) cudaFreeAsync(ix->levels, 0);
   if (ix->directory) cudaFreeAsync(ix->directory, 0);
   if (ix->sketch) cudaFreeAsync(ix->sketch, 0);
+  if (ix->rank) cudaFreeAsync(ix->rank, 0);
   if (ix->keys_w0) cudaFreeAsync(ix->keys_w0, 0);
   if (ix->keys_shi) cudaFreeAsync(ix->keys_shi, 0);
   cudaStreamSynchronize(0);
@@ -501,6 +503,12 @@ static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, i
     }
     dv.sketch = ix->sketch;
   }
+  // inverse permutation (id -> sorted position): lets the general path take
+  // the smallest ids of a tier that spans most of the corpus in id order
+  LCP_TRY(dalloc(&ix->rank, std::max(1ll, n), acct, st));
+  k_invert<<<blocks_for(n, 256), 256, 0, st>>>(ix->order, n, ix->rank);
+  LCP_CK_LAUNCH();
+  dv.rank = ix->rank;
 
   phase("sketch");
   // TAL bucket structure — tal.py:42-82

@@ -1435,6 +1435,9 @@ __global__ void __launch_bounds__(GEN_THREADS)
   __shared__ u32 s_rank;
   __shared__ unsigned long long s_sym;
   __shared__ long long s_pos;
+  __shared__ long long s_p0;    // a position with lcp = d_max (strict / complete)
+  __shared__ long long s_a, s_b;  // R(d* + 1) for the split selection
+  __shared__ int s_wc[GEN_THREADS / 32];
   __shared__ long long s_part[GEN_THREADS / 32][2];
   __shared__ u64 s_red[GEN_THREADS / 32][2];
   const int L = ix.L;
@@ -1516,6 +1519,7 @@ __global__ void __launch_bounds__(GEN_THREADS)
           s_dstar = dstar;
           s_md = dmax;
           s_sym = 0;
+          s_p0 = pos < ix.n && wl[pos - wlo] == dmax ? pos : pos - 1;
         }
       }
     } else if (!fullscan && mode != 2 && ix.n > 0) {
@@ -1555,6 +1559,7 @@ __global__ void __launch_bounds__(GEN_THREADS)
           s_dstar = dstar;
           s_md = dmax;
           s_sym = 0;
+          s_p0 = p0;
         }
       }
     } else if (threadIdx.x == 0) {
@@ -1590,90 +1595,152 @@ __global__ void __launch_bounds__(GEN_THREADS)
         out_lcps[qi * stride + at + t] = (uint16_t)(L - (int)(c >> 32));
       }
     };
-
-    if (size <= GEN_CAP) {
-      int P = 1, Pt = 1;
-      while (P < size) P <<= 1;
-      while (Pt < take) Pt <<= 1;
-      constexpr int PER = GEN_CAP / GEN_THREADS;
-      u64 v[PER];
-#pragma unroll
-      for (int r = 0; r < PER; ++r) {
-        const int t = threadIdx.x + r * GEN_THREADS;
-        v[r] = ~0ull;
-        if (t < size) {
-          int l;
-          v[r] = it.comp(lo + t, &l);
-          sym += (unsigned long long)min(l + 1, L);
-          vand &= v[r];
-          vor |= v[r];
-        }
-        if (t < P) buf[t] = v[r];
-      }
-      if (take > 0 && 2 * Pt <= P) {
-        // select, then sort only the take smallest (a power of two at least
-        // half as large): threshold by radix select over the staged values,
-        // compaction through registers back into buf
-        block_and_or(vand, vor, s_red);
-        const u64 T = radix_select([&](long long i) { return buf[i]; }, 0, size, true, 0ull,
-                                   (u32)take, vand, vand ^ vor, hist, &s_prefix, &s_rank);
-        if (threadIdx.x == 0) s_cnt = 0;
-        __syncthreads();
-#pragma unroll
-        for (int r = 0; r < PER; ++r) warp_append(v[r] <= T, v[r], buf, &s_cnt, (u32)Pt);
-        __syncthreads();
-        for (int t = (int)take + threadIdx.x; t < Pt; t += GEN_THREADS) buf[t] = ~0ull;
-        P = Pt;
-      }
-      __syncthreads();
-      bitonic_sort_smem(buf, P);
-      emit(buf, 0, (int)take);
-    } else {
-      // one pass for symbols_compared and the value span, then rounds of
-      // GEN_CAP: radix select of the round's last value, collect (last, T], sort
-      for (long long i = lo + threadIdx.x; i < hi; i += GEN_THREADS) {
-        int l;
-        const u64 c = it.comp(i, &l);
-        sym += (unsigned long long)min(l + 1, L);
-        vand &= c;
-        vor |= c;
-      }
-      block_and_or(vand, vor, s_red);
-      long long emitted = 0;
-      u64 last = 0;
-      bool first = true;
-      auto get = [&](long long i) {
-        int l;
-        return it.comp(i, &l);
-      };
-      while (emitted < take) {
-        const u32 want = (u32)min((long long)GEN_CAP, take - emitted);
-        const u64 T = radix_select(get, lo, hi, first, last, want, vand, vand ^ vor, hist,
-                                   &s_prefix, &s_rank);
-        if (threadIdx.x == 0) s_cnt = 0;
-        __syncthreads();
-        for (long long b = lo; b < hi; b += GEN_THREADS) {
-          const long long i = b + threadIdx.x;
-          u64 c = 0;
-          bool in = false;
-          if (i < hi) {
-            c = get(i);
-            in = (first || c > last) && c <= T;
+    // the take smallest composites of sorted positions (full scan: original
+    // rows) [lo, hi), ascending, written from output slot `at`
+    // the take smallest composites of sorted positions (full scan: original
+    // rows) [lo, hi), ascending, written from output slot `at`
+    auto select_range = [&](const long long lo, const long long hi, const long long take,
+                            const long long at) {
+      const long long size = hi - lo;
+      if (size <= GEN_CAP) {
+        int P = 1, Pt = 1;
+        while (P < size) P <<= 1;
+        while (Pt < take) Pt <<= 1;
+        constexpr int PER = GEN_CAP / GEN_THREADS;
+        u64 v[PER];
+  #pragma unroll
+        for (int r = 0; r < PER; ++r) {
+          const int t = threadIdx.x + r * GEN_THREADS;
+          v[r] = ~0ull;
+          if (t < size) {
+            int l;
+            v[r] = it.comp(lo + t, &l);
+            sym += (unsigned long long)min(l + 1, L);
+            vand &= v[r];
+            vor |= v[r];
           }
-          warp_append(in, c, buf, &s_cnt, GEN_CAP);
+          if (t < P) buf[t] = v[r];
         }
-        __syncthreads();
-        int P = 1;
-        while (P < (int)want) P <<= 1;
-        for (int t = (int)want + threadIdx.x; t < P; t += GEN_THREADS) buf[t] = ~0ull;
+        if (take > 0 && 2 * Pt <= P) {
+          // select, then sort only the take smallest (a power of two at least
+          // half as large): threshold by radix select over the staged values,
+          // compaction through registers back into buf
+          block_and_or(vand, vor, s_red);
+          const u64 T = radix_select([&](long long i) { return buf[i]; }, 0, size, true, 0ull,
+                                     (u32)take, vand, vand ^ vor, hist, &s_prefix, &s_rank);
+          if (threadIdx.x == 0) s_cnt = 0;
+          __syncthreads();
+  #pragma unroll
+          for (int r = 0; r < PER; ++r) warp_append(v[r] <= T, v[r], buf, &s_cnt, (u32)Pt);
+          __syncthreads();
+          for (int t = (int)take + threadIdx.x; t < Pt; t += GEN_THREADS) buf[t] = ~0ull;
+          P = Pt;
+        }
         __syncthreads();
         bitonic_sort_smem(buf, P);
-        emit(buf, emitted, (int)want);
-        __syncthreads();
-        last = T;
-        first = false;
-        emitted += want;
+        emit(buf, at, (int)take);
+      } else {
+        // one pass for symbols_compared and the value span, then rounds of
+        // GEN_CAP: radix select of the round's last value, collect (last, T], sort
+        for (long long i = lo + threadIdx.x; i < hi; i += GEN_THREADS) {
+          int l;
+          const u64 c = it.comp(i, &l);
+          sym += (unsigned long long)min(l + 1, L);
+          vand &= c;
+          vor |= c;
+        }
+        block_and_or(vand, vor, s_red);
+        long long emitted = 0;
+        u64 last = 0;
+        bool first = true;
+        auto get = [&](long long i) {
+          int l;
+          return it.comp(i, &l);
+        };
+        while (emitted < take) {
+          const u32 want = (u32)min((long long)GEN_CAP, take - emitted);
+          const u64 T = radix_select(get, lo, hi, first, last, want, vand, vand ^ vor, hist,
+                                     &s_prefix, &s_rank);
+          if (threadIdx.x == 0) s_cnt = 0;
+          __syncthreads();
+          for (long long b = lo; b < hi; b += GEN_THREADS) {
+            const long long i = b + threadIdx.x;
+            u64 c = 0;
+            bool in = false;
+            if (i < hi) {
+              c = get(i);
+              in = (first || c > last) && c <= T;
+            }
+            warp_append(in, c, buf, &s_cnt, GEN_CAP);
+          }
+          __syncthreads();
+          int P = 1;
+          while (P < (int)want) P <<= 1;
+          for (int t = (int)want + threadIdx.x; t < P; t += GEN_THREADS) buf[t] = ~0ull;
+          __syncthreads();
+          bitonic_sort_smem(buf, P);
+          emit(buf, at + emitted, (int)want);
+          __syncthreads();
+          last = T;
+          first = false;
+          emitted += want;
+        }
       }
+    };
+    // Strict / complete over a range beyond GEN_CAP whose lcp = d* tier
+    // (R(d*) minus R(d*+1)) covers at least n/16 items, e.g. d* = 0: sorted
+    // R(d*+1) (fewer than need items), then the tier's m smallest ids taken in
+    // id order through rank[] (about n / |tier| <= 16 probes per id taken),
+    // which is already the output order.  (A sparse tier stays on the plain
+    // selection: routing it through an id-only selection too cost 7 -> 5
+    // resident CTAs per SM, a net loss.)
+    bool split = false;
+    if (!fullscan && mode != 2 && size > GEN_CAP) {
+      if (warp == 0) {
+        long long a = lo, b = lo;  // R(d* + 1), empty when d* = d_max
+        const int d1 = s_dstar + 1;
+        if (d1 <= s_dmax) {
+          a = run_edge_any(ix, q, d1, s_p0, -1);
+          b = run_edge_any(ix, q, d1, s_p0, ix.n) + 1;
+        }
+        if (lane == 0) {
+          s_a = a;
+          s_b = b;
+        }
+      }
+      __syncthreads();
+      split = 16 * (size - (s_b - s_a)) >= ix.n;
+    }
+    if (split) {
+      const long long sa = s_a, sb = s_b, c1 = sb - sa, m = take - c1;
+      select_range(sa, sb, c1, 0);
+      const uint16_t dl = (uint16_t)s_dstar;
+      long long got = 0;
+      for (long long base = 0; got < m && base < ix.n; base += GEN_THREADS) {
+        const long long id = base + threadIdx.x;
+        bool in = false;
+        if (id < ix.n) {
+          const long long p = __ldg(ix.rank + id);
+          in = p >= lo && p < hi && (p < sa || p >= sb);
+        }
+        const unsigned bal = __ballot_sync(LCP_FULL_MASK, in);
+        if (lane == 0) s_wc[warp] = __popc(bal);
+        __syncthreads();
+        long long slot = got + __popc(bal & ((1u << lane) - 1u));
+        int tot = 0;
+        for (int w = 0; w < GEN_THREADS / 32; ++w) {
+          if (w < warp) slot += s_wc[w];
+          tot += s_wc[w];
+        }
+        if (in && slot < m) {
+          out_ids[qi * stride + c1 + slot] = (u32)id;
+          out_lcps[qi * stride + c1 + slot] = dl;
+        }
+        got += tot;
+        __syncthreads();
+      }
+    } else {
+      select_range(lo, hi, take, 0);
     }
     // reduce symbols_compared (TAL accounting)
 #pragma unroll
