@@ -953,46 +953,63 @@ __global__ void __launch_bounds__(NS > 2 ? QW_MAX_THREADS / 2 : QW_MAX_THREADS, 
     // R(d*) past the region: outside it every item has lcp == d*
     const C tier = make_comp<C>(dstar, 0u, L, idbits);
     const bool sketch_ok = need - above <= LCP_SK_LIST;  // tier supplies <= 32 items
-    if (s > 0 && r0 == first_valid) {
-      long long e = s;
-      for (int chunk = 0;; ++chunk) {
-        if (chunk == EXT_SCAN_CHUNKS && sketch_ok) {
-          u64 qk1[1] = {q};
-          const long long r = dstar ? run_edge<1>(ix, qk1, dstar, e, -1) : 0;
-          lst = tier_offer_n<C, NS>(ix, r, e, tier, lst, need);
-          rsize += e - r;
-          rlo = r;
-          break;
-        }
-        const long long i = e - 32 + lane;
-        const int li = i >= 0 ? min(__clzll((long long)(__ldg(keys + i) ^ q)) >> lb, L) : -1;
-        const bool c = li >= dstar;
-        lst.offer(c ? make_comp<C>(li, __ldg(order + i), L, idbits) : ~C(0), need);
-        const unsigned m = __ballot_sync(LCP_FULL_MASK, c);
-        rsize += __popc(m);
-        if (m) rlo = e - 32 + (__ffs(m) - 1);
-        e -= 32;
-        if (!(m == LCP_FULL_MASK && e > 0)) break;
-      }
+    // up to EXT_SCAN_CHUNKS chunks outward on each side
+    bool goL = s > 0 && r0 == first_valid, goR = end < n && s + r0 + cnt == end;
+    long long eL = s, eR = end;  // [eL, eR) is scanned
+    for (int chunk = 0; goL && chunk < EXT_SCAN_CHUNKS; ++chunk) {
+      const long long i = eL - 32 + lane;
+      const int li = i >= 0 ? min(__clzll((long long)(__ldg(keys + i) ^ q)) >> lb, L) : -1;
+      const bool c = li >= dstar;
+      lst.offer(c ? make_comp<C>(li, __ldg(order + i), L, idbits) : ~C(0), need);
+      const unsigned m = __ballot_sync(LCP_FULL_MASK, c);
+      rsize += __popc(m);
+      if (m) rlo = eL - 32 + (__ffs(m) - 1);
+      eL -= 32;
+      goL = m == LCP_FULL_MASK && eL > 0;
     }
-    if (end < n && s + r0 + cnt == end) {
-      long long e = end;
-      for (int chunk = 0;; ++chunk) {
-        if (chunk == EXT_SCAN_CHUNKS && sketch_ok) {
-          u64 qk1[1] = {q};
-          const long long r = dstar ? run_edge<1>(ix, qk1, dstar, e - 1, n) + 1 : n;
-          lst = tier_offer_n<C, NS>(ix, e, r, tier, lst, need);
-          rsize += r - e;
-          break;
+    for (int chunk = 0; goR && chunk < EXT_SCAN_CHUNKS; ++chunk) {
+      const long long i = eR + lane;
+      const int li = i < n ? min(__clzll((long long)(__ldg(keys + i) ^ q)) >> lb, L) : -1;
+      const bool c = li >= dstar;
+      lst.offer(c ? make_comp<C>(li, __ldg(order + i), L, idbits) : ~C(0), need);
+      const unsigned m = __ballot_sync(LCP_FULL_MASK, c);
+      rsize += __popc(m);
+      eR += 32;
+      goR = m == LCP_FULL_MASK && eR < n;
+    }
+    if (goL || goR) {
+      // the run goes on: its ends by run_edge; every item past the scanned
+      // span has lcp == d* (R(d*+1) lies in the region), so only ids matter
+      u64 qk1[1] = {q};
+      const long long rl = goL ? (dstar ? run_edge<1>(ix, qk1, dstar, eL, -1) : 0) : eL;
+      const long long rr = goR ? (dstar ? run_edge<1>(ix, qk1, dstar, eR - 1, n) + 1 : n) : eR;
+      const long long rest = (eL - rl) + (rr - eR);
+      rsize += rest;
+      if (goL) rlo = rl;
+      if (sketch_ok) {  // the id sketch: 32 smallest ids per block
+        if (goL) lst = tier_offer_n<C, NS>(ix, rl, eL, tier, lst, need);
+        if (goR) lst = tier_offer_n<C, NS>(ix, eR, rr, tier, lst, need);
+      } else if (16 * rest >= n) {
+        // most of the corpus: ids in ascending order through rank[], until
+        // the list is full and no later id can enter
+        for (long long base = 0; base < n && (tier | (C)base) < lst.thr; base += 32) {
+          const long long id = base + lane;
+          C cv = ~C(0);
+          if (id < n) {
+            const long long p = __ldg(ix.rank + id);
+            if ((p >= rl && p < eL) || (p >= eR && p < rr)) cv = tier | (C)id;
+          }
+          lst.offer(cv, need);
         }
-        const long long i = e + lane;
-        const int li = i < n ? min(__clzll((long long)(__ldg(keys + i) ^ q)) >> lb, L) : -1;
-        const bool c = li >= dstar;
-        lst.offer(c ? make_comp<C>(li, __ldg(order + i), L, idbits) : ~C(0), need);
-        const unsigned m = __ballot_sync(LCP_FULL_MASK, c);
-        rsize += __popc(m);
-        e += 32;
-        if (!(m == LCP_FULL_MASK && e < n)) break;
+      } else {  // position by position, ids only
+        for (long long base = rl; base < eL; base += 32) {
+          const long long i = base + lane;
+          lst.offer(i < eL ? (tier | (C)__ldg(order + i)) : ~C(0), need);
+        }
+        for (long long base = eR; base < rr; base += 32) {
+          const long long i = base + lane;
+          lst.offer(i < rr ? (tier | (C)__ldg(order + i)) : ~C(0), need);
+        }
       }
     }
     const int take = (int)min((long long)need, rsize);

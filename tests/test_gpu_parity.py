@@ -672,3 +672,44 @@ def test_large_k_vs_oracle(gpu, oracle_lib, wide, monkeypatch):
             for i in range(len(qs)):
                 assert b.pairs(i) == list(zip(ids[i, :hits[i]].tolist(), lcps[i, :hits[i]].tolist())), (name, k, i)
             assert np.array_equal(b.aux[:, 1].astype(np.int64), sym)
+
+
+@pytest.mark.parametrize("wide", [False, True])
+def test_w1_large_alphabet_vs_oracle(gpu, oracle_lib, wide, monkeypatch):
+    """W = 1 with a large alphabet (short keys): d* drops to 0 or 1 once k
+    passes the depth-1 bucket size, so R(d*) spans most of the corpus (the
+    id-order walk through rank[]) or a mid-sized run (position by position)
+    beyond the id sketch's 32 per block.  Complete, strict and TAL at k up to
+    128 (the list kernel) against the oracle, work counters included."""
+    if wide:
+        monkeypatch.setenv("LCP_FORCE_WIDE_COMPOSITE", "1")
+    cases = [
+        ("s65536-L4", lg.generate_dataset(60_000, 4, 65536, seed=40)),
+        ("s256-L8", lg.generate_dataset(60_000, 8, 256, seed=41)),
+        ("s256-L8-clustered", lg.generate_dataset(40_000, 8, 256, seed=42, distribution="clustered")),
+    ]
+    for name, ds in cases:
+        idx = lg.build(ds)
+        assert idx.native.words == 1
+        sigma = ds.alphabet.size
+        ot = oracle_lib.OracleTrie(ds.items, sigma)
+        qs = np.vstack([lg.generate_queries(ds, 48, seed=43),
+                        lg.generate_queries(ds, 48, seed=44, prefix_len=1)])
+        for k in (17, 32, 33, 50, 64, 100, 128):
+            for mode in ("complete", "strict"):
+                b = idx.query_batch(qs, k, mode)
+                ids, lcps, hits, md, sym, nodes = ot.query_batch(qs, k, mode)
+                for i in range(len(qs)):
+                    exp = list(zip(ids[i, :hits[i]].tolist(), lcps[i, :hits[i]].tolist()))
+                    assert b.pairs(i) == exp, (name, k, mode, i)
+                w = idx.new_work_report()
+                idx.query_batch(qs, k, mode, work=w)
+                assert w.nodes_visited == int(nodes.sum()), (name, k, mode)
+        eng = lg.build_tal(ds, sigma)
+        ote = oracle_lib.OracleTal(ds.items, sigma, eng.bucket_depth)
+        for k in (17, 33, 64, 128):
+            b = eng.query_batch(qs, k)
+            ids, lcps, hits, items_, sym = ote.query_batch(qs, k)
+            for i in range(len(qs)):
+                assert b.pairs(i) == list(zip(ids[i, :hits[i]].tolist(), lcps[i, :hits[i]].tolist())), (name, k, i)
+            assert np.array_equal(b.aux[:, 1].astype(np.int64), sym)
