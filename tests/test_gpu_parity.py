@@ -713,3 +713,31 @@ def test_w1_large_alphabet_vs_oracle(gpu, oracle_lib, wide, monkeypatch):
             for i in range(len(qs)):
                 assert b.pairs(i) == list(zip(ids[i, :hits[i]].tolist(), lcps[i, :hits[i]].tolist())), (name, k, i)
             assert np.array_equal(b.aux[:, 1].astype(np.int64), sym)
+
+
+def test_wide_keys_list_kernel_vs_oracle(gpu, oracle_lib):
+    """W in 2..8 with 32 < k <= 128 (k_query_warp_kn): windows, chunk
+    extension, sketch / rank-walk / position tiers, against the oracle."""
+    cases = [
+        ("s256-W4", lg.generate_dataset(120_000, 32, 256, seed=50)),
+        ("s65536-W8", lg.generate_dataset(60_000, 32, 65536, seed=51)),
+        ("s16-W2", lg.generate_dataset(80_000, 32, 16, seed=52)),
+        ("s256-W4-clustered", lg.generate_dataset(60_000, 32, 256, seed=53, distribution="clustered")),
+    ]
+    for name, ds in cases:
+        idx = lg.build(ds)
+        assert 2 <= idx.native.words <= 8
+        ot = oracle_lib.OracleTrie(ds.items, ds.alphabet.size)
+        qs = np.vstack([lg.generate_queries(ds, 48, seed=54),
+                        lg.generate_queries(ds, 48, seed=55, prefix_len=2)])
+        for k in (33, 48, 64, 65, 100, 128):
+            for mode in ("complete", "strict"):
+                b = idx.query_batch(qs, k, mode)
+                ids, lcps, hits, md, sym, nodes = ot.query_batch(qs, k, mode)
+                for i in range(len(qs)):
+                    exp = list(zip(ids[i, :hits[i]].tolist(), lcps[i, :hits[i]].tolist()))
+                    assert b.pairs(i) == exp, (name, k, mode, i)
+                    assert int(b.matched_depth[i]) == md[i]
+                w = idx.new_work_report()
+                idx.query_batch(qs, k, mode, work=w)
+                assert w.nodes_visited == int(nodes.sum()) and w.symbols_compared == int(sym.sum()), (name, k, mode)
