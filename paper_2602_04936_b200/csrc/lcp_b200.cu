@@ -1265,26 +1265,30 @@ static int query_impl(const lcp_index* ix, lcp_workspace* ws, const uint16_t* qu
     LCP_CK_LAUNCH();
     return LCP_OK;
   }
-  if (dv.W > 1 && dv.W <= 8 && mode != LCP_MODE_TAL && needk > FAST_KMAX && needk <= 128) {
-    // 32 < need <= 128, W > 1: warp per query with a 2- or 4-slot list
+  if (dv.W > 1 && dv.W <= 8 && needk > FAST_KMAX && needk <= 128) {
+    // 32 < need <= 128, W > 1 (strict, complete, TAL): warp per query with a
+    // 2- or 4-slot list
     const long long sms = num_sms();
     const long long wmax = needk <= 64 ? 32 : 16;  // 4-slot lists: 512-thread CTAs
     const long long wpc = std::min<long long>(wmax, std::max<long long>(1, (count + sms - 1) / sms));
     const unsigned block = (unsigned)(wpc * 32);
     const unsigned grid = (unsigned)std::min<long long>((count + wpc - 1) / wpc, 8ll * sms);
     const size_t smem0 = 16 + (size_t)dv.smem_entries * dv.W * 8;
-#define LCP_WKN(WM, NS)                                                                          \
+#define LCP_WKN1(WM, NS, TL)                                                                     \
   do {                                                                                           \
-    allow_dyn_smem<k_query_warp_kn<WM, NS>>();                                                   \
-    k_query_warp_kn<WM, NS><<<grid, block, smem0 + (size_t)wpc * 32 * NS * 8, st>>>(            \
+    allow_dyn_smem<k_query_warp_kn<WM, NS, TL>>();                                               \
+    k_query_warp_kn<WM, NS, TL><<<grid, block, smem0 + (size_t)wpc * 32 * NS * 8, st>>>(        \
         dv, queries, count, k, mode, out_stride, ids, lcps, hits, md, ax, errp);                 \
   } while (0)
+#define LCP_WKN(WM, NS) \
+  do { if (mode == LCP_MODE_TAL) LCP_WKN1(WM, NS, true); else LCP_WKN1(WM, NS, false); } while (0)
     if (needk <= 64) {
       if (dv.W == 2) LCP_WKN(2, 2); else if (dv.W <= 4) LCP_WKN(4, 2); else LCP_WKN(8, 2);
     } else {
       if (dv.W == 2) LCP_WKN(2, 4); else if (dv.W <= 4) LCP_WKN(4, 4); else LCP_WKN(8, 4);
     }
 #undef LCP_WKN
+#undef LCP_WKN1
     LCP_CK_LAUNCH();
     return LCP_OK;
   }

@@ -1113,13 +1113,186 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, 1)
   }
 }
 
+// bucket [lo, hi) of the query's d-prefix: dense directory (tal.py:138-143)
+// or binary search on the packed d-prefixes (tal.py:124-136)
+__device__ __forceinline__ void tal_bucket(const DevIndex& ix, const u64* qk,
+                                           const uint16_t* qrow, long long& lo,
+                                           long long& hi) {
+  const int d = ix.tal_depth;
+  if (d == 0) {
+    lo = 0;
+    hi = ix.n;
+    return;
+  }
+  if (ix.directory) {
+    long long code = 0;
+    for (int j = 0; j < d; ++j) code = code * ix.sigma + qrow[j];
+    lo = ix.directory[code];
+    hi = ix.directory[code + 1];
+    return;
+  }
+  long long a = 0, b = ix.n;
+  while (a < b) {
+    long long m = (a + b) >> 1;
+    if (prefix_cmp(ix.keys + m * ix.W, qk, d, ix) < 0) a = m + 1;
+    else b = m;
+  }
+  lo = a;
+  b = ix.n;
+  while (a < b) {
+    long long m = (a + b) >> 1;
+    if (prefix_cmp(ix.keys + m * ix.W, qk, d, ix) <= 0) a = m + 1;
+    else b = m;
+  }
+  hi = a;
+}
+
+// symbols_compared = sum over the bucket [blo, bhi) of min(lcp + 1, L)
+// (tal.py:173-177) for W > 1: a coalesced sweep of the sorted first-word
+// plane, 4 loads in flight per lane; only keys equal to q in the whole first
+// word compare further words.  The warp total on every lane.
+template <int WMAX>
+__device__ __forceinline__ unsigned long long tal_sym_warp(const DevIndex& ix, const u64 (&qk)[WMAX],
+                                                           long long blo, long long bhi) {
+  const int lane = lane_id();
+  const int L = ix.L, lb = ix.lb;
+  unsigned long long sym = 0;
+  for (long long i0 = blo + lane; i0 < bhi; i0 += 128) {
+    u64 x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long i = i0 + 32 * u;
+      x[u] = i < bhi ? __ldg(ix.keys_w0 + i) ^ qk[0] : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long i = i0 + 32 * u;
+      if (i < bhi) {
+        const int li = x[u] ? (__clzll((long long)x[u]) >> lb) : lcp_at<WMAX>(ix, i, qk);
+        sym += (unsigned)min(li + 1, L);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sym += __shfl_xor_sync(LCP_FULL_MASK, sym, o);
+  return sym;
+}
+
 // ---------------------------------------------------------------------------
-// strict / complete, 32 < need <= 32 * NS <= 128, 2 <= W <= WMAX <= 8: one warp
-// per query with an NS-slot top-k list.  Window [pos - 32 NS, pos + 32 NS)
-// after the 64-ary search; extension as in k_query_w1_kn (chunks, then the
-// run's ends by run_edge and ids only: sketch, rank walk or positions).
+// TAL, k <= 32, 2 <= W <= WMAX <= 8 (tal.py:116-194): one warp per query.
+// The answer is the complete-mode answer with need = k whenever the bucket
+// holds >= k items (then d* >= depth, so R(d*) lies inside the bucket);
+// smaller buckets are ranked whole.  symbols_compared = sum over the bucket of
+// min(lcp + 1, L) comes from a coalesced sweep of the sorted first-word plane;
+// only keys equal to q in the whole first word compare further words.
 // ---------------------------------------------------------------------------
-template <int WMAX, int NS>
+template <int WMAX>
+__global__ void __launch_bounds__(QW_MAX_THREADS, 1)
+    k_query_warp_tal(const __grid_constant__ DevIndex ix, const uint16_t* __restrict__ queries,
+                     int count, int k, int stride, u32* __restrict__ out_ids,
+                     uint16_t* __restrict__ out_lcps, int* __restrict__ out_hits,
+                     uint16_t* __restrict__ out_md, u64* __restrict__ out_aux,
+                     int* __restrict__ err) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  u64* bar = reinterpret_cast<u64*>(smem_raw);
+  u64* staged = reinterpret_cast<u64*>(smem_raw + 16);
+  stage_levels(ix, bar, staged);
+  const int lane = lane_id();
+  const int warp = threadIdx.x >> 5;
+  const int warps = blockDim.x >> 5;
+  const long long n = ix.n;
+  const int L = ix.L;
+  const int depth = ix.tal_depth;
+  for (long long qi = (long long)blockIdx.x * warps + warp; qi < count;
+       qi += (long long)gridDim.x * warps) {
+    u64 qk[WMAX];
+    if (!warp_pack_query<WMAX>(queries + qi * L, ix, qk)) {
+      if (lane == 0) {
+        atomicOr(err, 1);
+        out_hits[qi] = 0;
+        out_md[qi] = 0;
+        out_aux[2 * qi] = 0;
+        out_aux[2 * qi + 1] = 0;
+      }
+      continue;
+    }
+    long long blo, bhi;
+    tal_bucket(ix, qk, queries + qi * L, blo, bhi);
+    const unsigned long long sym = tal_sym_warp<WMAX>(ix, qk, blo, bhi);
+    const long long bs = bhi - blo;
+    if (bs < k) {  // the whole bucket (empty: no hits, nothing scanned, tal.py:168-171)
+      u64 cv = ~0ull;
+      if (lane < bs) cv = make_comp<u64>(lcp_at<WMAX>(ix, blo + lane, qk), ix.order[blo + lane], L, 32);
+      int rank = 0;
+      for (int jj = 0; jj < (int)bs; ++jj) rank += __shfl_sync(LCP_FULL_MASK, cv, jj) < cv;
+      if (lane < bs) {
+        out_ids[qi * stride + rank] = (u32)(cv & 0xffffffffull);
+        out_lcps[qi * stride + rank] = (uint16_t)(L - (int)(cv >> 32));
+      }
+      if (lane == 0) {
+        out_hits[qi] = (int)bs;
+        out_md[qi] = (uint16_t)depth;
+        out_aux[2 * qi] = (u64)bs;
+        out_aux[2 * qi + 1] = bs ? sym : 0ull;
+      }
+      continue;
+    }
+    // complete-mode answer with need = k (as k_query_warp)
+    const long long pos = warp_lower_bound<WMAX>(ix, staged, qk);
+    const long long s = pos - 32;
+    int l[2];
+    u32 id[2];
+    int dmax = -1;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const long long i = s + t * 32 + lane;
+      const bool ok = i >= 0 && i < n;
+      l[t] = ok ? lcp_at<WMAX>(ix, i, qk) : -1;
+      id[t] = ok ? ix.order[i] : 0u;
+      dmax = max(dmax, l[t]);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) dmax = max(dmax, __shfl_xor_sync(LCP_FULL_MASK, dmax, o));
+    const int dstar = window_dstar<2>(l, dmax, k);
+    u64 comp[2];
+    int cnt = 0, r0 = 64;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const bool c = l[t] >= dstar;
+      comp[t] = c ? make_comp<u64>(l[t], id[t], L, 32) : ~0ull;
+      const unsigned m = __ballot_sync(LCP_FULL_MASK, c);
+      cnt += __popc(m);
+      if (m && r0 == 64) r0 = t * 32 + __ffs(m) - 1;
+    }
+    u64 slot = sort_run<u64, 2>(comp, r0, cnt, k);
+    long long rsize = cnt, rlo = s + r0;
+    const long long first_valid = s < 0 ? -s : 0;
+    const long long end = min(s + 64, n);
+    extend_range<u64, WMAX>(ix, qk, dstar, k, s > 0 && r0 == first_valid, s, end < n && s + r0 + cnt == end,
+                            end, 32, slot, rsize, rlo);
+    if (lane < k) {
+      out_ids[qi * stride + lane] = (u32)(slot & 0xffffffffull);
+      out_lcps[qi * stride + lane] = (uint16_t)(L - (int)(slot >> 32));
+    }
+    if (lane == 0) {
+      out_hits[qi] = k;
+      out_md[qi] = (uint16_t)depth;
+      out_aux[2 * qi] = (u64)bs;
+      out_aux[2 * qi + 1] = sym;
+    }
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// strict / complete / TAL, 32 < need <= 32 * NS <= 128, 2 <= W <= WMAX <= 8:
+// one warp per query with an NS-slot top-k list.  Window [pos - 32 NS,
+// pos + 32 NS) after the 64-ary search; extension as in k_query_w1_kn (chunks,
+// then the run's ends by run_edge and ids only: sketch, rank walk or
+// positions).  TAL as in k_query_warp_tal: the whole bucket when it holds
+// fewer than k items, else the complete answer with need = k.
+// ---------------------------------------------------------------------------
+template <int WMAX, int NS, bool TAL>
 __global__ void __launch_bounds__(NS > 2 ? QW_MAX_THREADS / 2 : QW_MAX_THREADS, 1)
     k_query_warp_kn(const __grid_constant__ DevIndex ix, const uint16_t* __restrict__ queries,
                     int count, int k, int mode, int stride, u32* __restrict__ out_ids,
@@ -1136,7 +1309,7 @@ __global__ void __launch_bounds__(NS > 2 ? QW_MAX_THREADS / 2 : QW_MAX_THREADS, 
   const int warps = blockDim.x >> 5;
   const long long n = ix.n;
   const int L = ix.L;
-  const bool complete = mode == 1;
+  const bool complete = TAL || mode == 1;  // TAL: the complete answer with need = k
   u64* scb = reinterpret_cast<u64*>(smem_raw + 16 + (size_t)ix.smem_entries * ix.W * 8) +
              warp * (32 * NS);
 
@@ -1152,6 +1325,37 @@ __global__ void __launch_bounds__(NS > 2 ? QW_MAX_THREADS / 2 : QW_MAX_THREADS, 
         out_aux[2 * qi + 1] = 0;
       }
       continue;
+    }
+    TopKN<u64, NS> lst;
+    lst.init(scb);
+    long long blo = 0, bhi = n;
+    unsigned long long tsym = 0;
+    if constexpr (TAL) {
+      tal_bucket(ix, qk, queries + qi * L, blo, bhi);
+      tsym = tal_sym_warp<WMAX>(ix, qk, blo, bhi);
+      const long long bs = bhi - blo;
+      if (bs < k) {  // the whole bucket, ranked (an empty one included)
+        for (long long base = blo; base < bhi; base += 32) {
+          const long long i = base + lane;
+          lst.offer(i < bhi ? make_comp<u64>(lcp_at<WMAX>(ix, i, qk), __ldg(ix.order + i), L, 32)
+                            : ~0ull, k);
+        }
+#pragma unroll
+        for (int j = 0; j < NS; ++j) {
+          if (lane + 32 * j < bs) {
+            const u64 w = lst.s[j];
+            out_ids[(size_t)qi * stride + lane + 32 * j] = (u32)(w & 0xffffffffull);
+            out_lcps[(size_t)qi * stride + lane + 32 * j] = (uint16_t)(L - (int)(w >> 32));
+          }
+        }
+        if (lane == 0) {
+          out_hits[qi] = (int)bs;
+          out_md[qi] = (uint16_t)ix.tal_depth;
+          out_aux[2 * qi] = (u64)bs;
+          out_aux[2 * qi + 1] = tsym;
+        }
+        continue;
+      }
     }
     const long long pos = warp_lower_bound<WMAX>(ix, staged, qk);
     const long long s = pos - 32 * NS;  // window [s, s + 32 T), warp-strided
@@ -1169,8 +1373,6 @@ __global__ void __launch_bounds__(NS > 2 ? QW_MAX_THREADS / 2 : QW_MAX_THREADS, 
     dmax = (int)__reduce_max_sync(LCP_FULL_MASK, (unsigned)(dmax + 1)) - 1;
     const int need = complete ? (int)min((long long)k, n) : k;
     const int dstar = complete ? window_dstar<T>(l, dmax, need) : dmax;
-    TopKN<u64, NS> lst;
-    lst.init(scb);
     int cnt = 0, r0 = 32 * T, above = 0;
 #pragma unroll
     for (int t = 0; t < T; ++t) {
@@ -1252,171 +1454,18 @@ __global__ void __launch_bounds__(NS > 2 ? QW_MAX_THREADS / 2 : QW_MAX_THREADS, 
     }
     if (lane == 0) {
       out_hits[qi] = take;
-      out_md[qi] = (uint16_t)dmax;
-      out_aux[2 * qi] = (u64)(u32)dmax | ((u64)(u32)dstar << 32);
-      out_aux[2 * qi + 1] = (u64)rsize | ((u64)rlo << 32);
+      if constexpr (TAL) {
+        out_md[qi] = (uint16_t)ix.tal_depth;
+        out_aux[2 * qi] = (u64)(bhi - blo);
+        out_aux[2 * qi + 1] = tsym;
+      } else {
+        out_md[qi] = (uint16_t)dmax;
+        out_aux[2 * qi] = (u64)(u32)dmax | ((u64)(u32)dstar << 32);
+        out_aux[2 * qi + 1] = (u64)rsize | ((u64)rlo << 32);
+      }
     }
   }
 }
-
-// bucket [lo, hi) of the query's d-prefix: dense directory (tal.py:138-143)
-// or binary search on the packed d-prefixes (tal.py:124-136)
-__device__ __forceinline__ void tal_bucket(const DevIndex& ix, const u64* qk,
-                                           const uint16_t* qrow, long long& lo,
-                                           long long& hi) {
-  const int d = ix.tal_depth;
-  if (d == 0) {
-    lo = 0;
-    hi = ix.n;
-    return;
-  }
-  if (ix.directory) {
-    long long code = 0;
-    for (int j = 0; j < d; ++j) code = code * ix.sigma + qrow[j];
-    lo = ix.directory[code];
-    hi = ix.directory[code + 1];
-    return;
-  }
-  long long a = 0, b = ix.n;
-  while (a < b) {
-    long long m = (a + b) >> 1;
-    if (prefix_cmp(ix.keys + m * ix.W, qk, d, ix) < 0) a = m + 1;
-    else b = m;
-  }
-  lo = a;
-  b = ix.n;
-  while (a < b) {
-    long long m = (a + b) >> 1;
-    if (prefix_cmp(ix.keys + m * ix.W, qk, d, ix) <= 0) a = m + 1;
-    else b = m;
-  }
-  hi = a;
-}
-
-// ---------------------------------------------------------------------------
-// TAL, k <= 32, 2 <= W <= WMAX <= 8 (tal.py:116-194): one warp per query.
-// The answer is the complete-mode answer with need = k whenever the bucket
-// holds >= k items (then d* >= depth, so R(d*) lies inside the bucket);
-// smaller buckets are ranked whole.  symbols_compared = sum over the bucket of
-// min(lcp + 1, L) comes from a coalesced sweep of the sorted first-word plane;
-// only keys equal to q in the whole first word compare further words.
-// ---------------------------------------------------------------------------
-template <int WMAX>
-__global__ void __launch_bounds__(QW_MAX_THREADS, 1)
-    k_query_warp_tal(const __grid_constant__ DevIndex ix, const uint16_t* __restrict__ queries,
-                     int count, int k, int stride, u32* __restrict__ out_ids,
-                     uint16_t* __restrict__ out_lcps, int* __restrict__ out_hits,
-                     uint16_t* __restrict__ out_md, u64* __restrict__ out_aux,
-                     int* __restrict__ err) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  u64* bar = reinterpret_cast<u64*>(smem_raw);
-  u64* staged = reinterpret_cast<u64*>(smem_raw + 16);
-  stage_levels(ix, bar, staged);
-  const int lane = lane_id();
-  const int warp = threadIdx.x >> 5;
-  const int warps = blockDim.x >> 5;
-  const long long n = ix.n;
-  const int L = ix.L, lb = ix.lb;
-  const int depth = ix.tal_depth;
-  for (long long qi = (long long)blockIdx.x * warps + warp; qi < count;
-       qi += (long long)gridDim.x * warps) {
-    u64 qk[WMAX];
-    if (!warp_pack_query<WMAX>(queries + qi * L, ix, qk)) {
-      if (lane == 0) {
-        atomicOr(err, 1);
-        out_hits[qi] = 0;
-        out_md[qi] = 0;
-        out_aux[2 * qi] = 0;
-        out_aux[2 * qi + 1] = 0;
-      }
-      continue;
-    }
-    long long blo, bhi;
-    tal_bucket(ix, qk, queries + qi * L, blo, bhi);
-    // symbols_compared over the bucket
-    unsigned long long sym = 0;
-    for (long long i0 = blo + lane; i0 < bhi; i0 += 128) {  // 4 independent loads per lane
-      u64 x[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const long long i = i0 + 32 * u;
-        x[u] = i < bhi ? __ldg(ix.keys_w0 + i) ^ qk[0] : 0ull;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const long long i = i0 + 32 * u;
-        if (i < bhi) {
-          const int li = x[u] ? (__clzll((long long)x[u]) >> lb) : lcp_at<WMAX>(ix, i, qk);
-          sym += (unsigned)min(li + 1, L);
-        }
-      }
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) sym += __shfl_xor_sync(LCP_FULL_MASK, sym, o);
-    const long long bs = bhi - blo;
-    if (bs < k) {  // the whole bucket (empty: no hits, nothing scanned, tal.py:168-171)
-      u64 cv = ~0ull;
-      if (lane < bs) cv = make_comp<u64>(lcp_at<WMAX>(ix, blo + lane, qk), ix.order[blo + lane], L, 32);
-      int rank = 0;
-      for (int jj = 0; jj < (int)bs; ++jj) rank += __shfl_sync(LCP_FULL_MASK, cv, jj) < cv;
-      if (lane < bs) {
-        out_ids[qi * stride + rank] = (u32)(cv & 0xffffffffull);
-        out_lcps[qi * stride + rank] = (uint16_t)(L - (int)(cv >> 32));
-      }
-      if (lane == 0) {
-        out_hits[qi] = (int)bs;
-        out_md[qi] = (uint16_t)depth;
-        out_aux[2 * qi] = (u64)bs;
-        out_aux[2 * qi + 1] = bs ? sym : 0ull;
-      }
-      continue;
-    }
-    // complete-mode answer with need = k (as k_query_warp)
-    const long long pos = warp_lower_bound<WMAX>(ix, staged, qk);
-    const long long s = pos - 32;
-    int l[2];
-    u32 id[2];
-    int dmax = -1;
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      const long long i = s + t * 32 + lane;
-      const bool ok = i >= 0 && i < n;
-      l[t] = ok ? lcp_at<WMAX>(ix, i, qk) : -1;
-      id[t] = ok ? ix.order[i] : 0u;
-      dmax = max(dmax, l[t]);
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) dmax = max(dmax, __shfl_xor_sync(LCP_FULL_MASK, dmax, o));
-    const int dstar = window_dstar<2>(l, dmax, k);
-    u64 comp[2];
-    int cnt = 0, r0 = 64;
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      const bool c = l[t] >= dstar;
-      comp[t] = c ? make_comp<u64>(l[t], id[t], L, 32) : ~0ull;
-      const unsigned m = __ballot_sync(LCP_FULL_MASK, c);
-      cnt += __popc(m);
-      if (m && r0 == 64) r0 = t * 32 + __ffs(m) - 1;
-    }
-    u64 slot = sort_run<u64, 2>(comp, r0, cnt, k);
-    long long rsize = cnt, rlo = s + r0;
-    const long long first_valid = s < 0 ? -s : 0;
-    const long long end = min(s + 64, n);
-    extend_range<u64, WMAX>(ix, qk, dstar, k, s > 0 && r0 == first_valid, s, end < n && s + r0 + cnt == end,
-                            end, 32, slot, rsize, rlo);
-    if (lane < k) {
-      out_ids[qi * stride + lane] = (u32)(slot & 0xffffffffull);
-      out_lcps[qi * stride + lane] = (uint16_t)(L - (int)(slot >> 32));
-    }
-    if (lane == 0) {
-      out_hits[qi] = k;
-      out_md[qi] = (uint16_t)depth;
-      out_aux[2 * qi] = (u64)bs;
-      out_aux[2 * qi + 1] = sym;
-    }
-  }
-}
-
 
 // ---------------------------------------------------------------------------
 // General path: any k, any W, all modes + full scan.  One CTA per query;

@@ -717,7 +717,9 @@ def test_w1_large_alphabet_vs_oracle(gpu, oracle_lib, wide, monkeypatch):
 
 def test_wide_keys_list_kernel_vs_oracle(gpu, oracle_lib):
     """W in 2..8 with 32 < k <= 128 (k_query_warp_kn): windows, chunk
-    extension, sketch / rank-walk / position tiers, against the oracle."""
+    extension, sketch / rank-walk / position tiers, and TAL (whole small
+    buckets, complete answers in large ones, the sweep counter), against the
+    oracle."""
     cases = [
         ("s256-W4", lg.generate_dataset(120_000, 32, 256, seed=50)),
         ("s65536-W8", lg.generate_dataset(60_000, 32, 65536, seed=51)),
@@ -741,3 +743,14 @@ def test_wide_keys_list_kernel_vs_oracle(gpu, oracle_lib):
                 w = idx.new_work_report()
                 idx.query_batch(qs, k, mode, work=w)
                 assert w.nodes_visited == int(nodes.sum()) and w.symbols_compared == int(sym.sum()), (name, k, mode)
+        for buckets in (ds.alphabet.size, ds.alphabet.size ** 2):
+            eng = lg.build_tal(ds, buckets)
+            ote = oracle_lib.OracleTal(ds.items, ds.alphabet.size, eng.bucket_depth)
+            for k in (33, 64, 100, 128):
+                b = eng.query_batch(qs, k)
+                ids, lcps, hits, items_, sym = ote.query_batch(qs, k)
+                for i in range(len(qs)):
+                    exp = list(zip(ids[i, :hits[i]].tolist(), lcps[i, :hits[i]].tolist()))
+                    assert b.pairs(i) == exp, (name, buckets, k, i)
+                assert np.array_equal(b.aux[:, 0].astype(np.int64), items_)
+                assert np.array_equal(b.aux[:, 1].astype(np.int64), sym)
