@@ -1,7 +1,9 @@
 """Distil ncu reports into profiles/ (run here, after gpurun brought them back).
 
     python tools/ncu_summary.py gpurun_out/prof_query_r01.ncu-rep:k_query_w1 \
-        gpurun_out/prof_fullscan_r01.ncu-rep:k_fullscan_w1 ... --launches gpurun_out/launches.csv
+        gpurun_out/ncu_raw_fullscan_r01.csv:k_fullscan_w1 ... --launches gpurun_out/launches.csv
+
+(each spec is an .ncu-rep or its exported `--page raw --csv` page)
 
 Writes profiles/ncu_summary.json (per-kernel duration, DRAM bytes, issue and
 occupancy figures; bench.py reads dram_bytes_per_launch as roofline.traffic)
@@ -33,8 +35,11 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "nseco
 
 
 def raw(rep: str) -> dict:
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True, check=True).stdout
+    if rep.endswith(".csv"):  # an exported `--page raw --csv` page
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True, check=True).stdout
     r = list(csv.reader(io.StringIO(out)))
     h, u, v = r[0], r[1], r[2]
     return {k: (val, unit) for k, unit, val in zip(h, u, v)}

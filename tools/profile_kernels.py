@@ -1,6 +1,6 @@
 """Minimal launcher for ncu captures of one kernel family.
 
-    python tools/profile_kernels.py query|fullscan|tal|build [--launches N]
+    python tools/profile_kernels.py query|fullscan|tal|build|strict [--launches N] [--k K]
 
 Builds the BASELINE config-3 index (N=2M, L=32, sigma=4) and launches the
 chosen path a few times on one stream (no L2 flush between launches), so an
@@ -22,6 +22,7 @@ def main() -> None:
     ap.add_argument("--launches", type=int, default=6)
     ap.add_argument("--batch", type=int, default=4096)
     ap.add_argument("--time", action="store_true")
+    ap.add_argument("--k", type=int, default=10)  # 64: k_query_w1_kn, 1000: k_query_general
     args = ap.parse_args()
 
     import torch
@@ -31,7 +32,7 @@ def main() -> None:
     ds = lg.generate_dataset(2_000_000, 32, 4, seed=3)
     qs = lg.generate_queries(ds, args.batch, seed=4)
     dq = torch.from_numpy(qs).cuda()
-    k = 10
+    k = args.k
     ids = torch.empty((args.batch, k), dtype=torch.int32, device="cuda")
     lcps = torch.empty((args.batch, k), dtype=torch.int16, device="cuda")
     hits = torch.empty(args.batch, dtype=torch.int32, device="cuda")
