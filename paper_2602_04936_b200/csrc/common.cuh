@@ -32,7 +32,8 @@ struct DevIndex {
   const u32* keys_hi;     // W == 1: high 32 bits of keys_orig (SoA plane for the scan)
   const u32* keys_lo;     // W == 1: low 32 bits of keys_orig
   const u64* levels;      // concatenated search-level tables (W words per entry)
-  const u64* keys_w0;     // W > 1 with TAL: first word of each sorted key (coalesced bucket sweep)
+  const u64* keys_w0;     // W > 1: first word of each sorted key (coalesced compares, TAL sweep)
+  const u64* levels_w0;   // first word of each search-table entry (== levels when W == 1)
   const u32* keys_shi;    // W == 1 with TAL: high 32 bits of each sorted key (bucket sweep)
   const long long* directory;  // TAL dense directory (sigma**d + 1) or null
   long long n;

@@ -243,6 +243,7 @@ struct lcp_index {
   u32* sketch = nullptr;
   u32* rank = nullptr;  // original id -> sorted position
   u64* keys_w0 = nullptr;
+  u64* levels_w0 = nullptr;  // W > 1: first word of each search-table entry
   u32* keys_shi = nullptr;
   std::vector<long long> level_offset;  // cached trie level offsets
 };
@@ -301,6 +302,7 @@ int lcp_index_free(lcp_index* ix) {
   if (ix->sketch) cudaFreeAsync(ix->sketch, 0);
   if (ix->rank) cudaFreeAsync(ix->rank, 0);
   if (ix->keys_w0) cudaFreeAsync(ix->keys_w0, 0);
+  if (ix->levels_w0) cudaFreeAsync(ix->levels_w0, 0);
   if (ix->keys_shi) cudaFreeAsync(ix->keys_shi, 0);
   cudaStreamSynchronize(0);
   delete ix;
@@ -462,6 +464,19 @@ static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, i
     LCP_CK_LAUNCH();
   }
   dv.levels = ix->levels;
+  dv.levels_w0 = ix->levels;
+  if (W > 1) {  // first-word planes: W > 1 comparisons read 8 B per entry / key
+    // (coalesced) and the whole key only when the first words are equal
+    const long long lt = std::max(2ll, total);
+    LCP_TRY(dalloc(&ix->levels_w0, lt, acct, st));
+    k_first_word<<<blocks_for(lt, 256), 256, 0, st>>>(ix->levels, lt, W, ix->levels_w0);
+    LCP_CK_LAUNCH();
+    dv.levels_w0 = ix->levels_w0;
+    LCP_TRY(dalloc(&ix->keys_w0, std::max(1ll, n), acct, st));
+    k_first_word<<<blocks_for(n, 256), 256, 0, st>>>(ix->keys, n, W, ix->keys_w0);
+    LCP_CK_LAUNCH();
+    dv.keys_w0 = ix->keys_w0;
+  }
   dv.smem_levels = 0;
   dv.smem_entries = 0;
   static const long long smem_cap = [] {  // LCP_SMEM_STAGE_CAP: A/B hook (bytes)
@@ -513,12 +528,8 @@ static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, i
   phase("sketch");
   // TAL bucket structure — tal.py:42-82
   if (tal_depth >= 0) {
-    if (W > 1) {  // first-word plane of the sorted keys for the coalesced bucket sweep
-      LCP_TRY(dalloc(&ix->keys_w0, n, acct, st));
-      k_first_word<<<blocks_for(n, 256), 256, 0, st>>>(ix->keys, n, W, ix->keys_w0);
-      LCP_CK_LAUNCH();
-      dv.keys_w0 = ix->keys_w0;
-    } else {  // high-word plane of the sorted keys: the sweep reads 4 B per key
+    if (W == 1) {  // high-word plane of the sorted keys: the sweep reads 4 B per key
+                   // (W > 1 sweeps the first-word plane built with the levels)
       LCP_TRY(dalloc(&ix->keys_shi, n + 64, acct, st));
       LCP_CK(cudaMemsetAsync(ix->keys_shi, 0, (size_t)(n + 64) * 4, st));
       k_hi_word<<<blocks_for(n, 256), 256, 0, st>>>(ix->keys, n, ix->keys_shi);

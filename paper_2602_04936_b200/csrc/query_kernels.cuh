@@ -74,6 +74,18 @@ __device__ __forceinline__ bool warp_pack_w1(const uint16_t* __restrict__ qrow, 
   return !__any_sync(LCP_FULL_MASK, bad);
 }
 
+// key i (sorted) < q for W > 1: first word from its plane, the rest on a tie
+template <int WMAX>
+__device__ __forceinline__ bool w0_less(u64 a0, const u64* key, const u64 (&qk)[WMAX],
+                                        const DevIndex& ix) {
+  if (a0 != qk[0]) return a0 < qk[0];
+#pragma unroll
+  for (int w = 1; w < WMAX; ++w) {
+    if (w < ix.W && key[w] != qk[w]) return key[w] < qk[w];
+  }
+  return false;
+}
+
 // lower_bound(keys, q) by a 64-ary search: every level is one coalesced
 // 64-separator read per warp (2 per lane) + 2 ballots.  Top levels come
 // from shared memory (staged by TMA bulk copy), the rest from L2/HBM.
@@ -93,10 +105,14 @@ __device__ __forceinline__ long long warp_lower_bound(const DevIndex& ix, const 
       tab = ix.levels + ix.level_off[j] * W;
       cnt = ix.level_cnt[j];
     }
-    if (j == ix.nlevels) {  // leaf block: 32 keys, one per lane
+    if (j == ix.nlevels) {  // leaf block: 16 keys, one per lane
       const long long base = blk * LCP_LEAF_KEYS;
       const long long i = base + lane;
-      const bool lt = lane < LCP_LEAF_KEYS && i < ix.n && key_less<WMAX>(ix.keys + i * W, qk, ix);
+      bool lt = false;
+      if (lane < LCP_LEAF_KEYS && i < ix.n) {
+        if constexpr (WMAX == 1) lt = key_less<WMAX>(ix.keys + i * W, qk, ix);
+        else lt = w0_less<WMAX>(__ldg(ix.keys_w0 + i), ix.keys + i * W, qk, ix);
+      }
       return base + (int)__reduce_add_sync(LCP_FULL_MASK, (u32)lt);
     }
     long long base = blk * LCP_SEARCH_FANOUT;
@@ -110,9 +126,18 @@ __device__ __forceinline__ long long warp_lower_bound(const DevIndex& ix, const 
       } else if (i0 < cnt) {
         lt0 = tab[i0] < qk[0];
       }
-    } else {
+    } else if (j < ix.smem_levels) {
       if (i0 < cnt) lt0 = key_less<WMAX>(tab + i0 * W, qk, ix);
       if (i0 + 1 < cnt) lt1 = key_less<WMAX>(tab + (i0 + 1) * W, qk, ix);
+    } else {  // global table: the two first words in one 16-byte load
+      const u64* w0 = ix.levels_w0 + ix.level_off[j];
+      if (i0 + 1 < cnt) {
+        const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(w0 + i0));
+        lt0 = w0_less<WMAX>(v.x, tab + i0 * W, qk, ix);
+        lt1 = w0_less<WMAX>(v.y, tab + (i0 + 1) * W, qk, ix);
+      } else if (i0 < cnt) {
+        lt0 = w0_less<WMAX>(__ldg(w0 + i0), tab + i0 * W, qk, ix);
+      }
     }
     int c = __popc(__ballot_sync(LCP_FULL_MASK, lt0)) + __popc(__ballot_sync(LCP_FULL_MASK, lt1));
     if (c == 0) return 0;  // only reachable at the root level
@@ -126,9 +151,23 @@ __device__ __forceinline__ int lcp_at(const DevIndex& ix, long long i, const u64
     u64 x = ix.keys[i] ^ qk[0];
     return x ? (__clzll((long long)x) >> ix.lb) : ix.L;
   } else {
-    return key_lcp<WMAX>(ix.keys + i * ix.W, qk, ix);
+    // the first word from its plane (coalesced across lanes); the rest of
+    // the key only when it equals q's
+    const u64 x = __ldg(ix.keys_w0 + i) ^ qk[0];
+    if (x) return __clzll((long long)x) >> ix.lb;
+    const u64* key = ix.keys + i * ix.W;
+#pragma unroll
+    for (int w = 1; w < WMAX; ++w) {
+      if (w < ix.W) {
+        const u64 y = key[w] ^ qk[w];
+        if (y) return w * ix.spw + (__clzll((long long)y) >> ix.lb);
+      }
+    }
+    return ix.L;
   }
 }
+
+
 
 // Stage the top search levels into shared memory with one TMA bulk copy.
 // stage_issue starts the copy; stage_wait blocks on its mbarrier (phase 0),
