@@ -486,7 +486,7 @@ static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, i
   for (int j = 0; j < h; ++j) {
     long long end = dv.level_off[j] +
                     (dv.level_cnt[j] + LCP_SEARCH_FANOUT - 1) / LCP_SEARCH_FANOUT * LCP_SEARCH_FANOUT;
-    if (end * W * 8 > smem_cap) break;
+    if (end * 8 > smem_cap) break;  // the first-word plane is staged
     dv.smem_levels = j + 1;
     dv.smem_entries = (int)end;
   }
@@ -1163,7 +1163,7 @@ static void launch_fast(const lcp_index* ix, const uint16_t* q, int count, int k
     const long long wpc = std::min<long long>(32, std::max<long long>(1, (count + sms - 1) / sms));
     const unsigned block = (unsigned)(wpc * 32);
     const unsigned grid = (unsigned)std::min<long long>((count + wpc - 1) / wpc, 4ll * sms);
-    const size_t smem = 16 + (size_t)dv.smem_entries * dv.W * 8;
+    const size_t smem = 16 + (size_t)dv.smem_entries * 8;
     k_query_warp_tal<WMAX><<<grid, block, smem, st>>>(dv, q, count, k, stride, ids, lcps, hits, md,
                                                       aux, err);
   } else {
@@ -1178,7 +1178,7 @@ static void launch_fast(const lcp_index* ix, const uint16_t* q, int count, int k
     long long wpc = std::min<long long>(32, std::max<long long>(wpc_min, (count + sms - 1) / sms));
     const unsigned block = (unsigned)(wpc * 32);
     unsigned grid = (unsigned)std::min<long long>((count + wpc - 1) / wpc, 4ll * sms);
-    size_t smem = 16 + (size_t)dv.smem_entries * dv.W * 8;
+    size_t smem = 16 + (size_t)dv.smem_entries * 8;
     if constexpr (WMAX == 1) {
       // leaf region: 64 keys cover the +-need window for need <= 16, 96 keys for <= 32
       const long long need = mode == LCP_MODE_COMPLETE ? std::min<long long>(k, dv.n) : k;
@@ -1284,7 +1284,7 @@ static int query_impl(const lcp_index* ix, lcp_workspace* ws, const uint16_t* qu
     const long long wpc = std::min<long long>(wmax, std::max<long long>(1, (count + sms - 1) / sms));
     const unsigned block = (unsigned)(wpc * 32);
     const unsigned grid = (unsigned)std::min<long long>((count + wpc - 1) / wpc, 8ll * sms);
-    const size_t smem0 = 16 + (size_t)dv.smem_entries * dv.W * 8;
+    const size_t smem0 = 16 + (size_t)dv.smem_entries * 8;
 #define LCP_WKN1(WM, NS, TL)                                                                     \
   do {                                                                                           \
     allow_dyn_smem<k_query_warp_kn<WM, NS, TL>>();                                               \

@@ -98,8 +98,8 @@ __device__ __forceinline__ long long warp_lower_bound(const DevIndex& ix, const 
   for (int j = 0;; ++j) {
     const u64* tab;
     long long cnt;
-    if (j < ix.smem_levels) {
-      tab = staged + ix.level_off[j] * W;
+    if (j < ix.smem_levels && WMAX == 1) {
+      tab = staged + ix.level_off[j];
       cnt = ix.level_cnt[j];
     } else {
       tab = ix.levels + ix.level_off[j] * W;
@@ -126,17 +126,17 @@ __device__ __forceinline__ long long warp_lower_bound(const DevIndex& ix, const 
       } else if (i0 < cnt) {
         lt0 = tab[i0] < qk[0];
       }
-    } else if (j < ix.smem_levels) {
-      if (i0 < cnt) lt0 = key_less<WMAX>(tab + i0 * W, qk, ix);
-      if (i0 + 1 < cnt) lt1 = key_less<WMAX>(tab + (i0 + 1) * W, qk, ix);
-    } else {  // global table: the two first words in one 16-byte load
-      const u64* w0 = ix.levels_w0 + ix.level_off[j];
-      if (i0 + 1 < cnt) {
-        const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(w0 + i0));
+    } else {  // first words (staged, or the global plane) in one 16-byte load;
+              // the whole entry from the global table only on a tie
+      const bool sm = j < ix.smem_levels;
+      const u64* w0 = (sm ? staged : ix.levels_w0) + ix.level_off[j];
+      if (i0 + 1 < cnt) {  // plain loads from shared memory, __ldg from global
+        const ulonglong2 v = sm ? *reinterpret_cast<const ulonglong2*>(w0 + i0)
+                                : __ldg(reinterpret_cast<const ulonglong2*>(w0 + i0));
         lt0 = w0_less<WMAX>(v.x, tab + i0 * W, qk, ix);
         lt1 = w0_less<WMAX>(v.y, tab + (i0 + 1) * W, qk, ix);
       } else if (i0 < cnt) {
-        lt0 = w0_less<WMAX>(__ldg(w0 + i0), tab + i0 * W, qk, ix);
+        lt0 = w0_less<WMAX>(sm ? w0[i0] : __ldg(w0 + i0), tab + i0 * W, qk, ix);
       }
     }
     int c = __popc(__ballot_sync(LCP_FULL_MASK, lt0)) + __popc(__ballot_sync(LCP_FULL_MASK, lt1));
@@ -180,9 +180,10 @@ __device__ __forceinline__ void stage_issue(const DevIndex& ix, u64* bar, u64* s
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    u32 bytes = (u32)ix.smem_entries * (u32)ix.W * 8u;
+    // the first-word plane (== levels when W == 1): 8 B per entry
+    u32 bytes = (u32)ix.smem_entries * 8u;
     mbar_arrive_expect_tx(bar, bytes);
-    bulk_g2s(staged, ix.levels, bytes, bar);
+    bulk_g2s(staged, ix.levels_w0, bytes, bar);
   }
 }
 
@@ -1349,7 +1350,7 @@ __global__ void __launch_bounds__(NS > 2 ? QW_MAX_THREADS / 2 : QW_MAX_THREADS, 
   const long long n = ix.n;
   const int L = ix.L;
   const bool complete = TAL || mode == 1;  // TAL: the complete answer with need = k
-  u64* scb = reinterpret_cast<u64*>(smem_raw + 16 + (size_t)ix.smem_entries * ix.W * 8) +
+  u64* scb = reinterpret_cast<u64*>(smem_raw + 16 + (size_t)ix.smem_entries * 8) +
              warp * (32 * NS);
 
   for (long long qi = (long long)blockIdx.x * warps + warp; qi < count;
