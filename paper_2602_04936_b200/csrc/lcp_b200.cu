@@ -464,7 +464,8 @@ static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, i
     LCP_CK_LAUNCH();
   }
   dv.levels = ix->levels;
-  dv.levels_w0 = ix->levels;
+  dv.levels_w0 = ix->levels;  // W == 1: the keys / levels are their own first-word planes
+  dv.keys_w0 = ix->keys;
   if (W > 1) {  // first-word planes: W > 1 comparisons read 8 B per entry / key
     // (coalesced) and the whole key only when the first words are equal
     const long long lt = std::max(2ll, total);

@@ -1623,6 +1623,27 @@ __device__ __forceinline__ long long prefix_bound(const DevIndex& ix, const u64*
   return a;
 }
 
+// Any-W helpers for the general path: the first word from the sorted
+// first-word plane (keys_w0 / levels_w0; the keys / levels themselves when
+// W == 1), the rest of the key only when the first words are equal.
+__device__ __forceinline__ int lcp_any(const DevIndex& ix, long long i, const u64* q) {
+  const u64 x = __ldg(ix.keys_w0 + i) ^ q[0];
+  if (x) return __clzll((long long)x) >> ix.lb;
+  const u64* key = ix.keys + i * ix.W;
+  for (int w = 1; w < ix.W; ++w) {
+    const u64 y = key[w] ^ q[w];
+    if (y) return w * ix.spw + (__clzll((long long)y) >> ix.lb);
+  }
+  return ix.L;
+}
+
+__device__ __forceinline__ bool less_any(const DevIndex& ix, u64 a0, const u64* key, const u64* q) {
+  if (a0 != q[0]) return a0 < q[0];
+  for (int w = 1; w < ix.W; ++w)
+    if (key[w] != q[w]) return key[w] < q[w];
+  return false;
+}
+
 // lower_bound(keys, q) for any W by one warp: 64-ary over the global search
 // tables (two separators per lane per level), then the 16-key leaf block
 __device__ __forceinline__ long long warp_lower_bound_any(const DevIndex& ix, const u64* q) {
@@ -1633,15 +1654,16 @@ __device__ __forceinline__ long long warp_lower_bound_any(const DevIndex& ix, co
     const u64* tab = ix.levels + ix.level_off[j] * W;
     const long long cnt = ix.level_cnt[j];
     const long long i0 = blk * LCP_SEARCH_FANOUT + 2 * lane;
-    const bool lt0 = i0 < cnt && key_less<0>(tab + i0 * W, q, ix);
-    const bool lt1 = i0 + 1 < cnt && key_less<0>(tab + (i0 + 1) * W, q, ix);
+    const u64* w0 = ix.levels_w0 + ix.level_off[j];
+    const bool lt0 = i0 < cnt && less_any(ix, __ldg(w0 + i0), tab + i0 * W, q);
+    const bool lt1 = i0 + 1 < cnt && less_any(ix, __ldg(w0 + i0 + 1), tab + (i0 + 1) * W, q);
     const int c = __popc(__ballot_sync(LCP_FULL_MASK, lt0)) + __popc(__ballot_sync(LCP_FULL_MASK, lt1));
     if (c == 0) return 0;  // only at the root: q <= every key
     blk = blk * LCP_SEARCH_FANOUT + c - 1;
   }
   const long long base = blk * LCP_LEAF_KEYS;
   const long long i = base + lane;
-  const bool lt = lane < LCP_LEAF_KEYS && i < ix.n && key_less<0>(ix.keys + i * W, q, ix);
+  const bool lt = lane < LCP_LEAF_KEYS && i < ix.n && less_any(ix, __ldg(ix.keys_w0 + i), ix.keys + i * W, q);
   return base + __popc(__ballot_sync(LCP_FULL_MASK, lt));
 }
 
@@ -1654,7 +1676,7 @@ __device__ __forceinline__ long long run_edge_any(const DevIndex& ix, const u64*
     if (span <= 1) return in;
     const long long step = (span + 31) >> 5;
     const long long off = step * (lane_id() + 1);
-    const bool inside = off < span && key_lcp<0>(ix.keys + (in + dir * off) * ix.W, q, ix) >= d;
+    const bool inside = off < span && lcp_any(ix, in + dir * off, q) >= d;
     const long long c = __popc(__ballot_sync(LCP_FULL_MASK, inside));
     if (step * (c + 1) < span) out = in + dir * step * (c + 1);
     in += dir * step * c;
@@ -1666,8 +1688,7 @@ struct GenItem {
   const u64* q;
   bool fullscan;
   __device__ __forceinline__ u64 comp(long long i, int* lcp_out) const {
-    const u64* key = fullscan ? ix->keys_orig + i * ix->W : ix->keys + i * ix->W;
-    int l = key_lcp<0>(key, q, *ix);
+    int l = fullscan ? key_lcp<0>(ix->keys_orig + i * ix->W, q, *ix) : lcp_any(*ix, i, q);
     *lcp_out = l;
     u32 id = fullscan ? (u32)i : ix->order[i];
     return make_composite(l, id, ix->L);
@@ -1716,7 +1737,7 @@ __global__ void __launch_bounds__(GEN_THREADS)
       int* wl = reinterpret_cast<int*>(buf);  // window lcps (<= GEN_CAP ints)
       int mymax = -1;
       for (int i = threadIdx.x; i < wn; i += GEN_THREADS) {
-        const int l = key_lcp<0>(ix.keys + (wlo + i) * ix.W, q, ix);
+        const int l = lcp_any(ix, wlo + i, q);
         wl[i] = l;
         mymax = max(mymax, l);
       }
@@ -1781,8 +1802,8 @@ __global__ void __launch_bounds__(GEN_THREADS)
       // both sides of the deepest match p0, and d* by binary search over depths
       if (warp == 0) {
         const long long pos = warp_lower_bound_any(ix, q);
-        const int lp = pos > 0 ? key_lcp<0>(ix.keys + (pos - 1) * ix.W, q, ix) : -1;
-        const int lq = pos < ix.n ? key_lcp<0>(ix.keys + pos * ix.W, q, ix) : -1;
+        const int lp = pos > 0 ? lcp_any(ix, pos - 1, q) : -1;
+        const int lq = pos < ix.n ? lcp_any(ix, pos, q) : -1;
         const int dmax = max(lp, lq);
         const long long p0 = lq == dmax ? pos : pos - 1;
         auto range = [&](int d, long long& a, long long& b) {
