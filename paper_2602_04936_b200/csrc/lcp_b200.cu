@@ -1316,6 +1316,15 @@ static int query_impl(const lcp_index* ix, lcp_workspace* ws, const uint16_t* qu
   k_pack<<<blocks_for((long long)count * dv.W, 256), 256, 0, st>>>(
       queries, count, dv.L, dv.W, dv.b, dv.spw, dv.sigma, ws->qkeys.as<u64>(), nullptr, errp);
   LCP_CK_LAUNCH();
+  if (dv.W > 8 && mode != LCP_MODE_TAL && k <= FAST_KMAX) {  // long keys: warp per query
+    const long long sms = num_sms();
+    const long long wpc = std::min<long long>(32, std::max<long long>(1, (count + sms - 1) / sms));
+    const unsigned grid = (unsigned)std::min<long long>((count + wpc - 1) / wpc, 8ll * sms);
+    k_query_warp_any<<<grid, (unsigned)(wpc * 32), 0, st>>>(dv, ws->qkeys.as<u64>(), count, k, mode,
+                                                            out_stride, ids, lcps, hits, md, ax);
+    LCP_CK_LAUNCH();
+    return LCP_OK;
+  }
   unsigned grid = (unsigned)gen_grid(count);
   k_query_general<<<grid, GEN_THREADS, 0, st>>>(dv, ws->qkeys.as<u64>(), queries, count, k, mode,
                                                 0, out_stride, ids, lcps, hits, md, ax);

@@ -1683,6 +1683,99 @@ __device__ __forceinline__ long long run_edge_any(const DevIndex& ix, const u64*
   }
 }
 
+// ---------------------------------------------------------------------------
+// strict / complete, k <= 32, W > 8 (long keys): one warp per query like
+// k_query_warp, with the packed query read from qkeys (k_pack) instead of
+// registers, so any W works: the any-W search, a 64-key window [pos - 32,
+// pos + 32), rank selection, extension by chunks and then run_edge_any + the
+// id sketch.  Compares read the first-word planes (lcp_any).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(QW_MAX_THREADS, 1)
+    k_query_warp_any(const __grid_constant__ DevIndex ix, const u64* __restrict__ qkeys, int count,
+                     int k, int mode, int stride, u32* __restrict__ out_ids,
+                     uint16_t* __restrict__ out_lcps, int* __restrict__ out_hits,
+                     uint16_t* __restrict__ out_md, u64* __restrict__ out_aux) {
+  const int lane = lane_id();
+  const int warp = threadIdx.x >> 5;
+  const int warps = blockDim.x >> 5;
+  const long long n = ix.n;
+  const int L = ix.L;
+  const bool complete = mode == 1;
+  for (long long qi = (long long)blockIdx.x * warps + warp; qi < count;
+       qi += (long long)gridDim.x * warps) {
+    const u64* q = qkeys + qi * ix.W;
+    const long long pos = warp_lower_bound_any(ix, q);
+    const long long s = pos - 32;  // window [s, s + 64), warp-strided
+    int l[2];
+    u32 id[2];
+    int dmax = -1;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const long long i = s + t * 32 + lane;
+      const bool ok = i >= 0 && i < n;
+      l[t] = ok ? lcp_any(ix, i, q) : -1;
+      id[t] = ok ? __ldg(ix.order + i) : 0u;
+      dmax = max(dmax, l[t]);
+    }
+    dmax = (int)__reduce_max_sync(LCP_FULL_MASK, (unsigned)(dmax + 1)) - 1;
+    const int need = complete ? (int)min((long long)k, n) : k;
+    const int dstar = complete ? window_dstar<2>(l, dmax, need) : dmax;
+    u64 comp[2];
+    int cnt = 0, r0 = 64;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const bool c = l[t] >= dstar;
+      comp[t] = c ? make_comp<u64>(l[t], id[t], L, 32) : ~0ull;
+      const unsigned m = __ballot_sync(LCP_FULL_MASK, c);
+      cnt += __popc(m);
+      if (m && r0 == 64) r0 = t * 32 + __ffs(m) - 1;
+    }
+    u64 slot = sort_run<u64, 2>(comp, r0, cnt, need);
+    u64 thr = __shfl_sync(LCP_FULL_MASK, slot, need - 1);
+    long long rsize = cnt, rlo = s + r0;
+    const long long first_valid = s < 0 ? -s : 0;
+    const long long end = min(s + 64, n);
+    const u64 tier = make_comp<u64>(dstar, 0u, L, 32);
+    bool goL = s > 0 && r0 == first_valid, goR = end < n && s + r0 + cnt == end;
+    long long eL = s, eR = end;  // [eL, eR) is scanned
+    const int ext_chunks = dstar ? EXT_SCAN_CHUNKS : 0;
+    for (int chunk = 0; goL && chunk < ext_chunks; ++chunk) {
+      const long long i = eL - 32 + lane;
+      const int li = i >= 0 ? lcp_any(ix, i, q) : -1;
+      const bool c = li >= dstar;
+      warp_offer(slot, thr, c ? make_comp<u64>(li, __ldg(ix.order + i), L, 32) : ~0ull, need);
+      const unsigned m = __ballot_sync(LCP_FULL_MASK, c);
+      rsize += __popc(m);
+      if (m) rlo = eL - 32 + (__ffs(m) - 1);
+      eL -= 32;
+      goL = m == LCP_FULL_MASK && eL > 0;
+    }
+    for (int chunk = 0; goR && chunk < ext_chunks; ++chunk) {
+      const long long i = eR + lane;
+      const int li = i < n ? lcp_any(ix, i, q) : -1;
+      const bool c = li >= dstar;
+      warp_offer(slot, thr, c ? make_comp<u64>(li, __ldg(ix.order + i), L, 32) : ~0ull, need);
+      const unsigned m = __ballot_sync(LCP_FULL_MASK, c);
+      rsize += __popc(m);
+      eR += 32;
+      goR = m == LCP_FULL_MASK && eR < n;
+    }
+    if (goL || goR) {  // past the scanned span every item has lcp == d*: the id sketch
+      const long long rl = goL ? (dstar ? run_edge_any(ix, q, dstar, eL, -1) : 0) : eL;
+      const long long rr = goR ? (dstar ? run_edge_any(ix, q, dstar, eR - 1, n) + 1 : n) : eR;
+      rsize += (eL - rl) + (rr - eR);
+      if (goL) {
+        rlo = rl;
+        slot = tier_offer<u64>(ix, rl, eL, tier, slot, need);
+      }
+      if (goR) slot = tier_offer<u64>(ix, eR, rr, tier, slot, need);
+    }
+    const int take = (int)min((long long)need, rsize);
+    write_result<u64>(qi, stride, take, L, slot, 32, dmax, dstar, rsize, rlo, out_ids, out_lcps,
+                      out_hits, out_md, out_aux);
+  }
+}
+
 struct GenItem {
   const DevIndex* ix;
   const u64* q;

@@ -754,3 +754,34 @@ def test_wide_keys_list_kernel_vs_oracle(gpu, oracle_lib):
                     assert b.pairs(i) == exp, (name, buckets, k, i)
                 assert np.array_equal(b.aux[:, 0].astype(np.int64), items_)
                 assert np.array_equal(b.aux[:, 1].astype(np.int64), sym)
+
+
+def test_long_keys_warp_kernel_vs_oracle(gpu, oracle_lib):
+    """W > 8 with k <= 32 (k_query_warp_any): the any-W search, window,
+    chunk extension and id-sketch long runs, at a scale where runs leave the
+    window, for uniform and clustered corpora and near-duplicate queries."""
+    cases = [
+        ("L300-s4", lg.generate_dataset(50_000, 300, 4, seed=60)),
+        ("L256-s256", lg.generate_dataset(30_000, 256, 256, seed=61)),
+        ("L300-s4-clustered", lg.generate_dataset(40_000, 300, 4, seed=62, distribution="clustered")),
+    ]
+    for name, ds in cases:
+        idx = lg.build(ds)
+        assert idx.native.words > 8
+        ot = oracle_lib.OracleTrie(ds.items, ds.alphabet.size)
+        near = ds.items[:16].copy()
+        near[:, -1] = (near[:, -1] + 1) % ds.alphabet.size
+        qs = np.vstack([lg.generate_queries(ds, 40, seed=63),
+                        lg.generate_queries(ds, 40, seed=64, prefix_len=ds.length // 4),
+                        lg.generate_queries(ds, 24, seed=65, prefix_len=2), near])
+        for k in (1, 5, 10, 16, 17, 32):
+            for mode in ("complete", "strict"):
+                b = idx.query_batch(qs, k, mode)
+                ids, lcps, hits, md, sym, nodes = ot.query_batch(qs, k, mode)
+                for i in range(len(qs)):
+                    exp = list(zip(ids[i, :hits[i]].tolist(), lcps[i, :hits[i]].tolist()))
+                    assert b.pairs(i) == exp, (name, k, mode, i)
+                    assert int(b.matched_depth[i]) == md[i]
+                w = idx.new_work_report()
+                idx.query_batch(qs, k, mode, work=w)
+                assert w.nodes_visited == int(nodes.sum()) and w.symbols_compared == int(sym.sum()), (name, k, mode)
