@@ -1325,6 +1325,23 @@ static int query_impl(const lcp_index* ix, lcp_workspace* ws, const uint16_t* qu
     LCP_CK_LAUNCH();
     return LCP_OK;
   }
+  if (dv.W > 8 && mode != LCP_MODE_TAL && needk > FAST_KMAX && needk <= 128) {  // long keys, lists
+    const long long sms = num_sms();
+    const long long wmax = needk <= 64 ? 32 : 16;  // 4-slot lists: 512-thread CTAs
+    const long long wpc = std::min<long long>(wmax, std::max<long long>(1, (count + sms - 1) / sms));
+    const unsigned grid = (unsigned)std::min<long long>((count + wpc - 1) / wpc, 8ll * sms);
+    if (needk <= 64) {
+      allow_dyn_smem<k_query_warp_any_kn<2>>();
+      k_query_warp_any_kn<2><<<grid, (unsigned)(wpc * 32), (size_t)wpc * 64 * 8, st>>>(
+          dv, ws->qkeys.as<u64>(), count, k, mode, out_stride, ids, lcps, hits, md, ax);
+    } else {
+      allow_dyn_smem<k_query_warp_any_kn<4>>();
+      k_query_warp_any_kn<4><<<grid, (unsigned)(wpc * 32), (size_t)wpc * 128 * 8, st>>>(
+          dv, ws->qkeys.as<u64>(), count, k, mode, out_stride, ids, lcps, hits, md, ax);
+    }
+    LCP_CK_LAUNCH();
+    return LCP_OK;
+  }
   unsigned grid = (unsigned)gen_grid(count);
   k_query_general<<<grid, GEN_THREADS, 0, st>>>(dv, ws->qkeys.as<u64>(), queries, count, k, mode,
                                                 0, out_stride, ids, lcps, hits, md, ax);

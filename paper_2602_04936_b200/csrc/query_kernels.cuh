@@ -1776,6 +1776,133 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// strict / complete, 32 < need <= 32 * NS <= 128, W > 8: k_query_warp_kn on
+// the packed-query buffer with the any-W helpers (see k_query_warp_any).
+// ---------------------------------------------------------------------------
+template <int NS>
+__global__ void __launch_bounds__(NS > 2 ? QW_MAX_THREADS / 2 : QW_MAX_THREADS, 1)
+    k_query_warp_any_kn(const __grid_constant__ DevIndex ix, const u64* __restrict__ qkeys,
+                        int count, int k, int mode, int stride, u32* __restrict__ out_ids,
+                        uint16_t* __restrict__ out_lcps, int* __restrict__ out_hits,
+                        uint16_t* __restrict__ out_md, u64* __restrict__ out_aux) {
+  constexpr int T = 2 * NS;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = lane_id();
+  const int warp = threadIdx.x >> 5;
+  const int warps = blockDim.x >> 5;
+  const long long n = ix.n;
+  const int L = ix.L;
+  const bool complete = mode == 1;
+  u64* scb = reinterpret_cast<u64*>(smem_raw) + warp * (32 * NS);
+  for (long long qi = (long long)blockIdx.x * warps + warp; qi < count;
+       qi += (long long)gridDim.x * warps) {
+    const u64* q = qkeys + qi * ix.W;
+    const long long pos = warp_lower_bound_any(ix, q);
+    const long long s = pos - 32 * NS;
+    int l[T];
+    u32 id[T];
+    int dmax = -1;
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const long long i = s + t * 32 + lane;
+      const bool ok = i >= 0 && i < n;
+      l[t] = ok ? lcp_any(ix, i, q) : -1;
+      id[t] = ok ? __ldg(ix.order + i) : 0u;
+      dmax = max(dmax, l[t]);
+    }
+    dmax = (int)__reduce_max_sync(LCP_FULL_MASK, (unsigned)(dmax + 1)) - 1;
+    const int need = complete ? (int)min((long long)k, n) : k;
+    const int dstar = complete ? window_dstar<T>(l, dmax, need) : dmax;
+    TopKN<u64, NS> lst;
+    lst.init(scb);
+    int cnt = 0, r0 = 32 * T, above = 0;
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const bool c = l[t] >= dstar;
+      const unsigned m = __ballot_sync(LCP_FULL_MASK, c);
+      cnt += __popc(m);
+      above += __popc(__ballot_sync(LCP_FULL_MASK, l[t] > dstar));
+      if (m && r0 == 32 * T) r0 = t * 32 + __ffs(m) - 1;
+      lst.offer(c ? make_comp<u64>(l[t], id[t], L, 32) : ~0ull, need);
+    }
+    const long long first_valid = s < 0 ? -s : 0;
+    const long long end = min(s + 32 * T, n);
+    long long rsize = cnt, rlo = s + r0;
+    const u64 tier = make_comp<u64>(dstar, 0u, L, 32);
+    const bool sketch_ok = need - above <= LCP_SK_LIST;
+    bool goL = s > 0 && r0 == first_valid, goR = end < n && s + r0 + cnt == end;
+    long long eL = s, eR = end;
+    const int ext_chunks = dstar ? EXT_SCAN_CHUNKS : 0;
+    for (int chunk = 0; goL && chunk < ext_chunks; ++chunk) {
+      const long long i = eL - 32 + lane;
+      const int li = i >= 0 ? lcp_any(ix, i, q) : -1;
+      const bool c = li >= dstar;
+      lst.offer(c ? make_comp<u64>(li, __ldg(ix.order + i), L, 32) : ~0ull, need);
+      const unsigned m = __ballot_sync(LCP_FULL_MASK, c);
+      rsize += __popc(m);
+      if (m) rlo = eL - 32 + (__ffs(m) - 1);
+      eL -= 32;
+      goL = m == LCP_FULL_MASK && eL > 0;
+    }
+    for (int chunk = 0; goR && chunk < ext_chunks; ++chunk) {
+      const long long i = eR + lane;
+      const int li = i < n ? lcp_any(ix, i, q) : -1;
+      const bool c = li >= dstar;
+      lst.offer(c ? make_comp<u64>(li, __ldg(ix.order + i), L, 32) : ~0ull, need);
+      const unsigned m = __ballot_sync(LCP_FULL_MASK, c);
+      rsize += __popc(m);
+      eR += 32;
+      goR = m == LCP_FULL_MASK && eR < n;
+    }
+    if (goL || goR) {
+      const long long rl = goL ? (dstar ? run_edge_any(ix, q, dstar, eL, -1) : 0) : eL;
+      const long long rr = goR ? (dstar ? run_edge_any(ix, q, dstar, eR - 1, n) + 1 : n) : eR;
+      const long long rest = (eL - rl) + (rr - eR);
+      rsize += rest;
+      if (goL) rlo = rl;
+      if (sketch_ok) {
+        if (goL) lst = tier_offer_n<u64, NS>(ix, rl, eL, tier, lst, need);
+        if (goR) lst = tier_offer_n<u64, NS>(ix, eR, rr, tier, lst, need);
+      } else if (16 * rest >= n) {
+        for (long long base = 0; base < n && (tier | (u64)base) < lst.thr; base += 32) {
+          const long long idv = base + lane;
+          u64 cv = ~0ull;
+          if (idv < n) {
+            const long long p = __ldg(ix.rank + idv);
+            if ((p >= rl && p < eL) || (p >= eR && p < rr)) cv = tier | (u64)idv;
+          }
+          lst.offer(cv, need);
+        }
+      } else {
+        for (long long base = rl; base < eL; base += 32) {
+          const long long i = base + lane;
+          lst.offer(i < eL ? (tier | (u64)__ldg(ix.order + i)) : ~0ull, need);
+        }
+        for (long long base = eR; base < rr; base += 32) {
+          const long long i = base + lane;
+          lst.offer(i < rr ? (tier | (u64)__ldg(ix.order + i)) : ~0ull, need);
+        }
+      }
+    }
+    const int take = (int)min((long long)need, rsize);
+#pragma unroll
+    for (int j = 0; j < NS; ++j) {
+      if (lane + 32 * j < take) {
+        const u64 w = lst.s[j];
+        out_ids[(size_t)qi * stride + lane + 32 * j] = (u32)(w & 0xffffffffull);
+        out_lcps[(size_t)qi * stride + lane + 32 * j] = (uint16_t)(L - (int)(w >> 32));
+      }
+    }
+    if (lane == 0) {
+      out_hits[qi] = take;
+      out_md[qi] = (uint16_t)dmax;
+      out_aux[2 * qi] = (u64)(u32)dmax | ((u64)(u32)dstar << 32);
+      out_aux[2 * qi + 1] = (u64)rsize | ((u64)rlo << 32);
+    }
+  }
+}
+
 struct GenItem {
   const DevIndex* ix;
   const u64* q;

@@ -757,7 +757,7 @@ def test_wide_keys_list_kernel_vs_oracle(gpu, oracle_lib):
 
 
 def test_long_keys_warp_kernel_vs_oracle(gpu, oracle_lib):
-    """W > 8 with k <= 32 (k_query_warp_any): the any-W search, window,
+    """W > 8 with k <= 128 (k_query_warp_any, k_query_warp_any_kn): the any-W search, window,
     chunk extension and id-sketch long runs, at a scale where runs leave the
     window, for uniform and clustered corpora and near-duplicate queries."""
     cases = [
@@ -774,7 +774,7 @@ def test_long_keys_warp_kernel_vs_oracle(gpu, oracle_lib):
         qs = np.vstack([lg.generate_queries(ds, 40, seed=63),
                         lg.generate_queries(ds, 40, seed=64, prefix_len=ds.length // 4),
                         lg.generate_queries(ds, 24, seed=65, prefix_len=2), near])
-        for k in (1, 5, 10, 16, 17, 32):
+        for k in (1, 5, 10, 16, 17, 32, 33, 64, 65, 100, 128):  # k_query_warp_any(_kn)
             for mode in ("complete", "strict"):
                 b = idx.query_batch(qs, k, mode)
                 ids, lcps, hits, md, sym, nodes = ot.query_batch(qs, k, mode)
