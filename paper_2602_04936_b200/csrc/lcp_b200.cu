@@ -1176,9 +1176,14 @@ static void launch_fast(const lcp_index* ix, const uint16_t* q, int count, int k
       const char* e = getenv("LCP_WPC_MIN");
       return e ? std::max(1ll, std::min(32ll, atoll(e))) : 1ll;
     }();
-    long long wpc = std::min<long long>(32, std::max<long long>(wpc_min, (count + sms - 1) / sms));
+    static const long long qpw = [] {  // LCP_QPW: A/B hook (queries per warp)
+      const char* e = getenv("LCP_QPW");
+      return e ? std::max(1ll, std::min(16ll, atoll(e))) : 1ll;
+    }();
+    const long long units = (count + qpw - 1) / qpw;
+    long long wpc = std::min<long long>(32, std::max<long long>(wpc_min, (units + sms - 1) / sms));
     const unsigned block = (unsigned)(wpc * 32);
-    unsigned grid = (unsigned)std::min<long long>((count + wpc - 1) / wpc, 4ll * sms);
+    unsigned grid = (unsigned)std::min<long long>((units + wpc - 1) / wpc, 4ll * sms);
     size_t smem = 16 + (size_t)dv.smem_entries * 8;
     if constexpr (WMAX == 1) {
       // leaf region: 64 keys cover the +-need window for need <= 16, 96 keys for <= 32
