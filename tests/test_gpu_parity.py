@@ -785,3 +785,57 @@ def test_long_keys_warp_kernel_vs_oracle(gpu, oracle_lib):
                 w = idx.new_work_report()
                 idx.query_batch(qs, k, mode, work=w)
                 assert w.nodes_visited == int(nodes.sum()) and w.symbols_compared == int(sym.sum()), (name, k, mode)
+
+
+@pytest.mark.parametrize("mode", ["strict", "complete"])
+def test_graph_replay_multistream_matches_sync(gpu, mode):
+    """The bench's device path: batches captured once in a CUDA graph, fanned
+    out over 4 streams sharing one workspace, replayed repeatedly. Every replay
+    must reproduce the synchronous host API's results bit for bit."""
+    import torch
+
+    from paper_2602_04936_b200._native import workspace
+
+    ds = lg.generate_dataset(200_000, 32, 4, seed=31)
+    idx = lg.build(ds)
+    k, nb, bs = 10, 4, 1024
+    qs = np.vstack([lg.generate_queries(ds, bs, seed=32 + b, prefix_len=(0 if b % 2 else 16))
+                    for b in range(nb)])
+    want = idx.query_batch(qs, k, mode)
+    dev = torch.device("cuda")
+    dq = torch.from_numpy(qs).to(dev).view(nb, bs, 32)
+    bufs = [(torch.empty((bs, k), dtype=torch.int32, device=dev),
+             torch.empty((bs, k), dtype=torch.int16, device=dev),
+             torch.empty(bs, dtype=torch.int32, device=dev),
+             torch.empty(bs, dtype=torch.int16, device=dev)) for _ in range(nb)]
+    workspace()  # allocated outside capture
+    main = torch.cuda.Stream()  # capture needs a non-default stream
+    main.wait_stream(torch.cuda.current_stream())
+    streams = [torch.cuda.Stream() for _ in range(nb)]
+    for b in range(nb):  # eager warm-up: workspace scratch grows outside capture
+        ids, lcps, hits, md = bufs[b]
+        idx.native.query_device(dq[b], k, mode, ids, lcps, hits, md, stream=main.cuda_stream)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=main):
+        for x in streams:
+            x.wait_stream(main)
+        for b, x in enumerate(streams):
+            ids, lcps, hits, md = bufs[b]
+            idx.native.query_device(dq[b], k, mode, ids, lcps, hits, md, stream=x.cuda_stream)
+        for x in streams:
+            main.wait_stream(x)
+    for _ in range(3):
+        for ids, lcps, hits, md in bufs:
+            ids.fill_(-1), lcps.fill_(-1), hits.fill_(-1), md.fill_(-1)
+        g.replay()
+        torch.cuda.synchronize()
+        for b, (ids, lcps, hits, md) in enumerate(bufs):
+            sl = slice(b * bs, (b + 1) * bs)
+            assert np.array_equal(hits.cpu().numpy(), want.hits[sl])
+            assert np.array_equal(md.cpu().numpy().view(np.uint16), want.matched_depth[sl])
+            got_ids, got_l = ids.cpu().numpy().view(np.uint32), lcps.cpu().numpy().view(np.uint16)
+            for i in range(0, bs, 7):
+                h = want.hits[b * bs + i]
+                assert np.array_equal(got_ids[i, :h], want.ids[b * bs + i, :h])
+                assert np.array_equal(got_l[i, :h], want.lcps[b * bs + i, :h])
