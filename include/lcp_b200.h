@@ -21,6 +21,10 @@
  *  - A built lcp_index is immutable; concurrent queries are safe as long as
  *    each thread uses its own lcp_workspace (reference: trie.py:19-20,
  *    SPEC.md:197-198 "queried concurrently without synchronization").
+ *    A workspace's scratch (packed queries, unrequested matched_depth / aux
+ *    outputs, full-scan lists) is shared by every call made with it, so
+ *    calls in flight at the same time on different streams need different
+ *    workspaces.
  */
 #ifndef LCP_B200_H
 #define LCP_B200_H

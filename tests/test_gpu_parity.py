@@ -787,16 +787,18 @@ def test_long_keys_warp_kernel_vs_oracle(gpu, oracle_lib):
                 assert w.nodes_visited == int(nodes.sum()) and w.symbols_compared == int(sym.sum()), (name, k, mode)
 
 
+@pytest.mark.parametrize("sigma", [4, 256])  # W = 1 and W = 4 (packed-query scratch)
 @pytest.mark.parametrize("mode", ["strict", "complete"])
-def test_graph_replay_multistream_matches_sync(gpu, mode):
+def test_graph_replay_multistream_matches_sync(gpu, mode, sigma):
     """The bench's device path: batches captured once in a CUDA graph, fanned
-    out over 4 streams sharing one workspace, replayed repeatedly. Every replay
-    must reproduce the synchronous host API's results bit for bit."""
+    out over 4 streams (one workspace each, per the header's contract),
+    replayed repeatedly. Every replay must reproduce the synchronous host API's
+    results bit for bit."""
     import torch
 
-    from paper_2602_04936_b200._native import workspace
+    from paper_2602_04936_b200._native import Workspace
 
-    ds = lg.generate_dataset(200_000, 32, 4, seed=31)
+    ds = lg.generate_dataset(200_000, 32, sigma, seed=31)
     idx = lg.build(ds)
     k, nb, bs = 10, 4, 1024
     qs = np.vstack([lg.generate_queries(ds, bs, seed=32 + b, prefix_len=(0 if b % 2 else 16))
@@ -808,13 +810,13 @@ def test_graph_replay_multistream_matches_sync(gpu, mode):
              torch.empty((bs, k), dtype=torch.int16, device=dev),
              torch.empty(bs, dtype=torch.int32, device=dev),
              torch.empty(bs, dtype=torch.int16, device=dev)) for _ in range(nb)]
-    workspace()  # allocated outside capture
+    wss = [Workspace() for _ in range(nb)]  # allocated outside capture
     main = torch.cuda.Stream()  # capture needs a non-default stream
     main.wait_stream(torch.cuda.current_stream())
     streams = [torch.cuda.Stream() for _ in range(nb)]
     for b in range(nb):  # eager warm-up: workspace scratch grows outside capture
         ids, lcps, hits, md = bufs[b]
-        idx.native.query_device(dq[b], k, mode, ids, lcps, hits, md, stream=main.cuda_stream)
+        idx.native.query_device(dq[b], k, mode, ids, lcps, hits, md, stream=main.cuda_stream, ws=wss[b])
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=main):
@@ -822,7 +824,7 @@ def test_graph_replay_multistream_matches_sync(gpu, mode):
             x.wait_stream(main)
         for b, x in enumerate(streams):
             ids, lcps, hits, md = bufs[b]
-            idx.native.query_device(dq[b], k, mode, ids, lcps, hits, md, stream=x.cuda_stream)
+            idx.native.query_device(dq[b], k, mode, ids, lcps, hits, md, stream=x.cuda_stream, ws=wss[b])
         for x in streams:
             main.wait_stream(x)
     for _ in range(3):
