@@ -277,7 +277,7 @@ def main() -> None:
                     torch.empty(BATCH, dtype=torch.int16, device=dev),
                     torch.empty((n_pool, BATCH, 2), dtype=torch.int64, device=dev))
 
-        from paper_2602_04936_b200._native import workspace
+        from paper_2602_04936_b200._native import Workspace, workspace
 
         workspace()  # created outside graph capture (it allocates)
         t_rep = time.perf_counter()
@@ -289,6 +289,7 @@ def main() -> None:
 
         def capture(n_steps: int, n_streams: int):
             streams = [torch.cuda.Stream(device=dev) for _ in range(n_streams)]
+            wss = [Workspace() for _ in range(n_streams)]  # one per stream (lcp_b200.h contract)
             bufs = [out_bufs() for _ in range(n_streams)]
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=main_stream):
@@ -298,9 +299,11 @@ def main() -> None:
                     x, (ids, lcps, hits, md, aux) = streams[i % n_streams], bufs[i % n_streams]
                     b = (i // R) % n_pool
                     replicas[i % R].native.query_device(dq[b], K, "complete", ids, lcps, hits, md,
-                                                       aux[b], stream=x.cuda_stream)
+                                                       aux[b], stream=x.cuda_stream,
+                                                       ws=wss[i % n_streams])
                 for x in streams:
                     main_stream.wait_stream(x)
+            g.workspaces = wss  # the graph holds their scratch pointers: keep them alive
             return g, bufs
 
         def run_steps(n_streams: int, steps: int, warmup: int):
