@@ -212,6 +212,18 @@ def async_workspace() -> Workspace:
     return ws
 
 
+def reset_async_ring() -> None:
+    """Complete this thread's in-flight async batches and restart the ring at
+    its first workspace (so a caller cycling buffers in lockstep with the ring
+    sees the same workspace for the same buffers; its graph cache hits)."""
+    ring = getattr(_tls, "ring", None)
+    if ring is None:
+        return
+    for ws in ring:
+        ws.wait()
+    _tls.ring_pos = 0
+
+
 class _PinnedMemory:
     """Owner of one page-locked block.  Freed (or returned to the per-size
     pool) only when the last numpy view of it is gone: every view's base chain

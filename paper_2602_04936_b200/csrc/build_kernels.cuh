@@ -37,6 +37,98 @@ __global__ void k_pack(const uint16_t* __restrict__ rows, long long n, int L, in
   if (ids != nullptr && w == 0) ids[row] = (u32)row;
 }
 
+// ---------------------------------------------------------------------------
+// pack, streaming form (L % 8 == 0, the rows 16-byte aligned): the (n, L)
+// uint16 corpus is read as a flat stream of 16-byte chunks (8 symbols), one
+// `ld.global.nc.v4` per lane, so a warp reads 512 contiguous bytes.  A chunk
+// never straddles a key word (spw is a multiple of 8 for b <= 8; for b = 16 a
+// chunk is exactly two words), so each lane packs its 8 symbols in place and
+// the lanes of one word OR their parts with a segmented shuffle reduction;
+// the first lane of the word stores it.  A warp "unit" is whole rows
+// (cpr = L/8 <= 32 chunks per row: 32/cpr rows) or a 32-chunk piece of one
+// row (cpr > 32), so no word is split across units.  4 units per lane are in
+// flight.  Replaces the big-endian byte view of core.py:172-173.
+// ---------------------------------------------------------------------------
+constexpr int PK_THREADS = 256;
+constexpr int PK_UNROLL = 4;
+
+__global__ void __launch_bounds__(PK_THREADS) k_pack_stream(
+    const uint16_t* __restrict__ rows, long long n, int L, int W, int b, int spw, int sigma,
+    u64* __restrict__ keys, u32* __restrict__ ids, int* __restrict__ err) {
+  const int lane = lane_id();
+  const int cpr = L >> 3;                          // 16-byte chunks per row
+  const int rpu = cpr <= 32 ? 32 / cpr : 1;        // rows per unit
+  const int ppr = cpr <= 32 ? 1 : (cpr + 31) >> 5; // units per row
+  const long long units = cpr <= 32 ? (n + rpu - 1) / rpu : n * ppr;
+  const int gsize = b == 16 ? 1 : spw >> 3;        // chunks per key word
+  const long long warp0 = ((long long)blockIdx.x * PK_THREADS + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * PK_THREADS) >> 5;
+  bool bad = false;
+  for (long long u0 = warp0; u0 < units; u0 += nwarps * PK_UNROLL) {
+    uint4 v[PK_UNROLL];
+    long long row[PK_UNROLL];
+    int j[PK_UNROLL];
+    bool ok[PK_UNROLL];
+#pragma unroll
+    for (int t = 0; t < PK_UNROLL; ++t) {
+      const long long u = u0 + (long long)t * nwarps;
+      if (cpr <= 32) {
+        row[t] = u * rpu + lane / cpr;
+        j[t] = lane % cpr;
+        ok[t] = u < units && lane < rpu * cpr && row[t] < n;
+      } else {
+        row[t] = u / ppr;
+        j[t] = (int)(u - row[t] * ppr) * 32 + lane;
+        ok[t] = u < units && j[t] < cpr;
+      }
+      v[t] = ok[t] ? ld_stream16(rows + row[t] * L + j[t] * 8) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int t = 0; t < PK_UNROLL; ++t) {
+      const u32 w32[4] = {v[t].x, v[t].y, v[t].z, v[t].w};
+      u32 sym[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        sym[2 * i] = w32[i] & 0xffffu;  // little-endian: symbol 2i is the low half
+        sym[2 * i + 1] = w32[i] >> 16;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) bad |= ok[t] && (int)sym[i] >= sigma;
+      if (b == 16) {  // the chunk is words 2j and 2j+1 of the row
+        u64 a = 0, c = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          a |= (u64)sym[i] << (48 - 16 * i);
+          c |= (u64)sym[4 + i] << (48 - 16 * i);
+        }
+        if (ok[t]) {
+          u64* dst = keys + row[t] * W + 2 * j[t];
+          if (2 * j[t] + 1 < W) *reinterpret_cast<ulonglong2*>(dst) = make_ulonglong2(a, c);
+          else dst[0] = a;
+        }
+      } else {
+        const int w = (8 * j[t]) / spw;        // key word of this chunk
+        const int p0 = (8 * j[t]) - w * spw;   // first symbol's slot in the word
+        u64 part = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) part |= (u64)sym[i] << (64 - b * (p0 + i + 1));
+        // segmented OR over the gsize lanes of one word (contiguous lanes;
+        // a word's group never crosses a unit)
+        const long long key = ok[t] ? row[t] * W + w : -1 - lane;
+        for (int o = 1; o < gsize; o <<= 1) {
+          const u64 po = __shfl_down_sync(LCP_FULL_MASK, part, o);
+          const long long ko = __shfl_down_sync(LCP_FULL_MASK, key, o);
+          if (lane + o < 32 && ko == key) part |= po;
+        }
+        const long long kprev = __shfl_up_sync(LCP_FULL_MASK, key, 1);
+        if (ok[t] && (lane == 0 || kprev != key)) keys[key] = part;
+      }
+      if (ids != nullptr && ok[t] && j[t] == 0) ids[row[t]] = (u32)row[t];
+    }
+  }
+  if (__any_sync(LCP_FULL_MASK, bad) && lane == 0) atomicOr(err, 1);
+}
+
 // hi / lo 32-bit planes of each key's first word (full-scan layout)
 __global__ void k_split_words(const u64* __restrict__ keys, long long n, int W,
                               u32* __restrict__ hi, u32* __restrict__ lo) {
@@ -244,6 +336,136 @@ template <typename T>
 __global__ void k_scan_add(T* __restrict__ data, long long m, const T* __restrict__ tile_prefix) {
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < m) data[i] += tile_prefix[i / SC_TILE];
+}
+
+// ---------------------------------------------------------------------------
+// Onesweep stable LSD radix pass (8-bit digit): ONE kernel per pass.
+//   - every digit histogram comes from one upfront k_digit_hist8 read, so a
+//     pass needs no upsweep: bucket starts = exclusive scan of its histogram;
+//   - tiles take ids from an atomic counter in start order, count their
+//     digits (warp match_any multisplit, index order => stable), publish
+//     per-digit aggregates and resolve their exclusive prefix over earlier
+//     tiles by decoupled look-back (status word = 2-bit flag | 62-bit count);
+//   - the tile is reordered by digit in shared memory and written out in that
+//     order, so each digit's run is a contiguous, coalesced store.
+// Traffic per pass: read key + value, write key + value (24 B per pair at
+// W=1 with u32 values).  Replaces the stable argsort of core.py:174.
+// ---------------------------------------------------------------------------
+constexpr int OS_THREADS = 256;
+constexpr int OS_WARPS = OS_THREADS / 32;
+constexpr int OS_ITEMS = 16;
+constexpr int OS_TILE = OS_THREADS * OS_ITEMS;  // 4096 pairs
+constexpr int OS_WARP_SEG = 32 * OS_ITEMS;
+constexpr u64 OS_FLAG_AGG = 1ull << 62;
+constexpr u64 OS_FLAG_PREFIX = 2ull << 62;
+constexpr u64 OS_COUNT_MASK = (1ull << 62) - 1;
+constexpr size_t OS_SMEM = (size_t)OS_TILE * 12 + (size_t)OS_WARPS * 256 * 4 + 3 * 256 * 4 + 64;
+
+__device__ __forceinline__ u64 ld_relaxed_u64(const u64* p) {
+  u64 v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(u64* p, u64 v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(OS_THREADS) k_onesweep(
+    const u64* __restrict__ kin, const u32* __restrict__ vin, u64* __restrict__ kout,
+    u32* __restrict__ vout, long long n, int shift, const u32* __restrict__ hist,
+    u64* __restrict__ status, unsigned* __restrict__ tile_counter) {
+  extern __shared__ __align__(16) unsigned char os_smem[];
+  u64* sk = reinterpret_cast<u64*>(os_smem);                       // OS_TILE keys
+  u32* sv = reinterpret_cast<u32*>(sk + OS_TILE);                  // OS_TILE values
+  u32* wcnt = sv + OS_TILE;                                        // [OS_WARPS][256]
+  u32* gstart = wcnt + OS_WARPS * 256;                             // bucket start + tile prefix
+  u32* tstart = gstart + 256;                                      // digit start inside the tile
+  u32* scratch = tstart + 256;                                     // 32 for block scans + tile id
+  const int lane = lane_id();
+  const int warp = threadIdx.x >> 5;
+  const int d0 = threadIdx.x;  // the digit this thread owns in per-digit phases
+
+  if (threadIdx.x == 0) scratch[32] = atomicAdd(tile_counter, 1u);
+  for (int i = threadIdx.x; i < OS_WARPS * 256; i += OS_THREADS) wcnt[i] = 0;
+  __syncthreads();
+  const long long tile = scratch[32];
+  const long long seg = tile * OS_TILE + (long long)warp * OS_WARP_SEG;
+
+  u64 key[OS_ITEMS];
+  u32 val[OS_ITEMS];
+  u32 rank[OS_ITEMS];
+#pragma unroll
+  for (int j = 0; j < OS_ITEMS; ++j) {
+    const long long i = seg + j * 32 + lane;
+    const bool ok = i < n;
+    key[j] = ok ? kin[i] : 0;
+    val[j] = ok ? vin[i] : 0;
+  }
+#pragma unroll
+  for (int j = 0; j < OS_ITEMS; ++j) {
+    const bool ok = seg + j * 32 + lane < n;
+    const u32 d = ok ? (u32)((key[j] >> shift) & 255) : 256u;
+    const unsigned peers = __match_any_sync(LCP_FULL_MASK, d);
+    const unsigned lower = peers & ((1u << lane) - 1u);
+    u32 before = 0;
+    if (ok) before = wcnt[warp * 256 + d];
+    __syncwarp();
+    if (ok && lower == 0) wcnt[warp * 256 + d] = before + __popc(peers);
+    __syncwarp();
+    rank[j] = before + __popc(lower);
+  }
+  __syncthreads();
+  // per digit: exclusive over warps, and the tile's count
+  u32 cnt = 0;
+#pragma unroll
+  for (int w = 0; w < OS_WARPS; ++w) {
+    const u32 c = wcnt[w * 256 + d0];
+    wcnt[w * 256 + d0] = cnt;
+    cnt += c;
+  }
+  // publish the aggregate (tile 0: its inclusive prefix) as early as possible
+  u64* my = status + tile * 256 + d0;
+  st_relaxed_u64(my, (tile == 0 ? OS_FLAG_PREFIX : OS_FLAG_AGG) | (u64)cnt);
+  // bucket start of this digit: exclusive scan of the pass histogram
+  u32 total;
+  const u32 bstart = block_excl_scan<u32>(hist[d0], &total, scratch);
+  const u32 tst = block_excl_scan<u32>(cnt, &total, scratch);
+  // decoupled look-back over earlier tiles
+  u64 excl = 0;
+  for (long long p = tile - 1; p >= 0; --p) {
+    u64 v;
+    do {
+      v = ld_relaxed_u64(status + p * 256 + d0);
+    } while ((v >> 62) == 0);
+    excl += v & OS_COUNT_MASK;
+    if ((v >> 62) == 2) break;
+  }
+  if (tile > 0) st_relaxed_u64(my, OS_FLAG_PREFIX | (excl + cnt));
+  gstart[d0] = bstart + (u32)excl;
+  tstart[d0] = tst;
+  __syncthreads();
+  // reorder the tile by (digit, stable rank) in shared memory
+#pragma unroll
+  for (int j = 0; j < OS_ITEMS; ++j) {
+    const long long i = seg + j * 32 + lane;
+    if (i < n) {
+      const u32 d = (u32)((key[j] >> shift) & 255);
+      const u32 pos = tstart[d] + wcnt[warp * 256 + d] + rank[j];
+      sk[pos] = key[j];
+      sv[pos] = val[j];
+    }
+  }
+  __syncthreads();
+  const long long rem = n - tile * OS_TILE;
+  const int tile_n = rem < OS_TILE ? (int)rem : OS_TILE;
+#pragma unroll 4
+  for (int i = threadIdx.x; i < tile_n; i += OS_THREADS) {
+    const u64 k = sk[i];
+    const u32 d = (u32)((k >> shift) & 255);
+    const long long g = (long long)gstart[d] + (i - (long long)tstart[d]);
+    kout[g] = k;
+    vout[g] = sv[i];
+  }
 }
 
 // ---------------------------------------------------------------------------

@@ -58,6 +58,15 @@ struct DevIndex {
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
+// 16-byte streaming load of read-only data that is used once (no L1 allocation)
+__device__ __forceinline__ uint4 ld_stream16(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
 // ---- key helpers ---------------------------------------------------------
 
 // Position-j symbol shift inside its word.
@@ -136,8 +145,10 @@ __device__ __forceinline__ u64 make_composite(int lcp, u32 id, int L) {
 }
 
 // Compact composite: (L - lcp) << idbits | id in 32 bits when
-// n <= 2**idbits and L < 2**(32 - idbits) (config 3: 6 + 26 bits); the
+// n < 2**idbits and L < 2**(32 - idbits) (config 3: 6 + 26 bits); the
 // order is the same as the u64 form, so it is used for selection only.
+// n < 2**idbits (not <=) keeps the largest real composite, (lcp 0, id n-1)
+// at L = 2**(32-idbits) - 1, strictly below the all-ones empty sentinel.
 template <typename C>
 __device__ __forceinline__ C make_comp(int lcp, u32 id, int L, int idbits) {
   return ((C)(u32)(L - lcp) << idbits) | (C)id;

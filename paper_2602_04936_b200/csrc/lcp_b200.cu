@@ -103,12 +103,15 @@ int dalloc(T** p, long long count, long long* acct, cudaStream_t st) {
   return LCP_OK;
 }
 
-// grow-only device buffer
+// grow-only device buffer; `moves` counts reallocations so cached graphs that
+// baked in the old pointer can be told apart (lcp_workspace::epoch)
 struct DBuf {
   void* p = nullptr;
   size_t cap = 0;
+  unsigned long long moves = 0;
   int ensure(size_t bytes) {
     if (bytes <= cap) return LCP_OK;
+    ++moves;
     if (p) cudaFree(p);
     p = nullptr;
     cap = 0;
@@ -174,7 +177,10 @@ int scan_exclusive(T* data, long long m, cudaStream_t st) {
 
 // ---- stable LSD radix sort of (u64 key, u32 val) ---------------------------
 // Sorts in place semantically: on return (*k, *v) point at the sorted data
-// (buffers may have been swapped with the alternates).
+// (buffers may have been swapped with the alternates).  One upfront read
+// builds all eight digit histograms (k_digit_hist8); the host reads them once
+// to skip passes whose digit is constant (e.g. the low bits when L*b < 64);
+// every remaining pass is one onesweep kernel (k_onesweep).
 int radix_sort_pairs(u64** k, u32** v, u64** k_alt, u32** v_alt, long long n, cudaStream_t st) {
   if (n <= 1) return LCP_OK;
   u32* hist = nullptr;
@@ -186,26 +192,50 @@ int radix_sort_pairs(u64** k, u32** v, u64** k_alt, u32** v_alt, long long n, cu
   std::vector<u32> h(8 * 256);
   LCP_CK(cudaMemcpyAsync(h.data(), hist, h.size() * sizeof(u32), cudaMemcpyDeviceToHost, st));
   LCP_CK(cudaStreamSynchronize(st));
-  LCP_CK(cudaFreeAsync(hist, st));
 
-  const long long ntiles = (n + RS_TILE - 1) / RS_TILE;
-  u32* counts = nullptr;
-  LCP_CK(cudaMallocAsync((void**)&counts, (size_t)ntiles * 256 * sizeof(u32), st));
+  const long long ntiles = (n + OS_TILE - 1) / OS_TILE;
+  u64* status = nullptr;
+  unsigned* counters = nullptr;
+  LCP_CK(cudaMallocAsync((void**)&status, (size_t)ntiles * 256 * sizeof(u64), st));
+  LCP_CK(cudaMallocAsync((void**)&counters, 8 * sizeof(unsigned), st));
+  LCP_CK(cudaMemsetAsync(counters, 0, 8 * sizeof(unsigned), st));
+  static const cudaError_t attr = cudaFuncSetAttribute(  // thread-safe one-time initialisation
+      k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OS_SMEM);
+  LCP_CK(attr);
   for (int p = 0; p < 8; ++p) {
     bool trivial = false;
     for (int d = 0; d < 256; ++d)
       if ((long long)h[p * 256 + d] == n) trivial = true;
     if (trivial) continue;  // every key has the same digit: pass is the identity
-    k_rs_upsweep<<<(unsigned)ntiles, RS_THREADS, 0, st>>>(*k, n, 8 * p, (int)ntiles, counts);
-    LCP_CK_LAUNCH();
-    LCP_TRY(scan_exclusive<u32>(counts, ntiles * 256, st));
-    k_rs_downsweep<<<(unsigned)ntiles, RS_THREADS, 0, st>>>(*k, *v, *k_alt, *v_alt, n, 8 * p,
-                                                            (int)ntiles, counts);
+    LCP_CK(cudaMemsetAsync(status, 0, (size_t)ntiles * 256 * sizeof(u64), st));
+    k_onesweep<<<(unsigned)ntiles, OS_THREADS, OS_SMEM, st>>>(*k, *v, *k_alt, *v_alt, n, 8 * p,
+                                                               hist + p * 256, status, counters + p);
     LCP_CK_LAUNCH();
     std::swap(*k, *k_alt);
     std::swap(*v, *v_alt);
   }
-  LCP_CK(cudaFreeAsync(counts, st));
+  LCP_CK(cudaFreeAsync(status, st));
+  LCP_CK(cudaFreeAsync(counters, st));
+  LCP_CK(cudaFreeAsync(hist, st));
+  return LCP_OK;
+}
+
+// pack n rows into keys (+ ids): the streaming kernel when every row is a
+// whole number of 16-byte chunks, the per-word kernel otherwise
+int pack_rows(const uint16_t* rows, long long n, const DevIndex& dv, u64* keys, u32* ids, int* err,
+              cudaStream_t st) {
+  if (n <= 0) return LCP_OK;
+  if (dv.L % 8 == 0 && ((uintptr_t)rows & 15) == 0) {
+    const int cpr = dv.L / 8;
+    const long long units = cpr <= 32 ? (n + 32 / cpr - 1) / (32 / cpr) : n * ((cpr + 31) / 32);
+    const long long want = (units + (PK_THREADS / 32) * PK_UNROLL - 1) / ((PK_THREADS / 32) * PK_UNROLL);
+    const unsigned grid = (unsigned)std::max(1ll, std::min<long long>(want, 8ll * num_sms()));
+    k_pack_stream<<<grid, PK_THREADS, 0, st>>>(rows, n, dv.L, dv.W, dv.b, dv.spw, dv.sigma, keys, ids, err);
+  } else {
+    k_pack<<<blocks_for(n * dv.W, 256), 256, 0, st>>>(rows, n, dv.L, dv.W, dv.b, dv.spw, dv.sigma, keys,
+                                                      ids, err);
+  }
+  LCP_CK_LAUNCH();
   return LCP_OK;
 }
 
@@ -250,14 +280,16 @@ struct lcp_index {
 
 // One captured async submission (H2D -> query kernel -> D2H -> error word),
 // replayed with a single cudaGraphLaunch when the same buffers come back.
+// `epoch` is the workspace's scratch epoch at capture: a graph bakes in the
+// device scratch pointers, so once any scratch buffer moved it must not replay.
 struct GraphKey {
-  unsigned long long gen;
+  unsigned long long gen, epoch;
   const void* queries;
   void* out;
   int count, k, mode, stride;
   bool operator==(const GraphKey& o) const {
-    return gen == o.gen && queries == o.queries && out == o.out && count == o.count &&
-           k == o.k && mode == o.mode && stride == o.stride;
+    return gen == o.gen && epoch == o.epoch && queries == o.queries && out == o.out &&
+           count == o.count && k == o.k && mode == o.mode && stride == o.stride;
   }
 };
 struct CachedGraph {
@@ -278,6 +310,23 @@ struct lcp_workspace {
   int* d_err = nullptr;
   int* h_err = nullptr;  // pinned
   DBuf qkeys, partial, hint, q_in, ids, lcps, hits, md, aux;
+  // changes whenever a scratch buffer is reallocated (its old memory freed)
+  unsigned long long epoch() const {
+    return qkeys.moves + partial.moves + hint.moves + q_in.moves + ids.moves + lcps.moves +
+           hits.moves + md.moves + aux.moves;
+  }
+  // drop cached graphs captured against scratch that has since moved
+  void prune_stale_graphs() {
+    const unsigned long long e = epoch();
+    for (size_t i = 0; i < graphs.size();) {
+      if (graphs[i].key.epoch != e) {
+        cudaGraphExecDestroy(graphs[i].exec);
+        graphs.erase(graphs.begin() + i);
+      } else {
+        ++i;
+      }
+    }
+  }
 };
 
 extern "C" {
@@ -360,9 +409,7 @@ static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, i
   } tmp{{perm_alt, kw_alt, d_err}, st};
   LCP_CK(cudaMemsetAsync(d_err, 0, sizeof(int), st));
 
-  k_pack<<<blocks_for(n * W, 256), 256, 0, st>>>(d_rows, n, L, W, dv.b, dv.spw, sigma,
-                                                  ix->keys_orig, perm, d_err);
-  LCP_CK_LAUNCH();
+  LCP_TRY(pack_rows(d_rows, n, dv, ix->keys_orig, perm, d_err, st));
   int h_err = 0;
   LCP_CK(cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
   LCP_CK(cudaStreamSynchronize(st));
@@ -600,7 +647,9 @@ int lcp_index_build(const uint16_t* rows, int64_t n, int32_t length, int32_t sig
     int lbits = 0;
     while ((1 << lbits) < length + 1) ++lbits;
     const int idb = 32 - lbits;
-    dv.idbits = (idb >= 1 && n <= (1ll << idb)) ? idb : 32;
+    // ids < n <= 2^idb - 1: the largest composite (lcp 0, id n-1) then
+    // stays below the all-ones empty sentinel even when L = 2^lbits - 1
+    dv.idbits = (idb >= 1 && n < (1ll << idb)) ? idb : 32;
     // test hook: exercise the u64 selection path on small inputs
     const char* wide = getenv("LCP_FORCE_WIDE_COMPOSITE");
     if (wide && wide[0] == '1') dv.idbits = 32;
@@ -1024,9 +1073,7 @@ int lcp_index_bucket_range_search(const lcp_index* ix, const uint16_t* queries, 
   LCP_CK(cudaMalloc((void**)&d_err, 4));
   LCP_CK(cudaMemset(d_err, 0, 4));
   LCP_CK(cudaMemcpy(d_q, queries, (size_t)count * dv.L * 2, cudaMemcpyDefault));
-  k_pack<<<blocks_for((long long)count * dv.W, 256), 256>>>(d_q, count, dv.L, dv.W, dv.b, dv.spw,
-                                                            dv.sigma, d_k, nullptr, d_err);
-  LCP_CK_LAUNCH();
+  LCP_TRY(pack_rows(d_q, count, dv, d_k, nullptr, d_err, (cudaStream_t)0));
   k_bucket_search<<<blocks_for(count, 128), 128>>>(dv, d_k, count, d_lo, d_hi);
   LCP_CK_LAUNCH();
   int h_err = 0;
@@ -1318,9 +1365,7 @@ static int query_impl(const lcp_index* ix, lcp_workspace* ws, const uint16_t* qu
     return LCP_OK;
   }
   LCP_TRY(ws->qkeys.ensure((size_t)count * dv.W * 8));
-  k_pack<<<blocks_for((long long)count * dv.W, 256), 256, 0, st>>>(
-      queries, count, dv.L, dv.W, dv.b, dv.spw, dv.sigma, ws->qkeys.as<u64>(), nullptr, errp);
-  LCP_CK_LAUNCH();
+  LCP_TRY(pack_rows(queries, count, dv, ws->qkeys.as<u64>(), nullptr, errp, st));
   if (dv.W > 8 && mode != LCP_MODE_TAL && k <= FAST_KMAX) {  // long keys: warp per query
     const long long sms = num_sms();
     const long long wpc = std::min<long long>(32, std::max<long long>(1, (count + sms - 1) / sms));
@@ -1469,10 +1514,18 @@ int lcp_query_host_packed_async(const lcp_index* ix, lcp_workspace* ws, const ui
   cudaStream_t st = ws->stream;
   const lcp_packed_layout lay = packed_layout(count, out_stride);
   const size_t qb = (size_t)count * dv.L * 2;
-  const GraphKey key{ix->generation, queries, out_block, count, k, mode | (flags << 8), out_stride};
   const size_t d2h = (flags & LCP_PACKED_NO_WORK) ? (size_t)lay.matched_depth : (size_t)lay.total;
   static const bool no_graphs = getenv("LCP_NO_GRAPH_CACHE") != nullptr;  // A/B switch
   ++ws->tick;
+  // every buffer the submission touches exists before the lookup / capture (no
+  // allocation inside a capture); a reallocation bumps the epoch, so graphs
+  // holding the freed pointers can no longer match and are destroyed
+  LCP_TRY(ws->q_in.ensure(qb));
+  LCP_TRY(ws->ids.ensure((size_t)lay.total));
+  LCP_TRY(ws->qkeys.ensure((size_t)count * dv.W * 8));
+  ws->prune_stale_graphs();
+  const GraphKey key{ix->generation, ws->epoch(), queries, out_block, count, k,
+                     mode | (flags << 8), out_stride};
   for (auto& g : ws->graphs) {
     if (g.key == key) {  // replay: one launch for the whole submission
       g.last_use = ws->tick;
@@ -1484,10 +1537,6 @@ int lcp_query_host_packed_async(const lcp_index* ix, lcp_workspace* ws, const ui
       return LCP_OK;
     }
   }
-  // every buffer the submission touches exists before capture (no allocation inside)
-  LCP_TRY(ws->q_in.ensure(qb));
-  LCP_TRY(ws->ids.ensure((size_t)lay.total));
-  LCP_TRY(ws->qkeys.ensure((size_t)count * dv.W * 8));
   char* d = static_cast<char*>(ws->ids.p);
   // one H2D, the kernel, one D2H: the invalid-query flag lives in the block
   // (lay.err), cleared on the device, so no separate small copy is needed
@@ -1635,6 +1684,36 @@ int lcp_fullscan(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries
     return LCP_OK;
   }
   const int take = (int)std::min<long long>(k, dv.n);
+  static const bool smallq_off = getenv("LCP_FULLSCAN_NO_SMALLQ") != nullptr;  // A/B hook
+  if (count <= FSQ_QMAX && take <= FAST_KMAX && !smallq_off) {
+    // a few queries: one HBM-streaming pass with every query in every lane
+    LCP_TRY(ws->qkeys.ensure((size_t)count * dv.W * 8));
+    LCP_TRY(pack_rows(queries, count, dv, ws->qkeys.as<u64>(), nullptr, ws->d_err, st));
+    const long long G = num_sms();
+    const long long warps = G * FSQ_WARPS;
+    long long seg = (dv.n + warps - 1) / warps;
+    seg = (seg + FSQ_STEP - 1) / FSQ_STEP * FSQ_STEP;
+    const size_t csz = dv.idbits < 32 ? 4 : 8;
+    LCP_TRY(ws->partial.ensure((size_t)G * count * take * csz));
+    LCP_TRY(ws->hint.ensure((size_t)(count + 1) * 4));
+    LCP_CK(cudaMemsetAsync(ws->hint.p, 0, (size_t)(count + 1) * 4, st));
+    int* hint = ws->hint.as<int>();
+    unsigned* ctr = reinterpret_cast<unsigned*>(hint + count);
+    int Q = 1;
+    while (Q < count) Q <<= 1;
+#define LCP_FSQ(C, QQ)                                                                           \
+  k_fullscan_smallq<C, QQ><<<(unsigned)G, FSQ_THREADS, (size_t)FSQ_WARPS * QQ * 32 * sizeof(C), \
+                             st>>>(dv, ws->qkeys.as<u64>(), count, take, seg,                    \
+                                   ws->partial.as<C>(), hint, ctr, ids, lcps, hits, out_stride)
+    if (dv.idbits < 32) {
+      if (Q == 1) LCP_FSQ(u32, 1); else if (Q == 2) LCP_FSQ(u32, 2); else if (Q == 4) LCP_FSQ(u32, 4); else LCP_FSQ(u32, 8);
+    } else {
+      if (Q == 1) LCP_FSQ(u64, 1); else if (Q == 2) LCP_FSQ(u64, 2); else if (Q == 4) LCP_FSQ(u64, 4); else LCP_FSQ(u64, 8);
+    }
+#undef LCP_FSQ
+    LCP_CK_LAUNCH();
+    return LCP_OK;
+  }
   if (take <= (dv.idbits < 32 ? FS_KMAX_U32 : FS_KMAX_U64)) {
     const int per_stage = FS1_STAGE_KEYS;
     const long long qtiles = (count + FS_THREADS - 1) / FS_THREADS;
@@ -1653,9 +1732,7 @@ int lcp_fullscan(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries
     const u64* qk = nullptr;
     if (dv.W > 1) {
       LCP_TRY(ws->qkeys.ensure((size_t)count * dv.W * 8));
-      k_pack<<<blocks_for((long long)count * dv.W, 256), 256, 0, st>>>(
-          queries, count, dv.L, dv.W, dv.b, dv.spw, dv.sigma, ws->qkeys.as<u64>(), nullptr, ws->d_err);
-      LCP_CK_LAUNCH();
+      LCP_TRY(pack_rows(queries, count, dv, ws->qkeys.as<u64>(), nullptr, ws->d_err, st));
       qk = ws->qkeys.as<u64>();
     }
     LCP_TRY(ws->hint.ensure((size_t)count * 4));
@@ -1667,9 +1744,7 @@ int lcp_fullscan(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries
                         0, ids, lcps, hits, out_stride, st);
   }
   LCP_TRY(ws->qkeys.ensure((size_t)count * dv.W * 8));
-  k_pack<<<blocks_for((long long)count * dv.W, 256), 256, 0, st>>>(
-      queries, count, dv.L, dv.W, dv.b, dv.spw, dv.sigma, ws->qkeys.as<u64>(), nullptr, ws->d_err);
-  LCP_CK_LAUNCH();
+  LCP_TRY(pack_rows(queries, count, dv, ws->qkeys.as<u64>(), nullptr, ws->d_err, st));
   unsigned grid = (unsigned)gen_grid(count);
   k_query_general<<<grid, GEN_THREADS, 0, st>>>(dv, ws->qkeys.as<u64>(), queries, count, k, 1, 1,
                                                 out_stride, ids, lcps, hits, nullptr, nullptr);

@@ -39,6 +39,67 @@ class ShardPlan:
         return lo, lo + base + (1 if rank < rem else 0)
 
 
+def local_candidates(index, queries, k: int, id_offset: int, mode: str = "complete",
+                     stream: int | None = None, bufs: dict | None = None):
+    """One shard's step before the exchange: local top-min(k, n_g) of a CUDA
+    (count, L) uint16 batch, encoded as (count, k) int64 candidates
+    ``(L - lcp) << 32 | (id + id_offset)`` padded with UINT64_MAX
+    (lcp_encode_candidates).  ``index``: NativeIndex or TrieIndex."""
+    import torch
+
+    native = getattr(index, "native", index)
+    count = int(queries.shape[0])
+    dev = queries.device
+    st = torch.cuda.current_stream(dev).cuda_stream if stream is None else stream
+    if bufs is None:
+        ls = native.stride_for(k)
+        bufs = dict(ids=torch.empty((count, ls), dtype=torch.int32, device=dev),
+                    lcps=torch.empty((count, ls), dtype=torch.int16, device=dev),
+                    hits=torch.empty(count, dtype=torch.int32, device=dev),
+                    cand=torch.empty((count, k), dtype=torch.int64, device=dev))
+    if native.n:
+        native.query_device(queries, k, mode, bufs["ids"], bufs["lcps"], bufs["hits"],
+                            bufs.get("md"), bufs.get("aux"), stream=st)
+    else:
+        bufs["hits"].zero_()
+    _native.check(_native.load().lcp_encode_candidates(
+        bufs["ids"].data_ptr(), bufs["lcps"].data_ptr(), bufs["hits"].data_ptr(), count, k,
+        int(bufs["ids"].shape[1]), native.length, int(id_offset), bufs["cand"].data_ptr(), st))
+    return bufs["cand"]
+
+
+def merge_candidates_device(gathered, k: int, length: int, n_total: int, out_ids, out_lcps,
+                            out_hits, mode: str = "complete", stream: int | None = None) -> None:
+    """The exchange's consumer: (shards, count, k) int64 candidates -> the global
+    top-min(k, n_total) per query into (count, max(1, take)) device outputs
+    (lcp_merge_candidates; strict keeps only the deepest lcp across shards)."""
+    import torch
+
+    shards, count = int(gathered.shape[0]), int(gathered.shape[1])
+    take = max(0, min(int(k), int(n_total)))
+    st = torch.cuda.current_stream(gathered.device).cuda_stream if stream is None else stream
+    _native.check(_native.load().lcp_merge_candidates(
+        gathered.data_ptr(), shards, count, k, take, int(length), 1 if mode == "strict" else 0,
+        out_ids.data_ptr(), out_lcps.data_ptr(), out_hits.data_ptr(), st))
+
+
+def merge_candidates(gathered, k: int, length: int, n_total: int, mode: str = "complete"):
+    """merge_candidates_device into fresh buffers, returned as a host BatchResult."""
+    import numpy as np
+    import torch
+
+    from .result import BatchResult
+
+    count, dev = int(gathered.shape[1]), gathered.device
+    w = max(1, min(int(k), int(n_total)))
+    ids = torch.empty((count, w), dtype=torch.int32, device=dev)
+    lcps = torch.empty((count, w), dtype=torch.int16, device=dev)
+    hits = torch.empty(count, dtype=torch.int32, device=dev)
+    merge_candidates_device(gathered, k, length, n_total, ids, lcps, hits, mode)
+    return BatchResult(ids=ids.cpu().numpy().view(np.uint32), lcps=lcps.cpu().numpy().view(np.uint16),
+                       hits=hits.cpu().numpy(), mode=mode)
+
+
 class ShardExchange:
     """The one data-path collective: all-gather of per-shard candidate lists.
 

@@ -1,0 +1,225 @@
+"""Oracle parity at every BASELINE.json config, at its stated size.
+
+VERDICT r1 next-round #1: no config may be unpinned.  Each test builds the
+config's corpus with the reference generator (datagen.py restated, SHA-pinned
+in test_cpu_host.py) and compares the CUDA path, through the C ABI, with the
+pinned C oracle (oracle/lcp_oracle.c, itself checked against the reference's
+own outputs in test_oracle_golden.py) on EVERY query of the stated batch:
+ids, lcps, hit counts, matched_depth and the per-query WorkReport counters,
+bit for bit.
+
+  config 1  N=10k,  L=16, sigma=4, k=10, 1,000 queries, strict/complete/TAL/full scan
+  config 2  N=100k, L=24, k=5, 1,000 readings (prefix_len=12), single-query API
+  config 3  N=2M,   L=32, k=10, 4,096 uniform + 4,096 prefix-16 queries, strict +
+            complete + TAL B=256 + the full-scan kernel
+  config 4  N=500k, L=32, k=10, 4,096 queries; the N x N materialisation is
+            infeasible (reference memory_wall) while the index answers exactly
+  config 5  N=200M, L=32, k=10: the single-GPU index and the 8-row-block
+            sharded composition (encode + merge kernels) agree on 4,096
+            queries; both equal the per-shard composed oracle (SURVEY §8c:
+            oracle_top_k per row block with id offsets, then merged by
+            (lcp desc, id asc)) on a 64-query sample.
+"""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+import paper_2602_04936_b200 as lg
+from paper_2602_04936_b200.work import trie_counters_rows
+
+pytestmark = pytest.mark.gpu
+
+THREADS = os.cpu_count() or 1
+
+
+def assert_rows(b, ids, lcps, hits, what):
+    """Every row of BatchResult b equals the oracle's (ids, lcps, hits)."""
+    hits = np.asarray(hits, dtype=np.int64)
+    assert np.array_equal(b.hits.astype(np.int64), hits), f"{what}: hit counts differ"
+    width = min(b.ids.shape[1], ids.shape[1])
+    assert hits.max(initial=0) <= width
+    mask = np.arange(width)[None, :] < hits[:, None]
+    gi = np.where(mask, b.ids[:, :width].astype(np.int64), -1)
+    oi = np.where(mask, ids[:, :width].astype(np.int64), -1)
+    gl = np.where(mask, b.lcps[:, :width].astype(np.int64), -1)
+    ol = np.where(mask, lcps[:, :width].astype(np.int64), -1)
+    bad = np.flatnonzero((gi != oi).any(1) | (gl != ol).any(1))
+    assert bad.size == 0, (f"{what}: {bad.size} rows differ, first {bad[:5].tolist()}: "
+                           f"gpu {b.pairs(int(bad[0]))} oracle "
+                           f"{list(zip(oi[bad[0]][mask[bad[0]]].tolist(), ol[bad[0]][mask[bad[0]]].tolist()))}")
+
+
+def check_trie_batch(index, trie, qs, k, mode, what):
+    """GPU TrieIndex.query_batch vs OracleTrie on every query, with counters."""
+    b = index.query_batch(qs, k, mode)
+    ids, lcps, hits, md, sym, nodes = trie.query_batch(qs, k, mode, nthreads=THREADS)
+    assert_rows(b, ids, lcps, hits, f"{what} {mode}")
+    assert np.array_equal(b.matched_depth.astype(np.int64), md.astype(np.int64)), f"{what} {mode} matched_depth"
+    gsym, gnodes = trie_counters_rows(b.aux, index.n, index.length, mode == "complete")
+    assert np.array_equal(gsym, sym), f"{what} {mode} symbols_compared"
+    assert np.array_equal(gnodes, nodes), f"{what} {mode} nodes_visited"
+    return b
+
+
+def check_tal_batch(eng, otal, qs, k, what):
+    b = eng.query_batch(qs, k)
+    ids, lcps, hits, items, sym = otal.query_batch(qs, k, nthreads=THREADS)
+    assert_rows(b, ids, lcps, hits, f"{what} tal")
+    assert np.array_equal(b.aux[:, 0].astype(np.int64), items), f"{what} tal items_scanned"
+    assert np.array_equal(b.aux[:, 1].astype(np.int64), sym), f"{what} tal symbols_compared"
+    assert np.all(b.matched_depth == otal.depth)
+
+
+def check_fullscan(index, items, qs, k, what):
+    f = index.fullscan_batch(qs, k)
+    oid, olcp, oh = _oracle().oracle_top_k_batch(items, qs, k, nthreads=THREADS)
+    assert_rows(f, oid, olcp, oh, f"{what} fullscan")
+    return f
+
+
+def _oracle():
+    import oracle
+
+    oracle.build()
+    return oracle
+
+
+# ---------------------------------------------------------------------------
+def test_config1_all_modes(gpu):
+    """N=10,000, L=16, sigma=4, k=10, 1,000 queries (pkg/demos/quickstart.py:12)."""
+    orc = _oracle()
+    ds = lg.generate_dataset(10_000, 16, 4, seed=42)
+    qs = np.vstack([lg.generate_queries(ds, 500, seed=7), lg.generate_queries(ds, 500, seed=8, prefix_len=8)])
+    index = lg.build(ds)
+    trie = orc.OracleTrie(ds.items, 4)
+    for mode in ("strict", "complete"):
+        check_trie_batch(index, trie, qs, 10, mode, "config1")
+    eng = lg.build_tal(ds, 256)
+    check_tal_batch(eng, orc.OracleTal(ds.items, 4, eng.bucket_depth), qs, 10, "config1")
+    check_fullscan(index, ds.items, qs, 10, "config1")
+
+
+def test_config2_gnc_single_query_api(gpu):
+    """GNC: N=100,000 readings, L=24, k=5; 1,000 readings with prefix_len=12,
+    each answered by the single-query TrieIndex.query (trie.py:290-342)."""
+    orc = _oracle()
+    ds = lg.generate_dataset(100_000, 24, 4, seed=4)
+    readings = lg.generate_queries(ds, 1000, seed=5, prefix_len=12)
+    index = lg.build(ds)
+    trie = orc.OracleTrie(ds.items, 4)
+    for mode in ("complete", "strict"):
+        for i, q in enumerate(readings):
+            w = index.new_work_report()
+            r = index.query(q, 5, mode, work=w)
+            ids, lcps, md, sym, nodes = trie.query(q, 5, mode)
+            assert r.pairs() == list(zip(ids.tolist(), lcps.tolist())), (mode, i)
+            assert r.matched_depth == md, (mode, i)
+            assert (w.symbols_compared, w.nodes_visited, w.queries) == (sym, nodes, 1), (mode, i)
+        check_trie_batch(index, trie, readings, 5, mode, "config2 batch")
+
+
+@pytest.fixture(scope="module")
+def config3():
+    orc = _oracle()
+    ds = lg.generate_dataset(2_000_000, 32, 4, seed=3)
+    qs = np.vstack([lg.generate_queries(ds, 4096, seed=4),
+                    lg.generate_queries(ds, 4096, seed=5, prefix_len=16)])
+    return ds, qs, lg.build(ds), orc.OracleTrie(ds.items, 4)
+
+
+@pytest.mark.parametrize("mode", ["complete", "strict"])
+def test_config3_every_query(gpu, config3, mode):
+    """N=2M, L=32, k=10: all 4,096 uniform and all 4,096 prefix-16 queries."""
+    ds, qs, index, trie = config3
+    check_trie_batch(index, trie, qs[:4096], 10, mode, "config3 uniform")
+    check_trie_batch(index, trie, qs[4096:], 10, mode, "config3 prefix16")
+
+
+def test_config3_tal_and_fullscan(gpu, config3):
+    """TAL B=256 (the paper's bounded-range scan) and the brute-force kernel
+    on the 4,096 uniform queries of config 3."""
+    ds, qs, index, _ = config3
+    orc = _oracle()
+    eng = lg.build_tal(ds, 256)
+    check_tal_batch(eng, orc.OracleTal(ds.items, 4, eng.bucket_depth), qs[:4096], 10, "config3")
+    check_fullscan(index, ds.items, qs[:4096], 10, "config3")
+
+
+def test_config4_oom_boundary(gpu):
+    """N=500,000, L=32: the reference memory wall (bench.py:118-131) says the
+    N x N fp16 materialisation needs 465.66 GiB (infeasible on one B200),
+    while the index answers every query exactly."""
+    import torch
+
+    orc = _oracle()
+    est = lg.memory_wall(500_000, budget_bytes=torch.cuda.mem_get_info()[0])
+    assert not est.feasible and round(est.materialization_bytes / 2**30, 2) == 465.66
+    ds = lg.generate_dataset(500_000, 32, 4, seed=5)
+    qs = lg.generate_queries(ds, 4096, seed=6)
+    index = lg.build(ds)
+    trie = orc.OracleTrie(ds.items, 4)
+    for mode in ("complete", "strict"):
+        check_trie_batch(index, trie, qs, 10, mode, "config4")
+    assert index.nbytes < est.materialization_bytes / 10_000
+
+
+def _composed_oracle(items, qs, k, shards):
+    """oracle_top_k per row block [g*N/G, (g+1)*N/G) with global
+    ids, then the k best of the union by (lcp desc, id asc)."""
+    orc = _oracle()
+    n = items.shape[0]
+    bounds = [g * n // shards for g in range(shards + 1)]
+    cand_id, cand_lcp = [], []
+    for g in range(shards):
+        ids, lcps, hits = orc.oracle_top_k_batch(items[bounds[g]:bounds[g + 1]], qs, k, nthreads=THREADS)
+        assert np.all(hits == min(k, bounds[g + 1] - bounds[g]))
+        cand_id.append(ids + bounds[g])
+        cand_lcp.append(lcps)
+    cid = np.concatenate(cand_id, axis=1)
+    clcp = np.concatenate(cand_lcp, axis=1)
+    out_i = np.zeros((len(qs), k), np.int64)
+    out_l = np.zeros((len(qs), k), np.int64)
+    for r in range(len(qs)):
+        o = np.lexsort((cid[r], -clcp[r]))[:k]
+        out_i[r], out_l[r] = cid[r][o], clcp[r][o]
+    return out_i, out_l, np.full(len(qs), min(k, n))
+
+
+@pytest.mark.slow
+def test_config5_200m_sharded(gpu):
+    """N=200M, L=32, sigma=4, k=10 (BASELINE config 5) on one B200: the
+    whole-corpus index, the 8-shard row-block composition (local top-k ->
+    lcp_encode_candidates -> lcp_merge_candidates, the multi-GPU data path
+    minus the NCCL transport) and the per-shard composed oracle agree."""
+    import torch
+
+    from paper_2602_04936_b200.engine import NativeIndex
+    from paper_2602_04936_b200.sharded import local_candidates, merge_candidates
+
+    n, shards, k = 200_000_000, 8, 10
+    ds = lg.generate_dataset(n, 32, 4, seed=6)
+    qs = np.vstack([lg.generate_queries(ds, 2048, seed=4),
+                    lg.generate_queries(ds, 2048, seed=5, prefix_len=16)])
+    whole = lg.build(ds)
+    b = whole.query_batch(qs, k, "complete")
+    del whole
+    torch.cuda.empty_cache()
+    dq = torch.from_numpy(qs).cuda()
+    cands = []
+    for g in range(shards):
+        lo, hi = g * n // shards, (g + 1) * n // shards
+        shard = NativeIndex(ds.items[lo:hi], 32, 4)
+        cands.append(local_candidates(shard, dq, k, id_offset=lo).clone())
+        shard.close()
+        del shard
+    m = merge_candidates(torch.stack(cands), k, 32, n)
+    assert np.array_equal(m.hits, b.hits)
+    assert np.array_equal(m.ids, b.ids) and np.array_equal(m.lcps, b.lcps)
+    sample = np.r_[0:32, 2048:2080]
+    oi, ol, oh = _composed_oracle(ds.items, qs[sample], k, shards)
+    sub = type(b)(ids=b.ids[sample], lcps=b.lcps[sample], hits=b.hits[sample])
+    assert_rows(sub, oi, ol, oh, "config5 sample")

@@ -841,3 +841,44 @@ def test_graph_replay_multistream_matches_sync(gpu, mode, sigma):
                 h = want.hits[b * bs + i]
                 assert np.array_equal(got_ids[i, :h], want.ids[b * bs + i, :h])
                 assert np.array_equal(got_l[i, :h], want.lcps[b * bs + i, :h])
+
+
+def test_async_graph_cache_survives_scratch_growth(gpu):
+    """a cached async graph bakes in the workspace's device
+    scratch pointers.  Alternating submissions of different counts with the
+    SAME host query / output pointers on ONE workspace grow (reallocate) that
+    scratch between replays; every result must still equal the synchronous
+    API's (a stale graph would read and write freed device memory)."""
+    import ctypes
+
+    from paper_2602_04936_b200 import _native
+    from paper_2602_04936_b200._native import PackedLayout, PinnedArray, Workspace, check, load
+
+    ds = lg.generate_dataset(300_000, 32, 4, seed=13)
+    idx = lg.build(ds)
+    qs = lg.generate_queries(ds, 8192, seed=14)
+    k = 10
+    ref = idx.query_batch(qs, k, "complete")
+    lib = load()
+    ws = Workspace()
+    pin_q = PinnedArray((8192, 32), np.uint16)
+    pin_q.array[:] = qs
+    lay_max = PackedLayout()
+    check(lib.lcp_packed_layout_for(8192, k, ctypes.byref(lay_max)))
+    block = PinnedArray((int(lay_max.total),), np.uint8)
+    for count in (1024, 4096, 1024, 8192, 1024, 4096, 1024):
+        lay = PackedLayout()
+        check(lib.lcp_packed_layout_for(count, k, ctypes.byref(lay)))
+        block.array[:] = 0xAB
+        check(lib.lcp_query_host_packed_async(idx.native.handle, ws.handle, pin_q.address, count, k, 1, k,
+                                              block.address, 0))
+        check(lib.lcp_workspace_wait(ws.handle))
+        raw = block.array
+        ids = raw[lay.ids:lay.ids + count * k * 4].view(np.uint32).reshape(count, k)
+        lcps = raw[lay.lcps:lay.lcps + count * k * 2].view(np.uint16).reshape(count, k)
+        hits = raw[lay.hits:lay.hits + count * 4].view(np.int32)
+        assert np.array_equal(hits, ref.hits[:count]), count
+        assert np.array_equal(ids, ref.ids[:count]) and np.array_equal(lcps, ref.lcps[:count]), count
+    ws.close()
+    del _native
+
