@@ -174,6 +174,47 @@ def cpu_reference(ds, queries: np.ndarray, k: int, budget_s: float, nthreads: in
     return done / el, done, el, trie
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def python_reference(n_queries: int = 2048) -> dict:
+    """The reference's OWN Python path on the host cores (BASELINE.md §2,
+    SURVEY §8d): the unmodified lcpsearch installed in baseline/_ref
+    (tools/install_reference.sh), trie.build + the bench's own query loop
+    _query_stream(index, queries, 10, "complete", workers=w) for w in
+    {1, 2, 4, cpu_count} (pkg/src/lcpsearch/bench.py:245-270)."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "lcpsearch")):
+        return {"unavailable": "reference not installed in baseline/_ref (tools/install_reference.sh)"}
+    sys.path.insert(0, ref)
+    try:
+        import lcpsearch
+        from lcpsearch.bench import _query_stream
+    finally:
+        sys.path.remove(ref)
+    ds = lcpsearch.generate_dataset(N_ITEMS, SEQ_LEN, SIGMA, seed=3)
+    t0 = time.perf_counter()
+    index = lcpsearch.build(ds)
+    build_s = time.perf_counter() - t0
+    qs = lcpsearch.generate_queries(ds, n_queries, seed=4)
+    out = {"build_s": round(build_s, 3), "queries": n_queries, "unit": "queries/s",
+           "api": "lcpsearch.bench._query_stream(trie.build(ds), q, 10, 'complete', workers=w)"}
+    sweep = {}
+    for w in sorted({1, 2, 4, os.cpu_count() or 1}):
+        _, _, el = _query_stream(index, qs, K, "complete", w)
+        sweep[str(w)] = round(n_queries / el, 1)
+    out["workers_sweep"] = sweep
+    out["value"] = max(sweep.values())
+    return out
+
+
 def run_reference(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -204,6 +245,7 @@ def run_reference(args) -> None:
         "config": bench_config(args.gpus),
         "impl": "reference",
         "cpu_baseline": {"value": value, "unit": "queries/s", "cores": nthreads, "kind": "port",
+                         "cpu_model": cpu_model(),
                          "sample": f"{args.steps} batches x {BATCH} queries; C restatement of "
                                    "trie.build/TrieIndex.query (oracle/lcp_oracle.c), pthreads"},
         "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -444,6 +486,8 @@ def main() -> None:
                 continue
             sweep[str(w)] = cpu_reference(ds, qs, K, min(1.5, args.cpu_budget_s), w, trie=trie)[0]
         line["cpu_baseline"]["threads_sweep"] = sweep
+        line["cpu_baseline"]["cpu_model"] = cpu_model()
+        line["cpu_baseline"]["python_reference"] = python_reference()
         if not args.no_extras:
             flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
             line["extras"] = extras(idx, ds, qs, main_stream, flush_buf)

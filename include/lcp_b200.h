@@ -201,6 +201,51 @@ int lcp_merge_candidates(const uint64_t* cand, int32_t shards, int32_t count, in
  *  merges with one warp per query, larger take with one CTA per query for
  *  shards * k <= 8192.) */
 
+/* ---- device-side routing for sharded query steps (no reference
+ * counterpart; SURVEY §8e lexicographic range sharding).  Every entry point
+ * is asynchronous on `stream` with device buffers and never synchronises the
+ * host, so a whole sharded step can be captured in one CUDA graph.
+ *
+ * pack_queries : rows (count*length u16) -> packed keys (count*words u64),
+ *                the index's key encoding (order-preserving).
+ * route_queries: owner(q) = #splitters <= q (splitters: nsplit sorted packed
+ *                keys, nsplit = world - 1).  thresholds == NULL: select the
+ *                queries this `rank` owns; else select the queries another
+ *                rank owns for which this rank is nonempty and
+ *                max(lcp(q, first[rank]), lcp(q, last[rank])) >= thresholds[q]
+ *                (first/last: world packed keys).  Selected rows are written
+ *                densely to out_rows (count*length u16 capacity), their
+ *                batch positions to out_sel, their number to *d_count
+ *                (device int; reset by the call).  Selection order within the
+ *                dense batch is unspecified; results are scattered back by
+ *                out_sel, so outputs are deterministic.
+ * query_counted: lcp_query over `capacity` rows of which *d_count (device)
+ *                are live; grids are sized for `expected` rows.
+ * shard_thresholds: thresholds[sel[i]] = the lcp of hit need-1 (complete;
+ *                -1 if fewer hits) or matched_depth (strict; -1 if none), for
+ *                i < *d_count.
+ * encode_candidates_sel: cand[sel[i]*k + j] = (length - lcp) << 32 |
+ *                (gids ? gids[id] : id) + id_offset for j < hits[i], else
+ *                UINT64_MAX, for i < *d_count (rows not selected untouched). */
+int lcp_pack_queries(const lcp_index* index, lcp_workspace* ws, const uint16_t* rows, int32_t count,
+                     uint64_t* keys, void* stream);
+int lcp_route_queries(const lcp_index* index, lcp_workspace* ws, const uint16_t* queries,
+                      int32_t count, const uint64_t* splitters, int32_t nsplit,
+                      const uint64_t* first, const uint64_t* last, const int32_t* nonempty,
+                      int32_t rank, const int32_t* thresholds, uint16_t* out_rows,
+                      int32_t* out_sel, int32_t* d_count, void* stream);
+int lcp_query_counted(const lcp_index* index, lcp_workspace* ws, const uint16_t* queries,
+                      int32_t capacity, const int32_t* d_count, int32_t expected, int32_t k,
+                      int32_t mode, int32_t out_stride, uint32_t* ids, uint16_t* lcps,
+                      int32_t* hits, uint16_t* matched_depth, uint64_t* aux, void* stream);
+int lcp_shard_thresholds(const uint16_t* lcps, const int32_t* hits, const uint16_t* matched_depth,
+                         const int32_t* sel, const int32_t* d_count, int32_t capacity, int32_t stride,
+                         int32_t need, int32_t strict, int32_t* thresholds, void* stream);
+int lcp_encode_candidates_sel(const uint32_t* ids, const uint16_t* lcps, const int32_t* hits,
+                              const int32_t* sel, const int32_t* d_count, int32_t capacity, int32_t k,
+                              int32_t in_stride, int32_t length, const int64_t* gids,
+                              int64_t id_offset, uint64_t* cand, void* stream);
+
 /* ---- host staging (no reference counterpart) -----------------------------
  * Page-locked host buffers so *_host calls DMA directly (cudaHostAlloc). */
 int lcp_pinned_alloc(int64_t bytes, void** out);

@@ -90,6 +90,11 @@ SIGNATURES = {
     "lcp_fullscan_host": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _I32, _P, _P, _P]),
     "lcp_encode_candidates": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _I32, _I32, _I64, _P, _P]),
     "lcp_merge_candidates": (ctypes.c_int, [_P, _I32, _I32, _I32, _I32, _I32, _I32, _P, _P, _P, _P]),
+    "lcp_pack_queries": (ctypes.c_int, [_P, _P, _P, _I32, _P, _P]),
+    "lcp_route_queries": (ctypes.c_int, [_P, _P, _P, _I32, _P, _I32, _P, _P, _P, _I32, _P, _P, _P, _P, _P]),
+    "lcp_query_counted": (ctypes.c_int, [_P, _P, _P, _I32, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P]),
+    "lcp_shard_thresholds": (ctypes.c_int, [_P, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _P, _P]),
+    "lcp_encode_candidates_sel": (ctypes.c_int, [_P, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _P, _I64, _P, _P]),
     "lcp_pinned_alloc": (ctypes.c_int, [_I64, ctypes.POINTER(_P)]),
     "lcp_pinned_free": (ctypes.c_int, [_P]),
     "lcp_stream_sync": (ctypes.c_int, [_P]),

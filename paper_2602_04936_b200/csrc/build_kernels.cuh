@@ -129,6 +129,74 @@ __global__ void __launch_bounds__(PK_THREADS) k_pack_stream(
   if (__any_sync(LCP_FULL_MASK, bad) && lane == 0) atomicOr(err, 1);
 }
 
+// Aligned streaming pack, the common shapes (B = bits per symbol as a
+// template constant; L a multiple of the 64/B symbols of a key word and
+// L/8 dividing 32, e.g. L = 16, 32, 64 at sigma <= 256): a warp unit is 32/cpr
+// whole rows, every lane owns a fixed (row-in-unit, chunk) slot, the 8-symbol
+// chunk is packed with constant shifts into its 8*B-bit field, and the lanes of
+// one word sit in an aligned group of 8/B lanes, so the word is OR-reduced
+// with xor shuffles on its 32-bit halves.  ~50 lane instructions per 16-byte
+// chunk instead of ~240 in the general form (ncu: k_pack_stream issue-bound
+// at 70 % issue-slot use, 20 % of HBM).
+template <int B>
+__global__ void __launch_bounds__(PK_THREADS) k_pack_aligned(
+    const uint16_t* __restrict__ rows, long long n, int L, int W, int sigma,
+    u64* __restrict__ keys, u32* __restrict__ ids, int* __restrict__ err) {
+  constexpr int GS = B >= 8 ? 1 : 8 / B;  // lanes per key word
+  const int lane = lane_id();
+  const int cpr = L >> 3;
+  const int rpu = 32 / cpr;
+  const int rr = lane / cpr, j = lane - rr * cpr;  // loop invariants
+  const int g = j & (GS - 1);                       // chunk slot inside the word
+  const int w = B == 16 ? 2 * j : j / GS;           // (first) key word of the chunk
+  const int fshift = B >= 8 ? 0 : 64 - 8 * B * (g + 1);
+  const long long units = (n + rpu - 1) / rpu;
+  const long long warp0 = ((long long)blockIdx.x * PK_THREADS + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * PK_THREADS) >> 5;
+  u32 vmax = 0;
+  for (long long u0 = warp0; u0 < units; u0 += nwarps * PK_UNROLL) {
+    uint4 v[PK_UNROLL];
+#pragma unroll
+    for (int t = 0; t < PK_UNROLL; ++t) {
+      const long long row = (u0 + (long long)t * nwarps) * rpu + rr;
+      v[t] = row < n ? ld_stream16(rows + row * L + j * 8) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int t = 0; t < PK_UNROLL; ++t) {
+      const long long row = (u0 + (long long)t * nwarps) * rpu + rr;
+      const bool ok = row < n;
+      vmax = __vmaxu2(vmax, __vmaxu2(__vmaxu2(v[t].x, v[t].y), __vmaxu2(v[t].z, v[t].w)));
+      // symbol 2i is the low half of word i (little-endian rows)
+      const u32 sy[8] = {v[t].x & 0xffffu, v[t].x >> 16, v[t].y & 0xffffu, v[t].y >> 16,
+                         v[t].z & 0xffffu, v[t].z >> 16, v[t].w & 0xffffu, v[t].w >> 16};
+      if constexpr (B == 16) {
+        const u64 a = ((u64)sy[0] << 48) | ((u64)sy[1] << 32) | ((u64)sy[2] << 16) | sy[3];
+        const u64 c = ((u64)sy[4] << 48) | ((u64)sy[5] << 32) | ((u64)sy[6] << 16) | sy[7];
+        if (ok) *reinterpret_cast<ulonglong2*>(keys + row * W + w) = make_ulonglong2(a, c);
+      } else if constexpr (B == 8) {
+        const u32 hi = (sy[0] << 24) | (sy[1] << 16) | (sy[2] << 8) | sy[3];
+        const u32 lo = (sy[4] << 24) | (sy[5] << 16) | (sy[6] << 8) | sy[7];
+        if (ok) keys[row * W + w] = ((u64)hi << 32) | lo;
+      } else {
+        u32 c = 0;  // the chunk's 8*B-bit field, most significant symbol first
+#pragma unroll
+        for (int i = 0; i < 8; ++i) c |= sy[i] << (8 * B - B * (i + 1));
+        const u64 part = (u64)c << fshift;
+        u32 hi = (u32)(part >> 32), lo = (u32)part;
+#pragma unroll
+        for (int o = 1; o < GS; o <<= 1) {
+          hi |= __shfl_xor_sync(LCP_FULL_MASK, hi, o);
+          lo |= __shfl_xor_sync(LCP_FULL_MASK, lo, o);
+        }
+        if (ok && g == 0) keys[row * W + w] = ((u64)hi << 32) | lo;
+      }
+      if (ids != nullptr && ok && j == 0) ids[row] = (u32)row;
+    }
+  }
+  const u32 m = max(vmax & 0xffffu, vmax >> 16);
+  if (__any_sync(LCP_FULL_MASK, (int)m >= sigma) && lane == 0) atomicOr(err, 1);
+}
+
 // hi / lo 32-bit planes of each key's first word (full-scan layout)
 __global__ void k_split_words(const u64* __restrict__ keys, long long n, int W,
                               u32* __restrict__ hi, u32* __restrict__ lo) {
@@ -359,6 +427,7 @@ constexpr int OS_WARP_SEG = 32 * OS_ITEMS;
 constexpr u64 OS_FLAG_AGG = 1ull << 62;
 constexpr u64 OS_FLAG_PREFIX = 2ull << 62;
 constexpr u64 OS_COUNT_MASK = (1ull << 62) - 1;
+constexpr int OS_LB_WIN = 16;  // look-back statuses loaded per round trip (first hop: 8)
 constexpr size_t OS_SMEM = (size_t)OS_TILE * 12 + (size_t)OS_WARPS * 256 * 4 + 3 * 256 * 4 + 64;
 
 __device__ __forceinline__ u64 ld_relaxed_u64(const u64* p) {
@@ -370,7 +439,7 @@ __device__ __forceinline__ void st_relaxed_u64(u64* p, u64 v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-__global__ void __launch_bounds__(OS_THREADS) k_onesweep(
+__global__ void __launch_bounds__(OS_THREADS, 3) k_onesweep(
     const u64* __restrict__ kin, const u32* __restrict__ vin, u64* __restrict__ kout,
     u32* __restrict__ vout, long long n, int shift, const u32* __restrict__ hist,
     u64* __restrict__ status, unsigned* __restrict__ tile_counter) {
@@ -426,25 +495,15 @@ __global__ void __launch_bounds__(OS_THREADS) k_onesweep(
   // publish the aggregate (tile 0: its inclusive prefix) as early as possible
   u64* my = status + tile * 256 + d0;
   st_relaxed_u64(my, (tile == 0 ? OS_FLAG_PREFIX : OS_FLAG_AGG) | (u64)cnt);
-  // bucket start of this digit: exclusive scan of the pass histogram
+  // bucket start of this digit (exclusive scan of the pass histogram) and the
+  // digit's start inside the tile
   u32 total;
   const u32 bstart = block_excl_scan<u32>(hist[d0], &total, scratch);
   const u32 tst = block_excl_scan<u32>(cnt, &total, scratch);
-  // decoupled look-back over earlier tiles
-  u64 excl = 0;
-  for (long long p = tile - 1; p >= 0; --p) {
-    u64 v;
-    do {
-      v = ld_relaxed_u64(status + p * 256 + d0);
-    } while ((v >> 62) == 0);
-    excl += v & OS_COUNT_MASK;
-    if ((v >> 62) == 2) break;
-  }
-  if (tile > 0) st_relaxed_u64(my, OS_FLAG_PREFIX | (excl + cnt));
-  gstart[d0] = bstart + (u32)excl;
   tstart[d0] = tst;
   __syncthreads();
-  // reorder the tile by (digit, stable rank) in shared memory
+  // reorder the tile by (digit, stable rank) in shared memory: this needs only
+  // tile-local counts, so it runs before the look-back and frees the registers
 #pragma unroll
   for (int j = 0; j < OS_ITEMS; ++j) {
     const long long i = seg + j * 32 + lane;
@@ -455,6 +514,37 @@ __global__ void __launch_bounds__(OS_THREADS) k_onesweep(
       sv[pos] = val[j];
     }
   }
+  // decoupled look-back over earlier tiles, OS_LB_WIN statuses per round trip
+  // (independent loads): a tile with no resolved predecessor in reach would
+  // otherwise walk back one dependent L2 round trip per tile, which is what
+  // bounds the first wave (ncu: ~16 hops per tile at 2M, 47 us per pass)
+  u64 excl = 0;
+  long long p = tile - 1;
+  int win = 8;
+  while (p >= 0) {
+    u64 v[OS_LB_WIN];
+#pragma unroll
+    for (int i = 0; i < OS_LB_WIN; ++i)
+      v[i] = (i < win && p - i >= 0) ? ld_relaxed_u64(status + (p - i) * 256 + d0) : OS_FLAG_PREFIX;
+    int used = 0;
+    bool resolved = false;
+#pragma unroll
+    for (int i = 0; i < OS_LB_WIN; ++i) {
+      if (i < win && !resolved && used == i) {
+        const u64 f = v[i] >> 62;
+        if (f != 0) {
+          excl += v[i] & OS_COUNT_MASK;
+          resolved = f == 2;
+          used = i + 1;
+        }
+      }
+    }
+    if (resolved) break;
+    p -= used;  // used < win: tile p was not ready yet; poll it again
+    win = OS_LB_WIN;
+  }
+  if (tile > 0) st_relaxed_u64(my, OS_FLAG_PREFIX | (excl + cnt));
+  gstart[d0] = bstart + (u32)excl;
   __syncthreads();
   const long long rem = n - tile * OS_TILE;
   const int tile_n = rem < OS_TILE ? (int)rem : OS_TILE;

@@ -54,6 +54,9 @@ struct DevIndex {
   long long sk_off[LCP_MAX_LEVELS];  // block offset of level j (lists of LCP_SK_LIST)
   long long sk_cnt[LCP_MAX_LEVELS];  // blocks at level j
   int sk_levels;
+  // per launch, normally null: a device int capping `count` (a batch whose size
+  // is only known on the device, e.g. the queries a range shard owns)
+  const int* dcount;
 };
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }

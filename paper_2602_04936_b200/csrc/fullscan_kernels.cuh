@@ -222,29 +222,47 @@ __global__ void __launch_bounds__(FS_THREADS)
 // Small query batches (count <= FSQ_QMAX, need <= 32): HBM-streaming scan.
 //
 // With a handful of queries the corpus pass is bandwidth-, not issue-bound
-// (3 lane instructions per (key, query) against 8 B per key), so the layout
+// (~2 lane instructions per (key, query) against 4 B per key), so the layout
 // flips: every lane holds ALL the batch's query words, one CTA per SM of 16
-// warps streams the hi / lo planes of the keys' first words with 16-byte
-// `ld.global.nc` loads (4 keys per lane per plane, FSQ_UNROLL groups in
-// flight), each warp over its own contiguous id segment.  Per (key, query) the
-// fast path is xor + min + compare on the hi word against the query's bound;
-// a warp enters the exact path (full first word, further words for W > 1,
-// warp top-k insertion by composite) only when some lane has a survivor.
-// Bounds tighten from the warp's own full list (worst kept lcp + 1: ids only
-// grow along a segment) and from a per-query global hint (atomicMax of every
-// full list's worst kept lcp).  Each CTA merges its warps' lists in shared
-// memory; the last CTA to finish merges the CTAs' lists, writes the outputs
-// and resets the hint / counter, so one launch is the whole query.
+// warps streams the hi plane of the keys' first words with 16-byte
+// `ld.global.nc` loads (4 keys per load, FSQ_UNROLL loads in flight per lane),
+// each warp over its own contiguous id segment.  Per (key, query) the fast
+// path is xor + min on the hi word against the query's bound; the lo word
+// (and further words for W > 1) is read only for the rare survivors, whose
+// exact composites go into a warp top-k list.  Bounds tighten from the warp's
+// own full list (worst kept lcp + 1: ids only grow along a segment) and from a
+// per-query global hint (atomicMax of every full list's worst kept lcp).
+// Each CTA tree-merges its warps' lists in shared memory; the last CTA to
+// finish merges the CTAs' lists with all its warps, writes the outputs and
+// resets the hint / counter, so one launch is the whole query.
 // Replaces oracle._lcp_profile + oracle_top_k (oracle.py:38-59) for the
 // single-query / small-batch calls of the reference API.
 // ---------------------------------------------------------------------------
 constexpr int FSQ_THREADS = 512;
 constexpr int FSQ_WARPS = FSQ_THREADS / 32;
 constexpr int FSQ_QMAX = 8;
-constexpr int FSQ_STEP = 512;                      // keys per warp step (4 x 4 or 2 x 4 per lane)
-// 4-key groups per lane per step: fewer with more queries (register budget)
+constexpr int FSQ_STEP = 1024;  // segment granularity (keys); >= one warp step for every Q
+// 16-byte hi-plane loads per lane per step: fewer with more queries (registers)
 template <int Q>
-__host__ __device__ constexpr int fsq_unroll() { return Q <= 4 ? 4 : 2; }
+__host__ __device__ constexpr int fsq_unroll() { return Q <= 2 ? 8 : (Q <= 4 ? 4 : 2); }
+
+// merge the sorted 32-slot warp lists buf[0..n) (one per 32 entries) into
+// buf[0]: a tree over the CTA's warps, `groups` independent trees side by side
+// (tree g: lists g*n .. g*n+n-1); all threads of the CTA call it
+template <typename C>
+__device__ void cta_tree_merge(C* buf, int n, int groups) {
+  const int lane = lane_id(), warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int half = (n + 1) >> 1, width = n; width > 1; width = half, half = (half + 1) >> 1) {
+    const int pairs = width - half;  // list i < pairs absorbs list i + half
+    for (int t = warp; t < pairs * groups; t += nw) {
+      const int g = t / pairs, i = t - g * pairs;
+      C* dst = buf + (g * n + i) * 32;
+      const C* src = buf + (g * n + i + half) * 32;
+      dst[lane] = warp_merge32(dst[lane], src[lane]);
+    }
+    __syncthreads();
+  }
+}
 
 template <typename C, int Q>
 __global__ void __launch_bounds__(FSQ_THREADS, 1)
@@ -252,17 +270,16 @@ __global__ void __launch_bounds__(FSQ_THREADS, 1)
                       C* __restrict__ partial, int* __restrict__ hint, unsigned* __restrict__ done_ctr,
                       u32* __restrict__ out_ids, uint16_t* __restrict__ out_lcps,
                       int* __restrict__ out_hits, int out_stride) {
+  constexpr int U = fsq_unroll<Q>();
   extern __shared__ __align__(16) unsigned char fsq_smem[];
-  C* wl = reinterpret_cast<C*>(fsq_smem);  // [FSQ_WARPS][Q][32] warp lists
+  C* wl = reinterpret_cast<C*>(fsq_smem);  // [Q][FSQ_WARPS][32] warp lists
   __shared__ int s_last;
-  constexpr int FSQ_UNROLL = fsq_unroll<Q>();
   const int lane = lane_id(), warp = threadIdx.x >> 5;
   const int L = ix.L, W = ix.W, lb = ix.lb, b = ix.b;
   const int idbits = sizeof(C) == 8 ? 32 : ix.idbits;
   const long long n = ix.n;
 
   u32 qh[Q], ql[Q], limh[Q];
-  u64 limm1[Q];
   C slot[Q], thr[Q];
   int a[Q], a_own[Q];
 #pragma unroll
@@ -274,22 +291,21 @@ __global__ void __launch_bounds__(FSQ_THREADS, 1)
     thr[q] = ~C(0);
     a[q] = q < count ? 0 : L + 1;  // absent queries never admit a key
     a_own[q] = 0;
-    limm1[q] = q < count ? ~0ull : 0ull;
     limh[q] = q < count ? ~0u : 0u;
   }
-  auto set_bound = [&](int q, int na) {  // survive iff lcp >= na  <=>  (key ^ q) <= limm1
+  // survive iff lcp >= na; on the hi word: (hi ^ qh) <= limh is necessary
+  auto set_bound = [&](int q, int na) {
     a[q] = na;
     const int bits = na * b;
-    limm1[q] = na > L ? 0ull : (bits >= 64 ? 0ull : (~0ull >> bits));
-    limh[q] = (u32)(limm1[q] >> 32);
+    limh[q] = na > L ? 0u : (bits >= 32 ? 0u : (~0u >> bits));
   };
 
   const long long gw = (long long)blockIdx.x * FSQ_WARPS + warp;
   const long long k0 = gw * seg;
   const long long k1 = min(n, k0 + seg);
   int step = 0;
-  for (long long base = k0; base < k1; base += 128 * FSQ_UNROLL, ++step) {
-    if ((step & 3) == 0) {  // other warps' bounds (global hint), every 4 steps
+  for (long long base = k0; base < k1; base += 128 * U, ++step) {
+    if ((step & 1) == 0) {  // other warps' bounds (global hint)
       const int hv = lane < Q && lane < count ? *(volatile int*)(hint + lane) : 0;
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
@@ -297,73 +313,67 @@ __global__ void __launch_bounds__(FSQ_THREADS, 1)
         if (g > a[q]) set_bound(q, g);
       }
     }
-    uint4 h[FSQ_UNROLL], lo[FSQ_UNROLL];
+    uint4 h[U];
 #pragma unroll
-    for (int u = 0; u < FSQ_UNROLL; ++u) {
-      const long long i = base + u * 128 + lane * 4;  // planes are padded past n
-      h[u] = ld_stream16(ix.keys_hi + i);
-      lo[u] = ld_stream16(ix.keys_lo + i);
-    }
+    for (int u = 0; u < U; ++u) h[u] = ld_stream16(ix.keys_hi + base + u * 128 + lane * 4);  // padded past n
     unsigned surv = 0;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       u32 m = ~0u;
 #pragma unroll
-      for (int u = 0; u < FSQ_UNROLL; ++u)
+      for (int u = 0; u < U; ++u)
         m = min(m, min(min(h[u].x ^ qh[q], h[u].y ^ qh[q]), min(h[u].z ^ qh[q], h[u].w ^ qh[q])));
       surv |= (u32)(m <= limh[q]) << q;
     }
     surv = __reduce_or_sync(LCP_FULL_MASK, surv);
-    if (surv) {
+    if (!surv) continue;
 #pragma unroll
-      for (int q = 0; q < Q; ++q) {
-        if (!((surv >> q) & 1)) continue;
+    for (int q = 0; q < Q; ++q) {
+      if (!((surv >> q) & 1)) continue;
 #pragma unroll
-        for (int u = 0; u < FSQ_UNROLL; ++u) {
-          const u32 hh[4] = {h[u].x, h[u].y, h[u].z, h[u].w};
-          const u32 ll[4] = {lo[u].x, lo[u].y, lo[u].z, lo[u].w};
+      for (int u = 0; u < U; ++u) {
+        const u32 hh[4] = {h[u].x, h[u].y, h[u].z, h[u].w};
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const long long i = base + u * 128 + lane * 4 + j;
-            const u64 x = ((u64)(hh[j] ^ qh[q]) << 32) | (u64)(ll[j] ^ ql[q]);
-            C c = ~C(0);
-            if (i < k1 && x <= limm1[q]) {
-              int l = x ? (__clzll((long long)x) >> lb) : L;
-              if (!x && W > 1) {  // first word equal: finish on the remaining words
-                const u64* key = ix.keys_orig + i * W;
-                const u64* qk = qkeys + (long long)q * W;
-                for (int w = 1; w < W; ++w) {
-                  const u64 y = key[w] ^ qk[w];
-                  if (y) {
-                    l = w * ix.spw + (__clzll((long long)y) >> lb);
-                    break;
-                  }
+        for (int j = 0; j < 4; ++j) {
+          const long long i = base + u * 128 + lane * 4 + j;
+          C c = ~C(0);
+          if (i < k1 && (hh[j] ^ qh[q]) <= limh[q]) {  // rare: finish on the lo word
+            const u64 x = ((u64)(hh[j] ^ qh[q]) << 32) | (u64)(__ldg(ix.keys_lo + i) ^ ql[q]);
+            int l = x ? (__clzll((long long)x) >> lb) : L;
+            if (!x && W > 1) {  // first word equal: finish on the remaining words
+              const u64* key = ix.keys_orig + i * W;
+              const u64* qk = qkeys + (long long)q * W;
+              for (int w = 1; w < W; ++w) {
+                const u64 y = key[w] ^ qk[w];
+                if (y) {
+                  l = w * ix.spw + (__clzll((long long)y) >> lb);
+                  break;
                 }
               }
-              if (l >= a[q]) c = make_comp<C>(l, (u32)i, L, idbits);
             }
-            warp_offer<C, true>(slot[q], thr[q], c, need);
+            if (l >= a[q]) c = make_comp<C>(min(l, L), (u32)i, L, idbits);
           }
+          warp_offer<C, true>(slot[q], thr[q], c, need);
         }
-        if (thr[q] != ~C(0)) {  // full: later keys of this segment have larger ids
-          const int t = L - (int)(widen_comp<C>(thr[q], idbits) >> 32);
-          if (t + 1 > a_own[q]) {
-            a_own[q] = t + 1;
-            if (lane == 0) atomicMax(hint + q, t);
-          }
-          if (a_own[q] > a[q]) set_bound(q, a_own[q]);
+      }
+      if (thr[q] != ~C(0)) {  // full: later keys of this segment have larger ids
+        const int t = L - (int)(widen_comp<C>(thr[q], idbits) >> 32);
+        if (t + 1 > a_own[q]) {
+          a_own[q] = t + 1;
+          if (lane == 0) atomicMax(hint + q, t);
         }
+        if (a_own[q] > a[q]) set_bound(q, a_own[q]);
       }
     }
   }
-  // CTA merge: warp lists -> one list per query
+  // CTA merge: 16 warp lists per query -> one (tree of warp merges)
 #pragma unroll
-  for (int q = 0; q < Q; ++q) wl[(warp * Q + q) * 32 + lane] = slot[q];
+  for (int q = 0; q < Q; ++q) wl[(q * FSQ_WARPS + warp) * 32 + lane] = slot[q];
   __syncthreads();
-  for (int q = warp; q < Q && q < count; q += FSQ_WARPS) {
-    C v = wl[q * 32 + lane];
-    for (int w = 1; w < FSQ_WARPS; ++w) v = warp_merge32(v, wl[(w * Q + q) * 32 + lane]);
-    if (lane < need) partial[((long long)blockIdx.x * count + q) * need + lane] = v;
+  cta_tree_merge<C>(wl, FSQ_WARPS, min(Q, count));
+  for (int t = threadIdx.x; t < count * need; t += FSQ_THREADS) {
+    const int q = t / need, j = t - q * need;
+    partial[((long long)blockIdx.x * count + q) * need + j] = wl[(q * FSQ_WARPS) * 32 + j];
   }
   __threadfence();
   __syncthreads();
@@ -371,24 +381,36 @@ __global__ void __launch_bounds__(FSQ_THREADS, 1)
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  for (int q = warp; q < count; q += FSQ_WARPS) {
+  // last CTA: the grid's lists per query, spread over all warps (warp w takes
+  // CTA lists w', w' + P, ... of query w % Q), then a tree merge per query
+  const int qn = min(Q, count);
+  const int P = FSQ_WARPS / qn;  // warps per query
+  if (warp < qn * P) {
+    const int q = warp % qn, part = warp / qn;
     C sl = ~C(0), th = ~C(0);
-    const long long tot = (long long)gridDim.x * need;
-    for (long long t0 = 0; t0 < tot; t0 += 32) {
-      const long long t = t0 + lane;
-      C c = ~C(0);
-      if (t < tot) c = *(volatile C*)(partial + ((t / need) * count + q) * need + (t % need));
-      warp_offer<C, true>(sl, th, c, need);
+    // lane l takes CTA list part + (r + l) * P; the lists' entries are offered
+    // row by row (each list is sorted, so late rows rarely beat the threshold)
+    for (long long r = 0; part + r * P < (long long)gridDim.x; r += 32) {
+      const long long li = part + (r + lane) * P;
+      for (int j = 0; j < need; ++j) {
+        C c = ~C(0);
+        if (li < gridDim.x) c = *(volatile C*)(partial + (li * count + q) * need + j);
+        warp_offer<C, true>(sl, th, c, need);
+      }
     }
-    if (lane < need) {
-      const u64 w64 = widen_comp<C>(sl, idbits);
-      out_ids[(long long)q * out_stride + lane] = (u32)(w64 & 0xffffffffull);
-      out_lcps[(long long)q * out_stride + lane] = (uint16_t)(L - (int)(w64 >> 32));
-    }
-    if (lane == 0) {
-      out_hits[q] = need;
-      hint[q] = 0;  // ready for the next launch (graph replays)
-    }
+    wl[(q * P + part) * 32 + lane] = sl;
+  }
+  __syncthreads();
+  cta_tree_merge<C>(wl, P, qn);
+  for (int t = threadIdx.x; t < count * need; t += FSQ_THREADS) {
+    const int q = t / need, j = t - q * need;
+    const u64 w64 = widen_comp<C>(wl[(q * P) * 32 + j], idbits);
+    out_ids[(long long)q * out_stride + j] = (u32)(w64 & 0xffffffffull);
+    out_lcps[(long long)q * out_stride + j] = (uint16_t)(L - (int)(w64 >> 32));
+  }
+  for (int q = threadIdx.x; q < count; q += FSQ_THREADS) {
+    out_hits[q] = need;
+    hint[q] = 0;  // ready for the next launch (graph replays)
   }
   if (threadIdx.x == 0) *done_ctr = 0;
 }

@@ -22,6 +22,7 @@
 #include "common.cuh"
 #include "fullscan_kernels.cuh"
 #include "query_kernels.cuh"
+#include "shard_kernels.cuh"
 
 namespace {
 
@@ -225,8 +226,22 @@ int radix_sort_pairs(u64** k, u32** v, u64** k_alt, u32** v_alt, long long n, cu
 int pack_rows(const uint16_t* rows, long long n, const DevIndex& dv, u64* keys, u32* ids, int* err,
               cudaStream_t st) {
   if (n <= 0) return LCP_OK;
-  if (dv.L % 8 == 0 && ((uintptr_t)rows & 15) == 0) {
-    const int cpr = dv.L / 8;
+  const int cpr = dv.L / 8;
+  if (dv.L % 8 == 0 && ((uintptr_t)rows & 15) == 0 && dv.L % dv.spw == 0 && cpr <= 32 &&
+      32 % cpr == 0) {
+    const long long units = (n + 32 / cpr - 1) / (32 / cpr);
+    const long long want = (units + (PK_THREADS / 32) * PK_UNROLL - 1) / ((PK_THREADS / 32) * PK_UNROLL);
+    const unsigned grid = (unsigned)std::max(1ll, std::min<long long>(want, 8ll * num_sms()));
+#define LCP_PKA(BB) k_pack_aligned<BB><<<grid, PK_THREADS, 0, st>>>(rows, n, dv.L, dv.W, dv.sigma, keys, ids, err)
+    switch (dv.b) {
+      case 1: LCP_PKA(1); break;
+      case 2: LCP_PKA(2); break;
+      case 4: LCP_PKA(4); break;
+      case 8: LCP_PKA(8); break;
+      default: LCP_PKA(16); break;
+    }
+#undef LCP_PKA
+  } else if (dv.L % 8 == 0 && ((uintptr_t)rows & 15) == 0) {
     const long long units = cpr <= 32 ? (n + 32 / cpr - 1) / (32 / cpr) : n * ((cpr + 31) / 32);
     const long long want = (units + (PK_THREADS / 32) * PK_UNROLL - 1) / ((PK_THREADS / 32) * PK_UNROLL);
     const unsigned grid = (unsigned)std::max(1ll, std::min<long long>(want, 8ll * num_sms()));
@@ -1202,15 +1217,14 @@ static void launch_w1(const DevIndex& dv, int mode, unsigned grid, unsigned bloc
 }
 
 template <int WMAX>
-static void launch_fast(const lcp_index* ix, const uint16_t* q, int count, int k, int mode,
+static void launch_fast(const DevIndex& dv, const uint16_t* q, int count, int gcount, int k, int mode,
                         int stride, u32* ids, uint16_t* lcps, int* hits, uint16_t* md, u64* aux,
                         int* err, cudaStream_t st, lcp_workspace* ws) {
-  const DevIndex& dv = ix->dv;
   if (mode == LCP_MODE_TAL && WMAX > 1) {
     const long long sms = num_sms();
-    const long long wpc = std::min<long long>(32, std::max<long long>(1, (count + sms - 1) / sms));
+    const long long wpc = std::min<long long>(32, std::max<long long>(1, (gcount + sms - 1) / sms));
     const unsigned block = (unsigned)(wpc * 32);
-    const unsigned grid = (unsigned)std::min<long long>((count + wpc - 1) / wpc, 4ll * sms);
+    const unsigned grid = (unsigned)std::min<long long>((gcount + wpc - 1) / wpc, 4ll * sms);
     const size_t smem = 16 + (size_t)dv.smem_entries * 8;
     k_query_warp_tal<WMAX><<<grid, block, smem, st>>>(dv, q, count, k, stride, ids, lcps, hits, md,
                                                       aux, err);
@@ -1227,7 +1241,7 @@ static void launch_fast(const lcp_index* ix, const uint16_t* q, int count, int k
       const char* e = getenv("LCP_QPW");
       return e ? std::max(1ll, std::min(16ll, atoll(e))) : 1ll;
     }();
-    const long long units = (count + qpw - 1) / qpw;
+    const long long units = (gcount + qpw - 1) / qpw;
     long long wpc = std::min<long long>(32, std::max<long long>(wpc_min, (units + sms - 1) / sms));
     const unsigned block = (unsigned)(wpc * 32);
     unsigned grid = (unsigned)std::min<long long>((units + wpc - 1) / wpc, 4ll * sms);
@@ -1255,10 +1269,13 @@ extern "C" {
 
 // lcp_query's body; `errp` is the device int the kernels raise on an invalid
 // query symbol (the workspace's flag, or a slot of a packed output block)
+// `dcount` (device int, may be null) caps the batch on the device: `count` is
+// then the capacity of the buffers and `gcount` the expected size the grids
+// are sized for (the kernels' grid-stride loops cover any count up to capacity)
 static int query_impl(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries,
                       int32_t count, int32_t k, int32_t mode, int32_t out_stride, uint32_t* ids,
                       uint16_t* lcps, int32_t* hits, uint16_t* matched_depth, uint64_t* aux,
-                      void* stream, int* errp) {
+                      void* stream, int* errp, const int* dcount = nullptr, int gcount = -1) {
   if (!ix || !ws) return fail(LCP_ERR_INVALID_INPUT, "null index or workspace");
   if (k < 1) return fail(LCP_ERR_INVALID_INPUT, "k must be >= 1, got " + std::to_string(k));
   if (mode < 0 || mode > 2)
@@ -1266,8 +1283,11 @@ static int query_impl(const lcp_index* ix, lcp_workspace* ws, const uint16_t* qu
                                            std::to_string(mode));
   if (mode == LCP_MODE_TAL && ix->tal_depth < 0)
     return fail(LCP_ERR_STATE, "index was built without a TAL bucket structure");
-  const DevIndex& dv = ix->dv;
+  DevIndex dvl = ix->dv;
+  dvl.dcount = dcount;
+  const DevIndex& dv = dvl;
   if (count < 0) return fail(LCP_ERR_INVALID_INPUT, "count must be >= 0");
+  if (!dcount || gcount < 1 || gcount > count) gcount = count;
   if (count == 0) return LCP_OK;
   const long long need_stride = std::min<long long>(k, std::max(1ll, dv.n));
   if (out_stride < need_stride)
@@ -1304,9 +1324,9 @@ static int query_impl(const lcp_index* ix, lcp_workspace* ws, const uint16_t* qu
     // which now runs only when LCP_KN_MIN raises the threshold
     const long long sms = num_sms();
     const long long wmax = needk <= 64 ? 32 : 16;  // 4-slot lists: 512-thread CTAs
-    const long long wpc = std::min<long long>(wmax, std::max<long long>(1, (count + sms - 1) / sms));
+    const long long wpc = std::min<long long>(wmax, std::max<long long>(1, (gcount + sms - 1) / sms));
     const unsigned block = (unsigned)(wpc * 32);
-    const unsigned grid = (unsigned)std::min<long long>((count + wpc - 1) / wpc, 8ll * sms);
+    const unsigned grid = (unsigned)std::min<long long>((gcount + wpc - 1) / wpc, 8ll * sms);
     // staged levels, then one 32 * NS-entry merge buffer per warp
     const size_t smem0 = 16 + (size_t)dv.smem_entries * 8;
 #define LCP_KN(C, M, NS)                                                                         \
@@ -1334,9 +1354,9 @@ static int query_impl(const lcp_index* ix, lcp_workspace* ws, const uint16_t* qu
     // 2- or 4-slot list
     const long long sms = num_sms();
     const long long wmax = needk <= 64 ? 32 : 16;  // 4-slot lists: 512-thread CTAs
-    const long long wpc = std::min<long long>(wmax, std::max<long long>(1, (count + sms - 1) / sms));
+    const long long wpc = std::min<long long>(wmax, std::max<long long>(1, (gcount + sms - 1) / sms));
     const unsigned block = (unsigned)(wpc * 32);
-    const unsigned grid = (unsigned)std::min<long long>((count + wpc - 1) / wpc, 8ll * sms);
+    const unsigned grid = (unsigned)std::min<long long>((gcount + wpc - 1) / wpc, 8ll * sms);
     const size_t smem0 = 16 + (size_t)dv.smem_entries * 8;
 #define LCP_WKN1(WM, NS, TL)                                                                     \
   do {                                                                                           \
@@ -1357,10 +1377,10 @@ static int query_impl(const lcp_index* ix, lcp_workspace* ws, const uint16_t* qu
     return LCP_OK;
   }
   if (dv.W <= 8 && k <= FAST_KMAX) {
-    if (dv.W == 1) launch_fast<1>(ix, queries, count, k, mode, out_stride, ids, lcps, hits, md, ax, errp, st, ws);
-    else if (dv.W == 2) launch_fast<2>(ix, queries, count, k, mode, out_stride, ids, lcps, hits, md, ax, errp, st, ws);
-    else if (dv.W <= 4) launch_fast<4>(ix, queries, count, k, mode, out_stride, ids, lcps, hits, md, ax, errp, st, ws);
-    else launch_fast<8>(ix, queries, count, k, mode, out_stride, ids, lcps, hits, md, ax, errp, st, ws);
+    if (dv.W == 1) launch_fast<1>(dv, queries, count, gcount, k, mode, out_stride, ids, lcps, hits, md, ax, errp, st, ws);
+    else if (dv.W == 2) launch_fast<2>(dv, queries, count, gcount, k, mode, out_stride, ids, lcps, hits, md, ax, errp, st, ws);
+    else if (dv.W <= 4) launch_fast<4>(dv, queries, count, gcount, k, mode, out_stride, ids, lcps, hits, md, ax, errp, st, ws);
+    else launch_fast<8>(dv, queries, count, gcount, k, mode, out_stride, ids, lcps, hits, md, ax, errp, st, ws);
     LCP_CK_LAUNCH();
     return LCP_OK;
   }
@@ -1368,8 +1388,8 @@ static int query_impl(const lcp_index* ix, lcp_workspace* ws, const uint16_t* qu
   LCP_TRY(pack_rows(queries, count, dv, ws->qkeys.as<u64>(), nullptr, errp, st));
   if (dv.W > 8 && mode != LCP_MODE_TAL && k <= FAST_KMAX) {  // long keys: warp per query
     const long long sms = num_sms();
-    const long long wpc = std::min<long long>(32, std::max<long long>(1, (count + sms - 1) / sms));
-    const unsigned grid = (unsigned)std::min<long long>((count + wpc - 1) / wpc, 8ll * sms);
+    const long long wpc = std::min<long long>(32, std::max<long long>(1, (gcount + sms - 1) / sms));
+    const unsigned grid = (unsigned)std::min<long long>((gcount + wpc - 1) / wpc, 8ll * sms);
     k_query_warp_any<<<grid, (unsigned)(wpc * 32), 0, st>>>(dv, ws->qkeys.as<u64>(), count, k, mode,
                                                             out_stride, ids, lcps, hits, md, ax);
     LCP_CK_LAUNCH();
@@ -1378,8 +1398,8 @@ static int query_impl(const lcp_index* ix, lcp_workspace* ws, const uint16_t* qu
   if (dv.W > 8 && mode != LCP_MODE_TAL && needk > FAST_KMAX && needk <= 128) {  // long keys, lists
     const long long sms = num_sms();
     const long long wmax = needk <= 64 ? 32 : 16;  // 4-slot lists: 512-thread CTAs
-    const long long wpc = std::min<long long>(wmax, std::max<long long>(1, (count + sms - 1) / sms));
-    const unsigned grid = (unsigned)std::min<long long>((count + wpc - 1) / wpc, 8ll * sms);
+    const long long wpc = std::min<long long>(wmax, std::max<long long>(1, (gcount + sms - 1) / sms));
+    const unsigned grid = (unsigned)std::min<long long>((gcount + wpc - 1) / wpc, 8ll * sms);
     if (needk <= 64) {
       allow_dyn_smem<k_query_warp_any_kn<2>>();
       k_query_warp_any_kn<2><<<grid, (unsigned)(wpc * 32), (size_t)wpc * 64 * 8, st>>>(
@@ -1392,7 +1412,7 @@ static int query_impl(const lcp_index* ix, lcp_workspace* ws, const uint16_t* qu
     LCP_CK_LAUNCH();
     return LCP_OK;
   }
-  unsigned grid = (unsigned)gen_grid(count);
+  unsigned grid = (unsigned)gen_grid(gcount);
   k_query_general<<<grid, GEN_THREADS, 0, st>>>(dv, ws->qkeys.as<u64>(), queries, count, k, mode,
                                                 0, out_stride, ids, lcps, hits, md, ax);
   LCP_CK_LAUNCH();
@@ -1798,6 +1818,75 @@ int lcp_merge_candidates(const uint64_t* cand, int32_t shards, int32_t count, in
     return fail(LCP_ERR_INVALID_INPUT, "merge needs 0 <= take <= k");
   return launch_merge((const u64*)cand, shards, count, k, (long long)count * k, k, take, length,
                       strict, ids, lcps, hits, std::max(1, take), (cudaStream_t)stream);
+}
+
+// ---- device-side routing for sharded steps (shard_kernels.cuh) ----------------
+int lcp_pack_queries(const lcp_index* ix, lcp_workspace* ws, const uint16_t* rows, int32_t count,
+                     uint64_t* keys, void* stream) {
+  if (!ix || !ws) return fail(LCP_ERR_INVALID_INPUT, "null index or workspace");
+  if (count <= 0) return LCP_OK;
+  if (!rows || !keys) return fail(LCP_ERR_INVALID_INPUT, "null rows or keys");
+  return pack_rows(rows, count, ix->dv, reinterpret_cast<u64*>(keys), nullptr, ws->d_err,
+                   (cudaStream_t)stream);
+}
+
+int lcp_route_queries(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries, int32_t count,
+                      const uint64_t* splitters, int32_t nsplit, const uint64_t* first,
+                      const uint64_t* last, const int32_t* nonempty, int32_t rank,
+                      const int32_t* thresholds, uint16_t* out_rows, int32_t* out_sel,
+                      int32_t* d_count, void* stream) {
+  if (!ix || !ws) return fail(LCP_ERR_INVALID_INPUT, "null index or workspace");
+  if (!d_count || !out_sel || !out_rows) return fail(LCP_ERR_INVALID_INPUT, "null route output");
+  if (nsplit < 0 || rank < 0 || rank > nsplit) return fail(LCP_ERR_INVALID_INPUT, "bad rank / splitter count");
+  if (thresholds && (!first || !last || !nonempty))
+    return fail(LCP_ERR_INVALID_INPUT, "consult routing needs first / last rows and nonempty flags");
+  cudaStream_t st = (cudaStream_t)stream;
+  LCP_CK(cudaMemsetAsync(d_count, 0, sizeof(int32_t), st));
+  if (count <= 0) return LCP_OK;
+  const DevIndex& dv = ix->dv;
+  LCP_TRY(ws->qkeys.ensure((size_t)count * dv.W * 8));
+  LCP_TRY(pack_rows(queries, count, dv, ws->qkeys.as<u64>(), nullptr, ws->d_err, st));
+  k_route_queries<<<blocks_for(count, RT_THREADS), RT_THREADS, 0, st>>>(
+      ws->qkeys.as<u64>(), queries, count, dv.L, dv.W, dv.spw, dv.lb,
+      reinterpret_cast<const u64*>(splitters), nsplit, reinterpret_cast<const u64*>(first),
+      reinterpret_cast<const u64*>(last), nonempty, rank, thresholds, out_rows, out_sel, d_count);
+  LCP_CK_LAUNCH();
+  return LCP_OK;
+}
+
+int lcp_query_counted(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries,
+                      int32_t capacity, const int32_t* d_count, int32_t expected, int32_t k,
+                      int32_t mode, int32_t out_stride, uint32_t* ids, uint16_t* lcps, int32_t* hits,
+                      uint16_t* matched_depth, uint64_t* aux, void* stream) {
+  if (!ws) return fail(LCP_ERR_INVALID_INPUT, "null index or workspace");
+  if (!d_count) return fail(LCP_ERR_INVALID_INPUT, "null device count");
+  return query_impl(ix, ws, queries, capacity, k, mode, out_stride, ids, lcps, hits, matched_depth,
+                    aux, stream, ws->d_err, d_count, expected);
+}
+
+int lcp_shard_thresholds(const uint16_t* lcps, const int32_t* hits, const uint16_t* matched_depth,
+                         const int32_t* sel, const int32_t* d_count, int32_t capacity, int32_t stride,
+                         int32_t need, int32_t strict, int32_t* thresholds, void* stream) {
+  if (capacity <= 0) return LCP_OK;
+  if (!lcps || !hits || !sel || !d_count || !thresholds || (strict && !matched_depth))
+    return fail(LCP_ERR_INVALID_INPUT, "null threshold argument");
+  k_shard_threshold<<<blocks_for(capacity, 256), 256, 0, (cudaStream_t)stream>>>(
+      lcps, hits, matched_depth, sel, d_count, stride, need, strict, thresholds);
+  LCP_CK_LAUNCH();
+  return LCP_OK;
+}
+
+int lcp_encode_candidates_sel(const uint32_t* ids, const uint16_t* lcps, const int32_t* hits,
+                              const int32_t* sel, const int32_t* d_count, int32_t capacity, int32_t k,
+                              int32_t in_stride, int32_t length, const int64_t* gids,
+                              int64_t id_offset, uint64_t* cand, void* stream) {
+  if (capacity <= 0) return LCP_OK;
+  if (k < 1 || in_stride < 1) return fail(LCP_ERR_INVALID_INPUT, "k and in_stride must be >= 1");
+  k_encode_sel<<<blocks_for((long long)capacity * k, 256), 256, 0, (cudaStream_t)stream>>>(
+      ids, lcps, hits, sel, d_count, capacity, k, in_stride, length,
+      reinterpret_cast<const long long*>(gids), id_offset, reinterpret_cast<u64*>(cand));
+  LCP_CK_LAUNCH();
+  return LCP_OK;
 }
 
 int lcp_pinned_alloc(int64_t bytes, void** out) {

@@ -522,6 +522,7 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, MODE == 2 ? 1 : 2)
   const bool has0 = lane < L, has1 = lane + 32 < L;
   const int sh0 = 64 - b * (lane + 1), sh1 = 64 - b * (lane + 33);
 
+  if (ix.dcount) count = min(count, *ix.dcount);  // device-resident batch size (lcp_query_counted)
   for (int qi = blockIdx.x * warps + warp; qi < count; qi += gridDim.x * warps) {
     LCP_STAMP(qi, 0);
     const uint16_t* qrow = queries + (size_t)qi * L;
@@ -893,6 +894,7 @@ __global__ void __launch_bounds__(NS > 2 ? QW_MAX_THREADS / 2 : QW_MAX_THREADS, 
   const bool has0 = lane < L, has1 = lane + 32 < L;
   const int sh0 = 64 - b * (lane + 1), sh1 = 64 - b * (lane + 33);
 
+  if (ix.dcount) count = min(count, *ix.dcount);  // device-resident batch size (lcp_query_counted)
   for (int qi = blockIdx.x * warps + warp; qi < count; qi += gridDim.x * warps) {
     const uint16_t* qrow = queries + (size_t)qi * L;
     const u32 s0 = has0 ? qrow[lane] : 0u;
@@ -1100,6 +1102,7 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, 1)
   const bool complete = mode == 1;
 
   const int warps = blockDim.x >> 5;
+  if (ix.dcount) count = min(count, *ix.dcount);  // device-resident batch size (lcp_query_counted)
   for (long long qi = (long long)blockIdx.x * warps + warp; qi < count;
        qi += (long long)gridDim.x * warps) {
     u64 qk[WMAX];
@@ -1243,6 +1246,7 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, 1)
   const long long n = ix.n;
   const int L = ix.L;
   const int depth = ix.tal_depth;
+  if (ix.dcount) count = min(count, *ix.dcount);  // device-resident batch size (lcp_query_counted)
   for (long long qi = (long long)blockIdx.x * warps + warp; qi < count;
        qi += (long long)gridDim.x * warps) {
     u64 qk[WMAX];
@@ -1353,6 +1357,7 @@ __global__ void __launch_bounds__(NS > 2 ? QW_MAX_THREADS / 2 : QW_MAX_THREADS, 
   u64* scb = reinterpret_cast<u64*>(smem_raw + 16 + (size_t)ix.smem_entries * 8) +
              warp * (32 * NS);
 
+  if (ix.dcount) count = min(count, *ix.dcount);  // device-resident batch size (lcp_query_counted)
   for (long long qi = (long long)blockIdx.x * warps + warp; qi < count;
        qi += (long long)gridDim.x * warps) {
     u64 qk[WMAX];
@@ -1701,6 +1706,7 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, 1)
   const long long n = ix.n;
   const int L = ix.L;
   const bool complete = mode == 1;
+  if (ix.dcount) count = min(count, *ix.dcount);  // device-resident batch size (lcp_query_counted)
   for (long long qi = (long long)blockIdx.x * warps + warp; qi < count;
        qi += (long long)gridDim.x * warps) {
     const u64* q = qkeys + qi * ix.W;
@@ -1795,6 +1801,7 @@ __global__ void __launch_bounds__(NS > 2 ? QW_MAX_THREADS / 2 : QW_MAX_THREADS, 
   const int L = ix.L;
   const bool complete = mode == 1;
   u64* scb = reinterpret_cast<u64*>(smem_raw) + warp * (32 * NS);
+  if (ix.dcount) count = min(count, *ix.dcount);  // device-resident batch size (lcp_query_counted)
   for (long long qi = (long long)blockIdx.x * warps + warp; qi < count;
        qi += (long long)gridDim.x * warps) {
     const u64* q = qkeys + qi * ix.W;
@@ -1938,6 +1945,7 @@ __global__ void __launch_bounds__(GEN_THREADS)
   const int L = ix.L;
   const int lane = lane_id(), warp = threadIdx.x >> 5;
 
+  if (ix.dcount) count = min(count, *ix.dcount);  // device-resident batch size (lcp_query_counted)
   for (long long qi = blockIdx.x; qi < count; qi += gridDim.x) {
     const u64* q = qkeys + qi * ix.W;
     // strict / complete with need <= GEN_CAP / 2: CTA-cooperative setup.

@@ -117,14 +117,35 @@ class _Collectives:
         return out.to(t.device)
 
 
+def pack_keys_host(rows: np.ndarray, length: int, sigma: int) -> np.ndarray:
+    """(m, L) symbols -> (m, W) uint64 packed keys in the extension's encoding
+    (common.cuh: b = ceil(log2 sigma) rounded up to a power of two, 64/b
+    symbols per word, most significant first).  Setup-time helper for the
+    few rows routing needs on the device (splitters, shard boundaries)."""
+    need = max(1, int(np.ceil(np.log2(sigma))))
+    b = 1
+    while b < need:
+        b <<= 1
+    spw = 64 // b
+    words = (length + spw - 1) // spw
+    rows = np.asarray(rows, dtype=np.uint64).reshape(-1, length)
+    out = np.zeros((rows.shape[0], words), dtype=np.uint64)
+    for j in range(length):
+        out[:, j // spw] |= rows[:, j] << np.uint64(64 - b * (j % spw + 1))
+    return out
+
+
 class GpuEngine:
-    """Local top-k on this rank's range: the CUDA index (NativeIndex)."""
+    """Local top-k on this rank's range: the CUDA index (NativeIndex; an empty
+    range still gets an n = 0 index, which the device routing needs for the
+    key encoding)."""
 
     def __init__(self, rows: np.ndarray, length: int, sigma: int):
         from .engine import NativeIndex
 
         self.length, self.n = int(length), int(rows.shape[0])
-        self.native = NativeIndex(rows, length, sigma) if self.n else None
+        self.sigma = int(sigma)
+        self.native = NativeIndex(rows, length, sigma)
         self.device = "cuda"
 
     def first_last_rows(self) -> np.ndarray:
@@ -293,3 +314,142 @@ class RangeShardedIndex:
         self._answer(q, mine, kk, mode, cand)
         gathered = self.coll.all_gather(cand)
         return self.engine.merge(gathered, take, mode == "strict")
+
+    # --------------------------------------------------- device-routed step
+    # The same protocol as query(), with no host round trip: routing, the
+    # consult rule and the compactions run as kernels (shard_kernels.cuh) and
+    # the exchanges as NCCL collectives on the current stream, so the whole
+    # step can be captured in a CUDA graph.
+    def _device_state(self):
+        import torch
+
+        if getattr(self, "_dev", None) is None:
+            if not isinstance(self.engine, GpuEngine):
+                raise InvalidInputError("query_device needs the CUDA engine (GpuEngine)")
+            L, sigma = self.length, self.sigma
+            spl = pack_keys_host(self.splitters.cpu().numpy(), L, sigma)
+            first = pack_keys_host(self.first.cpu().numpy(), L, sigma)
+            last = pack_keys_host(self.last.cpu().numpy(), L, sigma)
+            dev = torch.device("cuda", torch.cuda.current_device())
+            as_dev = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).to(dev)
+            self._dev = dict(
+                splitters=as_dev(spl), first=as_dev(first), last=as_dev(last),
+                nonempty=self.nonempty.to(torch.int32).to(dev),
+                gids=self.gids.to(torch.int64).to(dev),
+                bufs={})
+        return self._dev
+
+    def _step_buffers(self, count: int, kk: int):
+        import torch
+
+        st = self._device_state()
+        key = (count, kk)
+        if key not in st["bufs"]:
+            dev = st["splitters"].device
+            L = self.length
+            ls = max(1, min(kk, max(1, self.n_local)))
+            mk = lambda *shape, dt: torch.zeros(shape, dtype=dt, device=dev)
+            st["bufs"][key] = dict(
+                rows=mk(count, L, dt=torch.int16), sel=mk(count, dt=torch.int32),
+                cnt=mk(2, dt=torch.int32), ids=mk(count, ls, dt=torch.int32),
+                lcps=mk(count, ls, dt=torch.int16), hits=mk(count, dt=torch.int32),
+                md=mk(count, dt=torch.int16), tq=mk(count, dt=torch.int32),
+                cand=mk(count, kk, dt=torch.int64),
+                gathered=mk(self.world, count, kk, dt=torch.int64),
+                ws=None)
+        return st["bufs"][key]
+
+    def query_device(self, queries, k: int, mode: str = "complete", out=None):
+        """Global top-k of a broadcast (count, L) uint16 CUDA batch, on the
+        current stream, without synchronising the host.  Returns (or fills)
+        (ids int32 (count, max(1, take)), lcps int16, hits int32)."""
+        import torch
+
+        from . import _native
+        from ._native import Workspace, check, load
+
+        if mode not in ("complete", "strict"):
+            raise InvalidInputError(f"sharded mode must be 'strict' or 'complete', got {mode!r}")
+        if k < 1:
+            raise InvalidInputError(f"k must be >= 1, got {k}")
+        take = max(0, min(int(k), self.n_total))
+        if take * self.world > 8192:
+            raise InvalidInputError("sharded merge supports world * min(k, n) <= 8192")
+        st = self._device_state()
+        count, L = int(queries.shape[0]), self.length
+        kk = max(1, take)
+        b = self._step_buffers(count, kk)
+        if b["ws"] is None:
+            b["ws"] = Workspace()
+        ws = b["ws"]
+        lib = load()
+        stream = torch.cuda.current_stream().cuda_stream
+        native = self.engine.native
+        q = queries.contiguous()
+        ls = int(b["ids"].shape[1])
+        strict = 1 if mode == "strict" else 0
+        need = take if mode == "complete" else kk
+        expected = max(1, (count + self.world - 1) // self.world * 5 // 4)
+        b["tq"].fill_(-1)
+        b["cand"].fill_(-1)  # UINT64_MAX: no candidate
+        cnt_own, cnt_con = b["cnt"][0:1], b["cnt"][1:2]
+
+        def answer(cnt, exp):
+            check(lib.lcp_query_counted(native.handle, ws.handle, b["rows"].data_ptr(), count,
+                                        cnt.data_ptr(), exp, kk, _native.MODE_CODES[mode], ls,
+                                        b["ids"].data_ptr(), b["lcps"].data_ptr(),
+                                        b["hits"].data_ptr(), b["md"].data_ptr(), None, stream))
+
+        def encode(cnt):
+            check(lib.lcp_encode_candidates_sel(
+                b["ids"].data_ptr(), b["lcps"].data_ptr(), b["hits"].data_ptr(), b["sel"].data_ptr(),
+                cnt.data_ptr(), count, kk, ls, L, st["gids"].data_ptr(), 0, b["cand"].data_ptr(), stream))
+
+        # 1. the queries this rank owns: answer, threshold, candidates
+        check(lib.lcp_route_queries(native.handle, ws.handle, q.data_ptr(), count,
+                                    st["splitters"].data_ptr(), self.world - 1, None, None, None,
+                                    self.rank, None, b["rows"].data_ptr(), b["sel"].data_ptr(),
+                                    cnt_own.data_ptr(), stream))
+        answer(cnt_own, expected)
+        check(lib.lcp_shard_thresholds(b["lcps"].data_ptr(), b["hits"].data_ptr(), b["md"].data_ptr(),
+                                       b["sel"].data_ptr(), cnt_own.data_ptr(), count, ls, need, strict,
+                                       b["tq"].data_ptr(), stream))
+        encode(cnt_own)
+        # 2. thresholds of every query from its owner (one int per query)
+        self._all_reduce_max_(b["tq"])
+        # 3. the queries other ranks own whose answer may reach into this range
+        check(lib.lcp_route_queries(native.handle, ws.handle, q.data_ptr(), count,
+                                    st["splitters"].data_ptr(), self.world - 1, st["first"].data_ptr(),
+                                    st["last"].data_ptr(), st["nonempty"].data_ptr(), self.rank,
+                                    b["tq"].data_ptr(), b["rows"].data_ptr(), b["sel"].data_ptr(),
+                                    cnt_con.data_ptr(), stream))
+        answer(cnt_con, max(1, count // 16))
+        encode(cnt_con)
+        # 4. candidates of every rank, merged
+        self._all_gather_into_(b["gathered"], b["cand"])
+        if out is None:
+            out = (torch.empty((count, kk), dtype=torch.int32, device=q.device),
+                   torch.empty((count, kk), dtype=torch.int16, device=q.device),
+                   torch.empty(count, dtype=torch.int32, device=q.device))
+        ids, lcps, hits = out
+        check(lib.lcp_merge_candidates(b["gathered"].data_ptr(), self.world, count, kk, take, L, strict,
+                                       ids.data_ptr(), lcps.data_ptr(), hits.data_ptr(), stream))
+        return ids, lcps, hits
+
+    def _all_reduce_max_(self, t) -> None:
+        c = self.coll
+        if c.nccl:
+            c.dist.all_reduce(t, op=c.dist.ReduceOp.MAX, group=c.group)
+        else:  # gloo (multi-process tests on one GPU): host staging, not capturable
+            h = t.cpu()
+            c.dist.all_reduce(h, op=c.dist.ReduceOp.MAX, group=c.group)
+            t.copy_(h)
+
+    def _all_gather_into_(self, out, t) -> None:
+        c = self.coll
+        if c.nccl:
+            c.dist.all_gather_into_tensor(out, t, group=c.group)
+        else:
+            h = out.cpu()
+            c.dist.all_gather(list(h.unbind(0)), t.cpu(), group=c.group)
+            out.copy_(h)

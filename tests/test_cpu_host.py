@@ -181,3 +181,15 @@ def test_dataset_file_round_trip(tmp_path):
     path.write_bytes(b"NOPE" + path.read_bytes()[4:])
     with pytest.raises(InvalidInputError):
         storage.read_dataset(str(path))
+
+
+def test_row_block_generator_matches_full_dataset():
+    """datagen.generate_row_block == slices of generate_dataset (config-5 shards)."""
+    from paper_2602_04936_b200.datagen import generate_dataset, generate_row_block
+
+    for n, L, sigma, seed in ((1000, 32, 4, 6), (777, 16, 2, 3), (512, 8, 256, 1), (300, 24, 65536, 9)):
+        full = generate_dataset(n, L, sigma, seed=seed).items
+        step = 16 // np.gcd(16, L)
+        for lo in range(0, n, max(step, n // 7 // step * step)):
+            hi = min(n, lo + 123)
+            assert np.array_equal(generate_row_block(n, L, sigma, seed, lo, hi), full[lo:hi]), (n, L, lo)

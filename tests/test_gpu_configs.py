@@ -223,3 +223,31 @@ def test_config5_200m_sharded(gpu):
     oi, ol, oh = _composed_oracle(ds.items, qs[sample], k, shards)
     sub = type(b)(ids=b.ids[sample], lcps=b.lcps[sample], hits=b.hits[sample])
     assert_rows(sub, oi, ol, oh, "config5 sample")
+
+
+@pytest.mark.parametrize("n,L,sigma", [(2_000_000, 32, 4), (300_000, 32, 65536), (100_000, 24, 4),
+                                       (50_000, 16, 2), (37, 12, 3)])
+def test_fullscan_small_batches(gpu, n, L, sigma):
+    """The small-batch streaming scan (count <= 8: every lane holds every
+    query; one launch incl. the cross-CTA merge) equals the oracle's
+    oracle_top_k (oracle.py:38-59) for 1..8 queries, k up to 32, both
+    composite widths; also through the single-query oracle_top_k API."""
+    import os as _os
+
+    orc = _oracle()
+    ds = lg.generate_dataset(n, L, sigma, seed=21)
+    qs = np.vstack([lg.generate_queries(ds, 4, seed=22), lg.generate_queries(ds, 4, seed=23, prefix_len=L // 2)])
+    for wide in ("0", "1"):
+        _os.environ["LCP_FORCE_WIDE_COMPOSITE"] = wide
+        try:
+            index = lg.build(ds)
+        finally:
+            _os.environ.pop("LCP_FORCE_WIDE_COMPOSITE", None)
+        for count in (1, 2, 3, 5, 8):
+            for k in (1, 10, 32):
+                f = index.fullscan_batch(qs[:count], k)
+                oid, olcp, oh = orc.oracle_top_k_batch(ds.items, qs[:count], k, nthreads=THREADS)
+                assert_rows(f, oid, olcp, oh, f"smallq n={n} count={count} k={k} wide={wide}")
+        r = lg.oracle_top_k(ds, qs[5], 10)
+        oid, olcp = orc.oracle_top_k(ds.items, qs[5], 10)
+        assert r.pairs() == list(zip(oid.tolist(), olcp.tolist()))

@@ -526,12 +526,32 @@ def _range_gpu_worker(rank, world, port, backend):
             dq = torch.from_numpy(qs).cuda()
             for k in (1, 10, 32, 50):
                 for mode in ("complete", "strict"):
-                    ids, lcps, hits = (t.cpu() for t in sh.query(dq, k, mode))
                     fids, flcps, fhits, _, _, _ = full.query_batch(qs, k, mode)
-                    for i in range(len(qs)):
-                        h = int(hits[i])
-                        assert list(zip(ids[i, :h].tolist(), lcps[i, :h].tolist())) == \
-                            list(zip(fids[i, :fhits[i]].tolist(), flcps[i, :fhits[i]].tolist())), (n, k, mode, i)
+                    # host-bookkeeping protocol and the device-routed step
+                    for ids, lcps, hits in (sh.query(dq, k, mode), sh.query_device(dq, k, mode)):
+                        ids, lcps, hits = ids.cpu().long() & 0xFFFFFFFF, lcps.cpu().long() & 0xFFFF, hits.cpu()
+                        for i in range(len(qs)):
+                            h = int(hits[i])
+                            assert list(zip(ids[i, :h].tolist(), lcps[i, :h].tolist())) == \
+                                list(zip(fids[i, :fhits[i]].tolist(), flcps[i, :fhits[i]].tolist())), (n, k, mode, i)
+            if backend == "nccl":
+                # the device-routed step has no host round trip: capture it once
+                # in a CUDA graph and replay it
+                s = torch.cuda.Stream()
+                s.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(s):
+                    ref = [t.clone() for t in sh.query_device(dq, 10, "complete")]
+                    out = tuple(torch.empty_like(t) for t in ref)
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, stream=s):
+                        sh.query_device(dq, 10, "complete", out=out)
+                    for t in out:
+                        t.zero_()
+                    g.replay()
+                    g.replay()
+                torch.cuda.synchronize()
+                for a, b in zip(ref, out):
+                    assert torch.equal(a, b)
     finally:
         dist.destroy_process_group()
 
