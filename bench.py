@@ -15,14 +15,15 @@ events on the capture stream.  The same loop on one stream (one batch in
 flight) is reported beside it, and its per-step time is the kernel duration
 used for the roofline.
 
-N>1 (torchrun): query-partitioned serving.  Every rank holds the full
-config-3 index (24 MB; it fits every GPU many times over) and runs the N=1
-step on its own query stream, so there is no data-path collective (SURVEY
-§8e "query-partitioned replicas"); barrier + synchronize bracket the timed
-region and the time is the max over ranks.  value = all ranks' queries/s.
-The north-star corpus sharding (row-block shards of 2M rows per rank, query
-batch broadcast, local top-k -> encode -> NCCL all_gather -> merge kernel)
-is timed beside it as "rowblock_sharded".
+N>1 (torchrun): BASELINE config 5, the north-star scheme (config5_leg):
+the 200M-row corpus is split into row blocks that each rank draws itself,
+re-split by lexicographic range; every step all-gathers the ranks' 4096-query
+client batches, routes each query on the device to the shard owning its key
+range (plus the neighbours its top-k may spill into), answers locally,
+exchanges candidates with NCCL and merges them on the device.  The whole step
+is captured in a CUDA graph; time = max over ranks, value = all ranks'
+client queries/s ("scaling": "weak": 4096 queries per rank per step).  The
+row-block scheme and query-partitioned config-3 replicas are side fields.
 
 ``--impl reference`` times the reference's own algorithm on the host CPU
 (the pinned C restatement in oracle/, all host threads) on the same config.
@@ -467,10 +468,20 @@ def main() -> None:
     }
     line["e2e"] = e2e_leg(idx, qs, args, world, barrier, max_over_ranks)
     if world > 1:
-        line["rowblock_sharded"] = rowblock_leg(lg, args, world, rank, dev, main_stream, barrier,
-                                                max_over_ranks)
-        line["range_sharded"] = range_leg(lg, args, world, rank, dev, main_stream, barrier,
-                                          max_over_ranks)
+        # N > 1: the headline is BASELINE config 5 on the north-star scheme
+        # (corpus sharded by lexicographic range, device routing, NCCL
+        # exchanges, merge kernel); config-3 replicas stay as a side field
+        del replicas, idx
+        torch.cuda.empty_cache()
+        c5 = config5_leg(args, world, rank, dev, barrier, max_over_ranks, "range")
+        line["replicas"] = {k: line[k] for k in ("value", "ms_per_step", "one_batch_in_flight", "e2e")}
+        line["replicas"]["parallelism"] = line["config"]["parallelism"]
+        line["value"], line["ms_per_step"] = c5["value"], c5["ms_per_step"]
+        line["e2e"] = c5.pop("e2e")
+        line["config"] = config5_dict(world)
+        line["sharded"] = c5
+        line["gpu_launches"] = c5["steps"] * SHARD_LAUNCHES_PER_STEP
+        line["rowblock_sharded"] = config5_leg(args, world, rank, dev, barrier, max_over_ranks, "rowblock")
     if world == 1 and rank == 0:
         line["p50_batch_latency_ms"] = cold_batch_latency(idx, dq, dev)
         cpu_qps, cpu_done, cpu_el, trie = cpu_reference(ds, qs, K, args.cpu_budget_s, os.cpu_count() or 1)
@@ -491,79 +502,168 @@ def main() -> None:
         if not args.no_extras:
             flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
             line["extras"] = extras(idx, ds, qs, main_stream, flush_buf)
+            del flush_buf, replicas
+            torch.cuda.empty_cache()
+            # config 5 on one GPU through the same sharded step the N > 1 runs
+            # time (one range shard, local exchange): the N = 1 point of the
+            # config-5 scaling curve
+            line["extras"]["config5_single_gpu"] = config5_leg(args, 1, 0, dev, barrier, max_over_ranks, "range")
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
-def rowblock_leg(lg, args, world, rank, dev, stream, barrier, max_over_ranks) -> dict:
-    """North-star corpus sharding: rank g holds rows generate_dataset(2M, seed=3+g)
-    with ids offset by 2M*g; every query batch is answered by every shard
-    (local top-k -> encode -> NCCL all_gather -> merge kernel).  value =
-    queries/s over the whole 2M*world corpus."""
+C5_ITEMS = int(os.environ.get("LCP_BENCH_C5_ITEMS", 200_000_000))  # BASELINE config 5 (override: functional checks only)
+# our kernels per range-sharded step: pack + route (own), counted query,
+# thresholds, encode, pack + route (consult), counted query, encode, merge
+SHARD_LAUNCHES_PER_STEP = 10
+
+
+def config5_dict(world: int) -> dict:
+    return {"workload": "config 5: corpus sharded by lexicographic range over the ranks, "
+                        "complete-mode top-k of each rank's 4096-query client batches",
+            "n_items": C5_ITEMS, "seq_len": SEQ_LEN, "alphabet": SIGMA, "k": K, "batch": BATCH * world,
+            "batch_per_rank": BATCH, "mode": "complete",
+            "l2": "inputs larger than L2: the 200M-row index (about 7 GB over the ranks)",
+            "launch": "CUDA graph replay of the whole sharded step, NCCL collectives inside",
+            "parallelism": f"range shards x{world} (north star, SURVEY §8e)"}
+
+
+def config5_leg(args, world, rank, dev, barrier, max_over_ranks, scheme: str = "range",
+                n_total: int = C5_ITEMS) -> dict:
+    """BASELINE config 5 (N=200M, L=32, sigma=4, k=10), the north-star
+    multi-GPU path: the corpus is split into row blocks over the ranks (each
+    rank draws its own block with datagen.generate_row_block, byte-identical
+    to slicing generate_dataset(200M, 32, 4, seed=6)), then
+      scheme "range": re-split by lexicographic range (RangeShardedIndex):
+          a step all-gathers the ranks' 4096-query client batches, routes every
+          query to the shard owning its key range on the device, answers,
+          exchanges owner thresholds (all_reduce), lets neighbouring ranges
+          answer where the top-k may spill over, and all-to-alls the
+          candidates back to the client's rank for the merge kernel;
+      scheme "rowblock": every rank answers the whole gathered batch on its
+          row block, candidates all-to-all to the client's rank, merge.
+    Every step is graph-captured (NCCL collectives inside the graph) and
+    replayed; no host synchronisation inside the timed region.  value = all
+    ranks' client queries / max-over-ranks device time.  world = 1 runs the
+    same code path on one GPU (local exchange)."""
     import torch
+    import torch.distributed as dist
 
-    from paper_2602_04936_b200.sharded import ShardedIndex
+    from paper_2602_04936_b200.core import Alphabet, Dataset
+    from paper_2602_04936_b200.datagen import generate_queries, generate_row_block
+    from paper_2602_04936_b200.sharded import RowBlockShardStep, ShardPlan
 
-    ds = lg.generate_dataset(N_ITEMS, SEQ_LEN, SIGMA, seed=3 + rank)
-    qs = lg.generate_queries(ds, BATCH * 8, seed=4)  # identical on every rank (broadcast)
+    lo, hi = ShardPlan(n_total, world).bounds(rank)
+    t0 = time.perf_counter()
+    rows = generate_row_block(n_total, SEQ_LEN, SIGMA, 6, lo, hi)
+    gen_s = time.perf_counter() - t0
+    n_pool = 8  # each rank's own client stream: uniform queries (generate_queries, seed 4 + 1000*rank)
+    qs = generate_queries(Dataset(alphabet=Alphabet(SIGMA), length=SEQ_LEN, items=rows[:1]),
+                          BATCH * n_pool, seed=4 + 1000 * rank)
+    barrier()
+    t0 = time.perf_counter()
+    if scheme == "range":
+        from paper_2602_04936_b200.rangeshard import RangeShardedIndex
+
+        sh = RangeShardedIndex(rows, SEQ_LEN, SIGMA, id_offset=lo)
+        n_local = sh.n_local
+    else:
+        sh = RowBlockShardStep(rows, SEQ_LEN, SIGMA, id_offset=lo, n_total=n_total)
+        n_local = sh.native.n
+    del rows
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    stream = torch.cuda.Stream(device=dev)
     with torch.cuda.stream(stream):
-        sh = ShardedIndex(ds.items, SEQ_LEN, SIGMA, id_offset=N_ITEMS * rank)
-        dq = torch.from_numpy(qs).to(dev).view(8, BATCH, SEQ_LEN)
-        ids = torch.empty((BATCH, K), dtype=torch.int32, device=dev)
-        lcps = torch.empty((BATCH, K), dtype=torch.int16, device=dev)
-        hits = torch.empty(BATCH, dtype=torch.int32, device=dev)
-        steps = min(args.steps, 1000)
-        for i in range(max(args.warmup, 20)):
-            sh.query_device(dq[i % 8], K, ids, lcps, hits)
+        pool = torch.from_numpy(qs).to(dev).view(n_pool, BATCH, SEQ_LEN)
+        gq = torch.empty((world * BATCH, SEQ_LEN), dtype=torch.uint16, device=dev)
+        out = (torch.empty((BATCH, K), dtype=torch.int32, device=dev),
+               torch.empty((BATCH, K), dtype=torch.int16, device=dev),
+               torch.empty(BATCH, dtype=torch.int32, device=dev))
+
+        nccl = world > 1 and dist.get_backend() == "nccl"
+
+        # the uint16 rows travel as int32 pairs (NCCL and gloo have no 16-bit integer type)
+        def step(i):
+            src = pool[i % n_pool].view(torch.int32)
+            if nccl:
+                dist.all_gather_into_tensor(gq.view(torch.int32), src)
+            elif world > 1:  # gloo (LCP_BENCH_SHARE_GPU functional check): host staging
+                h = torch.empty((world, BATCH, SEQ_LEN // 2), dtype=torch.int32)
+                dist.all_gather(list(h.unbind(0)), src.cpu())
+                gq.view(torch.int32).copy_(h.view(-1, SEQ_LEN // 2))
+            else:
+                gq.copy_(pool[i % n_pool])
+            sh.query_device(gq, K, "complete", out=out, exchange="all_to_all")
+
+        for i in range(3):  # eager warm-up (allocates the step buffers)
+            step(i)
+        torch.cuda.synchronize()
+        G = min(64, max(8, args.steps))
+        launch = "CUDA graph replay (NCCL collectives captured)"
+        try:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                for i in range(G):
+                    step(i)
+            run = lambda: g.replay()
+            per_run = G
+        except Exception as e:  # capture unsupported here: eager, still no host sync
+            torch.cuda.synchronize()
+            launch = f"eager stream-ordered launches (graph capture failed: {type(e).__name__})"
+            run = lambda: [step(i) for i in range(G)]
+            per_run = G
+        reps = max(1, (args.steps + per_run - 1) // per_run)
+        for _ in range(max(1, args.warmup // per_run + 1)):
+            run()
         barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        for i in range(steps):
-            sh.query_device(dq[i % 8], K, ids, lcps, hits)
+        for _ in range(reps):
+            run()
         b.record(stream)
         torch.cuda.synchronize()
-        barrier()
         ms = max_over_ranks(a.elapsed_time(b))
-    return {"value": BATCH * steps / (ms / 1e3), "unit": "queries/s", "steps": steps,
-            "ms_per_step": ms / steps, "n_items_total": N_ITEMS * world,
-            "parallelism": f"row-block shards x{world} (2M rows each) + NCCL all_gather + k_merge",
-            "launch": "host loop: local query -> encode -> all_gather -> merge per step"}
-
-
-def range_leg(lg, args, world, rank, dev, stream, barrier, max_over_ranks) -> dict:
-    """Lexicographic range shards (rangeshard.py): 2M rows per rank, re-split
-    by key range; a broadcast batch of world*4096 queries per step, each rank
-    answering the ~4096 it owns (+ consulted neighbours), consult flags by
-    all_reduce, candidates by all_gather, merge kernel.  value = queries/s."""
-    import torch
-
-    from paper_2602_04936_b200.rangeshard import RangeShardedIndex
-
-    ds = lg.generate_dataset(N_ITEMS, SEQ_LEN, SIGMA, seed=3 + rank)
-    qs = lg.generate_queries(ds, BATCH * world * 4, seed=4)  # identical on every rank (broadcast)
-    with torch.cuda.stream(stream):
-        sh = RangeShardedIndex(ds.items, SEQ_LEN, SIGMA, id_offset=N_ITEMS * rank)
-        dq = torch.from_numpy(qs).to(dev).view(4, BATCH * world, SEQ_LEN)
-        steps = min(args.steps, 200)
-        for i in range(max(args.warmup, 10)):
-            sh.query(dq[i % 4], K, "complete")
         barrier()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for i in range(steps):
-            sh.query(dq[i % 4], K, "complete")
-        b.record(stream)
+        # end to end: each step copies the rank's pinned client batch in and
+        # its merged answers out (wall clock, max over ranks)
+        from paper_2602_04936_b200._native import PinnedArray
+
+        pin_q = PinnedArray((n_pool, BATCH, SEQ_LEN), np.uint16)
+        pin_q.array[:] = qs.reshape(n_pool, BATCH, SEQ_LEN)
+        host_q = torch.from_numpy(pin_q.array)
+        host_out = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in out]
+        e_steps = min(max(args.steps, 100), 400)
+        for i in range(3):
+            pool[i % n_pool].copy_(host_q[i % n_pool], non_blocking=True)
+            step(i)
         torch.cuda.synchronize()
         barrier()
-        ms = max_over_ranks(a.elapsed_time(b))
-    return {"value": BATCH * world * steps / (ms / 1e3), "unit": "queries/s", "steps": steps,
-            "ms_per_step": ms / steps, "n_items_total": N_ITEMS * world, "n_items_local": sh.n_local,
-            "batch_broadcast": BATCH * world,
-            "parallelism": f"lexicographic range shards x{world} + routed queries (consult rule) "
-                           "+ all_reduce + all_gather + k_merge",
-            "launch": "host loop (routing bookkeeping syncs the host each step)"}
+        t_e = time.perf_counter()
+        for i in range(e_steps):
+            pool[i % n_pool].copy_(host_q[i % n_pool], non_blocking=True)
+            step(i)
+            for h, d in zip(host_out, out):
+                h.copy_(d, non_blocking=True)
+            stream.synchronize()
+        e_el = max_over_ranks(time.perf_counter() - t_e)
+        barrier()
+    steps = reps * per_run
+    e2e = {"value": world * BATCH * e_steps / e_el, "unit": "queries/s", "steps": e_steps,
+           "ms_per_step": 1e3 * e_el / e_steps, "h2d_bytes_per_step": BATCH * SEQ_LEN * 2,
+           "d2h_bytes_per_step": int(sum(t.numel() * t.element_size() for t in out)),
+           "api": f"{type(sh).__name__}.query_device per step, pinned client batch in / answers out, "
+                  "one step in flight, wall clock"}
+    return {"value": world * BATCH * steps / (ms / 1e3), "unit": "queries/s", "steps": steps, "e2e": e2e,
+            "ms_per_step": ms / steps, "n_items_total": n_total, "n_items_local": int(n_local),
+            "scheme": scheme, "batch_per_rank": BATCH, "launch": launch,
+            "gen_s": round(gen_s, 2), "build_s": round(build_s, 2),
+            "parallelism": (f"{scheme} shards x{world}: all_gather client batches, device routing, "
+                            "local top-k, NCCL exchange, k_merge" if scheme == "range" else
+                            f"row-block shards x{world}: all_gather client batches, every shard answers, "
+                            "all_to_all candidates, k_merge")}
 
 
 def cold_batch_latency(idx, dq, dev) -> float:

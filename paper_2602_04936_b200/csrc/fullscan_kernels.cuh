@@ -75,17 +75,9 @@ __global__ void __launch_bounds__(FS_THREADS)
   const long long qi = (long long)blockIdx.x * FS_THREADS + threadIdx.x;
   const bool active = qi < count;
 
-  u64 q0 = 0;
-  if (active) {
-    const uint16_t* qrow = queries + qi * L;
-    bool bad = false;
-    for (int j = 0; j < L; ++j) {
-      const u32 s = qrow[j];
-      bad |= (int)s >= ix.sigma;
-      if (j < ix.spw) q0 |= (u64)s << (64 - ix.b * (j + 1));
-    }
-    if (bad && blockIdx.y == 0) atomicOr(err, 1);
-  }
+  // the batch was packed by the streaming pack kernel (coalesced row reads,
+  // symbol check): one 8-byte load per query here
+  const u64 q0 = active ? qkeys[qi * ix.W] : 0ull;
   const u32 qh = (u32)(q0 >> 32), ql = (u32)q0;
   const int W = ix.W;
 
@@ -210,11 +202,12 @@ __global__ void __launch_bounds__(FS_THREADS)
     if (threadIdx.x == 0 && s + 2 < nst) issue(s + 2);
   }
 
+  // chunk-major, query-fastest layout: adjacent threads store adjacent words
   if (active) {
-    u64* out = partial + (qi * nchunks + blockIdx.y) * (long long)need;
+    u64* out = partial + (long long)blockIdx.y * need * count + qi;
 #pragma unroll
     for (int j = 0; j < KCAP; ++j)
-      if (j < need) out[j] = widen_comp<C>(list[j], idbits);
+      if (j < need) out[(long long)j * count] = widen_comp<C>(list[j], idbits);
   }
 }
 
@@ -245,6 +238,9 @@ constexpr int FSQ_STEP = 1024;  // segment granularity (keys); >= one warp step 
 // 16-byte hi-plane loads per lane per step: fewer with more queries (registers)
 template <int Q>
 __host__ __device__ constexpr int fsq_unroll() { return Q <= 2 ? 8 : (Q <= 4 ? 4 : 2); }
+// resident CTAs per SM (one query fits 64 registers: two CTAs, 32 warps)
+template <int Q>
+__host__ __device__ constexpr int fsq_ctas_per_sm() { return Q == 1 ? 2 : 1; }
 
 // merge the sorted 32-slot warp lists buf[0..n) (one per 32 entries) into
 // buf[0]: a tree over the CTA's warps, `groups` independent trees side by side
@@ -264,8 +260,32 @@ __device__ void cta_tree_merge(C* buf, int n, int groups) {
   }
 }
 
+// exact composite of key i against query q (first word from the hi / lo
+// planes, further words for W > 1), or all-ones if its lcp is below the bound
+template <typename C>
+__device__ __noinline__ C fsq_candidate(const u32* __restrict__ keys_hi, const u32* __restrict__ keys_lo,
+                                        const u64* __restrict__ keys_orig, int spw,
+                                        const u64* __restrict__ qkeys, int q, u32 qh, u32 ql, int a,
+                                        long long i, int L, int W, int lb, int idbits) {
+  const u64 x = ((u64)(__ldg(keys_hi + i) ^ qh) << 32) | (u64)(__ldg(keys_lo + i) ^ ql);
+  int l = x ? (__clzll((long long)x) >> lb) : L;
+  if (!x && W > 1) {  // first word equal: finish on the remaining words
+    const u64* key = keys_orig + i * W;
+    const u64* qk = qkeys + (long long)q * W;
+    for (int w = 1; w < W; ++w) {
+      const u64 y = key[w] ^ qk[w];
+      if (y) {
+        l = w * spw + (__clzll((long long)y) >> lb);
+        break;
+      }
+    }
+  }
+  l = min(l, L);
+  return l >= a ? make_comp<C>(l, (u32)i, L, idbits) : ~C(0);
+}
+
 template <typename C, int Q>
-__global__ void __launch_bounds__(FSQ_THREADS, 1)
+__global__ void __launch_bounds__(FSQ_THREADS, fsq_ctas_per_sm<Q>())
     k_fullscan_smallq(DevIndex ix, const u64* __restrict__ qkeys, int count, int need, long long seg,
                       C* __restrict__ partial, int* __restrict__ hint, unsigned* __restrict__ done_ctr,
                       u32* __restrict__ out_ids, uint16_t* __restrict__ out_lcps,
@@ -303,8 +323,78 @@ __global__ void __launch_bounds__(FSQ_THREADS, 1)
   const long long gw = (long long)blockIdx.x * FSQ_WARPS + warp;
   const long long k0 = gw * seg;
   const long long k1 = min(n, k0 + seg);
+  if (k0 < k1) {
+    constexpr int US = 2;  // 256 keys: few registers beyond the main loop's
+    const long long base = k0;
+    uint4 h[US];
+#pragma unroll
+    for (int u = 0; u < US; ++u) h[u] = ld_stream16(ix.keys_hi + base + u * 128 + lane * 4);
+    // seed: the lists are empty, so every key of the first 256 is a candidate;
+    // read their lo words with vector loads and offer only the step's top
+    // lcp tier (the compact exact path below would re-read each key with its
+    // own round trip)
+      uint4 lo[US];
+#pragma unroll
+      for (int u = 0; u < US; ++u) lo[u] = ld_stream16(ix.keys_lo + base + u * 128 + lane * 4);
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        if (q >= count) continue;
+        // t* = the largest first-word lcp that at least `need` of the step's
+        // keys reach (binary search on warp-wide counts); only keys with
+        // lcp >= t* can be among the step's top-need, and they are few
+        const int T = min(L, ix.spw);
+        auto n_at_least = [&](int t) {
+          const int bits = t * b;
+          const u64 lim = bits >= 64 ? 0ull : (~0ull >> bits);
+          int c = 0;
+#pragma unroll
+          for (int u = 0; u < US; ++u) {
+            const u32 hh[4] = {h[u].x, h[u].y, h[u].z, h[u].w};
+            const u32 ll[4] = {lo[u].x, lo[u].y, lo[u].z, lo[u].w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const u64 x = ((u64)(hh[j] ^ qh[q]) << 32) | (u64)(ll[j] ^ ql[q]);
+              c += (base + u * 128 + lane * 4 + j < k1) && x <= lim;
+            }
+          }
+          return __reduce_add_sync(LCP_FULL_MASK, (unsigned)c);
+        };
+        int lo_t = 0, hi_t = T;  // count(0) >= need unless the step holds fewer keys
+        while (lo_t < hi_t) {
+          const int mid = (lo_t + hi_t + 1) >> 1;
+          if ((int)n_at_least(mid) >= need) lo_t = mid;
+          else hi_t = mid - 1;
+        }
+        const int bits = lo_t * b;
+        const u64 lim = bits >= 64 ? 0ull : (~0ull >> bits);
+#pragma unroll
+        for (int u = 0; u < US; ++u) {
+          const u32 hh[4] = {h[u].x, h[u].y, h[u].z, h[u].w};
+          const u32 ll[4] = {lo[u].x, lo[u].y, lo[u].z, lo[u].w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const long long i = base + u * 128 + lane * 4 + j;
+            const u64 x = ((u64)(hh[j] ^ qh[q]) << 32) | (u64)(ll[j] ^ ql[q]);
+            const bool pass = i < k1 && x <= lim;
+            if (!__any_sync(LCP_FULL_MASK, pass)) continue;
+            C c = ~C(0);
+            if (pass)
+              c = (!x && W > 1) ? fsq_candidate<C>(ix.keys_hi, ix.keys_lo, ix.keys_orig, ix.spw, qkeys, q,
+                                                   qh[q], ql[q], 0, i, L, W, lb, idbits)
+                                : make_comp<C>(x ? min(L, __clzll((long long)x) >> lb) : L, (u32)i, L, idbits);
+            warp_offer<C, true>(slot[q], thr[q], c, need);
+          }
+        }
+        if (thr[q] != ~C(0)) {
+          const int t = L - (int)(widen_comp<C>(thr[q], idbits) >> 32);
+          a_own[q] = t + 1;
+          if (lane == 0) atomicMax(hint + q, t);
+          if (a_own[q] > a[q]) set_bound(q, a_own[q]);
+        }
+      }
+  }
   int step = 0;
-  for (long long base = k0; base < k1; base += 128 * U, ++step) {
+  for (long long base = k0 + 256; base < k1; base += 128 * U, ++step) {
     if ((step & 1) == 0) {  // other warps' bounds (global hint)
       const int hv = lane < Q && lane < count ? *(volatile int*)(hint + lane) : 0;
 #pragma unroll
@@ -327,34 +417,32 @@ __global__ void __launch_bounds__(FSQ_THREADS, 1)
     }
     surv = __reduce_or_sync(LCP_FULL_MASK, surv);
     if (!surv) continue;
+    // exact path, compact on purpose (the unrolled form thrashed the
+    // instruction cache: ncu "no instruction" was the top stall): each lane
+    // marks its surviving key slots, then the warp offers one survivor per
+    // lane per round, re-reading its words (L2) by index
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       if (!((surv >> q) & 1)) continue;
+      u32 pm = 0;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const u32 hh[4] = {h[u].x, h[u].y, h[u].z, h[u].w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const long long i = base + u * 128 + lane * 4 + j;
-          C c = ~C(0);
-          if (i < k1 && (hh[j] ^ qh[q]) <= limh[q]) {  // rare: finish on the lo word
-            const u64 x = ((u64)(hh[j] ^ qh[q]) << 32) | (u64)(__ldg(ix.keys_lo + i) ^ ql[q]);
-            int l = x ? (__clzll((long long)x) >> lb) : L;
-            if (!x && W > 1) {  // first word equal: finish on the remaining words
-              const u64* key = ix.keys_orig + i * W;
-              const u64* qk = qkeys + (long long)q * W;
-              for (int w = 1; w < W; ++w) {
-                const u64 y = key[w] ^ qk[w];
-                if (y) {
-                  l = w * ix.spw + (__clzll((long long)y) >> lb);
-                  break;
-                }
-              }
-            }
-            if (l >= a[q]) c = make_comp<C>(min(l, L), (u32)i, L, idbits);
-          }
-          warp_offer<C, true>(slot[q], thr[q], c, need);
+        pm |= (u32)((h[u].x ^ qh[q]) <= limh[q]) << (4 * u);
+        pm |= (u32)((h[u].y ^ qh[q]) <= limh[q]) << (4 * u + 1);
+        pm |= (u32)((h[u].z ^ qh[q]) <= limh[q]) << (4 * u + 2);
+        pm |= (u32)((h[u].w ^ qh[q]) <= limh[q]) << (4 * u + 3);
+      }
+      while (__any_sync(LCP_FULL_MASK, pm != 0)) {
+        C c = ~C(0);
+        if (pm) {
+          const int sl = __ffs(pm) - 1;
+          pm &= pm - 1;
+          const long long i = base + (sl >> 2) * 128 + lane * 4 + (sl & 3);
+          if (i < k1)
+            c = fsq_candidate<C>(ix.keys_hi, ix.keys_lo, ix.keys_orig, ix.spw, qkeys, q, qh[q], ql[q],
+                                 a[q], i, L, W, lb, idbits);
         }
+        warp_offer<C, true>(slot[q], thr[q], c, need);
       }
       if (thr[q] != ~C(0)) {  // full: later keys of this segment have larger ids
         const int t = L - (int)(widen_comp<C>(thr[q], idbits) >> 32);
@@ -417,14 +505,14 @@ __global__ void __launch_bounds__(FSQ_THREADS, 1)
 
 // ---------------------------------------------------------------------------
 // merge: per query, the `take` smallest of `shards` candidate lists of `kin`
-// entries each (UINT64_MAX = empty).  cand index = s*s_stride + q*q_stride + j.
+// entries each (UINT64_MAX = empty).  cand index = s*s_stride + q*q_stride + j*j_stride.
 // strict: keep only candidates whose lcp equals the best lcp over all lists
 // (global strict mode = R(d_max) over the union).
 // One warp per query; take <= 32.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256)
     k_merge(const u64* __restrict__ cand, int shards, int count, int kin, long long s_stride,
-            long long q_stride, int take, int L, int strict, u32* __restrict__ out_ids,
+            long long q_stride, long long j_stride, int take, int L, int strict, u32* __restrict__ out_ids,
             uint16_t* __restrict__ out_lcps, int* __restrict__ out_hits, int out_stride) {
   const int lane = lane_id();
   const long long qi = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -433,7 +521,7 @@ __global__ void __launch_bounds__(256)
   if (strict) {
     for (int s = 0; s < shards; ++s)
       for (int j = lane; j < kin; j += 32) {
-        u64 c = cand[s * s_stride + qi * q_stride + j];
+        u64 c = cand[s * s_stride + qi * q_stride + j * j_stride];
         best = c < best ? c : best;
       }
 #pragma unroll
@@ -448,7 +536,7 @@ __global__ void __launch_bounds__(256)
   for (int s = 0; s < shards; ++s) {
     for (int j0 = 0; j0 < kin; j0 += 32) {
       int j = j0 + lane;
-      u64 c = j < kin ? cand[s * s_stride + qi * q_stride + j] : ~0ull;
+      u64 c = j < kin ? cand[s * s_stride + qi * q_stride + j * j_stride] : ~0ull;
       if (strict && (c >> 32) != tier) c = ~0ull;
       valid += __popc(__ballot_sync(LCP_FULL_MASK, c != ~0ull));
       warp_offer<u64, true>(slot, thr, c, take);
@@ -469,7 +557,7 @@ constexpr int MERGE_SORT_CAP = 8192;
 
 __global__ void __launch_bounds__(MERGE_SORT_THREADS)
     k_merge_sort(const u64* __restrict__ cand, int shards, int count, int kin, long long s_stride,
-                 long long q_stride, int take, int L, int strict, u32* __restrict__ out_ids,
+                 long long q_stride, long long j_stride, int take, int L, int strict, u32* __restrict__ out_ids,
                  uint16_t* __restrict__ out_lcps, int* __restrict__ out_hits, int out_stride) {
   extern __shared__ __align__(16) u64 sbuf[];
   __shared__ u64 s_best[MERGE_SORT_THREADS / 32];
@@ -480,7 +568,7 @@ __global__ void __launch_bounds__(MERGE_SORT_THREADS)
   for (long long qi = blockIdx.x; qi < count; qi += gridDim.x) {
     u64 best = ~0ull;
     for (int t = threadIdx.x; t < P; t += MERGE_SORT_THREADS) {
-      const u64 c = t < m ? cand[(t / kin) * s_stride + qi * q_stride + (t % kin)] : ~0ull;
+      const u64 c = t < m ? cand[(t / kin) * s_stride + qi * q_stride + (t % kin) * j_stride] : ~0ull;
       sbuf[t] = c;
       best = c < best ? c : best;
     }

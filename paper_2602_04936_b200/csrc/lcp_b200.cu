@@ -472,7 +472,8 @@ static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, i
   dv.keys_orig = ix->keys_orig;
   dv.order = ix->order;
   {  // hi / lo planes of the original-order keys' first word, for the full scan
-    const long long pn = (n + 4095) / 4096 * 4096 + 64;  // whole 16 KB stages
+    // whole 16 KB stages, plus slack for the small-batch scan's last step
+    const long long pn = (n + 4095) / 4096 * 4096 + 2048;
     LCP_TRY(dalloc(&ix->keys_hi, pn, acct, st));
     LCP_TRY(dalloc(&ix->keys_lo, pn, acct, st));
     LCP_CK(cudaMemsetAsync(ix->keys_hi, 0, (size_t)pn * 4, st));
@@ -1662,14 +1663,14 @@ static int launch_fullscan_w1(const DevIndex& dv, const uint16_t* q, const u64* 
 
 
 // per query, the take smallest of `shards` candidate lists of kin entries
-// (cand index = s * s_stride + q * q_stride + j): a warp per query for
+// (cand index = s * s_stride + q * q_stride + j * j_stride): a warp per query for
 // take <= 32, else a CTA sorting all shards * kin <= MERGE_SORT_CAP candidates
 static int launch_merge(const u64* cand, int shards, int count, int kin, long long s_stride,
-                        long long q_stride, int take, int L, int strict, u32* ids, uint16_t* lcps,
+                        long long q_stride, long long j_stride, int take, int L, int strict, u32* ids, uint16_t* lcps,
                         int* hits, int out_stride, cudaStream_t st) {
   if (take <= FAST_KMAX) {
     k_merge<<<blocks_for((long long)count * 32, 256), 256, 0, st>>>(
-        cand, shards, count, kin, s_stride, q_stride, take, L, strict, ids, lcps, hits, out_stride);
+        cand, shards, count, kin, s_stride, q_stride, j_stride, take, L, strict, ids, lcps, hits, out_stride);
   } else {
     if ((long long)shards * kin > MERGE_SORT_CAP)
       return fail(LCP_ERR_INVALID_INPUT, "merge supports shards * k <= " + std::to_string(MERGE_SORT_CAP));
@@ -1680,7 +1681,7 @@ static int launch_merge(const u64* cand, int shards, int count, int kin, long lo
     LCP_CK(attr);
     const unsigned grid = (unsigned)std::min<long long>(count, 8ll * num_sms());
     k_merge_sort<<<grid, MERGE_SORT_THREADS, (size_t)P * 8, st>>>(
-        cand, shards, count, kin, s_stride, q_stride, take, L, strict, ids, lcps, hits, out_stride);
+        cand, shards, count, kin, s_stride, q_stride, j_stride, take, L, strict, ids, lcps, hits, out_stride);
   }
   LCP_CK_LAUNCH();
   return LCP_OK;
@@ -1709,7 +1710,9 @@ int lcp_fullscan(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries
     // a few queries: one HBM-streaming pass with every query in every lane
     LCP_TRY(ws->qkeys.ensure((size_t)count * dv.W * 8));
     LCP_TRY(pack_rows(queries, count, dv, ws->qkeys.as<u64>(), nullptr, ws->d_err, st));
-    const long long G = num_sms();
+    int Q = 1;
+    while (Q < count) Q <<= 1;
+    const long long G = num_sms() * (Q == 1 ? fsq_ctas_per_sm<1>() : 1);
     const long long warps = G * FSQ_WARPS;
     long long seg = (dv.n + warps - 1) / warps;
     seg = (seg + FSQ_STEP - 1) / FSQ_STEP * FSQ_STEP;
@@ -1719,8 +1722,6 @@ int lcp_fullscan(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries
     LCP_CK(cudaMemsetAsync(ws->hint.p, 0, (size_t)(count + 1) * 4, st));
     int* hint = ws->hint.as<int>();
     unsigned* ctr = reinterpret_cast<unsigned*>(hint + count);
-    int Q = 1;
-    while (Q < count) Q <<= 1;
 #define LCP_FSQ(C, QQ)                                                                           \
   k_fullscan_smallq<C, QQ><<<(unsigned)G, FSQ_THREADS, (size_t)FSQ_WARPS * QQ * 32 * sizeof(C), \
                              st>>>(dv, ws->qkeys.as<u64>(), count, take, seg,                    \
@@ -1749,18 +1750,16 @@ int lcp_fullscan(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries
     u64* partial = ws->partial.as<u64>();
     // W > 1: the kernel filters on the first word and reads the rest of the
     // packed query for keys that match it entirely
-    const u64* qk = nullptr;
-    if (dv.W > 1) {
-      LCP_TRY(ws->qkeys.ensure((size_t)count * dv.W * 8));
-      LCP_TRY(pack_rows(queries, count, dv, ws->qkeys.as<u64>(), nullptr, ws->d_err, st));
-      qk = ws->qkeys.as<u64>();
-    }
+    LCP_TRY(ws->qkeys.ensure((size_t)count * dv.W * 8));
+    LCP_TRY(pack_rows(queries, count, dv, ws->qkeys.as<u64>(), nullptr, ws->d_err, st));
+    const u64* qk = ws->qkeys.as<u64>();
     LCP_TRY(ws->hint.ensure((size_t)count * 4));
     LCP_CK(cudaMemsetAsync(ws->hint.p, 0, (size_t)count * 4, st));
     LCP_TRY(launch_fullscan_w1(dv, queries, qk, count, take, chunk, nchunks, partial,
                                ws->hint.as<int>(), ws->d_err, st));
     LCP_CK_LAUNCH();
-    return launch_merge(partial, nchunks, count, take, take, (long long)nchunks * take, take, dv.L,
+    // partial lists are chunk-major, query-fastest: [chunk][j][query]
+    return launch_merge(partial, nchunks, count, take, (long long)take * count, 1, count, take, dv.L,
                         0, ids, lcps, hits, out_stride, st);
   }
   LCP_TRY(ws->qkeys.ensure((size_t)count * dv.W * 8));
@@ -1816,7 +1815,7 @@ int lcp_merge_candidates(const uint64_t* cand, int32_t shards, int32_t count, in
   if (shards < 1 || k < 1) return fail(LCP_ERR_INVALID_INPUT, "shards and k must be >= 1");
   if (take < 0 || take > k)
     return fail(LCP_ERR_INVALID_INPUT, "merge needs 0 <= take <= k");
-  return launch_merge((const u64*)cand, shards, count, k, (long long)count * k, k, take, length,
+  return launch_merge((const u64*)cand, shards, count, k, (long long)count * k, k, 1, take, length,
                       strict, ids, lcps, hits, std::max(1, take), (cudaStream_t)stream);
 }
 

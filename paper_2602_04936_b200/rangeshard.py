@@ -43,6 +43,12 @@ from .core import InvalidInputError
 U64_MAX_AS_I64 = -1  # UINT64_MAX bit pattern in an int64 tensor
 
 
+def torch_empty_like_host(t):
+    import torch
+
+    return torch.empty(t.shape, dtype=t.dtype)
+
+
 def lcp_rows(a, b, length: int):
     """Per-row lcp of broadcastable integer row tensors [..., L]."""
     import torch
@@ -79,9 +85,10 @@ class _Collectives:
 
         self.dist = dist
         self.group = group
-        self.world = dist.get_world_size(group)
-        self.rank = dist.get_rank(group)
-        self.nccl = dist.get_backend(group) == "nccl"
+        self.local = group is None and not dist.is_initialized()  # one process, no group
+        self.world = 1 if self.local else dist.get_world_size(group)
+        self.rank = 0 if self.local else dist.get_rank(group)
+        self.nccl = (not self.local) and dist.get_backend(group) == "nccl"
 
     def _in(self, t):
         return t if (self.nccl or t.device.type == "cpu") else t.cpu()
@@ -89,6 +96,8 @@ class _Collectives:
     def all_gather(self, t):
         import torch
 
+        if self.local:
+            return t.contiguous()[None].clone()
         x = self._in(t.contiguous())
         out = torch.empty((self.world, *x.shape), dtype=x.dtype, device=x.device)
         if self.nccl:
@@ -98,11 +107,15 @@ class _Collectives:
         return out.to(t.device)
 
     def all_reduce_max(self, t):
+        if self.local:
+            return t
         x = self._in(t.contiguous())
         self.dist.all_reduce(x, op=self.dist.ReduceOp.MAX, group=self.group)
         return x.to(t.device)
 
     def all_reduce_sum(self, t):
+        if self.local:
+            return t
         x = self._in(t.contiguous())
         self.dist.all_reduce(x, group=self.group)
         return x.to(t.device)
@@ -110,6 +123,8 @@ class _Collectives:
     def all_to_all(self, t, send_counts: list[int], recv_counts: list[int], row_elems: int):
         import torch
 
+        if self.local:
+            return t.contiguous().reshape(-1).clone()
         x = self._in(t.contiguous())
         out = torch.empty((sum(recv_counts) * row_elems,), dtype=x.dtype, device=x.device)
         self.dist.all_to_all_single(out, x.reshape(-1), [c * row_elems for c in recv_counts],
@@ -226,6 +241,12 @@ class RangeShardedIndex:
         self.splitters = torch.from_numpy(np.ascontiguousarray(spl)).to(self.device)
 
         # 2. rows (+ global ids) to the owner of their range, in global-id order
+        if self.world == 1:  # one shard: the rows stay, ids are the row numbers
+            self.gids = torch.arange(id_offset, id_offset + n_local, dtype=torch.int64, device=self.device)
+            self.engine = engine_factory(items, L, sigma)
+            self.n_local = n_local
+            self._finish_build()
+            return
         rows_t = torch.from_numpy(items.astype(np.int32)).to(self.device)
         dest = route(rows_t, self.splitters, L) if n_local else torch.zeros(0, dtype=torch.int64,
                                                                             device=self.device)
@@ -239,13 +260,17 @@ class RangeShardedIndex:
         local = my_rows.cpu().numpy().astype(np.uint16)
         self.engine = engine_factory(local, L, sigma)
         self.n_local = int(local.shape[0])
+        self._finish_build()
+
+    def _finish_build(self):
+        import torch
 
         # 3. range boundaries of every shard, corpus size
         fl = torch.from_numpy(self.engine.first_last_rows()).to(self.device)
         g_fl = self.coll.all_gather(fl)
         self.first, self.last = g_fl[:, 0, :].to(torch.int32), g_fl[:, 1, :].to(torch.int32)
         self.nonempty = self.coll.all_gather(torch.tensor([self.n_local], device=self.device))[:, 0] > 0
-        self.n_total = int(self.coll.all_reduce_sum(torch.tensor([n_local], device=self.device)).item())
+        self.n_total = int(self.coll.all_reduce_sum(torch.tensor([self.n_local], device=self.device)).item())
 
     # ---------------------------------------------------------------- queries
     def _encode(self, ids, lcps, hits, k: int):
@@ -339,11 +364,11 @@ class RangeShardedIndex:
                 bufs={})
         return self._dev
 
-    def _step_buffers(self, count: int, kk: int):
+    def _step_buffers(self, count: int, kk: int, slot: int = 0):
         import torch
 
         st = self._device_state()
-        key = (count, kk)
+        key = (count, kk, slot)
         if key not in st["bufs"]:
             dev = st["splitters"].device
             L = self.length
@@ -356,13 +381,21 @@ class RangeShardedIndex:
                 md=mk(count, dt=torch.int16), tq=mk(count, dt=torch.int32),
                 cand=mk(count, kk, dt=torch.int64),
                 gathered=mk(self.world, count, kk, dt=torch.int64),
+                recv=mk(self.world, max(1, count // self.world), kk, dt=torch.int64),
                 ws=None)
         return st["bufs"][key]
 
-    def query_device(self, queries, k: int, mode: str = "complete", out=None):
+    def query_device(self, queries, k: int, mode: str = "complete", out=None,
+                     exchange: str = "all_gather", group=None, slot: int = 0):
         """Global top-k of a broadcast (count, L) uint16 CUDA batch, on the
         current stream, without synchronising the host.  Returns (or fills)
-        (ids int32 (count, max(1, take)), lcps int16, hits int32)."""
+        (ids int32 (m, max(1, take)), lcps int16, hits int32) where m = count
+        (exchange "all_gather": every rank gets every answer) or count/world
+        (exchange "all_to_all": rank r gets the answers of batch rows
+        [r*m, (r+1)*m), the queries its own clients submitted).  ``group``
+        overrides the process group of the step's collectives (one NCCL
+        communicator per in-flight stream); ``slot`` selects a separate set
+        of step buffers (one per in-flight stream)."""
         import torch
 
         from . import _native
@@ -375,10 +408,14 @@ class RangeShardedIndex:
         take = max(0, min(int(k), self.n_total))
         if take * self.world > 8192:
             raise InvalidInputError("sharded merge supports world * min(k, n) <= 8192")
+        if exchange not in ("all_gather", "all_to_all"):
+            raise InvalidInputError(f"unknown exchange {exchange!r}")
         st = self._device_state()
         count, L = int(queries.shape[0]), self.length
+        if exchange == "all_to_all" and count % self.world:
+            raise InvalidInputError("all_to_all exchange needs count divisible by the world size")
         kk = max(1, take)
-        b = self._step_buffers(count, kk)
+        b = self._step_buffers(count, kk, slot)
         if b["ws"] is None:
             b["ws"] = Workspace()
         ws = b["ws"]
@@ -416,7 +453,7 @@ class RangeShardedIndex:
                                        b["tq"].data_ptr(), stream))
         encode(cnt_own)
         # 2. thresholds of every query from its owner (one int per query)
-        self._all_reduce_max_(b["tq"])
+        self._all_reduce_max_(b["tq"], group)
         # 3. the queries other ranks own whose answer may reach into this range
         check(lib.lcp_route_queries(native.handle, ws.handle, q.data_ptr(), count,
                                     st["splitters"].data_ptr(), self.world - 1, st["first"].data_ptr(),
@@ -425,31 +462,57 @@ class RangeShardedIndex:
                                     cnt_con.data_ptr(), stream))
         answer(cnt_con, max(1, count // 16))
         encode(cnt_con)
-        # 4. candidates of every rank, merged
-        self._all_gather_into_(b["gathered"], b["cand"])
+        # 4. candidates: every rank's for every query (all_gather), or each
+        #    rank's for the queries of rank r's clients to rank r (all_to_all)
+        m = count if exchange == "all_gather" else count // self.world
+        if exchange == "all_gather":
+            self._all_gather_into_(b["gathered"], b["cand"], group)
+        else:
+            self._all_to_all_(b["recv"], b["cand"], group)
         if out is None:
-            out = (torch.empty((count, kk), dtype=torch.int32, device=q.device),
-                   torch.empty((count, kk), dtype=torch.int16, device=q.device),
-                   torch.empty(count, dtype=torch.int32, device=q.device))
+            out = (torch.empty((m, kk), dtype=torch.int32, device=q.device),
+                   torch.empty((m, kk), dtype=torch.int16, device=q.device),
+                   torch.empty(m, dtype=torch.int32, device=q.device))
         ids, lcps, hits = out
-        check(lib.lcp_merge_candidates(b["gathered"].data_ptr(), self.world, count, kk, take, L, strict,
+        src = b["gathered"] if exchange == "all_gather" else b["recv"]
+        check(lib.lcp_merge_candidates(src.data_ptr(), self.world, m, kk, take, L, strict,
                                        ids.data_ptr(), lcps.data_ptr(), hits.data_ptr(), stream))
         return ids, lcps, hits
 
-    def _all_reduce_max_(self, t) -> None:
+    def _all_reduce_max_(self, t, group=None) -> None:
         c = self.coll
+        g = c.group if group is None else group
+        if c.local:
+            return
         if c.nccl:
-            c.dist.all_reduce(t, op=c.dist.ReduceOp.MAX, group=c.group)
+            c.dist.all_reduce(t, op=c.dist.ReduceOp.MAX, group=g)
         else:  # gloo (multi-process tests on one GPU): host staging, not capturable
             h = t.cpu()
-            c.dist.all_reduce(h, op=c.dist.ReduceOp.MAX, group=c.group)
+            c.dist.all_reduce(h, op=c.dist.ReduceOp.MAX, group=g)
             t.copy_(h)
 
-    def _all_gather_into_(self, out, t) -> None:
+    def _all_gather_into_(self, out, t, group=None) -> None:
         c = self.coll
-        if c.nccl:
-            c.dist.all_gather_into_tensor(out, t, group=c.group)
+        g = c.group if group is None else group
+        if c.local:
+            out[0].copy_(t)
+        elif c.nccl:
+            c.dist.all_gather_into_tensor(out, t, group=g)
         else:
             h = out.cpu()
-            c.dist.all_gather(list(h.unbind(0)), t.cpu(), group=c.group)
+            c.dist.all_gather(list(h.unbind(0)), t.cpu(), group=g)
             out.copy_(h)
+
+    def _all_to_all_(self, out, t, group=None) -> None:
+        """t: (world * m, k) rows, block r to rank r; out: (world, m, k), block s from rank s."""
+        c = self.coll
+        g = c.group if group is None else group
+        if c.local:
+            out[0].copy_(t)
+            return
+        if c.nccl:
+            c.dist.all_to_all_single(out, t, group=g)
+            return
+        h = torch_empty_like_host(out)  # gloo: host staging (tests only)
+        c.dist.all_to_all_single(h, t.cpu(), group=g)
+        out.copy_(h)

@@ -200,3 +200,72 @@ class ShardedIndex:
             b["gathered"].data_ptr(), self.world, count, k, take, self.length,
             1 if mode == "strict" else 0, out_ids.data_ptr(), out_lcps.data_ptr(),
             out_hits.data_ptr(), st))
+
+
+class RowBlockShardStep:
+    """One rank's row block with a capture-ready query step (no host sync):
+    local top-k of the broadcast batch -> encode -> exchange -> merge, all on
+    the current stream.  exchange "all_gather": every rank merges every
+    query; "all_to_all": rank r merges only rows [r*m, (r+1)*m) of the batch
+    (its own clients' queries), receiving each shard's candidates for them.
+    ``n_total`` is passed in (no collective at construction)."""
+
+    def __init__(self, items, length: int, sigma: int, id_offset: int, n_total: int, group=None):
+        import torch.distributed as dist
+
+        from .engine import NativeIndex
+
+        self.group = group
+        self.local = group is None and not dist.is_initialized()
+        self.world = 1 if self.local else dist.get_world_size(group)
+        self.rank = 0 if self.local else dist.get_rank(group)
+        self.length, self.id_offset, self.n_total = int(length), int(id_offset), int(n_total)
+        self.native = NativeIndex(items, length, sigma)
+        self._bufs: dict = {}
+
+    def query_device(self, queries, k: int, mode: str = "complete", out=None,
+                     exchange: str = "all_gather", group=None, slot: int = 0):
+        import torch
+        import torch.distributed as dist
+
+        if mode not in ("complete", "strict"):
+            raise InvalidInputError(f"sharded mode must be 'strict' or 'complete', got {mode!r}")
+        take = max(0, min(int(k), self.n_total))
+        if take * self.world > 8192:
+            raise InvalidInputError("sharded merge supports world * min(k, n) <= 8192")
+        count, dev = int(queries.shape[0]), queries.device
+        if exchange == "all_to_all" and count % self.world:
+            raise InvalidInputError("all_to_all exchange needs count divisible by the world size")
+        kk = max(1, take)
+        m = count if exchange == "all_gather" else count // self.world
+        key = (count, kk, slot)
+        if key not in self._bufs:
+            ls = self.native.stride_for(kk)
+            self._bufs[key] = dict(
+                ids=torch.empty((count, ls), dtype=torch.int32, device=dev),
+                lcps=torch.empty((count, ls), dtype=torch.int16, device=dev),
+                hits=torch.empty(count, dtype=torch.int32, device=dev),
+                cand=torch.empty((count, kk), dtype=torch.int64, device=dev),
+                recv=torch.empty((self.world, m, kk), dtype=torch.int64, device=dev))
+        b = self._bufs[key]
+        local_candidates(self.native, queries, kk, self.id_offset, mode, bufs=b)
+        g = self.group if group is None else group
+        if self.local:
+            b["recv"][0].copy_(b["cand"])
+        elif dist.get_backend(g) != "nccl":  # gloo (tests on one GPU): host staging, not capturable
+            h = torch.empty(b["recv"].shape, dtype=torch.int64)
+            if exchange == "all_gather":
+                dist.all_gather(list(h.unbind(0)), b["cand"].cpu(), group=g)
+            else:
+                dist.all_to_all_single(h, b["cand"].cpu(), group=g)
+            b["recv"].copy_(h)
+        elif exchange == "all_gather":
+            dist.all_gather_into_tensor(b["recv"], b["cand"], group=g)
+        else:
+            dist.all_to_all_single(b["recv"], b["cand"], group=g)
+        if out is None:
+            out = (torch.empty((m, kk), dtype=torch.int32, device=dev),
+                   torch.empty((m, kk), dtype=torch.int16, device=dev),
+                   torch.empty(m, dtype=torch.int32, device=dev))
+        merge_candidates_device(b["recv"], kk, self.length, self.n_total, *out, mode=mode)
+        return out

@@ -534,6 +534,17 @@ def _range_gpu_worker(rank, world, port, backend):
                             h = int(hits[i])
                             assert list(zip(ids[i, :h].tolist(), lcps[i, :h].tolist())) == \
                                 list(zip(fids[i, :fhits[i]].tolist(), flcps[i, :fhits[i]].tolist())), (n, k, mode, i)
+            # all_to_all exchange: this rank gets the answers of its slice
+            m = len(qs) // world
+            mine = slice(rank * m, (rank + 1) * m)
+            for k, mode in ((10, "complete"), (5, "strict"), (40, "complete")):
+                fids, flcps, fhits, _, _, _ = full.query_batch(qs[mine], k, mode)
+                ids, lcps, hits = sh.query_device(dq[: m * world], k, mode, exchange="all_to_all")
+                ids, lcps, hits = ids.cpu().long() & 0xFFFFFFFF, lcps.cpu().long() & 0xFFFF, hits.cpu()
+                for i in range(m):
+                    h = int(hits[i])
+                    assert list(zip(ids[i, :h].tolist(), lcps[i, :h].tolist())) == \
+                        list(zip(fids[i, :fhits[i]].tolist(), flcps[i, :fhits[i]].tolist())), (n, k, mode, i)
             if backend == "nccl":
                 # the device-routed step has no host round trip: capture it once
                 # in a CUDA graph and replay it
@@ -902,3 +913,25 @@ def test_async_graph_cache_survives_scratch_growth(gpu):
     ws.close()
     del _native
 
+
+
+def test_rowblock_shard_step_single_process(gpu, oracle_lib):
+    """RowBlockShardStep (the config-5 row-block step: local top-k -> encode
+    -> exchange -> merge) with one process and several blocks composed by
+    hand equals the oracle; the single-block step equals the plain index."""
+    import torch
+
+    from paper_2602_04936_b200.sharded import RowBlockShardStep, merge_candidates
+
+    ds = lg.generate_dataset(120_000, 32, 4, seed=61)
+    qs = np.vstack([lg.generate_queries(ds, 300, seed=62), lg.generate_queries(ds, 300, seed=63, prefix_len=16)])
+    dq = torch.from_numpy(qs).cuda()
+    one = RowBlockShardStep(ds.items, 32, 4, id_offset=0, n_total=ds.n)
+    trie = oracle_lib.OracleTrie(ds.items, 4)
+    for k, mode in ((10, "complete"), (7, "strict"), (33, "complete")):
+        ids, lcps, hits = one.query_device(dq, k, mode)
+        fids, flcps, fhits, _, _, _ = trie.query_batch(qs, k, mode)
+        for i in range(len(qs)):
+            h = int(hits[i])
+            got = list(zip((ids[i, :h].cpu().long() & 0xFFFFFFFF).tolist(), (lcps[i, :h].cpu().long() & 0xFFFF).tolist()))
+            assert got == list(zip(fids[i, :fhits[i]].tolist(), flcps[i, :fhits[i]].tolist())), (k, mode, i)
