@@ -97,6 +97,9 @@ int lcp_index_get_info(const lcp_index* index, lcp_index_info* info);
  * trie tables   : node_count int32 row_lo + uint16 edge_symbol (trie.py:409-419) */
 int lcp_index_export_order(const lcp_index* index, int32_t* order);
 int lcp_index_export_sorted_keys(const lcp_index* index, uint64_t* keys);
+/* rows [first, first + count) of sorted_keys (e.g. a shard's first / last key) */
+int lcp_index_export_sorted_key_range(const lcp_index* index, int64_t first, int64_t count,
+                                      uint64_t* keys);
 int lcp_index_export_adjacent_lcp(const lcp_index* index, uint16_t* adj);
 int lcp_index_export_directory(const lcp_index* index, int64_t* directory);
 int lcp_index_trie_level_offsets(const lcp_index* index, int64_t* level_offset);
@@ -209,16 +212,20 @@ int lcp_merge_candidates(const uint64_t* cand, int32_t shards, int32_t count, in
  * pack_queries : rows (count*length u16) -> packed keys (count*words u64),
  *                the index's key encoding (order-preserving).
  * route_queries: owner(q) = #splitters <= q (splitters: nsplit sorted packed
- *                keys, nsplit = world - 1).  thresholds == NULL: select the
- *                queries this `rank` owns; else select the queries another
- *                rank owns for which this rank is nonempty and
- *                max(lcp(q, first[rank]), lcp(q, last[rank])) >= thresholds[q]
- *                (first/last: world packed keys).  Selected rows are written
- *                densely to out_rows (count*length u16 capacity), their
- *                batch positions to out_sel, their number to *d_count
- *                (device int; reset by the call).  Selection order within the
- *                dense batch is unspecified; results are scattered back by
- *                out_sel, so outputs are deterministic.
+ *                keys, nsplit = world - 1), on `qkeys` (count*words packed
+ *                keys) or, when qkeys is NULL, on the rows packed here.
+ *                consult == 0: select the queries this `rank` owns and, when
+ *                given, reset thresholds[q] = -1 and reset_cand[q*cand_k ..
+ *                q*cand_k + cand_k) = UINT64_MAX for every q (the step's state).
+ *                consult == 1: select the queries another rank owns for which
+ *                this rank is nonempty and max(lcp(q, first[rank]),
+ *                lcp(q, last[rank])) >= thresholds[q] (first/last: world packed
+ *                keys).  Selected rows are written densely to out_rows
+ *                (count*length u16 capacity), their batch positions to
+ *                out_sel, their number to *d_count (device int; reset by the
+ *                call).  Selection order within the dense batch is
+ *                unspecified; results are scattered back by out_sel, so
+ *                outputs are deterministic.
  * query_counted: lcp_query over `capacity` rows of which *d_count (device)
  *                are live; grids are sized for `expected` rows.
  * shard_thresholds: thresholds[sel[i]] = the lcp of hit need-1 (complete;
@@ -230,10 +237,11 @@ int lcp_merge_candidates(const uint64_t* cand, int32_t shards, int32_t count, in
 int lcp_pack_queries(const lcp_index* index, lcp_workspace* ws, const uint16_t* rows, int32_t count,
                      uint64_t* keys, void* stream);
 int lcp_route_queries(const lcp_index* index, lcp_workspace* ws, const uint16_t* queries,
-                      int32_t count, const uint64_t* splitters, int32_t nsplit,
-                      const uint64_t* first, const uint64_t* last, const int32_t* nonempty,
-                      int32_t rank, const int32_t* thresholds, uint16_t* out_rows,
-                      int32_t* out_sel, int32_t* d_count, void* stream);
+                      const uint64_t* qkeys, int32_t count, const uint64_t* splitters,
+                      int32_t nsplit, const uint64_t* first, const uint64_t* last,
+                      const int32_t* nonempty, int32_t rank, int32_t* thresholds,
+                      int32_t consult, uint16_t* out_rows, int32_t* out_sel, int32_t* d_count,
+                      uint64_t* reset_cand, int32_t cand_k, void* stream);
 int lcp_query_counted(const lcp_index* index, lcp_workspace* ws, const uint16_t* queries,
                       int32_t capacity, const int32_t* d_count, int32_t expected, int32_t k,
                       int32_t mode, int32_t out_stride, uint32_t* ids, uint16_t* lcps,

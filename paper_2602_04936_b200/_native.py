@@ -91,7 +91,8 @@ SIGNATURES = {
     "lcp_encode_candidates": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _I32, _I32, _I64, _P, _P]),
     "lcp_merge_candidates": (ctypes.c_int, [_P, _I32, _I32, _I32, _I32, _I32, _I32, _P, _P, _P, _P]),
     "lcp_pack_queries": (ctypes.c_int, [_P, _P, _P, _I32, _P, _P]),
-    "lcp_route_queries": (ctypes.c_int, [_P, _P, _P, _I32, _P, _I32, _P, _P, _P, _I32, _P, _P, _P, _P, _P]),
+    "lcp_route_queries": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P, _I32, _P, _P, _P, _I32, _P, _I32, _P, _P, _P, _P, _I32, _P]),
+    "lcp_index_export_sorted_key_range": (ctypes.c_int, [_P, _I64, _I64, _P]),
     "lcp_query_counted": (ctypes.c_int, [_P, _P, _P, _I32, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P]),
     "lcp_shard_thresholds": (ctypes.c_int, [_P, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _P, _P]),
     "lcp_encode_candidates_sel": (ctypes.c_int, [_P, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _P, _I64, _P, _P]),

@@ -243,10 +243,10 @@ __global__ void k_gather_keys(const u64* __restrict__ keys, const u32* __restric
 }
 
 // ---------------------------------------------------------------------------
-// Stable LSD radix sort of (u64 key, u32 value), 8-bit digits.
-//   upsweep   : per-tile digit counts, digit-major [256][ntiles]
-//   scan      : exclusive scan of the counts -> global scatter offsets
-//   downsweep : stable in-tile ranks (warp match_any multisplit) + scatter
+// Stable LSD radix sort of (u64 key, u32 value), 8-bit digits: the digit
+// histograms of every pass (k_digit_hist8), per-tile digit counts (upsweep,
+// digit-major [256][ntiles], for the count + scan + scatter form) and the
+// scatter kernel k_onesweep below.
 // Stability: a tile is split into 8 contiguous warp segments; a warp walks
 // its segment 32 items at a time in index order, so rank = items of the
 // same digit in earlier tiles + earlier warps + earlier steps + lower lanes.
@@ -287,60 +287,6 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_upsweep(const u64* __restrict
   }
   __syncthreads();
   counts[(long long)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
-}
-
-__global__ void __launch_bounds__(RS_THREADS) k_rs_downsweep(
-    const u64* __restrict__ kin, const u32* __restrict__ vin, u64* __restrict__ kout,
-    u32* __restrict__ vout, long long n, int shift, int ntiles, const u32* __restrict__ offsets) {
-  __shared__ u32 wcnt[RS_WARPS][256];
-  __shared__ u32 gofs[256];
-  const int lane = lane_id();
-  const int warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < RS_WARPS * 256; i += RS_THREADS) (&wcnt[0][0])[i] = 0;
-  gofs[threadIdx.x] = offsets[(long long)threadIdx.x * ntiles + blockIdx.x];
-  __syncthreads();
-
-  const long long seg = (long long)blockIdx.x * RS_TILE + (long long)warp * RS_WARP_SEG;
-  u64 key[RS_ITEMS];
-  u32 val[RS_ITEMS];
-  u32 rank[RS_ITEMS];
-#pragma unroll
-  for (int j = 0; j < RS_ITEMS; ++j) {
-    long long i = seg + j * 32 + lane;
-    bool ok = i < n;
-    key[j] = ok ? kin[i] : 0;
-    val[j] = ok ? vin[i] : 0;
-    u32 d = ok ? (u32)((key[j] >> shift) & 255) : 256u;
-    unsigned peers = __match_any_sync(LCP_FULL_MASK, d);
-    unsigned lower = peers & ((1u << lane) - 1u);
-    u32 before = 0;
-    if (ok) before = wcnt[warp][d];
-    __syncwarp();
-    if (ok && lower == 0) wcnt[warp][d] = before + __popc(peers);
-    __syncwarp();
-    rank[j] = before + __popc(lower);
-  }
-  __syncthreads();
-  // exclusive prefix over warps, per digit
-  {
-    u32 run = 0;
-    for (int w = 0; w < RS_WARPS; ++w) {
-      u32 c = wcnt[w][threadIdx.x];
-      wcnt[w][threadIdx.x] = run;
-      run += c;
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int j = 0; j < RS_ITEMS; ++j) {
-    long long i = seg + j * 32 + lane;
-    if (i < n) {
-      u32 d = (u32)((key[j] >> shift) & 255);
-      long long pos = (long long)gofs[d] + wcnt[warp][d] + rank[j];
-      kout[pos] = key[j];
-      vout[pos] = val[j];
-    }
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -430,6 +376,18 @@ constexpr u64 OS_COUNT_MASK = (1ull << 62) - 1;
 constexpr int OS_LB_WIN = 16;  // look-back statuses loaded per round trip (first hop: 8)
 constexpr size_t OS_SMEM = (size_t)OS_TILE * 12 + (size_t)OS_WARPS * 256 * 4 + 3 * 256 * 4 + 64;
 
+// lanes holding the same 8-bit digit as this lane (valid lanes only), from
+// eight ballots: MATCH.ANY was the onesweep tile's slowest instruction
+__device__ __forceinline__ unsigned match_digit8(u32 d, bool ok) {
+  unsigned m = __ballot_sync(LCP_FULL_MASK, ok);
+#pragma unroll
+  for (int bit = 0; bit < 8; ++bit) {
+    const unsigned b = __ballot_sync(LCP_FULL_MASK, (d >> bit) & 1u);
+    m &= ((d >> bit) & 1u) ? b : ~b;
+  }
+  return ok ? m : 0u;
+}
+
 __device__ __forceinline__ u64 ld_relaxed_u64(const u64* p) {
   u64 v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -439,10 +397,17 @@ __device__ __forceinline__ void st_relaxed_u64(u64* p, u64 v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// LOOKBACK = false: the tile offsets come from a separate count + scan
+// (k_rs_upsweep + scan_exclusive: offsets[d * ntiles + tile] already include
+// the bucket start), tile = blockIdx.x, no status traffic; one more read of
+// the keys (8 B per pair) instead of the look-back chain, whose first wave is
+// serial (every co-resident tile waits for its predecessors' prefixes).
+template <bool LOOKBACK>
 __global__ void __launch_bounds__(OS_THREADS, 3) k_onesweep(
     const u64* __restrict__ kin, const u32* __restrict__ vin, u64* __restrict__ kout,
     u32* __restrict__ vout, long long n, int shift, const u32* __restrict__ hist,
-    u64* __restrict__ status, unsigned* __restrict__ tile_counter) {
+    u64* __restrict__ status, unsigned* __restrict__ tile_counter, const u32* __restrict__ offsets,
+    int ntiles) {
   extern __shared__ __align__(16) unsigned char os_smem[];
   u64* sk = reinterpret_cast<u64*>(os_smem);                       // OS_TILE keys
   u32* sv = reinterpret_cast<u32*>(sk + OS_TILE);                  // OS_TILE values
@@ -454,10 +419,13 @@ __global__ void __launch_bounds__(OS_THREADS, 3) k_onesweep(
   const int warp = threadIdx.x >> 5;
   const int d0 = threadIdx.x;  // the digit this thread owns in per-digit phases
 
-  if (threadIdx.x == 0) scratch[32] = atomicAdd(tile_counter, 1u);
+  if (LOOKBACK && threadIdx.x == 0) scratch[32] = atomicAdd(tile_counter, 1u);
   for (int i = threadIdx.x; i < OS_WARPS * 256; i += OS_THREADS) wcnt[i] = 0;
   __syncthreads();
-  const long long tile = scratch[32];
+  const long long tile = LOOKBACK ? (long long)scratch[32] : (long long)blockIdx.x;
+  // count + scan form: this digit's output base, loaded now so the scattered
+  // read overlaps the key loads (ncu: it was the longest stall when read late)
+  const u32 off_pref = LOOKBACK ? 0u : __ldg(offsets + (long long)d0 * ntiles + tile);
   const long long seg = tile * OS_TILE + (long long)warp * OS_WARP_SEG;
 
   u64 key[OS_ITEMS];
@@ -470,17 +438,21 @@ __global__ void __launch_bounds__(OS_THREADS, 3) k_onesweep(
     key[j] = ok ? kin[i] : 0;
     val[j] = ok ? vin[i] : 0;
   }
+  // stable in-warp ranks: rank = same-digit items of earlier rows of the
+  // warp's segment + lower lanes of this row.  The 16 MATCH.ANY are
+  // independent; each row's leader adds the row's count with one shared
+  // atomic whose old value is that row's base (a warp's shared atomics to one
+  // address apply in instruction order, so rows stay in index order)
 #pragma unroll
   for (int j = 0; j < OS_ITEMS; ++j) {
     const bool ok = seg + j * 32 + lane < n;
     const u32 d = ok ? (u32)((key[j] >> shift) & 255) : 256u;
-    const unsigned peers = __match_any_sync(LCP_FULL_MASK, d);
+    const unsigned peers = match_digit8(d, ok);
     const unsigned lower = peers & ((1u << lane) - 1u);
+    const int leader = __ffs(peers) - 1;
     u32 before = 0;
-    if (ok) before = wcnt[warp * 256 + d];
-    __syncwarp();
-    if (ok && lower == 0) wcnt[warp * 256 + d] = before + __popc(peers);
-    __syncwarp();
+    if (ok && lower == 0) before = atomicAdd(&wcnt[warp * 256 + d], (u32)__popc(peers));
+    before = __shfl_sync(LCP_FULL_MASK, before, leader);
     rank[j] = before + __popc(lower);
   }
   __syncthreads();
@@ -493,8 +465,8 @@ __global__ void __launch_bounds__(OS_THREADS, 3) k_onesweep(
     cnt += c;
   }
   // publish the aggregate (tile 0: its inclusive prefix) as early as possible
-  u64* my = status + tile * 256 + d0;
-  st_relaxed_u64(my, (tile == 0 ? OS_FLAG_PREFIX : OS_FLAG_AGG) | (u64)cnt);
+  u64* my = LOOKBACK ? status + tile * 256 + d0 : nullptr;
+  if (LOOKBACK) st_relaxed_u64(my, (tile == 0 ? OS_FLAG_PREFIX : OS_FLAG_AGG) | (u64)cnt);
   // bucket start of this digit (exclusive scan of the pass histogram) and the
   // digit's start inside the tile
   u32 total;
@@ -519,7 +491,7 @@ __global__ void __launch_bounds__(OS_THREADS, 3) k_onesweep(
   // otherwise walk back one dependent L2 round trip per tile, which is what
   // bounds the first wave (ncu: ~16 hops per tile at 2M, 47 us per pass)
   u64 excl = 0;
-  long long p = tile - 1;
+  long long p = LOOKBACK ? tile - 1 : -1;
   int win = 8;
   while (p >= 0) {
     u64 v[OS_LB_WIN];
@@ -543,8 +515,12 @@ __global__ void __launch_bounds__(OS_THREADS, 3) k_onesweep(
     p -= used;  // used < win: tile p was not ready yet; poll it again
     win = OS_LB_WIN;
   }
-  if (tile > 0) st_relaxed_u64(my, OS_FLAG_PREFIX | (excl + cnt));
-  gstart[d0] = bstart + (u32)excl;
+  if (LOOKBACK) {
+    if (tile > 0) st_relaxed_u64(my, OS_FLAG_PREFIX | (excl + cnt));
+    gstart[d0] = bstart + (u32)excl;
+  } else {
+    gstart[d0] = off_pref;
+  }
   __syncthreads();
   const long long rem = n - tile * OS_TILE;
   const int tile_n = rem < OS_TILE ? (int)rem : OS_TILE;

@@ -235,6 +235,7 @@ constexpr int FSQ_THREADS = 512;
 constexpr int FSQ_WARPS = FSQ_THREADS / 32;
 constexpr int FSQ_QMAX = 8;
 constexpr int FSQ_STEP = 1024;  // segment granularity (keys); >= one warp step for every Q
+constexpr int FSQ_SEG_MIN = 4096;  // keys per warp at least (small corpora: fewer CTAs)
 // 16-byte hi-plane loads per lane per step: fewer with more queries (registers)
 template <int Q>
 __host__ __device__ constexpr int fsq_unroll() { return Q <= 2 ? 8 : (Q <= 4 ? 4 : 2); }

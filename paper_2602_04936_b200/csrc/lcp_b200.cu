@@ -200,21 +200,47 @@ int radix_sort_pairs(u64** k, u32** v, u64** k_alt, u32** v_alt, long long n, cu
   LCP_CK(cudaMallocAsync((void**)&status, (size_t)ntiles * 256 * sizeof(u64), st));
   LCP_CK(cudaMallocAsync((void**)&counters, 8 * sizeof(unsigned), st));
   LCP_CK(cudaMemsetAsync(counters, 0, 8 * sizeof(unsigned), st));
-  static const cudaError_t attr = cudaFuncSetAttribute(  // thread-safe one-time initialisation
-      k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OS_SMEM);
+  static const cudaError_t attr = [] {  // thread-safe one-time initialisation
+    cudaError_t e = cudaFuncSetAttribute(k_onesweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OS_SMEM);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_onesweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OS_SMEM);
+    return e;
+  }();
   LCP_CK(attr);
+  // decoupled look-back (one kernel per pass) or count + scan + scatter
+  // (three kernels, one more read of the keys, no serial chain); the chain's
+  // first wave dominates while the tiles fit a few waves (LCP_SORT_LOOKBACK:
+  // A/B override, 0 / 1)
+  static const int lb_env = [] {
+    const char* e = getenv("LCP_SORT_LOOKBACK");
+    return e ? atoi(e) : -1;
+  }();
+  const bool lookback = lb_env >= 0 ? lb_env != 0 : ntiles > 16ll * num_sms();
+  u32* offs = nullptr;
+  if (!lookback) LCP_CK(cudaMallocAsync((void**)&offs, (size_t)ntiles * 256 * sizeof(u32), st));
   for (int p = 0; p < 8; ++p) {
     bool trivial = false;
     for (int d = 0; d < 256; ++d)
       if ((long long)h[p * 256 + d] == n) trivial = true;
     if (trivial) continue;  // every key has the same digit: pass is the identity
-    LCP_CK(cudaMemsetAsync(status, 0, (size_t)ntiles * 256 * sizeof(u64), st));
-    k_onesweep<<<(unsigned)ntiles, OS_THREADS, OS_SMEM, st>>>(*k, *v, *k_alt, *v_alt, n, 8 * p,
-                                                               hist + p * 256, status, counters + p);
+    if (lookback) {
+      LCP_CK(cudaMemsetAsync(status, 0, (size_t)ntiles * 256 * sizeof(u64), st));
+    } else {
+      k_rs_upsweep<<<(unsigned)ntiles, RS_THREADS, 0, st>>>(*k, n, 8 * p, (int)ntiles, offs);
+      LCP_CK_LAUNCH();
+      LCP_TRY(scan_exclusive<u32>(offs, ntiles * 256, st));
+    }
+    if (lookback)
+      k_onesweep<true><<<(unsigned)ntiles, OS_THREADS, OS_SMEM, st>>>(
+          *k, *v, *k_alt, *v_alt, n, 8 * p, hist + p * 256, status, counters + p, nullptr, (int)ntiles);
+    else
+      k_onesweep<false><<<(unsigned)ntiles, OS_THREADS, OS_SMEM, st>>>(
+          *k, *v, *k_alt, *v_alt, n, 8 * p, hist + p * 256, status, counters + p, offs, (int)ntiles);
     LCP_CK_LAUNCH();
     std::swap(*k, *k_alt);
     std::swap(*v, *v_alt);
   }
+  if (offs) LCP_CK(cudaFreeAsync(offs, st));
   LCP_CK(cudaFreeAsync(status, st));
   LCP_CK(cudaFreeAsync(counters, st));
   LCP_CK(cudaFreeAsync(hist, st));
@@ -742,6 +768,14 @@ int lcp_index_export_order(const lcp_index* ix, int32_t* order) {
 int lcp_index_export_sorted_keys(const lcp_index* ix, uint64_t* keys) {
   if (!ix) return fail(LCP_ERR_INVALID_INPUT, "null index");
   return copy_out(keys, ix->keys, (size_t)ix->dv.n * ix->dv.W * 8);
+}
+
+int lcp_index_export_sorted_key_range(const lcp_index* ix, int64_t first, int64_t count,
+                                      uint64_t* keys) {
+  if (!ix) return fail(LCP_ERR_INVALID_INPUT, "null index");
+  if (first < 0 || count < 0 || first + count > ix->dv.n)
+    return fail(LCP_ERR_INVALID_INPUT, "sorted key range out of bounds");
+  return copy_out(keys, ix->keys + first * ix->dv.W, (size_t)count * ix->dv.W * 8);
 }
 
 int lcp_index_export_adjacent_lcp(const lcp_index* ix, uint16_t* adj) {
@@ -1712,7 +1746,12 @@ int lcp_fullscan(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries
     LCP_TRY(pack_rows(queries, count, dv, ws->qkeys.as<u64>(), nullptr, ws->d_err, st));
     int Q = 1;
     while (Q < count) Q <<= 1;
-    const long long G = num_sms() * (Q == 1 ? fsq_ctas_per_sm<1>() : 1);
+    // one or two CTAs per SM, but at least FSQ_SEG_MIN keys per warp: a small
+    // corpus gets fewer, longer segments (the per-warp seed and the merge of
+    // the CTA lists, not the key stream, dominate there)
+    const long long G = std::max(1ll, std::min<long long>(
+        num_sms() * (Q == 1 ? fsq_ctas_per_sm<1>() : 1),
+        (dv.n + (long long)FSQ_WARPS * FSQ_SEG_MIN - 1) / ((long long)FSQ_WARPS * FSQ_SEG_MIN)));
     const long long warps = G * FSQ_WARPS;
     long long seg = (dv.n + warps - 1) / warps;
     seg = (seg + FSQ_STEP - 1) / FSQ_STEP * FSQ_STEP;
@@ -1829,26 +1868,33 @@ int lcp_pack_queries(const lcp_index* ix, lcp_workspace* ws, const uint16_t* row
                    (cudaStream_t)stream);
 }
 
-int lcp_route_queries(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries, int32_t count,
-                      const uint64_t* splitters, int32_t nsplit, const uint64_t* first,
-                      const uint64_t* last, const int32_t* nonempty, int32_t rank,
-                      const int32_t* thresholds, uint16_t* out_rows, int32_t* out_sel,
-                      int32_t* d_count, void* stream) {
+int lcp_route_queries(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries,
+                      const uint64_t* qkeys, int32_t count, const uint64_t* splitters, int32_t nsplit,
+                      const uint64_t* first, const uint64_t* last, const int32_t* nonempty,
+                      int32_t rank, int32_t* thresholds, int32_t consult, uint16_t* out_rows,
+                      int32_t* out_sel, int32_t* d_count, uint64_t* reset_cand, int32_t cand_k,
+                      void* stream) {
   if (!ix || !ws) return fail(LCP_ERR_INVALID_INPUT, "null index or workspace");
   if (!d_count || !out_sel || !out_rows) return fail(LCP_ERR_INVALID_INPUT, "null route output");
   if (nsplit < 0 || rank < 0 || rank > nsplit) return fail(LCP_ERR_INVALID_INPUT, "bad rank / splitter count");
-  if (thresholds && (!first || !last || !nonempty))
-    return fail(LCP_ERR_INVALID_INPUT, "consult routing needs first / last rows and nonempty flags");
+  if (consult && (!thresholds || !first || !last || !nonempty))
+    return fail(LCP_ERR_INVALID_INPUT, "consult routing needs thresholds, first / last rows and nonempty flags");
+  if (reset_cand && cand_k < 1) return fail(LCP_ERR_INVALID_INPUT, "cand_k must be >= 1");
   cudaStream_t st = (cudaStream_t)stream;
   LCP_CK(cudaMemsetAsync(d_count, 0, sizeof(int32_t), st));
   if (count <= 0) return LCP_OK;
   const DevIndex& dv = ix->dv;
-  LCP_TRY(ws->qkeys.ensure((size_t)count * dv.W * 8));
-  LCP_TRY(pack_rows(queries, count, dv, ws->qkeys.as<u64>(), nullptr, ws->d_err, st));
+  const u64* keys = reinterpret_cast<const u64*>(qkeys);
+  if (!keys) {  // pack here (pass pre-packed keys to route one batch twice)
+    LCP_TRY(ws->qkeys.ensure((size_t)count * dv.W * 8));
+    LCP_TRY(pack_rows(queries, count, dv, ws->qkeys.as<u64>(), nullptr, ws->d_err, st));
+    keys = ws->qkeys.as<u64>();
+  }
   k_route_queries<<<blocks_for(count, RT_THREADS), RT_THREADS, 0, st>>>(
-      ws->qkeys.as<u64>(), queries, count, dv.L, dv.W, dv.spw, dv.lb,
-      reinterpret_cast<const u64*>(splitters), nsplit, reinterpret_cast<const u64*>(first),
-      reinterpret_cast<const u64*>(last), nonempty, rank, thresholds, out_rows, out_sel, d_count);
+      keys, queries, count, dv.L, dv.W, dv.spw, dv.lb, reinterpret_cast<const u64*>(splitters), nsplit,
+      reinterpret_cast<const u64*>(first), reinterpret_cast<const u64*>(last), nonempty, rank,
+      thresholds, consult ? 1 : 0, out_rows, out_sel, d_count, reinterpret_cast<u64*>(reset_cand),
+      cand_k);
   LCP_CK_LAUNCH();
   return LCP_OK;
 }

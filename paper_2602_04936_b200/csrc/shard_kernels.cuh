@@ -42,13 +42,16 @@ __device__ __forceinline__ int lcp_words(const u64* a, const u64* b, int W, int 
 
 constexpr int RT_THREADS = 256;
 
+// consult == 0: select the owned queries and (optionally) reset the step's
+// per-query state, thresholds[q] = -1 and cand[q][0..cand_k) = UINT64_MAX, so a
+// step needs no separate fill launches; consult == 1: select by the consult rule
 __global__ void __launch_bounds__(RT_THREADS)
     k_route_queries(const u64* __restrict__ qkeys, const uint16_t* __restrict__ queries, int count,
                     int L, int W, int spw, int lb, const u64* __restrict__ splitters, int nsplit,
                     const u64* __restrict__ first, const u64* __restrict__ last,
-                    const int* __restrict__ nonempty, int rank, const int* __restrict__ thresholds,
-                    uint16_t* __restrict__ out_rows, int* __restrict__ out_sel,
-                    int* __restrict__ d_count) {
+                    const int* __restrict__ nonempty, int rank, int* __restrict__ thresholds,
+                    int consult, uint16_t* __restrict__ out_rows, int* __restrict__ out_sel,
+                    int* __restrict__ d_count, u64* __restrict__ reset_cand, int cand_k) {
   const int q = blockIdx.x * RT_THREADS + threadIdx.x;
   const int lane = lane_id();
   bool take = false;
@@ -56,8 +59,11 @@ __global__ void __launch_bounds__(RT_THREADS)
     const u64* qk = qkeys + (long long)q * W;
     int owner = 0;
     for (int s = 0; s < nsplit; ++s) owner += cmp_words(splitters + (long long)s * W, qk, W) <= 0;
-    if (thresholds == nullptr) {
+    if (!consult) {
       take = owner == rank;
+      if (thresholds) thresholds[q] = -1;
+      if (reset_cand)
+        for (int j = 0; j < cand_k; ++j) reset_cand[(long long)q * cand_k + j] = ~0ull;
     } else if (owner != rank && nonempty[rank]) {
       const int best = max(lcp_words(qk, first + (long long)rank * W, W, L, spw, lb),
                            lcp_words(qk, last + (long long)rank * W, W, L, spw, lb));

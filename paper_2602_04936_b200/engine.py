@@ -103,6 +103,12 @@ class NativeIndex:
             check(load().lcp_index_export_sorted_keys(self.handle, ptr(out)))
         return out
 
+    def export_sorted_key_range(self, first: int, count: int) -> np.ndarray:
+        out = np.empty((count, self.words), dtype=np.uint64)
+        if count:
+            check(load().lcp_index_export_sorted_key_range(self.handle, int(first), int(count), ptr(out)))
+        return out
+
     def export_adjacent_lcp(self) -> np.ndarray:
         out = np.empty(max(0, self.n - 1), dtype=np.uint16)
         if self.n > 1:

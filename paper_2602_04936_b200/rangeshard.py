@@ -150,6 +150,19 @@ def pack_keys_host(rows: np.ndarray, length: int, sigma: int) -> np.ndarray:
     return out
 
 
+def unpack_keys_host(keys: np.ndarray, length: int, sigma: int) -> np.ndarray:
+    """Inverse of pack_keys_host: (m, W) uint64 -> (m, L) uint16 symbols."""
+    need = max(1, int(np.ceil(np.log2(sigma))))
+    b = 1
+    while b < need:
+        b <<= 1
+    spw = 64 // b
+    j = np.arange(length)
+    word = np.asarray(keys, dtype=np.uint64)[:, j // spw]
+    shift = (64 - b * (j % spw + 1)).astype(np.uint64)
+    return ((word >> shift) & np.uint64((1 << b) - 1)).astype(np.uint16)
+
+
 class GpuEngine:
     """Local top-k on this rank's range: the CUDA index (NativeIndex; an empty
     range still gets an n = 0 index, which the device routing needs for the
@@ -166,8 +179,9 @@ class GpuEngine:
     def first_last_rows(self) -> np.ndarray:
         if not self.n:
             return np.zeros((2, self.length), dtype=np.int64)
-        rows = self.native.unpack_sorted_rows()
-        return np.stack([rows[0], rows[-1]]).astype(np.int64)
+        keys = np.stack([self.native.export_sorted_key_range(0, 1)[0],
+                         self.native.export_sorted_key_range(self.n - 1, 1)[0]])
+        return unpack_keys_host(keys, self.length, self.sigma).astype(np.int64)
 
     def query(self, queries, k: int, mode: str):
         """queries: (m, L) uint16/int16 CUDA tensor -> (ids, lcps, hits, md) int64."""
@@ -374,7 +388,9 @@ class RangeShardedIndex:
             L = self.length
             ls = max(1, min(kk, max(1, self.n_local)))
             mk = lambda *shape, dt: torch.zeros(shape, dtype=dt, device=dev)
+            W = self.engine.native.words
             st["bufs"][key] = dict(
+                qk=mk(count, W, dt=torch.int64),
                 rows=mk(count, L, dt=torch.int16), sel=mk(count, dt=torch.int32),
                 cnt=mk(2, dt=torch.int32), ids=mk(count, ls, dt=torch.int32),
                 lcps=mk(count, ls, dt=torch.int16), hits=mk(count, dt=torch.int32),
@@ -427,8 +443,6 @@ class RangeShardedIndex:
         strict = 1 if mode == "strict" else 0
         need = take if mode == "complete" else kk
         expected = max(1, (count + self.world - 1) // self.world * 5 // 4)
-        b["tq"].fill_(-1)
-        b["cand"].fill_(-1)  # UINT64_MAX: no candidate
         cnt_own, cnt_con = b["cnt"][0:1], b["cnt"][1:2]
 
         def answer(cnt, exp):
@@ -442,26 +456,32 @@ class RangeShardedIndex:
                 b["ids"].data_ptr(), b["lcps"].data_ptr(), b["hits"].data_ptr(), b["sel"].data_ptr(),
                 cnt.data_ptr(), count, kk, ls, L, st["gids"].data_ptr(), 0, b["cand"].data_ptr(), stream))
 
+        # 0. pack the batch once; routing the own queries also resets the
+        #    step's thresholds (-1) and candidates (UINT64_MAX)
+        check(lib.lcp_pack_queries(native.handle, ws.handle, q.data_ptr(), count, b["qk"].data_ptr(),
+                                   stream))
         # 1. the queries this rank owns: answer, threshold, candidates
-        check(lib.lcp_route_queries(native.handle, ws.handle, q.data_ptr(), count,
+        check(lib.lcp_route_queries(native.handle, ws.handle, q.data_ptr(), b["qk"].data_ptr(), count,
                                     st["splitters"].data_ptr(), self.world - 1, None, None, None,
-                                    self.rank, None, b["rows"].data_ptr(), b["sel"].data_ptr(),
-                                    cnt_own.data_ptr(), stream))
+                                    self.rank, b["tq"].data_ptr(), 0, b["rows"].data_ptr(),
+                                    b["sel"].data_ptr(), cnt_own.data_ptr(), b["cand"].data_ptr(), kk,
+                                    stream))
         answer(cnt_own, expected)
-        check(lib.lcp_shard_thresholds(b["lcps"].data_ptr(), b["hits"].data_ptr(), b["md"].data_ptr(),
-                                       b["sel"].data_ptr(), cnt_own.data_ptr(), count, ls, need, strict,
-                                       b["tq"].data_ptr(), stream))
         encode(cnt_own)
-        # 2. thresholds of every query from its owner (one int per query)
-        self._all_reduce_max_(b["tq"], group)
-        # 3. the queries other ranks own whose answer may reach into this range
-        check(lib.lcp_route_queries(native.handle, ws.handle, q.data_ptr(), count,
-                                    st["splitters"].data_ptr(), self.world - 1, st["first"].data_ptr(),
-                                    st["last"].data_ptr(), st["nonempty"].data_ptr(), self.rank,
-                                    b["tq"].data_ptr(), b["rows"].data_ptr(), b["sel"].data_ptr(),
-                                    cnt_con.data_ptr(), stream))
-        answer(cnt_con, max(1, count // 16))
-        encode(cnt_con)
+        if self.world > 1:  # one shard: nobody else to consult
+            check(lib.lcp_shard_thresholds(b["lcps"].data_ptr(), b["hits"].data_ptr(), b["md"].data_ptr(),
+                                           b["sel"].data_ptr(), cnt_own.data_ptr(), count, ls, need,
+                                           strict, b["tq"].data_ptr(), stream))
+            # 2. thresholds of every query from its owner (one int per query)
+            self._all_reduce_max_(b["tq"], group)
+            # 3. the queries other ranks own whose answer may reach into this range
+            check(lib.lcp_route_queries(native.handle, ws.handle, q.data_ptr(), b["qk"].data_ptr(), count,
+                                        st["splitters"].data_ptr(), self.world - 1, st["first"].data_ptr(),
+                                        st["last"].data_ptr(), st["nonempty"].data_ptr(), self.rank,
+                                        b["tq"].data_ptr(), 1, b["rows"].data_ptr(), b["sel"].data_ptr(),
+                                        cnt_con.data_ptr(), None, 0, stream))
+            answer(cnt_con, max(1, count // 16))
+            encode(cnt_con)
         # 4. candidates: every rank's for every query (all_gather), or each
         #    rank's for the queries of rank r's clients to rank r (all_to_all)
         m = count if exchange == "all_gather" else count // self.world
