@@ -339,7 +339,12 @@ def main() -> None:
         torch.cuda.synchronize()
         build_ms_steady = 1e3 * (time.perf_counter() - t_rep) / 7
         R = len(replicas)
-        G = R * n_pool  # steps per captured graph
+        # steps per captured graph: the whole timed region in one graph up to
+        # 8192 steps (a multiple of R * n_pool, so the replica / batch cycle
+        # stays aligned across replays beyond that); measured: per-step time
+        # is the same as with 64-step graphs replayed back to back, minus the
+        # graph-boundary gaps
+        G_MAX = 8192
 
         def capture(n_steps: int, n_streams: int):
             streams = [torch.cuda.Stream(device=dev) for _ in range(n_streams)]
@@ -361,6 +366,7 @@ def main() -> None:
             return g, bufs
 
         def run_steps(n_streams: int, steps: int, warmup: int):
+            G = min(steps, G_MAX)
             g, bufs = capture(G, n_streams)
             tail = steps % G
             gt = capture(tail, n_streams)[0] if tail else None
@@ -804,6 +810,19 @@ def extras(idx, ds, qs, stream, flush_buf) -> dict:
     out["fullscan_qps"] = BATCH / (ms / 1e3)
     out["fullscan_ms_per_batch"] = ms
     out["fullscan_key_stream_gbs"] = N_ITEMS * 8 / (ms / 1e3) / 1e9
+    # the single-query full scan (the reference's oracle_top_k(dataset, q, k)
+    # call): the small-batch streaming kernel, HBM-bound on large corpora
+    fs1_fn = lambda i: idx.native.fullscan_device(dq[i % n_pool][i % BATCH:i % BATCH + 1], K, ids[:1],
+                                                  lcps[:1], hits[:1], stream=st)
+    ms1, _ = per_step_ms(fs1_fn, 32, 5)
+    alg = N_ITEMS * algorithmic_key_bytes(SEQ_LEN, SIGMA) + (algorithmic_key_bytes(SEQ_LEN, SIGMA) + 6 * K)
+    peak = hbm_peak()[0]
+    out["fullscan_single_query"] = {
+        "us_per_query": ms1 * 1e3, "algorithmic_gbs": alg / (ms1 / 1e3) / 1e9,
+        "frac": alg / (ms1 / 1e3) / 1e9 / peak, "kernel": "k_fullscan_smallq<u32,1>",
+        "note": "N*K_b + K_b + 6k algorithmic bytes per call; the kernel reads the 4-byte hi plane "
+                "(half of K_b) and the rare survivors' lo words; 2M keys are one 8 MB pass, so the "
+                "launch, the seed and the merges dominate here (at N=200M: profiles/README.md)"}
     # TAL B=256 (paper's bounded-range scan)
     tal = lg.build_tal(ds, 256)
     tal_fn = lambda i: tal.native.query_device(dq[i % n_pool], K, "tal", ids, lcps, hits, stream=st)

@@ -15,7 +15,8 @@ import threading
 from .core import InternalInvariantError, InvalidInputError, InvalidStateError
 
 LIB_NAME = "_lcp_b200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+# LCP_B200_LIB: A/B hook for tools (a variant build of the same sources)
+LIB_PATH = os.environ.get("LCP_B200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 LCP_OK = 0
 LCP_ERR_INVALID_INPUT = 3

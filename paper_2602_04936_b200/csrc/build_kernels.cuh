@@ -253,8 +253,13 @@ __global__ void k_gather_keys(const u64* __restrict__ keys, const u32* __restric
 // ---------------------------------------------------------------------------
 constexpr int RS_THREADS = 256;
 constexpr int RS_WARPS = RS_THREADS / 32;
-constexpr int RS_ITEMS = 16;                     // per lane
-constexpr int RS_TILE = RS_THREADS * RS_ITEMS;   // 4096 keys
+#ifndef LCP_OS_ITEMS
+#define LCP_OS_ITEMS 8  // keys per lane of a sort tile: 2048-key tiles keep 4 tiles
+                        // resident per SM (16 per lane: 43 -> 31 us per pass at 2M
+                        // vs 8: 23.5 us; A/B with -DLCP_OS_ITEMS=16)
+#endif
+constexpr int RS_ITEMS = LCP_OS_ITEMS;           // per lane (== the scatter's tile)
+constexpr int RS_TILE = RS_THREADS * RS_ITEMS;   // keys per tile
 constexpr int RS_WARP_SEG = 32 * RS_ITEMS;       // 512 keys
 
 // all eight digit histograms of one word in one pass (pass-skip detection)
@@ -367,8 +372,9 @@ __global__ void k_scan_add(T* __restrict__ data, long long m, const T* __restric
 // ---------------------------------------------------------------------------
 constexpr int OS_THREADS = 256;
 constexpr int OS_WARPS = OS_THREADS / 32;
-constexpr int OS_ITEMS = 16;
-constexpr int OS_TILE = OS_THREADS * OS_ITEMS;  // 4096 pairs
+constexpr int OS_ITEMS = LCP_OS_ITEMS;
+constexpr int OS_TILE = OS_THREADS * OS_ITEMS;  // 2048 pairs (8 per lane)
+constexpr int OS_MIN_CTAS = OS_ITEMS <= 8 ? 4 : 3;  // resident tiles per SM the registers allow
 constexpr int OS_WARP_SEG = 32 * OS_ITEMS;
 constexpr u64 OS_FLAG_AGG = 1ull << 62;
 constexpr u64 OS_FLAG_PREFIX = 2ull << 62;
@@ -403,7 +409,7 @@ __device__ __forceinline__ void st_relaxed_u64(u64* p, u64 v) {
 // the keys (8 B per pair) instead of the look-back chain, whose first wave is
 // serial (every co-resident tile waits for its predecessors' prefixes).
 template <bool LOOKBACK>
-__global__ void __launch_bounds__(OS_THREADS, 3) k_onesweep(
+__global__ void __launch_bounds__(OS_THREADS, OS_MIN_CTAS) k_onesweep(
     const u64* __restrict__ kin, const u32* __restrict__ vin, u64* __restrict__ kout,
     u32* __restrict__ vout, long long n, int shift, const u32* __restrict__ hist,
     u64* __restrict__ status, unsigned* __restrict__ tile_counter, const u32* __restrict__ offsets,

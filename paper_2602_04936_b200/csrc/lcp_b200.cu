@@ -207,15 +207,15 @@ int radix_sort_pairs(u64** k, u32** v, u64** k_alt, u32** v_alt, long long n, cu
     return e;
   }();
   LCP_CK(attr);
-  // decoupled look-back (one kernel per pass) or count + scan + scatter
-  // (three kernels, one more read of the keys, no serial chain); the chain's
-  // first wave dominates while the tiles fit a few waves (LCP_SORT_LOOKBACK:
-  // A/B override, 0 / 1)
-  static const int lb_env = [] {
+  // count + scan + scatter (three kernels, one more read of the keys, no
+  // serial chain) or decoupled look-back (one kernel per pass).  Measured at
+  // 2M / 25M rows (2048-key tiles): 0.735 / 4.37 ms whole build against
+  // 0.79 / 4.79 ms with the look-back, whose first wave is a serial prefix
+  // chain; LCP_SORT_LOOKBACK=1 selects it (A/B hook)
+  static const bool lookback = [] {
     const char* e = getenv("LCP_SORT_LOOKBACK");
-    return e ? atoi(e) : -1;
+    return e && atoi(e) != 0;
   }();
-  const bool lookback = lb_env >= 0 ? lb_env != 0 : ntiles > 16ll * num_sms();
   u32* offs = nullptr;
   if (!lookback) LCP_CK(cudaMallocAsync((void**)&offs, (size_t)ntiles * 256 * sizeof(u32), st));
   for (int p = 0; p < 8; ++p) {

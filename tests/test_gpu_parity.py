@@ -550,19 +550,38 @@ def _range_gpu_worker(rank, world, port, backend):
                 # in a CUDA graph and replay it
                 s = torch.cuda.Stream()
                 s.wait_stream(torch.cuda.current_stream())
+                for exchange in ("all_gather", "all_to_all"):
+                    with torch.cuda.stream(s):
+                        ref = [t.clone() for t in sh.query_device(dq, 10, "complete", exchange=exchange)]
+                        out = tuple(torch.empty_like(t) for t in ref)
+                        g = torch.cuda.CUDAGraph()
+                        with torch.cuda.graph(g, stream=s):
+                            sh.query_device(dq, 10, "complete", out=out, exchange=exchange)
+                        for t in out:
+                            t.zero_()
+                        g.replay()
+                        g.replay()
+                    torch.cuda.synchronize()
+                    for a, b in zip(ref, out):
+                        assert torch.equal(a, b), exchange
+                # the row-block step through NCCL, captured the same way
+                from paper_2602_04936_b200.sharded import RowBlockShardStep
+
+                rb = RowBlockShardStep(ds.items, L, sigma, id_offset=0, n_total=n)
                 with torch.cuda.stream(s):
-                    ref = [t.clone() for t in sh.query_device(dq, 10, "complete")]
+                    ref = [t.clone() for t in rb.query_device(dq, 10, "complete", exchange="all_to_all")]
                     out = tuple(torch.empty_like(t) for t in ref)
                     g = torch.cuda.CUDAGraph()
                     with torch.cuda.graph(g, stream=s):
-                        sh.query_device(dq, 10, "complete", out=out)
-                    for t in out:
-                        t.zero_()
-                    g.replay()
+                        rb.query_device(dq, 10, "complete", out=out, exchange="all_to_all")
                     g.replay()
                 torch.cuda.synchronize()
-                for a, b in zip(ref, out):
-                    assert torch.equal(a, b)
+                fids, flcps, fhits, _, _, _ = full.query_batch(qs, 10, "complete")
+                ids, lcps, hits = (t.cpu() for t in out)
+                for i in range(len(qs)):
+                    h = int(hits[i])
+                    assert list(zip((ids[i, :h].long() & 0xFFFFFFFF).tolist(), (lcps[i, :h].long() & 0xFFFF).tolist())) == \
+                        list(zip(fids[i, :fhits[i]].tolist(), flcps[i, :fhits[i]].tolist())), ("rowblock", i)
     finally:
         dist.destroy_process_group()
 
