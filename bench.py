@@ -411,9 +411,15 @@ def main() -> None:
         sampler.start()
         total_ms, bufs2, (t0, t1) = run_steps(INFLIGHT, args.steps, args.warmup)
         clocks = sampler.stop(t0, t1)
-        aux_all = bufs1[0][4]
         gpu_launches = args.steps * world
         value = world * BATCH * args.steps / (total_ms / 1e3)
+        # |R(d*)| of every batch of the pool (a short timed region may not have
+        # touched all of them): one untimed launch per batch
+        ids_a, lcps_a, hits_a, md_a, aux_all = out_bufs()
+        for bb in range(n_pool):
+            idx.native.query_device(dq[bb], K, "complete", ids_a, lcps_a, hits_a, md_a, aux_all[bb],
+                                    stream=main_stream.cuda_stream)
+        torch.cuda.synchronize()
 
         # roofline of the dominant kernel (k_query_w1): algorithmic bytes / duration
         rsize = (aux_all[:, :, 1].cpu().numpy().astype(np.uint64) & np.uint64(0xFFFFFFFF)).astype(np.int64)
