@@ -296,8 +296,6 @@ int ilog2(int v) {
 
 }  // namespace
 
-static bool l2_persist_setup();
-
 // ===========================================================================
 struct lcp_index {
   DevIndex dv{};
@@ -604,8 +602,8 @@ static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, i
                                                                             ix->sketch);
     LCP_CK_LAUNCH();
     for (int j = 1; j < lv; ++j) {
-      k_id_sketch<LCP_SK_FANOUT * LCP_SK_LIST><<<sk_grid(dv.sk_cnt[j]), SK_THREADS, 0, st>>>(
-          ix->sketch + dv.sk_off[j - 1] * LCP_SK_LIST, dv.sk_cnt[j - 1] * LCP_SK_LIST, dv.sk_cnt[j],
+      k_id_sketch_cta<LCP_SK_FANOUT * LCP_SK_LIST><<<(unsigned)dv.sk_cnt[j], SK_THREADS, 0, st>>>(
+          ix->sketch + dv.sk_off[j - 1] * LCP_SK_LIST, dv.sk_cnt[j - 1] * LCP_SK_LIST,
           ix->sketch + dv.sk_off[j] * LCP_SK_LIST);
       LCP_CK_LAUNCH();
     }
@@ -721,7 +719,6 @@ int lcp_index_build(const uint16_t* rows, int64_t n, int32_t length, int32_t sig
     return LCP_OK;
   }
   keep_pool_mapped();
-  l2_persist_setup();
   cudaStream_t st;
   if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
     delete ix;
@@ -1150,7 +1147,6 @@ int lcp_index_bucket_range_search(const lcp_index* ix, const uint16_t* queries, 
 int lcp_workspace_create(lcp_workspace** out) {
   if (!out) return fail(LCP_ERR_INVALID_INPUT, "out must not be null");
   lcp_workspace* ws = new lcp_workspace();
-  l2_persist_setup();
   cudaError_t e = cudaStreamCreateWithFlags(&ws->stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaMalloc((void**)&ws->d_err, sizeof(int));
   if (e == cudaSuccess) e = cudaMemset(ws->d_err, 0, sizeof(int));
@@ -1234,67 +1230,6 @@ static void allow_dyn_smem() {
   (void)done;
 }
 
-// The search tables below the shared-memory levels (1 MB at config 3) are
-// read by every query, one 512 B block each, while the keys / ids of the leaf
-// regions stream through L2 once.  The launch marks the tables' address range
-// as persisting in L2 (an access-policy window on the launch, so it is part
-// of captured graphs too), so one of a query's three dependent round trips
-// stays an L2 hit under streaming traffic.  LCP_L2_PERSIST=0 turns it off.
-static bool l2_persist_setup() {
-  // first called from index build / workspace creation (outside any stream
-  // capture: cudaDeviceSetLimit would invalidate a capture in progress)
-  static const bool ok = [] {  // thread-safe one-time initialisation
-    const char* e = getenv("LCP_L2_PERSIST");
-    if (e && e[0] == '0') return false;
-    int dev = 0, maxp = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess ||
-        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev) != cudaSuccess || maxp <= 0) {
-      cudaGetLastError();
-      return false;
-    }
-    const size_t want = std::min<size_t>((size_t)maxp, 32ull << 20);
-    const bool set = cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess;
-    cudaGetLastError();
-    return set;
-  }();
-  return ok;
-}
-
-static size_t search_table_bytes(const DevIndex& dv) {
-  if (dv.nlevels <= dv.smem_levels) return 0;
-  const int j = dv.nlevels - 1;
-  const long long end = dv.level_off[j] + (dv.level_cnt[j] + LCP_SEARCH_FANOUT - 1) / LCP_SEARCH_FANOUT * LCP_SEARCH_FANOUT;
-  return (size_t)end * (size_t)dv.W * 8;
-}
-
-template <typename C, int T, int MODE>
-static void launch_w1_mode(const DevIndex& dv, unsigned grid, unsigned block, size_t smem, cudaStream_t st,
-                           const uint16_t* q, int count, int k, int stride, u32* ids, uint16_t* lcps,
-                           int* hits, uint16_t* md, u64* aux, int* err) {
-  const size_t tb = search_table_bytes(dv);
-  if (tb > 0 && l2_persist_setup()) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(block);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-    attr[0].val.accessPolicyWindow.base_ptr = const_cast<u64*>(dv.levels);
-    attr[0].val.accessPolicyWindow.num_bytes = tb;
-    attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
-    attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, k_query_w1<C, T, MODE>, dv, q, count, k, stride, ids, lcps, hits, md, aux,
-                           err) == cudaSuccess)
-      return;
-    cudaGetLastError();  // attribute refused: plain launch below
-  }
-  k_query_w1<C, T, MODE><<<grid, block, smem, st>>>(dv, q, count, k, stride, ids, lcps, hits, md, aux, err);
-}
-
 template <typename C, int T>
 static void launch_w1(const DevIndex& dv, int mode, unsigned grid, unsigned block, size_t smem,
                       cudaStream_t st, const uint16_t* q, int count, int k, int stride, u32* ids,
@@ -1306,11 +1241,11 @@ static void launch_w1(const DevIndex& dv, int mode, unsigned grid, unsigned bloc
   prefer_carveout<k_query_w1<C, T, 1>>(25);
   prefer_carveout<k_query_w1<C, T, 2>>(0);
   if (mode == LCP_MODE_STRICT)
-    launch_w1_mode<C, T, 0>(dv, grid, block, smem, st, q, count, k, stride, ids, lcps, hits, md, aux, err);
+    k_query_w1<C, T, 0><<<grid, block, smem, st>>>(dv, q, count, k, stride, ids, lcps, hits, md, aux, err);
   else if (mode == LCP_MODE_COMPLETE)
-    launch_w1_mode<C, T, 1>(dv, grid, block, smem, st, q, count, k, stride, ids, lcps, hits, md, aux, err);
+    k_query_w1<C, T, 1><<<grid, block, smem, st>>>(dv, q, count, k, stride, ids, lcps, hits, md, aux, err);
   else
-    launch_w1_mode<C, T, 2>(dv, grid, block, smem, st, q, count, k, stride, ids, lcps, hits, md, aux, err);
+    k_query_w1<C, T, 2><<<grid, block, smem, st>>>(dv, q, count, k, stride, ids, lcps, hits, md, aux, err);
 }
 
 template <int WMAX>
