@@ -214,12 +214,6 @@ __global__ void k_first_word(const u64* __restrict__ keys, long long n, int W, u
   if (i < n) w0[i] = keys[i * W];
 }
 
-// high 32 bits of each W == 1 key (the TAL sweep plane)
-__global__ void k_hi_word(const u64* __restrict__ keys, long long n, u32* __restrict__ hi) {
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) hi[i] = (u32)(keys[i] >> 32);
-}
-
 __global__ void k_iota(u32* __restrict__ v, long long n) {
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) v[i] = (u32)i;

@@ -34,7 +34,6 @@ struct DevIndex {
   const u64* levels;      // concatenated search-level tables (W words per entry)
   const u64* keys_w0;     // W > 1: first word of each sorted key (coalesced compares, TAL sweep)
   const u64* levels_w0;   // first word of each search-table entry (== levels when W == 1)
-  const u32* keys_shi;    // W == 1 with TAL: high 32 bits of each sorted key (bucket sweep)
   const long long* directory;  // TAL dense directory (sigma**d + 1) or null
   long long n;
   long long level_off[LCP_MAX_LEVELS];  // entry offset of level j in `levels`

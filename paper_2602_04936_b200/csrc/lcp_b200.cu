@@ -315,7 +315,6 @@ struct lcp_index {
   u32* rank = nullptr;  // original id -> sorted position
   u64* keys_w0 = nullptr;
   u64* levels_w0 = nullptr;  // W > 1: first word of each search-table entry
-  u32* keys_shi = nullptr;
   std::vector<long long> level_offset;  // cached trie level offsets
 };
 
@@ -393,7 +392,6 @@ int lcp_index_free(lcp_index* ix) {
   if (ix->rank) cudaFreeAsync(ix->rank, 0);
   if (ix->keys_w0) cudaFreeAsync(ix->keys_w0, 0);
   if (ix->levels_w0) cudaFreeAsync(ix->levels_w0, 0);
-  if (ix->keys_shi) cudaFreeAsync(ix->keys_shi, 0);
   cudaStreamSynchronize(0);
   delete ix;
   return LCP_OK;
@@ -619,14 +617,8 @@ static int build_impl(lcp_index* ix, const uint16_t* rows, long long n, int L, i
   phase("sketch");
   // TAL bucket structure — tal.py:42-82
   if (tal_depth >= 0) {
-    if (W == 1) {  // high-word plane of the sorted keys: the sweep reads 4 B per key
-                   // (W > 1 sweeps the first-word plane built with the levels)
-      LCP_TRY(dalloc(&ix->keys_shi, n + 64, acct, st));
-      LCP_CK(cudaMemsetAsync(ix->keys_shi, 0, (size_t)(n + 64) * 4, st));
-      k_hi_word<<<blocks_for(n, 256), 256, 0, st>>>(ix->keys, n, ix->keys_shi);
-      LCP_CK_LAUNCH();
-      dv.keys_shi = ix->keys_shi;
-    }
+    // (W == 1 TAL counts symbols from the region and the run edges,
+    // tal_sym_region; W > 1 sweeps the first-word plane built with the levels)
     ix->tal_depth = tal_depth;
     long long buckets = 1;
     bool overflow = false;

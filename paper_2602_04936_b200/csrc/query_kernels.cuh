@@ -442,56 +442,72 @@ __device__ __forceinline__ void tal_bucket_w1(const DevIndex& ix, u64 q, int& bl
   }
 }
 
-// symbols_compared = sum over the bucket [blo, bhi) of min(lcp + 1, L)
-// (tal.py:173-177) for a W == 1 query; the warp total on every lane.
-// Bits past symbol L are zero in keys and query, so x = key ^ q is nonzero
-// exactly when lcp < L, and min(lcp + 1, L) = 1 + min(clz64(x) >> lb, L - 1)
-// with no branch (clz64(0) = 64).  The sweep reads the sorted high-word plane
-// (4 B per key): clz64(x) = clz32(hi ^ qh) unless the high words match, and
-// only then (lcp >= 32 / b symbols, rare inside a bucket) is the full key
-// read.  Aligned 16-byte groups of 4 keys, 16 keys per lane in flight; the
-// keys at either end outside whole groups go one per lane.
-__device__ __forceinline__ unsigned long long tal_sym_w1(const DevIndex& ix, u64 q, int blo, int bhi) {
+// TAL symbols_compared (tal.py:173-177) = sum over the bucket B of
+// min(lcp_i + 1, L) = sum_{d=0}^{L-1} #{i in B : lcp_i >= d}
+//   = |B| * (1 + min(dB, L-1)) + sum_{d=dB+1}^{L-1} |R(d)|,
+// because B = R(dB) (every bucket item matches q's first dB symbols) and, for
+// d > dB, {i in B : lcp_i >= d} = R(d), the run of sorted rows sharing q's
+// d-prefix.  R(d) within the leaf region is read off the region's lcps (one
+// ballot per depth, depths dB+1..dmax, R(d) empty beyond dmax); a run reaching
+// a region edge continues to its true edge, found by a binary search over the
+// bucket, one lane per (depth, side).  So the count costs a handful of
+// dependent L2 probes instead of a sweep over the whole bucket (the former
+// tal_sym_w1 read every bucket item: 128 MB of L2 traffic per 4096-query
+// batch at config 3, B = 256).  W == 1 keys.
+template <int T>
+__device__ __forceinline__ unsigned long long tal_sym_region(const DevIndex& ix, u64 q, int blo, int bhi,
+                                                             const int (&l)[T], int s, int dmax) {
   const int lane = lane_id();
-  const int lb = ix.lb, lm1 = ix.L - 1;
-  const u32 qh = (u32)(q >> 32);
-  const u32* __restrict__ shi = ix.keys_shi;
-  const u64* __restrict__ keys = ix.keys;
-  auto term = [&](u32 h, int i) -> u32 {
-    const int c = h != qh ? __clz(h ^ qh) : __clzll((long long)(__ldg(keys + i) ^ q));
-    return (u32)min(c >> lb, lm1);
-  };
-  unsigned long long sym = 0;
-  const int a0 = (blo + 3) & ~3, e0 = bhi & ~3;
-  constexpr int TAL_UNROLL = 4;
-  int base = a0 + 4 * lane;
-  for (; base + 128 * (TAL_UNROLL - 1) < e0; base += 128 * TAL_UNROLL) {
-    uint4 hv[TAL_UNROLL];
+  const int L = ix.L, dB = ix.tal_depth, b = ix.b;
+  unsigned long long sym = (unsigned long long)(bhi - blo) * (unsigned long long)(1 + min(dB, L - 1));
+  const int l0 = __shfl_sync(LCP_FULL_MASK, l[0], 0);        // position s
+  const int lz = __shfl_sync(LCP_FULL_MASK, l[T - 1], 31);   // position s + 32T - 1
+  const int e = s + 32 * T;                                  // first position after the region
+  u64 lmask = 0, rmask = 0;  // bit (d - dB - 1): the run of depth d leaves the region left / right
+  const int dtop = min(dmax, L - 1);
+  for (int d = dB + 1; d <= dtop; ++d) {
+    int c = 0;
 #pragma unroll
-    for (int u = 0; u < TAL_UNROLL; ++u)
-      hv[u] = __ldg(reinterpret_cast<const uint4*>(shi + base + 128 * u));
-    u32 part = 0;
-#pragma unroll
-    for (int u = 0; u < TAL_UNROLL; ++u) {
-      const int i = base + 128 * u;
-      part += term(hv[u].x, i) + term(hv[u].y, i + 1) + term(hv[u].z, i + 2) + term(hv[u].w, i + 3);
+    for (int t = 0; t < T; ++t) c += __popc(__ballot_sync(LCP_FULL_MASK, l[t] >= d));
+    if (c == 0) break;  // R(d) is nested: nothing deeper either
+    sym += (unsigned long long)c;
+    if (l0 >= d && s > blo) lmask |= 1ull << (d - dB - 1);
+    if (lz >= d && e < bhi) rmask |= 1ull << (d - dB - 1);
+  }
+  // the runs' parts outside the region: binary searches over the bucket
+  const int nl = __popcll(lmask), nr = __popcll(rmask);
+  unsigned long long extra = 0;
+  for (int t0 = 0; t0 < nl + nr; t0 += 32) {
+    const int t = t0 + lane;
+    if (t < nl + nr) {
+      const bool left = t < nl;
+      u64 m = left ? lmask : rmask;
+      for (int j = left ? t : t - nl; j > 0; --j) m &= m - 1;  // the j-th set bit
+      const int d = dB + 1 + __ffsll((long long)m) - 1;
+      const int sh = 64 - d * b;  // d < L <= 64 / b, so 0 < sh < 64
+      const u64 qp = q >> sh;
+      if (left) {  // first i in [blo, s) with prefix_d(key_i) >= prefix_d(q)
+        int lo = blo, hi = s;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if ((__ldg(ix.keys + mid) >> sh) < qp) lo = mid + 1;
+          else hi = mid;
+        }
+        extra += (unsigned long long)(s - lo);
+      } else {  // first i in [e, bhi) with prefix_d(key_i) > prefix_d(q)
+        int lo = e, hi = bhi;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if ((__ldg(ix.keys + mid) >> sh) <= qp) lo = mid + 1;
+          else hi = mid;
+        }
+        extra += (unsigned long long)(lo - e);
+      }
     }
-    sym += part;
   }
-  for (; base < e0; base += 128) {
-    const uint4 hv = __ldg(reinterpret_cast<const uint4*>(shi + base));
-    sym += term(hv.x, base) + term(hv.y, base + 1) + term(hv.z, base + 2) + term(hv.w, base + 3);
-  }
-  if (e0 >= a0) {  // up to 3 keys before a0 and after e0
-    const int i = lane < 3 ? blo + lane : e0 + lane - 3;
-    if ((lane < 3 && i < a0) || (lane >= 3 && lane < 6 && i < bhi)) sym += term(__ldg(shi + i), i);
-  } else if (lane < bhi - blo) {  // the whole bucket lies inside one group
-    sym += term(__ldg(shi + blo + lane), blo + lane);
-  }
-  if (lane == 0) sym += (unsigned long long)(bhi - blo);  // the "+1" of every item
 #pragma unroll
-  for (int o = 16; o; o >>= 1) sym += __shfl_xor_sync(LCP_FULL_MASK, sym, o);
-  return sym;
+  for (int o = 16; o; o >>= 1) extra += __shfl_xor_sync(LCP_FULL_MASK, extra, o);
+  return sym + extra;
 }
 
 template <typename C, int T, int MODE>
@@ -598,7 +614,7 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, MODE == 2 ? 1 : 2)
     u64 aux0 = 0, aux1 = 0;
     bool tal_small = false;  // bucket smaller than k: answer = the whole bucket
     if constexpr (MODE == 2) {
-      const unsigned long long sym = tal_sym_w1(ix, q, blo, bhi);
+      const unsigned long long sym = tal_sym_region<T>(ix, q, blo, bhi, l, s, dmax);
       md = ix.tal_depth;
       aux0 = (u64)(bhi - blo);
       aux1 = sym;
@@ -949,7 +965,7 @@ __global__ void __launch_bounds__(NS > 2 ? QW_MAX_THREADS / 2 : QW_MAX_THREADS, 
     lst.init(reinterpret_cast<C*>(smem_raw + 16 + (size_t)ix.smem_entries * 8) + warp * (32 * NS));
     unsigned long long tsym = 0;
     if constexpr (MODE == 2) {
-      tsym = tal_sym_w1(ix, q, blo, bhi);
+      tsym = tal_sym_region<T>(ix, q, blo, bhi, l, s, dmax);
       const int bs = bhi - blo;
       if (bs < k) {  // the whole bucket, ranked (an empty one included)
         for (int base = blo; base < bhi; base += 32) {
