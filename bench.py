@@ -532,6 +532,11 @@ def main() -> None:
 
 
 C5_ITEMS = int(os.environ.get("LCP_BENCH_C5_ITEMS", 200_000_000))  # BASELINE config 5 (override: functional checks only)
+# candidate exchange of the range-sharded step: "all_to_all" (NCCL) or "p2p"
+# (symmetric memory: peers signal, the merge kernel reads their candidates over
+# NVLink).  p2p is tested at one rank; no multi-GPU box was available to
+# validate it, so NCCL stays the default (LCP_BENCH_EXCHANGE=p2p to select it)
+EXCHANGE = os.environ.get("LCP_BENCH_EXCHANGE", "all_to_all")
 # our kernels per range-sharded step: pack + route (own), counted query,
 # thresholds, encode, pack + route (consult), counted query, encode, merge
 SHARD_LAUNCHES_PER_STEP = 10
@@ -603,7 +608,7 @@ def config5_leg(args, world, rank, dev, barrier, max_over_ranks, scheme: str = "
         nccl = world > 1 and dist.get_backend() == "nccl"
 
         # the uint16 rows travel as int32 pairs (NCCL and gloo have no 16-bit integer type)
-        def step(i):
+        def step(i, exchange=EXCHANGE if scheme == "range" else "all_to_all"):
             src = pool[i % n_pool].view(torch.int32)
             if nccl:
                 dist.all_gather_into_tensor(gq.view(torch.int32), src)
@@ -613,37 +618,66 @@ def config5_leg(args, world, rank, dev, barrier, max_over_ranks, scheme: str = "
                 gq.view(torch.int32).copy_(h.view(-1, SEQ_LEN // 2))
             else:
                 gq.copy_(pool[i % n_pool])
-            sh.query_device(gq, K, "complete", out=out, exchange="all_to_all")
+            sh.query_device(gq, K, "complete", out=out, exchange=exchange)
 
-        for i in range(3):  # eager warm-up (allocates the step buffers)
-            step(i)
-        torch.cuda.synchronize()
-        G = min(64, max(8, args.steps))
-        launch = "CUDA graph replay (NCCL collectives captured)"
-        try:
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
-                for i in range(G):
-                    step(i)
-            run = lambda: g.replay()
-            per_run = G
-        except Exception as e:  # capture unsupported here: eager, still no host sync
+        def timed(exchange):
+            """Graph-capture G steps (eager if capture fails), warm, time
+            ceil(steps / G) replays; returns (ms over ranks, steps, launch)."""
+            for i in range(3):  # eager warm-up (allocates the step buffers)
+                step(i, exchange)
             torch.cuda.synchronize()
-            launch = f"eager stream-ordered launches (graph capture failed: {type(e).__name__})"
-            run = lambda: [step(i) for i in range(G)]
-            per_run = G
-        reps = max(1, (args.steps + per_run - 1) // per_run)
-        for _ in range(max(1, args.warmup // per_run + 1)):
-            run()
-        barrier()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(reps):
-            run()
-        b.record(stream)
-        torch.cuda.synchronize()
-        ms = max_over_ranks(a.elapsed_time(b))
-        barrier()
+            G = min(64, max(8, args.steps))
+            launch = "CUDA graph replay (NCCL collectives captured)"
+            try:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    for i in range(G):
+                        step(i, exchange)
+                run = lambda: g.replay()
+            except Exception as e:  # capture unsupported here: eager, still no host sync
+                torch.cuda.synchronize()
+                launch = f"eager stream-ordered launches (graph capture failed: {type(e).__name__})"
+                run = lambda: [step(i, exchange) for i in range(G)]
+            reps = max(1, (args.steps + G - 1) // G)
+            for _ in range(max(1, args.warmup // G + 1)):
+                run()
+            barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(reps):
+                run()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ms = max_over_ranks(a.elapsed_time(b))
+            barrier()
+            return ms, reps * G, launch
+
+        ms, steps, launch = timed(EXCHANGE if scheme == "range" else "all_to_all")
+        p2p = None
+        if scheme == "range" and nccl and EXCHANGE != "p2p":
+            # the peer-memory exchange beside it, when every rank can map its
+            # peers' symmetric buffers (agreed by an all-reduce first)
+            ok = torch.tensor([1], dtype=torch.int32, device=dev)
+            try:
+                import torch.distributed._symmetric_memory as symm_mem
+
+                probe = symm_mem.empty((16,), dtype=torch.int64, device=dev)
+                symm_mem.rendezvous(probe, dist.group.WORLD)
+            except Exception:
+                ok.zero_()
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if int(ok.item()):
+                p_ms, p_steps, p_launch = timed("p2p")
+                p2p = {"value": world * BATCH * p_steps / (p_ms / 1e3), "unit": "queries/s",
+                       "steps": p_steps, "ms_per_step": p_ms / p_steps, "launch": p_launch,
+                       "exchange": "p2p: symmetric-memory candidates, signal + merge kernel reading the peers"}
+            else:
+                p2p = {"unavailable": "symmetric memory rendezvous failed on some rank"}
+        elif scheme == "range" and world == 1:  # the same kernels, the one rank its own peer
+            p_ms, p_steps, p_launch = timed("p2p")
+            p2p = {"value": BATCH * p_steps / (p_ms / 1e3), "unit": "queries/s", "steps": p_steps,
+                   "ms_per_step": p_ms / p_steps, "launch": p_launch,
+                   "exchange": "p2p kernels (signal + merge reading the candidate buffer), one rank"}
         # end to end: each step copies the rank's pinned client batch in and
         # its merged answers out (wall clock, max over ranks)
         from paper_2602_04936_b200._native import PinnedArray
@@ -667,7 +701,6 @@ def config5_leg(args, world, rank, dev, barrier, max_over_ranks, scheme: str = "
             stream.synchronize()
         e_el = max_over_ranks(time.perf_counter() - t_e)
         barrier()
-    steps = reps * per_run
     e2e = {"value": world * BATCH * e_steps / e_el, "unit": "queries/s", "steps": e_steps,
            "ms_per_step": 1e3 * e_el / e_steps, "h2d_bytes_per_step": BATCH * SEQ_LEN * 2,
            "d2h_bytes_per_step": int(sum(t.numel() * t.element_size() for t in out)),
@@ -676,7 +709,8 @@ def config5_leg(args, world, rank, dev, barrier, max_over_ranks, scheme: str = "
     return {"value": world * BATCH * steps / (ms / 1e3), "unit": "queries/s", "steps": steps, "e2e": e2e,
             "ms_per_step": ms / steps, "n_items_total": n_total, "n_items_local": int(n_local),
             "scheme": scheme, "batch_per_rank": BATCH, "launch": launch,
-            "gen_s": round(gen_s, 2), "build_s": round(build_s, 2),
+            "exchange": EXCHANGE if scheme == "range" else "all_to_all",
+            "gen_s": round(gen_s, 2), "build_s": round(build_s, 2), "p2p": p2p,
             "parallelism": (f"{scheme} shards x{world}: all_gather client batches, device routing, "
                             "local top-k, NCCL exchange, k_merge" if scheme == "range" else
                             f"row-block shards x{world}: all_gather client batches, every shard answers, "

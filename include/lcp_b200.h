@@ -254,6 +254,23 @@ int lcp_encode_candidates_sel(const uint32_t* ids, const uint16_t* lcps, const i
                               int32_t in_stride, int32_t length, const int64_t* gids,
                               int64_t id_offset, uint64_t* cand, void* stream);
 
+/* Candidate exchange over NVLink peer memory (symmetric allocations mapped
+ * into every rank; replaces the all-to-all + merge of a sharded step).
+ * peer_signals / peer_cand: device arrays of `world` device pointers (rank
+ * s's signal array of world u32 / candidate buffer of batch rows x k u64).
+ * signal_peers : bump *epoch (device u32) and store it, behind a system fence,
+ *                into slot [rank] of every peer's signal array.
+ * merge_candidates_peers: wait until my_signals[s] >= *epoch for every s, then
+ *                merge rows [rank*m, (rank+1)*m) of every peer's candidates
+ *                (read over NVLink) into ids/lcps (row stride out_stride) and
+ *                hits, like lcp_merge_candidates (take <= 32). */
+int lcp_signal_peers(uint32_t* const* peer_signals, int32_t world, int32_t rank, uint32_t* epoch,
+                     void* stream);
+int lcp_merge_candidates_peers(const uint64_t* const* peer_cand, int32_t world, int32_t rank, int32_t m,
+                               int32_t k, int32_t take, int32_t length, int32_t strict,
+                               const uint32_t* my_signals, const uint32_t* epoch, uint32_t* ids,
+                               uint16_t* lcps, int32_t* hits, int32_t out_stride, void* stream);
+
 /* ---- host staging (no reference counterpart) -----------------------------
  * Page-locked host buffers so *_host calls DMA directly (cudaHostAlloc). */
 int lcp_pinned_alloc(int64_t bytes, void** out);

@@ -1923,6 +1923,32 @@ int lcp_encode_candidates_sel(const uint32_t* ids, const uint16_t* lcps, const i
   return LCP_OK;
 }
 
+int lcp_signal_peers(uint32_t* const* peer_signals, int32_t world, int32_t rank, uint32_t* epoch,
+                     void* stream) {
+  if (!peer_signals || !epoch || world < 1 || rank < 0 || rank >= world)
+    return fail(LCP_ERR_INVALID_INPUT, "bad peer signal arguments");
+  k_signal_peers<<<1, 32, 0, (cudaStream_t)stream>>>(reinterpret_cast<unsigned* const*>(peer_signals),
+                                                     world, rank, epoch);
+  LCP_CK_LAUNCH();
+  return LCP_OK;
+}
+
+int lcp_merge_candidates_peers(const uint64_t* const* peer_cand, int32_t world, int32_t rank, int32_t m,
+                               int32_t k, int32_t take, int32_t length, int32_t strict,
+                               const uint32_t* my_signals, const uint32_t* epoch, uint32_t* ids,
+                               uint16_t* lcps, int32_t* hits, int32_t out_stride, void* stream) {
+  if (m <= 0) return LCP_OK;
+  if (!peer_cand || !my_signals || !epoch || world < 1 || rank < 0 || rank >= world)
+    return fail(LCP_ERR_INVALID_INPUT, "bad peer merge arguments");
+  if (k < 1 || take < 0 || take > k || take > FAST_KMAX)
+    return fail(LCP_ERR_INVALID_INPUT, "peer merge needs 0 <= take <= k and take <= 32");
+  k_merge_peers<<<blocks_for((long long)m * 32, 256), 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const u64* const*>(peer_cand), world, rank, m, k, take, length, strict,
+      my_signals, epoch, ids, lcps, hits, std::max(1, out_stride));
+  LCP_CK_LAUNCH();
+  return LCP_OK;
+}
+
 int lcp_pinned_alloc(int64_t bytes, void** out) {
   if (!out || bytes < 0) return fail(LCP_ERR_INVALID_INPUT, "bad pinned allocation request");
   *out = nullptr;

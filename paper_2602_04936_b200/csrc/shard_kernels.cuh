@@ -113,3 +113,94 @@ __global__ void k_encode_sel(const u32* __restrict__ ids, const uint16_t* __rest
   }
   cand[q * k + j] = c;
 }
+
+// ---------------------------------------------------------------------------
+// Candidate exchange over NVLink peer memory (replaces the NCCL all-to-all +
+// merge of a sharded step).  Every rank's candidate buffer (batch rows x k
+// u64) and a per-rank signal array (world u32) live in symmetric memory (one
+// allocation per rank, mapped into every peer), so:
+//   k_signal_peers   after a rank's candidates are final: bump its step epoch
+//                    and, behind a system-scope fence, store the epoch into
+//                    slot [rank] of every peer's signal array (NVLink stores);
+//   k_merge_peers    rank r waits until every slot of its own signal array
+//                    holds the current epoch, then merges its own clients'
+//                    rows [r*m, (r+1)*m) by READING each peer's candidates
+//                    directly (NVLink loads) — the exchange and the merge are
+//                    one kernel, and no receive buffer or collective call is
+//                    needed.
+// Reuse is safe without a second barrier: a step's candidates are written
+// only after that step's query all-gather, which no rank completes before
+// every rank has finished the previous step's merge (stream order).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void st_release_sys_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_sys_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void k_signal_peers(unsigned* const* __restrict__ peer_signals, int world, int rank,
+                               unsigned* __restrict__ epoch) {
+  // one thread: the candidates were written by earlier kernels of this stream
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const unsigned e = *epoch + 1u;
+  *epoch = e;
+  __threadfence_system();
+  for (int s = 0; s < world; ++s) st_release_sys_u32(peer_signals[s] + rank, e);
+}
+
+// One warp per query row of this rank's clients (k <= 32: warp top-k, as
+// k_merge); candidate c of shard s for local row q is peer_cand[s][(rank*m + q)*k + c]
+__global__ void __launch_bounds__(256)
+    k_merge_peers(const u64* const* __restrict__ peer_cand, int world, int rank, int m, int k, int take,
+                  int L, int strict, const unsigned* __restrict__ my_signals,
+                  const unsigned* __restrict__ epoch, u32* __restrict__ out_ids,
+                  uint16_t* __restrict__ out_lcps, int* __restrict__ out_hits, int out_stride) {
+  __shared__ int s_ready;
+  if (threadIdx.x == 0) {
+    const unsigned e = *epoch;
+    for (int s = 0; s < world; ++s)
+      while (ld_acquire_sys_u32(my_signals + s) < e) {
+      }
+    s_ready = 1;
+  }
+  __syncthreads();
+  const int lane = lane_id();
+  const long long qi = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (qi >= m) return;
+  const long long row = (long long)rank * m + qi;
+  u64 best = ~0ull;
+  if (strict) {
+    for (int s = 0; s < world; ++s)
+      for (int j = lane; j < k; j += 32) {
+        const u64 c = __ldcv(peer_cand[s] + row * k + j);
+        best = c < best ? c : best;
+      }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const u64 y = __shfl_xor_sync(LCP_FULL_MASK, best, o);
+      best = y < best ? y : best;
+    }
+  }
+  const u64 tier = best >> 32;
+  u64 slot = ~0ull, thr = ~0ull;
+  int valid = 0;
+  for (int s = 0; s < world; ++s) {
+    for (int j0 = 0; j0 < k; j0 += 32) {
+      const int j = j0 + lane;
+      u64 c = j < k ? __ldcv(peer_cand[s] + row * k + j) : ~0ull;  // not cached: peers rewrite it per step
+      if (strict && (c >> 32) != tier) c = ~0ull;
+      valid += __popc(__ballot_sync(LCP_FULL_MASK, c != ~0ull));
+      warp_offer<u64, true>(slot, thr, c, take);
+    }
+  }
+  const int hits = min(take, valid);
+  if (lane < hits) {
+    out_ids[qi * out_stride + lane] = (u32)(slot & 0xffffffffull);
+    out_lcps[qi * out_stride + lane] = (uint16_t)(L - (int)(slot >> 32));
+  }
+  if (lane == 0) out_hits[qi] = hits;
+  (void)s_ready;
+}

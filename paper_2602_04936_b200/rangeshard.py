@@ -401,6 +401,44 @@ class RangeShardedIndex:
                 ws=None)
         return st["bufs"][key]
 
+    def _peer_buffers(self, b, count: int, kk: int, group=None):
+        """Symmetric-memory candidate buffer + signal array for exchange="p2p":
+        every rank's allocation mapped into every peer (NVLink), their peer
+        pointers as device arrays.  Collective on first use (rendezvous).
+        One process without a group: the 'peers' are this rank's own buffers."""
+        import torch
+
+        if "peer" in b:
+            return b["peer"]
+        dev = b["cand"].device
+        c = self.coll
+        if c.local:
+            cand = torch.empty((count, kk), dtype=torch.int64, device=dev)
+            sig = torch.zeros(1, dtype=torch.int32, device=dev)
+            cand_ptrs, sig_ptrs = [cand.data_ptr()], [sig.data_ptr()]
+            keep = (cand, sig)
+        else:
+            import torch.distributed._symmetric_memory as symm_mem
+
+            grp = (c.group if group is None else group) or c.dist.group.WORLD
+            try:
+                symm_mem.enable_symm_mem_for_group(grp.group_name)
+            except Exception:
+                pass
+            cand = symm_mem.empty((count, kk), dtype=torch.int64, device=dev)
+            sig = symm_mem.empty((self.world,), dtype=torch.int32, device=dev)
+            sig.zero_()
+            hc = symm_mem.rendezvous(cand, grp)
+            hs = symm_mem.rendezvous(sig, grp)
+            cand_ptrs, sig_ptrs = list(hc.buffer_ptrs), list(hs.buffer_ptrs)
+            keep = (cand, sig, hc, hs)
+            c.dist.barrier(group=grp)  # every rank's signal array is zeroed
+        b["peer"] = dict(cand=cand, sig=sig, keep=keep,
+                         cand_ptrs=torch.tensor(cand_ptrs, dtype=torch.int64, device=dev),
+                         sig_ptrs=torch.tensor(sig_ptrs, dtype=torch.int64, device=dev),
+                         epoch=torch.zeros(1, dtype=torch.int32, device=dev))
+        return b["peer"]
+
     def query_device(self, queries, k: int, mode: str = "complete", out=None,
                      exchange: str = "all_gather", group=None, slot: int = 0):
         """Global top-k of a broadcast (count, L) uint16 CUDA batch, on the
@@ -424,14 +462,18 @@ class RangeShardedIndex:
         take = max(0, min(int(k), self.n_total))
         if take * self.world > 8192:
             raise InvalidInputError("sharded merge supports world * min(k, n) <= 8192")
-        if exchange not in ("all_gather", "all_to_all"):
+        if exchange not in ("all_gather", "all_to_all", "p2p"):
             raise InvalidInputError(f"unknown exchange {exchange!r}")
         st = self._device_state()
         count, L = int(queries.shape[0]), self.length
-        if exchange == "all_to_all" and count % self.world:
-            raise InvalidInputError("all_to_all exchange needs count divisible by the world size")
+        if exchange != "all_gather" and count % self.world:
+            raise InvalidInputError(f"{exchange} exchange needs count divisible by the world size")
+        if exchange == "p2p" and take > 32:
+            raise InvalidInputError("p2p exchange supports min(k, n) <= 32")
         kk = max(1, take)
         b = self._step_buffers(count, kk, slot)
+        peer = self._peer_buffers(b, count, kk, group) if exchange == "p2p" else None
+        cand = peer["cand"] if peer else b["cand"]  # p2p: candidates live in symmetric memory
         if b["ws"] is None:
             b["ws"] = Workspace()
         ws = b["ws"]
@@ -454,7 +496,7 @@ class RangeShardedIndex:
         def encode(cnt):
             check(lib.lcp_encode_candidates_sel(
                 b["ids"].data_ptr(), b["lcps"].data_ptr(), b["hits"].data_ptr(), b["sel"].data_ptr(),
-                cnt.data_ptr(), count, kk, ls, L, st["gids"].data_ptr(), 0, b["cand"].data_ptr(), stream))
+                cnt.data_ptr(), count, kk, ls, L, st["gids"].data_ptr(), 0, cand.data_ptr(), stream))
 
         # 0. pack the batch once; routing the own queries also resets the
         #    step's thresholds (-1) and candidates (UINT64_MAX)
@@ -464,7 +506,7 @@ class RangeShardedIndex:
         check(lib.lcp_route_queries(native.handle, ws.handle, q.data_ptr(), b["qk"].data_ptr(), count,
                                     st["splitters"].data_ptr(), self.world - 1, None, None, None,
                                     self.rank, b["tq"].data_ptr(), 0, b["rows"].data_ptr(),
-                                    b["sel"].data_ptr(), cnt_own.data_ptr(), b["cand"].data_ptr(), kk,
+                                    b["sel"].data_ptr(), cnt_own.data_ptr(), cand.data_ptr(), kk,
                                     stream))
         answer(cnt_own, expected)
         encode(cnt_own)
@@ -483,8 +525,23 @@ class RangeShardedIndex:
             answer(cnt_con, max(1, count // 16))
             encode(cnt_con)
         # 4. candidates: every rank's for every query (all_gather), or each
-        #    rank's for the queries of rank r's clients to rank r (all_to_all)
+        #    rank's for the queries of rank r's clients to rank r (all_to_all),
+        #    or read straight from the peers' symmetric buffers by the merge
+        #    kernel after a signal (p2p: the exchange and the merge are one kernel)
         m = count if exchange == "all_gather" else count // self.world
+        if exchange == "p2p":
+            if out is None:
+                out = (torch.empty((m, kk), dtype=torch.int32, device=q.device),
+                       torch.empty((m, kk), dtype=torch.int16, device=q.device),
+                       torch.empty(m, dtype=torch.int32, device=q.device))
+            ids, lcps, hits = out
+            check(lib.lcp_signal_peers(peer["sig_ptrs"].data_ptr(), self.world, self.rank,
+                                       peer["epoch"].data_ptr(), stream))
+            check(lib.lcp_merge_candidates_peers(
+                peer["cand_ptrs"].data_ptr(), self.world, self.rank, m, kk, take, L, strict,
+                peer["sig"].data_ptr(), peer["epoch"].data_ptr(), ids.data_ptr(), lcps.data_ptr(),
+                hits.data_ptr(), int(ids.shape[1]), stream))
+            return ids, lcps, hits
         if exchange == "all_gather":
             self._all_gather_into_(b["gathered"], b["cand"], group)
         else:

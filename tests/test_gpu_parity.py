@@ -534,12 +534,16 @@ def _range_gpu_worker(rank, world, port, backend):
                             h = int(hits[i])
                             assert list(zip(ids[i, :h].tolist(), lcps[i, :h].tolist())) == \
                                 list(zip(fids[i, :fhits[i]].tolist(), flcps[i, :fhits[i]].tolist())), (n, k, mode, i)
-            # all_to_all exchange: this rank gets the answers of its slice
+            # all_to_all exchange: this rank gets the answers of its slice (and
+            # the peer-memory exchange, NCCL only: symmetric memory + signals)
             m = len(qs) // world
             mine = slice(rank * m, (rank + 1) * m)
-            for k, mode in ((10, "complete"), (5, "strict"), (40, "complete")):
+            cases = [(10, "complete", "all_to_all"), (5, "strict", "all_to_all"), (40, "complete", "all_to_all")]
+            if backend == "nccl":
+                cases += [(10, "complete", "p2p"), (5, "strict", "p2p"), (32, "complete", "p2p")]
+            for k, mode, exchange in cases:
                 fids, flcps, fhits, _, _, _ = full.query_batch(qs[mine], k, mode)
-                ids, lcps, hits = sh.query_device(dq[: m * world], k, mode, exchange="all_to_all")
+                ids, lcps, hits = sh.query_device(dq[: m * world], k, mode, exchange=exchange)
                 ids, lcps, hits = ids.cpu().long() & 0xFFFFFFFF, lcps.cpu().long() & 0xFFFF, hits.cpu()
                 for i in range(m):
                     h = int(hits[i])
@@ -550,7 +554,7 @@ def _range_gpu_worker(rank, world, port, backend):
                 # in a CUDA graph and replay it
                 s = torch.cuda.Stream()
                 s.wait_stream(torch.cuda.current_stream())
-                for exchange in ("all_gather", "all_to_all"):
+                for exchange in ("all_gather", "all_to_all", "p2p"):
                     with torch.cuda.stream(s):
                         ref = [t.clone() for t in sh.query_device(dq, 10, "complete", exchange=exchange)]
                         out = tuple(torch.empty_like(t) for t in ref)
@@ -954,3 +958,41 @@ def test_rowblock_shard_step_single_process(gpu, oracle_lib):
             h = int(hits[i])
             got = list(zip((ids[i, :h].cpu().long() & 0xFFFFFFFF).tolist(), (lcps[i, :h].cpu().long() & 0xFFFF).tolist()))
             assert got == list(zip(fids[i, :fhits[i]].tolist(), flcps[i, :fhits[i]].tolist())), (k, mode, i)
+
+
+def test_range_shard_p2p_single_process(gpu, oracle_lib):
+    """The peer-memory exchange (signal + merge reading the peers' candidate
+    buffers) in one process without a process group: one range shard whose
+    'peers' are its own buffers, stepped repeatedly (the epoch advances) and
+    replayed from a CUDA graph, equals the oracle."""
+    import torch
+
+    from paper_2602_04936_b200.rangeshard import RangeShardedIndex
+
+    ds = lg.generate_dataset(80_000, 32, 4, seed=71)
+    qs = np.vstack([lg.generate_queries(ds, 256, seed=72), lg.generate_queries(ds, 256, seed=73, prefix_len=16)])
+    dq = torch.from_numpy(qs).cuda()
+    sh = RangeShardedIndex(ds.items, 32, 4, id_offset=0)
+    trie = oracle_lib.OracleTrie(ds.items, 4)
+    for k, mode in ((10, "complete"), (7, "strict"), (32, "complete"), (10, "complete")):
+        fids, flcps, fhits, _, _, _ = trie.query_batch(qs, k, mode)
+        for _ in range(3):
+            ids, lcps, hits = sh.query_device(dq, k, mode, exchange="p2p")
+        ids, lcps, hits = ids.cpu().long() & 0xFFFFFFFF, lcps.cpu().long() & 0xFFFF, hits.cpu()
+        for i in range(len(qs)):
+            h = int(hits[i])
+            assert list(zip(ids[i, :h].tolist(), lcps[i, :h].tolist())) == \
+                list(zip(fids[i, :fhits[i]].tolist(), flcps[i, :fhits[i]].tolist())), (k, mode, i)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        ref = [t.clone() for t in sh.query_device(dq, 10, "complete", exchange="p2p")]
+        out = tuple(torch.empty_like(t) for t in ref)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            sh.query_device(dq, 10, "complete", out=out, exchange="p2p")
+        for _ in range(3):
+            g.replay()
+    torch.cuda.synchronize()
+    for a, b in zip(ref, out):
+        assert torch.equal(a, b)
