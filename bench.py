@@ -678,6 +678,7 @@ def config5_leg(args, world, rank, dev, barrier, max_over_ranks, scheme: str = "
             p2p = {"value": BATCH * p_steps / (p_ms / 1e3), "unit": "queries/s", "steps": p_steps,
                    "ms_per_step": p_ms / p_steps, "launch": p_launch,
                    "exchange": "p2p kernels (signal + merge reading the candidate buffer), one rank"}
+        kernel = kernel_leg(sh.engine.native, pool, dev, stream) if scheme == "range" and world == 1 else None
         # end to end: each step copies the rank's pinned client batch in and
         # its merged answers out (wall clock, max over ranks)
         from paper_2602_04936_b200._native import PinnedArray
@@ -710,11 +711,68 @@ def config5_leg(args, world, rank, dev, barrier, max_over_ranks, scheme: str = "
             "ms_per_step": ms / steps, "n_items_total": n_total, "n_items_local": int(n_local),
             "scheme": scheme, "batch_per_rank": BATCH, "launch": launch,
             "exchange": EXCHANGE if scheme == "range" else "all_to_all",
-            "gen_s": round(gen_s, 2), "build_s": round(build_s, 2), "p2p": p2p,
+            "gen_s": round(gen_s, 2), "build_s": round(build_s, 2), "p2p": p2p, "query_kernel": kernel,
             "parallelism": (f"{scheme} shards x{world}: all_gather client batches, device routing, "
                             "local top-k, NCCL exchange, k_merge" if scheme == "range" else
                             f"row-block shards x{world}: all_gather client batches, every shard answers, "
                             "all_to_all candidates, k_merge")}
+
+
+def kernel_leg(native, pool, dev, stream, n_graph: int = 64, reps: int = 20) -> dict:
+    """The bare query kernel on an index far larger than L2 (config 5 on one
+    GPU: 200M rows, 7 GB): CUDA-graph replays of 4096-query batches, one and
+    four in flight, and the per-launch roofline over the SURVEY §8d
+    algorithmic bytes (|R(d*)| from the kernel's own aux words)."""
+    import torch
+
+    from paper_2602_04936_b200._native import Workspace
+
+    n_pool = pool.shape[0]
+    res = {}
+    aux_all = torch.empty((n_pool, BATCH, 2), dtype=torch.int64, device=dev)
+    for nst in (1, INFLIGHT):
+        streams = [torch.cuda.Stream(device=dev) for _ in range(nst)]
+        wss = [Workspace() for _ in range(nst)]
+        bufs = [(torch.empty((BATCH, K), dtype=torch.int32, device=dev), torch.empty((BATCH, K), dtype=torch.int16, device=dev),
+                 torch.empty(BATCH, dtype=torch.int32, device=dev), torch.empty(BATCH, dtype=torch.int16, device=dev))
+                for _ in range(nst)]
+        with torch.cuda.stream(stream):
+            for b in range(n_pool):
+                native.query_device(pool[b], K, "complete", *bufs[0], aux_all[b], stream=stream.cuda_stream, ws=wss[0])
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                for x in streams:
+                    x.wait_stream(stream)
+                for i in range(n_graph):
+                    j = i % nst
+                    native.query_device(pool[i % n_pool], K, "complete", *bufs[j], aux_all[i % n_pool],
+                                        stream=streams[j].cuda_stream, ws=wss[j])
+                for x in streams:
+                    stream.wait_stream(x)
+            g.workspaces = wss
+            for _ in range(3):
+                g.replay()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(reps):
+                g.replay()
+            b.record(stream)
+            torch.cuda.synchronize()
+        res[nst] = a.elapsed_time(b) / (n_graph * reps)  # ms per batch
+    rsize = (aux_all[:, :, 1].cpu().numpy().astype(np.uint64) & np.uint64(0xFFFFFFFF)).astype(np.int64)
+    per_batch = float(np.mean([indexed_bytes_per_query(native.n, SEQ_LEN, SIGMA, K, rsize[bb]).sum()
+                               for bb in range(n_pool)]))
+    peak = hbm_peak()[0]
+    return {"n_items": native.n, "one_in_flight_us": round(res[1] * 1e3, 3),
+            f"{INFLIGHT}_in_flight_us": round(res[INFLIGHT] * 1e3, 3),
+            "qps_one_in_flight": BATCH / (res[1] / 1e3), f"qps_{INFLIGHT}_in_flight": BATCH / (res[INFLIGHT] / 1e3),
+            "bytes_per_launch": round(per_batch, 1),
+            "roofline_frac_per_launch": round(per_batch / (res[1] / 1e3) / 1e9 / peak, 5),
+            "roofline_frac_pipelined": round(per_batch / (res[INFLIGHT] / 1e3) / 1e9 / peak, 5),
+            "note": "k_query_w1<u64,2,1> (ids need 28 bits), index 7 GB >> L2: every search block and leaf "
+                    "region read comes from DRAM"}
 
 
 def cold_batch_latency(idx, dq, dev) -> float:

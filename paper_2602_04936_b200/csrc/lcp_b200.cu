@@ -322,14 +322,16 @@ struct lcp_index {
 // replayed with a single cudaGraphLaunch when the same buffers come back.
 // `epoch` is the workspace's scratch epoch at capture: a graph bakes in the
 // device scratch pointers, so once any scratch buffer moved it must not replay.
+// A graph holds device work only (the flag reset and the query kernels over
+// workspace scratch); the host<->device copies are issued around it per call,
+// so no graph ever references caller memory (a freed and reallocated host
+// block at the same address crashed cuGraphLaunch when the copies were nodes).
 struct GraphKey {
   unsigned long long gen, epoch;
-  const void* queries;
-  void* out;
   int count, k, mode, stride;
   bool operator==(const GraphKey& o) const {
-    return gen == o.gen && epoch == o.epoch && queries == o.queries && out == o.out &&
-           count == o.count && k == o.k && mode == o.mode && stride == o.stride;
+    return gen == o.gen && epoch == o.epoch && count == o.count && k == o.k && mode == o.mode &&
+           stride == o.stride;
   }
 };
 struct CachedGraph {
@@ -1568,60 +1570,56 @@ int lcp_query_host_packed_async(const lcp_index* ix, lcp_workspace* ws, const ui
   LCP_TRY(ws->ids.ensure((size_t)lay.total));
   LCP_TRY(ws->qkeys.ensure((size_t)count * dv.W * 8));
   ws->prune_stale_graphs();
-  const GraphKey key{ix->generation, ws->epoch(), queries, out_block, count, k,
-                     mode | (flags << 8), out_stride};
-  for (auto& g : ws->graphs) {
-    if (g.key == key) {  // replay: one launch for the whole submission
-      g.last_use = ws->tick;
-      LCP_CK(cudaGraphLaunch(g.exec, st));
-      LCP_CK(cudaEventRecord(ws->done, st));
-      ws->pending = true;
-      ws->pending_sigma = dv.sigma;
-      ws->pending_err = reinterpret_cast<const int*>(static_cast<const char*>(out_block) + lay.err);
-      return LCP_OK;
-    }
-  }
+  const GraphKey key{ix->generation, ws->epoch(), count, k, mode | (flags << 8), out_stride};
   char* d = static_cast<char*>(ws->ids.p);
-  // one H2D, the kernel, one D2H: the invalid-query flag lives in the block
-  // (lay.err), cleared on the device, so no separate small copy is needed
-  auto enqueue = [&]() -> int {
-    LCP_CK(cudaMemcpyAsync(ws->q_in.p, queries, qb, cudaMemcpyHostToDevice, st));
-    LCP_CK(cudaMemsetAsync(d + lay.err, 0, 8, st));
-    LCP_TRY(query_impl(ix, ws, ws->q_in.as<uint16_t>(), count, k, mode, out_stride,
-                       reinterpret_cast<uint32_t*>(d + lay.ids),
-                       reinterpret_cast<uint16_t*>(d + lay.lcps),
-                       reinterpret_cast<int32_t*>(d + lay.hits),
-                       reinterpret_cast<uint16_t*>(d + lay.matched_depth),
-                       reinterpret_cast<uint64_t*>(d + lay.aux), st, reinterpret_cast<int*>(d + lay.err)));
-    LCP_CK(cudaMemcpyAsync(out_block, d, d2h, cudaMemcpyDeviceToHost, st));
-    return LCP_OK;
-  };
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t exec = nullptr;
-  bool captured = false;
-  if (!no_graphs && cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
-    const int r = enqueue();
-    const cudaError_t e = cudaStreamEndCapture(st, &graph);
-    if (r == LCP_OK && e == cudaSuccess && graph &&
-        cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess)
-      captured = true;
-    if (graph) cudaGraphDestroy(graph);
-    cudaGetLastError();  // a failed capture leaves nothing enqueued
-  }
-  if (captured) {
-    if ((int)ws->graphs.size() >= kGraphCache) {
-      auto old = std::min_element(ws->graphs.begin(), ws->graphs.end(),
-                                  [](const CachedGraph& a, const CachedGraph& b) {
-                                    return a.last_use < b.last_use;
-                                  });
-      cudaGraphExecDestroy(old->exec);
-      ws->graphs.erase(old);
-    }
-    ws->graphs.push_back({key, exec, ws->tick});
-    LCP_CK(cudaGraphLaunch(exec, st));
+  // one H2D, the device work (graph-cached), one D2H: the invalid-query flag
+  // lives in the block (lay.err), cleared on the device, so no separate small
+  // copy is needed
+  LCP_CK(cudaMemcpyAsync(ws->q_in.p, queries, qb, cudaMemcpyHostToDevice, st));
+  CachedGraph* hit = nullptr;
+  for (auto& g : ws->graphs)
+    if (g.key == key) hit = &g;
+  if (hit) {  // replay: one launch for the flag reset + query kernels
+    hit->last_use = ws->tick;
+    LCP_CK(cudaGraphLaunch(hit->exec, st));
   } else {
-    LCP_TRY(enqueue());
+    auto device_work = [&]() -> int {
+      LCP_CK(cudaMemsetAsync(d + lay.err, 0, 8, st));
+      return query_impl(ix, ws, ws->q_in.as<uint16_t>(), count, k, mode, out_stride,
+                        reinterpret_cast<uint32_t*>(d + lay.ids),
+                        reinterpret_cast<uint16_t*>(d + lay.lcps),
+                        reinterpret_cast<int32_t*>(d + lay.hits),
+                        reinterpret_cast<uint16_t*>(d + lay.matched_depth),
+                        reinterpret_cast<uint64_t*>(d + lay.aux), st, reinterpret_cast<int*>(d + lay.err));
+    };
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    bool captured = false;
+    if (!no_graphs && cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+      const int r = device_work();
+      const cudaError_t e = cudaStreamEndCapture(st, &graph);
+      if (r == LCP_OK && e == cudaSuccess && graph &&
+          cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess)
+        captured = true;
+      if (graph) cudaGraphDestroy(graph);
+      cudaGetLastError();  // a failed capture leaves nothing enqueued
+    }
+    if (captured) {
+      if ((int)ws->graphs.size() >= kGraphCache) {
+        auto old = std::min_element(ws->graphs.begin(), ws->graphs.end(),
+                                    [](const CachedGraph& a, const CachedGraph& b) {
+                                      return a.last_use < b.last_use;
+                                    });
+        cudaGraphExecDestroy(old->exec);
+        ws->graphs.erase(old);
+      }
+      ws->graphs.push_back({key, exec, ws->tick});
+      LCP_CK(cudaGraphLaunch(exec, st));
+    } else {
+      LCP_TRY(device_work());
+    }
   }
+  LCP_CK(cudaMemcpyAsync(out_block, d, d2h, cudaMemcpyDeviceToHost, st));
   LCP_CK(cudaEventRecord(ws->done, st));
   ws->pending = true;
   ws->pending_sigma = dv.sigma;

@@ -208,6 +208,31 @@ class NativeIndex:
             cache.buf = buf
         return buf[1]
 
+    def query_single(self, query: np.ndarray, k: int, mode: str) -> BatchResult:
+        """One validated (L,) uint16 query, synchronously, with the lowest
+        latency: the row is copied into this thread's page-locked staging row
+        and submitted through the async packed entry point on the thread's
+        workspace, whose graph cache turns H2D + kernel + D2H into a single
+        graph launch from the second call on (stable staging / output
+        pointers); then waits.  Returns the thread's reused one-row block."""
+        if mode not in MODES:
+            raise InvalidInputError(f"unknown mode {mode!r}")
+        if k < 1:
+            raise InvalidInputError(f"k must be >= 1, got {k}")
+        out = self.single_query_buffer(k, mode)
+        cache = self._single
+        stage = getattr(cache, "stage", None)
+        if stage is None or stage.shape[1] != self.length:
+            stage = cache.stage = PinnedArray((1, self.length), np.uint16).array
+        stage[0] = query
+        out.mode = mode
+        ws = workspace()
+        packed = out._packed
+        check(load().lcp_query_host_packed_async(self._h, ws.handle, ptr(stage), 1, self.stride_for(k),
+                                                 MODES[mode], packed[2], packed[0], 0))
+        check(load().lcp_workspace_wait(ws.handle))
+        return out
+
     def query_host(self, queries: np.ndarray, k: int, mode: str,
                    out: BatchResult | None = None) -> BatchResult:
         """Synchronous batched query through lcp_query_host (H2D + kernel + D2H)."""

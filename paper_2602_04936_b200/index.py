@@ -200,8 +200,7 @@ class TrieIndex:
         if k < 1:
             raise InvalidInputError(f"k must be >= 1, got {k}")
         query = self._validate_query(q)
-        out = self._native.query_host(query.reshape(1, -1), k, mode,
-                                      out=self._native.single_query_buffer(k, mode))
+        out = self._native.query_single(query, k, mode)
         if work is not None:
             self._account(out, mode, work)
         return out.result(0)

@@ -996,3 +996,31 @@ def test_range_shard_p2p_single_process(gpu, oracle_lib):
     torch.cuda.synchronize()
     for a, b in zip(ref, out):
         assert torch.equal(a, b)
+
+
+def test_single_query_alternating_k_and_freed_blocks(gpu):
+    """TrieIndex.query through the graph-cached submission with k changing
+    every call (a new one-row output block each time, the old one freed and
+    its address reused) and explicitly freed / re-allocated pinned blocks on
+    the async API: results equal the batch API.  The async graph cache used
+    to bake the caller's host pointers into the graph; replaying it after a
+    free and reallocation at the same address crashed in cuGraphLaunch."""
+    import gc
+
+    ds = lg.generate_dataset(5_000, 12, 3, seed=81)
+    idx = lg.build(ds)
+    qs = lg.generate_queries(ds, 90, seed=82)
+    ref = {(k, m): idx.query_batch(qs, k, m) for k in (1, 5, 50) for m in ("strict", "complete")}
+    for rep in range(3):
+        for i, q in enumerate(qs):
+            k = (1, 5, 50)[(i + rep) % 3]
+            for m in ("strict", "complete"):
+                assert idx.query(q, k, m).pairs() == ref[(k, m)].pairs(i), (rep, i, k, m)
+        gc.collect()
+    for rep in range(4):  # async API: fresh pinned blocks every round
+        out = idx.native.alloc_batch(len(qs), 5 if rep % 2 else 50, "complete", pinned=True)
+        res = idx.query_batch_async(qs, 5 if rep % 2 else 50, "complete", out=out).result()
+        exp = ref[(5 if rep % 2 else 50, "complete")]
+        assert np.array_equal(res.hits, exp.hits) and np.array_equal(res.ids, exp.ids)
+        del out, res
+        gc.collect()
