@@ -1268,7 +1268,11 @@ static void launch_fast(const DevIndex& dv, const uint16_t* q, int count, int gc
       return e ? std::max(1ll, std::min(16ll, atoll(e))) : 1ll;
     }();
     const long long units = (gcount + qpw - 1) / qpw;
-    long long wpc = std::min<long long>(32, std::max<long long>(wpc_min, (units + sms - 1) / sms));
+    static const long long wpc_max = [] {  // LCP_WPC_MAX: A/B hook (warps per CTA cap)
+      const char* e = getenv("LCP_WPC_MAX");
+      return e ? std::max(1ll, std::min(32ll, atoll(e))) : 32ll;
+    }();
+    long long wpc = std::min<long long>(wpc_max, std::max<long long>(wpc_min, (units + sms - 1) / sms));
     const unsigned block = (unsigned)(wpc * 32);
     unsigned grid = (unsigned)std::min<long long>((units + wpc - 1) / wpc, 4ll * sms);
     size_t smem = 16 + (size_t)dv.smem_entries * 8;
