@@ -193,3 +193,32 @@ def test_row_block_generator_matches_full_dataset():
         for lo in range(0, n, max(step, n // 7 // step * step)):
             hi = min(n, lo + 123)
             assert np.array_equal(generate_row_block(n, L, sigma, seed, lo, hi), full[lo:hi]), (n, L, lo)
+
+
+def test_pack_keys_host_matches_encoding_and_roundtrips():
+    """rangeshard.pack_keys_host (the splitters / shard boundaries routing reads
+    on the device) uses the extension's key encoding: ordering of packed keys
+    equals the lexicographic order of the rows, and unpack inverts it."""
+    from paper_2602_04936_b200.rangeshard import pack_keys_host, unpack_keys_host
+
+    rng = np.random.default_rng(5)
+    for L, sigma in ((32, 4), (24, 4), (16, 2), (20, 65536), (7, 256), (100, 3), (1, 2)):
+        rows = rng.integers(0, sigma, size=(300, L)).astype(np.uint16)
+        keys = pack_keys_host(rows, L, sigma)
+        assert np.array_equal(unpack_keys_host(keys, L, sigma), rows)
+        order_rows = np.lexsort(rows.T[::-1])
+        order_keys = np.lexsort(keys.T[::-1])
+        assert np.array_equal(rows[order_rows], rows[order_keys])
+
+
+def test_bench_arms_share_one_config():
+    """bench.py: the reference arm and the repo arm name the same workload
+    (one bench_config function), so the driver's ratio compares like with like."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    assert mod.bench_config(1) == mod.bench_config(1)
+    src = open(os.path.join(ROOT, "bench.py")).read()
+    assert src.count('"config": bench_config(') == 2
