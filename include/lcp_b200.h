@@ -166,7 +166,12 @@ int lcp_query_host_packed(const lcp_index* index, lcp_workspace* ws, const uint1
  * and the single D2H copy on the workspace's stream and returns at once.  The
  * host buffers must stay untouched until lcp_workspace_wait(ws) returns.  At
  * most one batch in flight per workspace; use several workspaces to overlap
- * consecutive batches (transfers, kernels and host work run concurrently). */
+ * consecutive batches (transfers, kernels and host work run concurrently).
+ * Batches of up to 1024 queries (LCP_DIRECT_IO_MAX) whose query rows and
+ * output block both lie in lcp_pinned_alloc blocks skip the copies: the
+ * kernel reads the rows from and writes the results into host memory
+ * directly, which halves a small batch's round trip.  lcp_query_host_packed
+ * is this call followed by lcp_workspace_wait. */
 #define LCP_PACKED_NO_WORK 1 /* flags: skip matched_depth/aux in the D2H copy */
 int lcp_query_host_packed_async(const lcp_index* index, lcp_workspace* ws,
                                 const uint16_t* queries, int32_t count, int32_t k, int32_t mode,
@@ -272,7 +277,8 @@ int lcp_merge_candidates_peers(const uint64_t* const* peer_cand, int32_t world, 
                                uint16_t* lcps, int32_t* hits, int32_t out_stride, void* stream);
 
 /* ---- host staging (no reference counterpart) -----------------------------
- * Page-locked host buffers so *_host calls DMA directly (cudaHostAlloc). */
+ * Page-locked, device-mapped host buffers (cudaHostAlloc): *_host calls DMA
+ * directly, and small packed batches in them use direct host I/O. */
 int lcp_pinned_alloc(int64_t bytes, void** out);
 int lcp_pinned_free(void* p);
 /* Synchronise a stream (cudaStream_t as void*). */

@@ -10,6 +10,7 @@ from __future__ import annotations
 import glob
 import os
 import subprocess
+import sysconfig
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
@@ -37,7 +38,27 @@ def needs_build() -> bool:
     return any(os.path.getmtime(f) > t for f in _sources())
 
 
+HOST_SRC = os.path.join(CSRC, "host_submit.c")
+HOST_OUT = os.path.join(HERE, "_lcp_host" + (sysconfig.get_config_var("EXT_SUFFIX") or ".so"))
+
+
+def build_host(force: bool = False, verbose: bool = False) -> str:
+    """The CPython fast path for async submissions (csrc/host_submit.c)."""
+    if not force and os.path.exists(HOST_OUT) and os.path.getmtime(HOST_OUT) >= os.path.getmtime(HOST_SRC):
+        return HOST_OUT
+    cc = os.environ.get("CC", "gcc")
+    tmp = HOST_OUT + ".tmp"
+    cmd = [cc, "-O2", "-shared", "-fPIC", "-std=c11", "-Wall", "-Wextra",
+           "-I", sysconfig.get_paths()["include"], "-o", tmp, HOST_SRC]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.run(cmd, check=True)
+    os.replace(tmp, HOST_OUT)
+    return HOST_OUT
+
+
 def build_native(force: bool = False, verbose: bool = False) -> str:
+    build_host(force, verbose)
     if not force and not needs_build():
         return OUT
     nvcc = os.environ.get("NVCC", "nvcc")

@@ -130,6 +130,28 @@ def load() -> ctypes.CDLL:
         return lib
 
 
+_host_submit = False  # not yet looked up
+
+
+def host_submit():
+    """submit() of the CPython fast path (csrc/host_submit.c) bound to the
+    loaded library's lcp_query_host_packed_async, or None when the module is
+    not built (the ctypes call is then used; same entry point, same results)."""
+    global _host_submit
+    if _host_submit is False:
+        fn = None
+        if not os.environ.get("LCP_NO_HOST_EXT"):  # A/B switch
+            try:
+                from . import _lcp_host
+            except ImportError:
+                _lcp_host = None
+            if _lcp_host is not None:
+                _lcp_host.bind(ctypes.cast(load().lcp_query_host_packed_async, ctypes.c_void_p).value)
+                fn = _lcp_host.submit
+        _host_submit = fn
+    return _host_submit
+
+
 def last_error() -> str:
     msg = load().lcp_last_error()
     return msg.decode("utf-8", "replace") if msg else ""
@@ -168,6 +190,7 @@ class Workspace:
         h = ctypes.c_void_p()
         check(lib.lcp_workspace_create(ctypes.byref(h)))
         self.handle = h
+        self.address = int(h.value)  # for the fast submission path
         self.submitted = 0  # async batches submitted on this workspace
         self.completed = 0  # ... and waited for
 

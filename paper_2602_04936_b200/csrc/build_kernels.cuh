@@ -32,7 +32,7 @@ __global__ void k_pack(const uint16_t* __restrict__ rows, long long n, int L, in
     bad |= (int)s >= sigma;
     acc |= (u64)s << (64 - b * (j - j0 + 1));
   }
-  if (bad) atomicOr(err, 1);
+  if (bad) raise_flag(err);
   keys[t] = acc;
   if (ids != nullptr && w == 0) ids[row] = (u32)row;
 }
@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(PK_THREADS) k_pack_stream(
       if (ids != nullptr && ok[t] && j[t] == 0) ids[row[t]] = (u32)row[t];
     }
   }
-  if (__any_sync(LCP_FULL_MASK, bad) && lane == 0) atomicOr(err, 1);
+  if (__any_sync(LCP_FULL_MASK, bad) && lane == 0) raise_flag(err);
 }
 
 // Aligned streaming pack, the common shapes (B = bits per symbol as a
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(PK_THREADS) k_pack_aligned(
     }
   }
   const u32 m = max(vmax & 0xffffu, vmax >> 16);
-  if (__any_sync(LCP_FULL_MASK, (int)m >= sigma) && lane == 0) atomicOr(err, 1);
+  if (__any_sync(LCP_FULL_MASK, (int)m >= sigma) && lane == 0) raise_flag(err);
 }
 
 // hi / lo 32-bit planes of each key's first word (full-scan layout)

@@ -60,6 +60,11 @@ struct DevIndex {
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
+// raise an invalid-input flag: every writer stores 1, so a plain store is
+// enough — and it is valid on mapped host memory (a result block the kernel
+// writes directly), where device atomics are not guaranteed
+__device__ __forceinline__ void raise_flag(int* f) { *reinterpret_cast<volatile int*>(f) = 1; }
+
 // 16-byte streaming load of read-only data that is used once (no L1 allocation)
 __device__ __forceinline__ uint4 ld_stream16(const void* p) {
   uint4 v;

@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <map>
 #include <mutex>
 #include <cstdio>
 #include <string>
@@ -329,9 +330,13 @@ struct lcp_index {
 struct GraphKey {
   unsigned long long gen, epoch;
   int count, k, mode, stride;
+  // direct host I/O (small batches): the page-locked query / result blocks the
+  // kernels read and write; null when the submission copies through scratch
+  const void* hq;
+  const void* ho;
   bool operator==(const GraphKey& o) const {
     return gen == o.gen && epoch == o.epoch && count == o.count && k == o.k && mode == o.mode &&
-           stride == o.stride;
+           stride == o.stride && hq == o.hq && ho == o.ho;
   }
 };
 struct CachedGraph {
@@ -340,6 +345,26 @@ struct CachedGraph {
   unsigned long long last_use;
 };
 constexpr int kGraphCache = 16;
+
+// Live lcp_pinned_alloc blocks: base -> (bytes, device alias).  Direct host I/O
+// is used only for ranges inside one of them, so a kernel never dereferences
+// host memory that is not page-locked and mapped.
+struct PinnedBlock {
+  size_t bytes;
+  void* dev;
+};
+static std::mutex g_pinned_mu;
+static std::map<uintptr_t, PinnedBlock> g_pinned;
+
+static char* pinned_device_alias(const void* p, size_t bytes) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  std::lock_guard<std::mutex> g(g_pinned_mu);
+  auto it = g_pinned.upper_bound(a);
+  if (it == g_pinned.begin()) return nullptr;
+  --it;
+  if (!it->second.dev || a + bytes > it->first + it->second.bytes) return nullptr;
+  return static_cast<char*>(it->second.dev) + (a - it->first);
+}
 
 struct lcp_workspace {
   cudaStream_t stream = nullptr;
@@ -1525,31 +1550,10 @@ int lcp_packed_layout_for(int32_t count, int32_t out_stride, lcp_packed_layout* 
 int lcp_query_host_packed(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries,
                           int32_t count, int32_t k, int32_t mode, int32_t out_stride,
                           void* out_block) {
-  if (!ix || !ws) return fail(LCP_ERR_INVALID_INPUT, "null index or workspace");
-  if (count <= 0) return LCP_OK;
-  if (out_stride < 1 || !out_block || !queries)
-    return fail(LCP_ERR_INVALID_INPUT, "bad output block or queries");
-  const DevIndex& dv = ix->dv;
-  cudaStream_t st = ws->stream;
-  const lcp_packed_layout lay = packed_layout(count, out_stride);
-  const size_t qb = (size_t)count * dv.L * 2;
-  LCP_TRY(ws->q_in.ensure(qb));
-  LCP_TRY(ws->ids.ensure((size_t)lay.total));  // device mirror of the packed block
-  char* d = static_cast<char*>(ws->ids.p);
-  LCP_CK(cudaMemcpyAsync(ws->q_in.p, queries, qb, cudaMemcpyHostToDevice, st));
-  LCP_CK(cudaMemsetAsync(d + lay.err, 0, 8, st));
-  LCP_TRY(query_impl(ix, ws, ws->q_in.as<uint16_t>(), count, k, mode, out_stride,
-                     reinterpret_cast<uint32_t*>(d + lay.ids),
-                     reinterpret_cast<uint16_t*>(d + lay.lcps),
-                     reinterpret_cast<int32_t*>(d + lay.hits),
-                     reinterpret_cast<uint16_t*>(d + lay.matched_depth),
-                     reinterpret_cast<uint64_t*>(d + lay.aux), st, reinterpret_cast<int*>(d + lay.err)));
-  LCP_CK(cudaMemcpyAsync(out_block, d, (size_t)lay.total, cudaMemcpyDeviceToHost, st));
-  LCP_CK(cudaStreamSynchronize(st));
-  if (*reinterpret_cast<const int*>(static_cast<const char*>(out_block) + lay.err))
-    return fail(LCP_ERR_INVALID_INPUT,
-                "query symbol out of range for alphabet of size " + std::to_string(dv.sigma));
-  return LCP_OK;
+  // the asynchronous submission (graph-cached device work; direct host I/O for
+  // small batches in lcp_pinned_alloc blocks) followed by its wait
+  LCP_TRY(lcp_query_host_packed_async(ix, ws, queries, count, k, mode, out_stride, out_block, 0));
+  return lcp_workspace_wait(ws);
 }
 
 int lcp_query_host_packed_async(const lcp_index* ix, lcp_workspace* ws, const uint16_t* queries,
@@ -1574,28 +1578,54 @@ int lcp_query_host_packed_async(const lcp_index* ix, lcp_workspace* ws, const ui
   LCP_TRY(ws->ids.ensure((size_t)lay.total));
   LCP_TRY(ws->qkeys.ensure((size_t)count * dv.W * 8));
   ws->prune_stale_graphs();
-  const GraphKey key{ix->generation, ws->epoch(), count, k, mode | (flags << 8), out_stride};
   char* d = static_cast<char*>(ws->ids.p);
-  // one H2D, the device work (graph-cached), one D2H: the invalid-query flag
-  // lives in the block (lay.err), cleared on the device, so no separate small
-  // copy is needed
-  LCP_CK(cudaMemcpyAsync(ws->q_in.p, queries, qb, cudaMemcpyHostToDevice, st));
+  // Small batches whose query and result blocks come from lcp_pinned_alloc:
+  // the kernel reads the queries from, and writes the results into, host
+  // memory directly (mapped page-locked memory over PCIe).  A round trip then
+  // has no copy-engine work at all — the two copies' setup and the
+  // copy -> kernel -> copy hand-offs were most of a single query's latency.
+  // Large batches keep the copies: thousands of small PCIe transactions per
+  // batch cost more than two bulk copies.
+  static const int zc_max = [] {
+    const char* e = getenv("LCP_DIRECT_IO_MAX");
+    return e ? atoi(e) : 1024;  // tools/e2e_probe.py, tools/latency_probe.py
+  }();
+  char* zq = nullptr;
+  char* zo = nullptr;
+  if (count <= zc_max && dv.n > 0 && dv.W <= 8 && k <= FAST_KMAX) {  // kernels that read rows / write slots directly
+    zq = pinned_device_alias(queries, qb);
+    zo = zq ? pinned_device_alias(out_block, d2h) : nullptr;
+  }
+  const bool direct = zq && zo;
+  const GraphKey key{ix->generation, ws->epoch(), count, k, mode | (flags << 8), out_stride,
+                     direct ? queries : nullptr, direct ? out_block : nullptr};
+  if (direct) {
+    // the kernels only ever set the flag, so the host clears it
+    *reinterpret_cast<volatile int*>(static_cast<char*>(out_block) + lay.err) = 0;
+  } else {
+    // one H2D, the device work (graph-cached), one D2H: the invalid-query flag
+    // lives in the block (lay.err), cleared on the device, so no separate small
+    // copy is needed
+    LCP_CK(cudaMemcpyAsync(ws->q_in.p, queries, qb, cudaMemcpyHostToDevice, st));
+  }
+  char* o = direct ? zo : d;
+  // without work counters the block ends before matched_depth: those go to scratch
+  char* ow = direct && !(flags & LCP_PACKED_NO_WORK) ? zo : d;
+  auto device_work = [&]() -> int {
+    if (!direct) LCP_CK(cudaMemsetAsync(d + lay.err, 0, 8, st));
+    return query_impl(ix, ws, direct ? reinterpret_cast<const uint16_t*>(zq) : ws->q_in.as<uint16_t>(),
+                      count, k, mode, out_stride, reinterpret_cast<uint32_t*>(o + lay.ids),
+                      reinterpret_cast<uint16_t*>(o + lay.lcps), reinterpret_cast<int32_t*>(o + lay.hits),
+                      reinterpret_cast<uint16_t*>(ow + lay.matched_depth),
+                      reinterpret_cast<uint64_t*>(ow + lay.aux), st, reinterpret_cast<int*>(o + lay.err));
+  };
   CachedGraph* hit = nullptr;
   for (auto& g : ws->graphs)
     if (g.key == key) hit = &g;
-  if (hit) {  // replay: one launch for the flag reset + query kernels
+  if (hit) {  // replay: one launch for the device work
     hit->last_use = ws->tick;
     LCP_CK(cudaGraphLaunch(hit->exec, st));
   } else {
-    auto device_work = [&]() -> int {
-      LCP_CK(cudaMemsetAsync(d + lay.err, 0, 8, st));
-      return query_impl(ix, ws, ws->q_in.as<uint16_t>(), count, k, mode, out_stride,
-                        reinterpret_cast<uint32_t*>(d + lay.ids),
-                        reinterpret_cast<uint16_t*>(d + lay.lcps),
-                        reinterpret_cast<int32_t*>(d + lay.hits),
-                        reinterpret_cast<uint16_t*>(d + lay.matched_depth),
-                        reinterpret_cast<uint64_t*>(d + lay.aux), st, reinterpret_cast<int*>(d + lay.err));
-    };
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     bool captured = false;
@@ -1623,7 +1653,7 @@ int lcp_query_host_packed_async(const lcp_index* ix, lcp_workspace* ws, const ui
       LCP_TRY(device_work());
     }
   }
-  LCP_CK(cudaMemcpyAsync(out_block, d, d2h, cudaMemcpyDeviceToHost, st));
+  if (!direct) LCP_CK(cudaMemcpyAsync(out_block, d, d2h, cudaMemcpyDeviceToHost, st));
   LCP_CK(cudaEventRecord(ws->done, st));
   ws->pending = true;
   ws->pending_sigma = dv.sigma;
@@ -1954,12 +1984,25 @@ int lcp_merge_candidates_peers(const uint64_t* const* peer_cand, int32_t world, 
 int lcp_pinned_alloc(int64_t bytes, void** out) {
   if (!out || bytes < 0) return fail(LCP_ERR_INVALID_INPUT, "bad pinned allocation request");
   *out = nullptr;
-  LCP_CK(cudaHostAlloc(out, (size_t)std::max<int64_t>(bytes, 1), cudaHostAllocDefault));
+  const size_t size = (size_t)std::max<int64_t>(bytes, 1);
+  LCP_CK(cudaHostAlloc(out, size, cudaHostAllocMapped | cudaHostAllocPortable));
+  void* dev = nullptr;
+  if (cudaHostGetDevicePointer(&dev, *out, 0) != cudaSuccess) {
+    cudaGetLastError();
+    dev = nullptr;  // not device-addressable here: submissions copy instead
+  }
+  std::lock_guard<std::mutex> g(g_pinned_mu);
+  g_pinned[reinterpret_cast<uintptr_t>(*out)] = {size, dev};
   return LCP_OK;
 }
 
 int lcp_pinned_free(void* p) {
-  if (p) LCP_CK(cudaFreeHost(p));
+  if (!p) return LCP_OK;
+  {
+    std::lock_guard<std::mutex> g(g_pinned_mu);
+    g_pinned.erase(reinterpret_cast<uintptr_t>(p));
+  }
+  LCP_CK(cudaFreeHost(p));
   return LCP_OK;
 }
 

@@ -552,7 +552,7 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, MODE == 2 ? 1 : 2)
     if (any_bad) {
       stage_wait(ix, bar);
       if (lane == 0) {
-        atomicOr(err, 1);
+        raise_flag(err);
         out_hits[qi] = 0;
         out_md[qi] = 0;
         out_aux[2 * qi] = 0;
@@ -922,7 +922,7 @@ __global__ void __launch_bounds__(NS > 2 ? QW_MAX_THREADS / 2 : QW_MAX_THREADS, 
     stage_wait(ix, bar);
     if (__any_sync(LCP_FULL_MASK, bad)) {
       if (lane == 0) {
-        atomicOr(err, 1);
+        raise_flag(err);
         out_hits[qi] = 0;
         out_md[qi] = 0;
         out_aux[2 * qi] = 0;
@@ -1124,7 +1124,7 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, 1)
     u64 qk[WMAX];
     if (!warp_pack_query<WMAX>(queries + qi * L, ix, qk)) {
       if (lane == 0) {
-        atomicOr(err, 1);
+        raise_flag(err);
         out_hits[qi] = 0;
         out_md[qi] = 0;
         out_aux[2 * qi] = 0;
@@ -1268,7 +1268,7 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, 1)
     u64 qk[WMAX];
     if (!warp_pack_query<WMAX>(queries + qi * L, ix, qk)) {
       if (lane == 0) {
-        atomicOr(err, 1);
+        raise_flag(err);
         out_hits[qi] = 0;
         out_md[qi] = 0;
         out_aux[2 * qi] = 0;
@@ -1379,7 +1379,7 @@ __global__ void __launch_bounds__(NS > 2 ? QW_MAX_THREADS / 2 : QW_MAX_THREADS, 
     u64 qk[WMAX];
     if (!warp_pack_query<WMAX>(queries + qi * L, ix, qk)) {
       if (lane == 0) {
-        atomicOr(err, 1);
+        raise_flag(err);
         out_hits[qi] = 0;
         out_md[qi] = 0;
         out_aux[2 * qi] = 0;

@@ -271,10 +271,16 @@ class NativeIndex:
         if packed is None or packed[1] != count:
             raise InvalidInputError("async queries need a pinned output block from alloc_batch")
         out.mode = mode
+        h = self.handle
         ws = _native.async_workspace()
-        check(load().lcp_query_host_packed_async(
-            self._h, ws.handle, queries.__array_interface__["data"][0], count,
-            self.stride_for(k), MODES[mode], packed[2], packed[0], out._flags))
+        fast = _native.host_submit()
+        if fast is not None:  # csrc/host_submit.c: the same entry point without ctypes
+            check(fast(h.value, ws.address, queries, self.length, self.stride_for(k), MODES[mode],
+                       packed[2], packed[0], out._flags))
+        else:
+            check(load().lcp_query_host_packed_async(
+                h, ws.handle, queries.__array_interface__["data"][0], count,
+                self.stride_for(k), MODES[mode], packed[2], packed[0], out._flags))
         ws.submitted += 1
         return PendingBatch(ws, ws.submitted, out)
 

@@ -30,6 +30,8 @@ from .engine import NativeIndex
 from .result import BatchResult, QueryResult
 from .work import WorkReport, trie_counters, work_per_symbol
 
+_U16 = np.dtype(np.uint16)  # native-order uint16: the wire format of a query batch
+
 
 @dataclass(frozen=True)
 class TrieNodeView:
@@ -225,7 +227,7 @@ class TrieIndex:
         _native.ASYNC_DEPTH batches per thread overlap copies and kernels."""
         if mode not in ("strict", "complete"):
             raise InvalidInputError(f"mode must be 'strict' or 'complete', got {mode!r}")
-        if (type(queries) is np.ndarray and queries.dtype == np.uint16 and queries.ndim == 2
+        if (type(queries) is np.ndarray and queries.dtype is _U16 and queries.ndim == 2
                 and queries.shape[1] == self.length and queries.flags.c_contiguous):
             qs = queries  # already in the wire format; symbols are checked on the device
         else:

@@ -74,6 +74,23 @@ def test_ctypes_table_covers_header():
     assert sorted(SIGNATURES) == _header_functions()
 
 
+def test_host_submit_module_binds_the_abi_entry_point(native_lib):
+    """csrc/host_submit.c: built, bound to lcp_query_host_packed_async of the
+    loaded library, and it rejects a malformed query batch before any call."""
+    from paper_2602_04936_b200 import _native
+
+    submit = _native.host_submit()
+    assert submit is not None, "the CPython submission module is not built"
+    with pytest.raises(ValueError):  # wrong row length
+        submit(0, 0, np.zeros((4, 31), np.uint16), 32, 10, 1, 10, 0, 0)
+    with pytest.raises(ValueError):  # 4-byte items
+        submit(0, 0, np.zeros((4, 32), np.uint32), 32, 10, 1, 10, 0, 0)
+    with pytest.raises((ValueError, BufferError, TypeError)):  # not C-contiguous
+        submit(0, 0, np.zeros((32, 4), np.uint16).T, 4, 10, 1, 10, 0, 0)
+    with pytest.raises(TypeError):
+        submit(0, 0)
+
+
 def test_library_is_sm100a_only(native_lib):
     from paper_2602_04936_b200._native import LIB_PATH
 

@@ -339,7 +339,14 @@ def test_sharded_index_single_rank_nccl(gpu):
         dist.destroy_process_group()
 
 
-def test_async_pipeline_matches_sync(gpu):
+@pytest.mark.parametrize("path", ["host_ext", "ctypes"])
+def test_async_pipeline_matches_sync(gpu, path, monkeypatch):
+    from paper_2602_04936_b200 import _native
+
+    if path == "ctypes":  # the submission without csrc/host_submit.c
+        monkeypatch.setattr(_native, "_host_submit", None)
+    else:
+        assert _native.host_submit() is not None, "the CPython submission module is not built"
     ds = lg.generate_dataset(100_000, 24, 4, seed=41)
     idx = lg.build(ds)
     batches = [lg.generate_queries(ds, 777, seed=42 + b, prefix_len=b * 3) for b in range(7)]
@@ -1024,3 +1031,54 @@ def test_single_query_alternating_k_and_freed_blocks(gpu):
         assert np.array_equal(res.hits, exp.hits) and np.array_equal(res.ids, exp.ids)
         del out, res
         gc.collect()
+
+
+@pytest.mark.parametrize("sigma,length", [(4, 32), (65536, 12), (300, 40)])
+def test_direct_host_io_matches_copy_path(gpu, sigma, length):
+    """Small batches in lcp_pinned_alloc blocks are served with direct host
+    I/O (the kernels read rows from / write results into mapped host memory);
+    pageable queries take the copy path.  Both must give the same bytes, with
+    and without work counters, across the kernel routes (k <= 16 rank kernel,
+    17 <= k <= 32 list kernel, W == 1 and W > 1), and an invalid symbol must be
+    reported through the host-written flag and then cleared."""
+    from paper_2602_04936_b200._native import PinnedArray
+
+    ds = lg.generate_dataset(60_000, length, sigma, seed=77)
+    idx = lg.build(ds)
+    for count in (1, 7, 1024, 1025):
+        qs = lg.generate_queries(ds, count, seed=78 + count, prefix_len=length // 2)
+        pin = PinnedArray((count, length), np.uint16)
+        pin.array[:] = qs
+        for k in (1, 5, 10, 17, 32):
+            for mode in ("strict", "complete"):
+                ref = idx.query_batch(qs.copy(), k, mode)  # pageable rows: copies
+                for work in (True, False):
+                    out = idx.native.alloc_batch(count, k, mode, pinned=True, with_work=work)
+                    r = idx.query_batch_async(pin.array, k, mode, out=out).result()
+                    assert np.array_equal(r.hits, ref.hits), (count, k, mode, work)
+                    for q in range(count):
+                        h = int(ref.hits[q])
+                        assert np.array_equal(r.ids[q, :h], ref.ids[q, :h]), (count, k, mode, q)
+                        assert np.array_equal(r.lcps[q, :h], ref.lcps[q, :h]), (count, k, mode, q)
+                    if work:
+                        assert np.array_equal(r.matched_depth, ref.matched_depth)
+                        assert np.array_equal(r.aux, ref.aux)
+                sync = idx.query_batch(pin.array, k, mode,
+                                       out=idx.native.alloc_batch(count, k, mode, pinned=True))
+                assert np.array_equal(sync.hits, ref.hits) and np.array_equal(sync.aux, ref.aux)
+        bad = PinnedArray((count, length), np.uint16)
+        bad.array[:] = qs
+        bad.array[count - 1, 0] = sigma if sigma < 65536 else 0
+        if sigma < 65536:
+            out = idx.native.alloc_batch(count, 10, "complete", pinned=True)
+            with pytest.raises(lg.InvalidInputError):
+                idx.query_batch_async(bad.array, 10, "complete", out=out).result()
+            r = idx.query_batch_async(pin.array, 10, "complete", out=out).result()
+            ref = idx.query_batch(qs.copy(), 10, "complete")
+            assert np.array_equal(r.hits, ref.hits) and np.array_equal(r.aux, ref.aux)
+    # the single-query API (its own pinned stage and block) agrees as well
+    q = lg.generate_queries(ds, 3, seed=5)
+    for i in range(3):
+        a = idx.query(q[i], 10, "complete")
+        b = idx.query_batch(q[i:i + 1].copy(), 10, "complete")
+        assert list(a.indices) == list(b.ids[0, :int(b.hits[0])])
