@@ -131,25 +131,39 @@ def load() -> ctypes.CDLL:
 
 
 _host_submit = False  # not yet looked up
+_host_submit_wait = None
+
+
+def _bind_host_module() -> None:
+    global _host_submit, _host_submit_wait
+    fn = wait = None
+    if not os.environ.get("LCP_NO_HOST_EXT"):  # A/B switch
+        try:
+            from . import _lcp_host
+        except ImportError:
+            _lcp_host = None
+        if _lcp_host is not None:
+            lib = load()
+            _lcp_host.bind(ctypes.cast(lib.lcp_query_host_packed_async, ctypes.c_void_p).value,
+                           ctypes.cast(lib.lcp_workspace_wait, ctypes.c_void_p).value)
+            fn, wait = _lcp_host.submit, _lcp_host.submit_wait
+    _host_submit, _host_submit_wait = fn, wait
 
 
 def host_submit():
     """submit() of the CPython fast path (csrc/host_submit.c) bound to the
     loaded library's lcp_query_host_packed_async, or None when the module is
     not built (the ctypes call is then used; same entry point, same results)."""
-    global _host_submit
     if _host_submit is False:
-        fn = None
-        if not os.environ.get("LCP_NO_HOST_EXT"):  # A/B switch
-            try:
-                from . import _lcp_host
-            except ImportError:
-                _lcp_host = None
-            if _lcp_host is not None:
-                _lcp_host.bind(ctypes.cast(load().lcp_query_host_packed_async, ctypes.c_void_p).value)
-                fn = _lcp_host.submit
-        _host_submit = fn
+        _bind_host_module()
     return _host_submit
+
+
+def host_submit_wait():
+    """submit_wait() of the same module (submission + lcp_workspace_wait), or None."""
+    if _host_submit is False:
+        _bind_host_module()
+    return _host_submit_wait if _host_submit is not None else None
 
 
 def last_error() -> str:

@@ -9,6 +9,7 @@
  * directly: the queries' address comes from the buffer protocol, the function
  * address from the loaded C-ABI library (no link-time dependency on it), and
  * the GIL is released around the call so serving threads overlap.
+ * submit_wait() adds the wait (the single-query API's whole round trip).
  *
  * Built in-tree by _build.py (gcc, Python headers); _native.py uses ctypes
  * when the module is absent, so this is a speed path, never a semantic one.
@@ -21,25 +22,35 @@ typedef int (*submit_fn)(const void* index, void* ws, const uint16_t* queries, i
                          int32_t k, int32_t mode, int32_t out_stride, void* out_block,
                          int32_t flags);
 
-static submit_fn g_submit = NULL;
+typedef int (*wait_fn)(void* ws);
 
-static PyObject* bind(PyObject* self, PyObject* addr) {
+static submit_fn g_submit = NULL;
+static wait_fn g_wait = NULL;
+
+/* bind(address of lcp_query_host_packed_async, address of lcp_workspace_wait) */
+static PyObject* bind(PyObject* self, PyObject* const* args, Py_ssize_t nargs) {
   (void)self;
-  void* p = PyLong_AsVoidPtr(addr);
-  if (!p && PyErr_Occurred()) return NULL;
-  g_submit = (submit_fn)p;
+  if (nargs != 2) {
+    PyErr_SetString(PyExc_TypeError, "bind() takes 2 arguments");
+    return NULL;
+  }
+  void* s = PyLong_AsVoidPtr(args[0]);
+  void* w = PyLong_AsVoidPtr(args[1]);
+  if (PyErr_Occurred()) return NULL;
+  g_submit = (submit_fn)s;
+  g_wait = (wait_fn)w;
   Py_RETURN_NONE;
 }
 
 /* submit(index, ws, queries, length, k, mode, out_stride, out_block, flags) -> rc
- * queries: C-contiguous 2-D buffer of 2-byte items with `length` columns. */
-static PyObject* submit(PyObject* self, PyObject* const* args, Py_ssize_t nargs) {
-  (void)self;
+ * queries: C-contiguous 2-D buffer of 2-byte items with `length` columns.
+ * With `wait`, the workspace's batch is also waited for (one round trip). */
+static PyObject* submit_impl(PyObject* const* args, Py_ssize_t nargs, int wait) {
   if (nargs != 9) {
     PyErr_SetString(PyExc_TypeError, "submit() takes 9 arguments");
     return NULL;
   }
-  if (!g_submit) {
+  if (!g_submit || !g_wait) {
     PyErr_SetString(PyExc_RuntimeError, "submit(): bind() the C-ABI entry point first");
     return NULL;
   }
@@ -64,15 +75,29 @@ static PyObject* submit(PyObject* self, PyObject* const* args, Py_ssize_t nargs)
   Py_BEGIN_ALLOW_THREADS
   rc = g_submit(ix, ws, (const uint16_t*)v.buf, count, (int32_t)k, (int32_t)mode, (int32_t)stride, out,
                 (int32_t)flags);
+  if (rc == 0 && wait) rc = g_wait(ws);
   Py_END_ALLOW_THREADS
   PyBuffer_Release(&v);
   return PyLong_FromLong(rc);
 }
 
+static PyObject* submit(PyObject* self, PyObject* const* args, Py_ssize_t nargs) {
+  (void)self;
+  return submit_impl(args, nargs, 0);
+}
+
+static PyObject* submit_wait(PyObject* self, PyObject* const* args, Py_ssize_t nargs) {
+  (void)self;
+  return submit_impl(args, nargs, 1);
+}
+
 static PyMethodDef methods[] = {
-    {"bind", (PyCFunction)bind, METH_O, "bind(address of lcp_query_host_packed_async)"},
+    {"bind", (PyCFunction)(void (*)(void))bind, METH_FASTCALL,
+     "bind(address of lcp_query_host_packed_async, address of lcp_workspace_wait)"},
     {"submit", (PyCFunction)(void (*)(void))submit, METH_FASTCALL,
      "submit(index, ws, queries, length, k, mode, out_stride, out_block, flags) -> rc"},
+    {"submit_wait", (PyCFunction)(void (*)(void))submit_wait, METH_FASTCALL,
+     "submit_wait(...): submit, then lcp_workspace_wait(ws) -> rc"},
     {NULL, NULL, 0, NULL},
 };
 

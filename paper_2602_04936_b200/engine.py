@@ -214,7 +214,9 @@ class NativeIndex:
         and submitted through the async packed entry point on the thread's
         workspace, whose graph cache turns H2D + kernel + D2H into a single
         graph launch from the second call on (stable staging / output
-        pointers); then waits.  Returns the thread's reused one-row block."""
+        pointers), and — stage and block being lcp_pinned_alloc memory — the
+        kernel reads the row and writes the result over PCIe directly (no
+        copies); then waits.  Returns the thread's reused one-row block."""
         if mode not in MODES:
             raise InvalidInputError(f"unknown mode {mode!r}")
         if k < 1:
@@ -228,6 +230,11 @@ class NativeIndex:
         out.mode = mode
         ws = workspace()
         packed = out._packed
+        fast = _native.host_submit_wait()
+        if fast is not None:  # csrc/host_submit.c: submission + wait in one call
+            check(fast(self.handle.value, ws.address, stage, self.length, self.stride_for(k), MODES[mode],
+                       packed[2], packed[0], 0))
+            return out
         check(load().lcp_query_host_packed_async(self._h, ws.handle, ptr(stage), 1, self.stride_for(k),
                                                  MODES[mode], packed[2], packed[0], 0))
         check(load().lcp_workspace_wait(ws.handle))

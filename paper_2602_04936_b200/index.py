@@ -201,7 +201,11 @@ class TrieIndex:
             raise InvalidInputError(f"mode must be 'strict' or 'complete', got {mode!r}")
         if k < 1:
             raise InvalidInputError(f"k must be >= 1, got {k}")
-        query = self._validate_query(q)
+        if (type(q) is np.ndarray and q.dtype is _U16 and q.ndim == 1 and q.shape[0] == self.length
+                and self.n > 0):
+            query = q  # the kernel checks the symbols and raises the same error
+        else:
+            query = self._validate_query(q)
         out = self._native.query_single(query, k, mode)
         if work is not None:
             self._account(out, mode, work)

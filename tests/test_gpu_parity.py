@@ -125,6 +125,14 @@ def test_errors_are_reference_exceptions(gpu):
         idx.query([0], 2)
     with pytest.raises(lg.InvalidInputError):
         idx.query([0, 99], 2)
+    # a uint16 row goes straight to the kernel, which raises the same error
+    # (and the flag is cleared for the next query)
+    with pytest.raises(lg.InvalidInputError, match="out of range for alphabet of size 4"):
+        idx.query(np.array([0, 4], dtype=np.uint16), 2)
+    assert idx.query(np.array([0, 1], dtype=np.uint16), 2, "complete").pairs() == [(0, 2)]
+    empty = lg.build(lg.Dataset.from_rows(np.zeros((0, 2), dtype=np.uint16), 4))
+    with pytest.raises(lg.InvalidInputError):  # no kernel runs on an empty index: checked on the host
+        empty.query(np.array([0, 4], dtype=np.uint16), 2)
     # device-side symbol validation in the batched path
     with pytest.raises(lg.InvalidInputError):
         idx.query_batch(np.array([[0, 1], [0, 3], [0, 9]], dtype=np.uint16), 2)
