@@ -597,14 +597,19 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, MODE == 2 ? 1 : 2)
     int dmax = -1;
     // unconditional loads at a clamped index (n >= 1), masked afterwards;
     // lcp = min(clz64(key ^ q) >> lb, L) is exact for W == 1 (clz64(0) = 64)
+    u64 key[T];
 #pragma unroll
     for (int t = 0; t < T; ++t) {
-      const int i = s + t * 32 + lane;
-      const bool ok = (unsigned)i < (unsigned)n;
-      const int ic = min(max(i, 0), n - 1);
-      const u64 key = __ldg(keys + ic);
+      const int ic = min(max(s + t * 32 + lane, 0), n - 1);
+      key[t] = __ldg(keys + ic);
       id[t] = __ldg(order + ic);
-      l[t] = ok ? min(__clzll((long long)(key ^ q)) >> lb, L) : -1;
+    }
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      // branch-free (-1 outside [0, n)): a branch here let the compiler sink
+      // the key load behind it
+      const int ok_mask = (unsigned)(s + t * 32 + lane) < (unsigned)n ? 0 : -1;
+      l[t] = min(__clzll((long long)(key[t] ^ q)) >> lb, L) | ok_mask;
       dmax = max(dmax, l[t]);
     }
     dmax = (int)__reduce_max_sync(LCP_FULL_MASK, (unsigned)(dmax + 1)) - 1;
@@ -950,14 +955,19 @@ __global__ void __launch_bounds__(NS > 2 ? QW_MAX_THREADS / 2 : QW_MAX_THREADS, 
     int l[T];
     u32 id[T];
     int dmax = -1;
+    u64 key[T];
 #pragma unroll
     for (int t = 0; t < T; ++t) {
-      const int i = s + t * 32 + lane;
-      const bool ok = (unsigned)i < (unsigned)n;
-      const int ic = min(max(i, 0), n - 1);
-      const u64 key = __ldg(keys + ic);
+      const int ic = min(max(s + t * 32 + lane, 0), n - 1);
+      key[t] = __ldg(keys + ic);
       id[t] = __ldg(order + ic);
-      l[t] = ok ? min(__clzll((long long)(key ^ q)) >> lb, L) : -1;
+    }
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      // branch-free (-1 outside [0, n)): a branch here let the compiler sink
+      // the key load behind it
+      const int ok_mask = (unsigned)(s + t * 32 + lane) < (unsigned)n ? 0 : -1;
+      l[t] = min(__clzll((long long)(key[t] ^ q)) >> lb, L) | ok_mask;
       dmax = max(dmax, l[t]);
     }
     dmax = (int)__reduce_max_sync(LCP_FULL_MASK, (unsigned)(dmax + 1)) - 1;

@@ -332,6 +332,21 @@ def memoized_query(index: TrieIndex, q, k: int, mode: str = "strict",
     """TrieIndex.query served from ``cache`` on repeats (trie.py:464-488)."""
     if cache is None:
         raise InvalidInputError("memoized_query requires a cache")
+    if (type(q) is np.ndarray and q.dtype is _U16 and q.ndim == 1 and q.shape[0] == index.length
+            and q.flags.c_contiguous):
+        # a row already in the wire format is its own key: only validated
+        # queries are ever inserted, so a hit needs no validation, and a miss
+        # is validated below before it is counted (as the reference orders it)
+        key = (q.tobytes(), int(k), mode)
+        with cache._lock:
+            hit = cache._store.get(key)
+            if hit is not None:
+                cache.hits += 1
+        if hit is not None:
+            if work is not None:
+                work.cache_hits += 1
+                work.queries += 1
+            return hit
     query = index._validate_query(q)
     key = (query.tobytes(), int(k), mode)
     hit = cache.lookup(key)

@@ -1090,3 +1090,29 @@ def test_direct_host_io_matches_copy_path(gpu, sigma, length):
         a = idx.query(q[i], 10, "complete")
         b = idx.query_batch(q[i:i + 1].copy(), 10, "complete")
         assert list(a.indices) == list(b.ids[0, :int(b.hits[0])])
+
+
+def test_memoized_query_hits_and_counters(gpu):
+    """memoized_query (trie.py:464-488): uint16 rows hit without re-validation,
+    other inputs are validated first; counters and errors as the reference's."""
+    ds = lg.generate_dataset(20_000, 16, 4, seed=90)
+    idx = lg.build(ds)
+    qs = lg.generate_queries(ds, 8, seed=91, prefix_len=8)
+    cache = lg.QueryCache()
+    w = idx.new_work_report()
+    cold = [lg.memoized_query(idx, q, 10, "complete", cache, work=w) for q in qs]
+    assert cache.misses == 8 and cache.hits == 0 and w.cache_hits == 0
+    for q in qs:  # uint16 rows, lists and int64 rows all hit the same entries
+        for form in (q, q.tolist(), q.astype(np.int64)):
+            r = lg.memoized_query(idx, form, 10, "complete", cache, work=w)
+            assert r is cold[list(map(bytes, qs)).index(bytes(q))]
+    assert cache.hits == 24 and cache.misses == 8 and w.cache_hits == 24
+    bad = qs[0].copy()
+    bad[3] = 4
+    with pytest.raises(lg.InvalidInputError):
+        lg.memoized_query(idx, bad, 10, "complete", cache)
+    with pytest.raises(lg.InvalidInputError):  # 2-D, even though its bytes are cached
+        lg.memoized_query(idx, qs[:1], 10, "complete", cache)
+    assert cache.misses == 8 and cache.hits == 24
+    assert lg.memoized_query(idx, qs[0], 10, "strict", cache) is not cold[0]  # mode is in the key
+    assert cache.misses == 9
