@@ -537,6 +537,7 @@ C5_ITEMS = int(os.environ.get("LCP_BENCH_C5_ITEMS", 200_000_000))  # BASELINE co
 # NVLink).  p2p is tested at one rank; no multi-GPU box was available to
 # validate it, so NCCL stays the default (LCP_BENCH_EXCHANGE=p2p to select it)
 EXCHANGE = os.environ.get("LCP_BENCH_EXCHANGE", "all_to_all")
+C5_INFLIGHT = int(os.environ.get("LCP_BENCH_C5_INFLIGHT", "4"))  # sharded steps in flight per rank
 # our kernels per range-sharded step: pack + route (own), counted query,
 # thresholds, encode, pack + route (consult), counted query, encode, merge
 SHARD_LAUNCHES_PER_STEP = 10
@@ -598,46 +599,69 @@ def config5_leg(args, world, rank, dev, barrier, max_over_ranks, scheme: str = "
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0
     stream = torch.cuda.Stream(device=dev)
+    nccl = world > 1 and dist.get_backend() == "nccl"
+    # C5_INFLIGHT steps in flight, each on its own stream with its own step
+    # buffers (slot) and, under NCCL, its own communicator (process group):
+    # one step is a chain of small dependent launches and exchanges, so its
+    # latency, not any one kernel, bounds a single stream
+    n_slots = C5_INFLIGHT if world == 1 or nccl else 1
+    groups = [dist.new_group(list(range(world))) if nccl else None for _ in range(n_slots)]
+    slot_streams = [torch.cuda.Stream(device=dev) for _ in range(n_slots)]
     with torch.cuda.stream(stream):
         pool = torch.from_numpy(qs).to(dev).view(n_pool, BATCH, SEQ_LEN)
-        gq = torch.empty((world * BATCH, SEQ_LEN), dtype=torch.uint16, device=dev)
-        out = (torch.empty((BATCH, K), dtype=torch.int32, device=dev),
-               torch.empty((BATCH, K), dtype=torch.int16, device=dev),
-               torch.empty(BATCH, dtype=torch.int32, device=dev))
-
-        nccl = world > 1 and dist.get_backend() == "nccl"
+        gqs = [torch.empty((world * BATCH, SEQ_LEN), dtype=torch.uint16, device=dev) for _ in range(n_slots)]
+        outs = [(torch.empty((BATCH, K), dtype=torch.int32, device=dev),
+                 torch.empty((BATCH, K), dtype=torch.int16, device=dev),
+                 torch.empty(BATCH, dtype=torch.int32, device=dev)) for _ in range(n_slots)]
+        out = outs[0]
 
         # the uint16 rows travel as int32 pairs (NCCL and gloo have no 16-bit integer type)
-        def step(i, exchange=EXCHANGE if scheme == "range" else "all_to_all"):
-            src = pool[i % n_pool].view(torch.int32)
+        def step(i, exchange=EXCHANGE if scheme == "range" else "all_to_all", slot=0, rows=None):
+            rows = pool[i % n_pool] if rows is None else rows
+            src = rows.view(torch.int32)
+            gq = gqs[slot]
             if nccl:
-                dist.all_gather_into_tensor(gq.view(torch.int32), src)
+                dist.all_gather_into_tensor(gq.view(torch.int32), src, group=groups[slot])
             elif world > 1:  # gloo (LCP_BENCH_SHARE_GPU functional check): host staging
                 h = torch.empty((world, BATCH, SEQ_LEN // 2), dtype=torch.int32)
                 dist.all_gather(list(h.unbind(0)), src.cpu())
                 gq.view(torch.int32).copy_(h.view(-1, SEQ_LEN // 2))
             else:
-                gq.copy_(pool[i % n_pool])
-            sh.query_device(gq, K, "complete", out=out, exchange=exchange)
+                gq.copy_(rows)
+            sh.query_device(gq, K, "complete", out=outs[slot], exchange=exchange, group=groups[slot],
+                            slot=slot)
 
-        def timed(exchange):
-            """Graph-capture G steps (eager if capture fails), warm, time
-            ceil(steps / G) replays; returns (ms over ranks, steps, launch)."""
-            for i in range(3):  # eager warm-up (allocates the step buffers)
-                step(i, exchange)
+        def timed(exchange, inflight=1):
+            """Graph-capture G steps spread round-robin over `inflight` slot
+            streams (eager if capture fails), warm, time ceil(steps / G)
+            replays; returns (ms over ranks, steps, launch)."""
+            S = max(1, min(inflight, n_slots))
+
+            def run_steps(count):
+                for x in slot_streams[:S]:
+                    x.wait_stream(stream)
+                for i in range(count):
+                    with torch.cuda.stream(slot_streams[i % S]):
+                        step(i, exchange, i % S)
+                for x in slot_streams[:S]:
+                    stream.wait_stream(x)
+
+            for _ in range(3):  # eager warm-up (allocates every slot's step buffers)
+                run_steps(S)
             torch.cuda.synchronize()
             G = min(64, max(8, args.steps))
-            launch = "CUDA graph replay (NCCL collectives captured)"
+            G = (G + S - 1) // S * S
+            launch = (f"CUDA graph replay (NCCL collectives captured), {S} step(s) in flight"
+                      + (", one communicator per stream" if nccl and S > 1 else ""))
             try:
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=stream):
-                    for i in range(G):
-                        step(i, exchange)
+                    run_steps(G)
                 run = lambda: g.replay()
             except Exception as e:  # capture unsupported here: eager, still no host sync
                 torch.cuda.synchronize()
                 launch = f"eager stream-ordered launches (graph capture failed: {type(e).__name__})"
-                run = lambda: [step(i, exchange) for i in range(G)]
+                run = lambda: run_steps(G)
             reps = max(1, (args.steps + G - 1) // G)
             for _ in range(max(1, args.warmup // G + 1)):
                 run()
@@ -652,7 +676,8 @@ def config5_leg(args, world, rank, dev, barrier, max_over_ranks, scheme: str = "
             barrier()
             return ms, reps * G, launch
 
-        ms, steps, launch = timed(EXCHANGE if scheme == "range" else "all_to_all")
+        ms, steps, launch = timed(EXCHANGE if scheme == "range" else "all_to_all", n_slots)
+        ms1, steps1, _ = timed(EXCHANGE if scheme == "range" else "all_to_all", 1)
         p2p = None
         if scheme == "range" and nccl and EXCHANGE != "p2p":
             # the peer-memory exchange beside it, when every rank can map its
@@ -686,29 +711,69 @@ def config5_leg(args, world, rank, dev, barrier, max_over_ranks, scheme: str = "
         pin_q = PinnedArray((n_pool, BATCH, SEQ_LEN), np.uint16)
         pin_q.array[:] = qs.reshape(n_pool, BATCH, SEQ_LEN)
         host_q = torch.from_numpy(pin_q.array)
-        host_out = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in out]
+        # one graph per (slot, client batch): H2D of the pinned batch, the
+        # step, D2H of the answers into the slot's pinned block; n_slots
+        # steps in flight, a slot is reused once its previous step's answers
+        # have landed (event wait)
+        e_in = [torch.empty((BATCH, SEQ_LEN), dtype=torch.uint16, device=dev) for _ in range(n_slots)]
+        host_outs = [[torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in outs[s_]]
+                     for s_ in range(n_slots)]
+        exch = EXCHANGE if scheme == "range" else "all_to_all"
+
+        def e2e_step(i, s_):
+            e_in[s_].copy_(host_q[i % n_pool], non_blocking=True)
+            step(i, exch, s_, rows=e_in[s_])
+            for h, d in zip(host_outs[s_], outs[s_]):
+                h.copy_(d, non_blocking=True)
+
+        e_graphs = {}
+        e_launch = "one CUDA graph per (slot, client batch)"
+        try:
+            for s_ in range(n_slots):
+                for j in range(n_pool):
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, stream=slot_streams[s_]):
+                        e2e_step(j, s_)
+                    e_graphs[(s_, j)] = g
+        except Exception as e:
+            torch.cuda.synchronize()
+            e_graphs = {}
+            e_launch = f"eager launches (graph capture failed: {type(e).__name__})"
+
+        def e2e_submit(i, s_):
+            with torch.cuda.stream(slot_streams[s_]):
+                if e_graphs:
+                    e_graphs[(s_, i % n_pool)].replay()
+                else:
+                    e2e_step(i, s_)
+
         e_steps = min(max(args.steps, 100), 400)
-        for i in range(3):
-            pool[i % n_pool].copy_(host_q[i % n_pool], non_blocking=True)
-            step(i)
+        e_steps = (e_steps + n_slots * n_pool - 1) // (n_slots * n_pool) * (n_slots * n_pool)
+        events = [torch.cuda.Event() for _ in range(n_slots)]
+        for i in range(n_slots * n_pool):
+            e2e_submit(i, i % n_slots)
         torch.cuda.synchronize()
         barrier()
         t_e = time.perf_counter()
         for i in range(e_steps):
-            pool[i % n_pool].copy_(host_q[i % n_pool], non_blocking=True)
-            step(i)
-            for h, d in zip(host_out, out):
-                h.copy_(d, non_blocking=True)
-            stream.synchronize()
+            s_ = i % n_slots
+            if i >= n_slots:
+                events[s_].synchronize()
+            e2e_submit(i, s_)
+            events[s_].record(slot_streams[s_])
+        torch.cuda.synchronize()
         e_el = max_over_ranks(time.perf_counter() - t_e)
         barrier()
     e2e = {"value": world * BATCH * e_steps / e_el, "unit": "queries/s", "steps": e_steps,
            "ms_per_step": 1e3 * e_el / e_steps, "h2d_bytes_per_step": BATCH * SEQ_LEN * 2,
            "d2h_bytes_per_step": int(sum(t.numel() * t.element_size() for t in out)),
            "api": f"{type(sh).__name__}.query_device per step, pinned client batch in / answers out, "
-                  "one step in flight, wall clock"}
+                  f"{n_slots} step(s) in flight ({e_launch}), wall clock"}
     return {"value": world * BATCH * steps / (ms / 1e3), "unit": "queries/s", "steps": steps, "e2e": e2e,
-            "ms_per_step": ms / steps, "n_items_total": n_total, "n_items_local": int(n_local),
+            "ms_per_step": ms / steps, "steps_in_flight": n_slots,
+            "one_step_in_flight": {"value": world * BATCH * steps1 / (ms1 / 1e3), "unit": "queries/s",
+                                   "ms_per_step": ms1 / steps1},
+            "n_items_total": n_total, "n_items_local": int(n_local),
             "scheme": scheme, "batch_per_rank": BATCH, "launch": launch,
             "exchange": EXCHANGE if scheme == "range" else "all_to_all",
             "gen_s": round(gen_s, 2), "build_s": round(build_s, 2), "p2p": p2p, "query_kernel": kernel,

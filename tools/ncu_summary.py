@@ -3,7 +3,8 @@
     python tools/ncu_summary.py gpurun_out/prof_query_r01.ncu-rep:k_query_w1 \
         gpurun_out/ncu_raw_fullscan_r01.csv:k_fullscan_w1 ... --launches gpurun_out/launches.csv
 
-(each spec is an .ncu-rep or its exported `--page raw --csv` page)
+(each spec is an .ncu-rep or its exported `--page raw --csv` page; --update
+replaces only the named kernels' entries of the existing summary)
 
 Writes profiles/ncu_summary.json (per-kernel duration, DRAM bytes, issue and
 occupancy figures; bench.py reads dram_bytes_per_launch as roofline.traffic)
@@ -48,11 +49,14 @@ def raw(rep: str) -> dict:
 def main() -> None:
     args = sys.argv[1:]
     launches = None
+    update = "--update" in args  # keep the other kernels' entries of the existing summary
+    args = [a for a in args if a != "--update"]
     if "--launches" in args:
         i = args.index("--launches")
         launches = args[i + 1]
         args = args[:i] + args[i + 2:]
-    summary = {}
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    summary = json.load(open(path)) if update and os.path.exists(path) else {}
     for spec in args:
         rep, name = spec.split(":")
         d = raw(rep)
@@ -74,7 +78,7 @@ def main() -> None:
         e["dram_bytes_per_launch"] = e.get("dram_read_bytes", 0) + e.get("dram_write_bytes", 0)
         summary[name] = e
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-    with open(os.path.join(ROOT, "profiles", "ncu_summary.json"), "w") as f:
+    with open(path, "w") as f:
         json.dump(summary, f, indent=1)
     if launches:
         rows = list(csv.reader(open(launches)))
