@@ -169,6 +169,49 @@ __device__ __forceinline__ int lcp_at(const DevIndex& ix, long long i, const u64
 
 
 
+// Leaf-region loads for the W > 1 kernels: every lane issues its T first-word
+// and T id loads (clamped index) before using any of them, so the region is
+// one round trip; a conditional load (`ok ? lcp_at(...) : -1`) was compiled
+// into one branch per row, serialising T round trips.  The remaining words
+// are read only for rows equal to q in the first word.  lcp -1 outside [0, n).
+template <int WMAX>
+__device__ __forceinline__ int lcp_rest(const DevIndex& ix, long long i, const u64 (&qk)[WMAX]) {
+  const u64* key = ix.keys + i * ix.W;
+#pragma unroll
+  for (int w = 1; w < WMAX; ++w) {
+    if (w < ix.W) {
+      const u64 y = key[w] ^ qk[w];
+      if (y) return w * ix.spw + (__clzll((long long)y) >> ix.lb);
+    }
+  }
+  return ix.L;
+}
+
+template <int WMAX, int T>
+__device__ __forceinline__ int region_lcps(const DevIndex& ix, long long s, const u64 (&qk)[WMAX],
+                                           int (&l)[T], u32 (&id)[T]) {
+  const long long n = ix.n;
+  const u64* w0 = WMAX == 1 ? ix.keys : ix.keys_w0;
+  u64 x0[T];
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    const long long ic = min(max(s + t * 32 + lane_id(), 0ll), n - 1);
+    x0[t] = __ldg(w0 + ic) ^ qk[0];
+    id[t] = __ldg(ix.order + ic);
+  }
+  int dmax = -1;
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    const long long i = s + t * 32 + lane_id();
+    int lv;
+    if (x0[t]) lv = __clzll((long long)x0[t]) >> ix.lb;
+    else lv = WMAX == 1 ? ix.L : lcp_rest<WMAX>(ix, min(max(i, 0ll), n - 1), qk);
+    l[t] = lv | ((i >= 0 && i < n) ? 0 : -1);
+    dmax = max(dmax, l[t]);
+  }
+  return dmax;
+}
+
 // Stage the top search levels into shared memory with one TMA bulk copy.
 // stage_issue starts the copy; stage_wait blocks on its mbarrier (phase 0),
 // so warps can load and pack their first query while the copy is in flight.
@@ -1146,15 +1189,7 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, 1)
     const long long s = pos - 32;  // window [s, s+64), warp-strided
     int l[2];
     u32 id[2];
-    int dmax = -1;
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      const long long i = s + t * 32 + lane;
-      const bool ok = i >= 0 && i < n;
-      l[t] = ok ? lcp_at<WMAX>(ix, i, qk) : -1;
-      id[t] = ok ? ix.order[i] : 0u;
-      dmax = max(dmax, l[t]);
-    }
+    int dmax = region_lcps<WMAX, 2>(ix, s, qk, l, id);
 #pragma unroll
     for (int o = 16; o; o >>= 1) dmax = max(dmax, __shfl_xor_sync(LCP_FULL_MASK, dmax, o));
     const int need = complete ? (int)min((long long)k, n) : k;
@@ -1312,15 +1347,7 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, 1)
     const long long s = pos - 32;
     int l[2];
     u32 id[2];
-    int dmax = -1;
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      const long long i = s + t * 32 + lane;
-      const bool ok = i >= 0 && i < n;
-      l[t] = ok ? lcp_at<WMAX>(ix, i, qk) : -1;
-      id[t] = ok ? ix.order[i] : 0u;
-      dmax = max(dmax, l[t]);
-    }
+    int dmax = region_lcps<WMAX, 2>(ix, s, qk, l, id);
 #pragma unroll
     for (int o = 16; o; o >>= 1) dmax = max(dmax, __shfl_xor_sync(LCP_FULL_MASK, dmax, o));
     const int dstar = window_dstar<2>(l, dmax, k);
@@ -1432,15 +1459,7 @@ __global__ void __launch_bounds__(NS > 2 ? QW_MAX_THREADS / 2 : QW_MAX_THREADS, 
     const long long s = pos - 32 * NS;  // window [s, s + 32 T), warp-strided
     int l[T];
     u32 id[T];
-    int dmax = -1;
-#pragma unroll
-    for (int t = 0; t < T; ++t) {
-      const long long i = s + t * 32 + lane;
-      const bool ok = i >= 0 && i < n;
-      l[t] = ok ? lcp_at<WMAX>(ix, i, qk) : -1;
-      id[t] = ok ? __ldg(ix.order + i) : 0u;
-      dmax = max(dmax, l[t]);
-    }
+    int dmax = region_lcps<WMAX, T>(ix, s, qk, l, id);
     dmax = (int)__reduce_max_sync(LCP_FULL_MASK, (unsigned)(dmax + 1)) - 1;
     const int need = complete ? (int)min((long long)k, n) : k;
     const int dstar = complete ? window_dstar<T>(l, dmax, need) : dmax;
@@ -1741,12 +1760,18 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, 1)
     int l[2];
     u32 id[2];
     int dmax = -1;
+    u64 x0[2];  // both rows' first words and ids in flight together (see region_lcps)
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const long long ic = min(max(s + t * 32 + lane, 0ll), n - 1);
+      x0[t] = __ldg(ix.keys_w0 + ic) ^ q[0];
+      id[t] = __ldg(ix.order + ic);
+    }
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
       const long long i = s + t * 32 + lane;
-      const bool ok = i >= 0 && i < n;
-      l[t] = ok ? lcp_any(ix, i, q) : -1;
-      id[t] = ok ? __ldg(ix.order + i) : 0u;
+      const int lv = x0[t] ? (__clzll((long long)x0[t]) >> ix.lb) : lcp_any(ix, min(max(i, 0ll), n - 1), q);
+      l[t] = lv | ((i >= 0 && i < n) ? 0 : -1);
       dmax = max(dmax, l[t]);
     }
     dmax = (int)__reduce_max_sync(LCP_FULL_MASK, (unsigned)(dmax + 1)) - 1;

@@ -158,13 +158,11 @@ __global__ void __launch_bounds__(256)
                   int L, int strict, const unsigned* __restrict__ my_signals,
                   const unsigned* __restrict__ epoch, u32* __restrict__ out_ids,
                   uint16_t* __restrict__ out_lcps, int* __restrict__ out_hits, int out_stride) {
-  __shared__ int s_ready;
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0) {  // one thread waits; the barrier releases the CTA
     const unsigned e = *epoch;
     for (int s = 0; s < world; ++s)
       while (ld_acquire_sys_u32(my_signals + s) < e) {
       }
-    s_ready = 1;
   }
   __syncthreads();
   const int lane = lane_id();
@@ -202,5 +200,4 @@ __global__ void __launch_bounds__(256)
     out_lcps[qi * out_stride + lane] = (uint16_t)(L - (int)(slot >> 32));
   }
   if (lane == 0) out_hits[qi] = hits;
-  (void)s_ready;
 }
