@@ -168,12 +168,18 @@ class GpuEngine:
     range still gets an n = 0 index, which the device routing needs for the
     key encoding)."""
 
-    def __init__(self, rows: np.ndarray, length: int, sigma: int):
+    def __init__(self, rows, length: int, sigma: int):
+        """rows: (n, L) uint16 numpy array, or a contiguous CUDA tensor of
+        2-byte symbols (int16/uint16 bit patterns), built in place on the GPU."""
         from .engine import NativeIndex
 
         self.length, self.n = int(length), int(rows.shape[0])
         self.sigma = int(sigma)
-        self.native = NativeIndex(rows, length, sigma)
+        if hasattr(rows, "data_ptr"):
+            assert rows.is_cuda and rows.element_size() == 2 and rows.is_contiguous()
+            self.native = NativeIndex.from_device(rows.data_ptr() if self.n else 0, self.n, length, sigma)
+        else:
+            self.native = NativeIndex(rows, length, sigma)
         self.device = "cuda"
 
     def first_last_rows(self) -> np.ndarray:
@@ -261,7 +267,8 @@ class RangeShardedIndex:
             self.n_local = n_local
             self._finish_build()
             return
-        rows_t = torch.from_numpy(items.astype(np.int32)).to(self.device)
+        # the rows cross PCIe once, as 2-byte symbols, and widen on the device
+        rows_t = torch.from_numpy(items.view(np.int16)).to(self.device).to(torch.int32) & 0xFFFF
         dest = route(rows_t, self.splitters, L) if n_local else torch.zeros(0, dtype=torch.int64,
                                                                             device=self.device)
         perm = torch.sort(dest, stable=True).indices
@@ -271,7 +278,12 @@ class RangeShardedIndex:
         gids = torch.arange(id_offset, id_offset + n_local, dtype=torch.int64, device=self.device)
         my_rows = self.coll.all_to_all(rows_t[perm], sc, rc, L).reshape(-1, L)
         self.gids = self.coll.all_to_all(gids[perm], sc, rc, 1)
-        local = my_rows.cpu().numpy().astype(np.uint16)
+        if engine_factory is GpuEngine and my_rows.is_cuda:
+            # the received rows stay on the device: the index is built from them
+            # in place (uint16 bit patterns in an int16 tensor)
+            local = my_rows.to(torch.int16).contiguous()
+        else:
+            local = my_rows.cpu().numpy().astype(np.uint16)
         self.engine = engine_factory(local, L, sigma)
         self.n_local = int(local.shape[0])
         self._finish_build()
