@@ -491,22 +491,26 @@ __device__ __forceinline__ void tal_bucket_w1(const DevIndex& ix, u64 q, int& bl
 // because B = R(dB) (every bucket item matches q's first dB symbols) and, for
 // d > dB, {i in B : lcp_i >= d} = R(d), the run of sorted rows sharing q's
 // d-prefix.  R(d) within the leaf region is read off the region's lcps (one
-// ballot per depth, depths dB+1..dmax, R(d) empty beyond dmax); a run reaching
-// a region edge continues to its true edge, found by a binary search over the
-// bucket, one lane per (depth, side).  So the count costs a handful of
-// dependent L2 probes instead of a sweep over the whole bucket (the former
-// tal_sym_w1 read every bucket item: 128 MB of L2 traffic per 4096-query
-// batch at config 3, B = 256).  W == 1 keys.
+// ballot per depth, depths dB+1..dmax, R(d) empty beyond dmax).  A run that
+// reaches a region edge continues to its true edge: left of the region the
+// lcps are non-decreasing towards q's position, right of it non-increasing,
+// so each edge is the boundary of a monotone predicate.  All those searches
+// (one per (depth, side), at most 32) run together: the warp splits into
+// groups of G = 32 / #searches lanes, each group probes G points of its
+// interval per round, so an interval shrinks (G+1)-fold per dependent L2 round
+// trip (the former lane-per-search binary search took log2|B| round trips).
+// So the count costs a few dependent probes instead of a sweep over the whole
+// bucket (the former tal_sym_w1 read every bucket item: 128 MB of L2 traffic
+// per 4096-query batch at config 3, B = 256).  W == 1 keys.
 template <int T>
 __device__ __forceinline__ unsigned long long tal_sym_region(const DevIndex& ix, u64 q, int blo, int bhi,
                                                              const int (&l)[T], int s, int dmax) {
   const int lane = lane_id();
-  const int L = ix.L, dB = ix.tal_depth, b = ix.b;
+  const int L = ix.L, dB = ix.tal_depth, lb = ix.lb;
   unsigned long long sym = (unsigned long long)(bhi - blo) * (unsigned long long)(1 + min(dB, L - 1));
   const int l0 = __shfl_sync(LCP_FULL_MASK, l[0], 0);        // position s
   const int lz = __shfl_sync(LCP_FULL_MASK, l[T - 1], 31);   // position s + 32T - 1
   const int e = s + 32 * T;                                  // first position after the region
-  u64 lmask = 0, rmask = 0;  // bit (d - dB - 1): the run of depth d leaves the region left / right
   const int dtop = min(dmax, L - 1);
   for (int d = dB + 1; d <= dtop; ++d) {
     int c = 0;
@@ -514,39 +518,50 @@ __device__ __forceinline__ unsigned long long tal_sym_region(const DevIndex& ix,
     for (int t = 0; t < T; ++t) c += __popc(__ballot_sync(LCP_FULL_MASK, l[t] >= d));
     if (c == 0) break;  // R(d) is nested: nothing deeper either
     sym += (unsigned long long)c;
-    if (l0 >= d && s > blo) lmask |= 1ull << (d - dB - 1);
-    if (lz >= d && e < bhi) rmask |= 1ull << (d - dB - 1);
   }
-  // the runs' parts outside the region: binary searches over the bucket
-  const int nl = __popcll(lmask), nr = __popcll(rmask);
+  // runs leaving the region: depths dB+1..Dl on the left (R(d) contains
+  // position s iff l0 >= d), dB+1..Dr on the right
+  const int nl = s > blo ? max(0, min(l0, dtop) - dB) : 0;
+  const int nr = e < bhi ? max(0, min(lz, dtop) - dB) : 0;
+  const int K = nl + nr;
+  if (K == 0) return sym;
   unsigned long long extra = 0;
-  for (int t0 = 0; t0 < nl + nr; t0 += 32) {
-    const int t = t0 + lane;
-    if (t < nl + nr) {
-      const bool left = t < nl;
-      u64 m = left ? lmask : rmask;
-      for (int j = left ? t : t - nl; j > 0; --j) m &= m - 1;  // the j-th set bit
-      const int d = dB + 1 + __ffsll((long long)m) - 1;
-      const int sh = 64 - d * b;  // d < L <= 64 / b, so 0 < sh < 64
-      const u64 qp = q >> sh;
-      if (left) {  // first i in [blo, s) with prefix_d(key_i) >= prefix_d(q)
-        int lo = blo, hi = s;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if ((__ldg(ix.keys + mid) >> sh) < qp) lo = mid + 1;
-          else hi = mid;
+  for (int k0 = 0; k0 < K; k0 += 32) {  // K <= L - 1 < 64: at most two passes
+    const int kn = min(32, K - k0);
+    // lanes per search G = 2^j - 1 <= 32 / kn: the G probes split an interval
+    // into 2^j parts with shifts (no division)
+    const int j = 31 - __clz(32 / kn + 1);
+    const int G = (1 << j) - 1;
+    const int g = lane / G, r = lane - g * G;
+    const int k = k0 + g;                  // this lane's search (valid iff g < kn)
+    const bool live = g < kn;
+    const bool left = k < nl;
+    const int d = dB + 1 + (left ? k : k - nl);
+    // left: first i in [blo, s) with lcp_i >= d; right: first i in [e, bhi)
+    // with lcp_i < d.  The answer lies in [lo, hi].
+    int lo = left ? blo : e, hi = left ? s : bhi;
+    const unsigned gmask = live ? (G == 32 ? LCP_FULL_MASK : (((1u << G) - 1u) << (g * G))) : 0u;
+    while (__any_sync(LCP_FULL_MASK, live && lo < hi)) {
+      const int span = hi - lo;  // lo < hi: probe G interior points of [lo, hi)
+      const int p = lo + (int)(((long long)(r + 1) * span) >> j);
+      bool pred = false;
+      if (live && lo < hi) {
+        const u64 x = __ldg(ix.keys + p) ^ q;
+        const int lp = x ? min(__clzll((long long)x) >> lb, L) : L;
+        pred = left ? lp >= d : lp < d;
+      }
+      const unsigned m = __ballot_sync(LCP_FULL_MASK, pred) & gmask;
+      if (live && lo < hi) {
+        if (m) {  // first true probe r*: answer in (p_{r*-1}, p_{r*}]
+          const int rs = __ffs(m) - 1 - g * G;
+          hi = lo + (int)(((long long)(rs + 1) * span) >> j);
+          if (rs > 0) lo = lo + (int)(((long long)rs * span) >> j) + 1;
+        } else {  // every probe false: answer in (p_{G-1}, hi]
+          lo = lo + (int)(((long long)G * span) >> j) + 1;
         }
-        extra += (unsigned long long)(s - lo);
-      } else {  // first i in [e, bhi) with prefix_d(key_i) > prefix_d(q)
-        int lo = e, hi = bhi;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if ((__ldg(ix.keys + mid) >> sh) <= qp) lo = mid + 1;
-          else hi = mid;
-        }
-        extra += (unsigned long long)(lo - e);
       }
     }
+    if (live && r == 0) extra += left ? (unsigned long long)(s - lo) : (unsigned long long)(lo - e);
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) extra += __shfl_xor_sync(LCP_FULL_MASK, extra, o);

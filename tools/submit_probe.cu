@@ -72,8 +72,22 @@ int main() {
            1e6 * t_sub / STEPS, 1e6 * t_wait / STEPS);
     for (auto x : ge) CK(cudaGraphExecDestroy(x));
   }
+  // host allocation flags: default, mapped|portable (lcp_pinned_alloc),
+  // write-combined (source of H2D only)
+  const unsigned flag_sets[3] = {cudaHostAllocDefault, cudaHostAllocMapped | cudaHostAllocPortable,
+                                 cudaHostAllocWriteCombined | cudaHostAllocMapped | cudaHostAllocPortable};
+  for (int fs = 0; fs < 3; ++fs) {
+    for (int i = 0; i < D; ++i) {
+      CK(cudaFreeHost(hin[i]));
+      CK(cudaHostAlloc(&hin[i], B, flag_sets[fs]));
+      if (fs < 2) {
+        CK(cudaFreeHost(hout[i]));
+        CK(cudaHostAlloc(&hout[i], B, flag_sets[fs]));
+      }
+    }
   // copy-engine duplex: H2D only, D2H only, and both at once on separate
   // streams (no dependencies), 256 KB each, depth 8
+  printf("host flags %s\n", fs == 0 ? "default" : fs == 1 ? "mapped|portable" : "write-combined (H2D source)");
   for (int mode = 0; mode < 3; ++mode) {
     CK(cudaDeviceSynchronize());
     const auto t0 = std::chrono::steady_clock::now();
@@ -90,6 +104,7 @@ int main() {
     const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     printf("%s: %.2f us per 256 KB copy\n", mode == 0 ? "H2D only" : mode == 1 ? "D2H only" : "H2D and D2H mixed",
            1e6 * el / STEPS);
+  }
   }
   return 0;
 }
