@@ -601,9 +601,13 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, MODE == 2 ? 1 : 2)
     LCP_STAMP(qi, 0);
     const uint16_t* qrow = queries + (size_t)qi * L;
     const u32 s0 = has0 ? qrow[lane] : 0u;
-    const u32 s1 = has1 ? qrow[lane + 32] : 0u;
-    const bool bad = (has0 && (int)s0 >= ix.sigma) || (has1 && (int)s1 >= ix.sigma);
-    const u64 v = (has0 ? (u64)s0 << sh0 : 0ull) | (has1 ? (u64)s1 << sh1 : 0ull);
+    bool bad = has0 && (int)s0 >= ix.sigma;
+    u64 v = has0 ? (u64)s0 << sh0 : 0ull;
+    if (L > 32) {  // warp-uniform: only sigma = 2 keys hold more than 32 symbols
+      const u32 s1 = has1 ? qrow[lane + 32] : 0u;
+      bad |= has1 && (int)s1 >= ix.sigma;
+      v |= has1 ? (u64)s1 << sh1 : 0ull;
+    }
     const u64 q = ((u64)__reduce_or_sync(LCP_FULL_MASK, (u32)(v >> 32)) << 32) |
                   (u64)__reduce_or_sync(LCP_FULL_MASK, (u32)v);
     const bool any_bad = __any_sync(LCP_FULL_MASK, bad);
