@@ -537,7 +537,11 @@ C5_ITEMS = int(os.environ.get("LCP_BENCH_C5_ITEMS", 200_000_000))  # BASELINE co
 # NVLink).  p2p is tested at one rank; no multi-GPU box was available to
 # validate it, so NCCL stays the default (LCP_BENCH_EXCHANGE=p2p to select it)
 EXCHANGE = os.environ.get("LCP_BENCH_EXCHANGE", "all_to_all")
-C5_INFLIGHT = int(os.environ.get("LCP_BENCH_C5_INFLIGHT", "4"))  # sharded steps in flight per rank
+# sharded steps in flight per rank (tools/c5_probe.py at 25M rows, one GPU:
+# 2 / 4 / 8 slots -> 204 / 344 / 411 M q/s); under NCCL each slot holds its own
+# communicator, so fewer of them there
+C5_INFLIGHT = int(os.environ.get("LCP_BENCH_C5_INFLIGHT", "8"))
+C5_INFLIGHT_NCCL = int(os.environ.get("LCP_BENCH_C5_INFLIGHT_NCCL", "4"))
 # our kernels per range-sharded step: pack + route (own), counted query,
 # thresholds, encode, pack + route (consult), counted query, encode, merge
 SHARD_LAUNCHES_PER_STEP = 10
@@ -604,7 +608,7 @@ def config5_leg(args, world, rank, dev, barrier, max_over_ranks, scheme: str = "
     # buffers (slot) and, under NCCL, its own communicator (process group):
     # one step is a chain of small dependent launches and exchanges, so its
     # latency, not any one kernel, bounds a single stream
-    n_slots = C5_INFLIGHT if world == 1 or nccl else 1
+    n_slots = C5_INFLIGHT if world == 1 else (min(C5_INFLIGHT, C5_INFLIGHT_NCCL) if nccl else 1)
     groups = [dist.new_group(list(range(world))) if nccl else None for _ in range(n_slots)]
     slot_streams = [torch.cuda.Stream(device=dev) for _ in range(n_slots)]
     with torch.cuda.stream(stream):
