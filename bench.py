@@ -384,9 +384,11 @@ def main() -> None:
             barrier()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             # one more untimed replay queued right ahead of the start event keeps
-            # the GPU busy while the host enqueues the timed graph, so the timed
-            # region starts on a warm pipeline instead of an idle GPU (what a
-            # serving loop sees) and a short --steps run matches a long one
+            # the GPU busy while the host enqueues the timed graph, so no host
+            # launch latency lands inside the region.  The region itself still
+            # starts at that replay's join, with an empty pipeline: a short
+            # --steps run includes one fill and one drain (about one batch's
+            # latency), which a long run amortises
             (gt if gt is not None else g).replay()
             t0 = time.perf_counter()
             a.record(main_stream)
