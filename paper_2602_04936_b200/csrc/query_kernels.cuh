@@ -41,6 +41,15 @@ template <int WMAX>
 __device__ __forceinline__ bool warp_pack_query(const uint16_t* __restrict__ qrow,
                                                 const DevIndex& ix, u64 (&qk)[WMAX]) {
   const int lane = lane_id();
+  if (ix.L <= 32) {  // warp-uniform: one symbol per lane, selected into its word
+    const bool has = lane < ix.L;
+    const u32 s = has ? qrow[lane] : 0u;
+    const u64 v = has ? (u64)s << sym_shift(lane, ix) : 0ull;
+    const int wj = lane >> (6 - ix.lb);
+#pragma unroll
+    for (int w = 0; w < WMAX; ++w) qk[w] = warp_or64(w == wj ? v : 0ull);
+    return !__any_sync(LCP_FULL_MASK, has && (int)s >= ix.sigma);
+  }
 #pragma unroll
   for (int w = 0; w < WMAX; ++w) qk[w] = 0;
   bool bad = false;
