@@ -221,6 +221,17 @@ __device__ __forceinline__ int region_lcps(const DevIndex& ix, long long s, cons
   return dmax;
 }
 
+// lcp of sorted row i (0 <= i < n) against q, with the row's id loaded in the
+// same round trip (the id is needed only when the row qualifies, but loading
+// it after the lcp would cost a second dependent round trip)
+template <int WMAX>
+__device__ __forceinline__ int lcp_id_at(const DevIndex& ix, long long i, const u64 (&qk)[WMAX], u32& id) {
+  const u64 x = __ldg((WMAX == 1 ? ix.keys : ix.keys_w0) + i) ^ qk[0];
+  id = __ldg(ix.order + i);
+  if (x) return __clzll((long long)x) >> ix.lb;
+  return WMAX == 1 ? ix.L : lcp_rest<WMAX>(ix, i, qk);
+}
+
 // Stage the top search levels into shared memory with one TMA bulk copy.
 // stage_issue starts the copy; stage_wait blocks on its mbarrier (phase 0),
 // so warps can load and pack their first query while the copy is in flight.
@@ -364,9 +375,10 @@ __device__ __forceinline__ void extend_range(const DevIndex& ix, const u64 (&qk)
       break;
     }
     long long i = e - 32 + lane;
-    int l = i >= 0 ? lcp_at<WMAX>(ix, i, qk) : -1;
+    u32 oid;
+    const int l = lcp_id_at<WMAX>(ix, max(i, 0ll), qk, oid) | (i >= 0 ? 0 : -1);
     bool c = l >= dstar;
-    warp_offer(slot, thr, c ? make_comp<C>(l, ix.order[i], L, idbits) : ~C(0), need);
+    warp_offer(slot, thr, c ? make_comp<C>(l, oid, L, idbits) : ~C(0), need);
     unsigned m = __ballot_sync(LCP_FULL_MASK, c);
     rsize += __popc(m);
     if (m) rlo = e - 32 + (__ffs(m) - 1);
@@ -383,9 +395,10 @@ __device__ __forceinline__ void extend_range(const DevIndex& ix, const u64 (&qk)
       break;
     }
     long long i = e + lane;
-    int l = i < n ? lcp_at<WMAX>(ix, i, qk) : -1;
+    u32 oid;
+    const int l = lcp_id_at<WMAX>(ix, min(i, n - 1), qk, oid) | (i < n ? 0 : -1);
     bool c = l >= dstar;
-    warp_offer(slot, thr, c ? make_comp<C>(l, ix.order[i], L, idbits) : ~C(0), need);
+    warp_offer(slot, thr, c ? make_comp<C>(l, oid, L, idbits) : ~C(0), need);
     unsigned m = __ballot_sync(LCP_FULL_MASK, c);
     rsize += __popc(m);
     e += 32;
