@@ -611,7 +611,9 @@ def config5_leg(args, world, rank, dev, barrier, max_over_ranks, scheme: str = "
     # one step is a chain of small dependent launches and exchanges, so its
     # latency, not any one kernel, bounds a single stream
     n_slots = C5_INFLIGHT if world == 1 else (min(C5_INFLIGHT, C5_INFLIGHT_NCCL) if nccl else 1)
-    groups = [dist.new_group(list(range(world))) if nccl else None for _ in range(n_slots)]
+    # slot 0 keeps the default group (the p2p leg's symmetric-memory
+    # rendezvous runs on it); slots 1.. get their own communicators
+    groups = [dist.new_group(list(range(world))) if nccl and s_ > 0 else None for s_ in range(n_slots)]
     slot_streams = [torch.cuda.Stream(device=dev) for _ in range(n_slots)]
     with torch.cuda.stream(stream):
         pool = torch.from_numpy(qs).to(dev).view(n_pool, BATCH, SEQ_LEN)
