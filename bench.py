@@ -999,6 +999,26 @@ def extras(idx, ds, qs, stream, flush_buf) -> dict:
     tal_fn = lambda i: tal.native.query_device(dq[i % n_pool], K, "tal", ids, lcps, hits, stream=st)
     ms, _ = per_step_ms(tal_fn, 8, 5)
     out["tal256_qps"] = BATCH / (ms / 1e3)
+    # SURVEY §8d TAL bytes: keys + ids of every distinct bucket the batch hits,
+    # plus 8 + K_b + 6k per query.  That is the TAL algorithm's traffic (it
+    # scans the bucket); the kernel gets the same answer and counters without
+    # sweeping it, so this fraction credits the algorithm, not bytes moved
+    try:
+        qs0 = qs[:BATCH].astype(np.int64)
+        code = np.zeros(BATCH, np.int64)
+        for j in range(tal.bucket_depth):
+            code = code * SIGMA + qs0[:, j]
+        dirs = tal.directory
+        uniq = np.unique(code)
+        kb = algorithmic_key_bytes(SEQ_LEN, SIGMA)
+        tal_bytes = float((dirs[uniq + 1] - dirs[uniq]).sum()) * (kb + 4) + BATCH * (8 + kb + 6 * K)
+        out["tal256_roofline"] = {
+            "bytes_per_batch": tal_bytes, "buckets_hit": int(uniq.size), "batch_us": ms * 1e3,
+            "achieved_gbs": tal_bytes / (ms / 1e3) / 1e9, "frac": tal_bytes / (ms / 1e3) / 1e9 / peak,
+            "formula": "SURVEY §8d: sum over distinct buckets hit of |B|*(K_b+4) + Q*(8 + K_b + 6k); "
+                       "one batch in flight, back-to-back graph replays"}
+    except Exception as e:  # pragma: no cover - reporting only
+        out["tal256_roofline"] = {"unavailable": f"{type(e).__name__}: {e}"}
     # energy: NVML counter over >= 3 s of graph-replayed batches (gross, and net of idle)
     energy = nvml_energy()
     if energy is not None:
