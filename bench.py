@@ -1103,6 +1103,26 @@ def extras(idx, ds, qs, stream, flush_buf) -> dict:
     out["gnc_single_query"] = {"hz": len(lat) / float(np.sum(lat)), "p50_ms": 1e3 * float(np.median(lat)),
                                "p99_ms": 1e3 * float(np.percentile(lat, 99)),
                                "api": "TrieIndex.query(q, 5, 'complete') per step, N=100k, L=24"}
+    # the same loop in latency mode: a resident warp answers through mailboxes
+    # in page-locked host memory (no launch, copy or event per query); every
+    # answer is checked against the batch API (nothing in the block
+    # synchronises the device: the warp stays resident while it is in use)
+    ref = gi.query_batch(readings, 5, "complete")
+    lat = []
+    with gi.low_latency(5, "complete"):
+        for q in readings[:20]:
+            gi.query(q, 5, "complete")
+        for i, q in enumerate(readings):
+            t0 = time.perf_counter()
+            r = gi.query(q, 5, "complete")
+            lat.append(time.perf_counter() - t0)
+            if r.pairs() != ref.pairs(i):
+                raise RuntimeError(f"latency-mode answer {i} differs from the batch API")
+    out["gnc_single_query_low_latency"] = {
+        "hz": len(lat) / float(np.sum(lat)), "p50_ms": 1e3 * float(np.median(lat)),
+        "p99_ms": 1e3 * float(np.percentile(lat, 99)),
+        "api": "with TrieIndex.low_latency(5, 'complete'): TrieIndex.query(q, 5, 'complete') per step, "
+               "N=100k, L=24 (csrc/serve_kernels.cuh)"}
     return out
 
 

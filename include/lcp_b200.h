@@ -276,6 +276,28 @@ int lcp_merge_candidates_peers(const uint64_t* const* peer_cand, int32_t world, 
                                const uint32_t* my_signals, const uint32_t* epoch, uint32_t* ids,
                                uint16_t* lcps, int32_t* hits, int32_t out_stride, void* stream);
 
+/* ---- single-query server (latency mode; the reference answers one query
+ * per call, trie.py:290-342, and its GNC loop calls it back to back,
+ * bench.py:353) ------------------------------------------------------------
+ * One resident warp answers single queries through two mailboxes in
+ * page-locked host memory (serve_kernels.cuh): lcp_server_query copies the
+ * row at `query_row` into the request mailbox, the warp answers it with the
+ * batch kernel's per-query code and sends the packed answer back in one
+ * burst, and lcp_server_query unpacks it into `out_block`
+ * (lcp_packed_layout_for(1, out_stride), work counters included): no launch,
+ * copy or event per query.  `query_row` and `out_block` are ordinary host
+ * memory.  W == 1, strict or complete, min(k, n) <= 16 and out_stride <= 16
+ * (else LCP_ERR_STATE: use the batch path).  lcp_server_query spins until
+ * the answer is in; LCP_ERR_INVALID_INPUT for a symbol >= sigma.  The warp
+ * exits after 100 ms without a request (so a device-wide synchronisation
+ * never waits on it for long) and is relaunched on the next query.  One
+ * server per thread; lcp_server_stop ends and frees it. */
+typedef struct lcp_server lcp_server;
+int lcp_server_start(const lcp_index* index, int32_t k, int32_t mode, int32_t out_stride,
+                     const uint16_t* query_row, void* out_block, lcp_server** out);
+int lcp_server_query(lcp_server* server);
+int lcp_server_stop(lcp_server* server);
+
 /* ---- host staging (no reference counterpart) -----------------------------
  * Page-locked, device-mapped host buffers (cudaHostAlloc): *_host calls DMA
  * directly, and small packed batches in them use direct host I/O. */

@@ -99,6 +99,9 @@ SIGNATURES = {
     "lcp_encode_candidates_sel": (ctypes.c_int, [_P, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _P, _I64, _P, _P]),
     "lcp_signal_peers": (ctypes.c_int, [_P, _I32, _I32, _P, _P]),
     "lcp_merge_candidates_peers": (ctypes.c_int, [_P, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _I32, _P]),
+    "lcp_server_start": (ctypes.c_int, [_P, _I32, _I32, _I32, _P, _P, ctypes.POINTER(_P)]),
+    "lcp_server_query": (ctypes.c_int, [_P]),
+    "lcp_server_stop": (ctypes.c_int, [_P]),
     "lcp_pinned_alloc": (ctypes.c_int, [_I64, ctypes.POINTER(_P)]),
     "lcp_pinned_free": (ctypes.c_int, [_P]),
     "lcp_stream_sync": (ctypes.c_int, [_P]),

@@ -24,6 +24,7 @@
 #include "fullscan_kernels.cuh"
 #include "query_kernels.cuh"
 #include "shard_kernels.cuh"
+#include "serve_kernels.cuh"
 
 namespace {
 
@@ -1978,6 +1979,168 @@ int lcp_merge_candidates_peers(const uint64_t* const* peer_cand, int32_t world, 
       reinterpret_cast<const u64* const*>(peer_cand), world, rank, m, k, take, length, strict,
       my_signals, epoch, ids, lcps, hits, std::max(1, out_stride));
   LCP_CK_LAUNCH();
+  return LCP_OK;
+}
+
+// ---- persistent single-query server (serve_kernels.cuh) ----------------------
+}  // extern "C"
+
+struct lcp_server {
+  const lcp_index* ix = nullptr;
+  unsigned* box = nullptr;      // page-locked mailboxes: request (8 sectors), response (8 sectors)
+  unsigned* d_box = nullptr;    // device alias
+  cudaStream_t stream = nullptr;
+  const uint16_t* row = nullptr;  // the caller's query row (host)
+  char* out = nullptr;            // the caller's packed block (host)
+  lcp_packed_layout lay{};
+  int k = 0, mode = 0, stride = 0, nq = 0, nr = 0;
+  unsigned seq = 0;
+  size_t smem = 0;
+  int (*launch)(lcp_server*, unsigned) = nullptr;
+};
+
+template <typename C, int T, int MODE>
+static int serve_launch(lcp_server* s, unsigned last) {
+  static const bool attr = [] {
+    cudaFuncSetAttribute(k_serve_w1<C, T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaGetLastError();
+    return true;
+  }();
+  (void)attr;
+  k_serve_w1<C, T, MODE><<<1, 32, s->smem, s->stream>>>(s->ix->dv, s->d_box, s->d_box + SERVE_SECTORS * 8,
+                                                        last, s->k, s->stride);
+  LCP_CK_LAUNCH();
+  return LCP_OK;
+}
+
+extern "C" {
+
+int lcp_server_start(const lcp_index* ix, int32_t k, int32_t mode, int32_t out_stride, const uint16_t* query_row,
+                     void* out_block, lcp_server** out) {
+  if (!ix || !out || !query_row || !out_block) return fail(LCP_ERR_INVALID_INPUT, "null argument");
+  *out = nullptr;
+  const DevIndex& dv = ix->dv;
+  if (mode != LCP_MODE_STRICT && mode != LCP_MODE_COMPLETE)
+    return fail(LCP_ERR_STATE, "the single-query server runs strict and complete mode");
+  if (dv.W != 1 || dv.n < 1 || k < 1 || k > FAST_KMAX)
+    return fail(LCP_ERR_STATE, "the single-query server needs W == 1, n >= 1 and k <= 32");
+  const long long need = mode == LCP_MODE_COMPLETE ? std::min<long long>(k, dv.n) : k;
+  if (need >= 17 || out_stride > 16) return fail(LCP_ERR_STATE, "the single-query server handles need <= 16");
+  const long long ns = std::max<long long>(1, std::min<long long>(k, dv.n));
+  if (out_stride < ns) return fail(LCP_ERR_INVALID_INPUT, "out_stride must be >= min(k, n)");
+  const int nq = (dv.L + SERVE_SYMS_PER_SECTOR - 1) / SERVE_SYMS_PER_SECTOR;
+  const int nr = (SERVE_P_IDS + 6 * out_stride + SERVE_PAYLOAD_PER_SECTOR - 1) / SERVE_PAYLOAD_PER_SECTOR;
+  if (nq > SERVE_SECTORS || nr > SERVE_SECTORS) return fail(LCP_ERR_STATE, "query row too long for the server");
+  auto* s = new lcp_server();
+  s->ix = ix;
+  s->k = k;
+  s->mode = mode;
+  s->stride = out_stride;
+  s->nq = nq;
+  s->nr = nr;
+  s->lay = packed_layout(1, out_stride);
+  s->row = query_row;
+  s->out = static_cast<char*>(out_block);
+  s->smem = 16 + (size_t)dv.smem_entries * 8 + 2 * SERVE_SECTORS * 8 * 4;
+  void* c = nullptr;
+  const size_t bytes = 2 * SERVE_SECTORS * 32;
+  if (cudaHostAlloc(&c, bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
+      cudaHostGetDevicePointer(reinterpret_cast<void**>(&s->d_box), c, 0) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    if (c) cudaFreeHost(c);
+    delete s;
+    return fail(LCP_ERR_CUDA, "server allocation failed");
+  }
+  s->box = static_cast<unsigned*>(c);
+  memset(s->box, 0, bytes);
+  const bool u32c = dv.idbits < 32;
+  if (mode == LCP_MODE_STRICT) s->launch = u32c ? serve_launch<u32, 2, 0> : serve_launch<u64, 2, 0>;
+  else s->launch = u32c ? serve_launch<u32, 2, 1> : serve_launch<u64, 2, 1>;
+  const int r = s->launch(s, 0);
+  if (r != LCP_OK) {
+    cudaStreamDestroy(s->stream);
+    cudaFreeHost(s->box);
+    delete s;
+    return r;
+  }
+  *out = s;
+  return LCP_OK;
+}
+
+// write tag `t` into every request sector, each after its symbols
+static void serve_post(lcp_server* s, unsigned t) {
+  const int L = s->ix->dv.L;
+  for (int j = 0; j < s->nq; ++j) {
+    unsigned* sec = s->box + j * 8;
+    const int first = j * SERVE_SYMS_PER_SECTOR;
+    const int cnt = std::min(SERVE_SYMS_PER_SECTOR, L - first);
+    memcpy(sec, s->row + first, (size_t)cnt * 2);
+    __atomic_store_n(sec + 7, t, __ATOMIC_RELEASE);
+  }
+}
+
+int lcp_server_query(lcp_server* s) {
+  if (!s) return fail(LCP_ERR_INVALID_INPUT, "null server");
+  const unsigned want = ++s->seq;
+  if (want & SERVE_STOP) return fail(LCP_ERR_STATE, "single-query server sequence exhausted");
+  serve_post(s, want);
+  unsigned* resp = s->box + SERVE_SECTORS * 8;
+  const auto t_start = std::chrono::steady_clock::now();
+  for (unsigned spins = 1;; ++spins) {
+    bool ready = true;
+    for (int j = 0; j < s->nr && ready; ++j) ready = __atomic_load_n(resp + j * 8 + 7, __ATOMIC_ACQUIRE) == want;
+    if (ready) break;
+    if ((spins & 4095) == 0) {  // the warp idles out after SERVE_IDLE_NS: relaunch it
+      if (std::chrono::steady_clock::now() - t_start > std::chrono::seconds(2)) {
+        std::string tags;
+        for (int j = 0; j < s->nr; ++j) tags += " " + std::to_string(__atomic_load_n(resp + j * 8 + 7, __ATOMIC_ACQUIRE));
+        std::string rq;
+        for (int j = 0; j < s->nq; ++j) rq += " " + std::to_string(__atomic_load_n(s->box + j * 8 + 7, __ATOMIC_ACQUIRE));
+        return fail(LCP_ERR_INTERNAL, "single-query server: no answer after 2 s (request " + std::to_string(want) +
+                                          ", request tags" + rq + ", response tags" + tags + ", stream " +
+                                          cudaGetErrorString(cudaStreamQuery(s->stream)) + ")");
+      }
+      const cudaError_t e = cudaStreamQuery(s->stream);
+      if (e == cudaSuccess) {
+        bool again = true;
+        for (int j = 0; j < s->nr && again; ++j) again = __atomic_load_n(resp + j * 8 + 7, __ATOMIC_ACQUIRE) == want;
+        if (again) break;
+        LCP_TRY(s->launch(s, want - 1));
+      } else if (e != cudaErrorNotReady) {
+        return fail(LCP_ERR_CUDA, std::string("single-query server: ") + cudaGetErrorString(e));
+      }
+    }
+#if defined(__x86_64__)
+    __builtin_ia32_pause();
+#endif
+  }
+  // unpack the payload (28 bytes per sector) into the caller's packed block
+  unsigned char pay[SERVE_SECTORS * SERVE_PAYLOAD_PER_SECTOR];
+  for (int j = 0; j < s->nr; ++j) memcpy(pay + j * SERVE_PAYLOAD_PER_SECTOR, resp + j * 8, SERVE_PAYLOAD_PER_SECTOR);
+  const int st = s->stride;
+  memcpy(s->out + s->lay.ids, pay + SERVE_P_IDS, (size_t)st * 4);
+  memcpy(s->out + s->lay.lcps, pay + SERVE_P_IDS + 4 * st, (size_t)st * 2);
+  memcpy(s->out + s->lay.hits, pay + SERVE_P_HITS, 4);
+  memcpy(s->out + s->lay.matched_depth, pay + SERVE_P_MD, 2);
+  memcpy(s->out + s->lay.aux, pay + SERVE_P_AUX, 16);
+  int err = 0;
+  memcpy(&err, pay + SERVE_P_ERR, 4);
+  memcpy(s->out + s->lay.err, &err, 4);
+  if (err)
+    return fail(LCP_ERR_INVALID_INPUT,
+                "query symbol out of range for alphabet of size " + std::to_string(s->ix->dv.sigma));
+  return LCP_OK;
+}
+
+int lcp_server_stop(lcp_server* s) {
+  if (!s) return LCP_OK;
+  serve_post(s, (s->seq + 1) | SERVE_STOP);
+  const cudaError_t e = cudaStreamSynchronize(s->stream);
+  cudaStreamDestroy(s->stream);
+  cudaFreeHost(s->box);
+  delete s;
+  if (e != cudaSuccess) return fail(LCP_ERR_CUDA, std::string("single-query server: ") + cudaGetErrorString(e));
   return LCP_OK;
 }
 

@@ -590,21 +590,16 @@ __device__ __forceinline__ unsigned long long tal_sym_region(const DevIndex& ix,
   return sym + extra;
 }
 
+// One query of k_query_w1 (below) for the warp: row `qrow`, output slot qi.
+// Shared by the batch kernel and the persistent single-query server.
 template <typename C, int T, int MODE>
-__global__ void __launch_bounds__(QW_MAX_THREADS, MODE == 2 ? 1 : 2)
-    k_query_w1(const __grid_constant__ DevIndex ix, const uint16_t* __restrict__ queries, int count, int k,
-               int stride, u32* __restrict__ out_ids, uint16_t* __restrict__ out_lcps,
-               int* __restrict__ out_hits, uint16_t* __restrict__ out_md,
-               u64* __restrict__ out_aux, int* __restrict__ err) {
+__device__ __forceinline__ void query_w1_one(const DevIndex& ix, const uint16_t* __restrict__ qrow, int qi,
+                                             int k, int stride, u32* __restrict__ out_ids,
+                                             uint16_t* __restrict__ out_lcps, int* __restrict__ out_hits,
+                                             uint16_t* __restrict__ out_md, u64* __restrict__ out_aux,
+                                             int* __restrict__ err, u64* bar, const u64* staged) {
   // MODE: 0 strict, 1 complete, 2 tal (trie.MODE_CODES)
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  u64* bar = reinterpret_cast<u64*>(smem_raw);
-  u64* staged = reinterpret_cast<u64*>(smem_raw + 16);
-  stage_issue(ix, bar, staged);
-
   const int lane = lane_id();
-  const int warp = threadIdx.x >> 5;
-  const int warps = blockDim.x >> 5;
   const int n = (int)ix.n;  // < 2**31 by contract
   const int L = ix.L;
   const int b = ix.b, lb = ix.lb;
@@ -618,204 +613,218 @@ __global__ void __launch_bounds__(QW_MAX_THREADS, MODE == 2 ? 1 : 2)
   const bool has0 = lane < L, has1 = lane + 32 < L;
   const int sh0 = 64 - b * (lane + 1), sh1 = 64 - b * (lane + 33);
 
-  if (ix.dcount) count = min(count, *ix.dcount);  // device-resident batch size (lcp_query_counted)
-  for (int qi = blockIdx.x * warps + warp; qi < count; qi += gridDim.x * warps) {
-    LCP_STAMP(qi, 0);
-    const uint16_t* qrow = queries + (size_t)qi * L;
-    const u32 s0 = has0 ? qrow[lane] : 0u;
-    bool bad = has0 && (int)s0 >= ix.sigma;
-    u64 v = has0 ? (u64)s0 << sh0 : 0ull;
-    if (L > 32) {  // warp-uniform: only sigma = 2 keys hold more than 32 symbols
-      const u32 s1 = has1 ? qrow[lane + 32] : 0u;
-      bad |= has1 && (int)s1 >= ix.sigma;
-      v |= has1 ? (u64)s1 << sh1 : 0ull;
+  LCP_STAMP(qi, 0);
+  const u32 s0 = has0 ? qrow[lane] : 0u;
+  bool bad = has0 && (int)s0 >= ix.sigma;
+  u64 v = has0 ? (u64)s0 << sh0 : 0ull;
+  if (L > 32) {  // warp-uniform: only sigma = 2 keys hold more than 32 symbols
+    const u32 s1 = has1 ? qrow[lane + 32] : 0u;
+    bad |= has1 && (int)s1 >= ix.sigma;
+    v |= has1 ? (u64)s1 << sh1 : 0ull;
+  }
+  const u64 q = ((u64)__reduce_or_sync(LCP_FULL_MASK, (u32)(v >> 32)) << 32) |
+                (u64)__reduce_or_sync(LCP_FULL_MASK, (u32)v);
+  const bool any_bad = __any_sync(LCP_FULL_MASK, bad);
+  if (any_bad) {
+    stage_wait(ix, bar);
+    if (lane == 0) {
+      raise_flag(err);
+      out_hits[qi] = 0;
+      out_md[qi] = 0;
+      out_aux[2 * qi] = 0;
+      out_aux[2 * qi + 1] = 0;
     }
-    const u64 q = ((u64)__reduce_or_sync(LCP_FULL_MASK, (u32)(v >> 32)) << 32) |
-                  (u64)__reduce_or_sync(LCP_FULL_MASK, (u32)v);
-    const bool any_bad = __any_sync(LCP_FULL_MASK, bad);
-    if (any_bad) {
-      stage_wait(ix, bar);
+    return;
+  }
+  // TAL: the query's d-prefix bucket [blo, bhi) (tal.py:116-143), looked up
+  // before the search so the directory read overlaps it
+  int blo = 0, bhi = n;
+  if constexpr (MODE == 2) tal_bucket_w1(ix, q, blo, bhi);
+  stage_wait(ix, bar);  // first iteration: the query load overlaps the copy
+  LCP_STAMP(qi, 1);
+  // 64-ary search down to the 16-key leaf block holding lower_bound(q).
+  // Only the root can count 0 separators below q (q <= every key: pos = 0);
+  // below it, a child block starts with its parent's separator, which is < q.
+  int blk = 0;
+  if (ix.nlevels > 0) {
+    const int c0 = ix.smem_levels > 0 ? level_count(staged, 0, q) : level_count_g(ix.levels, 0, q);
+    if (c0 > 0) {
+      blk = c0 - 1;
+      int j = 1;
+#pragma unroll 1
+      for (; j < ix.smem_levels; ++j)
+        blk = blk * LCP_SEARCH_FANOUT + level_count(staged + (int)ix.level_off[j], blk, q) - 1;
+#pragma unroll 1
+      for (; j < ix.nlevels; ++j)
+        blk = blk * LCP_SEARCH_FANOUT + level_count_g(ix.levels + (int)ix.level_off[j], blk, q) - 1;
+    }
+  }
+  LCP_STAMP(qi, 2);
+  // Leaf block [B, B+16) holds pos = lower_bound(q) in (B, B+16] (or
+  // pos = 0); the region is warp-strided (item t*32 + lane) and pos is
+  // never materialised.
+  static_assert(LCP_LEAF_KEYS == 16, "region offsets below assume 16-key leaf blocks");
+  // pos in (B, B + 16]: the region [B - (16T - 8), ...) of 32T keys holds
+  // [pos - need, pos + need) for need <= 16 (T=2) / 32 (T=3) with the
+  // slack split evenly around the leaf block
+  const int s = blk * LCP_LEAF_KEYS - (16 * T - 8);
+  int l[T];
+  u32 id[T];
+  int dmax = -1;
+  // unconditional loads at a clamped index (n >= 1), masked afterwards;
+  // lcp = min(clz64(key ^ q) >> lb, L) is exact for W == 1 (clz64(0) = 64)
+  u64 key[T];
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    const int ic = min(max(s + t * 32 + lane, 0), n - 1);
+    key[t] = __ldg(keys + ic);
+    id[t] = __ldg(order + ic);
+  }
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    // branch-free (-1 outside [0, n)): a branch here let the compiler sink
+    // the key load behind it
+    const int ok_mask = (unsigned)(s + t * 32 + lane) < (unsigned)n ? 0 : -1;
+    l[t] = min(__clzll((long long)(key[t] ^ q)) >> lb, L) | ok_mask;
+    dmax = max(dmax, l[t]);
+  }
+  dmax = (int)__reduce_max_sync(LCP_FULL_MASK, (unsigned)(dmax + 1)) - 1;
+  LCP_STAMP(qi, 3);
+
+  int md = dmax;
+  u64 aux0 = 0, aux1 = 0;
+  bool tal_small = false;  // bucket smaller than k: answer = the whole bucket
+  if constexpr (MODE == 2) {
+    const unsigned long long sym = tal_sym_region<T>(ix, q, blo, bhi, l, s, dmax);
+    md = ix.tal_depth;
+    aux0 = (u64)(bhi - blo);
+    aux1 = sym;
+    tal_small = bhi - blo < k;
+    if (bhi == blo) {  // empty bucket: no hits, nothing scanned (tal.py:168-171)
       if (lane == 0) {
-        raise_flag(err);
         out_hits[qi] = 0;
-        out_md[qi] = 0;
+        out_md[qi] = (uint16_t)md;
         out_aux[2 * qi] = 0;
         out_aux[2 * qi + 1] = 0;
       }
-      continue;
+      return;
     }
-    // TAL: the query's d-prefix bucket [blo, bhi) (tal.py:116-143), looked up
-    // before the search so the directory read overlaps it
-    int blo = 0, bhi = n;
-    if constexpr (MODE == 2) tal_bucket_w1(ix, q, blo, bhi);
-    stage_wait(ix, bar);  // first iteration: the query load overlaps the copy
-    LCP_STAMP(qi, 1);
-    // 64-ary search down to the 16-key leaf block holding lower_bound(q).
-    // Only the root can count 0 separators below q (q <= every key: pos = 0);
-    // below it, a child block starts with its parent's separator, which is < q.
-    int blk = 0;
-    if (ix.nlevels > 0) {
-      const int c0 = ix.smem_levels > 0 ? level_count(staged, 0, q) : level_count_g(ix.levels, 0, q);
-      if (c0 > 0) {
-        blk = c0 - 1;
-        int j = 1;
-#pragma unroll 1
-        for (; j < ix.smem_levels; ++j)
-          blk = blk * LCP_SEARCH_FANOUT + level_count(staged + (int)ix.level_off[j], blk, q) - 1;
-#pragma unroll 1
-        for (; j < ix.nlevels; ++j)
-          blk = blk * LCP_SEARCH_FANOUT + level_count_g(ix.levels + (int)ix.level_off[j], blk, q) - 1;
-      }
+  }
+  if (tal_small) {
+    // |bucket| < k <= 32: rank the whole bucket, one item per lane
+    const int bs = bhi - blo;
+    C cv = ~C(0);
+    if (lane < bs) {
+      const u64 x = __ldg(keys + blo + lane) ^ q;
+      const int ll = x ? (__clzll((long long)x) >> lb) : L;
+      cv = make_comp<C>(ll, __ldg(order + blo + lane), L, idbits);
     }
-    LCP_STAMP(qi, 2);
-    // Leaf block [B, B+16) holds pos = lower_bound(q) in (B, B+16] (or
-    // pos = 0); the region is warp-strided (item t*32 + lane) and pos is
-    // never materialised.
-    static_assert(LCP_LEAF_KEYS == 16, "region offsets below assume 16-key leaf blocks");
-    // pos in (B, B + 16]: the region [B - (16T - 8), ...) of 32T keys holds
-    // [pos - need, pos + need) for need <= 16 (T=2) / 32 (T=3) with the
-    // slack split evenly around the leaf block
-    const int s = blk * LCP_LEAF_KEYS - (16 * T - 8);
-    int l[T];
-    u32 id[T];
-    int dmax = -1;
-    // unconditional loads at a clamped index (n >= 1), masked afterwards;
-    // lcp = min(clz64(key ^ q) >> lb, L) is exact for W == 1 (clz64(0) = 64)
-    u64 key[T];
-#pragma unroll
-    for (int t = 0; t < T; ++t) {
-      const int ic = min(max(s + t * 32 + lane, 0), n - 1);
-      key[t] = __ldg(keys + ic);
-      id[t] = __ldg(order + ic);
+    int rank = 0;
+    for (int jj = 0; jj < bs; ++jj) rank += __shfl_sync(LCP_FULL_MASK, cv, jj) < cv;
+    if (lane < bs) {
+      const u64 w = widen_comp<C>(cv, idbits);
+      out_ids[(size_t)qi * stride + rank] = (u32)(w & 0xffffffffull);
+      out_lcps[(size_t)qi * stride + rank] = (uint16_t)(L - (int)(w >> 32));
     }
-#pragma unroll
-    for (int t = 0; t < T; ++t) {
-      // branch-free (-1 outside [0, n)): a branch here let the compiler sink
-      // the key load behind it
-      const int ok_mask = (unsigned)(s + t * 32 + lane) < (unsigned)n ? 0 : -1;
-      l[t] = min(__clzll((long long)(key[t] ^ q)) >> lb, L) | ok_mask;
-      dmax = max(dmax, l[t]);
+    if (lane == 0) {
+      out_hits[qi] = bs;
+      out_md[qi] = (uint16_t)md;
+      out_aux[2 * qi] = aux0;
+      out_aux[2 * qi + 1] = aux1;
     }
-    dmax = (int)__reduce_max_sync(LCP_FULL_MASK, (unsigned)(dmax + 1)) - 1;
-    LCP_STAMP(qi, 3);
+    return;
+  }
 
-    int md = dmax;
-    u64 aux0 = 0, aux1 = 0;
-    bool tal_small = false;  // bucket smaller than k: answer = the whole bucket
-    if constexpr (MODE == 2) {
-      const unsigned long long sym = tal_sym_region<T>(ix, q, blo, bhi, l, s, dmax);
-      md = ix.tal_depth;
-      aux0 = (u64)(bhi - blo);
-      aux1 = sym;
-      tal_small = bhi - blo < k;
-      if (bhi == blo) {  // empty bucket: no hits, nothing scanned (tal.py:168-171)
-        if (lane == 0) {
-          out_hits[qi] = 0;
-          out_md[qi] = (uint16_t)md;
-          out_aux[2 * qi] = 0;
-          out_aux[2 * qi + 1] = 0;
-        }
-        continue;
-      }
-    }
-    if (tal_small) {
-      // |bucket| < k <= 32: rank the whole bucket, one item per lane
-      const int bs = bhi - blo;
-      C cv = ~C(0);
-      if (lane < bs) {
-        const u64 x = __ldg(keys + blo + lane) ^ q;
-        const int ll = x ? (__clzll((long long)x) >> lb) : L;
-        cv = make_comp<C>(ll, __ldg(order + blo + lane), L, idbits);
-      }
-      int rank = 0;
-      for (int jj = 0; jj < bs; ++jj) rank += __shfl_sync(LCP_FULL_MASK, cv, jj) < cv;
-      if (lane < bs) {
-        const u64 w = widen_comp<C>(cv, idbits);
-        out_ids[(size_t)qi * stride + rank] = (u32)(w & 0xffffffffull);
-        out_lcps[(size_t)qi * stride + rank] = (uint16_t)(L - (int)(w >> 32));
-      }
-      if (lane == 0) {
-        out_hits[qi] = bs;
-        out_md[qi] = (uint16_t)md;
-        out_aux[2 * qi] = aux0;
-        out_aux[2 * qi + 1] = aux1;
-      }
-      continue;
-    }
-
-    const int dstar = MODE == 0 ? dmax : window_dstar<T>(l, dmax, need);
-    if constexpr (MODE != 2) {
-      aux0 = (u64)(u32)dmax | ((u64)(u32)dstar << 32);
-    }
-    C comp[T];
-    int cnt = 0, r0 = 32 * T;
+  const int dstar = MODE == 0 ? dmax : window_dstar<T>(l, dmax, need);
+  if constexpr (MODE != 2) {
+    aux0 = (u64)(u32)dmax | ((u64)(u32)dstar << 32);
+  }
+  C comp[T];
+  int cnt = 0, r0 = 32 * T;
 #pragma unroll
-    for (int t = 0; t < T; ++t) {
-      const bool c = l[t] >= dstar;
-      comp[t] = c ? make_comp<C>(l[t], id[t], L, idbits) : ~C(0);
-      const unsigned m = __ballot_sync(LCP_FULL_MASK, c);
-      cnt += __popc(m);
-      if (m && r0 == 32 * T) r0 = t * 32 + __ffs(m) - 1;
-    }
-    const int first_valid = s < 0 ? -s : 0;
-    const int end = min(s + 32 * T, n);
-    const bool left = s > 0 && r0 == first_valid;
-    const bool right = end < n && s + r0 + cnt == end;
-    LCP_STAMP(qi, 4);
-    if (!left && !right && cnt <= 32) {
-      // R(d*) lies inside the region: compact the run to one candidate per
-      // lane and rank it by all-pairs comparison (independent shuffles, no
-      // sorting network); the lane of rank r writes output slot r.
-      const int t0 = r0 >> 5, e = r0 + lane;
-      const C a = __shfl_sync(LCP_FULL_MASK, pick_slot<C, T>(comp, t0), e & 31);
-      const C bb = __shfl_sync(LCP_FULL_MASK, pick_slot<C, T>(comp, t0 + 1), e & 31);
-      const C cv = lane < cnt ? (((e >> 5) == t0) ? a : bb) : ~C(0);
-      // all-pairs rank in blocks of 8 with immediate shuffle lanes; lanes >= cnt
-      // hold all-ones and never count, so only the block guard is needed
-      int rank = 0;
+  for (int t = 0; t < T; ++t) {
+    const bool c = l[t] >= dstar;
+    comp[t] = c ? make_comp<C>(l[t], id[t], L, idbits) : ~C(0);
+    const unsigned m = __ballot_sync(LCP_FULL_MASK, c);
+    cnt += __popc(m);
+    if (m && r0 == 32 * T) r0 = t * 32 + __ffs(m) - 1;
+  }
+  const int first_valid = s < 0 ? -s : 0;
+  const int end = min(s + 32 * T, n);
+  const bool left = s > 0 && r0 == first_valid;
+  const bool right = end < n && s + r0 + cnt == end;
+  LCP_STAMP(qi, 4);
+  if (!left && !right && cnt <= 32) {
+    // R(d*) lies inside the region: compact the run to one candidate per
+    // lane and rank it by all-pairs comparison (independent shuffles, no
+    // sorting network); the lane of rank r writes output slot r.
+    const int t0 = r0 >> 5, e = r0 + lane;
+    const C a = __shfl_sync(LCP_FULL_MASK, pick_slot<C, T>(comp, t0), e & 31);
+    const C bb = __shfl_sync(LCP_FULL_MASK, pick_slot<C, T>(comp, t0 + 1), e & 31);
+    const C cv = lane < cnt ? (((e >> 5) == t0) ? a : bb) : ~C(0);
+    // all-pairs rank in blocks of 8 with immediate shuffle lanes; lanes >= cnt
+    // hold all-ones and never count, so only the block guard is needed
+    int rank = 0;
 #pragma unroll
-      for (int blk8 = 0; blk8 < 32; blk8 += 8) {
-        if (blk8 >= cnt) break;
+    for (int blk8 = 0; blk8 < 32; blk8 += 8) {
+      if (blk8 >= cnt) break;
 #pragma unroll
-        for (int jj = 0; jj < 8; ++jj) rank += __shfl_sync(LCP_FULL_MASK, cv, blk8 + jj) < cv;
-      }
-      LCP_STAMP(qi, 5);
-      const int take = min(need, cnt);
-      if (lane < cnt && rank < take) {
-        const u64 w = widen_comp<C>(cv, idbits);
-        out_ids[(size_t)qi * stride + rank] = (u32)(w & 0xffffffffull);
-        out_lcps[(size_t)qi * stride + rank] = (uint16_t)(L - (int)(w >> 32));
-      }
-      if (lane == 0) {
-        out_hits[qi] = take;
-        out_md[qi] = (uint16_t)md;
-        out_aux[2 * qi] = aux0;
-        out_aux[2 * qi + 1] = MODE == 2 ? aux1 : ((u64)(u32)cnt | ((u64)(u32)(s + r0) << 32));
-      }
-      LCP_STAMP(qi, 6);
-      LCP_STAMP(qi, 7);
-      continue;
+      for (int jj = 0; jj < 8; ++jj) rank += __shfl_sync(LCP_FULL_MASK, cv, blk8 + jj) < cv;
     }
-    C slot = sort_run<C, T>(comp, r0, cnt, need);
     LCP_STAMP(qi, 5);
-    u64 qk[1] = {q};
-    long long rsize = cnt, rlo = s + r0;
-    extend_range<C, 1>(ix, qk, dstar, need, left, s, right, end, idbits, slot, rsize, rlo);
-    LCP_STAMP(qi, 6);
-    const int take = (int)min((long long)need, rsize);
-    if (lane < take) {
-      const u64 w = widen_comp<C>(slot, idbits);
-      out_ids[(size_t)qi * stride + lane] = (u32)(w & 0xffffffffull);
-      out_lcps[(size_t)qi * stride + lane] = (uint16_t)(L - (int)(w >> 32));
+    const int take = min(need, cnt);
+    if (lane < cnt && rank < take) {
+      const u64 w = widen_comp<C>(cv, idbits);
+      out_ids[(size_t)qi * stride + rank] = (u32)(w & 0xffffffffull);
+      out_lcps[(size_t)qi * stride + rank] = (uint16_t)(L - (int)(w >> 32));
     }
     if (lane == 0) {
       out_hits[qi] = take;
       out_md[qi] = (uint16_t)md;
       out_aux[2 * qi] = aux0;
-      out_aux[2 * qi + 1] = MODE == 2 ? aux1 : ((u64)rsize | ((u64)rlo << 32));
+      out_aux[2 * qi + 1] = MODE == 2 ? aux1 : ((u64)(u32)cnt | ((u64)(u32)(s + r0) << 32));
     }
+    LCP_STAMP(qi, 6);
     LCP_STAMP(qi, 7);
+    return;
   }
+  C slot = sort_run<C, T>(comp, r0, cnt, need);
+  LCP_STAMP(qi, 5);
+  u64 qk[1] = {q};
+  long long rsize = cnt, rlo = s + r0;
+  extend_range<C, 1>(ix, qk, dstar, need, left, s, right, end, idbits, slot, rsize, rlo);
+  LCP_STAMP(qi, 6);
+  const int take = (int)min((long long)need, rsize);
+  if (lane < take) {
+    const u64 w = widen_comp<C>(slot, idbits);
+    out_ids[(size_t)qi * stride + lane] = (u32)(w & 0xffffffffull);
+    out_lcps[(size_t)qi * stride + lane] = (uint16_t)(L - (int)(w >> 32));
+  }
+  if (lane == 0) {
+    out_hits[qi] = take;
+    out_md[qi] = (uint16_t)md;
+    out_aux[2 * qi] = aux0;
+    out_aux[2 * qi + 1] = MODE == 2 ? aux1 : ((u64)rsize | ((u64)rlo << 32));
+  }
+  LCP_STAMP(qi, 7);
+}
+
+template <typename C, int T, int MODE>
+__global__ void __launch_bounds__(QW_MAX_THREADS, MODE == 2 ? 1 : 2)
+    k_query_w1(const __grid_constant__ DevIndex ix, const uint16_t* __restrict__ queries, int count, int k,
+               int stride, u32* __restrict__ out_ids, uint16_t* __restrict__ out_lcps,
+               int* __restrict__ out_hits, uint16_t* __restrict__ out_md,
+               u64* __restrict__ out_aux, int* __restrict__ err) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  u64* bar = reinterpret_cast<u64*>(smem_raw);
+  u64* staged = reinterpret_cast<u64*>(smem_raw + 16);
+  stage_issue(ix, bar, staged);
+  const int warp = threadIdx.x >> 5;
+  const int warps = blockDim.x >> 5;
+  if (ix.dcount) count = min(count, *ix.dcount);  // device-resident batch size (lcp_query_counted)
+  for (int qi = blockIdx.x * warps + warp; qi < count; qi += gridDim.x * warps)
+    query_w1_one<C, T, MODE>(ix, queries + (size_t)qi * ix.L, qi, k, stride, out_ids, out_lcps, out_hits,
+                             out_md, out_aux, err, bar, staged);
 }
 
 // ---------------------------------------------------------------------------

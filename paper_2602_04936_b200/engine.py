@@ -325,6 +325,45 @@ class NativeIndex:
             ptr(ids), ptr(lcps), ptr(hits), st))
 
 
+class SingleQueryServer:
+    """Latency mode for one thread's single queries (lcp_server_*,
+    csrc/serve_kernels.cuh): a resident warp answers each query written into
+    a page-locked row, straight into a page-locked packed block, with no
+    launch, copy or event per query.  Raises InvalidStateError for shapes
+    the server does not cover (W > 1, min(k, n) > 16, TAL)."""
+
+    def __init__(self, native: "NativeIndex", k: int, mode: str):
+        if mode not in MODES:
+            raise InvalidInputError(f"unknown mode {mode!r}")
+        self.k, self.mode = int(k), mode
+        self._h = None
+        self.row = PinnedArray((1, native.length), np.uint16)
+        self.out = native.alloc_batch(1, k, mode, pinned=True)
+        self.out.mode = mode
+        packed = self.out._packed
+        h = ctypes.c_void_p()
+        check(load().lcp_server_start(native.handle, native.stride_for(k), MODES[mode], packed[2],
+                                      self.row.address, packed[0], ctypes.byref(h)))
+        self._h = h
+        self._native = native  # the index outlives the server
+
+    def query(self, query: np.ndarray) -> BatchResult:
+        self.row.array[0] = query
+        check(load().lcp_server_query(self._h))
+        return self.out
+
+    def close(self) -> None:
+        if self._h:
+            h, self._h = self._h, None
+            check(load().lcp_server_stop(h))
+
+    def __del__(self) -> None:  # pragma: no cover - interpreter shutdown order
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class PendingBatch:
     """An in-flight async batch; result() blocks until its D2H copy landed."""
 

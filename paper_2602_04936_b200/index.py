@@ -14,6 +14,7 @@ never used by the query path.
 
 from __future__ import annotations
 
+import contextlib
 import threading
 from dataclasses import dataclass
 
@@ -73,6 +74,7 @@ class TrieIndex:
         self.sigma = native.sigma
         self.c_sym = work_per_symbol(self.length)
         self._lock = threading.Lock()
+        self._tls = threading.local()  # this thread's latency-mode server (low_latency)
         self._order: np.ndarray | None = None
         self._arena: tuple[np.ndarray, np.ndarray, np.ndarray] | None = None
 
@@ -206,10 +208,47 @@ class TrieIndex:
             query = q  # the kernel checks the symbols and raises the same error
         else:
             query = self._validate_query(q)
-        out = self._native.query_single(query, k, mode)
+        tls = getattr(self, "_tls", None)
+        srv = getattr(tls, "server", None) if tls is not None else None
+        if srv is not None and srv.k == k and srv.mode == mode:
+            out = srv.query(query)  # latency mode (low_latency)
+        else:
+            out = self._native.query_single(query, k, mode)
         if work is not None:
             self._account(out, mode, work)
         return out.result(0)
+
+    @contextlib.contextmanager
+    def low_latency(self, k: int, mode: str = "complete"):
+        """Within the block, this thread's ``query(q, k, mode)`` calls are
+        answered by a resident GPU warp polling page-locked host memory (no
+        launch, copy or event per query; engine.SingleQueryServer).  Shapes
+        the server does not cover (W > 1, min(k, n) > 16) keep the launch
+        path.  Do not synchronise the whole device inside the block: the warp
+        stays resident until it has been idle for 100 ms."""
+        from .core import InvalidStateError
+        from .engine import SingleQueryServer
+
+        if mode not in ("strict", "complete"):
+            raise InvalidInputError(f"mode must be 'strict' or 'complete', got {mode!r}")
+        if k < 1:
+            raise InvalidInputError(f"k must be >= 1, got {k}")
+        srv = None
+        if self.n > 0:
+            try:
+                srv = SingleQueryServer(self._native, k, mode)
+            except InvalidStateError:
+                srv = None
+        if getattr(self, "_tls", None) is None:
+            self._tls = threading.local()
+        prev = getattr(self._tls, "server", None)
+        self._tls.server = srv
+        try:
+            yield self
+        finally:
+            self._tls.server = prev
+            if srv is not None:
+                srv.close()
 
     def query_batch(self, queries, k: int, mode: str = "complete", work: WorkReport | None = None,
                     out: BatchResult | None = None) -> BatchResult:

@@ -1116,3 +1116,72 @@ def test_memoized_query_hits_and_counters(gpu):
     assert cache.misses == 8 and cache.hits == 24
     assert lg.memoized_query(idx, qs[0], 10, "strict", cache) is not cold[0]  # mode is in the key
     assert cache.misses == 9
+
+
+def test_low_latency_server(gpu):
+    """TrieIndex.low_latency: a resident warp answers single queries through
+    page-locked mailboxes (csrc/serve_kernels.cuh).  Answers and work
+    counters equal the batch API for strict / complete, k up to 16, rows of
+    1 to 4 request sectors; shapes it does not serve fall back; an invalid
+    symbol is reported; the warp idles out (a device synchronisation inside
+    the block returns) and is relaunched; threads get their own servers."""
+    import threading
+    import time
+
+    import torch
+
+    for n, L, sigma, seed in ((100_000, 24, 4, 4), (5, 16, 4, 6), (30_000, 48, 2, 7), (20_000, 32, 4, 8)):
+        ds = lg.generate_dataset(n, L, sigma, seed=seed)
+        idx = lg.build(ds)
+        qs = np.vstack([lg.generate_queries(ds, 40, seed=seed + 1),
+                        lg.generate_queries(ds, 40, seed=seed + 2, prefix_len=L // 2)])
+        for k in (1, 5, 10, 16, 20):
+            for mode in ("strict", "complete"):
+                ref = idx.query_batch(qs, k, mode)
+                w_ref, w_got = idx.new_work_report(), idx.new_work_report()
+                idx.query_batch(qs, k, mode, work=w_ref)
+                with idx.low_latency(k, mode):
+                    for i in range(len(qs)):
+                        r = idx.query(qs[i], k, mode, work=w_got)
+                        assert r.pairs() == ref.pairs(i), (n, L, k, mode, i)
+                        assert r.matched_depth == int(ref.matched_depth[i])
+                assert w_got.symbols_compared == w_ref.symbols_compared
+                assert w_got.nodes_visited == w_ref.nodes_visited
+    ds = lg.generate_dataset(50_000, 16, 4, seed=9)
+    idx = lg.build(ds)
+    qs = lg.generate_queries(ds, 8, seed=10)
+    ref = idx.query_batch(qs, 10, "complete")
+    with idx.low_latency(10, "complete"):
+        assert idx._tls.server is not None
+        bad = qs[0].copy()
+        bad[5] = 4
+        with pytest.raises(lg.InvalidInputError, match="alphabet of size 4"):
+            idx.query(bad, 10, "complete")
+        assert idx.query(qs[1], 10, "complete").pairs() == ref.pairs(1)
+        t0 = time.perf_counter()
+        torch.cuda.synchronize()  # waits for the warp to idle out (100 ms)
+        assert time.perf_counter() - t0 < 5.0
+        assert idx.query(qs[2], 10, "complete").pairs() == ref.pairs(2)  # relaunched
+        assert idx.query(qs[3], 10, "strict").pairs() == idx.query_batch(qs[3:4], 10, "strict").pairs(0)
+
+    errors = []
+
+    def worker(t):
+        try:
+            with idx.low_latency(10, "complete"):
+                for i in range(len(qs)):
+                    assert idx.query(qs[i], 10, "complete").pairs() == ref.pairs(i)
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(e)
+
+    threads = [threading.Thread(target=worker, args=(t,)) for t in range(3)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    wide = lg.build(lg.generate_dataset(2000, 32, 65536, seed=11))  # W > 1: not served, same API
+    q = lg.generate_queries(lg.generate_dataset(2000, 32, 65536, seed=11), 1, seed=12)[0]
+    with wide.low_latency(5, "complete"):
+        assert wide._tls.server is None
+        assert wide.query(q, 5, "complete").pairs() == wide.query_batch(q[None], 5, "complete").pairs(0)
