@@ -2068,14 +2068,15 @@ int lcp_server_start(const lcp_index* ix, int32_t k, int32_t mode, int32_t out_s
   return LCP_OK;
 }
 
-// write tag `t` into every request sector, each after its symbols
-static void serve_post(lcp_server* s, unsigned t) {
+// write tag `t` into every request sector, each after its symbols (the
+// caller's row; none for a stop request, whose row may already be gone)
+static void serve_post(lcp_server* s, unsigned t, bool with_row) {
   const int L = s->ix->dv.L;
   for (int j = 0; j < s->nq; ++j) {
     unsigned* sec = s->box + j * 8;
     const int first = j * SERVE_SYMS_PER_SECTOR;
     const int cnt = std::min(SERVE_SYMS_PER_SECTOR, L - first);
-    memcpy(sec, s->row + first, (size_t)cnt * 2);
+    if (with_row) memcpy(sec, s->row + first, (size_t)cnt * 2);
     __atomic_store_n(sec + 7, t, __ATOMIC_RELEASE);
   }
 }
@@ -2084,7 +2085,7 @@ int lcp_server_query(lcp_server* s) {
   if (!s) return fail(LCP_ERR_INVALID_INPUT, "null server");
   const unsigned want = ++s->seq;
   if (want & SERVE_STOP) return fail(LCP_ERR_STATE, "single-query server sequence exhausted");
-  serve_post(s, want);
+  serve_post(s, want, true);
   unsigned* resp = s->box + SERVE_SECTORS * 8;
   const auto t_start = std::chrono::steady_clock::now();
   for (unsigned spins = 1;; ++spins) {
@@ -2135,7 +2136,7 @@ int lcp_server_query(lcp_server* s) {
 
 int lcp_server_stop(lcp_server* s) {
   if (!s) return LCP_OK;
-  serve_post(s, (s->seq + 1) | SERVE_STOP);
+  serve_post(s, (s->seq + 1) | SERVE_STOP, false);
   const cudaError_t e = cudaStreamSynchronize(s->stream);
   cudaStreamDestroy(s->stream);
   cudaFreeHost(s->box);
