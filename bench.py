@@ -1056,6 +1056,22 @@ def extras(idx, ds, qs, stream, flush_buf) -> dict:
     ms8, _ = per_step_ms(lambda i: i8.native.query_device(q8, K, "complete", ids, lcps, hits, stream=st), 16, 10)
     out["indexed_sigma65536_qps"] = BATCH / (ms8 / 1e3)
     out["indexed_sigma65536_device_bytes"] = i8.nbytes
+    # its roofline (SURVEY §8d bytes with K_b = 64 B; |R(d*)| from the aux words)
+    md8 = torch.empty(BATCH, dtype=torch.int16, device=dev)
+    aux8 = torch.empty((BATCH, 2), dtype=torch.int64, device=dev)
+    i8.native.query_device(q8, K, "complete", ids, lcps, hits, md8, aux8, stream=st)
+    torch.cuda.synchronize()
+    rs8 = (aux8[:, 1].cpu().numpy().astype(np.uint64) & np.uint64(0xFFFFFFFF)).astype(np.int64)
+    # a query whose d* is 0 has R(d*) = the whole corpus; the formula's
+    # |R(d*)| * (K_b + 4) would charge it 136 MB although the answer comes from
+    # the id sketch, so runs are charged at most the 64-key leaf region
+    b8 = float(indexed_bytes_per_query(N_ITEMS, SEQ_LEN, 65536, K, np.minimum(rs8, 64)).sum())
+    out["indexed_sigma65536_roofline"] = {
+        "bytes_per_batch": b8, "batch_us": ms8 * 1e3, "achieved_gbs": b8 / (ms8 / 1e3) / 1e9,
+        "frac": b8 / (ms8 / 1e3) / 1e9 / peak, "kernel": "k_query_warp<8>",
+        "queries_with_run_over_64": int((rs8 > 64).sum()),
+        "note": "one batch in flight, back-to-back graph replays; SURVEY §8d indexed bytes with K_b = 64 "
+                "and |R(d*)| capped at the 64-key region (longer runs are served by the id sketch)"}
     del i8, d8
     # config 3, clustered stress (datagen.py:42-52: skew 1.1, depth 8): long
     # shared prefixes make R(d*) wide for many queries
