@@ -137,8 +137,9 @@ class TalEngine:
         if k < 1:
             raise InvalidInputError(f"k must be >= 1, got {k}")
         query = self._validate_query(q)
-        out = self._native.query_host(query.reshape(1, -1), k, "tal",
-                                      out=self._native.single_query_buffer(k, "tal"))
+        # the single-query path: pinned staging row and block, so the kernel
+        # reads the row and writes the answer over PCIe directly (no copies)
+        out = self._native.query_single(query, k, "tal")
         report = self.new_work_report()
         report.queries = 1
         items, sym = tal_counters(out.aux)
