@@ -101,31 +101,28 @@ __device__ __forceinline__ bool w0_less(u64 a0, const u64* key, const u64 (&qk)[
 template <int WMAX>
 __device__ __forceinline__ long long warp_lower_bound(const DevIndex& ix, const u64* staged,
                                                       const u64 (&qk)[WMAX]) {
+  // 32-bit positions (n < 2**31 by contract): the 64-bit index arithmetic
+  // was a large share of the W > 1 kernels' instructions
   const int lane = lane_id();
   const int W = ix.W;
-  long long blk = 0;
+  const int n = (int)ix.n;
+  int blk = 0;
   for (int j = 0;; ++j) {
-    const u64* tab;
-    long long cnt;
-    if (j < ix.smem_levels && WMAX == 1) {
-      tab = staged + ix.level_off[j];
-      cnt = ix.level_cnt[j];
-    } else {
-      tab = ix.levels + ix.level_off[j] * W;
-      cnt = ix.level_cnt[j];
-    }
+    const int off = (int)ix.level_off[j];
+    const int cnt = (int)ix.level_cnt[j];
+    const u64* tab = (j < ix.smem_levels && WMAX == 1) ? staged + off : ix.levels + (size_t)off * W;
     if (j == ix.nlevels) {  // leaf block: 16 keys, one per lane
-      const long long base = blk * LCP_LEAF_KEYS;
-      const long long i = base + lane;
+      const int base = blk * LCP_LEAF_KEYS;
+      const int i = base + lane;
       bool lt = false;
-      if (lane < LCP_LEAF_KEYS && i < ix.n) {
-        if constexpr (WMAX == 1) lt = key_less<WMAX>(ix.keys + i * W, qk, ix);
-        else lt = w0_less<WMAX>(__ldg(ix.keys_w0 + i), ix.keys + i * W, qk, ix);
+      if (lane < LCP_LEAF_KEYS && i < n) {
+        if constexpr (WMAX == 1) lt = key_less<WMAX>(ix.keys + (size_t)i * W, qk, ix);
+        else lt = w0_less<WMAX>(__ldg(ix.keys_w0 + i), ix.keys + (size_t)i * W, qk, ix);
       }
       return base + (int)__reduce_add_sync(LCP_FULL_MASK, (u32)lt);
     }
-    long long base = blk * LCP_SEARCH_FANOUT;
-    long long i0 = base + 2 * lane;
+    const int base = blk * LCP_SEARCH_FANOUT;
+    const int i0 = base + 2 * lane;
     bool lt0 = false, lt1 = false;
     if constexpr (WMAX == 1) {
       if (i0 + 1 < cnt) {
@@ -138,17 +135,17 @@ __device__ __forceinline__ long long warp_lower_bound(const DevIndex& ix, const 
     } else {  // first words (staged, or the global plane) in one 16-byte load;
               // the whole entry from the global table only on a tie
       const bool sm = j < ix.smem_levels;
-      const u64* w0 = (sm ? staged : ix.levels_w0) + ix.level_off[j];
+      const u64* w0 = (sm ? staged : ix.levels_w0) + off;
       if (i0 + 1 < cnt) {  // plain loads from shared memory, __ldg from global
         const ulonglong2 v = sm ? *reinterpret_cast<const ulonglong2*>(w0 + i0)
                                 : __ldg(reinterpret_cast<const ulonglong2*>(w0 + i0));
-        lt0 = w0_less<WMAX>(v.x, tab + i0 * W, qk, ix);
-        lt1 = w0_less<WMAX>(v.y, tab + (i0 + 1) * W, qk, ix);
+        lt0 = w0_less<WMAX>(v.x, tab + (size_t)i0 * W, qk, ix);
+        lt1 = w0_less<WMAX>(v.y, tab + (size_t)(i0 + 1) * W, qk, ix);
       } else if (i0 < cnt) {
-        lt0 = w0_less<WMAX>(sm ? w0[i0] : __ldg(w0 + i0), tab + i0 * W, qk, ix);
+        lt0 = w0_less<WMAX>(sm ? w0[i0] : __ldg(w0 + i0), tab + (size_t)i0 * W, qk, ix);
       }
     }
-    int c = __popc(__ballot_sync(LCP_FULL_MASK, lt0)) + __popc(__ballot_sync(LCP_FULL_MASK, lt1));
+    const int c = (int)__reduce_add_sync(LCP_FULL_MASK, (u32)lt0 + (u32)lt1);
     if (c == 0) return 0;  // only reachable at the root level
     blk = base + c - 1;
   }
