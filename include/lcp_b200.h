@@ -296,6 +296,9 @@ typedef struct lcp_server lcp_server;
 int lcp_server_start(const lcp_index* index, int32_t k, int32_t mode, int32_t out_stride,
                      const uint16_t* query_row, void* out_block, lcp_server** out);
 int lcp_server_query(lcp_server* server);
+/* lcp_server_query with the query read from `row` (L symbols) instead of the
+ * row given at start. */
+int lcp_server_query_row(lcp_server* server, const uint16_t* row);
 int lcp_server_stop(lcp_server* server);
 
 /* ---- host staging (no reference counterpart) -----------------------------

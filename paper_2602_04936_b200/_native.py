@@ -101,6 +101,7 @@ SIGNATURES = {
     "lcp_merge_candidates_peers": (ctypes.c_int, [_P, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _I32, _P]),
     "lcp_server_start": (ctypes.c_int, [_P, _I32, _I32, _I32, _P, _P, ctypes.POINTER(_P)]),
     "lcp_server_query": (ctypes.c_int, [_P]),
+    "lcp_server_query_row": (ctypes.c_int, [_P, _P]),
     "lcp_server_stop": (ctypes.c_int, [_P]),
     "lcp_pinned_alloc": (ctypes.c_int, [_I64, ctypes.POINTER(_P)]),
     "lcp_pinned_free": (ctypes.c_int, [_P]),
@@ -135,11 +136,12 @@ def load() -> ctypes.CDLL:
 
 _host_submit = False  # not yet looked up
 _host_submit_wait = None
+_host_server_query = None
 
 
 def _bind_host_module() -> None:
-    global _host_submit, _host_submit_wait
-    fn = wait = None
+    global _host_submit, _host_submit_wait, _host_server_query
+    fn = wait = srvq = None
     if not os.environ.get("LCP_NO_HOST_EXT"):  # A/B switch
         try:
             from . import _lcp_host
@@ -148,9 +150,10 @@ def _bind_host_module() -> None:
         if _lcp_host is not None:
             lib = load()
             _lcp_host.bind(ctypes.cast(lib.lcp_query_host_packed_async, ctypes.c_void_p).value,
-                           ctypes.cast(lib.lcp_workspace_wait, ctypes.c_void_p).value)
-            fn, wait = _lcp_host.submit, _lcp_host.submit_wait
-    _host_submit, _host_submit_wait = fn, wait
+                           ctypes.cast(lib.lcp_workspace_wait, ctypes.c_void_p).value,
+                           ctypes.cast(lib.lcp_server_query_row, ctypes.c_void_p).value)
+            fn, wait, srvq = _lcp_host.submit, _lcp_host.submit_wait, _lcp_host.server_query
+    _host_submit, _host_submit_wait, _host_server_query = fn, wait, srvq
 
 
 def host_submit():
@@ -160,6 +163,13 @@ def host_submit():
     if _host_submit is False:
         _bind_host_module()
     return _host_submit
+
+
+def host_server_query():
+    """server_query(server, row) of the same module (lcp_server_query_row), or None."""
+    if _host_submit is False:
+        _bind_host_module()
+    return _host_server_query if _host_submit is not None else None
 
 
 def host_submit_wait():

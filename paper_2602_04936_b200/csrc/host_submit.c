@@ -23,23 +23,57 @@ typedef int (*submit_fn)(const void* index, void* ws, const uint16_t* queries, i
                          int32_t flags);
 
 typedef int (*wait_fn)(void* ws);
+typedef int (*server_fn)(void* server, const uint16_t* row);
 
 static submit_fn g_submit = NULL;
 static wait_fn g_wait = NULL;
+static server_fn g_server = NULL;
 
-/* bind(address of lcp_query_host_packed_async, address of lcp_workspace_wait) */
+/* bind(addresses of lcp_query_host_packed_async, lcp_workspace_wait,
+ *      lcp_server_query_row) */
 static PyObject* bind(PyObject* self, PyObject* const* args, Py_ssize_t nargs) {
   (void)self;
-  if (nargs != 2) {
-    PyErr_SetString(PyExc_TypeError, "bind() takes 2 arguments");
+  if (nargs != 3) {
+    PyErr_SetString(PyExc_TypeError, "bind() takes 3 arguments");
     return NULL;
   }
   void* s = PyLong_AsVoidPtr(args[0]);
   void* w = PyLong_AsVoidPtr(args[1]);
+  void* q = PyLong_AsVoidPtr(args[2]);
   if (PyErr_Occurred()) return NULL;
   g_submit = (submit_fn)s;
   g_wait = (wait_fn)w;
+  g_server = (server_fn)q;
   Py_RETURN_NONE;
+}
+
+/* server_query(server, row) -> rc: one latency-mode query (lcp_server_query_row)
+ * with the row taken through the buffer protocol (1-D, 2-byte items) */
+static PyObject* server_query(PyObject* self, PyObject* const* args, Py_ssize_t nargs) {
+  (void)self;
+  if (nargs != 2) {
+    PyErr_SetString(PyExc_TypeError, "server_query() takes 2 arguments");
+    return NULL;
+  }
+  if (!g_server) {
+    PyErr_SetString(PyExc_RuntimeError, "server_query(): bind() the C-ABI entry points first");
+    return NULL;
+  }
+  void* srv = PyLong_AsVoidPtr(args[0]);
+  if (PyErr_Occurred()) return NULL;
+  Py_buffer v;
+  if (PyObject_GetBuffer(args[1], &v, PyBUF_C_CONTIGUOUS | PyBUF_ND) < 0) return NULL;
+  if (v.ndim != 1 || v.itemsize != 2) {
+    PyBuffer_Release(&v);
+    PyErr_SetString(PyExc_ValueError, "the query must be a C-contiguous 1-D 2-byte array");
+    return NULL;
+  }
+  int rc;
+  Py_BEGIN_ALLOW_THREADS
+  rc = g_server(srv, (const uint16_t*)v.buf);
+  Py_END_ALLOW_THREADS
+  PyBuffer_Release(&v);
+  return PyLong_FromLong(rc);
 }
 
 /* submit(index, ws, queries, length, k, mode, out_stride, out_block, flags) -> rc
@@ -93,7 +127,9 @@ static PyObject* submit_wait(PyObject* self, PyObject* const* args, Py_ssize_t n
 
 static PyMethodDef methods[] = {
     {"bind", (PyCFunction)(void (*)(void))bind, METH_FASTCALL,
-     "bind(address of lcp_query_host_packed_async, address of lcp_workspace_wait)"},
+     "bind(addresses of lcp_query_host_packed_async, lcp_workspace_wait, lcp_server_query_row)"},
+    {"server_query", (PyCFunction)(void (*)(void))server_query, METH_FASTCALL,
+     "server_query(server, row) -> rc (lcp_server_query_row)"},
     {"submit", (PyCFunction)(void (*)(void))submit, METH_FASTCALL,
      "submit(index, ws, queries, length, k, mode, out_stride, out_block, flags) -> rc"},
     {"submit_wait", (PyCFunction)(void (*)(void))submit_wait, METH_FASTCALL,

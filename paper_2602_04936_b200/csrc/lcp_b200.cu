@@ -2081,6 +2081,15 @@ static void serve_post(lcp_server* s, unsigned t, bool with_row) {
   }
 }
 
+int lcp_server_query_row(lcp_server* s, const uint16_t* row) {
+  if (!s || !row) return fail(LCP_ERR_INVALID_INPUT, "null server or row");
+  const uint16_t* keep = s->row;
+  s->row = row;
+  const int r = lcp_server_query(s);
+  s->row = keep;
+  return r;
+}
+
 int lcp_server_query(lcp_server* s) {
   if (!s) return fail(LCP_ERR_INVALID_INPUT, "null server");
   const unsigned want = ++s->seq;

@@ -348,6 +348,11 @@ class SingleQueryServer:
         self._native = native  # the index outlives the server
 
     def query(self, query: np.ndarray) -> BatchResult:
+        """``query``: a validated (L,) row (uint16 or any 2-byte integer array)."""
+        fast = _native.host_server_query()
+        if fast is not None and query.dtype.itemsize == 2 and query.flags.c_contiguous:
+            check(fast(self._h.value, query))  # csrc/host_submit.c: the row read in place
+            return self.out
         self.row.array[0] = query
         check(load().lcp_server_query(self._h))
         return self.out
