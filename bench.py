@@ -519,14 +519,23 @@ def main() -> None:
         line["cpu_baseline"]["cpu_model"] = cpu_model()
         line["cpu_baseline"]["python_reference"] = python_reference()
         if not args.no_extras:
-            flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-            line["extras"] = extras(idx, ds, qs, main_stream, flush_buf)
-            del flush_buf, replicas
-            torch.cuda.empty_cache()
+            # side measurements: a failure is recorded in the line, never
+            # allowed to suppress the headline line itself
+            try:
+                flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+                line["extras"] = extras(idx, ds, qs, main_stream, flush_buf)
+                del flush_buf, replicas
+                torch.cuda.empty_cache()
+            except Exception as e:  # pragma: no cover - reported in the line
+                line["extras"] = {"error": f"{type(e).__name__}: {e}"}
             # config 5 on one GPU through the same sharded step the N > 1 runs
             # time (one range shard, local exchange): the N = 1 point of the
             # config-5 scaling curve
-            line["extras"]["config5_single_gpu"] = config5_leg(args, 1, 0, dev, barrier, max_over_ranks, "range")
+            try:
+                line["extras"]["config5_single_gpu"] = config5_leg(args, 1, 0, dev, barrier, max_over_ranks,
+                                                                   "range")
+            except Exception as e:  # pragma: no cover - reported in the line
+                line["extras"]["config5_single_gpu"] = {"error": f"{type(e).__name__}: {e}"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
