@@ -36,6 +36,8 @@ so the protocol is testable without a GPU.
 
 from __future__ import annotations
 
+import warnings
+
 import numpy as np
 
 from .core import InvalidInputError
@@ -268,7 +270,11 @@ class RangeShardedIndex:
             self._finish_build()
             return
         # the rows cross PCIe once, as 2-byte symbols, and widen on the device
-        rows_t = torch.from_numpy(items.view(np.int16)).to(self.device).to(torch.int32) & 0xFFFF
+        # (the host view is only read: torch's read-only-array warning is moot)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", UserWarning)
+            host = torch.from_numpy(items.view(np.int16))
+        rows_t = host.to(self.device).to(torch.int32) & 0xFFFF
         dest = route(rows_t, self.splitters, L) if n_local else torch.zeros(0, dtype=torch.int64,
                                                                             device=self.device)
         perm = torch.sort(dest, stable=True).indices
