@@ -1253,8 +1253,7 @@ static void allow_dyn_smem() {
 template <typename C, int T>
 static void launch_w1(const DevIndex& dv, int mode, unsigned grid, unsigned block, size_t smem,
                       cudaStream_t st, const uint16_t* q, int count, int k, int stride, u32* ids,
-                      uint16_t* lcps, int* hits, uint16_t* md, u64* aux, int* err,
-                      lcp_workspace* ws) {
+                      uint16_t* lcps, int* hits, uint16_t* md, u64* aux, int* err) {
   // strict / complete keep 25 % shared memory (two 1024-thread batches per SM);
   // TAL wants the largest L1 for the grouped bucket sweep
   prefer_carveout<k_query_w1<C, T, 0>>(25);
@@ -1306,11 +1305,11 @@ static void launch_fast(const DevIndex& dv, const uint16_t* q, int count, int gc
       // leaf region: 64 keys cover the +-need window for need <= 16, 96 keys for <= 32
       const long long need = mode == LCP_MODE_COMPLETE ? std::min<long long>(k, dv.n) : k;
       if (dv.idbits < 32) {
-        if (need <= 16) launch_w1<u32, 2>(dv, mode, grid, block, smem, st, q, count, k, stride, ids, lcps, hits, md, aux, err, ws);
-        else launch_w1<u32, 3>(dv, mode, grid, block, smem, st, q, count, k, stride, ids, lcps, hits, md, aux, err, ws);
+        if (need <= 16) launch_w1<u32, 2>(dv, mode, grid, block, smem, st, q, count, k, stride, ids, lcps, hits, md, aux, err);
+        else launch_w1<u32, 3>(dv, mode, grid, block, smem, st, q, count, k, stride, ids, lcps, hits, md, aux, err);
       } else {
-        if (need <= 16) launch_w1<u64, 2>(dv, mode, grid, block, smem, st, q, count, k, stride, ids, lcps, hits, md, aux, err, ws);
-        else launch_w1<u64, 3>(dv, mode, grid, block, smem, st, q, count, k, stride, ids, lcps, hits, md, aux, err, ws);
+        if (need <= 16) launch_w1<u64, 2>(dv, mode, grid, block, smem, st, q, count, k, stride, ids, lcps, hits, md, aux, err);
+        else launch_w1<u64, 3>(dv, mode, grid, block, smem, st, q, count, k, stride, ids, lcps, hits, md, aux, err);
       }
     }
     else
