@@ -23,6 +23,14 @@ class QueryResult:
     matched_depth: int
     mode: str
 
+    @classmethod
+    def _new(cls, indices, lcps, matched_depth: int, mode: str) -> "QueryResult":
+        """The dataclass constructor without the frozen-field setattr calls
+        (a single query's result is built on the latency-critical path)."""
+        obj = object.__new__(cls)
+        obj.__dict__.update(indices=indices, lcps=lcps, matched_depth=matched_depth, mode=mode)
+        return obj
+
     def pairs(self) -> list[tuple[int, int]]:
         return list(zip(self.indices.tolist(), self.lcps.tolist()))
 
@@ -84,17 +92,13 @@ class BatchResult:
 
     def result(self, q: int) -> QueryResult:
         """QueryResult of row q, dtypes as the reference returns them."""
-        h = int(self.hits[q])
-        md = int(self.matched_depth[q]) if self.matched_depth is not None else 0
+        h = int(self.hits.item(q))
+        md = int(self.matched_depth.item(q)) if self.matched_depth is not None else 0
         if h == 0:
             return empty_result(self.mode, md)
         id_dtype = np.int64 if self.mode == "tal" else np.int32
-        return QueryResult(
-            indices=self.ids[q, :h].astype(id_dtype),
-            lcps=self.lcps[q, :h].astype(np.int64),
-            matched_depth=md,
-            mode=self.mode,
-        )
+        return QueryResult._new(self.ids[q, :h].astype(id_dtype), self.lcps[q, :h].astype(np.int64), md,
+                                self.mode)
 
     def fullscan_result(self, q: int) -> FullScanResult:
         h = int(self.hits[q])
