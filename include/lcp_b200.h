@@ -286,7 +286,7 @@ int lcp_merge_candidates_peers(const uint64_t* const* peer_cand, int32_t world, 
  * burst, and lcp_server_query unpacks it into `out_block`
  * (lcp_packed_layout_for(1, out_stride), work counters included): no launch,
  * copy or event per query.  `query_row` and `out_block` are ordinary host
- * memory.  W == 1, strict or complete, min(k, n) <= 16 and out_stride <= 16
+ * memory.  W == 1, strict, complete or TAL, k <= 32 and out_stride <= 32
  * (else LCP_ERR_STATE: use the batch path).  lcp_server_query spins until
  * the answer is in; LCP_ERR_INVALID_INPUT for a symbol >= sigma.  The warp
  * exits after 100 ms without a request (so a device-wide synchronisation

@@ -2019,12 +2019,13 @@ int lcp_server_start(const lcp_index* ix, int32_t k, int32_t mode, int32_t out_s
   if (!ix || !out || !query_row || !out_block) return fail(LCP_ERR_INVALID_INPUT, "null argument");
   *out = nullptr;
   const DevIndex& dv = ix->dv;
-  if (mode != LCP_MODE_STRICT && mode != LCP_MODE_COMPLETE)
-    return fail(LCP_ERR_STATE, "the single-query server runs strict and complete mode");
+  if (mode < 0 || mode > 2) return fail(LCP_ERR_INVALID_INPUT, "unknown mode");
+  if (mode == LCP_MODE_TAL && ix->tal_depth < 0)
+    return fail(LCP_ERR_STATE, "index was built without a TAL bucket structure");
   if (dv.W != 1 || dv.n < 1 || k < 1 || k > FAST_KMAX)
     return fail(LCP_ERR_STATE, "the single-query server needs W == 1, n >= 1 and k <= 32");
   const long long need = mode == LCP_MODE_COMPLETE ? std::min<long long>(k, dv.n) : k;
-  if (need >= 17 || out_stride > 16) return fail(LCP_ERR_STATE, "the single-query server handles need <= 16");
+  if (need > 32 || out_stride > 32) return fail(LCP_ERR_STATE, "the single-query server handles k <= 32");
   const long long ns = std::max<long long>(1, std::min<long long>(k, dv.n));
   if (out_stride < ns) return fail(LCP_ERR_INVALID_INPUT, "out_stride must be >= min(k, n)");
   const int nq = (dv.L + SERVE_SYMS_PER_SECTOR - 1) / SERVE_SYMS_PER_SECTOR;
@@ -2053,9 +2054,14 @@ int lcp_server_start(const lcp_index* ix, int32_t k, int32_t mode, int32_t out_s
   }
   s->box = static_cast<unsigned*>(c);
   memset(s->box, 0, bytes);
-  const bool u32c = dv.idbits < 32;
-  if (mode == LCP_MODE_STRICT) s->launch = u32c ? serve_launch<u32, 2, 0> : serve_launch<u64, 2, 0>;
-  else s->launch = u32c ? serve_launch<u32, 2, 1> : serve_launch<u64, 2, 1>;
+  // the batch kernel's per-query body: 64-key leaf region for need <= 16,
+  // 96 keys up to 32 (the batch path runs the list kernel there)
+  static int (*const table[2][2][3])(lcp_server*, unsigned) = {
+      {{serve_launch<u32, 2, 0>, serve_launch<u32, 2, 1>, serve_launch<u32, 2, 2>},
+       {serve_launch<u32, 3, 0>, serve_launch<u32, 3, 1>, serve_launch<u32, 3, 2>}},
+      {{serve_launch<u64, 2, 0>, serve_launch<u64, 2, 1>, serve_launch<u64, 2, 2>},
+       {serve_launch<u64, 3, 0>, serve_launch<u64, 3, 1>, serve_launch<u64, 3, 2>}}};
+  s->launch = table[dv.idbits < 32 ? 0 : 1][need <= 16 ? 0 : 1][mode];
   const int r = s->launch(s, 0);
   if (r != LCP_OK) {
     cudaStreamDestroy(s->stream);

@@ -330,7 +330,7 @@ class SingleQueryServer:
     csrc/serve_kernels.cuh): a resident warp answers each query written into
     a page-locked row, straight into a page-locked packed block, with no
     launch, copy or event per query.  Raises InvalidStateError for shapes
-    the server does not cover (W > 1, min(k, n) > 16, TAL)."""
+    the server does not cover (W > 1, k > 32)."""
 
     def __init__(self, native: "NativeIndex", k: int, mode: str):
         if mode not in MODES:

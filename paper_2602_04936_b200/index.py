@@ -223,8 +223,7 @@ class TrieIndex:
         """Within the block, this thread's ``query(q, k, mode)`` calls are
         answered by a resident GPU warp polling page-locked host memory (no
         launch, copy or event per query; engine.SingleQueryServer).  Shapes
-        the server does not cover (W > 1, min(k, n) > 16) keep the launch
-        path.  Do not synchronise the whole device inside the block: the warp
+        the server does not cover (W > 1, k > 32) keep the launch path.  Do not synchronise the whole device inside the block: the warp
         stays resident until it has been idle for 100 ms."""
         from .core import InvalidStateError
         from .engine import SingleQueryServer

@@ -11,6 +11,9 @@ sum(min(lcp + 1, L)) exactly like tal.py:173-193.
 
 from __future__ import annotations
 
+import contextlib
+import threading
+
 import numpy as np
 
 from .core import InvalidInputError, dataset_parts, validate_query_batch, validate_query_row
@@ -137,9 +140,14 @@ class TalEngine:
         if k < 1:
             raise InvalidInputError(f"k must be >= 1, got {k}")
         query = self._validate_query(q)
-        # the single-query path: pinned staging row and block, so the kernel
-        # reads the row and writes the answer over PCIe directly (no copies)
-        out = self._native.query_single(query, k, "tal")
+        tls = getattr(self, "_tls", None)
+        srv = getattr(tls, "server", None) if tls is not None else None
+        if srv is not None and srv.k == k:
+            out = srv.query(query)  # latency mode (low_latency)
+        else:
+            # the single-query path: pinned staging row and block, so the kernel
+            # reads the row and writes the answer over PCIe directly (no copies)
+            out = self._native.query_single(query, k, "tal")
         report = self.new_work_report()
         report.queries = 1
         items, sym = tal_counters(out.aux)
@@ -151,6 +159,34 @@ class TalEngine:
             work.items_scanned += report.items_scanned
             work.queries += 1
         return out.result(0), report
+
+    @contextlib.contextmanager
+    def low_latency(self, k: int):
+        """Within the block, this thread's ``query(q, k)`` calls are answered
+        by a resident GPU warp (engine.SingleQueryServer, TAL mode); shapes it
+        does not cover keep the launch path.  Do not synchronise the whole
+        device inside the block (the warp stays resident until 100 ms idle)."""
+        from .core import InvalidStateError
+        from .engine import SingleQueryServer
+
+        if k < 1:
+            raise InvalidInputError(f"k must be >= 1, got {k}")
+        srv = None
+        if self.n > 0:
+            try:
+                srv = SingleQueryServer(self._native, k, "tal")
+            except InvalidStateError:
+                srv = None
+        if getattr(self, "_tls", None) is None:
+            self._tls = threading.local()
+        prev = getattr(self._tls, "server", None)
+        self._tls.server = srv
+        try:
+            yield self
+        finally:
+            self._tls.server = prev
+            if srv is not None:
+                srv.close()
 
     def query_batch(self, queries, k: int, work: WorkReport | None = None,
                     out: BatchResult | None = None) -> BatchResult:

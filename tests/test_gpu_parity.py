@@ -1135,7 +1135,7 @@ def test_low_latency_server(gpu):
         idx = lg.build(ds)
         qs = np.vstack([lg.generate_queries(ds, 40, seed=seed + 1),
                         lg.generate_queries(ds, 40, seed=seed + 2, prefix_len=L // 2)])
-        for k in (1, 5, 10, 16, 20):
+        for k in (1, 5, 10, 16, 20, 32, 40):  # 64- and 96-key regions; 40: not served
             for mode in ("strict", "complete"):
                 ref = idx.query_batch(qs, k, mode)
                 w_ref, w_got = idx.new_work_report(), idx.new_work_report()
@@ -1180,6 +1180,21 @@ def test_low_latency_server(gpu):
     for t in threads:
         t.join()
     assert not errors, errors
+    # TAL through the server: answers and the bucket counters per query
+    tds = lg.generate_dataset(60_000, 16, 4, seed=13)
+    eng = lg.build_tal(tds, 256)
+    tq = np.vstack([lg.generate_queries(tds, 30, seed=14), lg.generate_queries(tds, 30, seed=15, prefix_len=6)])
+    for k in (3, 10, 24):
+        ref = eng.query_batch(tq, k)
+        exp = [eng.query(tq[i], k) for i in range(len(tq))]  # launch path
+        with eng.low_latency(k):
+            assert eng._tls.server is not None
+            for i in range(len(tq)):
+                res, rep = eng.query(tq[i], k)
+                assert res.to_bytes() == exp[i][0].to_bytes(), (k, i)
+                assert res.pairs() == ref.pairs(i), (k, i)
+                assert (rep.items_scanned, rep.symbols_compared) == (exp[i][1].items_scanned,
+                                                                     exp[i][1].symbols_compared), (k, i)
     wide = lg.build(lg.generate_dataset(2000, 32, 65536, seed=11))  # W > 1: not served, same API
     q = lg.generate_queries(lg.generate_dataset(2000, 32, 65536, seed=11), 1, seed=12)[0]
     with wide.low_latency(5, "complete"):
